@@ -1,0 +1,131 @@
+/*
+ * gtree_b200.h -- C ABI of the B200-native GTree (arXiv 2305.00645) MPC
+ * decision-tree hot path: three-party 2-out-of-3 replicated secret sharing
+ * over Z_2^64 / Z_2^32, all three parties simulated on one device exactly as
+ * the reference `obtree` package simulates them on three threads.
+ *
+ * Conventions (every entry point):
+ *   - share arrays are DEVICE pointers to component-major uint64 arrays
+ *     [3][...]; component i is party (i+1)'s `lo` (AVec.lo, reference
+ *     pkg/src/obtree/rss.py:53-63) and party (i+1) holds (c[i], c[(i+1)%3]);
+ *   - boolean share arrays are [3][n] uint8 in {0,1} (BitVec, rss.py:151-160);
+ *   - `width` is the ring width l in {8, 32, 64}; values are stored masked;
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream); calls are
+ *     asynchronous on it, re-entrant per stream, and do not allocate: the
+ *     caller owns all memory (workspace sizes are queried up front); the one
+ *     exception is gt_argmin, which takes stream-ordered scratch
+ *     (cudaMallocAsync) for its per-row tournament;
+ *   - return GT_OK, GT_EINVAL (bad arguments -> the reference's
+ *     ValueError/UsageError) or GT_ECUDA (launch/runtime failure -> the
+ *     reference's protocol errors, CLI exit code 2, cli.py:53-56);
+ *     gt_last_error() gives the message of the last failure on this thread;
+ *   - `op` values name the gadget call site for the counter-based PRG; the
+ *     library's own training/inference drivers use op ids < 2^31, so
+ *     standalone gadget calls should use op >= 2^31 to stay disjoint.
+ */
+#ifndef GTREE_B200_H
+#define GTREE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GT_OK 0
+#define GT_EINVAL 1
+#define GT_ECUDA 2
+
+#define GT_ABI_VERSION 1
+
+typedef struct {
+  uint32_t k0, k1;
+} gt_key;
+
+/* dealer key (correlated material, dealer.py:43-84) and the three pairwise
+ * keys; pair[i] is the seed party i+1 shares with its successor
+ * (SeedSetup.pair_seeds[i+1], transport.py:97-124). */
+typedef struct {
+  gt_key dealer;
+  gt_key pair[3];
+} gt_keys;
+
+int gt_abi_version(void);
+const char* gt_last_error(void);
+
+/* ---- standalone gadgets (reference pkg/src/obtree/gadgets.py, rss.py) ---- */
+
+/* PartyEngine.mul, rss.py:386-400: z = x*y with one reshare. */
+int gt_mul(int width, const uint64_t* x, const uint64_t* y, uint64_t* z, uint64_t n, const gt_keys* keys,
+           uint32_t op, void* stream);
+/* eq, gadgets.py:120-130: out = [x == y]; y (shared) or y_pub ([n] public) or both NULL (y = 0). */
+int gt_eq(int width, const uint64_t* x, const uint64_t* y, const uint64_t* y_pub, uint8_t* out, uint64_t n,
+          const gt_keys* keys, uint32_t op, void* stream);
+/* lt, gadgets.py:188-216: out = [x < y] unsigned; y shared or y_pub public. */
+int gt_lt(int width, const uint64_t* x, const uint64_t* y, const uint64_t* y_pub, uint8_t* out, uint64_t n,
+          const gt_keys* keys, uint32_t op, void* stream);
+/* b2a, gadgets.py:223-231. */
+int gt_b2a(int width, const uint8_t* bits, uint64_t* out, uint64_t n, const gt_keys* keys, uint32_t op,
+           void* stream);
+/* select_share, gadgets.py:238-253: out = w1 + cond*(w2-w1); payload [3][n_cond*group]. */
+int gt_select(int width, const uint64_t* w1, const uint64_t* w2, const uint8_t* cond, uint64_t* out,
+              uint64_t n_cond, uint64_t group, const gt_keys* keys, uint32_t op, void* stream);
+/* truncate, gadgets.py:260-288 (unsigned, exact floor). */
+int gt_truncate(int width, const uint64_t* x, uint64_t* out, uint64_t n, int k, const gt_keys* keys, uint32_t op,
+                void* stream);
+/* division, gadgets.py:310-349 (width 32 or 64). */
+int gt_division(int width, const uint64_t* p, const uint64_t* q, uint64_t* out, uint64_t n, int tau,
+                const gt_keys* keys, uint32_t op, void* stream);
+/* argmin_masked, gadgets.py:366-401: scores [3][n][m] (width), avail [3][n][m]
+ * bits, out [3][n] index shares in Z_2^64. */
+int gt_argmin(int width, const uint64_t* scores, const uint8_t* avail, uint64_t* out, uint64_t n, uint64_t m,
+              uint64_t worst, const gt_keys* keys, uint32_t op, void* stream);
+/* oaa, oaa.py:20-35: out[i] = table[idx[i]] (0 when out of range). */
+int gt_oaa(int width, const uint64_t* table, uint64_t m, const uint64_t* idx, uint64_t* out, uint64_t n,
+           const gt_keys* keys, uint32_t op, void* stream);
+/* row_lookup, oaa.py:38-55: rows [3][n][m]; out[i] = rows[i][idx[i]]. */
+int gt_row_lookup(int width, const uint64_t* rows, uint64_t m, const uint64_t* idx, uint64_t* out, uint64_t n,
+                  const gt_keys* keys, uint32_t op, void* stream);
+
+/* ---- secure training (train_tree, train.py:222-311, heuristic "mpc") ---- */
+
+typedef struct {
+  int32_t depth;       /* resolved depth H (train.py:195-200) */
+  int32_t tau;         /* fixed-point bits (TrainConfig.tau) */
+  int32_t score_width; /* score ring width, 32 or 64 (TrainConfig.score_ring) */
+  int32_t nf;          /* features = n_columns - 1, 1..64 */
+  int32_t policy;      /* 0 = fixed, 1 = grow (one opened stop bit per level) */
+  int32_t reserved;
+  uint64_t n_total;     /* global sample count (counter_shift, train.py:189-192) */
+  uint64_t n_local;     /* samples resident on this device */
+  uint64_t sample_base; /* global index of the first local sample */
+} gt_train_cfg;
+
+/* Sum-allreduce of `count` uint64 words in place (count partials of one
+ * level, sample-sharded training).  NULL = single device. */
+typedef int (*gt_allreduce_fn)(uint64_t* buf, uint64_t count, void* stream, void* user);
+
+uint64_t gt_train_workspace_bytes(const gt_train_cfg* cfg);
+
+/* features [3][n_local][nf], labels [3][n_local], filler [2^depth-1] public
+ * placeholder stream (tree.py:160-169) in device memory; outputs T, F
+ * [3][2^depth-1] shares; *depth_out = trained depth (< depth only under the
+ * grow policy). */
+int gt_train(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* labels, const uint64_t* filler,
+             uint64_t* T, uint64_t* F, int32_t* depth_out, void* workspace, uint64_t workspace_bytes,
+             const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user, void* stream);
+
+/* ---- secure inference (infer_batch, infer.py:91-106) ---- */
+
+/* tree [3][2^depth-1] heap-ordered payload shares, queries [3][n][nf];
+ * instance_base = global index of query 0 (instance sharding); out [3][n]
+ * predicted labels; slot_out [3][n] final heap slot (nullable). */
+int gt_infer(int depth, const uint64_t* tree, const uint64_t* queries, uint64_t n, uint64_t nf,
+             uint64_t instance_base, uint64_t* out, uint64_t* slot_out, const gt_keys* keys, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GTREE_B200_H */

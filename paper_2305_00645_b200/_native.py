@@ -1,0 +1,123 @@
+"""ctypes binding of the in-tree sm_100a library ``libgtree_b200.so``.
+
+The library is the product: every share computation of the training and
+inference path runs in its CUDA kernels (include/gtree_b200.h).  There is no
+CPU fallback -- if the library is missing or no CUDA device is present, the
+entry points raise instead of computing anything on the host.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgtree_b200.so")
+
+GT_OK, GT_EINVAL, GT_ECUDA = 0, 1, 2
+ABI_VERSION = 1
+
+
+class ProtocolError(RuntimeError):
+    """Device/launch failure inside a protocol run (reference exit code 2,
+    cli.py:53-56: ShareError/MaterialError/TransportError class)."""
+
+
+class gt_key(ctypes.Structure):
+    _fields_ = [("k0", ctypes.c_uint32), ("k1", ctypes.c_uint32)]
+
+
+class gt_keys(ctypes.Structure):
+    _fields_ = [("dealer", gt_key), ("pair", gt_key * 3)]
+
+
+class gt_train_cfg(ctypes.Structure):
+    _fields_ = [
+        ("depth", ctypes.c_int32),
+        ("tau", ctypes.c_int32),
+        ("score_width", ctypes.c_int32),
+        ("nf", ctypes.c_int32),
+        ("policy", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("n_total", ctypes.c_uint64),
+        ("n_local", ctypes.c_uint64),
+        ("sample_base", ctypes.c_uint64),
+    ]
+
+
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p)
+
+_u64p = ctypes.c_void_p
+_SIGS = {
+    "gt_abi_version": (ctypes.c_int, []),
+    "gt_last_error": (ctypes.c_char_p, []),
+    "gt_mul": (ctypes.c_int, [ctypes.c_int, _u64p, _u64p, _u64p, ctypes.c_uint64, ctypes.POINTER(gt_keys),
+                              ctypes.c_uint32, ctypes.c_void_p]),
+    "gt_eq": (ctypes.c_int, [ctypes.c_int, _u64p, _u64p, _u64p, _u64p, ctypes.c_uint64, ctypes.POINTER(gt_keys),
+                             ctypes.c_uint32, ctypes.c_void_p]),
+    "gt_lt": (ctypes.c_int, [ctypes.c_int, _u64p, _u64p, _u64p, _u64p, ctypes.c_uint64, ctypes.POINTER(gt_keys),
+                             ctypes.c_uint32, ctypes.c_void_p]),
+    "gt_b2a": (ctypes.c_int, [ctypes.c_int, _u64p, _u64p, ctypes.c_uint64, ctypes.POINTER(gt_keys), ctypes.c_uint32,
+                              ctypes.c_void_p]),
+    "gt_select": (ctypes.c_int, [ctypes.c_int, _u64p, _u64p, _u64p, _u64p, ctypes.c_uint64, ctypes.c_uint64,
+                                 ctypes.POINTER(gt_keys), ctypes.c_uint32, ctypes.c_void_p]),
+    "gt_truncate": (ctypes.c_int, [ctypes.c_int, _u64p, _u64p, ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(gt_keys),
+                                   ctypes.c_uint32, ctypes.c_void_p]),
+    "gt_division": (ctypes.c_int, [ctypes.c_int, _u64p, _u64p, _u64p, ctypes.c_uint64, ctypes.c_int,
+                                   ctypes.POINTER(gt_keys), ctypes.c_uint32, ctypes.c_void_p]),
+    "gt_argmin": (ctypes.c_int, [ctypes.c_int, _u64p, _u64p, _u64p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                 ctypes.POINTER(gt_keys), ctypes.c_uint32, ctypes.c_void_p]),
+    "gt_oaa": (ctypes.c_int, [ctypes.c_int, _u64p, ctypes.c_uint64, _u64p, _u64p, ctypes.c_uint64,
+                              ctypes.POINTER(gt_keys), ctypes.c_uint32, ctypes.c_void_p]),
+    "gt_row_lookup": (ctypes.c_int, [ctypes.c_int, _u64p, ctypes.c_uint64, _u64p, _u64p, ctypes.c_uint64,
+                                     ctypes.POINTER(gt_keys), ctypes.c_uint32, ctypes.c_void_p]),
+    "gt_train_workspace_bytes": (ctypes.c_uint64, [ctypes.POINTER(gt_train_cfg)]),
+    "gt_train": (ctypes.c_int, [ctypes.POINTER(gt_train_cfg), _u64p, _u64p, _u64p, _u64p, _u64p,
+                                ctypes.POINTER(ctypes.c_int32), ctypes.c_void_p, ctypes.c_uint64,
+                                ctypes.POINTER(gt_keys), ALLREDUCE_FN, ctypes.c_void_p, ctypes.c_void_p]),
+    "gt_infer": (ctypes.c_int, [ctypes.c_int, _u64p, _u64p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                _u64p, _u64p, ctypes.POINTER(gt_keys), ctypes.c_void_p]),
+}
+EXPORTS = tuple(_SIGS)
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load (once) and type the C ABI.  Raises ImportError if the library is
+    not built -- there is deliberately no fallback path."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is missing: build it with `make` or __graft_entry__.build() "
+                              "(the B200 path has no CPU fallback)")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.gt_abi_version() != ABI_VERSION:
+            raise ImportError(f"{path}: ABI version {lib.gt_abi_version()} != {ABI_VERSION}")
+        _lib = lib
+        return lib
+
+
+def check(rc: int) -> None:
+    if rc == GT_OK:
+        return
+    msg = (load().gt_last_error() or b"").decode(errors="replace")
+    if rc == GT_EINVAL:
+        raise ValueError(msg)
+    raise ProtocolError(msg)
+
+
+def require_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("the B200 path needs a CUDA device; there is no CPU fallback")
+    return torch

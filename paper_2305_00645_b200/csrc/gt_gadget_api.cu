@@ -1,0 +1,320 @@
+// Standalone gadget entry points of the C ABI (include/gtree_b200.h).  These
+// run one reference gadget call (gadgets.py / oaa.py / rss.py) over a batch
+// of lanes; the training and inference drivers use the same per-lane device
+// functions fused into larger kernels.
+#include <string>
+
+#include "gt_common.cuh"
+#include "gt_lookup.cuh"
+
+namespace gt {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail_cuda(cudaError_t e, const char* where) {
+  set_error(std::string(where) + ": " + cudaGetErrorString(e));
+  return GT_ECUDA;
+}
+int fail_inval(const std::string& msg) {
+  set_error(msg);
+  return GT_EINVAL;
+}
+
+namespace {
+
+constexpr int TPB = 256;
+
+inline unsigned blocks_for(uint64_t n) { return (unsigned)((n + TPB - 1) / TPB); }
+
+__device__ __forceinline__ A3 ld3(const uint64_t* p, uint64_t n, uint64_t i) {
+  return a3(p[i], p[n + i], p[2 * n + i]);
+}
+__device__ __forceinline__ void st3(uint64_t* p, uint64_t n, uint64_t i, const A3& a) {
+  p[i] = a.v[0];
+  p[n + i] = a.v[1];
+  p[2 * n + i] = a.v[2];
+}
+__device__ __forceinline__ B3 ldb(const uint8_t* p, uint64_t n, uint64_t i) {
+  B3 b;
+  b.v[0] = p[i] & 1;
+  b.v[1] = p[n + i] & 1;
+  b.v[2] = p[2 * n + i] & 1;
+  return b;
+}
+__device__ __forceinline__ void stb(uint8_t* p, uint64_t n, uint64_t i, const B3& b) {
+  p[i] = (uint8_t)(b.v[0] & 1);
+  p[n + i] = (uint8_t)(b.v[1] & 1);
+  p[2 * n + i] = (uint8_t)(b.v[2] & 1);
+}
+template <int L>
+__device__ __forceinline__ A3 operand_y(const uint64_t* y, const uint64_t* ypub, uint64_t n, uint64_t i) {
+  if (y) return ld3(y, n, i);
+  return a3_const(ypub ? (ypub[i] & Ring<L>::M) : 0ull);
+}
+
+template <int L>
+__global__ void k_mul(const uint64_t* x, const uint64_t* y, uint64_t* z, uint64_t n, Keys K, uint32_t op) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  st3(z, n, i, mul<L>(K, op, 0, 0, i, ld3(x, n, i), ld3(y, n, i)));
+}
+
+template <int L>
+__global__ void k_eq(const uint64_t* x, const uint64_t* y, const uint64_t* ypub, uint8_t* out, uint64_t n, Keys K,
+                     uint32_t op) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  stb(out, n, i, eqz<L>(K, op, 0, i, diff<L>(ld3(x, n, i), operand_y<L>(y, ypub, n, i))));
+}
+
+template <int L>
+__global__ void k_lt(const uint64_t* x, const uint64_t* y, const uint64_t* ypub, uint8_t* out, uint64_t n, Keys K,
+                     uint32_t op) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  stb(out, n, i, lt<L>(K, op, 0, i, ld3(x, n, i), operand_y<L>(y, ypub, n, i)));
+}
+
+template <int L>
+__global__ void k_b2a(const uint8_t* bits, uint64_t* out, uint64_t n, Keys K, uint32_t op) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  st3(out, n, i, b2a<L>(K, op, 0, i, ldb(bits, n, i)));
+}
+
+// one thread per payload element; the condition's b2a is recomputed per
+// element of its group (same lane/op/sub -> identical dabit).
+template <int L>
+__global__ void k_select(const uint64_t* w1, const uint64_t* w2, const uint8_t* cond, uint64_t* out, uint64_t ncond,
+                         uint64_t group, Keys K, uint32_t op) {
+  uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t n = ncond * group;
+  if (e >= n) return;
+  uint64_t c = e / group, k = e % group;
+  const A3 ca = b2a<L>(K, op, 0, c, ldb(cond, ncond, c));
+  st3(out, n, e, select_with<L>(K, op, 0, (uint32_t)k, c, ld3(w1, n, e), ld3(w2, n, e), ca));
+}
+
+template <int L>
+__global__ void k_trunc(const uint64_t* x, uint64_t* out, uint64_t n, int k, Keys K, uint32_t op) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  st3(out, n, i, trunc<L>(K, op, 0, i, ld3(x, n, i), k));
+}
+
+template <int L>
+__global__ void k_division(const uint64_t* p, const uint64_t* q, uint64_t* out, uint64_t n, DivParams d, Keys K,
+                           uint32_t op) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  st3(out, n, i, division<L>(K, op, 0, i, ld3(p, n, i), ld3(q, n, i), d));
+}
+
+// argmin_masked, one row per thread; subs: 0/1 masking select, round r at
+// 2+5r (lt), 3+5r/4+5r (value select), 5+5r/6+5r (index select, Z_2^64).
+constexpr int ARGMIN_MAX = 128;
+template <int L>
+__global__ void k_argmin(const uint64_t* scores, const uint8_t* avail, uint64_t* out, uint64_t n, uint64_t m,
+                         uint64_t worst, Keys K, uint32_t op, uint64_t* scratch) {
+  uint64_t row = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  const uint64_t nm = n * m;
+  uint64_t* vals = scratch + row * (6 * m);  // [3][m] values, [3][m] indices
+  uint64_t* idxs = vals + 3 * m;
+  for (uint64_t j = 0; j < m; ++j) {
+    const uint64_t e = row * m + j;
+    const A3 v = select1<L>(K, op, 0, e, a3_const(worst & Ring<L>::M), ld3(scores, nm, e), ldb(avail, nm, e));
+    for (int c = 0; c < 3; ++c) {
+      vals[c * m + j] = v.v[c];
+      idxs[c * m + j] = c == 0 ? j : 0;
+    }
+  }
+  uint64_t cur = m;
+  for (int r = 0; cur > 1; ++r) {
+    const uint64_t pairs = cur / 2;
+    const uint32_t base = 2 + 5 * r;
+    for (uint64_t p = 0; p < pairs; ++p) {
+      const uint64_t lane = row * m + p;
+      const A3 av = a3(vals[2 * p], vals[m + 2 * p], vals[2 * m + 2 * p]);
+      const A3 bv = a3(vals[2 * p + 1], vals[m + 2 * p + 1], vals[2 * m + 2 * p + 1]);
+      const A3 ai = a3(idxs[2 * p], idxs[m + 2 * p], idxs[2 * m + 2 * p]);
+      const A3 bi = a3(idxs[2 * p + 1], idxs[m + 2 * p + 1], idxs[2 * m + 2 * p + 1]);
+      const B3 cw = lt<L>(K, op, base, lane, bv, av);
+      const A3 nv = select1<L>(K, op, base + 1, lane, av, bv, cw);
+      const A3 ni = select1<64>(K, op, base + 3, lane, ai, bi, cw);
+      for (int c = 0; c < 3; ++c) {  // p <= 2p: in-place compaction is safe
+        vals[c * m + p] = nv.v[c];
+        idxs[c * m + p] = ni.v[c];
+      }
+    }
+    if (cur & 1) {
+      for (int c = 0; c < 3; ++c) {
+        vals[c * m + pairs] = vals[c * m + cur - 1];
+        idxs[c * m + pairs] = idxs[c * m + cur - 1];
+      }
+    }
+    cur = pairs + (cur & 1);
+  }
+  out[row] = idxs[0];
+  out[n + row] = idxs[m];
+  out[2 * n + row] = idxs[2 * m];
+}
+
+template <int L>
+__global__ void k_oaa(const uint64_t* table, uint64_t m, const uint64_t* idx, uint64_t* out, uint64_t n, Keys K,
+                      uint32_t op) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  auto entry = [&](int j) { return ld3(table, m, (uint64_t)j); };
+  st3(out, n, i, lookup_partial<L>(K, op, i, ld3(idx, n, i), (int)m, 0, 1, entry));
+}
+
+template <int L>
+__global__ void k_row_lookup(const uint64_t* rows, uint64_t m, const uint64_t* idx, uint64_t* out, uint64_t n, Keys K,
+                             uint32_t op) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t nm = n * m;
+  auto entry = [&](int j) { return ld3(rows, nm, i * m + (uint64_t)j); };
+  st3(out, n, i, lookup_partial<L>(K, op, i, ld3(idx, n, i), (int)m, 0, 1, entry));
+}
+
+bool width_ok(int w) { return w == 8 || w == 32 || w == 64; }
+
+}  // namespace
+}  // namespace gt
+
+using namespace gt;
+
+#define GT_DISPATCH(width, KERNEL, GRID, ...)                                   \
+  do {                                                                          \
+    cudaStream_t _s = (cudaStream_t)stream;                                     \
+    if ((width) == 64) KERNEL<64><<<(GRID), TPB, 0, _s>>>(__VA_ARGS__);         \
+    else if ((width) == 32) KERNEL<32><<<(GRID), TPB, 0, _s>>>(__VA_ARGS__);    \
+    else KERNEL<8><<<(GRID), TPB, 0, _s>>>(__VA_ARGS__);                        \
+  } while (0)
+
+#define GT_CHECK_COMMON(width, keys)                                             \
+  do {                                                                           \
+    if (!width_ok(width)) return fail_inval("unsupported ring width");           \
+    if (!(keys)) return fail_inval("keys must not be NULL");                     \
+  } while (0)
+
+extern "C" {
+
+int gt_abi_version(void) { return GT_ABI_VERSION; }
+const char* gt_last_error(void) { return g_last_error.c_str(); }
+
+int gt_mul(int width, const uint64_t* x, const uint64_t* y, uint64_t* z, uint64_t n, const gt_keys* keys, uint32_t op,
+           void* stream) {
+  GT_CHECK_COMMON(width, keys);
+  if (n == 0) return GT_OK;
+  if (!x || !y || !z) return fail_inval("gt_mul: NULL operand");
+  GT_DISPATCH(width, k_mul, blocks_for(n), x, y, z, n, to_keys(keys), op);
+  GT_LAUNCH_CHECK("gt_mul");
+  return GT_OK;
+}
+
+int gt_eq(int width, const uint64_t* x, const uint64_t* y, const uint64_t* y_pub, uint8_t* out, uint64_t n,
+          const gt_keys* keys, uint32_t op, void* stream) {
+  GT_CHECK_COMMON(width, keys);
+  if (n == 0) return GT_OK;
+  if (!x || !out) return fail_inval("gt_eq: NULL operand");
+  GT_DISPATCH(width, k_eq, blocks_for(n), x, y, y_pub, out, n, to_keys(keys), op);
+  GT_LAUNCH_CHECK("gt_eq");
+  return GT_OK;
+}
+
+int gt_lt(int width, const uint64_t* x, const uint64_t* y, const uint64_t* y_pub, uint8_t* out, uint64_t n,
+          const gt_keys* keys, uint32_t op, void* stream) {
+  GT_CHECK_COMMON(width, keys);
+  if (n == 0) return GT_OK;
+  if (!x || !out) return fail_inval("gt_lt: NULL operand");
+  GT_DISPATCH(width, k_lt, blocks_for(n), x, y, y_pub, out, n, to_keys(keys), op);
+  GT_LAUNCH_CHECK("gt_lt");
+  return GT_OK;
+}
+
+int gt_b2a(int width, const uint8_t* bits, uint64_t* out, uint64_t n, const gt_keys* keys, uint32_t op,
+           void* stream) {
+  GT_CHECK_COMMON(width, keys);
+  if (n == 0) return GT_OK;
+  if (!bits || !out) return fail_inval("gt_b2a: NULL operand");
+  GT_DISPATCH(width, k_b2a, blocks_for(n), bits, out, n, to_keys(keys), op);
+  GT_LAUNCH_CHECK("gt_b2a");
+  return GT_OK;
+}
+
+int gt_select(int width, const uint64_t* w1, const uint64_t* w2, const uint8_t* cond, uint64_t* out, uint64_t n_cond,
+              uint64_t group, const gt_keys* keys, uint32_t op, void* stream) {
+  GT_CHECK_COMMON(width, keys);
+  if (group == 0 || group > 512) return fail_inval("payload size must be a multiple of condition size (group 1..512)");
+  if (n_cond == 0) return GT_OK;
+  if (!w1 || !w2 || !cond || !out) return fail_inval("gt_select: NULL operand");
+  GT_DISPATCH(width, k_select, blocks_for(n_cond * group), w1, w2, cond, out, n_cond, group, to_keys(keys), op);
+  GT_LAUNCH_CHECK("gt_select");
+  return GT_OK;
+}
+
+int gt_truncate(int width, const uint64_t* x, uint64_t* out, uint64_t n, int k, const gt_keys* keys, uint32_t op,
+                void* stream) {
+  GT_CHECK_COMMON(width, keys);
+  if (k < 0 || k >= width) return fail_inval("truncation amount out of range for width");
+  if (n == 0) return GT_OK;
+  if (!x || !out) return fail_inval("gt_truncate: NULL operand");
+  GT_DISPATCH(width, k_trunc, blocks_for(n), x, out, n, k, to_keys(keys), op);
+  GT_LAUNCH_CHECK("gt_truncate");
+  return GT_OK;
+}
+
+int gt_division(int width, const uint64_t* p, const uint64_t* q, uint64_t* out, uint64_t n, int tau,
+                const gt_keys* keys, uint32_t op, void* stream) {
+  GT_CHECK_COMMON(width, keys);
+  bool ok = false;
+  DivParams d = div_params(width, tau, &ok);
+  if (!ok || tau < 0 || tau >= width - 2) return fail_inval("division unsupported at this width/tau");
+  if (n == 0) return GT_OK;
+  if (!p || !q || !out) return fail_inval("gt_division: NULL operand");
+  GT_DISPATCH(width, k_division, blocks_for(n), p, q, out, n, d, to_keys(keys), op);
+  GT_LAUNCH_CHECK("gt_division");
+  return GT_OK;
+}
+
+int gt_argmin(int width, const uint64_t* scores, const uint8_t* avail, uint64_t* out, uint64_t n, uint64_t m,
+              uint64_t worst, const gt_keys* keys, uint32_t op, void* stream) {
+  GT_CHECK_COMMON(width, keys);
+  if (m == 0 || m > ARGMIN_MAX) return fail_inval("argmin: need 1 <= m <= 128 columns");
+  if (n == 0) return GT_OK;
+  if (!scores || !avail || !out) return fail_inval("gt_argmin: NULL operand");
+  uint64_t* scratch = nullptr;
+  cudaStream_t s = (cudaStream_t)stream;
+  GT_CUDA_CHECK(cudaMallocAsync((void**)&scratch, n * 6 * m * sizeof(uint64_t), s));
+  GT_DISPATCH(width, k_argmin, blocks_for(n), scores, avail, out, n, m, worst, to_keys(keys), op, scratch);
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(scratch, s);
+  if (e != cudaSuccess) return fail_cuda(e, "gt_argmin");
+  return GT_OK;
+}
+
+int gt_oaa(int width, const uint64_t* table, uint64_t m, const uint64_t* idx, uint64_t* out, uint64_t n,
+           const gt_keys* keys, uint32_t op, void* stream) {
+  GT_CHECK_COMMON(width, keys);
+  if (n == 0) return GT_OK;
+  if (!idx || !out || (m && !table)) return fail_inval("gt_oaa: NULL operand");
+  GT_DISPATCH(width, k_oaa, blocks_for(n), table, m, idx, out, n, to_keys(keys), op);
+  GT_LAUNCH_CHECK("gt_oaa");
+  return GT_OK;
+}
+
+int gt_row_lookup(int width, const uint64_t* rows, uint64_t m, const uint64_t* idx, uint64_t* out, uint64_t n,
+                  const gt_keys* keys, uint32_t op, void* stream) {
+  GT_CHECK_COMMON(width, keys);
+  if (n == 0) return GT_OK;
+  if (!idx || !out || (m && !rows)) return fail_inval("gt_row_lookup: NULL operand");
+  GT_DISPATCH(width, k_row_lookup, blocks_for(n), rows, m, idx, out, n, to_keys(keys), op);
+  GT_LAUNCH_CHECK("gt_row_lookup");
+  return GT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,394 @@
+// Per-lane MPC gadgets over 2-out-of-3 replicated secret sharing, all three
+// parties co-resident.  One lane = one element of a reference gadget call;
+// every function below computes the three parties' local steps for that lane
+// and treats each reshare / open as the algebraic identity it is when the
+// three parties live in the same register file (the message bytes are
+// accounted analytically by the host ledger, paper_2305_00645_b200/ledger.py).
+//
+// Representation: an arithmetic share is the three additive
+// components A3.v[0..2] with x = v0 + v1 + v2 mod 2^L; party p (1-based)
+// holds (v[p-1], v[p mod 3]) as (lo, hi) exactly as rss.py:1-9.  A boolean
+// share B3 holds three XOR components; inside eq/lt one 64-bit word carries
+// all L bit planes of one element (bit j = plane j), so the reference's plane
+// loops (gadgets.py:81-185) become in-word shifts and masks.  Public
+// constants act on component 0 (party 1 lo / party 3 hi, rss.py:313-367).
+#pragma once
+#include "gt_prg.cuh"
+
+namespace gt {
+
+template <int L>
+struct Ring {
+  static constexpr uint64_t M = (L == 64) ? ~0ull : ((1ull << L) - 1ull);
+};
+
+struct A3 {
+  uint64_t v[3];
+};
+struct B3 {
+  uint64_t v[3];
+};
+
+__device__ __forceinline__ uint64_t lowmask(int k) { return k >= 64 ? ~0ull : ((1ull << k) - 1ull); }
+
+__device__ __forceinline__ A3 a3(uint64_t a, uint64_t b, uint64_t c) {
+  A3 r;
+  r.v[0] = a;
+  r.v[1] = b;
+  r.v[2] = c;
+  return r;
+}
+__device__ __forceinline__ A3 a3_const(uint64_t c) { return a3(c, 0, 0); }  // const_a, rss.py:313-324
+
+template <int L>
+__device__ __forceinline__ A3 add(const A3& x, const A3& y) {
+  return a3((x.v[0] + y.v[0]) & Ring<L>::M, (x.v[1] + y.v[1]) & Ring<L>::M, (x.v[2] + y.v[2]) & Ring<L>::M);
+}
+template <int L>
+__device__ __forceinline__ A3 diff(const A3& x, const A3& y) {
+  return a3((x.v[0] - y.v[0]) & Ring<L>::M, (x.v[1] - y.v[1]) & Ring<L>::M, (x.v[2] - y.v[2]) & Ring<L>::M);
+}
+template <int L>
+__device__ __forceinline__ A3 add_pub(A3 x, uint64_t c) {  // rss.py:341-348
+  x.v[0] = (x.v[0] + c) & Ring<L>::M;
+  return x;
+}
+template <int L>
+__device__ __forceinline__ A3 mul_pub(const A3& x, uint64_t c) {  // rss.py:88-90
+  return a3((x.v[0] * c) & Ring<L>::M, (x.v[1] * c) & Ring<L>::M, (x.v[2] * c) & Ring<L>::M);
+}
+template <int L>
+__device__ __forceinline__ A3 rsub_pub(uint64_t c, const A3& x) {  // rss.py:355-356
+  return add_pub<L>(a3((0 - x.v[0]) & Ring<L>::M, (0 - x.v[1]) & Ring<L>::M, (0 - x.v[2]) & Ring<L>::M), c);
+}
+template <int L>
+__device__ __forceinline__ uint64_t open(const A3& x) {  // open_a, rss.py:371-377
+  return (x.v[0] + x.v[1] + x.v[2]) & Ring<L>::M;
+}
+
+// ---------------------------------------------------------------------------
+// communicating primitives
+// ---------------------------------------------------------------------------
+
+// Hadamard product + reshare (PartyEngine.mul, rss.py:386-400):
+//   z_i = x_i y_i + x_{i+1} y_i + x_i y_{i+1} + F(k_i) - F(k_{i-1})
+template <int L>
+__device__ __forceinline__ A3 mul_z(const A3& x, const A3& y, const uint64_t F[3]) {
+  A3 z;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int j = (i + 1) % 3, p = (i + 2) % 3;
+    z.v[i] = (y.v[i] * (x.v[i] + x.v[j]) + x.v[i] * y.v[j] + F[i] - F[p]) & Ring<L>::M;
+  }
+  return z;
+}
+
+template <int L>
+__device__ __forceinline__ A3 mul(const Keys& K, uint32_t op, uint32_t sub, uint32_t field, uint64_t lane,
+                                  const A3& x, const A3& y) {
+  uint64_t F[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) F[i] = word(K.pair[i], op, sub, field, lane);
+  return mul_z<L>(x, y, F);
+}
+
+// AND with reshare (and_bits, rss.py:402-409) on bit-vector words; zero-share
+// bits Z_i ^ Z_{i-1} restricted to `zmask`.
+__device__ __forceinline__ B3 and_z(const B3& a, const B3& b, const uint64_t Z[3]) {
+  B3 z;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int j = (i + 1) % 3, p = (i + 2) % 3;
+    z.v[i] = (a.v[i] & b.v[i]) ^ (a.v[j] & b.v[i]) ^ (a.v[i] & b.v[j]) ^ Z[i] ^ Z[p];
+  }
+  return z;
+}
+
+__device__ __forceinline__ B3 and_gate(const Keys& K, uint32_t op, uint32_t sub, uint32_t field, uint64_t lane,
+                                       const B3& a, const B3& b, uint64_t zmask) {
+  uint64_t Z[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) Z[i] = word(K.pair[i], op, sub, field, lane) & zmask;
+  return and_z(a, b, Z);
+}
+
+__device__ __forceinline__ B3 bxor(const B3& a, const B3& b) {
+  B3 r;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) r.v[i] = a.v[i] ^ b.v[i];
+  return r;
+}
+__device__ __forceinline__ B3 bnot(B3 a, uint64_t m) {  // xor_pub(ones), rss.py:358-367
+  a.v[0] ^= m;
+  return a;
+}
+// or_bits = x ^ y ^ (x & y), rss.py:411-412
+__device__ __forceinline__ B3 or_gate(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const B3& x,
+                                      const B3& y, uint64_t zmask) {
+  return bxor(bxor(x, y), and_gate(K, op, sub, 0, lane, x, y, zmask));
+}
+
+// AND over the low k bit planes of the word (and_reduce, gadgets.py:94-109):
+// level with k rows ANDs plane j with plane j+half (j < half), an odd last
+// plane is carried to position half.  Gate j of a level draws zero bit
+// (off + j) of pair-word `field`; off advances by half per level (<= 63 bits).
+__device__ __forceinline__ B3 and_reduce(const Keys& K, uint32_t op, uint32_t sub, uint32_t field, uint64_t lane,
+                                         B3 P, int k) {
+  uint64_t Zw[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) Zw[i] = word(K.pair[i], op, sub, field, lane);
+  int off = 0;
+  while (k > 1) {
+    const int half = k >> 1;
+    const uint64_t lm = lowmask(half);
+    B3 a, b;
+    uint64_t Z[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      a.v[i] = P.v[i] & lm;
+      b.v[i] = (P.v[i] >> half) & lm;
+      Z[i] = (Zw[i] >> off) & lm;
+    }
+    B3 m = and_z(a, b, Z);
+    if (k & 1) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) m.v[i] |= ((P.v[i] >> (k - 1)) & 1ull) << half;
+    }
+    P = m;
+    off += half;
+    k = half + (k & 1);
+  }
+  return P;
+}
+
+// ---------------------------------------------------------------------------
+// comparisons (masked opening + boolean circuit on public c vs shared r)
+// ---------------------------------------------------------------------------
+
+// [d == 0] for d = x - y already formed (eq, gadgets.py:120-130).
+// dealer fields: r=0 Rb0=1 Rb1=2 R0=3 R1=4; pair field 0 = AND-tree zero bits.
+template <int L>
+__device__ __forceinline__ B3 eqz(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const A3& d) {
+  constexpr uint64_t M = Ring<L>::M;
+  const uint64_t r = word(K.dealer, op, sub, 0, lane) & M;
+  const uint64_t Rb0 = word(K.dealer, op, sub, 1, lane) & M;
+  const uint64_t Rb1 = word(K.dealer, op, sub, 2, lane) & M;
+  const uint64_t R0 = word(K.dealer, op, sub, 3, lane) & M;
+  const uint64_t R1 = word(K.dealer, op, sub, 4, lane) & M;
+  const uint64_t R2 = (r - R0 - R1) & M;  // make_arith_shares, rss.py:205-211
+  const uint64_t Rb2 = r ^ Rb0 ^ Rb1;     // _value_bit_words, dealer.py:411-417
+  const uint64_t c = open<L>(a3(d.v[0] + R0, d.v[1] + R1, d.v[2] + R2));
+  const uint64_t notc = ~c & M;
+  B3 P;
+  P.v[0] = Rb0 ^ notc;  // xor_pub(planes, ~c)
+  P.v[1] = Rb1;
+  P.v[2] = Rb2;
+  return and_reduce(K, op, sub, 0, lane, P, L);
+}
+
+// Kogge-Stone borrow prefix on (g, p) words (_prefix_borrow, gadgets.py:137-160).
+// Level with shift s: pg = p & (g << s), pp = p & (p << s) for bits >= s (two
+// batched AND lanes per row); bits < s keep g and p, as the reference does.
+// Level l draws pair fields fb + 2l (pg) and fb + 2l + 1 (pp).
+template <int L>
+__device__ __forceinline__ B3 prefix_borrow(const Keys& K, uint32_t op, uint32_t sub, uint32_t fb, uint64_t lane,
+                                            B3 g, B3 p) {
+  constexpr uint64_t M = Ring<L>::M;
+  int lvl = 0;
+#pragma unroll
+  for (int s = 1; s < L; s <<= 1, ++lvl) {
+    const uint64_t hm = M & ~lowmask(s);
+    B3 gs, ps;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      gs.v[i] = (g.v[i] << s) & M;
+      ps.v[i] = (p.v[i] << s) & M;
+    }
+    const B3 pg = and_gate(K, op, sub, fb + 2 * lvl, lane, p, gs, hm);
+    const B3 pp = and_gate(K, op, sub, fb + 2 * lvl + 1, lane, p, ps, hm);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      g.v[i] ^= pg.v[i];
+      p.v[i] = (p.v[i] & lowmask(s)) | pp.v[i];
+    }
+  }
+  return g;
+}
+
+// Borrow rows S[i] = [c mod 2^{i+1} < r mod 2^{i+1}] for public c
+// (_borrow_scan, gadgets.py:163-171): g = r & ~c, p = r ^ ~c.
+template <int L>
+__device__ __forceinline__ B3 borrow_scan(const Keys& K, uint32_t op, uint32_t sub, uint32_t fb, uint64_t lane,
+                                          uint64_t c, const B3& Rb) {
+  constexpr uint64_t M = Ring<L>::M;
+  const uint64_t notc = ~c & M;
+  B3 g, p;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    g.v[i] = Rb.v[i] & notc;
+    p.v[i] = Rb.v[i];
+  }
+  p.v[0] ^= notc;
+  return prefix_borrow<L>(K, op, sub, fb, lane, g, p);
+}
+
+// Shared bits of (c - r) (_masked_diff_bits, gadgets.py:174-185).
+template <int L>
+__device__ __forceinline__ B3 masked_diff_bits(const Keys& K, uint32_t op, uint32_t sub, uint32_t fb, uint64_t lane,
+                                               uint64_t c, const B3& Rb) {
+  constexpr uint64_t M = Ring<L>::M;
+  const B3 s = borrow_scan<L>(K, op, sub, fb, lane, c, Rb);
+  B3 d;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) d.v[i] = Rb.v[i] ^ ((s.v[i] << 1) & M);
+  d.v[0] ^= c;
+  return d;
+}
+
+// [x < y] unsigned (lt, gadgets.py:188-216); result in bit 0.
+// dealer fields: x-edabit 0..4, y-edabit 5..9; pair fields: x scan [0,12),
+// y scan [12,24), generate gate 24, final prefix [26,38).
+template <int L>
+__device__ __forceinline__ B3 lt(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const A3& x, const A3& y) {
+  constexpr uint64_t M = Ring<L>::M;
+  B3 xb, yb;
+  {
+    const uint64_t r = word(K.dealer, op, sub, 0, lane) & M;
+    B3 Rb;
+    Rb.v[0] = word(K.dealer, op, sub, 1, lane) & M;
+    Rb.v[1] = word(K.dealer, op, sub, 2, lane) & M;
+    Rb.v[2] = r ^ Rb.v[0] ^ Rb.v[1];
+    const uint64_t R0 = word(K.dealer, op, sub, 3, lane) & M, R1 = word(K.dealer, op, sub, 4, lane) & M;
+    const uint64_t c = open<L>(a3(x.v[0] + R0, x.v[1] + R1, x.v[2] + (r - R0 - R1)));
+    xb = masked_diff_bits<L>(K, op, sub, 0, lane, c, Rb);
+  }
+  {
+    const uint64_t r = word(K.dealer, op, sub, 5, lane) & M;
+    B3 Rb;
+    Rb.v[0] = word(K.dealer, op, sub, 6, lane) & M;
+    Rb.v[1] = word(K.dealer, op, sub, 7, lane) & M;
+    Rb.v[2] = r ^ Rb.v[0] ^ Rb.v[1];
+    const uint64_t R0 = word(K.dealer, op, sub, 8, lane) & M, R1 = word(K.dealer, op, sub, 9, lane) & M;
+    const uint64_t c = open<L>(a3(y.v[0] + R0, y.v[1] + R1, y.v[2] + (r - R0 - R1)));
+    yb = masked_diff_bits<L>(K, op, sub, 12, lane, c, Rb);
+  }
+  const B3 g = and_gate(K, op, sub, 24, lane, yb, bnot(xb, M), M);
+  const B3 p = bnot(bxor(xb, yb), M);
+  B3 rows = prefix_borrow<L>(K, op, sub, 26, lane, g, p);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) rows.v[i] = (rows.v[i] >> (L - 1)) & 1ull;
+  return rows;
+}
+
+// Boolean bit -> arithmetic share (b2a, gadgets.py:223-231); bit 0 of b.
+// dealer fields: A0=0 A1=1 bits=2 (beta=bit0, Bb0=bit1, Bb1=bit2).
+template <int L>
+__device__ __forceinline__ A3 b2a(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const B3& b) {
+  constexpr uint64_t M = Ring<L>::M;
+  const W2 w = word2(K.dealer, op, sub, 0, lane);
+  const uint64_t A0 = w.a & M, A1 = w.b & M;
+  const uint64_t bw = word(K.dealer, op, sub, 2, lane);
+  const uint64_t beta = bw & 1ull, Bb0 = (bw >> 1) & 1ull, Bb1 = (bw >> 2) & 1ull;
+  const uint64_t Bb2 = beta ^ Bb0 ^ Bb1;
+  const uint64_t A2 = (beta - A0 - A1) & M;  // _gen_dabits, dealer.py:420-424
+  const uint64_t e = ((b.v[0] ^ Bb0) ^ (b.v[1] ^ Bb1) ^ (b.v[2] ^ Bb2)) & 1ull;  // open_bits
+  const uint64_t coeff = (1ull - 2ull * e) & M;
+  return a3(((A0 * coeff) + e) & M, (A1 * coeff) & M, (A2 * coeff) & M);
+}
+
+// select_share (gadgets.py:238-253) for one condition lane and one payload
+// element: w1 + b2a(c) * (w2 - w1); b2a at `sub`, mul at `sub + 1`, `field`
+// = payload index inside the condition's group.
+template <int L>
+__device__ __forceinline__ A3 select_with(const Keys& K, uint32_t op, uint32_t sub, uint32_t field, uint64_t lane,
+                                          const A3& w1, const A3& w2, const A3& ca) {
+  return add<L>(w1, mul<L>(K, op, sub + 1, field, lane, diff<L>(w2, w1), ca));
+}
+template <int L>
+__device__ __forceinline__ A3 select1(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const A3& w1,
+                                      const A3& w2, const B3& cond) {
+  const A3 ca = b2a<L>(K, op, sub, lane, cond);
+  return select_with<L>(K, op, sub, 0, lane, w1, w2, ca);
+}
+
+// Exact floor(x / 2^k), unsigned (truncate, gadgets.py:260-288).  Uses subs
+// sub (opening + borrow scan, dealer fields r=0 Rb0=1 Rb1=2 R0=3 R1=4 S0=5
+// S1=6), sub+1 (b2a of the wrap bit), sub+2 (b2a of the low borrow).
+template <int L>
+__device__ __forceinline__ A3 trunc(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const A3& x, int k) {
+  constexpr uint64_t M = Ring<L>::M;
+  if (k == 0) return x;
+  const uint64_t r = word(K.dealer, op, sub, 0, lane) & M;
+  B3 Rb;
+  Rb.v[0] = word(K.dealer, op, sub, 1, lane) & M;
+  Rb.v[1] = word(K.dealer, op, sub, 2, lane) & M;
+  Rb.v[2] = r ^ Rb.v[0] ^ Rb.v[1];
+  const uint64_t R0 = word(K.dealer, op, sub, 3, lane) & M, R1 = word(K.dealer, op, sub, 4, lane) & M;
+  const uint64_t S0 = word(K.dealer, op, sub, 5, lane) & M, S1 = word(K.dealer, op, sub, 6, lane) & M;
+  const uint64_t S2 = ((r >> k) - S0 - S1) & M;  // _gen_truncpairs, dealer.py:427-432
+  const uint64_t c = open<L>(a3(x.v[0] + R0, x.v[1] + R1, x.v[2] + (r - R0 - R1)));
+  const B3 s = borrow_scan<L>(K, op, sub, 0, lane, c, Rb);
+  B3 wrap, lowb;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    wrap.v[i] = (s.v[i] >> (L - 1)) & 1ull;
+    lowb.v[i] = (s.v[i] >> (k - 1)) & 1ull;
+  }
+  const A3 wa = b2a<L>(K, op, sub + 1, lane, wrap);
+  const A3 ba = b2a<L>(K, op, sub + 2, lane, lowb);
+  const uint64_t sh = (1ull << (L - k)) & M;
+  A3 out = a3((wa.v[0] * sh - S0 - ba.v[0]) & M, (wa.v[1] * sh - S1 - ba.v[1]) & M,
+              (wa.v[2] * sh - S2 - ba.v[2]) & M);
+  return add_pub<L>(out, c >> k);
+}
+
+// Public fixed-point division schedule (div_params, gadgets.py:297-307).
+struct DivParams {
+  int bound, ti, sigma, kf, iters;
+  uint64_t w0;
+};
+// subs consumed by division(): 2*(bound-1) ladder subs + 8*iters + 12
+__host__ __device__ inline int div_subs(const DivParams& d) { return 2 * (d.bound - 1) + 8 * d.iters + 12; }
+
+// Ladder step j (1 <= j < bound): t_j = b2a(~[q < 2^j]) (gadgets.py:327-332).
+template <int L>
+__device__ __forceinline__ A3 div_ladder_term(const Keys& K, uint32_t op, uint32_t sub0, uint64_t lane, const A3& q,
+                                              int j, const DivParams& d) {
+  constexpr uint64_t M = Ring<L>::M;
+  const B3 below = lt<L>(K, op, sub0 + (j - 1), lane, q, a3_const((1ull << j) & M));
+  const A3 t = b2a<L>(K, op, sub0 + (d.bound - 1) + (j - 1), lane, bnot(below, 1ull));
+  return mul_pub<L>(t, 1ull << (d.bound - 1 - j));
+}
+
+// Newton part of division once v = 2^{B - bitlen(q)} is shared
+// (gadgets.py:338-349).  `sub` = first sub after the ladder.
+template <int L>
+__device__ __forceinline__ A3 div_newton(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const A3& p,
+                                         const A3& q, const A3& v, const DivParams& d) {
+  const A3 qn = mul<L>(K, op, sub, 0, lane, q, v);
+  const A3 qnorm = trunc<L>(K, op, sub + 1, lane, qn, d.bound - d.ti);
+  sub += 4;
+  A3 w = rsub_pub<L>(d.w0, mul_pub<L>(qnorm, 2));
+  for (int it = 0; it < d.iters; ++it) {
+    const A3 t = trunc<L>(K, op, sub + 1, lane, mul<L>(K, op, sub, 0, lane, qnorm, w), d.ti);
+    const A3 e = rsub_pub<L>(1ull << (d.ti + 1), t);
+    w = trunc<L>(K, op, sub + 5, lane, mul<L>(K, op, sub + 4, 0, lane, w, e), d.ti);
+    sub += 8;
+  }
+  A3 pn = mul<L>(K, op, sub, 0, lane, p, v);
+  if (d.sigma) pn = trunc<L>(K, op, sub + 1, lane, pn, d.sigma);
+  const A3 prod = add_pub<L>(mul<L>(K, op, sub + 4, 0, lane, pn, w), 1ull << (d.kf - 1));
+  return trunc<L>(K, op, sub + 5, lane, prod, d.kf);
+}
+
+// Full serial division for one lane (division, gadgets.py:310-349).
+template <int L>
+__device__ __forceinline__ A3 division(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const A3& p,
+                                       const A3& q, const DivParams& d) {
+  A3 acc = a3(0, 0, 0);
+  for (int j = 1; j < d.bound; ++j) acc = add<L>(acc, div_ladder_term<L>(K, op, sub, lane, q, j, d));
+  const A3 v = rsub_pub<L>(1ull << (d.bound - 1), acc);
+  return div_newton<L>(K, op, sub + 2 * (d.bound - 1), lane, p, q, v, d);
+}
+
+}  // namespace gt

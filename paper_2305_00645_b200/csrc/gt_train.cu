@@ -1,0 +1,764 @@
+// Secure level-wise training on device (reference train_tree,
+// pkg/src/obtree/train.py:222-311, heuristic "mpc", fixed/grow policies).
+//
+// Per level h (n_h = 2^h nodes, W = 2nf+1 sample columns):
+//   k_partition   (h > 0)  oaa on level h-1 payloads + row_lookup on features,
+//                          m_idx = 2 m_idx + d + 1             train.py:248-253
+//   k_count                one lane per (sample, node): eq, and is_leaf, b2a,
+//                          W products with reshare, summed over samples
+//                          into S[n][w] (+ mask column)        train.py:315-335
+//   allreduce(S)           sample-sharded runs only (linear in shares)
+//   k_node_hc              one CTA per node: counter assembly, _heuristic_mpc
+//                          (division ladder + Newton, masked argmin, budget
+//                          clear), replace                      train.py:256-276
+//   k_node_stop   (grow)   opened stop bit                     train.py:279-282
+//   k_node_finish          split (payload / child type / child counters) or
+//                          labels on the last level            train.py:284-306
+// Every lane's randomness is keyed by (op, sub, field, global lane), so the
+// shares produced are independent of sharding and of launch geometry.
+#include <algorithm>
+
+#include "gt_common.cuh"
+#include "gt_lookup.cuh"
+
+namespace gt {
+namespace {
+
+constexpr uint64_t F_LEAF = 1, F_DUMMY = 2;  // tree.py:40-42
+
+__device__ __forceinline__ A3 ld3s(const uint64_t* p, uint64_t stride, uint64_t i) {
+  return a3(p[i], p[stride + i], p[2 * stride + i]);
+}
+__device__ __forceinline__ void st3s(uint64_t* p, uint64_t stride, uint64_t i, const A3& a) {
+  p[i] = a.v[0];
+  p[stride + i] = a.v[1];
+  p[2 * stride + i] = a.v[2];
+}
+__device__ __forceinline__ B3 ldb3s(const uint64_t* p, uint64_t stride, uint64_t i) {
+  B3 b;
+  b.v[0] = p[i];
+  b.v[1] = p[stride + i];
+  b.v[2] = p[2 * stride + i];
+  return b;
+}
+
+// ---------------------------------------------------------------------------
+// init + count:0 products
+// ---------------------------------------------------------------------------
+
+__global__ void k_init(uint64_t* f, uint64_t* gam, uint64_t* cst, uint64_t fstride, uint64_t cstride, int cols,
+                       int nf) {
+  // f_level = const(1), gam = const bits(ones), c_start = 0   (train.py:235-238)
+  int t = threadIdx.x;
+  if (t < 3) {
+    f[t * fstride] = t == 0 ? F_LEAF : 0;
+    gam[t * fstride] = t == 0 ? lowmask(nf) : 0;
+  }
+  for (int e = t; e < 3 * cols; e += blockDim.x)
+    for (int c = 0; c < 3; ++c) cst[c * cstride + e] = 0;
+}
+
+__global__ void k_prods(const uint64_t* X, const uint64_t* Y, uint64_t* P, uint64_t N, int nf, uint64_t base, Keys K,
+                        uint32_t op) {
+  // prods = mul(features, labels[:, None])                     train.py:229-230
+  uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t total = N * (uint64_t)nf;
+  if (e >= total) return;
+  uint64_t s = e / nf;
+  uint32_t f = (uint32_t)(e % nf);
+  st3s(P, total, e, mul<64>(K, op, 0, f, base + s, ld3s(X, total, e), ld3s(Y, N, s)));
+}
+
+// ---------------------------------------------------------------------------
+// partition
+// ---------------------------------------------------------------------------
+
+template <int G>
+__global__ void k_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint64_t slots, int m, int nf,
+                            uint64_t N, uint64_t base, Keys K, uint32_t op_oaa, uint32_t op_row) {
+  extern __shared__ uint64_t tab[];  // [3][m] level h-1 payload table
+  for (int i = threadIdx.x; i < 3 * m; i += blockDim.x) tab[i] = T[(uint64_t)(i / m) * slots + (m - 1) + (i % m)];
+  __syncthreads();
+  const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t s = gt / G;
+  const int t = (int)(gt % G);
+  const bool valid = s < N;
+  const uint64_t nfx = N * (uint64_t)nf;
+  A3 idx = a3(0, 0, 0), part = a3(0, 0, 0);
+  if (valid) {
+    idx = ld3s(midx, N, s);
+    const A3 local = add_pub<64>(idx, 0ull - (uint64_t)(m - 1));
+    auto entry = [&](int j) { return a3(tab[j], tab[m + j], tab[2 * m + j]); };
+    part = lookup_partial<64>(K, op_oaa, base + s, local, m, t, G, entry);
+  }
+  const A3 feat = group_sum<G, 64>(part);
+  A3 part2 = a3(0, 0, 0);
+  if (valid) {
+    auto entry = [&](int f) { return ld3s(X, nfx, s * nf + f); };
+    part2 = lookup_partial<64>(K, op_row, base + s, feat, nf, t, G, entry);
+  }
+  const A3 dval = group_sum<G, 64>(part2);
+  if (valid && t == 0) st3s(midx, N, s, add_pub<64>(add<64>(mul_pub<64>(idx, 2), dval), 1));
+}
+
+// ---------------------------------------------------------------------------
+// count
+// ---------------------------------------------------------------------------
+
+constexpr int CNT_TPB = 256;
+constexpr int CNT_ITEMS = 4;
+
+struct CountArgs {
+  const uint64_t *X, *P, *Y, *midx, *f;
+  uint64_t* S;  // [3][n_h][W+1]
+  uint64_t N, base;
+  int nf, n_h, off, nb, ts, tiles_per_cta;
+  Keys K;
+  uint32_t op_leaf, op_cnt;
+};
+
+__global__ void __launch_bounds__(CNT_TPB) k_count(CountArgs a) {
+  extern __shared__ uint64_t sm[];
+  const int nf = a.nf, W = 2 * nf + 1, WP = nf + 1, NB = a.nb, TS = a.ts;
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int n0 = blockIdx.y * NB;
+  const int nb = min(NB, a.n_h - n0);
+  uint64_t* cols = sm;                  // [3][TS][W]
+  uint64_t* la = cols + 3 * TS * W;     // [3][TS][NB]
+  uint64_t* leaf = la + 3 * TS * NB;    // [3][NB]
+  const Keys& K = a.K;
+  const uint64_t nfx = a.N * (uint64_t)nf;
+
+  // is_leaf = eq(F_level, LEAF) (train.py:320); identical in every CTA
+  for (int t = tid; t < nb; t += bd) {
+    const B3 z = eqz<64>(K, a.op_leaf, 0, (uint64_t)(n0 + t), add_pub<64>(ld3s(a.f, a.n_h, n0 + t), 0ull - F_LEAF));
+    for (int c = 0; c < 3; ++c) leaf[c * NB + t] = z.v[c] & 1ull;
+  }
+
+  // work items (node n, column pair wp); replicas split the tile's samples
+  const int P = nb * WP;
+  const int R = P >= bd ? 1 : bd / P;
+  int item[CNT_ITEMS];
+  int nitems = 0, q = 0;
+  if (R > 1) {
+    if (tid < P * R) {
+      item[0] = tid % P;
+      q = tid / P;
+      nitems = 1;
+    }
+  } else {
+    for (int k = 0; k < CNT_ITEMS; ++k)
+      if (tid + k * bd < P) item[nitems++] = tid + k * bd;
+  }
+  uint64_t acc[CNT_ITEMS][2][3];
+#pragma unroll
+  for (int k = 0; k < CNT_ITEMS; ++k)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[k][h][c] = 0;
+
+  const uint64_t tile0 = (uint64_t)blockIdx.x * a.tiles_per_cta;
+  for (int tt = 0; tt < a.tiles_per_cta; ++tt) {
+    const uint64_t s0 = (tile0 + tt) * (uint64_t)TS;
+    if (s0 >= a.N) break;
+    const int cnt = (int)min((uint64_t)TS, a.N - s0);
+    __syncthreads();
+    for (int e = tid; e < cnt * W; e += bd) {
+      const int s = e / W, w = e % W;
+      const uint64_t sg = s0 + s;
+      for (int c = 0; c < 3; ++c) {
+        uint64_t v;
+        if (w < nf) v = a.X[c * nfx + sg * nf + w];
+        else if (w < 2 * nf) v = a.P[c * nfx + sg * nf + (w - nf)];
+        else v = a.Y[c * a.N + sg];
+        cols[(c * TS + s) * W + w] = v;
+      }
+    }
+    // lanes (s, n): la = b2a(eq(m_idx, off + n) & is_leaf[n])  train.py:328-331
+    for (int e = tid; e < cnt * nb; e += bd) {
+      const int s = e / nb, n = e % nb;
+      const uint64_t lane = (a.base + s0 + s) * (uint64_t)a.n_h + (uint64_t)(n0 + n);
+      const A3 d = add_pub<64>(ld3s(a.midx, a.N, s0 + s), 0ull - (uint64_t)(a.off + n0 + n));
+      const B3 hit = eqz<64>(K, a.op_cnt, 0, lane, d);
+      B3 lf;
+      for (int c = 0; c < 3; ++c) lf.v[c] = leaf[c * NB + n];
+      const B3 lcf = and_gate(K, a.op_cnt, 1, 0, lane, hit, lf, 1ull);
+      const A3 l = b2a<64>(K, a.op_cnt, 2, lane, lcf);
+      for (int c = 0; c < 3; ++c) la[(c * TS + s) * NB + n] = l.v[c];
+    }
+    __syncthreads();
+    // contrib = mul(rows, la) summed over samples        train.py:332-335
+#pragma unroll
+    for (int k = 0; k < CNT_ITEMS; ++k) {
+      if (k >= nitems) break;
+      const int n = item[k] / WP, wp = item[k] % WP;
+      const int w0 = 2 * wp, w1 = 2 * wp + 1;
+      for (int s = q; s < cnt; s += R) {
+        const uint64_t lane = (a.base + s0 + s) * (uint64_t)a.n_h + (uint64_t)(n0 + n);
+        const A3 l = a3(la[(0 * TS + s) * NB + n], la[(1 * TS + s) * NB + n], la[(2 * TS + s) * NB + n]);
+        const W2 F0 = word2(K.pair[0], a.op_cnt, 3, wp, lane);
+        const W2 F1 = word2(K.pair[1], a.op_cnt, 3, wp, lane);
+        const W2 F2 = word2(K.pair[2], a.op_cnt, 3, wp, lane);
+        {
+          const uint64_t Fa[3] = {F0.a, F1.a, F2.a};
+          const A3 y = a3(cols[(0 * TS + s) * W + w0], cols[(1 * TS + s) * W + w0], cols[(2 * TS + s) * W + w0]);
+          const A3 z = mul_z<64>(y, l, Fa);
+          for (int c = 0; c < 3; ++c) acc[k][0][c] += z.v[c];
+        }
+        if (w1 < W) {
+          const uint64_t Fb[3] = {F0.b, F1.b, F2.b};
+          const A3 y = a3(cols[(0 * TS + s) * W + w1], cols[(1 * TS + s) * W + w1], cols[(2 * TS + s) * W + w1]);
+          const A3 z = mul_z<64>(y, l, Fb);
+          for (int c = 0; c < 3; ++c) acc[k][1][c] += z.v[c];
+        } else {  // mask column: s_mask += la (local)
+          for (int c = 0; c < 3; ++c) acc[k][1][c] += l.v[c];
+        }
+      }
+    }
+  }
+  const uint64_t Sstride = (uint64_t)a.n_h * (W + 1);
+  for (int k = 0; k < nitems; ++k) {
+    const int n = item[k] / WP, wp = item[k] % WP;
+    for (int h = 0; h < 2; ++h) {
+      const int w = 2 * wp + h;
+      for (int c = 0; c < 3; ++c)
+        atomicAdd((unsigned long long*)&a.S[c * Sstride + (uint64_t)(n0 + n) * (W + 1) + w],
+                  (unsigned long long)acc[k][h][c]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// per-node step: counters, heuristic (mpc), replace
+// ---------------------------------------------------------------------------
+
+struct NodeArgs {
+  const uint64_t* S;          // [3][n_h][W+1]
+  const uint64_t* cst;        // [3][n_h][3][cols]
+  const uint64_t* f;          // [3][n_h]
+  const uint64_t* gam;        // [3][n_h] feature-budget bit words
+  const uint64_t* ceff_prev;  // [3][n_h/2][3][cols]
+  uint64_t* ceff;             // [3][n_h][3][cols]
+  uint64_t* hc;               // [4][3][n_h]: should_split, sd, new_f, new_gam
+  int n_h, nf, level, last, shift, tau;
+  DivParams d;
+  Keys K;
+};
+
+template <int SL>
+__global__ void __launch_bounds__(256) k_node_hc(NodeArgs a) {
+  extern __shared__ uint64_t sm[];
+  constexpr uint64_t MS = Ring<SL>::M;
+  const int n = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
+  const int nf = a.nf, cols = 2 * nf, W = cols + 1, n_h = a.n_h;
+  const int C3 = 3 * cols;
+  uint64_t* co = sm;              // [3][3*cols] c_orig
+  uint64_t* c32 = co + 3 * C3;    // [3][3*cols] truncated + ring_down
+  uint64_t* pr = c32 + 3 * C3;    // [3][4*cols] products
+  uint64_t* pv = pr + 12 * cols;  // [3][cols]
+  uint64_t* qs = pv + 3 * cols;
+  uint64_t* vac = qs + 3 * cols;
+  uint64_t* tm = vac + 3 * cols;
+  uint64_t* vals = tm + 3 * cols;  // [3][nf]
+  uint64_t* idxs = vals + 3 * nf;
+  uint64_t* nvals = idxs + 3 * nf;
+  uint64_t* nidxs = nvals + 3 * nf;
+  uint64_t* misc = nidxs + 3 * nf;  // zeros[3][3], hitw[3], ss[3], ca[3]
+  const Keys& K = a.K;
+  const uint32_t opH = op_id(a.level, SITE_HC), opR = op_id(a.level, SITE_REPLACE);
+  const uint64_t hs = (uint64_t)n_h;
+
+  // c_orig = c_start + assembled counters (train.py:256, 336-343)
+  for (int e = tid; e < 3 * C3; e += bd) {
+    const int c = e / C3, rk = e % C3, r = rk / cols, k = rk % cols, i = k >> 1, j = k & 1;
+    const uint64_t* Sn = a.S + (uint64_t)c * hs * (W + 1) + (uint64_t)n * (W + 1);
+    const uint64_t s1 = Sn[W], sx = Sn[i], sp = Sn[nf + i], sy = Sn[2 * nf];
+    uint64_t v;
+    if (r == 0) v = j ? sx : s1 - sx;
+    else if (r == 1) v = j ? sx - sp : s1 - sx - sy + sp;
+    else v = j ? sp : sy - sp;
+    co[e] = a.cst[(uint64_t)c * hs * C3 + (uint64_t)n * C3 + rk] + v;
+  }
+  __syncthreads();
+  auto CO = [&](int e) { return a3(co[e], co[C3 + e], co[2 * C3 + e]); };
+
+  if (!a.last) {
+    const A3 fl = ld3s(a.f, hs, n);
+    const B3 gam = ldb3s(a.gam, hs, n);
+    // zeros = eq([psi0, psi1, F - LEAF], 0)                 train.py:353-359
+    if (tid < 3) {
+      A3 v;
+      if (tid == 0) v = add<64>(CO(cols + 0), CO(cols + 1));
+      else if (tid == 1) v = add<64>(CO(2 * cols + 0), CO(2 * cols + 1));
+      else v = add_pub<64>(fl, 0ull - F_LEAF);
+      const B3 z = eqz<64>(K, opH, 0, (uint64_t)n * 3 + tid, v);
+      for (int c = 0; c < 3; ++c) misc[c * 3 + tid] = z.v[c] & 1ull;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      B3 p0, p1, act;
+      for (int c = 0; c < 3; ++c) {
+        p0.v[c] = misc[c * 3 + 0];
+        p1.v[c] = misc[c * 3 + 1];
+        act.v[c] = misc[c * 3 + 2];
+      }
+      // featureless = and_reduce(~gam), leafish, should_split   train.py:360-364
+      const B3 fless = and_reduce(K, opH, 1, 0, n, bnot(gam, lowmask(nf)), nf);
+      const B3 o1 = or_gate(K, opH, 2, n, p0, p1, 1ull);
+      const B3 leafish = or_gate(K, opH, 3, n, o1, fless, 1ull);
+      const B3 ss = and_gate(K, opH, 4, 0, n, act, bnot(leafish, 1ull), 1ull);
+      const A3 nf_sh = select1<64>(K, opH, 5, n, fl, a3(0, 0, 0), ss);
+      for (int c = 0; c < 3; ++c) {
+        a.hc[(0 * 3 + c) * hs + n] = ss.v[c] & 1ull;
+        a.hc[(2 * 3 + c) * hs + n] = nf_sh.v[c];
+      }
+    }
+    // counters: truncate by the public shift, ring_down      train.py:366-370
+    for (int e = tid; e < C3; e += bd) {
+      A3 x = CO(e);
+      if (a.shift) x = trunc<64>(K, opH, 7, (uint64_t)n * C3 + e, x, a.shift);
+      for (int c = 0; c < 3; ++c) c32[c * C3 + e] = x.v[c] & MS;
+    }
+    __syncthreads();
+    auto C32 = [&](int e) { return a3(c32[e], c32[C3 + e], c32[2 * C3 + e]); };
+    // prods = mul([c32, a], [c32, tot_rep])                   train.py:371-376
+    for (int e = tid; e < 4 * cols; e += bd) {
+      A3 x, y;
+      if (e < C3) {
+        x = C32(e);
+        y = x;
+      } else {
+        const int k = e - C3, i = k >> 1;
+        x = C32(k);
+        y = add<SL>(C32(2 * i), C32(2 * i + 1));
+      }
+      const A3 z = mul<SL>(K, opH, 10, 0, (uint64_t)n * 4 * cols + e, x, y);
+      for (int c = 0; c < 3; ++c) pr[c * 4 * cols + e] = z.v[c];
+    }
+    __syncthreads();
+    auto PR = [&](int e) { return a3(pr[e], pr[4 * cols + e], pr[8 * cols + e]); };
+    // P = a^2 - m0^2 - m1^2, qsafe = Q + b2a(eq(Q, 0))       train.py:377-381
+    for (int k = tid; k < cols; k += bd) {
+      const A3 p = diff<SL>(diff<SL>(PR(k), PR(cols + k)), PR(2 * cols + k));
+      const A3 q = PR(C3 + k);
+      const uint64_t lane = (uint64_t)n * cols + k;
+      const B3 qz = eqz<SL>(K, opH, 11, lane, q);
+      const A3 qsv = add<SL>(q, b2a<SL>(K, opH, 12, lane, qz));
+      for (int c = 0; c < 3; ++c) {
+        pv[c * cols + k] = p.v[c];
+        qs[c * cols + k] = qsv.v[c];
+        vac[c * cols + k] = 0;
+      }
+    }
+    __syncthreads();
+    auto QS = [&](int k) { return a3(qs[k], qs[cols + k], qs[2 * cols + k]); };
+    // division ladder: one lane per (column, power)         gadgets.py:327-336
+    const int nl = a.d.bound - 1;
+    for (int e = tid; e < nl * cols; e += bd) {
+      const int j = e / cols + 1, k = e % cols;
+      const A3 t = div_ladder_term<SL>(K, opH, 13, (uint64_t)n * cols + k, QS(k), j, a.d);
+      for (int c = 0; c < 3; ++c) atomicAdd((unsigned long long*)&vac[c * cols + k], (unsigned long long)t.v[c]);
+    }
+    __syncthreads();
+    // Newton reciprocal + rescale per column                gadgets.py:338-349
+    for (int k = tid; k < cols; k += bd) {
+      const A3 acc = a3(vac[k] & MS, vac[cols + k] & MS, vac[2 * cols + k] & MS);
+      const A3 v = rsub_pub<SL>(1ull << (a.d.bound - 1), acc);
+      const A3 p = a3(pv[k], pv[cols + k], pv[2 * cols + k]);
+      const A3 t = div_newton<SL>(K, opH, 13 + 2 * nl, (uint64_t)n * cols + k, p, QS(k), v, a.d);
+      for (int c = 0; c < 3; ++c) tm[c * cols + k] = t.v[c];
+    }
+    __syncthreads();
+    // scores + masked argmin (tournament)     train.py:383-385, gadgets.py:366-401
+    const uint32_t SA = 13 + div_subs(a.d);
+    const uint64_t worst = (1ull << (a.tau + 1)) & MS;
+    for (int i = tid; i < nf; i += bd) {
+      const A3 score = add<SL>(a3(tm[2 * i], tm[cols + 2 * i], tm[2 * cols + 2 * i]),
+                               a3(tm[2 * i + 1], tm[cols + 2 * i + 1], tm[2 * cols + 2 * i + 1]));
+      B3 av;
+      for (int c = 0; c < 3; ++c) av.v[c] = (gam.v[c] >> i) & 1ull;
+      const A3 v = select1<SL>(K, opH, SA, (uint64_t)n * nf + i, a3_const(worst), score, av);
+      for (int c = 0; c < 3; ++c) {
+        vals[c * nf + i] = v.v[c];
+        idxs[c * nf + i] = c == 0 ? (uint64_t)i : 0ull;
+      }
+    }
+    __syncthreads();
+    int m = nf;
+    for (int r = 0; m > 1; ++r) {
+      const int pairs = m / 2;
+      const uint32_t base = SA + 2 + 5 * r;
+      for (int p = tid; p < pairs; p += bd) {
+        const uint64_t lane = (uint64_t)n * nf + p;
+        const A3 av = a3(vals[2 * p], vals[nf + 2 * p], vals[2 * nf + 2 * p]);
+        const A3 bv = a3(vals[2 * p + 1], vals[nf + 2 * p + 1], vals[2 * nf + 2 * p + 1]);
+        const A3 ai = a3(idxs[2 * p], idxs[nf + 2 * p], idxs[2 * nf + 2 * p]);
+        const A3 bi = a3(idxs[2 * p + 1], idxs[nf + 2 * p + 1], idxs[2 * nf + 2 * p + 1]);
+        const B3 cw = lt<SL>(K, opH, base, lane, bv, av);
+        const A3 nv = select1<SL>(K, opH, base + 1, lane, av, bv, cw);
+        const A3 ni = select1<64>(K, opH, base + 3, lane, ai, bi, cw);
+        for (int c = 0; c < 3; ++c) {
+          nvals[c * nf + p] = nv.v[c];
+          nidxs[c * nf + p] = ni.v[c];
+        }
+      }
+      if (tid == 0 && (m & 1))
+        for (int c = 0; c < 3; ++c) {
+          nvals[c * nf + pairs] = vals[c * nf + m - 1];
+          nidxs[c * nf + pairs] = idxs[c * nf + m - 1];
+        }
+      __syncthreads();
+      const int nm = pairs + (m & 1);
+      for (int p = tid; p < nm; p += bd)
+        for (int c = 0; c < 3; ++c) {
+          vals[c * nf + p] = nvals[c * nf + p];
+          idxs[c * nf + p] = nidxs[c * nf + p];
+        }
+      __syncthreads();
+      m = nm;
+    }
+    const A3 sd = a3(idxs[0], idxs[nf], idxs[2 * nf]);
+    // gamma &= ~[sd == k]                                     train.py:386-387
+    const uint32_t SH = SA + 2 + 5 * 7;
+    uint64_t* hitw = misc + 9;
+    if (tid < 3) hitw[tid] = 0;
+    __syncthreads();
+    for (int f = tid; f < nf; f += bd) {
+      const B3 h = eqz<64>(K, opH, SH, (uint64_t)n * nf + f, add_pub<64>(sd, 0ull - (uint64_t)f));
+      for (int c = 0; c < 3; ++c) atomicOr((unsigned long long*)&hitw[c], (unsigned long long)((h.v[c] & 1ull) << f));
+    }
+    __syncthreads();
+    if (tid == 0) {
+      B3 hw;
+      for (int c = 0; c < 3; ++c) hw.v[c] = hitw[c];
+      const B3 ng = and_gate(K, opH, SH + 1, 0, n, gam, bnot(hw, lowmask(nf)), lowmask(nf));
+      for (int c = 0; c < 3; ++c) {
+        a.hc[(1 * 3 + c) * hs + n] = sd.v[c];
+        a.hc[(3 * 3 + c) * hs + n] = ng.v[c];
+      }
+    }
+  }
+
+  // replace: empty nodes adopt the parent's effective counters  train.py:269-276
+  uint64_t* ca = misc + 12;
+  if (a.level > 0) {
+    if (tid == 0) {
+      const B3 ie = eqz<64>(K, opR, 0, n, add<64>(CO(0), CO(1)));
+      const A3 c = b2a<64>(K, opR, 1, n, ie);
+      for (int i = 0; i < 3; ++i) ca[i] = c.v[i];
+    }
+    __syncthreads();
+    const A3 cav = a3(ca[0], ca[1], ca[2]);
+    const uint64_t pn = (uint64_t)(n >> 1);
+    for (int e = tid; e < C3; e += bd) {
+      const A3 par = ld3s(a.ceff_prev, (hs / 2) * C3, pn * C3 + e);
+      st3s(a.ceff, hs * C3, (uint64_t)n * C3 + e, select_with<64>(K, opR, 1, (uint32_t)e, n, CO(e), par, cav));
+    }
+  } else {
+    for (int e = tid; e < C3; e += bd) st3s(a.ceff, hs * C3, (uint64_t)n * C3 + e, CO(e));
+  }
+}
+
+// grow policy: all_declined = open(and_reduce(~is_int over nodes)) (train.py:279-282)
+__global__ void k_node_stop(const uint64_t* hc, int n_h, Keys K, uint32_t op, uint64_t* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  B3 w;
+  for (int c = 0; c < 3; ++c) {
+    uint64_t x = 0;
+    for (int n = 0; n < n_h; ++n) x |= (hc[c * (uint64_t)n_h + n] & 1ull) << n;
+    w.v[c] = x;
+  }
+  const B3 r = and_reduce(K, op, 0, 0, 0, bnot(w, lowmask(n_h)), n_h);
+  out[0] = (r.v[0] ^ r.v[1] ^ r.v[2]) & 1ull;  // open_bits
+}
+
+struct FinishArgs {
+  const uint64_t* hc;      // [4][3][n_h]
+  const uint64_t* ceff;    // [3][n_h][3][cols]
+  const uint64_t* f;       // [3][n_h]
+  const uint64_t* filler;  // public [slots]
+  uint64_t *T, *F;         // [3][slots]
+  uint64_t *f_nxt, *gam_nxt, *cst_nxt;  // children
+  uint64_t slots;
+  int n_h, nf, level, labels;
+  Keys K;
+};
+
+__global__ void __launch_bounds__(128) k_node_finish(FinishArgs a) {
+  __shared__ uint64_t ca[3];
+  const int n = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
+  const int cols = 2 * a.nf, C3 = 3 * cols;
+  const uint64_t hs = (uint64_t)a.n_h, slot = hs - 1 + n;
+  const Keys& K = a.K;
+  auto CE = [&](int e) { return ld3s(a.ceff, hs * C3, (uint64_t)n * C3 + e); };
+  if (a.labels) {
+    // labels = b2a(lt(psi0, psi1)) on effective counters      train.py:300-306
+    if (tid == 0) {
+      const uint32_t op = op_id(a.level, SITE_LABELS);
+      const A3 psi0 = add<64>(CE(cols), CE(cols + 1)), psi1 = add<64>(CE(2 * cols), CE(2 * cols + 1));
+      const A3 lab = b2a<64>(K, op, 1, n, lt<64>(K, op, 0, n, psi0, psi1));
+      st3s(a.T, a.slots, slot, lab);
+      st3s(a.F, a.slots, slot, ld3s(a.f, hs, n));
+    }
+    return;
+  }
+  const uint32_t op = op_id(a.level, SITE_SPLIT);
+  B3 ss;
+  for (int c = 0; c < 3; ++c) ss.v[c] = a.hc[(0 * 3 + c) * hs + n];
+  const uint64_t cs = 2 * hs;  // children per level
+  if (tid == 0) {
+    // payload, child type (train.py:286-289)
+    const A3 sd = ld3s(a.hc + 3 * hs, hs, n);
+    const A3 t = select_with<64>(K, op, 0, 0, n, a3_const(a.filler[slot]), sd, b2a<64>(K, op, 0, n, ss));
+    const A3 cf = select_with<64>(K, op, 2, 0, n, a3_const(F_DUMMY), a3_const(F_LEAF), b2a<64>(K, op, 2, n, ss));
+    const A3 c2 = b2a<64>(K, op, 4, n, ss);
+    for (int c = 0; c < 3; ++c) ca[c] = c2.v[c];
+    st3s(a.T, a.slots, slot, t);
+    st3s(a.F, a.slots, slot, ld3s(a.hc + 6 * hs, hs, n));
+    const A3 ng = ld3s(a.hc + 9 * hs, hs, n);
+    for (int ch = 0; ch < 2; ++ch) {
+      st3s(a.f_nxt, cs, 2 * n + ch, cf);
+      st3s(a.gam_nxt, cs, 2 * n + ch, ng);
+    }
+  }
+  __syncthreads();
+  // child counters = select(c_eff, 0, is_int)                 train.py:290
+  const A3 cav = a3(ca[0], ca[1], ca[2]);
+  for (int e = tid; e < C3; e += bd) {
+    const A3 cc = select_with<64>(K, op, 4, (uint32_t)e, n, CE(e), a3(0, 0, 0), cav);
+    for (int ch = 0; ch < 2; ++ch) st3s(a.cst_nxt, cs * C3, (uint64_t)(2 * n + ch) * C3 + e, cc);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// workspace
+// ---------------------------------------------------------------------------
+
+struct Layout {
+  uint64_t prods, midx, S, f[2], gam[2], cst[2], ceff[2], hc, stop, total;  // word offsets
+};
+
+Layout layout(const gt_train_cfg& c) {
+  const uint64_t N = c.n_local, nf = (uint64_t)c.nf, cols = 2 * nf, W = cols + 1;
+  const uint64_t nmax = 1ull << (c.depth - 1), ch = 2 * nmax;
+  Layout L;
+  uint64_t o = 0;
+  auto take = [&](uint64_t words) {
+    uint64_t r = o;
+    o += (words + 31) & ~31ull;  // 256-byte alignment
+    return r;
+  };
+  L.prods = take(3 * N * nf);
+  L.midx = take(3 * N);
+  L.S = take(3 * nmax * (W + 1));
+  for (int i = 0; i < 2; ++i) {
+    L.f[i] = take(3 * ch);
+    L.gam[i] = take(3 * ch);
+    L.cst[i] = take(3 * ch * 3 * cols);
+    L.ceff[i] = take(3 * nmax * 3 * cols);
+  }
+  L.hc = take(12 * nmax);
+  L.stop = take(4);
+  L.total = o;
+  return L;
+}
+
+int node_smem_bytes(int nf) {
+  const int cols = 2 * nf;
+  return (int)sizeof(uint64_t) * (9 * cols + 9 * cols + 12 * cols + 12 * cols + 12 * nf + 16);
+}
+
+template <int SL>
+int launch_node_hc(const NodeArgs& na, cudaStream_t s) {
+  const int smem = node_smem_bytes(na.nf);
+  if (smem > 48 * 1024) GT_CUDA_CHECK(cudaFuncSetAttribute(k_node_hc<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k_node_hc<SL><<<na.n_h, 256, smem, s>>>(na);
+  GT_LAUNCH_CHECK("k_node_hc");
+  return GT_OK;
+}
+
+int launch_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint64_t slots, int m, int nf, uint64_t N,
+                     uint64_t base, const Keys& K, int level, cudaStream_t s) {
+  constexpr int G = 8, TPB = 256;
+  const uint64_t threads = N * G;
+  const unsigned grid = (unsigned)((threads + TPB - 1) / TPB);
+  const int smem = 3 * m * (int)sizeof(uint64_t);
+  if (smem > 48 * 1024) GT_CUDA_CHECK(cudaFuncSetAttribute(k_partition<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k_partition<G><<<grid, TPB, smem, s>>>(X, midx, T, slots, m, nf, N, base, K, op_id(level, SITE_PART_OAA),
+                                         op_id(level, SITE_PART_ROW));
+  GT_LAUNCH_CHECK("k_partition");
+  return GT_OK;
+}
+
+int launch_count(CountArgs ca, cudaStream_t s, int num_sms) {
+  const int nf = ca.nf, W = 2 * nf + 1, WP = nf + 1;
+  ca.nb = std::max(1, std::min(ca.n_h, (CNT_ITEMS * CNT_TPB) / WP));
+  ca.nb = std::min(ca.nb, 32);
+  ca.ts = 32;
+  const unsigned gy = (unsigned)((ca.n_h + ca.nb - 1) / ca.nb);
+  const uint64_t tiles = (ca.N + ca.ts - 1) / ca.ts;
+  const uint64_t target = std::max<uint64_t>(1, (uint64_t)num_sms * 8 / gy);
+  const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>(tiles, target));
+  ca.tiles_per_cta = (int)((tiles + gx - 1) / gx);
+  const unsigned gxx = (unsigned)((tiles + ca.tiles_per_cta - 1) / ca.tiles_per_cta);
+  const int smem = (int)sizeof(uint64_t) * (3 * ca.ts * W + 3 * ca.ts * ca.nb + 3 * ca.nb);
+  if (smem > 48 * 1024) GT_CUDA_CHECK(cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k_count<<<dim3(gxx, gy), CNT_TPB, smem, s>>>(ca);
+  GT_LAUNCH_CHECK("k_count");
+  return GT_OK;
+}
+
+int counter_shift(uint64_t n, int score_width, int tau) {  // train.py:189-192
+  int headroom = (score_width - tau - 2) / 2;
+  int bl = 0;
+  while (bl < 64 && (n >> bl)) ++bl;
+  return std::max(0, bl - headroom);
+}
+
+}  // namespace
+}  // namespace gt
+
+using namespace gt;
+
+extern "C" {
+
+uint64_t gt_train_workspace_bytes(const gt_train_cfg* cfg) {
+  if (!cfg || cfg->depth < 1 || cfg->depth > 16 || cfg->nf < 1 || cfg->nf > 64) return 0;
+  return layout(*cfg).total * sizeof(uint64_t);
+}
+
+int gt_train(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* labels, const uint64_t* filler,
+             uint64_t* T, uint64_t* F, int32_t* depth_out, void* workspace, uint64_t workspace_bytes,
+             const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user, void* stream) {
+  if (!cfg || !keys) return fail_inval("gt_train: NULL cfg/keys");
+  const gt_train_cfg c = *cfg;
+  if (c.depth < 1 || c.depth > 16) return fail_inval("depth must be in 1..16");
+  if (c.nf < 1 || c.nf > 64) return fail_inval("need 1..64 features");
+  if (c.score_width != 32 && c.score_width != 64) return fail_inval("score ring width must be 32 or 64");
+  if (c.tau < 0 || c.tau >= c.score_width - 2) return fail_inval("fixed-point precision tau out of range");
+  if (c.n_total < 1) return fail_inval("dataset is empty");
+  if (c.n_local > c.n_total || c.sample_base + c.n_local > c.n_total) return fail_inval("bad sample shard");
+  if (c.policy != 0 && c.policy != 1) return fail_inval("policy must be fixed (0) or grow (1)");
+  if (c.policy == 1 && c.depth > 8) return fail_inval("grow policy supports depth <= 8");
+  bool ok = false;
+  const DivParams d = div_params(c.score_width, c.tau, &ok);
+  if (!ok) return fail_inval("division unsupported at this width/tau");
+  const Layout L = layout(c);
+  if (!workspace || workspace_bytes < L.total * sizeof(uint64_t)) return fail_inval("workspace too small");
+  if (c.n_local && (!features || !labels)) return fail_inval("NULL features/labels");
+  if (!filler || !T || !F) return fail_inval("NULL filler/T/F");
+
+  cudaStream_t s = (cudaStream_t)stream;
+  int dev = 0, num_sms = 148;
+  GT_CUDA_CHECK(cudaGetDevice(&dev));
+  GT_CUDA_CHECK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+  const Keys K = to_keys(keys);
+  uint64_t* ws = (uint64_t*)workspace;
+  const uint64_t N = c.n_local, nf = (uint64_t)c.nf, cols = 2 * nf, W = cols + 1;
+  const uint64_t slots = (1ull << c.depth) - 1;
+  const int shift = counter_shift(c.n_total, c.score_width, c.tau);
+  uint64_t *prods = ws + L.prods, *midx = ws + L.midx, *S = ws + L.S, *hc = ws + L.hc;
+  uint64_t *f[2] = {ws + L.f[0], ws + L.f[1]}, *gam[2] = {ws + L.gam[0], ws + L.gam[1]};
+  uint64_t *cst[2] = {ws + L.cst[0], ws + L.cst[1]}, *ceff[2] = {ws + L.ceff[0], ws + L.ceff[1]};
+  int cur = 0;
+
+  GT_CUDA_CHECK(cudaMemsetAsync(T, 0, 3 * slots * sizeof(uint64_t), s));
+  GT_CUDA_CHECK(cudaMemsetAsync(F, 0, 3 * slots * sizeof(uint64_t), s));
+  if (N) GT_CUDA_CHECK(cudaMemsetAsync(midx, 0, 3 * N * sizeof(uint64_t), s));  // m_idx = const(0)
+  k_init<<<1, 128, 0, s>>>(f[0], gam[0], cst[0], 1, 3 * cols, (int)cols, c.nf);
+  GT_LAUNCH_CHECK("k_init");
+  if (N) {
+    const uint64_t tot = N * nf;
+    k_prods<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(features, labels, prods, N, c.nf, c.sample_base, K,
+                                                          op_id(0, SITE_PRODS));
+    GT_LAUNCH_CHECK("k_prods");
+  }
+  int32_t trained = c.depth;
+  for (int level = 0; level < c.depth; ++level) {
+    const int n_h = 1 << level;
+    if (level > 0 && N) {
+      int rc = launch_partition(features, midx, T, slots, n_h / 2, c.nf, N, c.sample_base, K, level, s);
+      if (rc) return rc;
+    }
+    const uint64_t swords = 3ull * n_h * (W + 1);
+    GT_CUDA_CHECK(cudaMemsetAsync(S, 0, swords * sizeof(uint64_t), s));
+    if (N) {
+      CountArgs ca{};
+      ca.X = features;
+      ca.P = prods;
+      ca.Y = labels;
+      ca.midx = midx;
+      ca.f = f[cur];
+      ca.S = S;
+      ca.N = N;
+      ca.base = c.sample_base;
+      ca.nf = c.nf;
+      ca.n_h = n_h;
+      ca.off = n_h - 1;
+      ca.K = K;
+      ca.op_leaf = op_id(level, SITE_ISLEAF);
+      ca.op_cnt = op_id(level, SITE_COUNT);
+      int rc = launch_count(ca, s, num_sms);
+      if (rc) return rc;
+    }
+    if (allreduce) {
+      int rc = allreduce(S, swords, stream, allreduce_user);
+      if (rc) return fail_inval("allreduce callback failed");
+    }
+    bool last = level == c.depth - 1;
+    NodeArgs na{};
+    na.S = S;
+    na.cst = cst[cur];
+    na.f = f[cur];
+    na.gam = gam[cur];
+    na.ceff_prev = ceff[cur ^ 1];
+    na.ceff = ceff[cur];
+    na.hc = hc;
+    na.n_h = n_h;
+    na.nf = c.nf;
+    na.level = level;
+    na.last = last;
+    na.shift = shift;
+    na.tau = c.tau;
+    na.d = d;
+    na.K = K;
+    int rc = c.score_width == 32 ? launch_node_hc<32>(na, s) : launch_node_hc<64>(na, s);
+    if (rc) return rc;
+    if (!last && c.policy == 1) {
+      k_node_stop<<<1, 32, 0, s>>>(hc, n_h, K, op_id(level, SITE_STOP), ws + L.stop);
+      GT_LAUNCH_CHECK("k_node_stop");
+      uint64_t flag = 0;
+      GT_CUDA_CHECK(cudaMemcpyAsync(&flag, ws + L.stop, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+      GT_CUDA_CHECK(cudaStreamSynchronize(s));
+      if (flag) last = true;
+    }
+    FinishArgs fa{};
+    fa.hc = hc;
+    fa.ceff = ceff[cur];
+    fa.f = f[cur];
+    fa.filler = filler;
+    fa.T = T;
+    fa.F = F;
+    fa.f_nxt = f[cur ^ 1];
+    fa.gam_nxt = gam[cur ^ 1];
+    fa.cst_nxt = cst[cur ^ 1];
+    fa.slots = slots;
+    fa.n_h = n_h;
+    fa.nf = c.nf;
+    fa.level = level;
+    fa.labels = last;
+    fa.K = K;
+    k_node_finish<<<n_h, 128, 0, s>>>(fa);
+    GT_LAUNCH_CHECK("k_node_finish");
+    cur ^= 1;
+    if (last) {
+      trained = level + 1;
+      break;
+    }
+  }
+  if (depth_out) *depth_out = trained;
+  return GT_OK;
+}
+
+}  // extern "C"

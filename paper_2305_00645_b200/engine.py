@@ -1,0 +1,208 @@
+"""Drop-in per-party API: ``run_local`` / ``train_tree`` / ``infer_batch``.
+
+The reference runs the same protocol body on three party threads
+(``run_local``, rss.py:496-542) and each body calls ``train_tree(eng, X, y,
+cfg)`` (train.py:222) or ``infer_batch(eng, levels, queries)``
+(infer.py:91) on its own share pair.  Here the three co-resident parties meet
+at a rendezvous -- the pattern of the reference's ``EnclaveBridge``
+(transport.py:304-342): the three engines hand in their pairs, the last one
+to arrive checks replication consistency, runs ONE device call for all three
+parties, and every engine gets its own pair of the result back.  The
+run's transcript is the analytic ledger of exactly that protocol
+(ledger.py), so ``LocalRun.metrics`` reads like the reference's.
+"""
+
+from __future__ import annotations
+
+import threading
+import time
+from dataclasses import dataclass
+from typing import Callable, List, Optional, Sequence, Union
+
+import numpy as np
+
+from .ledger import REF_LANE_LIMIT, Ledger, Metrics, Transcript
+from .seeds import PARTIES, SeedSetup, derive_seed, filler_values, make_keys
+from .shares import RING64, AVec, ShareError, avecs_from_components, components_from_avecs, ring_of
+from .train import TrainConfig, TrainResult, resolved_depth, train_components
+
+
+class TransportError(RuntimeError):
+    """transport.py:40-41."""
+
+
+class _Rendezvous:
+    """Gather one request per party, compute once, scatter (EnclaveBridge)."""
+
+    def __init__(self, timeout: float):
+        self.timeout = timeout
+        self._cv = threading.Condition()
+        self._requests = {}
+        self._responses = {}
+        self._error: Optional[BaseException] = None
+        self._generation = 0
+        self.aborted = False
+
+    def abort(self) -> None:
+        with self._cv:
+            self.aborted = True
+            self._cv.notify_all()
+
+    def call(self, party: int, name: str, payload, compute: Callable[[List], List]):
+        with self._cv:
+            if self.aborted:
+                raise TransportError("round barrier broken (peer died or deadlock timeout)")
+            gen = self._generation
+            self._requests[party] = (name, payload)
+            if len(self._requests) == 3:
+                names = {self._requests[p][0] for p in PARTIES}
+                try:
+                    if len(names) != 1:
+                        raise TransportError(f"parties diverged: round tags {sorted(names)}")
+                    outs = compute([self._requests[p][1] for p in PARTIES])
+                    self._responses = {p: outs[p - 1] for p in PARTIES}
+                    self._error = None
+                except BaseException as e:  # noqa: BLE001 - re-raised on every party
+                    self._responses = {}
+                    self._error = e
+                self._requests = {}
+                self._generation += 1
+                self._cv.notify_all()
+            else:
+                deadline = time.monotonic() + self.timeout
+                while self._generation == gen and not self.aborted:
+                    left = deadline - time.monotonic()
+                    if left <= 0:
+                        raise TransportError("rendezvous timed out")
+                    self._cv.wait(timeout=left)
+                if self.aborted and self._generation == gen:
+                    raise TransportError("round barrier broken (peer died or deadlock timeout)")
+            if self._error is not None:
+                raise self._error
+            return self._responses[party]
+
+
+class PartyEngine:
+    """One party's handle (rss.py:270-298).  Protocol bodies written for the
+    reference receive this object; its device work happens at rendezvous."""
+
+    def __init__(self, party: int, seeds: SeedSetup, bridge: _Rendezvous, ledger: Ledger, dealer_seed: bytes,
+                 material=None, lane_limit: int = REF_LANE_LIMIT, device=None):
+        if party not in PARTIES:
+            raise ShareError(f"invalid party id {party}")
+        self.party = party
+        self.seeds = seeds
+        self.material = material
+        self.lane_limit = lane_limit
+        self.dealer_seed = dealer_seed
+        self.device = device
+        self._bridge = bridge
+        self._ledger = ledger
+        self._phase: List[str] = []
+
+    def phase(self, label: str):
+        return _Phase(self, label)
+
+    def tag(self, fallback: str) -> str:
+        return self._phase[-1] if self._phase else fallback
+
+
+class _Phase:
+    def __init__(self, eng: PartyEngine, label: str):
+        self.eng, self.label = eng, label
+
+    def __enter__(self):
+        self.eng._phase.append(self.label)
+        return self
+
+    def __exit__(self, *exc):
+        self.eng._phase.pop()
+        return False
+
+
+@dataclass
+class LocalRun:
+    results: List
+    transcript: Transcript
+    metrics: Metrics
+
+
+def run_local(fn: Callable[[PartyEngine], object], *, seeds: Union[SeedSetup, int], materials: Optional[Sequence] = None,
+              enclave_handler=None, lane_limit: int = REF_LANE_LIMIT, timeout: float = 300.0,
+              dealer_seed: Optional[bytes] = None, device=None) -> LocalRun:
+    """rss.py:496-542 with the three engines meeting on the device.
+    `materials` / `enclave_handler` are accepted for signature compatibility:
+    correlated material is generated in-kernel from `dealer_seed`
+    (default derive_seed(master, "live-dealer"), as cli.cmd_train)."""
+    if isinstance(seeds, int):
+        seeds = SeedSetup.from_int(seeds)
+    if dealer_seed is None:
+        dealer_seed = derive_seed(seeds.master, "live-dealer")
+    bridge = _Rendezvous(timeout)
+    ledger = Ledger(lane_limit)
+    engines = [PartyEngine(i, seeds, bridge, ledger, dealer_seed, materials[i - 1] if materials else None, lane_limit,
+                           device) for i in PARTIES]
+    results: List = [None, None, None]
+    errors: List = [None, None, None]
+
+    def body(idx: int) -> None:
+        try:
+            results[idx] = fn(engines[idx])
+        except BaseException as e:  # noqa: BLE001 - propagated below
+            errors[idx] = e
+            bridge.abort()
+
+    threads = [threading.Thread(target=body, args=(i,), name=f"party{i + 1}", daemon=True) for i in range(3)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=timeout * 4)
+        if t.is_alive():
+            bridge.abort()
+            raise TransportError("party thread failed to finish")
+    for e in errors:
+        if e is not None and not isinstance(e, TransportError):
+            raise e
+    for e in errors:
+        if e is not None:
+            raise e
+    return LocalRun(results=results, transcript=ledger.transcript, metrics=ledger.metrics())
+
+
+def train_tree(eng: PartyEngine, features, labels, cfg: TrainConfig) -> TrainResult:
+    """Per-party drop-in for train.py:222 (SPMD; all three parties call it)."""
+    n_samples, nf = features.shape
+
+    def compute(payloads):
+        X = components_from_avecs([p[0] for p in payloads])
+        Y = components_from_avecs([p[1] for p in payloads])
+        T, F, depth = train_components(X, Y.reshape(3, -1), cfg, eng.seeds, eng.dealer_seed, device=eng.device)
+        eng._ledger.train(n_samples, nf, resolved_depth(cfg, nf + 1), cfg.tau, cfg.score_ring.width,
+                          grow_stop_level=depth - 1, policy=cfg.policy)
+        tv, fv = avecs_from_components(T, RING64), avecs_from_components(F, RING64)
+        return [TrainResult(T=tv[i], F=fv[i], depth=depth) for i in range(3)]
+
+    return eng._bridge.call(eng.party, "train_tree", (features, labels), compute)
+
+
+def infer_batch(eng: PartyEngine, levels: List, queries) -> AVec:
+    """Per-party drop-in for infer.py:91 (levels sizes 1, 2, 4, ...)."""
+    n_queries, nf = queries.shape
+    depth = len(levels)
+
+    def compute(payloads):
+        from .infer import infer_components
+
+        tree = np.concatenate([components_from_avecs([p[0][t] for p in payloads]) for t in range(depth)], axis=1)
+        Q = components_from_avecs([p[1] for p in payloads])
+        keys = make_keys(eng.seeds, eng.dealer_seed)
+        out, _ = infer_components(tree, depth, Q, keys, device=eng.device)
+        eng._ledger.infer(n_queries, nf, depth)
+        return avecs_from_components(out, ring_of(levels[0]))
+
+    return eng._bridge.call(eng.party, "infer_batch", (levels, queries), compute)
+
+
+def open_results(run: LocalRun, pick=lambda r: r) -> np.ndarray:
+    """Reconstruct a vector from the three parties' returned AVecs."""
+    return components_from_avecs([pick(r) for r in run.results]).sum(axis=0, dtype=np.uint64)

@@ -1,0 +1,174 @@
+"""Share containers at the drop-in boundary and their device layout.
+
+The reference hands every party an ``AVec(ring, lo, hi)`` (rss.py:53-132) with
+party p holding components (s_p, s_{p+1}) of x = s_1 + s_2 + s_3 mod 2^l.
+On the device all three parties are co-resident, so a share is one
+component-major uint64 tensor ``[3, ...]`` with component i = party (i+1)'s
+``lo``; replication consistency then holds by construction.  This module
+converts between the two views and checks consistency on the way in exactly
+like ``reconstruct_pairs`` (rss.py:222-228).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Sequence, Tuple
+
+import numpy as np
+
+
+class ShareError(ValueError):
+    """rss.py:44-45."""
+
+
+class RingError(ValueError):
+    """ring.py:22-23."""
+
+
+@dataclass(frozen=True)
+class Ring:
+    """Z_{2^width}, width in {8, 32, 64} (ring.py:27-94)."""
+
+    width: int
+
+    def __post_init__(self) -> None:
+        if self.width not in (8, 32, 64):
+            raise RingError(f"unsupported ring width {self.width}; expected one of (8, 32, 64)")
+
+    @property
+    def mask(self) -> int:
+        return (1 << self.width) - 1
+
+    @property
+    def modulus(self) -> int:
+        return 1 << self.width
+
+    @property
+    def nbytes(self) -> int:
+        return self.width // 8
+
+    def reduce(self, x):
+        if isinstance(x, np.ndarray):
+            return x.astype(np.uint64, copy=False) & np.uint64(self.mask)
+        return int(x) & self.mask
+
+
+RING8, RING32, RING64 = Ring(8), Ring(32), Ring(64)
+
+
+@dataclass
+class AVec:
+    """One party's arithmetic share pair (rss.py:53-63)."""
+
+    ring: Ring
+    lo: np.ndarray
+    hi: np.ndarray
+
+    def __post_init__(self) -> None:
+        if self.lo.shape != self.hi.shape:
+            raise ShareError("share components disagree on shape")
+
+    @property
+    def shape(self) -> tuple:
+        return self.lo.shape
+
+    @property
+    def size(self) -> int:
+        return self.lo.size
+
+    def reshape(self, *shape) -> "AVec":
+        return AVec(self.ring, self.lo.reshape(*shape), self.hi.reshape(*shape))
+
+    def ravel(self) -> "AVec":
+        return AVec(self.ring, self.lo.ravel(), self.hi.ravel())
+
+    def take(self, idx) -> "AVec":
+        return AVec(self.ring, self.lo[idx], self.hi[idx])
+
+
+@dataclass
+class BitVec:
+    """One party's XOR-shared bits, uint8 {0,1} (rss.py:151-160)."""
+
+    lo: np.ndarray
+    hi: np.ndarray
+
+    @property
+    def shape(self) -> tuple:
+        return self.lo.shape
+
+
+def ring_of(vec) -> Ring:
+    r = getattr(vec, "ring", None)
+    return Ring(int(r.width)) if r is not None else RING64
+
+
+def components_from_pairs(pairs: Sequence[Tuple[np.ndarray, np.ndarray]], ring: Ring = RING64,
+                          check: bool = True) -> np.ndarray:
+    """Three parties' (lo, hi) pairs -> component-major [3, ...] uint64."""
+    if len(pairs) != 3:
+        raise ShareError("need the share pairs of exactly three parties")
+    los = [np.asarray(p[0], dtype=np.uint64) for p in pairs]
+    his = [np.asarray(p[1], dtype=np.uint64) for p in pairs]
+    shape = los[0].shape
+    if any(x.shape != shape for x in los + his):
+        raise ShareError("share components disagree on shape")
+    if check:
+        for i in range(3):
+            if not np.array_equal(his[i], los[(i + 1) % 3]):
+                raise ShareError("replication inconsistency between party pairs")
+    return np.stack([ring.reduce(x) for x in los])
+
+
+def components_from_avecs(vecs: Sequence, check: bool = True) -> np.ndarray:
+    ring = ring_of(vecs[0])
+    return components_from_pairs([(v.lo, v.hi) for v in vecs], ring, check)
+
+
+def pairs_from_components(comp: np.ndarray) -> List[Tuple[np.ndarray, np.ndarray]]:
+    comp = np.asarray(comp, dtype=np.uint64)
+    return [(comp[i].copy(), comp[(i + 1) % 3].copy()) for i in range(3)]
+
+
+def avecs_from_components(comp: np.ndarray, ring: Ring = RING64) -> List[AVec]:
+    return [AVec(ring, lo, hi) for lo, hi in pairs_from_components(comp)]
+
+
+def reconstruct(comp: np.ndarray, ring: Ring = RING64) -> np.ndarray:
+    c = np.asarray(comp, dtype=np.uint64)
+    return (c[0] + c[1] + c[2]) & np.uint64(ring.mask)
+
+
+def share_values(values: np.ndarray, ring: Ring, rng: np.random.Generator) -> np.ndarray:
+    """Fresh component-major sharing of public values (test/bench plumbing;
+    the dealer-side split of make_arith_shares, rss.py:205-211)."""
+    v = ring.reduce(np.asarray(values, dtype=np.uint64))
+    s1 = rng.integers(0, 1 << 63, v.shape, dtype=np.uint64) ^ (rng.integers(0, 1 << 63, v.shape, dtype=np.uint64) << np.uint64(1))
+    s2 = rng.integers(0, 1 << 63, v.shape, dtype=np.uint64) ^ (rng.integers(0, 1 << 63, v.shape, dtype=np.uint64) << np.uint64(1))
+    s1, s2 = ring.reduce(s1), ring.reduce(s2)
+    s3 = ring.reduce(v - s1 - s2)
+    return np.stack([s1, s2, s3])
+
+
+# --------------------------------------------------------------------------
+# device tensors (torch is plumbing: allocation, copies, streams)
+# --------------------------------------------------------------------------
+
+
+def to_device(arr: np.ndarray, device="cuda"):
+    import torch
+
+    a = np.ascontiguousarray(np.asarray(arr, dtype=np.uint64))
+    return torch.from_numpy(a.view(np.int64)).to(device)
+
+
+def from_device(t) -> np.ndarray:
+    return t.detach().cpu().numpy().view(np.uint64)
+
+
+def ptr(t) -> int:
+    if t is None:
+        return 0
+    if not t.is_contiguous():
+        raise ValueError("device share tensors must be contiguous")
+    return t.data_ptr()

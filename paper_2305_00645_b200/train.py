@@ -1,0 +1,169 @@
+"""Secure level-wise training on B200 (reference pkg/src/obtree/train.py).
+
+``TrainConfig`` / ``TrainResult`` / ``counter_shift`` / ``resolved_depth`` /
+``levels_of`` keep the reference's names and meaning (train.py:171-204).
+The level loop itself (partition -> count -> heuristic -> replace -> split /
+labels, train.py:222-311) runs natively: ``gt_train`` in the C ABI drives the
+sm_100a kernels level by level on one CUDA stream, calling back only for the
+per-level count allreduce of a sample-sharded run.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _native
+from .seeds import SeedSetup, filler_values, make_keys
+from .shares import RING32, RING64, AVec, Ring, components_from_pairs, from_device, ptr, to_device
+
+
+@dataclass
+class TrainConfig:
+    """train.py:171-179."""
+
+    depth: int = 4
+    tau: int = 10
+    heuristic: str = "mpc"  # "mpc" | "tee"
+    policy: str = "fixed"  # "fixed" | "grow" | "feature_cap"
+    max_depth: Optional[int] = None
+    score_ring: Ring = RING32
+    count_ring: Ring = RING64
+
+
+@dataclass
+class TrainResult:
+    """train.py:182-186 (T, F per party as AVec in the drop-in path)."""
+
+    T: object
+    F: object
+    depth: int
+
+
+def counter_shift(n_samples: int, cfg: TrainConfig) -> int:
+    """Public scale-down so squared counters fit the division domain (train.py:189-192)."""
+    headroom = (cfg.score_ring.width - cfg.tau - 2) // 2
+    return max(0, int(n_samples).bit_length() - headroom)
+
+
+def resolved_depth(cfg: TrainConfig, n_columns: int) -> int:
+    """train.py:195-200."""
+    if cfg.policy == "feature_cap":
+        return n_columns
+    if cfg.policy == "grow":
+        return cfg.max_depth if cfg.max_depth is not None else n_columns
+    return cfg.depth
+
+
+def levels_of(vec, depth: int) -> List:
+    """Heap-level slices of a payload vector (train.py:203-204)."""
+    return [vec.take(slice((1 << t) - 1, (1 << (t + 1)) - 1)) for t in range(depth)]
+
+
+def _validate(cfg: TrainConfig, nf: int) -> int:
+    if cfg.heuristic != "mpc":
+        raise NotImplementedError("heuristic 'tee' (attested helper) is not on the B200 path yet; use 'mpc'")
+    if cfg.policy not in ("fixed", "grow", "feature_cap"):
+        raise ValueError(f"unknown depth policy {cfg.policy!r}")
+    if cfg.count_ring.width != 64:
+        raise ValueError("counters live in Z_2^64 on the B200 path")
+    depth = resolved_depth(cfg, nf + 1)
+    if depth < 1:
+        raise ValueError("depth must be at least 1")
+    if cfg.score_ring.width not in (32, 64):
+        raise ValueError("score ring must be Z_2^32 or Z_2^64")
+    if not 0 <= cfg.tau < cfg.score_ring.width - 2:
+        raise ValueError(f"fixed-point precision tau={cfg.tau} must satisfy 0 <= tau < {cfg.score_ring.width - 2}")
+    return depth
+
+
+class DeviceTrainer:
+    """One training shape (samples on this device, features, depth) with its
+    device workspace; ``run`` can be called repeatedly (bench steps)."""
+
+    def __init__(self, n_local: int, nf: int, cfg: TrainConfig, *, n_total: Optional[int] = None,
+                 sample_base: int = 0, device=None):
+        torch = _native.require_cuda()
+        self.lib = _native.load()
+        self.depth = _validate(cfg, nf)
+        self.cfg = cfg
+        self.nf = nf
+        self.n_local = int(n_local)
+        self.n_total = int(n_total if n_total is not None else n_local)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        c = _native.gt_train_cfg()
+        c.depth = self.depth
+        c.tau = cfg.tau
+        c.score_width = cfg.score_ring.width
+        c.nf = nf
+        c.policy = 1 if cfg.policy == "grow" else 0
+        c.n_total = self.n_total
+        c.n_local = self.n_local
+        c.sample_base = int(sample_base)
+        self.c = c
+        nbytes = self.lib.gt_train_workspace_bytes(ctypes.byref(c))
+        if nbytes == 0:
+            raise ValueError("unsupported training shape (depth 1..16, 1..64 features)")
+        self.workspace = torch.empty(nbytes // 8, dtype=torch.int64, device=self.device)
+        slots = (1 << self.depth) - 1
+        self.T = torch.empty((3, slots), dtype=torch.int64, device=self.device)
+        self.F = torch.empty((3, slots), dtype=torch.int64, device=self.device)
+
+    def workspace_view(self, addr: int, count: int):
+        """Tensor view of `count` words of the workspace at device address `addr`."""
+        off = (addr - self.workspace.data_ptr()) // 8
+        return self.workspace[off:off + count]
+
+    def run(self, X, Y, filler, keys, *, allreduce=None, stream=None) -> int:
+        """X [3, n_local, nf], Y [3, n_local], filler [2^H - 1] device int64
+        tensors (uint64 bits).  Results land in self.T / self.F; returns the
+        trained depth."""
+        torch = _native.require_cuda()
+        if tuple(X.shape) != (3, self.n_local, self.nf) or tuple(Y.shape) != (3, self.n_local):
+            raise ValueError("features must be [3, n, nf] and labels [3, n] component shares")
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        d = ctypes.c_int32(0)
+        cb = _native.ALLREDUCE_FN(0) if allreduce is None else allreduce
+        rc = self.lib.gt_train(ctypes.byref(self.c), ptr(X), ptr(Y), ptr(filler), ptr(self.T), ptr(self.F),
+                               ctypes.byref(d), ptr(self.workspace), self.workspace.numel() * 8, ctypes.byref(keys),
+                               cb, None, ctypes.c_void_p(s.cuda_stream))
+        _native.check(rc)
+        return int(d.value)
+
+
+def train_components(X: np.ndarray, Y: np.ndarray, cfg: TrainConfig, seeds: SeedSetup, dealer_seed: bytes,
+                     *, device=None) -> Tuple[np.ndarray, np.ndarray, int]:
+    """Whole-run entry on component-major shares: X [3, N, nf], Y [3, N]
+    uint64 -> (T [3, slots], F [3, slots], depth) component shares."""
+    X = np.asarray(X, dtype=np.uint64)
+    Y = np.asarray(Y, dtype=np.uint64)
+    if X.ndim != 3 or X.shape[0] != 3 or Y.shape != (3, X.shape[1]):
+        raise ValueError("features must be [3, n, nf] and labels [3, n]")
+    n, nf = X.shape[1], X.shape[2]
+    if n == 0:
+        raise ValueError("dataset is empty")
+    tr = DeviceTrainer(n, nf, cfg, device=device)
+    fill = filler_values(seeds.filler_seed, (1 << tr.depth) - 1, nf + 1)
+    keys = make_keys(seeds, dealer_seed)
+    depth = tr.run(to_device(X, tr.device), to_device(Y, tr.device), to_device(fill, tr.device), keys)
+    slots = (1 << depth) - 1
+    return from_device(tr.T)[:, :slots].copy(), from_device(tr.F)[:, :slots].copy(), depth
+
+
+def train_3pc(x_pairs: Sequence, y_pairs: Sequence, cfg: TrainConfig, seeds: SeedSetup, dealer_seed: bytes,
+              *, device=None, check: bool = True):
+    """Whole-run entry on the three parties' replicated pairs (the form
+    ``share_values`` returns, dealer.py:619-623): x_pairs[i] = (lo, hi) of
+    party i+1, lo/hi shaped (N, nf); y_pairs[i] shaped (N,).  Returns
+    (T_pairs, F_pairs, depth) in the same per-party form."""
+    X = components_from_pairs(x_pairs, RING64, check)
+    Y = components_from_pairs(y_pairs, RING64, check)
+    if X.ndim != 3:
+        raise ValueError("features must be (n, nf) per party")
+    T, F, depth = train_components(X, Y.reshape(3, -1), cfg, seeds, dealer_seed, device=device)
+    from .shares import pairs_from_components
+
+    return pairs_from_components(T), pairs_from_components(F), depth

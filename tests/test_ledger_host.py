@@ -1,0 +1,137 @@
+"""Host logic (CPU): transcript ledger vs the reference's transcripts, seed
+derivation and filler stream vs the reference, share conversions, config
+helpers, and the C-ABI library's exported symbol set."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden_json, golden_npz
+from paper_2305_00645_b200 import ledger as L
+from paper_2305_00645_b200 import _native
+from paper_2305_00645_b200.seeds import SeedSetup, derive_seed, filler_values
+from paper_2305_00645_b200.shares import (RING32, RING64, ShareError, components_from_pairs, pairs_from_components,
+                                          reconstruct)
+from paper_2305_00645_b200.train import TrainConfig, counter_shift, levels_of, resolved_depth
+
+
+def _replay(name, v):
+    led = L.Ledger(v.get("lane_limit", L.REF_LANE_LIMIT))
+    if name.startswith("train"):
+        led.train(v["n"], v["d"] - 1, v["depth"])
+    elif name.startswith("infer"):
+        led.infer(v["n"], v["d"] - 1, v["depth"])
+    elif name.startswith("oaa"):
+        led.oaa(v["n"], v["m"], 64)
+        led.row_lookup(v["n"], v["m"], 64)
+    elif name.startswith("gadgets"):
+        w = int(name.split("_w")[1])
+        n = 37
+        led.eq(n, w), led.eq(n, w), led.lt(n, w), led.lt(n, w)
+        led.b2a(n), led.select(n, n, w), led.truncate(n, w, 3), led.mul(n, w)
+    elif name == "division_argmin":
+        led.division(11, 32, 10)
+        led.argmin(5, 13, 32)
+    return led
+
+
+def test_ledger_reproduces_reference_transcripts_record_for_record():
+    g = golden_json("transcripts.json")
+    assert len(g) >= 15
+    for name, v in g.items():
+        led = _replay(name, v)
+        assert led.transcript.records == [tuple(r) for r in v["records"]], name
+
+
+def test_ledger_c2_c3_totals_match_reference():
+    _, meta = golden_npz("c2c3.npz")
+    m = L.train_metrics(48842, 13, 7)
+    ref = meta["train_metrics"]
+    assert m.rounds == ref["rounds"] == 2147
+    assert m.bytes_by_pair == ref["bytes_by_pair"] and m.bytes_by_tag == ref["bytes_by_tag"]
+    assert m.rounds_by_tag == ref["rounds_by_tag"]
+    assert m.sent_by_party(1) == 1615326277
+    mi = L.infer_metrics(10_000, 13, 7)
+    assert mi.rounds == meta["infer_metrics"]["rounds"] == 126
+    assert mi.bytes_by_pair == meta["infer_metrics"]["bytes_by_pair"]
+
+
+def test_device_schedule_same_bytes_fewer_rounds():
+    ref = L.train_metrics(48842, 13, 7)
+    dev = L.train_metrics(48842, 13, 7, lane_limit=None)
+    assert dev.sent_by_party(1) == ref.sent_by_party(1)
+    assert dev.rounds < ref.rounds
+
+
+def test_transcript_shape_only_depends_on_public_sizes():
+    a = L.Ledger()
+    a.train(50, 3, 3)
+    b = L.Ledger()
+    b.train(50, 3, 3)
+    assert a.transcript.records == b.transcript.records
+
+
+def test_seeds_and_filler_match_reference():
+    kats = golden_json("kats.json")
+    for master_hex, want in kats["seeds"].items():
+        s = SeedSetup.from_master(bytes.fromhex(master_hex))
+        assert {str(i): s.pair_seeds[i].hex() for i in (1, 2, 3)} == want["pair"]
+        assert s.filler_seed.hex() == want["filler"]
+        assert filler_values(s.filler_seed, 127, 14).tolist() == want["filler_values_127_14"]
+        assert filler_values(s.filler_seed, 1023, 33).tolist() == want["filler_values_1023_33"]
+
+
+def test_counter_shift_and_config_helpers():
+    kats = golden_json("kats.json")["counter_shift"]
+    for n, want in kats.items():
+        assert counter_shift(int(n), TrainConfig()) == want
+        assert L.counter_shift(int(n)) == want
+    assert resolved_depth(TrainConfig(depth=3), 9) == 3
+    assert resolved_depth(TrainConfig(policy="feature_cap"), 4) == 4
+    assert resolved_depth(TrainConfig(policy="grow", max_depth=5), 9) == 5
+    from paper_2305_00645_b200.shares import AVec
+
+    vec = AVec(RING64, np.arange(7, dtype=np.uint64), np.zeros(7, dtype=np.uint64))
+    assert [p.size for p in levels_of(vec, 3)] == [1, 2, 4]  # test_train.py:203-206
+
+
+def test_share_conversion_and_consistency_check():
+    rng = np.random.default_rng(0)
+    comp = rng.integers(0, 1 << 63, (3, 11), dtype=np.uint64)
+    pairs = pairs_from_components(comp)
+    assert np.array_equal(components_from_pairs(pairs), comp)
+    bad = [(pairs[0][0], pairs[0][1] ^ np.uint64(1)), pairs[1], pairs[2]]
+    with pytest.raises(ShareError):
+        components_from_pairs(bad)
+    assert np.array_equal(reconstruct(comp, RING32), (comp[0] + comp[1] + comp[2]) & np.uint64(0xFFFFFFFF))
+
+
+def test_division_params_match_reference():
+    assert L.div_params(32, 10) == {"bound": 20, "ti": 14, "sigma": 7, "kf": 17, "iters": 6, "w0": 47746}
+    with pytest.raises(ValueError):
+        L.div_params(12, 10)  # test_gadgets.py:197-199
+
+
+def test_native_library_exports_every_header_symbol():
+    header = open(os.path.join(ROOT, "include", "gtree_b200.h")).read()
+    declared = set(re.findall(r"\b(gt_[a-z0-9_]+)\s*\(", header)) - {"gt_allreduce_fn"}
+    lib = ctypes.CDLL(_native.LIB_PATH)
+    for sym in sorted(declared):
+        assert hasattr(lib, sym), sym
+    assert declared == set(_native.EXPORTS)
+    assert lib.gt_abi_version() == _native.ABI_VERSION
+
+
+def test_product_has_no_cpu_fallback_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2305_00645_b200.train import train_components
+
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        train_components(np.zeros((3, 4, 2), np.uint64), np.zeros((3, 4), np.uint64), TrainConfig(depth=2),
+                         SeedSetup.from_int(1), b"\x00" * 16)
