@@ -116,6 +116,22 @@ int gt_train(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* 
              uint64_t* T, uint64_t* F, int32_t* depth_out, void* workspace, uint64_t workspace_bytes,
              const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user, void* stream);
 
+/* Per-kernel-class device time of one gt_train_ex call, measured with CUDA
+ * events recorded on `stream` around every launch (bench / roofline use). */
+typedef struct {
+  uint32_t launches; /* kernels launched by the call */
+  uint32_t n_prods, n_partition, n_count, n_node_hc, n_node_finish;
+  float ms_prods, ms_partition, ms_count, ms_node_hc, ms_node_finish;
+  float ms_total; /* first to last event */
+} gt_train_profile;
+
+/* gt_train plus optional profiling (prof may be NULL; when set, the call
+ * synchronizes `stream` before returning). */
+int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* labels, const uint64_t* filler,
+                uint64_t* T, uint64_t* F, int32_t* depth_out, void* workspace, uint64_t workspace_bytes,
+                const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user, void* stream,
+                gt_train_profile* prof);
+
 /* ---- secure inference (infer_batch, infer.py:91-106) ---- */
 
 /* tree [3][2^depth-1] heap-ordered payload shares, queries [3][n][nf];

@@ -46,6 +46,13 @@ class gt_train_cfg(ctypes.Structure):
     ]
 
 
+class gt_train_profile(ctypes.Structure):
+    _fields_ = [("launches", ctypes.c_uint32), ("n_prods", ctypes.c_uint32), ("n_partition", ctypes.c_uint32),
+                ("n_count", ctypes.c_uint32), ("n_node_hc", ctypes.c_uint32), ("n_node_finish", ctypes.c_uint32),
+                ("ms_prods", ctypes.c_float), ("ms_partition", ctypes.c_float), ("ms_count", ctypes.c_float),
+                ("ms_node_hc", ctypes.c_float), ("ms_node_finish", ctypes.c_float), ("ms_total", ctypes.c_float)]
+
+
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p)
 
 _u64p = ctypes.c_void_p
@@ -76,6 +83,10 @@ _SIGS = {
     "gt_train": (ctypes.c_int, [ctypes.POINTER(gt_train_cfg), _u64p, _u64p, _u64p, _u64p, _u64p,
                                 ctypes.POINTER(ctypes.c_int32), ctypes.c_void_p, ctypes.c_uint64,
                                 ctypes.POINTER(gt_keys), ALLREDUCE_FN, ctypes.c_void_p, ctypes.c_void_p]),
+    "gt_train_ex": (ctypes.c_int, [ctypes.POINTER(gt_train_cfg), _u64p, _u64p, _u64p, _u64p, _u64p,
+                                   ctypes.POINTER(ctypes.c_int32), ctypes.c_void_p, ctypes.c_uint64,
+                                   ctypes.POINTER(gt_keys), ALLREDUCE_FN, ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.POINTER(gt_train_profile)]),
     "gt_infer": (ctypes.c_int, [ctypes.c_int, _u64p, _u64p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                 _u64p, _u64p, ctypes.POINTER(gt_keys), ctypes.c_void_p]),
 }

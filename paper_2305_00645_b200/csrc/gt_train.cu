@@ -17,6 +17,8 @@
 // Every lane's randomness is keyed by (op, sub, field, global lane), so the
 // shares produced are independent of sharding and of launch geometry.
 #include <algorithm>
+#include <utility>
+#include <vector>
 
 #include "gt_common.cuh"
 #include "gt_lookup.cuh"
@@ -609,6 +611,62 @@ int launch_count(CountArgs ca, cudaStream_t s, int num_sms) {
   return GT_OK;
 }
 
+// CUDA-event timing of each launch (gt_train_ex with a profile struct).
+struct Prof {
+  enum Kind { PRODS, PARTITION, COUNT, NODE_HC, NODE_FINISH, NKIND };
+  gt_train_profile* out;
+  cudaStream_t s;
+  cudaEvent_t first = nullptr, a = nullptr;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> spans;
+  uint32_t launches = 0;
+  Prof(gt_train_profile* o, cudaStream_t st) : out(o), s(st) {}
+  ~Prof() {
+    for (auto& e : spans) {
+      cudaEventDestroy(e.second.first);
+      cudaEventDestroy(e.second.second);
+    }
+    if (first) cudaEventDestroy(first);
+  }
+  void begin() {
+    if (!out) return;
+    cudaEventCreate(&first);
+    cudaEventRecord(first, s);
+  }
+  void count_launch() { ++launches; }
+  void start() {
+    ++launches;
+    if (!out) return;
+    cudaEventCreate(&a);
+    cudaEventRecord(a, s);
+  }
+  void stop(int kind) {
+    if (!out) return;
+    cudaEvent_t b;
+    cudaEventCreate(&b);
+    cudaEventRecord(b, s);
+    spans.push_back({kind, {a, b}});
+  }
+  int finish() {
+    if (!out) return GT_OK;
+    GT_CUDA_CHECK(cudaStreamSynchronize(s));
+    gt_train_profile p{};
+    p.launches = launches;
+    float* ms[NKIND] = {&p.ms_prods, &p.ms_partition, &p.ms_count, &p.ms_node_hc, &p.ms_node_finish};
+    uint32_t* cnt[NKIND] = {&p.n_prods, &p.n_partition, &p.n_count, &p.n_node_hc, &p.n_node_finish};
+    cudaEvent_t last = first;
+    for (auto& e : spans) {
+      float t = 0.f;
+      GT_CUDA_CHECK(cudaEventElapsedTime(&t, e.second.first, e.second.second));
+      *ms[e.first] += t;
+      *cnt[e.first] += 1;
+      last = e.second.second;
+    }
+    GT_CUDA_CHECK(cudaEventElapsedTime(&p.ms_total, first, last));
+    *out = p;
+    return GT_OK;
+  }
+};
+
 int counter_shift(uint64_t n, int score_width, int tau) {  // train.py:189-192
   int headroom = (score_width - tau - 2) / 2;
   int bl = 0;
@@ -631,6 +689,14 @@ uint64_t gt_train_workspace_bytes(const gt_train_cfg* cfg) {
 int gt_train(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* labels, const uint64_t* filler,
              uint64_t* T, uint64_t* F, int32_t* depth_out, void* workspace, uint64_t workspace_bytes,
              const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user, void* stream) {
+  return gt_train_ex(cfg, features, labels, filler, T, F, depth_out, workspace, workspace_bytes, keys, allreduce,
+                     allreduce_user, stream, nullptr);
+}
+
+int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* labels, const uint64_t* filler,
+                uint64_t* T, uint64_t* F, int32_t* depth_out, void* workspace, uint64_t workspace_bytes,
+                const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user, void* stream,
+                gt_train_profile* prof) {
   if (!cfg || !keys) return fail_inval("gt_train: NULL cfg/keys");
   const gt_train_cfg c = *cfg;
   if (c.depth < 1 || c.depth > 16) return fail_inval("depth must be in 1..16");
@@ -650,6 +716,7 @@ int gt_train(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* 
   if (!filler || !T || !F) return fail_inval("NULL filler/T/F");
 
   cudaStream_t s = (cudaStream_t)stream;
+  Prof P(prof, s);
   int dev = 0, num_sms = 148;
   GT_CUDA_CHECK(cudaGetDevice(&dev));
   GT_CUDA_CHECK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
@@ -666,20 +733,26 @@ int gt_train(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* 
   GT_CUDA_CHECK(cudaMemsetAsync(T, 0, 3 * slots * sizeof(uint64_t), s));
   GT_CUDA_CHECK(cudaMemsetAsync(F, 0, 3 * slots * sizeof(uint64_t), s));
   if (N) GT_CUDA_CHECK(cudaMemsetAsync(midx, 0, 3 * N * sizeof(uint64_t), s));  // m_idx = const(0)
+  P.begin();
   k_init<<<1, 128, 0, s>>>(f[0], gam[0], cst[0], 1, 3 * cols, (int)cols, c.nf);
   GT_LAUNCH_CHECK("k_init");
+  P.count_launch();
   if (N) {
     const uint64_t tot = N * nf;
+    P.start();
     k_prods<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(features, labels, prods, N, c.nf, c.sample_base, K,
                                                           op_id(0, SITE_PRODS));
     GT_LAUNCH_CHECK("k_prods");
+    P.stop(Prof::PRODS);
   }
   int32_t trained = c.depth;
   for (int level = 0; level < c.depth; ++level) {
     const int n_h = 1 << level;
     if (level > 0 && N) {
+      P.start();
       int rc = launch_partition(features, midx, T, slots, n_h / 2, c.nf, N, c.sample_base, K, level, s);
       if (rc) return rc;
+      P.stop(Prof::PARTITION);
     }
     const uint64_t swords = 3ull * n_h * (W + 1);
     GT_CUDA_CHECK(cudaMemsetAsync(S, 0, swords * sizeof(uint64_t), s));
@@ -699,8 +772,10 @@ int gt_train(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* 
       ca.K = K;
       ca.op_leaf = op_id(level, SITE_ISLEAF);
       ca.op_cnt = op_id(level, SITE_COUNT);
+      P.start();
       int rc = launch_count(ca, s, num_sms);
       if (rc) return rc;
+      P.stop(Prof::COUNT);
     }
     if (allreduce) {
       int rc = allreduce(S, swords, stream, allreduce_user);
@@ -723,11 +798,14 @@ int gt_train(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* 
     na.tau = c.tau;
     na.d = d;
     na.K = K;
+    P.start();
     int rc = c.score_width == 32 ? launch_node_hc<32>(na, s) : launch_node_hc<64>(na, s);
     if (rc) return rc;
+    P.stop(Prof::NODE_HC);
     if (!last && c.policy == 1) {
       k_node_stop<<<1, 32, 0, s>>>(hc, n_h, K, op_id(level, SITE_STOP), ws + L.stop);
       GT_LAUNCH_CHECK("k_node_stop");
+      P.count_launch();
       uint64_t flag = 0;
       GT_CUDA_CHECK(cudaMemcpyAsync(&flag, ws + L.stop, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
       GT_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -749,8 +827,10 @@ int gt_train(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* 
     fa.level = level;
     fa.labels = last;
     fa.K = K;
+    P.start();
     k_node_finish<<<n_h, 128, 0, s>>>(fa);
     GT_LAUNCH_CHECK("k_node_finish");
+    P.stop(Prof::NODE_FINISH);
     cur ^= 1;
     if (last) {
       trained = level + 1;
@@ -758,7 +838,7 @@ int gt_train(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* 
     }
   }
   if (depth_out) *depth_out = trained;
-  return GT_OK;
+  return P.finish();
 }
 
 }  // extern "C"

@@ -117,19 +117,21 @@ class DeviceTrainer:
         off = (addr - self.workspace.data_ptr()) // 8
         return self.workspace[off:off + count]
 
-    def run(self, X, Y, filler, keys, *, allreduce=None, stream=None) -> int:
+    def run(self, X, Y, filler, keys, *, allreduce=None, stream=None, profile=None) -> int:
         """X [3, n_local, nf], Y [3, n_local], filler [2^H - 1] device int64
         tensors (uint64 bits).  Results land in self.T / self.F; returns the
-        trained depth."""
+        trained depth.  `profile` (a _native.gt_train_profile) receives the
+        CUDA-event device time per kernel class."""
         torch = _native.require_cuda()
         if tuple(X.shape) != (3, self.n_local, self.nf) or tuple(Y.shape) != (3, self.n_local):
             raise ValueError("features must be [3, n, nf] and labels [3, n] component shares")
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         d = ctypes.c_int32(0)
         cb = _native.ALLREDUCE_FN(0) if allreduce is None else allreduce
-        rc = self.lib.gt_train(ctypes.byref(self.c), ptr(X), ptr(Y), ptr(filler), ptr(self.T), ptr(self.F),
-                               ctypes.byref(d), ptr(self.workspace), self.workspace.numel() * 8, ctypes.byref(keys),
-                               cb, None, ctypes.c_void_p(s.cuda_stream))
+        prof = ctypes.byref(profile) if profile is not None else None
+        rc = self.lib.gt_train_ex(ctypes.byref(self.c), ptr(X), ptr(Y), ptr(filler), ptr(self.T), ptr(self.F),
+                                  ctypes.byref(d), ptr(self.workspace), self.workspace.numel() * 8,
+                                  ctypes.byref(keys), cb, None, ctypes.c_void_p(s.cuda_stream), prof)
         _native.check(rc)
         return int(d.value)
 
