@@ -36,12 +36,8 @@ int fail_inval(const std::string& msg);
 
 inline Keys to_keys(const gt_keys* k) {
   Keys K;
-  K.dealer.k0 = k->dealer.k0;
-  K.dealer.k1 = k->dealer.k1;
-  for (int i = 0; i < 3; ++i) {
-    K.pair[i].k0 = k->pair[i].k0;
-    K.pair[i].k1 = k->pair[i].k1;
-  }
+  K.dealer = expand_key(k->dealer.k0, k->dealer.k1);
+  for (int i = 0; i < 3; ++i) K.pair[i] = expand_key(k->pair[i].k0, k->pair[i].k1);
   return K;
 }
 

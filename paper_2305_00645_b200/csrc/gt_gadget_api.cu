@@ -5,6 +5,7 @@
 #include <string>
 
 #include "gt_common.cuh"
+#include "gt_division.cuh"
 #include "gt_lookup.cuh"
 
 namespace gt {
@@ -103,12 +104,16 @@ __global__ void k_trunc(const uint64_t* x, uint64_t* out, uint64_t n, int k, Key
   st3(out, n, i, trunc<L>(K, op, 0, i, ld3(x, n, i), k));
 }
 
+// one warp per division lane (gt_division.cuh), 4 warps per CTA
 template <int L>
 __global__ void k_division(const uint64_t* p, const uint64_t* q, uint64_t* out, uint64_t n, DivParams d, Keys K,
                            uint32_t op) {
-  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  extern __shared__ W2 tape_sm[];
+  const int warp = threadIdx.x >> 5;
+  const uint64_t i = (uint64_t)blockIdx.x * 4 + warp;
   if (i >= n) return;
-  st3(out, n, i, division<L>(K, op, 0, i, ld3(p, n, i), ld3(q, n, i), d));
+  const A3 r = division_warp<L>(K, op, 0, i, ld3(p, n, i), ld3(q, n, i), d, tape_sm + warp * newton_blocks<L>(d));
+  if ((threadIdx.x & 31) == 0) st3(out, n, i, r);
 }
 
 // argmin_masked, one row per thread; subs: 0/1 masking select, round r at
@@ -276,7 +281,22 @@ int gt_division(int width, const uint64_t* p, const uint64_t* q, uint64_t* out, 
   if (!ok || tau < 0 || tau >= width - 2) return fail_inval("division unsupported at this width/tau");
   if (n == 0) return GT_OK;
   if (!p || !q || !out) return fail_inval("gt_division: NULL operand");
-  GT_DISPATCH(width, k_division, blocks_for(n), p, q, out, n, d, to_keys(keys), op);
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned grid = (unsigned)((n + 3) / 4);
+  const Keys K = to_keys(keys);
+  if (width == 64) {
+    const int smem = 4 * newton_blocks<64>(d) * (int)sizeof(W2);
+    GT_CUDA_CHECK(cudaFuncSetAttribute(k_division<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_division<64><<<grid, 128, smem, s>>>(p, q, out, n, d, K, op);
+  } else if (width == 32) {
+    const int smem = 4 * newton_blocks<32>(d) * (int)sizeof(W2);
+    GT_CUDA_CHECK(cudaFuncSetAttribute(k_division<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_division<32><<<grid, 128, smem, s>>>(p, q, out, n, d, K, op);
+  } else {
+    const int smem = 4 * newton_blocks<8>(d) * (int)sizeof(W2);
+    GT_CUDA_CHECK(cudaFuncSetAttribute(k_division<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_division<8><<<grid, 128, smem, s>>>(p, q, out, n, d, K, op);
+  }
   GT_LAUNCH_CHECK("gt_division");
   return GT_OK;
 }

@@ -131,12 +131,8 @@ __device__ __forceinline__ B3 or_gate(const Keys& K, uint32_t op, uint32_t sub, 
 // AND over the low k bit planes of the word (and_reduce, gadgets.py:94-109):
 // level with k rows ANDs plane j with plane j+half (j < half), an odd last
 // plane is carried to position half.  Gate j of a level draws zero bit
-// (off + j) of pair-word `field`; off advances by half per level (<= 63 bits).
-__device__ __forceinline__ B3 and_reduce(const Keys& K, uint32_t op, uint32_t sub, uint32_t field, uint64_t lane,
-                                         B3 P, int k) {
-  uint64_t Zw[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) Zw[i] = word(K.pair[i], op, sub, field, lane);
+// (off + j) of the pair words Zw; off advances by half per level (<= 63 bits).
+__device__ __forceinline__ B3 and_reduce_w(B3 P, int k, const uint64_t Zw[3]) {
   int off = 0;
   while (k > 1) {
     const int half = k >> 1;
@@ -161,51 +157,76 @@ __device__ __forceinline__ B3 and_reduce(const Keys& K, uint32_t op, uint32_t su
   return P;
 }
 
+__device__ __forceinline__ B3 and_reduce(const Keys& K, uint32_t op, uint32_t sub, uint32_t field, uint64_t lane,
+                                         B3 P, int k) {
+  uint64_t Zw[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) Zw[i] = word(K.pair[i], op, sub, field, lane);
+  return and_reduce_w(P, k, Zw);
+}
+
 // ---------------------------------------------------------------------------
 // comparisons (masked opening + boolean circuit on public c vs shared r)
 // ---------------------------------------------------------------------------
 
-// [d == 0] for d = x - y already formed (eq, gadgets.py:120-130).
-// dealer fields: r=0 Rb0=1 Rb1=2 R0=3 R1=4; pair field 0 = AND-tree zero bits.
+// [d == 0] from an edabit (r, boolean word shares Rb0, Rb1) and the AND-tree
+// zero words Zw (eq, gadgets.py:120-130).  The arithmetic shares of r only
+// mask the opening, c = sum_i (d_i + R_i) = d + r, so they are not drawn.
 template <int L>
-__device__ __forceinline__ B3 eqz(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const A3& d) {
+__device__ __forceinline__ B3 eq_arith(const A3& d, uint64_t r, uint64_t Rb0, uint64_t Rb1, const uint64_t Zw[3]) {
   constexpr uint64_t M = Ring<L>::M;
-  const uint64_t r = word(K.dealer, op, sub, 0, lane) & M;
-  const uint64_t Rb0 = word(K.dealer, op, sub, 1, lane) & M;
-  const uint64_t Rb1 = word(K.dealer, op, sub, 2, lane) & M;
-  const uint64_t R0 = word(K.dealer, op, sub, 3, lane) & M;
-  const uint64_t R1 = word(K.dealer, op, sub, 4, lane) & M;
-  const uint64_t R2 = (r - R0 - R1) & M;  // make_arith_shares, rss.py:205-211
-  const uint64_t Rb2 = r ^ Rb0 ^ Rb1;     // _value_bit_words, dealer.py:411-417
-  const uint64_t c = open<L>(a3(d.v[0] + R0, d.v[1] + R1, d.v[2] + R2));
+  r &= M;
+  Rb0 &= M;
+  Rb1 &= M;
+  const uint64_t c = (open<L>(d) + r) & M;  // open_a(d + r)
   const uint64_t notc = ~c & M;
   B3 P;
   P.v[0] = Rb0 ^ notc;  // xor_pub(planes, ~c)
   P.v[1] = Rb1;
-  P.v[2] = Rb2;
-  return and_reduce(K, op, sub, 0, lane, P, L);
+  P.v[2] = r ^ Rb0 ^ Rb1;  // _value_bit_words, dealer.py:411-417
+  return and_reduce_w(P, L, Zw);
 }
+
+// standalone eq: dealer fields r=0 Rb0=1 Rb1=2; pair field 0 = AND-tree bits.
+template <int L>
+__device__ __forceinline__ B3 eqz(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const A3& d) {
+  const W2 d0 = word2(K.dealer, op, sub, 0, lane);
+  const uint64_t Rb1 = word(K.dealer, op, sub, 2, lane);
+  uint64_t Zw[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) Zw[i] = word(K.pair[i], op, sub, 0, lane);
+  return eq_arith<L>(d, d0.a, d0.b, Rb1, Zw);
+}
+
+template <int L>
+struct Levels {
+  static constexpr int n = (L == 64) ? 6 : (L == 32) ? 5 : 3;  // log2 L
+};
 
 // Kogge-Stone borrow prefix on (g, p) words (_prefix_borrow, gadgets.py:137-160).
 // Level with shift s: pg = p & (g << s), pp = p & (p << s) for bits >= s (two
 // batched AND lanes per row); bits < s keep g and p, as the reference does.
-// Level l draws pair fields fb + 2l (pg) and fb + 2l + 1 (pp).
+// blk[i * nlev + l] holds key i's zero words of level l: .a for pg, .b for pp
+// (= pair fields fb + 2l, fb + 2l + 1 of the live schedule).
 template <int L>
-__device__ __forceinline__ B3 prefix_borrow(const Keys& K, uint32_t op, uint32_t sub, uint32_t fb, uint64_t lane,
-                                            B3 g, B3 p) {
+__device__ __forceinline__ B3 prefix_borrow_blk(B3 g, B3 p, const W2* blk) {
   constexpr uint64_t M = Ring<L>::M;
-  int lvl = 0;
+  constexpr int NL = Levels<L>::n;
 #pragma unroll
-  for (int s = 1; s < L; s <<= 1, ++lvl) {
+  for (int lvl = 0; lvl < NL; ++lvl) {
+    const int s = 1 << lvl;
     const uint64_t hm = M & ~lowmask(s);
     B3 gs, ps;
+    uint64_t Zg[3], Zp[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       gs.v[i] = (g.v[i] << s) & M;
       ps.v[i] = (p.v[i] << s) & M;
+      Zg[i] = blk[i * NL + lvl].a & hm;
+      Zp[i] = blk[i * NL + lvl].b & hm;
     }
-    const B3 pg = and_gate(K, op, sub, fb + 2 * lvl, lane, p, gs, hm);
-    const B3 pp = and_gate(K, op, sub, fb + 2 * lvl + 1, lane, p, ps, hm);
+    const B3 pg = and_z(p, gs, Zg);
+    const B3 pp = and_z(p, ps, Zp);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       g.v[i] ^= pg.v[i];
@@ -215,8 +236,34 @@ __device__ __forceinline__ B3 prefix_borrow(const Keys& K, uint32_t op, uint32_t
   return g;
 }
 
+template <int L>
+__device__ __forceinline__ B3 prefix_borrow(const Keys& K, uint32_t op, uint32_t sub, uint32_t fb, uint64_t lane,
+                                            B3 g, B3 p) {
+  constexpr int NL = Levels<L>::n;
+  W2 blk[3 * NL];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int l = 0; l < NL; ++l) blk[i * NL + l] = word2(K.pair[i], op, sub, (fb >> 1) + l, lane);
+  return prefix_borrow_blk<L>(g, p, blk);
+}
+
 // Borrow rows S[i] = [c mod 2^{i+1} < r mod 2^{i+1}] for public c
 // (_borrow_scan, gadgets.py:163-171): g = r & ~c, p = r ^ ~c.
+template <int L>
+__device__ __forceinline__ B3 borrow_scan_blk(uint64_t c, const B3& Rb, const W2* blk) {
+  constexpr uint64_t M = Ring<L>::M;
+  const uint64_t notc = ~c & M;
+  B3 g, p;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    g.v[i] = Rb.v[i] & notc;
+    p.v[i] = Rb.v[i];
+  }
+  p.v[0] ^= notc;
+  return prefix_borrow_blk<L>(g, p, blk);
+}
+
 template <int L>
 __device__ __forceinline__ B3 borrow_scan(const Keys& K, uint32_t op, uint32_t sub, uint32_t fb, uint64_t lane,
                                           uint64_t c, const B3& Rb) {
@@ -280,20 +327,55 @@ __device__ __forceinline__ B3 lt(const Keys& K, uint32_t op, uint32_t sub, uint6
   return rows;
 }
 
-// Boolean bit -> arithmetic share (b2a, gadgets.py:223-231); bit 0 of b.
-// dealer fields: A0=0 A1=1 bits=2 (beta=bit0, Bb0=bit1, Bb1=bit2).
+// Boolean bit -> arithmetic share (b2a, gadgets.py:223-231) from a dabit:
+// arithmetic shares (A0, A1, beta - A0 - A1) and boolean shares of beta =
+// bit0 of `bits` with Bb0 = bit1, Bb1 = bit2 (_gen_dabits, dealer.py:420-424).
 template <int L>
-__device__ __forceinline__ A3 b2a(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const B3& b) {
+__device__ __forceinline__ A3 b2a_arith(const B3& b, uint64_t A0, uint64_t A1, uint64_t bits) {
   constexpr uint64_t M = Ring<L>::M;
-  const W2 w = word2(K.dealer, op, sub, 0, lane);
-  const uint64_t A0 = w.a & M, A1 = w.b & M;
-  const uint64_t bw = word(K.dealer, op, sub, 2, lane);
-  const uint64_t beta = bw & 1ull, Bb0 = (bw >> 1) & 1ull, Bb1 = (bw >> 2) & 1ull;
+  A0 &= M;
+  A1 &= M;
+  const uint64_t beta = bits & 1ull, Bb0 = (bits >> 1) & 1ull, Bb1 = (bits >> 2) & 1ull;
   const uint64_t Bb2 = beta ^ Bb0 ^ Bb1;
-  const uint64_t A2 = (beta - A0 - A1) & M;  // _gen_dabits, dealer.py:420-424
+  const uint64_t A2 = (beta - A0 - A1) & M;
   const uint64_t e = ((b.v[0] ^ Bb0) ^ (b.v[1] ^ Bb1) ^ (b.v[2] ^ Bb2)) & 1ull;  // open_bits
   const uint64_t coeff = (1ull - 2ull * e) & M;
   return a3(((A0 * coeff) + e) & M, (A1 * coeff) & M, (A2 * coeff) & M);
+}
+
+// standalone b2a: dealer fields A0=0 A1=1 bits=2.
+template <int L>
+__device__ __forceinline__ A3 b2a(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const B3& b) {
+  const W2 w = word2(K.dealer, op, sub, 0, lane);
+  return b2a_arith<L>(b, w.a, w.b, word(K.dealer, op, sub, 2, lane));
+}
+
+// One fused lookup / count lane (oaa.py:28-34, train.py:328-333): eq + b2a
+// (+ the select's reshare) draw from SIX Philox blocks, all halves used:
+//   dealer (sub,0) = (r, Rb0)   (sub,1) = (Rb1, A0)   (sub,2) = (A1, dabit bits)
+//   pair_i (sub,0) = (AND-tree zero word, mul zero-share word F_i)
+struct LaneRand {
+  uint64_t r, Rb0, Rb1, A0, A1, bits;
+  uint64_t Zw[3], F[3];
+};
+__device__ __forceinline__ LaneRand lane_rand(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane) {
+  LaneRand R;
+  const W2 d0 = word2(K.dealer, op, sub, 0, lane);
+  const W2 d1 = word2(K.dealer, op, sub, 1, lane);
+  const W2 d2 = word2(K.dealer, op, sub, 2, lane);
+  R.r = d0.a;
+  R.Rb0 = d0.b;
+  R.Rb1 = d1.a;
+  R.A0 = d1.b;
+  R.A1 = d2.a;
+  R.bits = d2.b;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const W2 p = word2(K.pair[i], op, sub, 0, lane);
+    R.Zw[i] = p.a;
+    R.F[i] = p.b;
+  }
+  return R;
 }
 
 // select_share (gadgets.py:238-253) for one condition lane and one payload
@@ -313,33 +395,75 @@ __device__ __forceinline__ A3 select1(const Keys& K, uint32_t op, uint32_t sub, 
 
 // Exact floor(x / 2^k), unsigned (truncate, gadgets.py:260-288).  Uses subs
 // sub (opening + borrow scan, dealer fields r=0 Rb0=1 Rb1=2 R0=3 R1=4 S0=5
-// S1=6), sub+1 (b2a of the wrap bit), sub+2 (b2a of the low borrow).
+// S1=6, pair fields 0..2*nlev-1), sub+1 (b2a of the wrap bit), sub+2 (b2a of
+// the low borrow).  In Philox blocks (TRUNC_BLOCKS of them, the order of a
+// tape): dealer (sub, 0..3), pair_i (sub, 0..nlev-1) for i = 0..2, dealer
+// (sub+1, 0..1), dealer (sub+2, 0..1).
 template <int L>
-__device__ __forceinline__ A3 trunc(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const A3& x, int k) {
+struct TruncRand {
+  static constexpr int NL = Levels<L>::n;
+  static constexpr int BLOCKS = 4 + 3 * NL + 4;
+  W2 b[BLOCKS];
+};
+
+template <int L>
+__device__ __forceinline__ void trunc_block_id(int j, uint32_t sub, int* key, uint32_t* s, uint32_t* pidx) {
+  constexpr int NL = Levels<L>::n;
+  if (j < 4) {
+    *key = -1, *s = sub, *pidx = j;
+  } else if (j < 4 + 3 * NL) {
+    *key = (j - 4) / NL, *s = sub, *pidx = (j - 4) % NL;
+  } else {
+    const int r = j - 4 - 3 * NL;
+    *key = -1, *s = sub + 1 + (r >> 1), *pidx = r & 1;
+  }
+}
+
+__device__ __forceinline__ W2 block_of(const Keys& K, int key, uint32_t op, uint32_t s, uint32_t pidx, uint64_t lane) {
+  return word2(key < 0 ? K.dealer : K.pair[key], op, s, pidx, lane);
+}
+
+template <int L>
+__device__ __forceinline__ A3 trunc_arith(const W2* b, const A3& x, int k) {
   constexpr uint64_t M = Ring<L>::M;
+  constexpr int NL = Levels<L>::n;
   if (k == 0) return x;
-  const uint64_t r = word(K.dealer, op, sub, 0, lane) & M;
+  const uint64_t r = b[0].a & M;
   B3 Rb;
-  Rb.v[0] = word(K.dealer, op, sub, 1, lane) & M;
-  Rb.v[1] = word(K.dealer, op, sub, 2, lane) & M;
+  Rb.v[0] = b[0].b & M;
+  Rb.v[1] = b[1].a & M;
   Rb.v[2] = r ^ Rb.v[0] ^ Rb.v[1];
-  const uint64_t R0 = word(K.dealer, op, sub, 3, lane) & M, R1 = word(K.dealer, op, sub, 4, lane) & M;
-  const uint64_t S0 = word(K.dealer, op, sub, 5, lane) & M, S1 = word(K.dealer, op, sub, 6, lane) & M;
+  const uint64_t S0 = b[2].b & M, S1 = b[3].a & M;
   const uint64_t S2 = ((r >> k) - S0 - S1) & M;  // _gen_truncpairs, dealer.py:427-432
-  const uint64_t c = open<L>(a3(x.v[0] + R0, x.v[1] + R1, x.v[2] + (r - R0 - R1)));
-  const B3 s = borrow_scan<L>(K, op, sub, 0, lane, c, Rb);
+  const uint64_t c = (open<L>(x) + r) & M;       // open_a(x + r)
+  const B3 s = borrow_scan_blk<L>(c, Rb, b + 4);
   B3 wrap, lowb;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     wrap.v[i] = (s.v[i] >> (L - 1)) & 1ull;
     lowb.v[i] = (s.v[i] >> (k - 1)) & 1ull;
   }
-  const A3 wa = b2a<L>(K, op, sub + 1, lane, wrap);
-  const A3 ba = b2a<L>(K, op, sub + 2, lane, lowb);
+  const W2* w = b + 4 + 3 * NL;
+  const A3 wa = b2a_arith<L>(wrap, w[0].a, w[0].b, w[1].a);
+  const A3 ba = b2a_arith<L>(lowb, w[2].a, w[2].b, w[3].a);
   const uint64_t sh = (1ull << (L - k)) & M;
   A3 out = a3((wa.v[0] * sh - S0 - ba.v[0]) & M, (wa.v[1] * sh - S1 - ba.v[1]) & M,
               (wa.v[2] * sh - S2 - ba.v[2]) & M);
   return add_pub<L>(out, c >> k);
+}
+
+template <int L>
+__device__ __forceinline__ A3 trunc(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const A3& x, int k) {
+  if (k == 0) return x;
+  W2 b[TruncRand<L>::BLOCKS];
+#pragma unroll
+  for (int j = 0; j < TruncRand<L>::BLOCKS; ++j) {
+    int key;
+    uint32_t s, pidx;
+    trunc_block_id<L>(j, sub, &key, &s, &pidx);
+    b[j] = block_of(K, key, op, s, pidx, lane);
+  }
+  return trunc_arith<L>(b, x, k);
 }
 
 // Public fixed-point division schedule (div_params, gadgets.py:297-307).

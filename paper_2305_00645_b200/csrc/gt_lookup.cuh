@@ -3,7 +3,8 @@
 // entry, the hit bit is converted (b2a) and multiplies the entry (select
 // against zero), and the picked shares are summed locally.  There is no
 // data-dependent addressing: every lane reads every entry.  Lane numbering
-// is (global index) * m + j, subs 0 (eq), 1 (b2a), 2 (mul).
+// is (global index) * m + j; the lane's eq, b2a and reshare draw from the six
+// Philox blocks of LaneRand at sub 0.
 #pragma once
 #include "gt_gadgets.cuh"
 
@@ -18,10 +19,11 @@ __device__ __forceinline__ A3 lookup_partial(const Keys& K, uint32_t op, uint64_
   for (int j = j0; j < m; j += js) {
     const uint64_t lane = gidx * (uint64_t)m + (uint64_t)j;
     const A3 d = add_pub<L>(idx, (0ull - (uint64_t)j) & Ring<L>::M);
-    const B3 hit = eqz<L>(K, op, 0, lane, d);
-    const A3 ca = b2a<L>(K, op, 1, lane, hit);
+    const LaneRand R = lane_rand(K, op, 0, lane);
+    const B3 hit = eq_arith<L>(d, R.r, R.Rb0, R.Rb1, R.Zw);
+    const A3 ca = b2a_arith<L>(hit, R.A0, R.A1, R.bits);
     // select_share(zero, rows, hit): w2 - w1 = rows (oaa.py:33)
-    acc = add<L>(acc, mul<L>(K, op, 2, 0, lane, entry(j), ca));
+    acc = add<L>(acc, mul_z<L>(entry(j), ca, R.F));
   }
   return acc;
 }

@@ -23,9 +23,21 @@
 
 namespace gt {
 
+// A Philox key with its 10-round schedule expanded once on the host
+// (k0 + r*W0, k1 + r*W1), so the round XORs take the round key straight from
+// the kernel's constant bank instead of re-deriving it per call.
 struct Key {
-  uint32_t k0, k1;
+  uint32_t k0[10], k1[10];
 };
+
+__host__ __device__ inline Key expand_key(uint32_t k0, uint32_t k1) {
+  Key k;
+  for (int r = 0; r < 10; ++r) {
+    k.k0[r] = k0 + (uint32_t)r * 0x9E3779B9u;
+    k.k1[r] = k1 + (uint32_t)r * 0xBB67AE85u;
+  }
+  return k;
+}
 
 // dealer key + the three pairwise keys; pair[i] is the seed shared by party
 // i+1 and its successor (SeedSetup.pair_seeds[i+1], transport.py:113-124).
@@ -38,19 +50,14 @@ struct W2 {
   uint64_t a, b;
 };
 
-__device__ __forceinline__ W2 philox(Key key, uint32_t op, uint32_t stream, uint64_t lane) {
+__device__ __forceinline__ W2 philox(const Key& key, uint32_t op, uint32_t stream, uint64_t lane) {
   uint32_t c0 = (uint32_t)lane, c1 = (uint32_t)(lane >> 32), c2 = stream, c3 = op;
-  uint32_t k0 = key.k0, k1 = key.k1;
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    if (r) {
-      k0 += 0x9E3779B9u;
-      k1 += 0xBB67AE85u;
-    }
     uint64_t p0 = (uint64_t)0xD2511F53u * c0;  // IMAD.WIDE.U32
     uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
-    uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
-    uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+    uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ key.k0[r];  // LOP3 with a c[] operand
+    uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ key.k1[r];
     c0 = n0;
     c1 = (uint32_t)p1;
     c2 = n2;
@@ -68,13 +75,13 @@ __device__ __forceinline__ uint32_t stream_of(uint32_t sub, uint32_t field) {
 
 // One 64-bit word of field `field` (fields 2j and 2j+1 share one Philox call;
 // when both are requested in one inlined scope the compiler CSEs the call).
-__device__ __forceinline__ uint64_t word(Key key, uint32_t op, uint32_t sub, uint32_t field, uint64_t lane) {
+__device__ __forceinline__ uint64_t word(const Key& key, uint32_t op, uint32_t sub, uint32_t field, uint64_t lane) {
   W2 w = philox(key, op, stream_of(sub, field), lane);
   return (field & 1) ? w.b : w.a;
 }
 
 // Both words of the block holding fields (2j, 2j+1).
-__device__ __forceinline__ W2 word2(Key key, uint32_t op, uint32_t sub, uint32_t pair_index, uint64_t lane) {
+__device__ __forceinline__ W2 word2(const Key& key, uint32_t op, uint32_t sub, uint32_t pair_index, uint64_t lane) {
   return philox(key, op, (sub << 8) | pair_index, lane);
 }
 

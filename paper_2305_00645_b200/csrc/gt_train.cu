@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "gt_common.cuh"
+#include "gt_division.cuh"
 #include "gt_lookup.cuh"
 
 namespace gt {
@@ -108,7 +109,8 @@ __global__ void k_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T
 // ---------------------------------------------------------------------------
 
 constexpr int CNT_TPB = 256;
-constexpr int CNT_ITEMS = 4;
+constexpr int CNT_ITEMS = 1;
+constexpr int CNT_MINB = 3;  // CTAs per SM the register budget is sized for
 
 struct CountArgs {
   const uint64_t *X, *P, *Y, *midx, *f;
@@ -119,7 +121,17 @@ struct CountArgs {
   uint32_t op_leaf, op_cnt;
 };
 
-__global__ void __launch_bounds__(CNT_TPB) k_count(CountArgs a) {
+// One CTA = (sample chunk, node block).  Per tile of TS samples:
+//  phase A, one lane per (sample, node):  la = b2a(eq(m_idx, off+n) & leaf[n])
+//    drawing the six Philox blocks of LaneRand at sub 0 (pair block half b
+//    = the AND gate's zero bit);
+//  phase B, one work item per (node, column pair): the W products
+//    mul(cols[s][w], la[s][n]) with their reshare (sub 3, field w), summed
+//    over the samples in registers; the mask column (w = W) adds la itself.
+// Every thread owns one item (replicas split the samples of a tile when there
+// are fewer items than threads); partial sums leave through one 64-bit
+// atomic per (item, column, component).
+__global__ void __launch_bounds__(CNT_TPB, CNT_MINB) k_count(CountArgs a) {
   extern __shared__ uint64_t sm[];
   const int nf = a.nf, W = 2 * nf + 1, WP = nf + 1, NB = a.nb, TS = a.ts;
   const int tid = threadIdx.x, bd = blockDim.x;
@@ -137,28 +149,17 @@ __global__ void __launch_bounds__(CNT_TPB) k_count(CountArgs a) {
     for (int c = 0; c < 3; ++c) leaf[c * NB + t] = z.v[c] & 1ull;
   }
 
-  // work items (node n, column pair wp); replicas split the tile's samples
   const int P = nb * WP;
-  const int R = P >= bd ? 1 : bd / P;
-  int item[CNT_ITEMS];
-  int nitems = 0, q = 0;
-  if (R > 1) {
-    if (tid < P * R) {
-      item[0] = tid % P;
-      q = tid / P;
-      nitems = 1;
-    }
-  } else {
-    for (int k = 0; k < CNT_ITEMS; ++k)
-      if (tid + k * bd < P) item[nitems++] = tid + k * bd;
-  }
-  uint64_t acc[CNT_ITEMS][2][3];
-#pragma unroll
-  for (int k = 0; k < CNT_ITEMS; ++k)
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) acc[k][h][c] = 0;
+  const int R = P >= bd ? 1 : bd / P;  // replicas split a tile's samples
+  const bool active = tid < P * R;
+  const int item = active ? tid % P : 0, q = tid / P;
+  const int n = item / WP, wp = item % WP;
+  const int w0 = 2 * wp, w1 = 2 * wp + 1;
+  const bool mask_col = w1 >= W;
+  // acc[h][c]: local cross terms of column w0 + h, component c;
+  // zacc[h][i]: sum of key i's zero-share words (alpha_i = F_i - F_{i-1} is
+  // applied once at the end: sum_s alpha_i = zacc[i] - zacc[i-1]).
+  uint64_t acc[2][3] = {{0, 0, 0}, {0, 0, 0}}, zacc[2][3] = {{0, 0, 0}, {0, 0, 0}};
 
   const uint64_t tile0 = (uint64_t)blockIdx.x * a.tiles_per_cta;
   for (int tt = 0; tt < a.tiles_per_cta; ++tt) {
@@ -169,6 +170,7 @@ __global__ void __launch_bounds__(CNT_TPB) k_count(CountArgs a) {
     for (int e = tid; e < cnt * W; e += bd) {
       const int s = e / W, w = e % W;
       const uint64_t sg = s0 + s;
+#pragma unroll
       for (int c = 0; c < 3; ++c) {
         uint64_t v;
         if (w < nf) v = a.X[c * nfx + sg * nf + w];
@@ -177,62 +179,86 @@ __global__ void __launch_bounds__(CNT_TPB) k_count(CountArgs a) {
         cols[(c * TS + s) * W + w] = v;
       }
     }
-    // lanes (s, n): la = b2a(eq(m_idx, off + n) & is_leaf[n])  train.py:328-331
+    // phase A                                             train.py:328-331
     for (int e = tid; e < cnt * nb; e += bd) {
-      const int s = e / nb, n = e % nb;
-      const uint64_t lane = (a.base + s0 + s) * (uint64_t)a.n_h + (uint64_t)(n0 + n);
-      const A3 d = add_pub<64>(ld3s(a.midx, a.N, s0 + s), 0ull - (uint64_t)(a.off + n0 + n));
-      const B3 hit = eqz<64>(K, a.op_cnt, 0, lane, d);
+      const int s = e / nb, nn = e % nb;
+      const uint64_t lane = (a.base + s0 + s) * (uint64_t)a.n_h + (uint64_t)(n0 + nn);
+      const A3 d = add_pub<64>(ld3s(a.midx, a.N, s0 + s), 0ull - (uint64_t)(a.off + n0 + nn));
+      const LaneRand Rr = lane_rand(K, a.op_cnt, 0, lane);
+      const B3 hit = eq_arith<64>(d, Rr.r, Rr.Rb0, Rr.Rb1, Rr.Zw);
       B3 lf;
-      for (int c = 0; c < 3; ++c) lf.v[c] = leaf[c * NB + n];
-      const B3 lcf = and_gate(K, a.op_cnt, 1, 0, lane, hit, lf, 1ull);
-      const A3 l = b2a<64>(K, a.op_cnt, 2, lane, lcf);
-      for (int c = 0; c < 3; ++c) la[(c * TS + s) * NB + n] = l.v[c];
+      uint64_t Z[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        lf.v[c] = leaf[c * NB + nn];
+        Z[c] = Rr.F[c] & 1ull;
+      }
+      const B3 lcf = and_z(hit, lf, Z);
+      const A3 l = b2a_arith<64>(lcf, Rr.A0, Rr.A1, Rr.bits);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) la[(c * TS + s) * NB + nn] = l.v[c];
     }
     __syncthreads();
-    // contrib = mul(rows, la) summed over samples        train.py:332-335
-#pragma unroll
-    for (int k = 0; k < CNT_ITEMS; ++k) {
-      if (k >= nitems) break;
-      const int n = item[k] / WP, wp = item[k] % WP;
-      const int w0 = 2 * wp, w1 = 2 * wp + 1;
-      for (int s = q; s < cnt; s += R) {
-        const uint64_t lane = (a.base + s0 + s) * (uint64_t)a.n_h + (uint64_t)(n0 + n);
-        const A3 l = a3(la[(0 * TS + s) * NB + n], la[(1 * TS + s) * NB + n], la[(2 * TS + s) * NB + n]);
+    // phase B: contrib = mul(rows, la) summed over samples   train.py:332-335
+    if (active) {
+      uint64_t lane = (a.base + s0 + q) * (uint64_t)a.n_h + (uint64_t)(n0 + n);
+      const uint64_t lstep = (uint64_t)R * a.n_h;
+      for (int s = q; s < cnt; s += R, lane += lstep) {
+        const uint64_t l0 = la[(0 * TS + s) * NB + n], l1 = la[(1 * TS + s) * NB + n], l2 = la[(2 * TS + s) * NB + n];
         const W2 F0 = word2(K.pair[0], a.op_cnt, 3, wp, lane);
         const W2 F1 = word2(K.pair[1], a.op_cnt, 3, wp, lane);
         const W2 F2 = word2(K.pair[2], a.op_cnt, 3, wp, lane);
         {
-          const uint64_t Fa[3] = {F0.a, F1.a, F2.a};
-          const A3 y = a3(cols[(0 * TS + s) * W + w0], cols[(1 * TS + s) * W + w0], cols[(2 * TS + s) * W + w0]);
-          const A3 z = mul_z<64>(y, l, Fa);
-          for (int c = 0; c < 3; ++c) acc[k][0][c] += z.v[c];
+          const uint64_t x0 = cols[(0 * TS + s) * W + w0], x1 = cols[(1 * TS + s) * W + w0],
+                         x2 = cols[(2 * TS + s) * W + w0];
+          // z_i = l_i (x_i + x_{i+1}) + x_i l_{i+1}   (rss.py:391-395, mul_z)
+          acc[0][0] += l0 * (x0 + x1) + x0 * l1;
+          acc[0][1] += l1 * (x1 + x2) + x1 * l2;
+          acc[0][2] += l2 * (x2 + x0) + x2 * l0;
+          zacc[0][0] += F0.a;
+          zacc[0][1] += F1.a;
+          zacc[0][2] += F2.a;
         }
-        if (w1 < W) {
-          const uint64_t Fb[3] = {F0.b, F1.b, F2.b};
-          const A3 y = a3(cols[(0 * TS + s) * W + w1], cols[(1 * TS + s) * W + w1], cols[(2 * TS + s) * W + w1]);
-          const A3 z = mul_z<64>(y, l, Fb);
-          for (int c = 0; c < 3; ++c) acc[k][1][c] += z.v[c];
+        if (!mask_col) {
+          const uint64_t x0 = cols[(0 * TS + s) * W + w1], x1 = cols[(1 * TS + s) * W + w1],
+                         x2 = cols[(2 * TS + s) * W + w1];
+          acc[1][0] += l0 * (x0 + x1) + x0 * l1;
+          acc[1][1] += l1 * (x1 + x2) + x1 * l2;
+          acc[1][2] += l2 * (x2 + x0) + x2 * l0;
+          zacc[1][0] += F0.b;
+          zacc[1][1] += F1.b;
+          zacc[1][2] += F2.b;
         } else {  // mask column: s_mask += la (local)
-          for (int c = 0; c < 3; ++c) acc[k][1][c] += l.v[c];
+          acc[1][0] += l0;
+          acc[1][1] += l1;
+          acc[1][2] += l2;
         }
       }
     }
   }
+  if (!active) return;
   const uint64_t Sstride = (uint64_t)a.n_h * (W + 1);
-  for (int k = 0; k < nitems; ++k) {
-    const int n = item[k] / WP, wp = item[k] % WP;
-    for (int h = 0; h < 2; ++h) {
-      const int w = 2 * wp + h;
-      for (int c = 0; c < 3; ++c)
-        atomicAdd((unsigned long long*)&a.S[c * Sstride + (uint64_t)(n0 + n) * (W + 1) + w],
-                  (unsigned long long)acc[k][h][c]);
-    }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int w = 2 * wp + h;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      atomicAdd((unsigned long long*)&a.S[c * Sstride + (uint64_t)(n0 + n) * (W + 1) + w],
+                (unsigned long long)(acc[h][c] + zacc[h][c] - zacc[h][(c + 2) % 3]));
   }
 }
 
 // ---------------------------------------------------------------------------
-// per-node step: counters, heuristic (mpc), replace
+// per-node heuristic (_heuristic_mpc, train.py:346-388) + replace, in three
+// kernels so no thread waits on another's serial chain:
+//   k_hc_pre   one CTA per node: counter assembly; warp 0 runs the short
+//              probe/featureless/should_split/new_f chain and then replace;
+//              warps 1-7 truncate + ring_down the counters, form the squares
+//              and Q products and the Q==0 fix (pv, qs -> global)
+//   k_hc_div   one WARP per (node, column): division_warp (ladder over the
+//              lanes, Newton chain from a cooperatively drawn Philox tape)
+//   k_hc_post  one CTA per node: scores, masked argmin tournament, budget
+//              clear
 // ---------------------------------------------------------------------------
 
 struct NodeArgs {
@@ -243,36 +269,29 @@ struct NodeArgs {
   const uint64_t* ceff_prev;  // [3][n_h/2][3][cols]
   uint64_t* ceff;             // [3][n_h][3][cols]
   uint64_t* hc;               // [4][3][n_h]: should_split, sd, new_f, new_gam
+  uint64_t* dv;               // [3][3][n_h*cols]: P, Q+[Q==0], division terms
   int n_h, nf, level, last, shift, tau;
   DivParams d;
   Keys K;
 };
 
+__device__ __forceinline__ void bar_workers() { asm volatile("bar.sync 1, 224;" ::: "memory"); }
+
 template <int SL>
-__global__ void __launch_bounds__(256) k_node_hc(NodeArgs a) {
+__global__ void __launch_bounds__(256) k_hc_pre(NodeArgs a) {
   extern __shared__ uint64_t sm[];
   constexpr uint64_t MS = Ring<SL>::M;
-  const int n = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
-  const int nf = a.nf, cols = 2 * nf, W = cols + 1, n_h = a.n_h;
-  const int C3 = 3 * cols;
-  uint64_t* co = sm;              // [3][3*cols] c_orig
-  uint64_t* c32 = co + 3 * C3;    // [3][3*cols] truncated + ring_down
-  uint64_t* pr = c32 + 3 * C3;    // [3][4*cols] products
-  uint64_t* pv = pr + 12 * cols;  // [3][cols]
-  uint64_t* qs = pv + 3 * cols;
-  uint64_t* vac = qs + 3 * cols;
-  uint64_t* tm = vac + 3 * cols;
-  uint64_t* vals = tm + 3 * cols;  // [3][nf]
-  uint64_t* idxs = vals + 3 * nf;
-  uint64_t* nvals = idxs + 3 * nf;
-  uint64_t* nidxs = nvals + 3 * nf;
-  uint64_t* misc = nidxs + 3 * nf;  // zeros[3][3], hitw[3], ss[3], ca[3]
+  const int n = blockIdx.x, tid = threadIdx.x;
+  const int nf = a.nf, cols = 2 * nf, W = cols + 1, C3 = 3 * cols;
+  const uint64_t hs = (uint64_t)a.n_h, lanes = hs * cols;
+  uint64_t* co = sm;            // [3][3*cols] c_orig
+  uint64_t* c32 = co + 3 * C3;  // [3][3*cols]
+  uint64_t* pr = c32 + 3 * C3;  // [3][4*cols]
   const Keys& K = a.K;
   const uint32_t opH = op_id(a.level, SITE_HC), opR = op_id(a.level, SITE_REPLACE);
-  const uint64_t hs = (uint64_t)n_h;
 
   // c_orig = c_start + assembled counters (train.py:256, 336-343)
-  for (int e = tid; e < 3 * C3; e += bd) {
+  for (int e = tid; e < 3 * C3; e += blockDim.x) {
     const int c = e / C3, rk = e % C3, r = rk / cols, k = rk % cols, i = k >> 1, j = k & 1;
     const uint64_t* Sn = a.S + (uint64_t)c * hs * (W + 1) + (uint64_t)n * (W + 1);
     const uint64_t s1 = Sn[W], sx = Sn[i], sp = Sn[nf + i], sy = Sn[2 * nf];
@@ -285,180 +304,191 @@ __global__ void __launch_bounds__(256) k_node_hc(NodeArgs a) {
   __syncthreads();
   auto CO = [&](int e) { return a3(co[e], co[C3 + e], co[2 * C3 + e]); };
 
-  if (!a.last) {
-    const A3 fl = ld3s(a.f, hs, n);
-    const B3 gam = ldb3s(a.gam, hs, n);
-    // zeros = eq([psi0, psi1, F - LEAF], 0)                 train.py:353-359
-    if (tid < 3) {
-      A3 v;
-      if (tid == 0) v = add<64>(CO(cols + 0), CO(cols + 1));
-      else if (tid == 1) v = add<64>(CO(2 * cols + 0), CO(2 * cols + 1));
-      else v = add_pub<64>(fl, 0ull - F_LEAF);
-      const B3 z = eqz<64>(K, opH, 0, (uint64_t)n * 3 + tid, v);
-      for (int c = 0; c < 3; ++c) misc[c * 3 + tid] = z.v[c] & 1ull;
-    }
-    __syncthreads();
-    if (tid == 0) {
+  if (tid < 32) {
+    const int wl = tid;
+    if (!a.last) {
+      // zeros = eq([psi0, psi1, F - LEAF], 0)                 train.py:353-359
+      const A3 fl = ld3s(a.f, hs, n);
+      B3 z = {{0, 0, 0}};
+      if (wl < 3) {
+        A3 v;
+        if (wl == 0) v = add<64>(CO(cols + 0), CO(cols + 1));
+        else if (wl == 1) v = add<64>(CO(2 * cols + 0), CO(2 * cols + 1));
+        else v = add_pub<64>(fl, 0ull - F_LEAF);
+        z = eqz<64>(K, opH, 0, (uint64_t)n * 3 + wl, v);
+      }
       B3 p0, p1, act;
+#pragma unroll
       for (int c = 0; c < 3; ++c) {
-        p0.v[c] = misc[c * 3 + 0];
-        p1.v[c] = misc[c * 3 + 1];
-        act.v[c] = misc[c * 3 + 2];
+        p0.v[c] = __shfl_sync(0xffffffffu, z.v[c], 0) & 1ull;
+        p1.v[c] = __shfl_sync(0xffffffffu, z.v[c], 1) & 1ull;
+        act.v[c] = __shfl_sync(0xffffffffu, z.v[c], 2) & 1ull;
       }
-      // featureless = and_reduce(~gam), leafish, should_split   train.py:360-364
-      const B3 fless = and_reduce(K, opH, 1, 0, n, bnot(gam, lowmask(nf)), nf);
-      const B3 o1 = or_gate(K, opH, 2, n, p0, p1, 1ull);
-      const B3 leafish = or_gate(K, opH, 3, n, o1, fless, 1ull);
-      const B3 ss = and_gate(K, opH, 4, 0, n, act, bnot(leafish, 1ull), 1ull);
-      const A3 nf_sh = select1<64>(K, opH, 5, n, fl, a3(0, 0, 0), ss);
-      for (int c = 0; c < 3; ++c) {
-        a.hc[(0 * 3 + c) * hs + n] = ss.v[c] & 1ull;
-        a.hc[(2 * 3 + c) * hs + n] = nf_sh.v[c];
-      }
-    }
-    // counters: truncate by the public shift, ring_down      train.py:366-370
-    for (int e = tid; e < C3; e += bd) {
-      A3 x = CO(e);
-      if (a.shift) x = trunc<64>(K, opH, 7, (uint64_t)n * C3 + e, x, a.shift);
-      for (int c = 0; c < 3; ++c) c32[c * C3 + e] = x.v[c] & MS;
-    }
-    __syncthreads();
-    auto C32 = [&](int e) { return a3(c32[e], c32[C3 + e], c32[2 * C3 + e]); };
-    // prods = mul([c32, a], [c32, tot_rep])                   train.py:371-376
-    for (int e = tid; e < 4 * cols; e += bd) {
-      A3 x, y;
-      if (e < C3) {
-        x = C32(e);
-        y = x;
-      } else {
-        const int k = e - C3, i = k >> 1;
-        x = C32(k);
-        y = add<SL>(C32(2 * i), C32(2 * i + 1));
-      }
-      const A3 z = mul<SL>(K, opH, 10, 0, (uint64_t)n * 4 * cols + e, x, y);
-      for (int c = 0; c < 3; ++c) pr[c * 4 * cols + e] = z.v[c];
-    }
-    __syncthreads();
-    auto PR = [&](int e) { return a3(pr[e], pr[4 * cols + e], pr[8 * cols + e]); };
-    // P = a^2 - m0^2 - m1^2, qsafe = Q + b2a(eq(Q, 0))       train.py:377-381
-    for (int k = tid; k < cols; k += bd) {
-      const A3 p = diff<SL>(diff<SL>(PR(k), PR(cols + k)), PR(2 * cols + k));
-      const A3 q = PR(C3 + k);
-      const uint64_t lane = (uint64_t)n * cols + k;
-      const B3 qz = eqz<SL>(K, opH, 11, lane, q);
-      const A3 qsv = add<SL>(q, b2a<SL>(K, opH, 12, lane, qz));
-      for (int c = 0; c < 3; ++c) {
-        pv[c * cols + k] = p.v[c];
-        qs[c * cols + k] = qsv.v[c];
-        vac[c * cols + k] = 0;
-      }
-    }
-    __syncthreads();
-    auto QS = [&](int k) { return a3(qs[k], qs[cols + k], qs[2 * cols + k]); };
-    // division ladder: one lane per (column, power)         gadgets.py:327-336
-    const int nl = a.d.bound - 1;
-    for (int e = tid; e < nl * cols; e += bd) {
-      const int j = e / cols + 1, k = e % cols;
-      const A3 t = div_ladder_term<SL>(K, opH, 13, (uint64_t)n * cols + k, QS(k), j, a.d);
-      for (int c = 0; c < 3; ++c) atomicAdd((unsigned long long*)&vac[c * cols + k], (unsigned long long)t.v[c]);
-    }
-    __syncthreads();
-    // Newton reciprocal + rescale per column                gadgets.py:338-349
-    for (int k = tid; k < cols; k += bd) {
-      const A3 acc = a3(vac[k] & MS, vac[cols + k] & MS, vac[2 * cols + k] & MS);
-      const A3 v = rsub_pub<SL>(1ull << (a.d.bound - 1), acc);
-      const A3 p = a3(pv[k], pv[cols + k], pv[2 * cols + k]);
-      const A3 t = div_newton<SL>(K, opH, 13 + 2 * nl, (uint64_t)n * cols + k, p, QS(k), v, a.d);
-      for (int c = 0; c < 3; ++c) tm[c * cols + k] = t.v[c];
-    }
-    __syncthreads();
-    // scores + masked argmin (tournament)     train.py:383-385, gadgets.py:366-401
-    const uint32_t SA = 13 + div_subs(a.d);
-    const uint64_t worst = (1ull << (a.tau + 1)) & MS;
-    for (int i = tid; i < nf; i += bd) {
-      const A3 score = add<SL>(a3(tm[2 * i], tm[cols + 2 * i], tm[2 * cols + 2 * i]),
-                               a3(tm[2 * i + 1], tm[cols + 2 * i + 1], tm[2 * cols + 2 * i + 1]));
-      B3 av;
-      for (int c = 0; c < 3; ++c) av.v[c] = (gam.v[c] >> i) & 1ull;
-      const A3 v = select1<SL>(K, opH, SA, (uint64_t)n * nf + i, a3_const(worst), score, av);
-      for (int c = 0; c < 3; ++c) {
-        vals[c * nf + i] = v.v[c];
-        idxs[c * nf + i] = c == 0 ? (uint64_t)i : 0ull;
-      }
-    }
-    __syncthreads();
-    int m = nf;
-    for (int r = 0; m > 1; ++r) {
-      const int pairs = m / 2;
-      const uint32_t base = SA + 2 + 5 * r;
-      for (int p = tid; p < pairs; p += bd) {
-        const uint64_t lane = (uint64_t)n * nf + p;
-        const A3 av = a3(vals[2 * p], vals[nf + 2 * p], vals[2 * nf + 2 * p]);
-        const A3 bv = a3(vals[2 * p + 1], vals[nf + 2 * p + 1], vals[2 * nf + 2 * p + 1]);
-        const A3 ai = a3(idxs[2 * p], idxs[nf + 2 * p], idxs[2 * nf + 2 * p]);
-        const A3 bi = a3(idxs[2 * p + 1], idxs[nf + 2 * p + 1], idxs[2 * nf + 2 * p + 1]);
-        const B3 cw = lt<SL>(K, opH, base, lane, bv, av);
-        const A3 nv = select1<SL>(K, opH, base + 1, lane, av, bv, cw);
-        const A3 ni = select1<64>(K, opH, base + 3, lane, ai, bi, cw);
+      if (wl == 0) {
+        // featureless = and_reduce(~gam), leafish, should_split   train.py:360-364
+        const B3 gam = ldb3s(a.gam, hs, n);
+        const B3 fless = and_reduce(K, opH, 1, 0, n, bnot(gam, lowmask(nf)), nf);
+        const B3 o1 = or_gate(K, opH, 2, n, p0, p1, 1ull);
+        const B3 leafish = or_gate(K, opH, 3, n, o1, fless, 1ull);
+        const B3 ss = and_gate(K, opH, 4, 0, n, act, bnot(leafish, 1ull), 1ull);
+        const A3 nfv = select1<64>(K, opH, 5, n, fl, a3(0, 0, 0), ss);
         for (int c = 0; c < 3; ++c) {
-          nvals[c * nf + p] = nv.v[c];
-          nidxs[c * nf + p] = ni.v[c];
+          a.hc[(0 * 3 + c) * hs + n] = ss.v[c] & 1ull;
+          a.hc[(2 * 3 + c) * hs + n] = nfv.v[c];
         }
       }
-      if (tid == 0 && (m & 1))
-        for (int c = 0; c < 3; ++c) {
-          nvals[c * nf + pairs] = vals[c * nf + m - 1];
-          nidxs[c * nf + pairs] = idxs[c * nf + m - 1];
-        }
-      __syncthreads();
-      const int nm = pairs + (m & 1);
-      for (int p = tid; p < nm; p += bd)
-        for (int c = 0; c < 3; ++c) {
-          vals[c * nf + p] = nvals[c * nf + p];
-          idxs[c * nf + p] = nidxs[c * nf + p];
-        }
-      __syncthreads();
-      m = nm;
     }
-    const A3 sd = a3(idxs[0], idxs[nf], idxs[2 * nf]);
-    // gamma &= ~[sd == k]                                     train.py:386-387
-    const uint32_t SH = SA + 2 + 5 * 7;
-    uint64_t* hitw = misc + 9;
-    if (tid < 3) hitw[tid] = 0;
-    __syncthreads();
-    for (int f = tid; f < nf; f += bd) {
-      const B3 h = eqz<64>(K, opH, SH, (uint64_t)n * nf + f, add_pub<64>(sd, 0ull - (uint64_t)f));
-      for (int c = 0; c < 3; ++c) atomicOr((unsigned long long*)&hitw[c], (unsigned long long)((h.v[c] & 1ull) << f));
-    }
-    __syncthreads();
-    if (tid == 0) {
-      B3 hw;
-      for (int c = 0; c < 3; ++c) hw.v[c] = hitw[c];
-      const B3 ng = and_gate(K, opH, SH + 1, 0, n, gam, bnot(hw, lowmask(nf)), lowmask(nf));
-      for (int c = 0; c < 3; ++c) {
-        a.hc[(1 * 3 + c) * hs + n] = sd.v[c];
-        a.hc[(3 * 3 + c) * hs + n] = ng.v[c];
+    // replace: empty nodes adopt the parent's effective counters  train.py:269-276
+    if (a.level > 0) {
+      A3 ca = a3(0, 0, 0);
+      if (wl == 0) ca = b2a<64>(K, opR, 1, n, eqz<64>(K, opR, 0, n, add<64>(CO(0), CO(1))));
+#pragma unroll
+      for (int c = 0; c < 3; ++c) ca.v[c] = __shfl_sync(0xffffffffu, ca.v[c], 0);
+      const uint64_t pn = (uint64_t)(n >> 1);
+      for (int e = wl; e < C3; e += 32) {
+        const A3 par = ld3s(a.ceff_prev, (hs / 2) * C3, pn * C3 + e);
+        st3s(a.ceff, hs * C3, (uint64_t)n * C3 + e, select_with<64>(K, opR, 1, (uint32_t)e, n, CO(e), par, ca));
       }
+    } else {
+      for (int e = wl; e < C3; e += 32) st3s(a.ceff, hs * C3, (uint64_t)n * C3 + e, CO(e));
+    }
+    return;
+  }
+  if (a.last) return;
+  const int wt = tid - 32, wn = blockDim.x - 32;  // 224 worker threads
+  // counters: truncate by the public shift, ring_down      train.py:366-370
+  for (int e = wt; e < C3; e += wn) {
+    A3 x = CO(e);
+    if (a.shift) x = trunc<64>(K, opH, 7, (uint64_t)n * C3 + e, x, a.shift);
+    for (int c = 0; c < 3; ++c) c32[c * C3 + e] = x.v[c] & MS;
+  }
+  bar_workers();
+  auto C32 = [&](int e) { return a3(c32[e], c32[C3 + e], c32[2 * C3 + e]); };
+  // prods = mul([c32, a], [c32, tot_rep])                   train.py:371-376
+  for (int e = wt; e < 4 * cols; e += wn) {
+    A3 x, y;
+    if (e < C3) {
+      x = C32(e);
+      y = x;
+    } else {
+      const int k = e - C3, i = k >> 1;
+      x = C32(k);
+      y = add<SL>(C32(2 * i), C32(2 * i + 1));
+    }
+    const A3 z = mul<SL>(K, opH, 10, 0, (uint64_t)n * 4 * cols + e, x, y);
+    for (int c = 0; c < 3; ++c) pr[c * 4 * cols + e] = z.v[c];
+  }
+  bar_workers();
+  auto PR = [&](int e) { return a3(pr[e], pr[4 * cols + e], pr[8 * cols + e]); };
+  // P = a^2 - m0^2 - m1^2, qsafe = Q + b2a(eq(Q, 0))       train.py:377-381
+  for (int k = wt; k < cols; k += wn) {
+    const A3 p = diff<SL>(diff<SL>(PR(k), PR(cols + k)), PR(2 * cols + k));
+    const A3 q = PR(C3 + k);
+    const uint64_t lane = (uint64_t)n * cols + k;
+    const B3 qz = eqz<SL>(K, opH, 11, lane, q);
+    const A3 qsv = add<SL>(q, b2a<SL>(K, opH, 12, lane, qz));
+    st3s(a.dv, lanes, lane, p);
+    st3s(a.dv + 3 * lanes, lanes, lane, qsv);
+  }
+}
+
+constexpr int DIV_WARPS = 4;
+
+template <int SL>
+__global__ void __launch_bounds__(32 * DIV_WARPS) k_hc_div(NodeArgs a) {
+  extern __shared__ W2 tape_sm[];
+  const int warp = threadIdx.x >> 5;
+  const uint64_t cols = 2 * (uint64_t)a.nf, lanes = (uint64_t)a.n_h * cols;
+  const uint64_t li = (uint64_t)blockIdx.x * DIV_WARPS + warp;
+  if (li >= lanes) return;  // whole warp exits together
+  W2* tape = tape_sm + (size_t)warp * newton_blocks<SL>(a.d);
+  const A3 p = ld3s(a.dv, lanes, li), q = ld3s(a.dv + 3 * lanes, lanes, li);
+  // terms = division(P, qsafe)                              train.py:382
+  const A3 t = division_warp<SL>(a.K, op_id(a.level, SITE_HC), 13, li, p, q, a.d, tape);
+  if ((threadIdx.x & 31) == 0) st3s(a.dv + 6 * lanes, lanes, li, t);
+}
+
+template <int SL>
+__global__ void __launch_bounds__(256) k_hc_post(NodeArgs a) {
+  extern __shared__ uint64_t sm[];
+  constexpr uint64_t MS = Ring<SL>::M;
+  const int n = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
+  const int nf = a.nf, cols = 2 * nf;
+  const uint64_t hs = (uint64_t)a.n_h, lanes = hs * cols;
+  uint64_t* vals = sm;  // [3][nf]
+  uint64_t* idxs = vals + 3 * nf;
+  uint64_t* nvals = idxs + 3 * nf;
+  uint64_t* nidxs = nvals + 3 * nf;
+  uint64_t* hitw = nidxs + 3 * nf;  // [3]
+  const Keys& K = a.K;
+  const uint32_t opH = op_id(a.level, SITE_HC);
+  const B3 gam = ldb3s(a.gam, hs, n);
+  const uint64_t* terms = a.dv + 6 * lanes;
+  auto TM = [&](int k) { return ld3s(terms, lanes, (uint64_t)n * cols + k); };
+  // scores + masked argmin (tournament)     train.py:383-385, gadgets.py:366-401
+  const uint32_t SA = 13 + div_subs(a.d);
+  const uint64_t worst = (1ull << (a.tau + 1)) & MS;
+  for (int i = tid; i < nf; i += bd) {
+    const A3 score = add<SL>(TM(2 * i), TM(2 * i + 1));
+    B3 av;
+    for (int c = 0; c < 3; ++c) av.v[c] = (gam.v[c] >> i) & 1ull;
+    const A3 v = select1<SL>(K, opH, SA, (uint64_t)n * nf + i, a3_const(worst), score, av);
+    for (int c = 0; c < 3; ++c) {
+      vals[c * nf + i] = v.v[c];
+      idxs[c * nf + i] = c == 0 ? (uint64_t)i : 0ull;
     }
   }
-
-  // replace: empty nodes adopt the parent's effective counters  train.py:269-276
-  uint64_t* ca = misc + 12;
-  if (a.level > 0) {
-    if (tid == 0) {
-      const B3 ie = eqz<64>(K, opR, 0, n, add<64>(CO(0), CO(1)));
-      const A3 c = b2a<64>(K, opR, 1, n, ie);
-      for (int i = 0; i < 3; ++i) ca[i] = c.v[i];
+  if (tid < 3) hitw[tid] = 0;
+  __syncthreads();
+  int m = nf;
+  for (int r = 0; m > 1; ++r) {
+    const int pairs = m / 2;
+    const uint32_t base = SA + 2 + 5 * r;
+    for (int p = tid; p < pairs; p += bd) {
+      const uint64_t lane = (uint64_t)n * nf + p;
+      const A3 av = a3(vals[2 * p], vals[nf + 2 * p], vals[2 * nf + 2 * p]);
+      const A3 bv = a3(vals[2 * p + 1], vals[nf + 2 * p + 1], vals[2 * nf + 2 * p + 1]);
+      const A3 ai = a3(idxs[2 * p], idxs[nf + 2 * p], idxs[2 * nf + 2 * p]);
+      const A3 bi = a3(idxs[2 * p + 1], idxs[nf + 2 * p + 1], idxs[2 * nf + 2 * p + 1]);
+      const B3 cw = lt<SL>(K, opH, base, lane, bv, av);
+      const A3 nv = select1<SL>(K, opH, base + 1, lane, av, bv, cw);
+      const A3 ni = select1<64>(K, opH, base + 3, lane, ai, bi, cw);
+      for (int c = 0; c < 3; ++c) {
+        nvals[c * nf + p] = nv.v[c];
+        nidxs[c * nf + p] = ni.v[c];
+      }
     }
+    if (tid == 0 && (m & 1))
+      for (int c = 0; c < 3; ++c) {
+        nvals[c * nf + pairs] = vals[c * nf + m - 1];
+        nidxs[c * nf + pairs] = idxs[c * nf + m - 1];
+      }
     __syncthreads();
-    const A3 cav = a3(ca[0], ca[1], ca[2]);
-    const uint64_t pn = (uint64_t)(n >> 1);
-    for (int e = tid; e < C3; e += bd) {
-      const A3 par = ld3s(a.ceff_prev, (hs / 2) * C3, pn * C3 + e);
-      st3s(a.ceff, hs * C3, (uint64_t)n * C3 + e, select_with<64>(K, opR, 1, (uint32_t)e, n, CO(e), par, cav));
+    const int nm = pairs + (m & 1);
+    for (int p = tid; p < nm; p += bd)
+      for (int c = 0; c < 3; ++c) {
+        vals[c * nf + p] = nvals[c * nf + p];
+        idxs[c * nf + p] = nidxs[c * nf + p];
+      }
+    __syncthreads();
+    m = nm;
+  }
+  const A3 sd = a3(idxs[0], idxs[nf], idxs[2 * nf]);
+  // gamma &= ~[sd == k]                                     train.py:386-387
+  const uint32_t SH = SA + 2 + 5 * 7;
+  for (int f = tid; f < nf; f += bd) {
+    const B3 h = eqz<64>(K, opH, SH, (uint64_t)n * nf + f, add_pub<64>(sd, 0ull - (uint64_t)f));
+    for (int c = 0; c < 3; ++c) atomicOr((unsigned long long*)&hitw[c], (unsigned long long)((h.v[c] & 1ull) << f));
+  }
+  __syncthreads();
+  if (tid == 0) {
+    B3 hw;
+    for (int c = 0; c < 3; ++c) hw.v[c] = hitw[c];
+    const B3 ng = and_gate(K, opH, SH + 1, 0, n, gam, bnot(hw, lowmask(nf)), lowmask(nf));
+    for (int c = 0; c < 3; ++c) {
+      a.hc[(1 * 3 + c) * hs + n] = sd.v[c];
+      a.hc[(3 * 3 + c) * hs + n] = ng.v[c];
     }
-  } else {
-    for (int e = tid; e < C3; e += bd) st3s(a.ceff, hs * C3, (uint64_t)n * C3 + e, CO(e));
   }
 }
 
@@ -538,7 +568,7 @@ __global__ void __launch_bounds__(128) k_node_finish(FinishArgs a) {
 // ---------------------------------------------------------------------------
 
 struct Layout {
-  uint64_t prods, midx, S, f[2], gam[2], cst[2], ceff[2], hc, stop, total;  // word offsets
+  uint64_t prods, midx, S, f[2], gam[2], cst[2], ceff[2], hc, dv, stop, total;  // word offsets
 };
 
 Layout layout(const gt_train_cfg& c) {
@@ -561,22 +591,30 @@ Layout layout(const gt_train_cfg& c) {
     L.ceff[i] = take(3 * nmax * 3 * cols);
   }
   L.hc = take(12 * nmax);
+  L.dv = take(9 * nmax * cols);
   L.stop = take(4);
   L.total = o;
   return L;
 }
 
-int node_smem_bytes(int nf) {
-  const int cols = 2 * nf;
-  return (int)sizeof(uint64_t) * (9 * cols + 9 * cols + 12 * cols + 12 * cols + 12 * nf + 16);
-}
-
 template <int SL>
 int launch_node_hc(const NodeArgs& na, cudaStream_t s) {
-  const int smem = node_smem_bytes(na.nf);
-  if (smem > 48 * 1024) GT_CUDA_CHECK(cudaFuncSetAttribute(k_node_hc<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_node_hc<SL><<<na.n_h, 256, smem, s>>>(na);
-  GT_LAUNCH_CHECK("k_node_hc");
+  const int cols = 2 * na.nf;
+  const int pre_smem = (int)sizeof(uint64_t) * (9 * cols + 9 * cols + 12 * cols);
+  if (pre_smem > 48 * 1024)
+    GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_pre<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, pre_smem));
+  k_hc_pre<SL><<<na.n_h, 256, pre_smem, s>>>(na);
+  GT_LAUNCH_CHECK("k_hc_pre");
+  if (na.last) return GT_OK;
+  const uint64_t lanes = (uint64_t)na.n_h * cols;
+  const int div_smem = (int)sizeof(W2) * DIV_WARPS * newton_blocks<SL>(na.d);
+  if (div_smem > 48 * 1024)
+    GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_div<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, div_smem));
+  k_hc_div<SL><<<(unsigned)((lanes + DIV_WARPS - 1) / DIV_WARPS), 32 * DIV_WARPS, div_smem, s>>>(na);
+  GT_LAUNCH_CHECK("k_hc_div");
+  const int post_smem = (int)sizeof(uint64_t) * (12 * na.nf + 4);
+  k_hc_post<SL><<<na.n_h, 256, post_smem, s>>>(na);
+  GT_LAUNCH_CHECK("k_hc_post");
   return GT_OK;
 }
 
@@ -590,24 +628,6 @@ int launch_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint6
   k_partition<G><<<grid, TPB, smem, s>>>(X, midx, T, slots, m, nf, N, base, K, op_id(level, SITE_PART_OAA),
                                          op_id(level, SITE_PART_ROW));
   GT_LAUNCH_CHECK("k_partition");
-  return GT_OK;
-}
-
-int launch_count(CountArgs ca, cudaStream_t s, int num_sms) {
-  const int nf = ca.nf, W = 2 * nf + 1, WP = nf + 1;
-  ca.nb = std::max(1, std::min(ca.n_h, (CNT_ITEMS * CNT_TPB) / WP));
-  ca.nb = std::min(ca.nb, 32);
-  ca.ts = 32;
-  const unsigned gy = (unsigned)((ca.n_h + ca.nb - 1) / ca.nb);
-  const uint64_t tiles = (ca.N + ca.ts - 1) / ca.ts;
-  const uint64_t target = std::max<uint64_t>(1, (uint64_t)num_sms * 8 / gy);
-  const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>(tiles, target));
-  ca.tiles_per_cta = (int)((tiles + gx - 1) / gx);
-  const unsigned gxx = (unsigned)((tiles + ca.tiles_per_cta - 1) / ca.tiles_per_cta);
-  const int smem = (int)sizeof(uint64_t) * (3 * ca.ts * W + 3 * ca.ts * ca.nb + 3 * ca.nb);
-  if (smem > 48 * 1024) GT_CUDA_CHECK(cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_count<<<dim3(gxx, gy), CNT_TPB, smem, s>>>(ca);
-  GT_LAUNCH_CHECK("k_count");
   return GT_OK;
 }
 
@@ -666,6 +686,46 @@ struct Prof {
     return GT_OK;
   }
 };
+
+// Node block size: the (node, column-pair) items of a block should fill the
+// 256 threads (<= CNT_ITEMS each) with as little idle as possible.
+int choose_node_block(int n_h, int WP) {
+  int best = 1;
+  double best_eff = -1.0;
+  for (int nb = 1; nb <= std::min(n_h, 64); ++nb) {
+    const int P = nb * WP;
+    if (P > CNT_ITEMS * CNT_TPB) break;
+    double eff;
+    if (P >= CNT_TPB) {
+      const int per = (P + CNT_TPB - 1) / CNT_TPB;
+      eff = (double)P / (double)(per * CNT_TPB);
+    } else {
+      eff = (double)(P * (CNT_TPB / P)) / CNT_TPB;
+    }
+    if (eff > best_eff + 1e-9 || (eff > best_eff - 1e-9 && nb > best)) {
+      best_eff = eff;
+      best = nb;
+    }
+  }
+  return best;
+}
+
+int launch_count(CountArgs ca, cudaStream_t s, int num_sms) {
+  const int nf = ca.nf, W = 2 * nf + 1, WP = nf + 1;
+  ca.nb = choose_node_block(ca.n_h, WP);
+  ca.ts = 32;
+  const unsigned gy = (unsigned)((ca.n_h + ca.nb - 1) / ca.nb);
+  const uint64_t tiles = (ca.N + ca.ts - 1) / ca.ts;
+  const uint64_t target = std::max<uint64_t>(1, (uint64_t)num_sms * CNT_MINB * 4 / gy);
+  const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>(tiles, target));
+  ca.tiles_per_cta = (int)((tiles + gx - 1) / gx);
+  const unsigned gxx = (unsigned)((tiles + ca.tiles_per_cta - 1) / ca.tiles_per_cta);
+  const int smem = (int)sizeof(uint64_t) * (3 * ca.ts * W + 3 * ca.ts * ca.nb + 3 * ca.nb);
+  if (smem > 48 * 1024) GT_CUDA_CHECK(cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k_count<<<dim3(gxx, gy), CNT_TPB, smem, s>>>(ca);
+  GT_LAUNCH_CHECK("k_count");
+  return GT_OK;
+}
 
 int counter_shift(uint64_t n, int score_width, int tau) {  // train.py:189-192
   int headroom = (score_width - tau - 2) / 2;
@@ -790,6 +850,7 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
     na.ceff_prev = ceff[cur ^ 1];
     na.ceff = ceff[cur];
     na.hc = hc;
+    na.dv = ws + L.dv;
     na.n_h = n_h;
     na.nf = c.nf;
     na.level = level;
@@ -802,6 +863,10 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
     int rc = c.score_width == 32 ? launch_node_hc<32>(na, s) : launch_node_hc<64>(na, s);
     if (rc) return rc;
     P.stop(Prof::NODE_HC);
+    if (!last) {  // k_hc_div + k_hc_post
+      P.count_launch();
+      P.count_launch();
+    }
     if (!last && c.policy == 1) {
       k_node_stop<<<1, 32, 0, s>>>(hc, n_h, K, op_id(level, SITE_STOP), ws + L.stop);
       GT_LAUNCH_CHECK("k_node_stop");
