@@ -138,4 +138,54 @@ __device__ __forceinline__ A3 division_warp(const Keys& K, uint32_t op, uint32_t
   return out;
 }
 
+// select_share on one lane from blocks: b2a dealer (sub, 0..1), reshare
+// pair_i (sub + 1, 0) (gadgets.py:238-253 with field 0).
+__device__ __forceinline__ void select_block_id(int j, uint32_t sub, int* key, uint32_t* s, uint32_t* pidx) {
+  if (j < 2) {
+    *key = -1, *s = sub, *pidx = j;
+  } else {
+    *key = j - 2, *s = sub + 1, *pidx = 0;
+  }
+}
+
+template <int L>
+__device__ __forceinline__ A3 select_arith(const W2* b, const A3& w1, const A3& w2, const B3& cond) {
+  const A3 ca = b2a_arith<L>(cond, b[0].a, b[0].b, b[1].a);
+  const uint64_t F[3] = {b[2].a, b[3].a, b[4].a};
+  return add<L>(w1, mul_z<L>(diff<L>(w2, w1), ca, F));
+}
+
+// One argmin tournament pair (gadgets.py:389-391) by one warp: the lt at
+// `base`, the value select at base+1 and the index select (Z_2^64) at base+3
+// draw ARGMIN_PAIR_BLOCKS<L> Philox blocks cooperatively into `tape`.
+template <int L>
+struct ArgminPair {
+  static constexpr int BLOCKS = LtRand<L>::BLOCKS + 10;
+};
+
+template <int L>
+__device__ __forceinline__ void argmin_pair_warp(const Keys& K, uint32_t op, uint32_t base, uint64_t lane, const A3& av,
+                                                 const A3& bv, const A3& ai, const A3& bi, W2* tape, A3* nv, A3* ni) {
+  const int wl = threadIdx.x & 31;
+  constexpr int LB = LtRand<L>::BLOCKS;
+  for (int j = wl; j < ArgminPair<L>::BLOCKS; j += 32) {
+    int key;
+    uint32_t s, pidx;
+    if (j < LB) {
+      lt_block_id<L>(j, base, &key, &pidx);
+      s = base;
+    } else if (j < LB + 5) {
+      select_block_id(j - LB, base + 1, &key, &s, &pidx);
+    } else {
+      select_block_id(j - LB - 5, base + 3, &key, &s, &pidx);
+    }
+    tape[j] = word2(key < 0 ? K.dealer : K.pair[key], op, s, pidx, lane);
+  }
+  __syncwarp();
+  const B3 cw = lt_arith<L>(tape, bv, av);  // challenger wins iff b < a
+  *nv = select_arith<L>(tape + LB, av, bv, cw);
+  *ni = select_arith<64>(tape + LB + 5, ai, bi, cw);
+  __syncwarp();
+}
+
 }  // namespace gt

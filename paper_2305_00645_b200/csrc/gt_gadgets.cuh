@@ -293,38 +293,87 @@ __device__ __forceinline__ B3 masked_diff_bits(const Keys& K, uint32_t op, uint3
 }
 
 // [x < y] unsigned (lt, gadgets.py:188-216); result in bit 0.
-// dealer fields: x-edabit 0..4, y-edabit 5..9; pair fields: x scan [0,12),
-// y scan [12,24), generate gate 24, final prefix [26,38).
+// Live fields: dealer x-edabit 0..4, y-edabit 5..9; pair x scan [0,12),
+// y scan [12,24), generate gate 24, final prefix [26,38).  As Philox blocks
+// in tape order (LtRand<L>::BLOCKS): dealer (sub, 0..3); x scan pair_i
+// (sub, l); y scan pair_i (sub, 6 + l); generate pair_i (sub, 12); prefix
+// pair_i (sub, 13 + l) -- i = 0..2, l = 0..nlev-1.
 template <int L>
-__device__ __forceinline__ B3 lt(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const A3& x, const A3& y) {
+struct LtRand {
+  static constexpr int NL = Levels<L>::n;
+  static constexpr int BLOCKS = 4 + 9 * NL + 3;
+};
+
+template <int L>
+__device__ __forceinline__ void lt_block_id(int j, uint32_t sub, int* key, uint32_t* pidx) {
+  constexpr int NL = Levels<L>::n;
+  if (j < 4) {
+    *key = -1, *pidx = j;
+    return;
+  }
+  j -= 4;
+  if (j < 3 * NL) {
+    *key = j / NL, *pidx = j % NL;
+  } else if (j < 6 * NL) {
+    j -= 3 * NL;
+    *key = j / NL, *pidx = 6 + j % NL;
+  } else if (j < 6 * NL + 3) {
+    *key = j - 6 * NL, *pidx = 12;
+  } else {
+    j -= 6 * NL + 3;
+    *key = j / NL, *pidx = 13 + j % NL;
+  }
+}
+
+template <int L>
+__device__ __forceinline__ B3 lt_arith(const W2* b, const A3& x, const A3& y) {
   constexpr uint64_t M = Ring<L>::M;
+  constexpr int NL = Levels<L>::n;
   B3 xb, yb;
   {
-    const uint64_t r = word(K.dealer, op, sub, 0, lane) & M;
+    const uint64_t r = b[0].a & M;  // fields 0 (r), 1 (Rb0), 2 (Rb1)
     B3 Rb;
-    Rb.v[0] = word(K.dealer, op, sub, 1, lane) & M;
-    Rb.v[1] = word(K.dealer, op, sub, 2, lane) & M;
+    Rb.v[0] = b[0].b & M;
+    Rb.v[1] = b[1].a & M;
     Rb.v[2] = r ^ Rb.v[0] ^ Rb.v[1];
-    const uint64_t R0 = word(K.dealer, op, sub, 3, lane) & M, R1 = word(K.dealer, op, sub, 4, lane) & M;
-    const uint64_t c = open<L>(a3(x.v[0] + R0, x.v[1] + R1, x.v[2] + (r - R0 - R1)));
-    xb = masked_diff_bits<L>(K, op, sub, 0, lane, c, Rb);
+    const uint64_t c = (open<L>(x) + r) & M;
+    const B3 sc = borrow_scan_blk<L>(c, Rb, b + 4);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) xb.v[i] = Rb.v[i] ^ ((sc.v[i] << 1) & M);
+    xb.v[0] ^= c;  // _masked_diff_bits, gadgets.py:174-185
   }
   {
-    const uint64_t r = word(K.dealer, op, sub, 5, lane) & M;
+    const uint64_t r = b[2].b & M;  // fields 5 (r), 6 (Rb0), 7 (Rb1)
     B3 Rb;
-    Rb.v[0] = word(K.dealer, op, sub, 6, lane) & M;
-    Rb.v[1] = word(K.dealer, op, sub, 7, lane) & M;
+    Rb.v[0] = b[3].a & M;
+    Rb.v[1] = b[3].b & M;
     Rb.v[2] = r ^ Rb.v[0] ^ Rb.v[1];
-    const uint64_t R0 = word(K.dealer, op, sub, 8, lane) & M, R1 = word(K.dealer, op, sub, 9, lane) & M;
-    const uint64_t c = open<L>(a3(y.v[0] + R0, y.v[1] + R1, y.v[2] + (r - R0 - R1)));
-    yb = masked_diff_bits<L>(K, op, sub, 12, lane, c, Rb);
+    const uint64_t c = (open<L>(y) + r) & M;
+    const B3 sc = borrow_scan_blk<L>(c, Rb, b + 4 + 3 * NL);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) yb.v[i] = Rb.v[i] ^ ((sc.v[i] << 1) & M);
+    yb.v[0] ^= c;
   }
-  const B3 g = and_gate(K, op, sub, 24, lane, yb, bnot(xb, M), M);
+  const uint64_t Zg[3] = {b[4 + 6 * NL].a & M, b[5 + 6 * NL].a & M, b[6 + 6 * NL].a & M};
+  const B3 g = and_z(yb, bnot(xb, M), Zg);
   const B3 p = bnot(bxor(xb, yb), M);
-  B3 rows = prefix_borrow<L>(K, op, sub, 26, lane, g, p);
+  B3 rows = prefix_borrow_blk<L>(g, p, b + 7 + 6 * NL);
 #pragma unroll
   for (int i = 0; i < 3; ++i) rows.v[i] = (rows.v[i] >> (L - 1)) & 1ull;
   return rows;
+}
+
+template <int L>
+__device__ __forceinline__ B3 lt(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const A3& x, const A3& y) {
+  W2 b[LtRand<L>::BLOCKS];
+#pragma unroll
+  for (int j = 0; j < LtRand<L>::BLOCKS; ++j) {
+    int key;
+    uint32_t pidx;
+    lt_block_id<L>(j, sub, &key, &pidx);
+    b[j] = word2(key < 0 ? K.dealer : K.pair[key], op, sub, pidx, lane);
+  }
+  return lt_arith<L>(b, x, y);
 }
 
 // Boolean bit -> arithmetic share (b2a, gadgets.py:223-231) from a dabit:

@@ -121,11 +121,30 @@ struct CountArgs {
   uint32_t op_leaf, op_cnt;
 };
 
+// sample column w of sample sg: [x | x*y | y]  (sample_cols, train.py:231-233)
+__device__ __forceinline__ void col3(const CountArgs& a, uint64_t sg, int w, int nf, uint64_t nfx, uint64_t& x0,
+                                     uint64_t& x1, uint64_t& x2) {
+  const uint64_t* base;
+  uint64_t stride, off;
+  if (w < nf) {
+    base = a.X, stride = nfx, off = sg * nf + w;
+  } else if (w < 2 * nf) {
+    base = a.P, stride = nfx, off = sg * nf + (w - nf);
+  } else {
+    base = a.Y, stride = a.N, off = sg;
+  }
+  x0 = __ldg(base + off);
+  x1 = __ldg(base + stride + off);
+  x2 = __ldg(base + 2 * stride + off);
+}
+
 // One CTA = (sample chunk, node block).  Per tile of TS samples:
 //  phase A, one lane per (sample, node):  la = b2a(eq(m_idx, off+n) & leaf[n])
 //    drawing the six Philox blocks of LaneRand at sub 0 (pair block half b
 //    = the AND gate's zero bit);
-//  phase B, one work item per (node, column pair): the W products
+//  phase B, one work item per (node, column pair): the W products (sample
+//    columns read straight from global/L1: every item of the tile reads the
+//    same rows)
 //    mul(cols[s][w], la[s][n]) with their reshare (sub 3, field w), summed
 //    over the samples in registers; the mask column (w = W) adds la itself.
 // Every thread owns one item (replicas split the samples of a tile when there
@@ -137,8 +156,7 @@ __global__ void __launch_bounds__(CNT_TPB, CNT_MINB) k_count(CountArgs a) {
   const int tid = threadIdx.x, bd = blockDim.x;
   const int n0 = blockIdx.y * NB;
   const int nb = min(NB, a.n_h - n0);
-  uint64_t* cols = sm;                  // [3][TS][W]
-  uint64_t* la = cols + 3 * TS * W;     // [3][TS][NB]
+  uint64_t* la = sm;                    // [3][TS][NB]
   uint64_t* leaf = la + 3 * TS * NB;    // [3][NB]
   const Keys& K = a.K;
   const uint64_t nfx = a.N * (uint64_t)nf;
@@ -167,18 +185,6 @@ __global__ void __launch_bounds__(CNT_TPB, CNT_MINB) k_count(CountArgs a) {
     if (s0 >= a.N) break;
     const int cnt = (int)min((uint64_t)TS, a.N - s0);
     __syncthreads();
-    for (int e = tid; e < cnt * W; e += bd) {
-      const int s = e / W, w = e % W;
-      const uint64_t sg = s0 + s;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        uint64_t v;
-        if (w < nf) v = a.X[c * nfx + sg * nf + w];
-        else if (w < 2 * nf) v = a.P[c * nfx + sg * nf + (w - nf)];
-        else v = a.Y[c * a.N + sg];
-        cols[(c * TS + s) * W + w] = v;
-      }
-    }
     // phase A                                             train.py:328-331
     for (int e = tid; e < cnt * nb; e += bd) {
       const int s = e / nb, nn = e % nb;
@@ -208,9 +214,10 @@ __global__ void __launch_bounds__(CNT_TPB, CNT_MINB) k_count(CountArgs a) {
         const W2 F0 = word2(K.pair[0], a.op_cnt, 3, wp, lane);
         const W2 F1 = word2(K.pair[1], a.op_cnt, 3, wp, lane);
         const W2 F2 = word2(K.pair[2], a.op_cnt, 3, wp, lane);
+        const uint64_t sg = s0 + s;
         {
-          const uint64_t x0 = cols[(0 * TS + s) * W + w0], x1 = cols[(1 * TS + s) * W + w0],
-                         x2 = cols[(2 * TS + s) * W + w0];
+          uint64_t x0, x1, x2;
+          col3(a, sg, w0, nf, nfx, x0, x1, x2);
           // z_i = l_i (x_i + x_{i+1}) + x_i l_{i+1}   (rss.py:391-395, mul_z)
           acc[0][0] += l0 * (x0 + x1) + x0 * l1;
           acc[0][1] += l1 * (x1 + x2) + x1 * l2;
@@ -220,8 +227,8 @@ __global__ void __launch_bounds__(CNT_TPB, CNT_MINB) k_count(CountArgs a) {
           zacc[0][2] += F2.a;
         }
         if (!mask_col) {
-          const uint64_t x0 = cols[(0 * TS + s) * W + w1], x1 = cols[(1 * TS + s) * W + w1],
-                         x2 = cols[(2 * TS + s) * W + w1];
+          uint64_t x0, x1, x2;
+          col3(a, sg, w1, nf, nfx, x0, x1, x2);
           acc[1][0] += l0 * (x0 + x1) + x0 * l1;
           acc[1][1] += l1 * (x1 + x2) + x1 * l2;
           acc[1][2] += l2 * (x2 + x0) + x2 * l0;
@@ -441,22 +448,24 @@ __global__ void __launch_bounds__(256) k_hc_post(NodeArgs a) {
   if (tid < 3) hitw[tid] = 0;
   __syncthreads();
   int m = nf;
+  const int warp = tid >> 5, nwarps = bd >> 5;
+  W2* tape = reinterpret_cast<W2*>(hitw + 4) + warp * ArgminPair<SL>::BLOCKS;
   for (int r = 0; m > 1; ++r) {
     const int pairs = m / 2;
     const uint32_t base = SA + 2 + 5 * r;
-    for (int p = tid; p < pairs; p += bd) {
+    for (int p = warp; p < pairs; p += nwarps) {  // one warp per tournament pair
       const uint64_t lane = (uint64_t)n * nf + p;
       const A3 av = a3(vals[2 * p], vals[nf + 2 * p], vals[2 * nf + 2 * p]);
       const A3 bv = a3(vals[2 * p + 1], vals[nf + 2 * p + 1], vals[2 * nf + 2 * p + 1]);
       const A3 ai = a3(idxs[2 * p], idxs[nf + 2 * p], idxs[2 * nf + 2 * p]);
       const A3 bi = a3(idxs[2 * p + 1], idxs[nf + 2 * p + 1], idxs[2 * nf + 2 * p + 1]);
-      const B3 cw = lt<SL>(K, opH, base, lane, bv, av);
-      const A3 nv = select1<SL>(K, opH, base + 1, lane, av, bv, cw);
-      const A3 ni = select1<64>(K, opH, base + 3, lane, ai, bi, cw);
-      for (int c = 0; c < 3; ++c) {
-        nvals[c * nf + p] = nv.v[c];
-        nidxs[c * nf + p] = ni.v[c];
-      }
+      A3 nv, ni;
+      argmin_pair_warp<SL>(K, opH, base, lane, av, bv, ai, bi, tape, &nv, &ni);
+      if ((tid & 31) == 0)
+        for (int c = 0; c < 3; ++c) {
+          nvals[c * nf + p] = nv.v[c];
+          nidxs[c * nf + p] = ni.v[c];
+        }
     }
     if (tid == 0 && (m & 1))
       for (int c = 0; c < 3; ++c) {
@@ -612,7 +621,7 @@ int launch_node_hc(const NodeArgs& na, cudaStream_t s) {
     GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_div<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, div_smem));
   k_hc_div<SL><<<(unsigned)((lanes + DIV_WARPS - 1) / DIV_WARPS), 32 * DIV_WARPS, div_smem, s>>>(na);
   GT_LAUNCH_CHECK("k_hc_div");
-  const int post_smem = (int)sizeof(uint64_t) * (12 * na.nf + 4);
+  const int post_smem = (int)sizeof(uint64_t) * (12 * na.nf + 4) + (int)sizeof(W2) * 8 * ArgminPair<SL>::BLOCKS;
   k_hc_post<SL><<<na.n_h, 256, post_smem, s>>>(na);
   GT_LAUNCH_CHECK("k_hc_post");
   return GT_OK;
@@ -713,14 +722,14 @@ int choose_node_block(int n_h, int WP) {
 int launch_count(CountArgs ca, cudaStream_t s, int num_sms) {
   const int nf = ca.nf, W = 2 * nf + 1, WP = nf + 1;
   ca.nb = choose_node_block(ca.n_h, WP);
-  ca.ts = 32;
+  ca.ts = std::max(32, std::min(256, ((CNT_TPB + ca.nb - 1) / ca.nb + 31) / 32 * 32));  // >= 256 phase-A lanes
   const unsigned gy = (unsigned)((ca.n_h + ca.nb - 1) / ca.nb);
   const uint64_t tiles = (ca.N + ca.ts - 1) / ca.ts;
   const uint64_t target = std::max<uint64_t>(1, (uint64_t)num_sms * CNT_MINB * 4 / gy);
   const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>(tiles, target));
   ca.tiles_per_cta = (int)((tiles + gx - 1) / gx);
   const unsigned gxx = (unsigned)((tiles + ca.tiles_per_cta - 1) / ca.tiles_per_cta);
-  const int smem = (int)sizeof(uint64_t) * (3 * ca.ts * W + 3 * ca.ts * ca.nb + 3 * ca.nb);
+  const int smem = (int)sizeof(uint64_t) * (3 * ca.ts * ca.nb + 3 * ca.nb);
   if (smem > 48 * 1024) GT_CUDA_CHECK(cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   k_count<<<dim3(gxx, gy), CNT_TPB, smem, s>>>(ca);
   GT_LAUNCH_CHECK("k_count");
