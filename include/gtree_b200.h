@@ -140,6 +140,14 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
 int gt_infer(int depth, const uint64_t* tree, const uint64_t* queries, uint64_t n, uint64_t nf,
              uint64_t instance_base, uint64_t* out, uint64_t* slot_out, const gt_keys* keys, void* stream);
 
+/* ---- diagnostics ---- */
+
+/* Peak counter-based PRG rate: `grid` x 256 threads each draw `iters`
+ * Philox4x32-10 blocks (distinct counters) and fold them into out[grid*256].
+ * The caller times it; blocks/s is the integer-ALU roof of the share kernels,
+ * whose correlated randomness is drawn the same way. */
+int gt_diag_philox(uint32_t grid, uint32_t iters, uint64_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -187,6 +187,20 @@ __global__ void k_row_lookup(const uint64_t* rows, uint64_t m, const uint64_t* i
 
 bool width_ok(int w) { return w == 8 || w == 32 || w == 64; }
 
+__global__ void __launch_bounds__(256) k_diag_philox(uint32_t iters, uint64_t* out, Keys K) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t acc = 0;
+  for (uint32_t i = 0; i < iters; i += 4) {
+    // four independent blocks per step, like three pair keys + a dealer key
+    const W2 a = word2(K.pair[0], i, 1, 0, t);
+    const W2 b = word2(K.pair[1], i, 1, 0, t);
+    const W2 c = word2(K.pair[2], i, 1, 0, t);
+    const W2 d = word2(K.dealer, i, 1, 0, t);
+    acc += a.a ^ b.b ^ c.a ^ d.b ^ a.b ^ b.a ^ c.b ^ d.a;
+  }
+  out[t] = acc;
+}
+
 }  // namespace
 }  // namespace gt
 
@@ -334,6 +348,16 @@ int gt_row_lookup(int width, const uint64_t* rows, uint64_t m, const uint64_t* i
   if (!idx || !out || (m && !rows)) return fail_inval("gt_row_lookup: NULL operand");
   GT_DISPATCH(width, k_row_lookup, blocks_for(n), rows, m, idx, out, n, to_keys(keys), op);
   GT_LAUNCH_CHECK("gt_row_lookup");
+  return GT_OK;
+}
+
+int gt_diag_philox(uint32_t grid, uint32_t iters, uint64_t* out, void* stream) {
+  if (!out || grid == 0) return fail_inval("gt_diag_philox: bad arguments");
+  gt_keys k{};
+  k.dealer.k0 = 1;
+  for (int i = 0; i < 3; ++i) k.pair[i].k0 = 2 + i;
+  k_diag_philox<<<grid, 256, 0, (cudaStream_t)stream>>>(iters, out, to_keys(&k));
+  GT_LAUNCH_CHECK("gt_diag_philox");
   return GT_OK;
 }
 

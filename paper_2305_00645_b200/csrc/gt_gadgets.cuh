@@ -187,6 +187,52 @@ __device__ __forceinline__ B3 eq_arith(const A3& d, uint64_t r, uint64_t Rb0, ui
   return and_reduce_w(P, L, Zw);
 }
 
+// One 32-bit AND gate with reshare: z_i = (a_i & b_i) ^ (a_{i+1} & b_i) ^
+// (a_i & b_{i+1}) ^ Z_i ^ Z_{i-1} = (b_i & (a_i ^ a_{i+1})) ^ (a_i & b_{i+1}) ^ ...
+__device__ __forceinline__ void and3_32(const uint32_t a[3], const uint32_t b[3], const uint32_t z[3], uint32_t o[3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int j = (i + 1) % 3, p = (i + 2) % 3;
+    o[i] = (b[i] & (a[i] ^ a[j])) ^ (a[i] & b[j]) ^ z[i] ^ z[p];
+  }
+}
+
+// eq at l = 64 with the AND tree on 32-bit halves: after the first level
+// (plane j & plane j+32 = low word & high word) every level fits 32 bits.
+// Same zero-bit layout as and_reduce_w: level bits at offsets 0, 32, 48, 56,
+// 60, 62 of the pair words.
+template <>
+__device__ __forceinline__ B3 eq_arith<64>(const A3& d, uint64_t r, uint64_t Rb0, uint64_t Rb1, const uint64_t Zw[3]) {
+  const uint64_t c = open<64>(d) + r;
+  const uint64_t P[3] = {Rb0 ^ ~c, Rb1, r ^ Rb0 ^ Rb1};
+  uint32_t a[3], b[3], z[3], w[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    a[i] = (uint32_t)P[i];
+    b[i] = (uint32_t)(P[i] >> 32);
+    z[i] = (uint32_t)Zw[i];
+  }
+  and3_32(a, b, z, w);
+  uint32_t zh[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) zh[i] = (uint32_t)(Zw[i] >> 32);
+#pragma unroll
+  for (int lvl = 1, half = 16, off = 0; lvl < 6; ++lvl, off += half, half >>= 1) {
+    const uint32_t lm = (1u << half) - 1u;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      a[i] = w[i] & lm;
+      b[i] = w[i] >> half;
+      z[i] = (zh[i] >> off) & lm;
+    }
+    and3_32(a, b, z, w);
+  }
+  B3 out;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) out.v[i] = w[i] & 1u;
+  return out;
+}
+
 // standalone eq: dealer fields r=0 Rb0=1 Rb1=2; pair field 0 = AND-tree bits.
 template <int L>
 __device__ __forceinline__ B3 eqz(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const A3& d) {

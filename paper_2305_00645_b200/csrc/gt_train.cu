@@ -121,23 +121,6 @@ struct CountArgs {
   uint32_t op_leaf, op_cnt;
 };
 
-// sample column w of sample sg: [x | x*y | y]  (sample_cols, train.py:231-233)
-__device__ __forceinline__ void col3(const CountArgs& a, uint64_t sg, int w, int nf, uint64_t nfx, uint64_t& x0,
-                                     uint64_t& x1, uint64_t& x2) {
-  const uint64_t* base;
-  uint64_t stride, off;
-  if (w < nf) {
-    base = a.X, stride = nfx, off = sg * nf + w;
-  } else if (w < 2 * nf) {
-    base = a.P, stride = nfx, off = sg * nf + (w - nf);
-  } else {
-    base = a.Y, stride = a.N, off = sg;
-  }
-  x0 = __ldg(base + off);
-  x1 = __ldg(base + stride + off);
-  x2 = __ldg(base + 2 * stride + off);
-}
-
 // One CTA = (sample chunk, node block).  Per tile of TS samples:
 //  phase A, one lane per (sample, node):  la = b2a(eq(m_idx, off+n) & leaf[n])
 //    drawing the six Philox blocks of LaneRand at sub 0 (pair block half b
@@ -174,6 +157,20 @@ __global__ void __launch_bounds__(CNT_TPB, CNT_MINB) k_count(CountArgs a) {
   const int n = item / WP, wp = item % WP;
   const int w0 = 2 * wp, w1 = 2 * wp + 1;
   const bool mask_col = w1 >= W;
+  // column w of sample s, component c: c_w[c * ccs_w + s * cst_w]  (sample_cols, train.py:231-233)
+  auto colptr = [&](int w, const uint64_t*& base, uint64_t& ccs, uint64_t& cst) {
+    if (w < nf) {
+      base = a.X + w, ccs = nfx, cst = (uint64_t)nf;
+    } else if (w < 2 * nf) {
+      base = a.P + (w - nf), ccs = nfx, cst = (uint64_t)nf;
+    } else {
+      base = a.Y, ccs = a.N, cst = 1;
+    }
+  };
+  const uint64_t *c0, *c1;
+  uint64_t ccs0, cst0, ccs1, cst1;
+  colptr(w0, c0, ccs0, cst0);
+  colptr(mask_col ? w0 : w1, c1, ccs1, cst1);
   // acc[h][c]: local cross terms of column w0 + h, component c;
   // zacc[h][i]: sum of key i's zero-share words (alpha_i = F_i - F_{i-1} is
   // applied once at the end: sum_s alpha_i = zacc[i] - zacc[i-1]).
@@ -209,15 +206,17 @@ __global__ void __launch_bounds__(CNT_TPB, CNT_MINB) k_count(CountArgs a) {
     if (active) {
       uint64_t lane = (a.base + s0 + q) * (uint64_t)a.n_h + (uint64_t)(n0 + n);
       const uint64_t lstep = (uint64_t)R * a.n_h;
-      for (int s = q; s < cnt; s += R, lane += lstep) {
-        const uint64_t l0 = la[(0 * TS + s) * NB + n], l1 = la[(1 * TS + s) * NB + n], l2 = la[(2 * TS + s) * NB + n];
+      const uint64_t* p0 = c0 + (s0 + q) * cst0;
+      const uint64_t* p1 = c1 + (s0 + q) * cst1;
+      const uint64_t* lp = la + (uint64_t)q * NB + n;
+      const uint64_t pst0 = (uint64_t)R * cst0, pst1 = (uint64_t)R * cst1, lpst = (uint64_t)R * NB;
+      for (int s = q; s < cnt; s += R, lane += lstep, p0 += pst0, p1 += pst1, lp += lpst) {
+        const uint64_t l0 = lp[0], l1 = lp[(uint64_t)TS * NB], l2 = lp[2ull * TS * NB];
         const W2 F0 = word2(K.pair[0], a.op_cnt, 3, wp, lane);
         const W2 F1 = word2(K.pair[1], a.op_cnt, 3, wp, lane);
         const W2 F2 = word2(K.pair[2], a.op_cnt, 3, wp, lane);
-        const uint64_t sg = s0 + s;
         {
-          uint64_t x0, x1, x2;
-          col3(a, sg, w0, nf, nfx, x0, x1, x2);
+          const uint64_t x0 = __ldg(p0), x1 = __ldg(p0 + ccs0), x2 = __ldg(p0 + 2 * ccs0);
           // z_i = l_i (x_i + x_{i+1}) + x_i l_{i+1}   (rss.py:391-395, mul_z)
           acc[0][0] += l0 * (x0 + x1) + x0 * l1;
           acc[0][1] += l1 * (x1 + x2) + x1 * l2;
@@ -227,8 +226,7 @@ __global__ void __launch_bounds__(CNT_TPB, CNT_MINB) k_count(CountArgs a) {
           zacc[0][2] += F2.a;
         }
         if (!mask_col) {
-          uint64_t x0, x1, x2;
-          col3(a, sg, w1, nf, nfx, x0, x1, x2);
+          const uint64_t x0 = __ldg(p1), x1 = __ldg(p1 + ccs1), x2 = __ldg(p1 + 2 * ccs1);
           acc[1][0] += l0 * (x0 + x1) + x0 * l1;
           acc[1][1] += l1 * (x1 + x2) + x1 * l2;
           acc[1][2] += l2 * (x2 + x0) + x2 * l0;

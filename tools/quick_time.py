@@ -34,3 +34,14 @@ for depth, nf, n in ((7, 13, 10_000), (10, 32, 1_000_000)):
     T = to_device(share(rng.integers(0, nf, (1 << depth) - 1), rng)); Q = to_device(share(rng.integers(0, 2, (n, nf)), rng))
     ms = timed(lambda: infer_device(T, depth, Q, keys))
     print(f"infer depth {depth} nf {nf} n {n} ms:", ms, "inst/s:", n / ms[0] * 1e3, flush=True)
+
+# Philox block throughput (integer-ALU roof of the share kernels)
+from paper_2305_00645_b200 import _native
+lib = _native.load()
+import ctypes
+grid, iters = 148 * 8 * 4, 4096
+out = torch.empty(grid * 256, dtype=torch.int64, device="cuda")
+def run():
+    _native.check(lib.gt_diag_philox(grid, iters, out.data_ptr(), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+ms = timed(run)
+print("philox blocks/s:", grid * 256 * iters / (ms[0] / 1e3), flush=True)
