@@ -193,6 +193,105 @@ def reference_arm(args, rank, world):
 # this framework
 # ---------------------------------------------------------------------------
 
+def _dev_share(values_u8, dev, gen):
+    """Component-major shares [3, ...] of public values, drawn on the device."""
+    import torch
+
+    v = torch.as_tensor(values_u8, device=dev).to(torch.int64)
+    s1 = torch.randint(-(2 ** 63), 2 ** 63 - 1, v.shape, dtype=torch.int64, device=dev, generator=gen)
+    s2 = torch.randint(-(2 ** 63), 2 ** 63 - 1, v.shape, dtype=torch.int64, device=dev, generator=gen)
+    return torch.stack([s1, s2, v - s1 - s2]).contiguous()
+
+
+def _events_time(fn, steps, warmup, flush, barrier, stream, max_over_ranks):
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(steps):
+        flush.zero_()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms.append(e0.elapsed_time(e1))
+    return max_over_ranks(sum(ms)) / steps / 1e3
+
+
+def scale_c4(ctx, steps, warmup):
+    """C4: 10^6 x 32 + label, depth 8, mpc; samples sharded, count allreduce."""
+    import torch
+
+    from oracle import shadow  # revealed-tree checker only
+    from paper_2305_00645_b200 import TrainConfig
+    from paper_2305_00645_b200.dist import make_allreduce, shard_range
+    from paper_2305_00645_b200.seeds import SeedSetup, derive_seed, filler_values, make_keys
+    from paper_2305_00645_b200.shares import from_device
+    from paper_2305_00645_b200.train import DeviceTrainer
+
+    dev, world, rank = ctx["dev"], ctx["world"], ctx["rank"]
+    n, nf, depth = 10 ** 6, 32, 8
+    data = np.random.default_rng(10 ** 6).integers(0, 2, (n, nf + 1), dtype=np.uint8)
+    seed = (40_000).to_bytes(16, "little")
+    setup = SeedSetup.from_master(derive_seed(seed, "run"))
+    keys = make_keys(setup, derive_seed(seed, "deal"))
+    fill = filler_values(setup.filler_seed, (1 << depth) - 1, nf + 1)
+    start, cnt = shard_range(n, world, rank)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    X = _dev_share(data[start:start + cnt, :-1], dev, gen)
+    Y = _dev_share(data[start:start + cnt, -1], dev, gen)
+    FL = torch.from_numpy(fill.view(np.int64)).to(dev)
+    tr = DeviceTrainer(cnt, nf, TrainConfig(depth=depth), n_total=n, sample_base=start, device=dev)
+    cb = make_allreduce(tr) if world > 1 else None
+    fn = (lambda: tr.run(X, Y, FL, keys, allreduce=cb))
+    if world == 1:
+        fn = tr.capture(X, Y, FL, keys)
+    t = _events_time(fn, steps, warmup, ctx["flush"], ctx["barrier"], ctx["stream"], ctx["max"])
+    T, F = from_device(tr.T).sum(axis=0), from_device(tr.F).sum(axis=0)
+    want_T, want_F = shadow.mpc_train(data, depth, fill)
+    return {"metric": "secure train s/tree (10^6 x 32, depth 8)", "value": t, "unit": "s/tree",
+            "scaling": "strong", "config": "C4: default_rng(10**6) 10^6 x 33 binary, depth 8, mpc; samples sharded",
+            "parity_tree_equals_shadow_oracle": bool(np.array_equal(T, want_T) and np.array_equal(F, want_F))}
+
+
+def scale_c5(ctx, steps, warmup):
+    """C5: 10^7 queries x 32 features on a 10-level tree; instance-sharded."""
+    import torch
+
+    from oracle import shadow  # prediction checker only
+    from paper_2305_00645_b200.dist import shard_range
+    from paper_2305_00645_b200.infer import infer_device
+    from paper_2305_00645_b200.shares import from_device
+
+    dev, world, rank = ctx["dev"], ctx["world"], ctx["rank"]
+    n, nf, depth = 10 ** 7, 32, 10
+    rng = np.random.default_rng(10)
+    Tv, _ = shadow.random_tree(rng, depth, nf + 1)
+    start, cnt = shard_range(n, world, rank)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(77 + rank)
+    qbits = torch.randint(0, 2, (cnt, nf), dtype=torch.uint8, device=dev, generator=gen)
+    Q = _dev_share(qbits, dev, gen)
+    T = _dev_share(torch.from_numpy(Tv.view(np.int64)).to(dev), dev, gen)
+    out = torch.empty((3, cnt), dtype=torch.int64, device=dev)
+    t = _events_time(lambda: infer_device(T, depth, Q, ctx["keys"], instance_base=start, out=out), steps, warmup,
+                     ctx["flush"], ctx["barrier"], ctx["stream"], ctx["max"])
+    sub = min(cnt, 200_000)
+    got = from_device(out[:, :sub]).sum(axis=0)
+    want = shadow.plaintext_infer(Tv, depth, qbits[:sub].cpu().numpy())
+    return {"metric": "secure inference instances/s (10^7 x 32, 10 levels)", "value": n / t, "unit": "instances/s",
+            "ms_per_step": t * 1e3, "scaling": "strong",
+            "config": "C5: random_tree(default_rng(10), 10, 33), 10^7 random queries; instances sharded",
+            "parity_predictions_equal_plaintext_first_2e5": bool(np.array_equal(got, want))}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -200,9 +299,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-scale", action="store_true", help="skip the C4/C5 10^6-scale secondaries")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return reference_arm(args, rank, world)
@@ -246,18 +346,18 @@ def main():
     cb = make_allreduce(tr) if world > 1 else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
+    ctx = {"dev": dev, "world": world, "rank": rank, "flush": flush, "barrier": barrier, "stream": stream,
+           "max": max_over_ranks, "keys": keys}
 
     def step(profile=None):
         return tr.run(X, Y, FL, keys, allreduce=cb, profile=profile)
 
+    # ---- device-resident timed region (value): CUDA-graph replay of whole trees ----
+    replay = tr.capture(X, Y, FL, keys) if world == 1 else None
+    run_tree = replay if replay is not None else step
     for _ in range(args.warmup):
-        step()
+        run_tree()
     torch.cuda.synchronize()
-
-    # ---- device-resident timed region (value) ----
-    prof_tot = {k: 0.0 for k in ("prods", "partition", "count", "node_hc", "node_finish")}
-    prof_n = {k: 0 for k in prof_tot}
-    launches = 0
     step_ms = []
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
@@ -265,20 +365,30 @@ def main():
             barrier()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            p = _native.gt_train_profile()
             e0.record(stream)
-            step(p)
+            run_tree()
             e1.record(stream)
             torch.cuda.synchronize()
             barrier()
             step_ms.append(e0.elapsed_time(e1))
-            launches += p.launches
-            for k in prof_tot:
-                prof_tot[k] += getattr(p, f"ms_{k}")
-                prof_n[k] += getattr(p, f"n_{k}")
-    total_ms = max_over_ranks(sum(step_ms))
-    value_s = total_ms / args.steps / 1e3
+    value_s = max_over_ranks(sum(step_ms)) / args.steps / 1e3
     clocks = clk.summary()
+
+    # ---- per-kernel CUDA-event durations: a second pass of K profiled steps ----
+    prof_tot = {k: 0.0 for k in ("prods", "partition", "count", "node_hc", "node_finish")}
+    prof_n = {k: 0 for k in prof_tot}
+    launches = 0
+    for _ in range(args.steps):
+        flush.zero_()
+        barrier()
+        torch.cuda.synchronize()
+        p = _native.gt_train_profile()
+        step(p)
+        barrier()
+        launches += p.launches
+        for k in prof_tot:
+            prof_tot[k] += getattr(p, f"ms_{k}")
+            prof_n[k] += getattr(p, f"n_{k}")
 
     # parity of what was timed: revealed tree == the reference's C2 tree
     z = np.load(os.path.join(ROOT, "tests", "golden", "c2c3.npz"))
@@ -318,33 +428,24 @@ def main():
     Tt = torch.from_numpy(np.ascontiguousarray(Tc).view(np.int64)).to(dev)
     Q = Qp.to(dev)
     out = torch.empty((3, qc), dtype=torch.int64, device=dev)
-    for _ in range(args.warmup):
-        infer_device(Tt, DEPTH_C2, Q, keys, instance_base=qs, out=out)
-    inf_ms, inf_e2e = [], []
+    inf_s = _events_time(lambda: infer_device(Tt, DEPTH_C2, Q, keys, instance_base=qs, out=out), args.steps,
+                         args.warmup, flush, barrier, stream, max_over_ranks)
     Oh = torch.empty((3, qc), dtype=torch.int64).pin_memory()
-    for _ in range(args.steps):
-        flush.zero_()
-        barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        infer_device(Tt, DEPTH_C2, Q, keys, instance_base=qs, out=out)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        inf_ms.append(e0.elapsed_time(e1))
-        e0.record(stream)
+
+    def inf_e2e():
         Q.copy_(Qp, non_blocking=True)
         infer_device(Tt, DEPTH_C2, Q, keys, instance_base=qs, out=out)
         Oh.copy_(out, non_blocking=True)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        inf_e2e.append(e0.elapsed_time(e1))
-        barrier()
-    inf_s = max_over_ranks(sum(inf_ms)) / args.steps / 1e3
-    inf_e2e_s = max_over_ranks(sum(inf_e2e)) / args.steps / 1e3
+
+    inf_e2e_s = _events_time(inf_e2e, args.steps, args.warmup, flush, barrier, stream, max_over_ranks)
     preds_ok = True
     if world == 1:
         preds_ok = bool(np.array_equal(from_device(out).sum(axis=0), z["preds"]))
+
+    scale = {}
+    if not args.no_scale:
+        scale["c4_train"] = scale_c4(ctx, max(3, args.steps // 2), args.warmup)
+        scale["c5_infer"] = scale_c5(ctx, max(3, args.steps // 2), args.warmup)
 
     if rank != 0:
         if world > 1:
@@ -359,7 +460,16 @@ def main():
     alg = bytes_of[dom] * args.steps
     achieved = alg / (prof_tot[dom] / 1e3) / 1e9 if prof_tot[dom] > 0 else 0.0
     nlaunch = max(1, prof_n[dom])
-    traffic = _traffic({"count": "k_count", "partition": "k_partition", "node_hc": "k_node_hc"}.get(dom, dom))
+    traffic = _traffic({"count": "k_count", "partition": "k_partition", "node_hc": "k_hc_div"}.get(dom, dom))
+    # integer-ALU roof: Philox blocks the dominant kernel draws vs the measured Philox peak
+    W = 2 * NF_C2 + 1
+    blocks = {"count": sum(cnt * (1 << h) * (6 + 3 * (NF_C2 + 1)) for h in range(DEPTH_C2)),
+              "partition": sum(cnt * ((1 << (h - 1)) + NF_C2) * 6 for h in range(1, DEPTH_C2))}.get(dom)
+    alu = None
+    if blocks:
+        alu = {"bound": "int-alu (Philox4x32-10 blocks)", "achieved_blocks_per_s": blocks * args.steps / (prof_tot[dom] / 1e3),
+               "peak_blocks_per_s": _philox_peak(), "note": "peak measured by gt_diag_philox on this GPU"}
+        alu["frac"] = alu["achieved_blocks_per_s"] / alu["peak_blocks_per_s"] if alu["peak_blocks_per_s"] else None
     cpu_base = None
     if world == 1 and not args.no_cpu_baseline:
         import oracle
@@ -386,8 +496,10 @@ def main():
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": bytes_of[dom] / max(1, prof_n[dom] // args.steps),
-                     "avg_launch_ms": prof_tot[dom] / nlaunch},
+                     "avg_launch_ms": prof_tot[dom] / nlaunch, "alu": alu},
         "kernel_ms_per_step": {k: v / args.steps for k, v in prof_tot.items()},
+        "timing": ("value: CUDA-graph replay of the whole tree (1 GPU) / stream launches (N>1); "
+                   "kernel_ms_per_step + roofline: separate pass of K steps with per-launch CUDA events"),
         "clocks": clocks,
         "secondary": {"metric": METRIC2, "value": N_C3 / inf_s, "unit": "instances/s", "ms_per_step": inf_s * 1e3,
                       "config": "C3: 10^4 queries x 13 features on the C2 tree (7 levels)",
@@ -395,12 +507,39 @@ def main():
                               "h2d_bytes_per_step": int(Qp.numel() * 8), "d2h_bytes_per_step": int(Oh.numel() * 8)},
                       "roofline": {"bound": "hbm", "kernel": "k_walk", "achieved": walk_alg / inf_s / 1e9,
                                    "peak": peak, "unit": "GB/s", "frac": walk_alg / inf_s / 1e9 / peak}},
+        "scale": scale,
     }
     if cpu_base is not None:
         line["cpu_baseline"] = cpu_base
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _philox_peak():
+    import ctypes
+
+    import torch
+
+    from paper_2305_00645_b200 import _native
+
+    lib = _native.load()
+    grid, iters = 148 * 32, 4096
+    out = torch.empty(grid * 256, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream()
+    run = lambda: _native.check(lib.gt_diag_philox(grid, iters, out.data_ptr(), ctypes.c_void_p(s.cuda_stream)))  # noqa: E731
+    run()
+    torch.cuda.synchronize()
+    best = None
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        run()
+        e1.record(s)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    return grid * 256 * iters / (best / 1e3)
 
 
 if __name__ == "__main__":

@@ -46,12 +46,12 @@ def allreduce_u64_(t, group=None) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
         return
     u = t.view(torch.int64)
-    limbs = torch.stack([(u >> (16 * k)) & 0xFFFF for k in range(4)])
+    limbs = torch.stack([(u >> (16 * k)) & 0xFFFF for k in range(4)]).cpu()  # gloo: host tensors
     dist.all_reduce(limbs, op=dist.ReduceOp.SUM, group=group)
-    acc = torch.zeros_like(u)
+    acc = torch.zeros_like(limbs[0])
     for k in range(4):
         acc = acc + (limbs[k] << (16 * k))  # wraps mod 2^64
-    u.copy_(acc)
+    u.copy_(acc.to(u.device))
 
 
 def make_allreduce(trainer, group=None):

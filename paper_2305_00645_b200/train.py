@@ -136,6 +136,25 @@ class DeviceTrainer:
         return int(d.value)
 
 
+    def capture(self, X, Y, filler, keys):
+        """Capture one whole training run (every level's kernels) into a CUDA
+        graph; returns a callable that replays it on the current stream.
+        Fixed policy only (grow opens a stop bit on the host mid-run)."""
+        torch = _native.require_cuda()
+        if self.cfg.policy == "grow":
+            raise ValueError("the grow policy synchronises with the host per level; it cannot be captured")
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self.run(X, Y, filler, keys, stream=s)  # warm: sets kernel attributes outside capture
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.run(X, Y, filler, keys, stream=s)
+        self._graph_refs = (X, Y, filler, keys)  # keep the captured buffers alive
+        return g.replay
+
+
 def train_components(X: np.ndarray, Y: np.ndarray, cfg: TrainConfig, seeds: SeedSetup, dealer_seed: bytes,
                      *, device=None) -> Tuple[np.ndarray, np.ndarray, int]:
     """Whole-run entry on component-major shares: X [3, N, nf], Y [3, N]

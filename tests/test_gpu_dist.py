@@ -1,0 +1,74 @@
+"""Sample-sharded device training across ranks (B200).  The GPU box gives
+one GPU, so two ranks share cuda:0 and reduce over gloo (NCCL refuses two
+ranks on one device); this drives the real multi-rank device path --
+DeviceTrainer with n_total/sample_base, the gt_train allreduce callback and
+dist.allreduce_u64_ -- and requires the tree SHARES to equal the
+single-device run bit for bit."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from conftest import ROOT, opened, run_keys, share
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, X, Y, fill, depth, keys_t, out_dir):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from paper_2305_00645_b200 import TrainConfig
+    from paper_2305_00645_b200._native import gt_keys
+    from paper_2305_00645_b200.dist import shard_range, train_sharded
+    from paper_2305_00645_b200.shares import from_device, to_device
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    k = gt_keys()
+    k.dealer.k0, k.dealer.k1 = keys_t[0]
+    for i in range(3):
+        k.pair[i].k0, k.pair[i].k1 = keys_t[i + 1]
+    n = X.shape[1]
+    start, cnt = shard_range(n, world, rank)
+    tr, d = train_sharded(to_device(np.ascontiguousarray(X[:, start:start + cnt])),
+                          to_device(np.ascontiguousarray(Y[:, start:start + cnt])), to_device(fill),
+                          TrainConfig(depth=depth), k, n_total=n, sample_base=start)
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), T=from_device(tr.T), F=from_device(tr.F), d=d)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_device_training_equals_single_device(tmp_path):
+    from paper_2305_00645_b200 import TrainConfig
+    from paper_2305_00645_b200.seeds import derive_seed, filler_values
+    from paper_2305_00645_b200.train import train_components
+
+    rng = np.random.default_rng(31)
+    data = rng.integers(0, 2, (5003, 10), dtype=np.uint8)
+    depth = 5
+    seed = b"\x52" * 16
+    setup, k, keys_t = run_keys(seed)
+    fill = filler_values(setup.filler_seed, (1 << depth) - 1, 10)
+    X, Y = share(data[:, :-1], rng), share(data[:, -1], rng)
+    T1, F1, _ = train_components(X, Y, TrainConfig(depth=depth), setup, derive_seed(seed, "deal"))
+    mp.spawn(_worker, args=(2, _port(), X, Y, fill, depth, keys_t, str(tmp_path)), nprocs=2, join=True)
+    for r in range(2):
+        z = np.load(tmp_path / f"r{r}.npz")
+        assert int(z["d"]) == depth
+        assert np.array_equal(z["T"], T1) and np.array_equal(z["F"], F1)
