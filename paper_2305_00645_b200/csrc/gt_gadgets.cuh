@@ -434,8 +434,10 @@ __device__ __forceinline__ A3 b2a_arith(const B3& b, uint64_t A0, uint64_t A1, u
   const uint64_t Bb2 = beta ^ Bb0 ^ Bb1;
   const uint64_t A2 = (beta - A0 - A1) & M;
   const uint64_t e = ((b.v[0] ^ Bb0) ^ (b.v[1] ^ Bb1) ^ (b.v[2] ^ Bb2)) & 1ull;  // open_bits
-  const uint64_t coeff = (1ull - 2ull * e) & M;
-  return a3(((A0 * coeff) + e) & M, (A1 * coeff) & M, (A2 * coeff) & M);
+  // A * (1 - 2e) as a conditional negate ((A ^ m) - m, m = -e): keeps the
+  // IMAD pipe for the Philox rounds and the share products
+  const uint64_t m = 0ull - e;
+  return a3((((A0 ^ m) - m) + e) & M, ((A1 ^ m) - m) & M, ((A2 ^ m) - m) & M);
 }
 
 // standalone b2a: dealer fields A0=0 A1=1 bits=2.

@@ -720,7 +720,11 @@ int choose_node_block(int n_h, int WP) {
 int launch_count(CountArgs ca, cudaStream_t s, int num_sms) {
   const int nf = ca.nf, W = 2 * nf + 1, WP = nf + 1;
   ca.nb = choose_node_block(ca.n_h, WP);
-  ca.ts = std::max(32, std::min(256, ((CNT_TPB + ca.nb - 1) / ca.nb + 31) / 32 * 32));  // >= 256 phase-A lanes
+  // tile: ~128 phase-A lanes per tile, but keep >= ~3 waves of CTAs on shallow levels
+  ca.ts = std::max(32, std::min(128, ((128 + ca.nb - 1) / ca.nb + 31) / 32 * 32));
+  while (ca.ts > 32 && ((ca.N + ca.ts - 1) / ca.ts) * (uint64_t)((ca.n_h + ca.nb - 1) / ca.nb) <
+                           (uint64_t)num_sms * CNT_MINB * 3)
+    ca.ts -= 32;
   const unsigned gy = (unsigned)((ca.n_h + ca.nb - 1) / ca.nb);
   const uint64_t tiles = (ca.N + ca.ts - 1) / ca.ts;
   const uint64_t target = std::max<uint64_t>(1, (uint64_t)num_sms * CNT_MINB * 4 / gy);
