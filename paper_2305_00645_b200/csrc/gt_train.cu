@@ -241,7 +241,29 @@ __global__ void __launch_bounds__(CNT_TPB, CNT_MINB) k_count(CountArgs a) {
       }
     }
   }
-  if (!active) return;
+  // sum_s alpha_i = zacc[i] - zacc[i-1]; replicas of an item meet in shared
+  // memory so each CTA adds one word per (item, column, component)
+  uint64_t part[2][3];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) part[h][c] = acc[h][c] + zacc[h][c] - zacc[h][(c + 2) % 3];
+  if (R > 1) {
+    __syncthreads();  // la is dead: reuse it as [R][P][6] scratch
+    if (active)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) la[((uint64_t)q * P + item) * 6 + h * 3 + c] = part[h][c];
+    __syncthreads();
+    if (active && q == 0)
+      for (int r = 1; r < R; ++r)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) part[h][c] += la[((uint64_t)r * P + item) * 6 + h * 3 + c];
+  }
+  if (!active || q != 0) return;
   const uint64_t Sstride = (uint64_t)a.n_h * (W + 1);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -249,7 +271,7 @@ __global__ void __launch_bounds__(CNT_TPB, CNT_MINB) k_count(CountArgs a) {
 #pragma unroll
     for (int c = 0; c < 3; ++c)
       atomicAdd((unsigned long long*)&a.S[c * Sstride + (uint64_t)(n0 + n) * (W + 1) + w],
-                (unsigned long long)(acc[h][c] + zacc[h][c] - zacc[h][(c + 2) % 3]));
+                (unsigned long long)part[h][c]);
   }
 }
 
@@ -720,18 +742,14 @@ int choose_node_block(int n_h, int WP) {
 int launch_count(CountArgs ca, cudaStream_t s, int num_sms) {
   const int nf = ca.nf, W = 2 * nf + 1, WP = nf + 1;
   ca.nb = choose_node_block(ca.n_h, WP);
-  // tile: ~128 phase-A lanes per tile, but keep >= ~3 waves of CTAs on shallow levels
-  ca.ts = std::max(32, std::min(128, ((128 + ca.nb - 1) / ca.nb + 31) / 32 * 32));
-  while (ca.ts > 32 && ((ca.N + ca.ts - 1) / ca.ts) * (uint64_t)((ca.n_h + ca.nb - 1) / ca.nb) <
-                           (uint64_t)num_sms * CNT_MINB * 3)
-    ca.ts -= 32;
+  ca.ts = std::max(32, std::min(256, ((CNT_TPB + ca.nb - 1) / ca.nb + 31) / 32 * 32));  // >= 256 phase-A lanes
   const unsigned gy = (unsigned)((ca.n_h + ca.nb - 1) / ca.nb);
   const uint64_t tiles = (ca.N + ca.ts - 1) / ca.ts;
-  const uint64_t target = std::max<uint64_t>(1, (uint64_t)num_sms * CNT_MINB * 4 / gy);
+  const uint64_t target = std::max<uint64_t>(1, (uint64_t)num_sms * CNT_MINB * 2 / gy);
   const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>(tiles, target));
   ca.tiles_per_cta = (int)((tiles + gx - 1) / gx);
   const unsigned gxx = (unsigned)((tiles + ca.tiles_per_cta - 1) / ca.tiles_per_cta);
-  const int smem = (int)sizeof(uint64_t) * (3 * ca.ts * ca.nb + 3 * ca.nb);
+  const int smem = (int)sizeof(uint64_t) * (std::max(3 * ca.ts * ca.nb, 6 * CNT_TPB) + 3 * ca.nb);
   if (smem > 48 * 1024) GT_CUDA_CHECK(cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   k_count<<<dim3(gxx, gy), CNT_TPB, smem, s>>>(ca);
   GT_LAUNCH_CHECK("k_count");
