@@ -96,7 +96,7 @@ typedef struct {
   int32_t score_width; /* score ring width, 32 or 64 (TrainConfig.score_ring) */
   int32_t nf;          /* features = n_columns - 1, 1..64 */
   int32_t policy;      /* 0 = fixed, 1 = grow (one opened stop bit per level) */
-  int32_t reserved;
+  int32_t heuristic;   /* 0 = mpc (on device), 1 = tee (trusted helper via callback) */
   uint64_t n_total;     /* global sample count (counter_shift, train.py:189-192) */
   uint64_t n_local;     /* samples resident on this device */
   uint64_t sample_base; /* global index of the first local sample */
@@ -116,6 +116,19 @@ int gt_train(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* 
              uint64_t* T, uint64_t* F, int32_t* depth_out, void* workspace, uint64_t workspace_bytes,
              const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user, void* stream);
 
+/* Trusted split helper of heuristic "tee" (reference _heuristic_tee /
+ * _labels_tee, train.py:391-415, EnclaveService enclave.py:94-185).  Called
+ * synchronously with DEVICE pointers on `stream`:
+ *   op 1 (split):  counters [3][n][3][2nf] (c_orig), gamma [3][n] bit words,
+ *                  types [3][n]; writes out [4][3][n] = should_split bits,
+ *                  best feature, new type, new gamma words (fresh shares);
+ *   op 2 (labels): counters = effective counters, gamma/types unused; writes
+ *                  out [3][n] majority-label shares.
+ * Returns 0 on success. */
+typedef int (*gt_heuristic_fn)(int op, int level, int n_nodes, int nf, const uint64_t* counters,
+                               const uint64_t* gamma, const uint64_t* types, uint64_t* out, void* stream,
+                               void* user);
+
 /* Per-kernel-class device time of one gt_train_ex call, measured with CUDA
  * events recorded on `stream` around every launch (bench / roofline use). */
 typedef struct {
@@ -125,12 +138,13 @@ typedef struct {
   float ms_total; /* first to last event */
 } gt_train_profile;
 
-/* gt_train plus optional profiling (prof may be NULL; when set, the call
- * synchronizes `stream` before returning). */
+/* gt_train plus the tee helper callback (required when cfg->heuristic = 1)
+ * and optional profiling (prof may be NULL; when set, the call synchronizes
+ * `stream` before returning). */
 int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* labels, const uint64_t* filler,
                 uint64_t* T, uint64_t* F, int32_t* depth_out, void* workspace, uint64_t workspace_bytes,
-                const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user, void* stream,
-                gt_train_profile* prof);
+                const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user, gt_heuristic_fn heuristic,
+                void* heuristic_user, void* stream, gt_train_profile* prof);
 
 /* ---- secure inference (infer_batch, infer.py:91-106) ---- */
 

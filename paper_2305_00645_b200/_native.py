@@ -39,7 +39,7 @@ class gt_train_cfg(ctypes.Structure):
         ("score_width", ctypes.c_int32),
         ("nf", ctypes.c_int32),
         ("policy", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("heuristic", ctypes.c_int32),
         ("n_total", ctypes.c_uint64),
         ("n_local", ctypes.c_uint64),
         ("sample_base", ctypes.c_uint64),
@@ -54,6 +54,8 @@ class gt_train_profile(ctypes.Structure):
 
 
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p)
+HEURISTIC_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
 
 _u64p = ctypes.c_void_p
 _SIGS = {
@@ -85,8 +87,8 @@ _SIGS = {
                                 ctypes.POINTER(gt_keys), ALLREDUCE_FN, ctypes.c_void_p, ctypes.c_void_p]),
     "gt_train_ex": (ctypes.c_int, [ctypes.POINTER(gt_train_cfg), _u64p, _u64p, _u64p, _u64p, _u64p,
                                    ctypes.POINTER(ctypes.c_int32), ctypes.c_void_p, ctypes.c_uint64,
-                                   ctypes.POINTER(gt_keys), ALLREDUCE_FN, ctypes.c_void_p, ctypes.c_void_p,
-                                   ctypes.POINTER(gt_train_profile)]),
+                                   ctypes.POINTER(gt_keys), ALLREDUCE_FN, ctypes.c_void_p, HEURISTIC_FN,
+                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(gt_train_profile)]),
     "gt_infer": (ctypes.c_int, [ctypes.c_int, _u64p, _u64p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                 _u64p, _u64p, ctypes.POINTER(gt_keys), ctypes.c_void_p]),
     "gt_diag_philox": (ctypes.c_int, [ctypes.c_uint32, ctypes.c_uint32, _u64p, ctypes.c_void_p]),

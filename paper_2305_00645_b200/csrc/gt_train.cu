@@ -297,6 +297,7 @@ struct NodeArgs {
   uint64_t* ceff;             // [3][n_h][3][cols]
   uint64_t* hc;               // [4][3][n_h]: should_split, sd, new_f, new_gam
   uint64_t* dv;               // [3][3][n_h*cols]: P, Q+[Q==0], division terms
+  uint64_t* co_out;           // [3][n_h][3][cols] c_orig for the tee helper (or null)
   int n_h, nf, level, last, shift, tau;
   DivParams d;
   Keys K;
@@ -330,10 +331,12 @@ __global__ void __launch_bounds__(256) k_hc_pre(NodeArgs a) {
   }
   __syncthreads();
   auto CO = [&](int e) { return a3(co[e], co[C3 + e], co[2 * C3 + e]); };
+  if (a.co_out)  // heuristic "tee": hand the counters to the trusted helper
+    for (int e = tid; e < C3; e += blockDim.x) st3s(a.co_out, hs * C3, (uint64_t)n * C3 + e, CO(e));
 
   if (tid < 32) {
     const int wl = tid;
-    if (!a.last) {
+    if (!a.last && !a.co_out) {
       // zeros = eq([psi0, psi1, F - LEAF], 0)                 train.py:353-359
       const A3 fl = ld3s(a.f, hs, n);
       B3 z = {{0, 0, 0}};
@@ -381,7 +384,7 @@ __global__ void __launch_bounds__(256) k_hc_pre(NodeArgs a) {
     }
     return;
   }
-  if (a.last) return;
+  if (a.last || a.co_out) return;
   const int wt = tid - 32, wn = blockDim.x - 32;  // 224 worker threads
   // counters: truncate by the public shift, ring_down      train.py:366-370
   for (int e = wt; e < C3; e += wn) {
@@ -541,6 +544,7 @@ struct FinishArgs {
   const uint64_t* filler;  // public [slots]
   uint64_t *T, *F;         // [3][slots]
   uint64_t *f_nxt, *gam_nxt, *cst_nxt;  // children
+  const uint64_t* lab;                  // [3][n_h] helper labels (heuristic tee) or null
   uint64_t slots;
   int n_h, nf, level, labels;
   Keys K;
@@ -553,6 +557,13 @@ __global__ void __launch_bounds__(128) k_node_finish(FinishArgs a) {
   const uint64_t hs = (uint64_t)a.n_h, slot = hs - 1 + n;
   const Keys& K = a.K;
   auto CE = [&](int e) { return ld3s(a.ceff, hs * C3, (uint64_t)n * C3 + e); };
+  if (a.labels && a.lab) {  // labels from the trusted helper (train.py:301-302)
+    if (tid == 0) {
+      st3s(a.T, a.slots, slot, ld3s(a.lab, hs, n));
+      st3s(a.F, a.slots, slot, ld3s(a.f, hs, n));
+    }
+    return;
+  }
   if (a.labels) {
     // labels = b2a(lt(psi0, psi1)) on effective counters      train.py:300-306
     if (tid == 0) {
@@ -597,7 +608,7 @@ __global__ void __launch_bounds__(128) k_node_finish(FinishArgs a) {
 // ---------------------------------------------------------------------------
 
 struct Layout {
-  uint64_t prods, midx, S, f[2], gam[2], cst[2], ceff[2], hc, dv, stop, total;  // word offsets
+  uint64_t prods, midx, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
 };
 
 Layout layout(const gt_train_cfg& c) {
@@ -621,6 +632,8 @@ Layout layout(const gt_train_cfg& c) {
   }
   L.hc = take(12 * nmax);
   L.dv = take(9 * nmax * cols);
+  L.co = take(3 * nmax * 3 * cols);
+  L.lab = take(3 * nmax);
   L.stop = take(4);
   L.total = o;
   return L;
@@ -634,7 +647,7 @@ int launch_node_hc(const NodeArgs& na, cudaStream_t s) {
     GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_pre<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, pre_smem));
   k_hc_pre<SL><<<na.n_h, 256, pre_smem, s>>>(na);
   GT_LAUNCH_CHECK("k_hc_pre");
-  if (na.last) return GT_OK;
+  if (na.last || na.co_out) return GT_OK;
   const uint64_t lanes = (uint64_t)na.n_h * cols;
   const int div_smem = (int)sizeof(W2) * DIV_WARPS * newton_blocks<SL>(na.d);
   if (div_smem > 48 * 1024)
@@ -779,13 +792,13 @@ int gt_train(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* 
              uint64_t* T, uint64_t* F, int32_t* depth_out, void* workspace, uint64_t workspace_bytes,
              const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user, void* stream) {
   return gt_train_ex(cfg, features, labels, filler, T, F, depth_out, workspace, workspace_bytes, keys, allreduce,
-                     allreduce_user, stream, nullptr);
+                     allreduce_user, nullptr, nullptr, stream, nullptr);
 }
 
 int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* labels, const uint64_t* filler,
                 uint64_t* T, uint64_t* F, int32_t* depth_out, void* workspace, uint64_t workspace_bytes,
-                const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user, void* stream,
-                gt_train_profile* prof) {
+                const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user, gt_heuristic_fn heuristic,
+                void* heuristic_user, void* stream, gt_train_profile* prof) {
   if (!cfg || !keys) return fail_inval("gt_train: NULL cfg/keys");
   const gt_train_cfg c = *cfg;
   if (c.depth < 1 || c.depth > 16) return fail_inval("depth must be in 1..16");
@@ -796,6 +809,9 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
   if (c.n_local > c.n_total || c.sample_base + c.n_local > c.n_total) return fail_inval("bad sample shard");
   if (c.policy != 0 && c.policy != 1) return fail_inval("policy must be fixed (0) or grow (1)");
   if (c.policy == 1 && c.depth > 8) return fail_inval("grow policy supports depth <= 8");
+  if (c.heuristic != 0 && c.heuristic != 1) return fail_inval("heuristic must be mpc (0) or tee (1)");
+  if (c.heuristic == 1 && !heuristic) return fail_inval("heuristic tee needs the trusted-helper callback");
+  const bool tee = c.heuristic == 1;
   bool ok = false;
   const DivParams d = div_params(c.score_width, c.tau, &ok);
   if (!ok) return fail_inval("division unsupported at this width/tau");
@@ -880,6 +896,7 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
     na.ceff = ceff[cur];
     na.hc = hc;
     na.dv = ws + L.dv;
+    na.co_out = tee ? ws + L.co : nullptr;
     na.n_h = n_h;
     na.nf = c.nf;
     na.level = level;
@@ -892,9 +909,13 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
     int rc = c.score_width == 32 ? launch_node_hc<32>(na, s) : launch_node_hc<64>(na, s);
     if (rc) return rc;
     P.stop(Prof::NODE_HC);
-    if (!last) {  // k_hc_div + k_hc_post
+    if (!last && !tee) {  // k_hc_div + k_hc_post
       P.count_launch();
       P.count_launch();
+    }
+    if (!last && tee) {
+      int hrc = heuristic(1, level, n_h, c.nf, ws + L.co, gam[cur], f[cur], hc, stream, heuristic_user);
+      if (hrc) return fail_inval("trusted helper (split) failed");
     }
     if (!last && c.policy == 1) {
       k_node_stop<<<1, 32, 0, s>>>(hc, n_h, K, op_id(level, SITE_STOP), ws + L.stop);
@@ -915,6 +936,12 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
     fa.f_nxt = f[cur ^ 1];
     fa.gam_nxt = gam[cur ^ 1];
     fa.cst_nxt = cst[cur ^ 1];
+    fa.lab = nullptr;
+    if (last && tee) {
+      int hrc = heuristic(2, level, n_h, c.nf, ceff[cur], nullptr, nullptr, ws + L.lab, stream, heuristic_user);
+      if (hrc) return fail_inval("trusted helper (labels) failed");
+      fa.lab = ws + L.lab;
+    }
     fa.slots = slots;
     fa.n_h = n_h;
     fa.nf = c.nf;

@@ -146,6 +146,16 @@ class Ledger:
     def or_bits(self, n: int) -> None:
         self.and_bits(n, "or")
 
+    def enclave_call(self, up: int, down: int, tag: str) -> None:
+        """EnclaveBridge.call (transport.py:316-342): one request up from every
+        party, one response down; two rounds, records interleaved per party."""
+        tag = self.tag(tag)
+        up_r, down_r = self.round_no + 1, self.round_no + 2
+        self.round_no = down_r
+        for p in PARTIES:
+            self.transcript.append(up_r, p, 0, up, tag)
+            self.transcript.append(down_r, 0, p, down, tag)
+
     # -- gadgets (gadgets.py) -------------------------------------------------
     def and_reduce(self, k: int, n: int) -> None:  # gadgets.py:94-109
         while k > 1:
@@ -261,8 +271,17 @@ class Ledger:
         self.eq(n_nodes * nf, 64)
         self.and_bits(n_nodes * nf)
 
+    def heuristic_tee(self, n_nodes: int, nf: int) -> None:  # train.py:391-406, enclave.py:60-86
+        cells = n_nodes * 3 * 2 * nf
+        up = 16 + 16 * cells + 2 * n_nodes * nf + 16 * n_nodes
+        down = 16 * n_nodes + 16 * n_nodes + 2 * n_nodes + 2 * n_nodes * nf
+        self.enclave_call(up, down, "hc_tee")
+
+    def labels_tee(self, n_nodes: int, nf: int) -> None:  # train.py:409-415
+        self.enclave_call(16 + 16 * n_nodes * 3 * 2 * nf, 16 * n_nodes, "labels_tee")
+
     def train(self, n: int, nf: int, depth: int, tau: int = 10, score_width: int = 32,
-              grow_stop_level: Optional[int] = None, policy: str = "fixed") -> int:
+              grow_stop_level: Optional[int] = None, policy: str = "fixed", heuristic: str = "mpc") -> int:
         """train_tree (train.py:222-311).  Under the grow policy the opened
         stop bit is data dependent; pass the level the run stopped at."""
         with self.phase("count:0"):
@@ -277,8 +296,12 @@ class Ledger:
                 self.count_level(n, n_nodes, nf)
             last = level == depth - 1
             if not last:
-                with self.phase(f"hc_mpc:{level}"):
-                    self.heuristic_mpc(n_nodes, nf, n, tau, score_width)
+                if heuristic == "tee":
+                    with self.phase(f"hc_tee:{level}"):
+                        self.heuristic_tee(n_nodes, nf)
+                else:
+                    with self.phase(f"hc_mpc:{level}"):
+                        self.heuristic_mpc(n_nodes, nf, n, tau, score_width)
             with self.phase(f"replace:{level}"):
                 if level > 0:
                     self.eq(n_nodes, 64)
@@ -296,8 +319,11 @@ class Ledger:
                     self.select(n_nodes, n_nodes * 3 * 2 * nf, 64)
                 continue
             with self.phase(f"labels:{level}"):
-                self.lt(n_nodes, 64)
-                self.b2a(n_nodes)
+                if heuristic == "tee":
+                    self.labels_tee(n_nodes, nf)
+                else:
+                    self.lt(n_nodes, 64)
+                    self.b2a(n_nodes)
             return level + 1
         raise AssertionError("unreachable")
 

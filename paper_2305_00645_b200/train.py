@@ -64,8 +64,8 @@ def levels_of(vec, depth: int) -> List:
 
 
 def _validate(cfg: TrainConfig, nf: int) -> int:
-    if cfg.heuristic != "mpc":
-        raise NotImplementedError("heuristic 'tee' (attested helper) is not on the B200 path yet; use 'mpc'")
+    if cfg.heuristic not in ("mpc", "tee"):
+        raise ValueError(f"unknown heuristic {cfg.heuristic!r}")
     if cfg.policy not in ("fixed", "grow", "feature_cap"):
         raise ValueError(f"unknown depth policy {cfg.policy!r}")
     if cfg.count_ring.width != 64:
@@ -100,6 +100,7 @@ class DeviceTrainer:
         c.score_width = cfg.score_ring.width
         c.nf = nf
         c.policy = 1 if cfg.policy == "grow" else 0
+        c.heuristic = 1 if cfg.heuristic == "tee" else 0
         c.n_total = self.n_total
         c.n_local = self.n_local
         c.sample_base = int(sample_base)
@@ -117,11 +118,13 @@ class DeviceTrainer:
         off = (addr - self.workspace.data_ptr()) // 8
         return self.workspace[off:off + count]
 
-    def run(self, X, Y, filler, keys, *, allreduce=None, stream=None, profile=None) -> int:
+    def run(self, X, Y, filler, keys, *, allreduce=None, stream=None, profile=None, enclave_seed=None) -> int:
         """X [3, n_local, nf], Y [3, n_local], filler [2^H - 1] device int64
         tensors (uint64 bits).  Results land in self.T / self.F; returns the
         trained depth.  `profile` (a _native.gt_train_profile) receives the
-        CUDA-event device time per kernel class."""
+        CUDA-event device time per kernel class.  Heuristic "tee" calls the
+        trusted helper (enclave.DeviceEnclave, seeded by `enclave_seed`, the
+        reference's SeedSetup.enclave_seed) once per level."""
         torch = _native.require_cuda()
         if tuple(X.shape) != (3, self.n_local, self.nf) or tuple(Y.shape) != (3, self.n_local):
             raise ValueError("features must be [3, n, nf] and labels [3, n] component shares")
@@ -129,9 +132,18 @@ class DeviceTrainer:
         d = ctypes.c_int32(0)
         cb = _native.ALLREDUCE_FN(0) if allreduce is None else allreduce
         prof = ctypes.byref(profile) if profile is not None else None
+        helper = None
+        hfn = _native.HEURISTIC_FN(0)
+        if self.cfg.heuristic == "tee":
+            from .enclave import DeviceEnclave
+
+            helper = DeviceEnclave(enclave_seed if enclave_seed is not None else b"\x00" * 16, self)
+            hfn = helper.fn
         rc = self.lib.gt_train_ex(ctypes.byref(self.c), ptr(X), ptr(Y), ptr(filler), ptr(self.T), ptr(self.F),
                                   ctypes.byref(d), ptr(self.workspace), self.workspace.numel() * 8,
-                                  ctypes.byref(keys), cb, None, ctypes.c_void_p(s.cuda_stream), prof)
+                                  ctypes.byref(keys), cb, None, hfn, None, ctypes.c_void_p(s.cuda_stream), prof)
+        if rc and helper is not None and getattr(helper, "error", None) is not None:
+            raise helper.error
         _native.check(rc)
         return int(d.value)
 
@@ -141,8 +153,8 @@ class DeviceTrainer:
         graph; returns a callable that replays it on the current stream.
         Fixed policy only (grow opens a stop bit on the host mid-run)."""
         torch = _native.require_cuda()
-        if self.cfg.policy == "grow":
-            raise ValueError("the grow policy synchronises with the host per level; it cannot be captured")
+        if self.cfg.policy == "grow" or self.cfg.heuristic == "tee":
+            raise ValueError("grow / tee synchronise with the host per level; they cannot be captured")
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(s):
@@ -169,7 +181,8 @@ def train_components(X: np.ndarray, Y: np.ndarray, cfg: TrainConfig, seeds: Seed
     tr = DeviceTrainer(n, nf, cfg, device=device)
     fill = filler_values(seeds.filler_seed, (1 << tr.depth) - 1, nf + 1)
     keys = make_keys(seeds, dealer_seed)
-    depth = tr.run(to_device(X, tr.device), to_device(Y, tr.device), to_device(fill, tr.device), keys)
+    depth = tr.run(to_device(X, tr.device), to_device(Y, tr.device), to_device(fill, tr.device), keys,
+                   enclave_seed=seeds.enclave_seed)
     slots = (1 << depth) - 1
     return from_device(tr.T)[:, :slots].copy(), from_device(tr.F)[:, :slots].copy(), depth
 

@@ -349,12 +349,29 @@ def make_c2c3():
     print(f"c2 {secs:.1f}s c3 {isecs:.1f}s")
 
 
+def make_tee():
+    """Reference transcripts of the trusted-helper path (heuristic "tee")."""
+    out = {}
+    for (n, d, depth, policy) in ((60, 4, 3, "fixed"), (150, 6, 4, "fixed"), (33, 3, 1, "fixed"), (80, 4, 3, "grow")):
+        data = np.random.default_rng(n + d + depth).integers(0, 2, (n, d), dtype=np.uint8)
+        cfg = TrainConfig(depth=depth if policy == "fixed" else 1, heuristic="tee", policy=policy,
+                          max_depth=depth if policy == "grow" else None)
+        T, F, dep, run = secure_train(data, cfg, b"\x45" * 16)
+        out[f"tee_n{n}_d{d}_h{depth}_{policy}"] = {"n": n, "d": d, "depth": depth, "policy": policy,
+                                                   "trained_depth": dep, "T": T.tolist(), "F": F.tolist(),
+                                                   "records": run.transcript.records}
+    with open(os.path.join(OUT, "transcripts_tee.json"), "w") as fh:
+        json.dump(out, fh)
+    print("tee done")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-c2", action="store_true")
     ap.add_argument("--only", default=None)
     a = ap.parse_args()
-    steps = {"kats": make_kats, "trees": make_trees, "infer": make_infer,
+    steps = {"tee": make_tee,
+             "kats": make_kats, "trees": make_trees, "infer": make_infer,
              "transcripts": make_transcripts, "c2c3": make_c2c3}
     for name, fn in steps.items():
         if a.only and name != a.only:

@@ -228,3 +228,48 @@ def test_dropin_run_local_train_and_infer():
     run2 = run_local(body2, seeds=setup)
     got = sum(r.lo for r in run2.results)
     assert np.array_equal(got, shadow.plaintext_infer(want_T, 3, q))
+
+
+def test_tee_heuristic_bit_identical_to_plaintext_trainer():
+    # reference acceptance criterion 4 (test_acceptance.py:180-193): the trusted
+    # path equals plaintext_train exactly; golden oT/oF are the reference's own
+    # plaintext_train outputs
+    from conftest import golden_npz
+    from paper_2305_00645_b200.shares import AVec
+
+    z, meta = golden_npz("trees_mpc.npz")
+    rng = np.random.default_rng(40)
+    for k, m in enumerate(meta):
+        data, seed = z[f"data{k}"], bytes.fromhex(m["seed"])
+        X, Y, T, F, d, setup, keys = _device_train(data, m["depth"], seed, rng, heuristic="tee")
+        assert d == m["depth"]
+        assert np.array_equal(opened(T), z[f"oT{k}"]) and np.array_equal(opened(F), z[f"oF{k}"]), m["name"]
+
+
+def test_tee_transcripts_and_grow_match_reference():
+    from conftest import golden_json
+    from paper_2305_00645_b200 import TrainConfig, run_local, train_tree
+    from paper_2305_00645_b200.seeds import SeedSetup, derive_seed
+    from paper_2305_00645_b200.shares import AVec, RING64, pairs_from_components
+
+    g = golden_json("transcripts_tee.json")
+    seed = b"\x45" * 16
+    setup = SeedSetup.from_master(derive_seed(seed, "run"))
+    rng = np.random.default_rng(41)
+    for name, v in g.items():
+        n, d, depth, policy = v["n"], v["d"], v["depth"], v["policy"]
+        data = np.random.default_rng(n + d + depth).integers(0, 2, (n, d), dtype=np.uint8)
+        xp = pairs_from_components(share(data[:, :-1], rng))
+        yp = pairs_from_components(share(data[:, -1], rng))
+        cfg = TrainConfig(depth=depth if policy == "fixed" else 1, heuristic="tee", policy=policy,
+                          max_depth=depth if policy == "grow" else None)
+
+        def body(eng):
+            return train_tree(eng, AVec(RING64, *xp[eng.party - 1]), AVec(RING64, *yp[eng.party - 1]), cfg)
+
+        run = run_local(body, seeds=setup, dealer_seed=derive_seed(seed, "deal"))
+        assert run.results[0].depth == v["trained_depth"]
+        T = sum(r.T.lo for r in run.results)
+        F = sum(r.F.lo for r in run.results)
+        assert T.tolist() == v["T"] and F.tolist() == v["F"], name
+        assert run.transcript.records == [tuple(r) for r in v["records"]], name

@@ -135,3 +135,57 @@ def test_product_has_no_cpu_fallback_without_gpu():
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         train_components(np.zeros((3, 4, 2), np.uint64), np.zeros((3, 4), np.uint64), TrainConfig(depth=2),
                          SeedSetup.from_int(1), b"\x00" * 16)
+
+
+def test_trusted_helper_decisions_reproduce_reference_plaintext_trees():
+    """enclave.split_decisions / majority_labels (the tee helper, host side)
+    driven through the plaintext level loop (tree.py:289-325) reproduce the
+    reference's plaintext_train trees (golden oT/oF) on every golden case."""
+    from conftest import golden_npz
+    from oracle import shadow
+    from paper_2305_00645_b200 import enclave as E
+
+    z, meta = golden_npz("trees_mpc.npz")
+    for k, m in enumerate(meta):
+        data, depth = z[f"data{k}"], m["depth"]
+        X, y = data[:, :-1], data[:, -1]
+        n, nf = X.shape
+        setup = SeedSetup.from_master(derive_seed(bytes.fromhex(m["seed"]), "run"))
+        fill = filler_values(setup.filler_seed, (1 << depth) - 1, data.shape[1])
+        T = np.zeros((1 << depth) - 1, dtype=np.uint64)
+        F = np.zeros_like(T)
+        node = np.zeros(n, dtype=np.int64)
+        types = np.array([E.F_LEAF])
+        gam = np.ones((1, nf), dtype=bool)
+        eff_prev = None
+        for level in range(depth):
+            nn, off = 1 << level, (1 << level) - 1
+            C = shadow.node_counters(X, y, node, nn)
+            eff = C.copy()
+            if level:
+                empty = (C[:, 0, 0] + C[:, 0, 1]) == 0
+                eff[empty] = eff_prev[np.arange(nn)[empty] // 2]
+            if level == depth - 1:
+                T[off:off + nn] = E.majority_labels(eff)
+                F[off:off + nn] = types
+                break
+            sd, new_f, is_int, new_g = E.split_decisions(C, gam, types)
+            T[off:off + nn] = np.where(is_int, sd, fill[off:off + nn])
+            F[off:off + nn] = new_f
+            sf = np.where(node >= 0, np.where(is_int, sd.astype(np.int64), -1)[np.maximum(node, 0)], -1)
+            go = np.where(sf >= 0, X[np.arange(n), np.maximum(sf, 0)], 0)
+            node = np.where(sf >= 0, 2 * node + go, -1)
+            types = np.repeat(np.where(is_int, E.F_LEAF, E.F_DUMMY), 2)
+            gam = np.repeat(new_g, 2, axis=0)
+            eff_prev = eff
+        assert np.array_equal(T, z[f"oT{k}"]) and np.array_equal(F, z[f"oF{k}"]), m["name"]
+
+
+def test_ledger_tee_transcripts_match_reference():
+    g = golden_json("transcripts_tee.json")
+    for name, v in g.items():
+        led = L.Ledger()
+        d = led.train(v["n"], v["d"] - 1, v["depth"], policy=v["policy"], heuristic="tee",
+                      grow_stop_level=v["trained_depth"] - 1)
+        assert d == v["trained_depth"]
+        assert led.transcript.records == [tuple(r) for r in v["records"]], name
