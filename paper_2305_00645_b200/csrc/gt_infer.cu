@@ -84,10 +84,25 @@ extern "C" int gt_infer(int depth, const uint64_t* tree, const uint64_t* queries
   int dev = 0, sms = 148;
   GT_CUDA_CHECK(cudaGetDevice(&dev));
   GT_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  // group size: enough threads to fill the GPU for small batches, G = 8 for large
-  const uint64_t lanes_per_query = ((1ull << depth) - 1) + (uint64_t)depth * nf;
-  const uint64_t fill = (uint64_t)sms * 2048;
-  if (n * 8 >= fill || lanes_per_query < 64)
-    return launch_walk<8>(tree, depth, queries, n, (int)nf, instance_base, out, slot_out, K, s);
-  return launch_walk<32>(tree, depth, queries, n, (int)nf, instance_base, out, slot_out, K, s);
+  // group size G (threads per query): the fewest idle lane-slots over the
+  // walk's lookups (sum over levels of ceil(2^t/G) + ceil(nf/G) rounds of G
+  // lanes) among the G that still give >= 4 resident warps per SMSP
+  const uint64_t target = (uint64_t)sms * 512;
+  int best = 32;
+  uint64_t best_work = ~0ull;
+  for (int G = 4; G <= 32; G <<= 1) {
+    uint64_t rounds = 0;
+    for (int t = 0; t < depth; ++t) rounds += ((1ull << t) + G - 1) / G + (nf + G - 1) / G;
+    const uint64_t work = rounds * G;
+    if (n * (uint64_t)G >= target && work < best_work) {
+      best_work = work;
+      best = G;
+    }
+  }
+  switch (best) {
+    case 4: return launch_walk<4>(tree, depth, queries, n, (int)nf, instance_base, out, slot_out, K, s);
+    case 8: return launch_walk<8>(tree, depth, queries, n, (int)nf, instance_base, out, slot_out, K, s);
+    case 16: return launch_walk<16>(tree, depth, queries, n, (int)nf, instance_base, out, slot_out, K, s);
+    default: return launch_walk<32>(tree, depth, queries, n, (int)nf, instance_base, out, slot_out, K, s);
+  }
 }

@@ -660,9 +660,10 @@ int launch_node_hc(const NodeArgs& na, cudaStream_t s) {
   return GT_OK;
 }
 
-int launch_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint64_t slots, int m, int nf, uint64_t N,
-                     uint64_t base, const Keys& K, int level, cudaStream_t s) {
-  constexpr int G = 8, TPB = 256;
+template <int G>
+int launch_partition_g(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint64_t slots, int m, int nf,
+                       uint64_t N, uint64_t base, const Keys& K, int level, cudaStream_t s) {
+  constexpr int TPB = 256;
   const uint64_t threads = N * G;
   const unsigned grid = (unsigned)((threads + TPB - 1) / TPB);
   const int smem = 3 * m * (int)sizeof(uint64_t);
@@ -671,6 +672,28 @@ int launch_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint6
                                          op_id(level, SITE_PART_ROW));
   GT_LAUNCH_CHECK("k_partition");
   return GT_OK;
+}
+
+// G threads per sample: the fewest idle lane-slots (ceil(m/G) + ceil(nf/G)
+// rounds of G lanes) among the G that keep >= 4 resident warps per SMSP.
+int launch_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint64_t slots, int m, int nf, uint64_t N,
+                     uint64_t base, const Keys& K, int level, cudaStream_t s, int num_sms) {
+  const uint64_t target = (uint64_t)num_sms * 512;
+  int best = 16;
+  uint64_t best_work = ~0ull;
+  for (int G = 2; G <= 16; G <<= 1) {
+    const uint64_t work = (uint64_t)G * ((m + G - 1) / G + (nf + G - 1) / G);
+    if (N * (uint64_t)G >= target && work < best_work) {
+      best_work = work;
+      best = G;
+    }
+  }
+  switch (best) {
+    case 2: return launch_partition_g<2>(X, midx, T, slots, m, nf, N, base, K, level, s);
+    case 4: return launch_partition_g<4>(X, midx, T, slots, m, nf, N, base, K, level, s);
+    case 8: return launch_partition_g<8>(X, midx, T, slots, m, nf, N, base, K, level, s);
+    default: return launch_partition_g<16>(X, midx, T, slots, m, nf, N, base, K, level, s);
+  }
 }
 
 // CUDA-event timing of each launch (gt_train_ex with a profile struct).
@@ -855,7 +878,7 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
     const int n_h = 1 << level;
     if (level > 0 && N) {
       P.start();
-      int rc = launch_partition(features, midx, T, slots, n_h / 2, c.nf, N, c.sample_base, K, level, s);
+      int rc = launch_partition(features, midx, T, slots, n_h / 2, c.nf, N, c.sample_base, K, level, s, num_sms);
       if (rc) return rc;
       P.stop(Prof::PARTITION);
     }
