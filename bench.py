@@ -442,6 +442,15 @@ def main():
     if world == 1:
         preds_ok = bool(np.array_equal(from_device(out).sum(axis=0), z["preds"]))
 
+    # ---- protocol option: dot-product reshare of the count cells (same tree) ----
+    tr_dot = DeviceTrainer(cnt, NF_C2, TrainConfig(depth=DEPTH_C2, count_reshare="dot"), n_total=N_C2,
+                           sample_base=start, device=dev)
+    cb_dot = make_allreduce(tr_dot) if world > 1 else None
+    run_dot = tr_dot.capture(X, Y, FL, keys) if world == 1 else (lambda: tr_dot.run(X, Y, FL, keys, allreduce=cb_dot))
+    dot_s = _events_time(run_dot, args.steps, args.warmup, flush, barrier, stream, max_over_ranks)
+    dot_ok = bool(np.array_equal(from_device(tr_dot.T).sum(axis=0), z["T"]) and
+                  np.array_equal(from_device(tr_dot.F).sum(axis=0), z["F"]))
+
     scale = {}
     if not args.no_scale:
         scale["c4_train"] = scale_c4(ctx, max(3, args.steps // 2), args.warmup)
@@ -508,6 +517,10 @@ def main():
                       "roofline": {"bound": "hbm", "kernel": "k_walk", "achieved": walk_alg / inf_s / 1e9,
                                    "peak": peak, "unit": "GB/s", "frac": walk_alg / inf_s / 1e9 / peak}},
         "scale": scale,
+        "option_dot_reshare": {"metric": METRIC, "value": dot_s, "unit": "s/tree",
+                               "config": "C2 with TrainConfig(count_reshare='dot'): count cells reshared once "
+                                         "(ABY3 dot product) instead of per (sample, node, column) product",
+                               "tree_equals_reference": dot_ok},
     }
     if cpu_base is not None:
         line["cpu_baseline"] = cpu_base

@@ -37,7 +37,7 @@ extern "C" {
 #define GT_EINVAL 1
 #define GT_ECUDA 2
 
-#define GT_ABI_VERSION 1
+#define GT_ABI_VERSION 2
 
 typedef struct {
   uint32_t k0, k1;
@@ -100,6 +100,12 @@ typedef struct {
   uint64_t n_total;     /* global sample count (counter_shift, train.py:189-192) */
   uint64_t n_local;     /* samples resident on this device */
   uint64_t sample_base; /* global index of the first local sample */
+  int32_t count_reshare; /* 0 = reshare every (sample, node, column) product as the
+                            reference does (train.py:333); 1 = dot-product reshare: the
+                            local products are summed over samples first and each counter
+                            cell is reshared once (same revealed tree, n_h*W instead of
+                            N*n_h*W reshared words per level) */
+  int32_t reserved;
 } gt_train_cfg;
 
 /* Sum-allreduce of `count` uint64 words in place (count partials of one

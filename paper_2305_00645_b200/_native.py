@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgtree_b200.so")
 
 GT_OK, GT_EINVAL, GT_ECUDA = 0, 1, 2
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class ProtocolError(RuntimeError):
@@ -43,6 +43,8 @@ class gt_train_cfg(ctypes.Structure):
         ("n_total", ctypes.c_uint64),
         ("n_local", ctypes.c_uint64),
         ("sample_base", ctypes.c_uint64),
+        ("count_reshare", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 

@@ -116,7 +116,7 @@ struct CountArgs {
   const uint64_t *X, *P, *Y, *midx, *f;
   uint64_t* S;  // [3][n_h][W+1]
   uint64_t N, base;
-  int nf, n_h, off, nb, ts, tiles_per_cta;
+  int nf, n_h, off, nb, ts, tiles_per_cta, dot;
   Keys K;
   uint32_t op_leaf, op_cnt;
 };
@@ -212,9 +212,12 @@ __global__ void __launch_bounds__(CNT_TPB, CNT_MINB) k_count(CountArgs a) {
       const uint64_t pst0 = (uint64_t)R * cst0, pst1 = (uint64_t)R * cst1, lpst = (uint64_t)R * NB;
       for (int s = q; s < cnt; s += R, lane += lstep, p0 += pst0, p1 += pst1, lp += lpst) {
         const uint64_t l0 = lp[0], l1 = lp[(uint64_t)TS * NB], l2 = lp[2ull * TS * NB];
-        const W2 F0 = word2(K.pair[0], a.op_cnt, 3, wp, lane);
-        const W2 F1 = word2(K.pair[1], a.op_cnt, 3, wp, lane);
-        const W2 F2 = word2(K.pair[2], a.op_cnt, 3, wp, lane);
+        W2 F0 = {0, 0}, F1 = {0, 0}, F2 = {0, 0};
+        if (!a.dot) {  // per-element reshare (train.py:333); dot mode reshares the cell sums once
+          F0 = word2(K.pair[0], a.op_cnt, 3, wp, lane);
+          F1 = word2(K.pair[1], a.op_cnt, 3, wp, lane);
+          F2 = word2(K.pair[2], a.op_cnt, 3, wp, lane);
+        }
         {
           const uint64_t x0 = __ldg(p0), x1 = __ldg(p0 + ccs0), x2 = __ldg(p0 + 2 * ccs0);
           // z_i = l_i (x_i + x_{i+1}) + x_i l_{i+1}   (rss.py:391-395, mul_z)
@@ -752,6 +755,19 @@ struct Prof {
   }
 };
 
+// Dot-product reshare of the counter cells (count_reshare = 1): ONE zero
+// share per (node, column) per level, added by the shard holding sample 0:
+// alpha_i = F(k_i) - F(k_{i-1}) at (op_cnt, sub 4, field w, lane n).
+__global__ void k_count_alpha(uint64_t* S, int n_h, int nf, Keys K, uint32_t op_cnt) {
+  const int W = 2 * nf + 1, n = blockIdx.x;
+  const uint64_t Sstride = (uint64_t)n_h * (W + 1);
+  for (int w = threadIdx.x; w < W; w += blockDim.x) {
+    uint64_t F[3];
+    for (int i = 0; i < 3; ++i) F[i] = word(K.pair[i], op_cnt, 4, (uint32_t)w, (uint64_t)n);
+    for (int c = 0; c < 3; ++c) S[c * Sstride + (uint64_t)n * (W + 1) + w] += F[c] - F[(c + 2) % 3];
+  }
+}
+
 // Node block size: the (node, column-pair) items of a block should fill the
 // 256 threads (<= CNT_ITEMS each) with as little idle as possible.
 int choose_node_block(int n_h, int WP) {
@@ -833,6 +849,7 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
   if (c.policy != 0 && c.policy != 1) return fail_inval("policy must be fixed (0) or grow (1)");
   if (c.policy == 1 && c.depth > 8) return fail_inval("grow policy supports depth <= 8");
   if (c.heuristic != 0 && c.heuristic != 1) return fail_inval("heuristic must be mpc (0) or tee (1)");
+  if (c.count_reshare != 0 && c.count_reshare != 1) return fail_inval("count_reshare must be 0 or 1");
   if (c.heuristic == 1 && !heuristic) return fail_inval("heuristic tee needs the trusted-helper callback");
   const bool tee = c.heuristic == 1;
   bool ok = false;
@@ -900,10 +917,16 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
       ca.K = K;
       ca.op_leaf = op_id(level, SITE_ISLEAF);
       ca.op_cnt = op_id(level, SITE_COUNT);
+      ca.dot = c.count_reshare == 1;
       P.start();
       int rc = launch_count(ca, s, num_sms);
       if (rc) return rc;
       P.stop(Prof::COUNT);
+    }
+    if (c.count_reshare == 1 && c.sample_base == 0) {
+      k_count_alpha<<<n_h, 64, 0, s>>>(S, n_h, c.nf, K, op_id(level, SITE_COUNT));
+      GT_LAUNCH_CHECK("k_count_alpha");
+      P.count_launch();
     }
     if (allreduce) {
       int rc = allreduce(S, swords, stream, allreduce_user);

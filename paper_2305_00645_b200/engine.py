@@ -178,7 +178,8 @@ def train_tree(eng: PartyEngine, features, labels, cfg: TrainConfig) -> TrainRes
         Y = components_from_avecs([p[1] for p in payloads])
         T, F, depth = train_components(X, Y.reshape(3, -1), cfg, eng.seeds, eng.dealer_seed, device=eng.device)
         eng._ledger.train(n_samples, nf, resolved_depth(cfg, nf + 1), cfg.tau, cfg.score_ring.width,
-                          grow_stop_level=depth - 1, policy=cfg.policy, heuristic=cfg.heuristic)
+                          grow_stop_level=depth - 1, policy=cfg.policy, heuristic=cfg.heuristic,
+                          count_reshare=cfg.count_reshare)
         tv, fv = avecs_from_components(T, RING64), avecs_from_components(F, RING64)
         return [TrainResult(T=tv[i], F=fv[i], depth=depth) for i in range(3)]
 

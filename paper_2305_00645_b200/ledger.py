@@ -238,7 +238,7 @@ class Ledger:
     row_lookup = oaa  # oaa.py:38-55 has the identical message pattern
 
     # -- protocols ------------------------------------------------------------
-    def count_level(self, n: int, n_nodes: int, nf: int) -> None:  # train.py:315-343
+    def count_level(self, n: int, n_nodes: int, nf: int, dot: bool = False) -> None:  # train.py:315-343
         width = 2 * nf + 1
         self.eq(n_nodes, 64)
         if self.lane_limit is None:
@@ -250,7 +250,10 @@ class Ledger:
             self.eq(span * n_nodes, 64)
             self.and_bits(span * n_nodes)
             self.b2a(span * n_nodes)
-            self.mul(span * n_nodes * width, 64, "count.mul")
+            if not dot:
+                self.mul(span * n_nodes * width, 64, "count.mul")
+        if dot and spans:  # one reshare of the summed cells (count_reshare="dot")
+            self.mul(n_nodes * width, 64, "count.mul")
 
     def heuristic_mpc(self, n_nodes: int, nf: int, n_samples: int, tau: int, score_width: int) -> None:
         cols = 2 * nf  # train.py:346-388
@@ -281,7 +284,8 @@ class Ledger:
         self.enclave_call(16 + 16 * n_nodes * 3 * 2 * nf, 16 * n_nodes, "labels_tee")
 
     def train(self, n: int, nf: int, depth: int, tau: int = 10, score_width: int = 32,
-              grow_stop_level: Optional[int] = None, policy: str = "fixed", heuristic: str = "mpc") -> int:
+              grow_stop_level: Optional[int] = None, policy: str = "fixed", heuristic: str = "mpc",
+              count_reshare: str = "elementwise") -> int:
         """train_tree (train.py:222-311).  Under the grow policy the opened
         stop bit is data dependent; pass the level the run stopped at."""
         with self.phase("count:0"):
@@ -293,7 +297,7 @@ class Ledger:
                     self.oaa(n, 1 << (level - 1), 64)
                     self.row_lookup(n, nf, 64)
             with self.phase(f"count:{level}"):
-                self.count_level(n, n_nodes, nf)
+                self.count_level(n, n_nodes, nf, dot=count_reshare == "dot")
             last = level == depth - 1
             if not last:
                 if heuristic == "tee":

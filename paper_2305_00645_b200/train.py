@@ -32,6 +32,11 @@ class TrainConfig:
     max_depth: Optional[int] = None
     score_ring: Ring = RING32
     count_ring: Ring = RING64
+    # B200 extension: "elementwise" reshares every count product like the
+    # reference (train.py:333); "dot" sums the local products over samples
+    # first and reshares each counter cell once (ABY3-style dot product) --
+    # same revealed tree, a fraction of the reshared words.
+    count_reshare: str = "elementwise"
 
 
 @dataclass
@@ -68,6 +73,8 @@ def _validate(cfg: TrainConfig, nf: int) -> int:
         raise ValueError(f"unknown heuristic {cfg.heuristic!r}")
     if cfg.policy not in ("fixed", "grow", "feature_cap"):
         raise ValueError(f"unknown depth policy {cfg.policy!r}")
+    if cfg.count_reshare not in ("elementwise", "dot"):
+        raise ValueError(f"unknown count_reshare {cfg.count_reshare!r}")
     if cfg.count_ring.width != 64:
         raise ValueError("counters live in Z_2^64 on the B200 path")
     depth = resolved_depth(cfg, nf + 1)
@@ -101,6 +108,7 @@ class DeviceTrainer:
         c.nf = nf
         c.policy = 1 if cfg.policy == "grow" else 0
         c.heuristic = 1 if cfg.heuristic == "tee" else 0
+        c.count_reshare = 1 if cfg.count_reshare == "dot" else 0
         c.n_total = self.n_total
         c.n_local = self.n_local
         c.sample_base = int(sample_base)

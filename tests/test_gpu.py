@@ -273,3 +273,15 @@ def test_tee_transcripts_and_grow_match_reference():
         F = sum(r.F.lo for r in run.results)
         assert T.tolist() == v["T"] and F.tolist() == v["F"], name
         assert run.transcript.records == [tuple(r) for r in v["records"]], name
+
+
+def test_dot_product_count_reshare_same_tree_and_oracle_shares():
+    rng = np.random.default_rng(42)
+    cases = list(ref_cases())
+    for m, data, Tref, Fref in cases[:12] + cases[-5:]:
+        seed = bytes.fromhex(m["seed"])
+        X, Y, T, F, d, setup, keys = _device_train(data, m["depth"], seed, rng, count_reshare="dot")
+        assert np.array_equal(opened(T), Tref) and np.array_equal(opened(F), Fref), m["name"]
+        fill = filler_values(setup.filler_seed, (1 << m["depth"]) - 1, data.shape[1])
+        To, Fo, _ = oracle.train(X, Y, fill, m["depth"], keys, count_reshare=1)
+        assert np.array_equal(T, To) and np.array_equal(F, Fo), m["name"]

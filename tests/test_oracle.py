@@ -128,3 +128,15 @@ def test_oracle_shares_independent_of_input_sharing():
         t, f, _ = oracle.train(share(data[:, :-1], rng), share(data[:, -1], rng), fill, m["depth"], keys)
         outs.append((opened(t), opened(f)))
     assert all(np.array_equal(a, b) for a, b in zip(outs[0], outs[1]))
+
+
+def test_oracle_dot_reshare_same_revealed_trees():
+    from paper_2305_00645_b200.seeds import filler_values
+
+    rng = np.random.default_rng(13)
+    for m, data, T, F in list(ref_cases())[:20]:
+        setup, _, keys = run_keys(bytes.fromhex(m["seed"]))
+        fill = filler_values(setup.filler_seed, (1 << m["depth"]) - 1, data.shape[1])
+        t, f, _ = oracle.train(share(data[:, :-1], rng), share(data[:, -1], rng), fill, m["depth"], keys,
+                               count_reshare=1)
+        assert np.array_equal(opened(t), T) and np.array_equal(opened(f), F), m["name"]
