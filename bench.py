@@ -318,10 +318,17 @@ def main():
     from paper_2305_00645_b200.shares import from_device
     from paper_2305_00645_b200.train import DeviceTrainer
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # GT_BENCH_DEVICE / GT_BENCH_BACKEND are test hooks (multi-rank dry run on
+    # one GPU over gloo); the driver's runs use one GPU per rank over NCCL
+    local_dev = int(os.environ.get("GT_BENCH_DEVICE", local))
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("GT_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if world > 1:
@@ -330,7 +337,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -359,7 +366,7 @@ def main():
         run_tree()
     torch.cuda.synchronize()
     step_ms = []
-    with ClockSampler(local) as clk:
+    with ClockSampler(local_dev) as clk:
         for _ in range(args.steps):
             flush.zero_()
             barrier()

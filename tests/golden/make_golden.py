@@ -349,6 +349,31 @@ def make_c2c3():
     print(f"c2 {secs:.1f}s c3 {isecs:.1f}s")
 
 
+def make_variants():
+    """MPC trees with a Z_2^64 score ring and other tau (TrainConfig.score_ring /
+    tau, train.py:171-179; cli --width / --tau)."""
+    from obtree.ring import Ring
+    arrays, meta = {}, []
+    cases = []
+    for i in range(6):
+        data, depth = _battery_dataset(100 + i)
+        cases.append((data, min(depth, 4), 64, 10))
+    for i in range(4):
+        data, depth = _battery_dataset(200 + i)
+        cases.append((data, min(depth, 4), 32, 8))
+    rng = np.random.default_rng(5)
+    cases.append((rng.integers(0, 2, (1500, 6), dtype=np.uint8), 3, 64, 12))
+    cases.append((rng.integers(0, 2, (2100, 5), dtype=np.uint8), 3, 32, 6))
+    for k, (data, depth, width, tau) in enumerate(cases):
+        seed = (9000 + k).to_bytes(16, "little")
+        T, F, dep, _ = secure_train(data, TrainConfig(depth=depth, tau=tau, score_ring=Ring(width)), seed)
+        arrays[f"data{k}"], arrays[f"T{k}"], arrays[f"F{k}"] = data, T, F
+        meta.append({"depth": depth, "width": width, "tau": tau, "seed": seed.hex()})
+    arrays["meta"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(OUT, "trees_variants.npz"), **arrays)
+    print("variants done")
+
+
 def make_tee():
     """Reference transcripts of the trusted-helper path (heuristic "tee")."""
     out = {}
@@ -370,7 +395,8 @@ if __name__ == "__main__":
     ap.add_argument("--skip-c2", action="store_true")
     ap.add_argument("--only", default=None)
     a = ap.parse_args()
-    steps = {"tee": make_tee,
+    steps = {"variants": make_variants,
+             "tee": make_tee,
              "kats": make_kats, "trees": make_trees, "infer": make_infer,
              "transcripts": make_transcripts, "c2c3": make_c2c3}
     for name, fn in steps.items():

@@ -285,3 +285,18 @@ def test_dot_product_count_reshare_same_tree_and_oracle_shares():
         fill = filler_values(setup.filler_seed, (1 << m["depth"]) - 1, data.shape[1])
         To, Fo, _ = oracle.train(X, Y, fill, m["depth"], keys, count_reshare=1)
         assert np.array_equal(T, To) and np.array_equal(F, Fo), m["name"]
+
+
+def test_score_ring64_and_tau_variants_match_reference_and_oracle():
+    from paper_2305_00645_b200.shares import Ring
+
+    z, meta = golden_npz("trees_variants.npz")
+    rng = np.random.default_rng(43)
+    for k, m in enumerate(meta):
+        data, seed = z[f"data{k}"], bytes.fromhex(m["seed"])
+        X, Y, T, F, d, setup, keys = _device_train(data, m["depth"], seed, rng, tau=m["tau"],
+                                                   score_ring=Ring(m["width"]))
+        assert np.array_equal(opened(T), z[f"T{k}"]) and np.array_equal(opened(F), z[f"F{k}"]), m
+        fill = filler_values(setup.filler_seed, (1 << m["depth"]) - 1, data.shape[1])
+        To, Fo, _ = oracle.train(X, Y, fill, m["depth"], keys, tau=m["tau"], score_width=m["width"])
+        assert np.array_equal(T, To) and np.array_equal(F, Fo), m

@@ -140,3 +140,17 @@ def test_oracle_dot_reshare_same_revealed_trees():
         t, f, _ = oracle.train(share(data[:, :-1], rng), share(data[:, -1], rng), fill, m["depth"], keys,
                                count_reshare=1)
         assert np.array_equal(opened(t), T) and np.array_equal(opened(f), F), m["name"]
+
+
+def test_oracle_score_ring64_and_tau_variants_match_reference():
+    from paper_2305_00645_b200.seeds import filler_values
+
+    z, meta = golden_npz("trees_variants.npz")
+    rng = np.random.default_rng(14)
+    for k, m in enumerate(meta):
+        data = z[f"data{k}"]
+        setup, _, keys = run_keys(bytes.fromhex(m["seed"]))
+        fill = filler_values(setup.filler_seed, (1 << m["depth"]) - 1, data.shape[1])
+        t, f, _ = oracle.train(share(data[:, :-1], rng), share(data[:, -1], rng), fill, m["depth"], keys,
+                               tau=m["tau"], score_width=m["width"])
+        assert np.array_equal(opened(t), z[f"T{k}"]) and np.array_equal(opened(f), z[f"F{k}"]), m
