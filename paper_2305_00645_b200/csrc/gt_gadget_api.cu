@@ -2,6 +2,7 @@
 // run one reference gadget call (gadgets.py / oaa.py / rss.py) over a batch
 // of lanes; the training and inference drivers use the same per-lane device
 // functions fused into larger kernels.
+#include <algorithm>
 #include <string>
 
 #include "gt_common.cuh"
@@ -110,9 +111,9 @@ __global__ void k_division(const uint64_t* p, const uint64_t* q, uint64_t* out, 
                            uint32_t op) {
   extern __shared__ W2 tape_sm[];
   const int warp = threadIdx.x >> 5;
-  const uint64_t i = (uint64_t)blockIdx.x * 4 + warp;
+  const uint64_t i = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (i >= n) return;
-  const A3 r = division_warp<L>(K, op, 0, i, ld3(p, n, i), ld3(q, n, i), d, tape_sm + warp * newton_blocks<L>(d));
+  const A3 r = division_warp<L>(K, op, 0, i, ld3(p, n, i), ld3(q, n, i), d, tape_sm + warp * division_tape_blocks<L>(d));
   if ((threadIdx.x & 31) == 0) st3(out, n, i, r);
 }
 
@@ -296,21 +297,19 @@ int gt_division(int width, const uint64_t* p, const uint64_t* q, uint64_t* out, 
   if (n == 0) return GT_OK;
   if (!p || !q || !out) return fail_inval("gt_division: NULL operand");
   cudaStream_t s = (cudaStream_t)stream;
-  const unsigned grid = (unsigned)((n + 3) / 4);
   const Keys K = to_keys(keys);
-  if (width == 64) {
-    const int smem = 4 * newton_blocks<64>(d) * (int)sizeof(W2);
-    GT_CUDA_CHECK(cudaFuncSetAttribute(k_division<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    k_division<64><<<grid, 128, smem, s>>>(p, q, out, n, d, K, op);
-  } else if (width == 32) {
-    const int smem = 4 * newton_blocks<32>(d) * (int)sizeof(W2);
-    GT_CUDA_CHECK(cudaFuncSetAttribute(k_division<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    k_division<32><<<grid, 128, smem, s>>>(p, q, out, n, d, K, op);
-  } else {
-    const int smem = 4 * newton_blocks<8>(d) * (int)sizeof(W2);
-    GT_CUDA_CHECK(cudaFuncSetAttribute(k_division<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    k_division<8><<<grid, 128, smem, s>>>(p, q, out, n, d, K, op);
-  }
+  auto launch = [&](auto kern, int blocks) -> int {
+    const int per_warp = blocks * (int)sizeof(W2);
+    const int wpc = std::max(1, std::min(4, (200 * 1024) / per_warp));
+    GT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, per_warp * wpc));
+    kern<<<(unsigned)((n + wpc - 1) / wpc), 32 * wpc, per_warp * wpc, s>>>(p, q, out, n, d, K, op);
+    return GT_OK;
+  };
+  int rc;
+  if (width == 64) rc = launch(k_division<64>, division_tape_blocks<64>(d));
+  else if (width == 32) rc = launch(k_division<32>, division_tape_blocks<32>(d));
+  else rc = launch(k_division<8>, division_tape_blocks<8>(d));
+  if (rc) return rc;
   GT_LAUNCH_CHECK("gt_division");
   return GT_OK;
 }

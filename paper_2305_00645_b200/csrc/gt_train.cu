@@ -282,8 +282,8 @@ __global__ void __launch_bounds__(CNT_TPB, CNT_MINB) k_count(CountArgs a) {
 // per-node heuristic (_heuristic_mpc, train.py:346-388) + replace, in three
 // kernels so no thread waits on another's serial chain:
 //   k_hc_pre   one CTA per node: counter assembly; warp 0 runs the short
-//              probe/featureless/should_split/new_f chain and then replace;
-//              warps 1-7 truncate + ring_down the counters, form the squares
+//              probe/featureless/should_split/new_f chain, warp 1 replace;
+//              warps 2-7 truncate + ring_down the counters, form the squares
 //              and Q products and the Q==0 fix (pv, qs -> global)
 //   k_hc_div   one WARP per (node, column): division_warp (ladder over the
 //              lanes, Newton chain from a cooperatively drawn Philox tape)
@@ -306,7 +306,7 @@ struct NodeArgs {
   Keys K;
 };
 
-__device__ __forceinline__ void bar_workers() { asm volatile("bar.sync 1, 224;" ::: "memory"); }
+__device__ __forceinline__ void bar_workers() { asm volatile("bar.sync 1, 192;" ::: "memory"); }
 
 template <int SL>
 __global__ void __launch_bounds__(256) k_hc_pre(NodeArgs a) {
@@ -371,6 +371,10 @@ __global__ void __launch_bounds__(256) k_hc_pre(NodeArgs a) {
         }
       }
     }
+    return;
+  }
+  if (tid < 64) {
+    const int wl = tid - 32;
     // replace: empty nodes adopt the parent's effective counters  train.py:269-276
     if (a.level > 0) {
       A3 ca = a3(0, 0, 0);
@@ -388,7 +392,7 @@ __global__ void __launch_bounds__(256) k_hc_pre(NodeArgs a) {
     return;
   }
   if (a.last || a.co_out) return;
-  const int wt = tid - 32, wn = blockDim.x - 32;  // 224 worker threads
+  const int wt = tid - 64, wn = blockDim.x - 64;  // 192 worker threads (warps 2-7)
   // counters: truncate by the public shift, ring_down      train.py:366-370
   for (int e = wt; e < C3; e += wn) {
     A3 x = CO(e);
@@ -425,16 +429,16 @@ __global__ void __launch_bounds__(256) k_hc_pre(NodeArgs a) {
   }
 }
 
-constexpr int DIV_WARPS = 4;
+constexpr int DIV_WARPS = 4;  // at most; fewer when the tape is large (score ring Z_2^64)
 
 template <int SL>
 __global__ void __launch_bounds__(32 * DIV_WARPS) k_hc_div(NodeArgs a) {
   extern __shared__ W2 tape_sm[];
-  const int warp = threadIdx.x >> 5;
+  const int warp = threadIdx.x >> 5, wpc = blockDim.x >> 5;
   const uint64_t cols = 2 * (uint64_t)a.nf, lanes = (uint64_t)a.n_h * cols;
-  const uint64_t li = (uint64_t)blockIdx.x * DIV_WARPS + warp;
+  const uint64_t li = (uint64_t)blockIdx.x * wpc + warp;
   if (li >= lanes) return;  // whole warp exits together
-  W2* tape = tape_sm + (size_t)warp * newton_blocks<SL>(a.d);
+  W2* tape = tape_sm + (size_t)warp * division_tape_blocks<SL>(a.d);
   const A3 p = ld3s(a.dv, lanes, li), q = ld3s(a.dv + 3 * lanes, lanes, li);
   // terms = division(P, qsafe)                              train.py:382
   const A3 t = division_warp<SL>(a.K, op_id(a.level, SITE_HC), 13, li, p, q, a.d, tape);
@@ -582,20 +586,21 @@ __global__ void __launch_bounds__(128) k_node_finish(FinishArgs a) {
   B3 ss;
   for (int c = 0; c < 3; ++c) ss.v[c] = a.hc[(0 * 3 + c) * hs + n];
   const uint64_t cs = 2 * hs;  // children per level
-  if (tid == 0) {
-    // payload, child type (train.py:286-289)
+  // the three selects of split:h are independent chains: one lane each
+  if (tid == 0) {  // payload T = is_int ? sd : filler        (train.py:287)
     const A3 sd = ld3s(a.hc + 3 * hs, hs, n);
-    const A3 t = select_with<64>(K, op, 0, 0, n, a3_const(a.filler[slot]), sd, b2a<64>(K, op, 0, n, ss));
-    const A3 cf = select_with<64>(K, op, 2, 0, n, a3_const(F_DUMMY), a3_const(F_LEAF), b2a<64>(K, op, 2, n, ss));
-    const A3 c2 = b2a<64>(K, op, 4, n, ss);
-    for (int c = 0; c < 3; ++c) ca[c] = c2.v[c];
-    st3s(a.T, a.slots, slot, t);
+    st3s(a.T, a.slots, slot, select_with<64>(K, op, 0, 0, n, a3_const(a.filler[slot]), sd, b2a<64>(K, op, 0, n, ss)));
     st3s(a.F, a.slots, slot, ld3s(a.hc + 6 * hs, hs, n));
+  } else if (tid == 1) {  // child type = is_int ? LEAF : DUMMY  (train.py:288-289)
+    const A3 cf = select_with<64>(K, op, 2, 0, n, a3_const(F_DUMMY), a3_const(F_LEAF), b2a<64>(K, op, 2, n, ss));
     const A3 ng = ld3s(a.hc + 9 * hs, hs, n);
     for (int ch = 0; ch < 2; ++ch) {
       st3s(a.f_nxt, cs, 2 * n + ch, cf);
       st3s(a.gam_nxt, cs, 2 * n + ch, ng);
     }
+  } else if (tid == 2) {  // child counters' condition
+    const A3 c2 = b2a<64>(K, op, 4, n, ss);
+    for (int c = 0; c < 3; ++c) ca[c] = c2.v[c];
   }
   __syncthreads();
   // child counters = select(c_eff, 0, is_int)                 train.py:290
@@ -652,10 +657,12 @@ int launch_node_hc(const NodeArgs& na, cudaStream_t s) {
   GT_LAUNCH_CHECK("k_hc_pre");
   if (na.last || na.co_out) return GT_OK;
   const uint64_t lanes = (uint64_t)na.n_h * cols;
-  const int div_smem = (int)sizeof(W2) * DIV_WARPS * newton_blocks<SL>(na.d);
+  const int per_warp = (int)sizeof(W2) * division_tape_blocks<SL>(na.d);
+  const int wpc = std::max(1, std::min(DIV_WARPS, (200 * 1024) / per_warp));
+  const int div_smem = per_warp * wpc;
   if (div_smem > 48 * 1024)
     GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_div<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, div_smem));
-  k_hc_div<SL><<<(unsigned)((lanes + DIV_WARPS - 1) / DIV_WARPS), 32 * DIV_WARPS, div_smem, s>>>(na);
+  k_hc_div<SL><<<(unsigned)((lanes + wpc - 1) / wpc), 32 * wpc, div_smem, s>>>(na);
   GT_LAUNCH_CHECK("k_hc_div");
   const int post_smem = (int)sizeof(uint64_t) * (12 * na.nf + 4) + (int)sizeof(W2) * 8 * ArgminPair<SL>::BLOCKS;
   k_hc_post<SL><<<na.n_h, 256, post_smem, s>>>(na);
