@@ -116,58 +116,32 @@ __device__ __forceinline__ A3 newton_from_tape(const A3& p, const A3& q, const A
   return truncT(prod, d.kf);
 }
 
-// Ladder step j's blocks (gadgets.py:327-332): lt at sub0+j-1 (LtRand order)
-// then the b2a of ~[q < 2^j] at sub0+nl+j-1 (dealer blocks 0, 1).
-template <int L>
-struct LadderStep {
-  static constexpr int BLOCKS = LtRand<L>::BLOCKS + 2;
-};
-
 template <int L>
 __host__ __device__ inline int division_tape_blocks(const DivParams& d) {
-  return (d.bound - 1) * LadderStep<L>::BLOCKS + newton_blocks<L>(d);
+  return newton_blocks<L>(d);
 }
 
 // Whole division lane by one warp; every lane returns the result.  `tape`
-// points at this warp's division_tape_blocks() W2 slots of shared memory:
-// the ladder's blocks, then the Newton chain's, all drawn by the 32 lanes
-// in parallel before any arithmetic.
+// points at this warp's division_tape_blocks() W2 slots of shared memory.
+// The ladder's steps run one per lane with in-register Philox (measured
+// faster than staging their ~1000 blocks through the tape); the Newton
+// chain's blocks are drawn by all 32 lanes into the tape first.
 template <int L>
 __device__ __forceinline__ A3 division_warp(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const A3& p,
                                             const A3& q, const DivParams& d, W2* tape) {
-  constexpr uint64_t M = Ring<L>::M;
-  constexpr int LB = LtRand<L>::BLOCKS, SB = LadderStep<L>::BLOCKS;
   const int wl = threadIdx.x & 31;
   const int nl = d.bound - 1;
-  for (int g = wl; g < nl * SB; g += 32) {
-    const int j = g / SB + 1, b = g % SB;
-    int key;
-    uint32_t s, pidx;
-    if (b < LB) {
-      lt_block_id<L>(b, sub + (j - 1), &key, &pidx);
-      s = sub + (j - 1);
-    } else {
-      key = -1, s = sub + nl + (j - 1), pidx = b - LB;
-    }
-    tape[g] = word2(key < 0 ? K.dealer : K.pair[key], op, s, pidx, lane);
-  }
-  W2* nt = tape + nl * SB;
-  newton_tape_fill<L>(K, op, sub + 2 * nl, lane, d, nt, wl);
-  __syncwarp();
   // ladder: step j = wl + 1 (+32 ...) on this lane
   A3 acc = a3(0, 0, 0);
-  for (int j = wl + 1; j <= nl; j += 32) {
-    const W2* t = tape + (j - 1) * SB;
-    const B3 below = lt_arith<L>(t, q, a3_const((1ull << j) & M));
-    const A3 tj = b2a_arith<L>(bnot(below, 1ull), t[LB].a, t[LB].b, t[LB + 1].a);
-    acc = add<L>(acc, mul_pub<L>(tj, 1ull << (d.bound - 1 - j)));
-  }
+  for (int j = wl + 1; j <= nl; j += 32) acc = add<L>(acc, div_ladder_term<L>(K, op, sub, lane, q, j, d));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
     for (int i = 0; i < 3; ++i) acc.v[i] = (acc.v[i] + __shfl_xor_sync(0xffffffffu, acc.v[i], o)) & Ring<L>::M;
   const A3 v = rsub_pub<L>(1ull << (d.bound - 1), acc);
-  const A3 out = newton_from_tape<L>(p, q, v, d, nt);
+  newton_tape_fill<L>(K, op, sub + 2 * nl, lane, d, tape, wl);
+  __syncwarp();
+  const A3 out = newton_from_tape<L>(p, q, v, d, tape);
   __syncwarp();
   return out;
 }
