@@ -98,3 +98,18 @@ def filler_values(seed: bytes, total: int, n_columns: int) -> np.ndarray:
     if n_columns < 2:
         raise ValueError("need at least one feature column")
     return aes_ctr_words(seed, total) % np.uint64(n_columns - 1)
+
+
+def share_values(values: np.ndarray, width: int, seed: bytes):
+    """The reference dealer's input split (dealer.py:619-623): AES-CTR stream
+    of derive_seed(seed, "input"); s1, s2 = next n words each, s3 = v - s1 - s2.
+    Returns the three parties' (lo, hi) pairs."""
+    mask = np.uint64((1 << width) - 1) if width < 64 else np.uint64(0xFFFFFFFFFFFFFFFF)
+    flat = np.asarray(values, dtype=np.uint64).ravel() & mask
+    n = flat.size
+    if width != 64:
+        raise ValueError("input sharing here is for the Z_2^64 count ring")
+    words = aes_ctr_words(derive_seed(seed, "input"), 2 * n)
+    s1, s2 = words[:n], words[n:]
+    s3 = flat - s1 - s2
+    return [(s1, s2), (s2, s3), (s3, s1)]

@@ -172,3 +172,50 @@ def ptr(t) -> int:
     if not t.is_contiguous():
         raise ValueError("device share tensors must be contiguous")
     return t.data_ptr()
+
+
+# --------------------------------------------------------------------------
+# on-disk share files (OBS1, reference rss.py:452-481)
+# --------------------------------------------------------------------------
+
+import struct as _struct
+
+SHARE_MAGIC = b"OBS1"
+_SHARE_HEADER = _struct.Struct("<4sBBBxQ")  # magic, width, kind, party, count
+
+
+def _pack(arr: np.ndarray, ring: Ring) -> bytes:
+    flat = np.ascontiguousarray(np.asarray(arr, dtype=np.uint64).ravel())
+    if ring.width == 64:
+        return flat.astype("<u8").tobytes()
+    if ring.width == 32:
+        return flat.astype("<u4").tobytes()
+    return flat.astype(np.uint8).tobytes()
+
+
+def _unpack(raw: bytes, ring: Ring, n: int) -> np.ndarray:
+    dt = {64: "<u8", 32: "<u4", 8: np.uint8}[ring.width]
+    return np.frombuffer(raw, dtype=dt, count=n).astype(np.uint64)
+
+
+def write_share_file(path: str, lo: np.ndarray, hi: np.ndarray, ring: Ring, party: int, kind: int = 0) -> None:
+    """One party's share pair, interleaved little-endian (rss.py:460-469)."""
+    lo = np.asarray(lo, dtype=np.uint64).ravel()
+    hi = np.asarray(hi, dtype=np.uint64).ravel()
+    inter = np.empty(lo.size * 2, dtype=np.uint64)
+    inter[0::2], inter[1::2] = lo, hi
+    with open(path, "wb") as f:
+        f.write(_SHARE_HEADER.pack(SHARE_MAGIC, ring.width, kind, party, lo.size))
+        f.write(_pack(inter, ring))
+
+
+def read_share_file(path: str):
+    """-> (lo, hi, ring, party) (rss.py:472-481)."""
+    with open(path, "rb") as f:
+        head = f.read(_SHARE_HEADER.size)
+        magic, width, kind, party, count = _SHARE_HEADER.unpack(head)
+        if magic != SHARE_MAGIC:
+            raise ShareError(f"{path}: not a share file")
+        ring = Ring(width)
+        inter = _unpack(f.read(2 * count * ring.nbytes), ring, 2 * count)
+    return inter[0::2], inter[1::2], ring, party

@@ -390,12 +390,90 @@ def make_tee():
     print("tee done")
 
 
+def make_cli():
+    """Run the reference CLI (obtree.cli.main) on small CSVs and record what
+    it writes: stdout lines, tree_meta/metrics/tree JSON, predictions.csv,
+    compare reports, bench tables and sha256 of the dealt share/seed files."""
+    import contextlib
+    import hashlib
+    import io
+    import tempfile
+    from pathlib import Path
+
+    from obtree import cli as ref_cli
+
+    gdir = Path(OUT) / "cli"
+    gdir.mkdir(exist_ok=True)
+    rng = np.random.default_rng(2024)
+    data = rng.integers(0, 2, (90, 6), dtype=np.uint8)
+    data[:, -1] = data[:, 0] ^ (data[:, 2] & rng.integers(0, 2, 90, dtype=np.uint8))
+    queries = rng.integers(0, 2, (40, 5), dtype=np.uint8)
+    tree_mod.save_csv(gdir / "data.csv", data)
+    tree_mod.save_csv(gdir / "queries.csv", queries)
+    (gdir / "run.conf").write_text("# flag defaults\ndepth = 3\nseed = 99\nprofile = test\n")
+    cases = {
+        "train_mpc": ["train", "--data", "{g}/data.csv", "--depth", "3", "--seed", "7", "--profile", "test",
+                      "--reveal", "--out", "{t}/train_mpc"],
+        "train_tee": ["train", "--data", "{g}/data.csv", "--depth", "4", "--heuristic", "tee", "--seed", "0x0badcafe",
+                      "--profile", "test", "--reveal", "--out", "{t}/train_tee"],
+        "train_grow": ["train", "--data", "{g}/data.csv", "--policy", "grow", "--max-depth", "4", "--seed", "5",
+                       "--profile", "test", "--reveal", "--out", "{t}/train_grow"],
+        "train_conf": ["train", "--config", "{g}/run.conf", "--data", "{g}/data.csv", "--reveal",
+                       "--out", "{t}/train_conf"],
+        "infer_dir": ["infer", "--tree-dir", "{t}/train_mpc", "--queries", "{g}/queries.csv", "--seed", "7",
+                      "--profile", "test", "--reveal", "--out", "{t}/infer_dir"],
+        "infer_plain": ["infer", "--tree", "{t}/train_tee/tree.json", "--queries", "{g}/queries.csv", "--seed", "3",
+                        "--profile", "test", "--reveal", "--out", "{t}/infer_plain"],
+        "compare_mpc": ["compare", "--data", "{g}/data.csv", "--depth", "3", "--seed", "11",
+                        "--out", "{t}/compare_mpc.json"],
+        "compare_tee": ["compare", "--data", "{g}/data.csv", "--depth", "3", "--heuristic", "tee", "--seed", "11",
+                        "--out", "{t}/compare_tee.json"],
+        "deal_train": ["deal", "--data", "{g}/data.csv", "--depth", "3", "--seed", "21", "--out", "{t}/deal_train"],
+        "train_deal": ["train", "--deal-dir", "{t}/deal_train", "--depth", "3", "--profile", "test", "--reveal",
+                       "--out", "{t}/train_deal"],
+        "bench_oaa": ["bench", "--suite", "oaa", "--lookups", "200", "--sizes", "1,8,64", "--out", "{t}/bench_oaa.json"],
+        "bench_train": ["bench", "--suite", "train", "--rows", "64", "--cols", "5", "--depths", "2,3",
+                        "--out", "{t}/bench_train.json"],
+        "bench_infer": ["bench", "--suite", "infer", "--rows", "100", "--depths", "3,5", "--out",
+                        "{t}/bench_infer.json"],
+        "err_reveal_prod": ["train", "--data", "{g}/data.csv", "--reveal", "--out", "{t}/x"],
+        "err_width": ["train", "--data", "{g}/data.csv", "--width", "4", "--out", "{t}/x"],
+        "err_tolerance": ["compare", "--data", "{g}/data.csv", "--depth", "1", "--seed", "11", "--split", "0.5",
+                          "--tolerance", "-1"],
+    }
+    files = ("tree.json", "tree_meta.json", "metrics.json", "predictions.csv")
+    out = {}
+    with tempfile.TemporaryDirectory() as t:
+        for name, argv in cases.items():
+            argv = [a.format(g=gdir, t=t) for a in argv]
+            buf = io.StringIO()
+            with contextlib.redirect_stdout(buf):
+                code = ref_cli.main(argv)
+            rec = {"argv": [a.replace(str(gdir), "{g}").replace(t, "{t}") for a in argv], "exit": code,
+                   "stdout": buf.getvalue().replace(t, "{t}"), "files": {}}
+            target = Path(argv[argv.index("--out") + 1]) if "--out" in argv else None
+            if target is not None and target.is_dir():
+                for f in files:
+                    if (target / f).exists():
+                        rec["files"][f] = (target / f).read_text()
+                if name.startswith("deal"):
+                    for p in sorted(target.rglob("*")):
+                        if p.is_file() and p.name != "material.bin":
+                            rec["files"][str(p.relative_to(target))] = hashlib.sha256(p.read_bytes()).hexdigest()
+            elif target is not None and target.exists():
+                rec["files"]["report"] = target.read_text()
+            out[name] = rec
+            print("cli", name, code)
+    with open(gdir / "cli.json", "w") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-c2", action="store_true")
     ap.add_argument("--only", default=None)
     a = ap.parse_args()
-    steps = {"variants": make_variants,
+    steps = {"cli": make_cli, "variants": make_variants,
              "tee": make_tee,
              "kats": make_kats, "trees": make_trees, "infer": make_infer,
              "transcripts": make_transcripts, "c2c3": make_c2c3}
