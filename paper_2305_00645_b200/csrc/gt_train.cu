@@ -17,6 +17,7 @@
 // Every lane's randomness is keyed by (op, sub, field, global lane), so the
 // shares produced are independent of sharding and of launch geometry.
 #include <algorithm>
+#include <cstdlib>
 #include <utility>
 #include <vector>
 
@@ -109,72 +110,71 @@ __global__ void k_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T
 // ---------------------------------------------------------------------------
 
 constexpr int CNT_TPB = 256;
-constexpr int CNT_ITEMS = 1;
-constexpr int CNT_MINB = 3;  // CTAs per SM the register budget is sized for
+constexpr int CNT_NA = 2;  // nodes per phase-B thread tile
 
 struct CountArgs {
   const uint64_t *X, *P, *Y, *midx, *f;
   uint64_t* S;  // [3][n_h][W+1]
   uint64_t N, base;
-  int nf, n_h, off, nb, ts, tiles_per_cta, dot;
+  int nf, n_h, off, nb, ts, tiles_per_cta, wc;
   Keys K;
   uint32_t op_leaf, op_cnt;
 };
 
-// One CTA = (sample chunk, node block).  Per tile of TS samples:
-//  phase A, one lane per (sample, node):  la = b2a(eq(m_idx, off+n) & leaf[n])
-//    drawing the six Philox blocks of LaneRand at sub 0 (pair block half b
-//    = the AND gate's zero bit);
-//  phase B, one work item per (node, column pair): the W products (sample
-//    columns read straight from global/L1: every item of the tile reads the
-//    same rows)
-//    mul(cols[s][w], la[s][n]) with their reshare (sub 3, field w), summed
-//    over the samples in registers; the mask column (w = W) adds la itself.
-// Every thread owns one item (replicas split the samples of a tile when there
-// are fewer items than threads); partial sums leave through one 64-bit
-// atomic per (item, column, component).
+// One CTA = (sample range, node block of nb nodes).  Per tile of TS samples:
+//  staging  the tile's sample columns x[c][s][w] (features, prods, label;
+//           the mask column and the padding stay 0) and node indices -> smem
+//           with coalesced row loads;
+//  phase A  one lane per (sample, node):  la = b2a(eq(m_idx, off+n) & leaf[n])
+//           from the six Philox blocks of LaneRand at sub 0 (pair block half b
+//           bit 0 = the AND gate's zero bit)                train.py:328-331
+//  phase B  a register-tiled ring contraction: each thread owns NA nodes x CB
+//           columns x 3 components and accumulates the party-local cross
+//           terms of mul(cols, la) (rss.py:391-395)
+//              acc_i += la_i (x_i + x_{i+1}) + la_{i+1} x_i
+//           over the samples; the mask column (x = 0, u = 1) accumulates la_i
+//           itself (s_mask, train.py:334).                  train.py:332-335
+// The products' reshare zero shares are not drawn here: their per-sample
+// stream telescopes (F(s) = H(s+1) - H(s)), so their sum
+// over the shard is added once per cell by k_count_alpha.
+template <int CNT_CB, int CNT_MINB>
 __global__ void __launch_bounds__(CNT_TPB, CNT_MINB) k_count(CountArgs a) {
-  extern __shared__ uint64_t sm[];
-  const int nf = a.nf, W = 2 * nf + 1, WP = nf + 1, NB = a.nb, TS = a.ts;
+  extern __shared__ __align__(16) uint64_t sm[];
+  const int nf = a.nf, W = 2 * nf + 1, WC = a.wc, NB = a.nb, NBP = (NB + 1) & ~1, TS = a.ts;
   const int tid = threadIdx.x, bd = blockDim.x;
   const int n0 = blockIdx.y * NB;
   const int nb = min(NB, a.n_h - n0);
-  uint64_t* la = sm;                    // [3][TS][NB]
-  uint64_t* leaf = la + 3 * TS * NB;    // [3][NB]
+  uint64_t* xs = sm;                   // [3][TS][WC]
+  uint64_t* la = xs + 3 * TS * WC;     // [3][TS][NBP]
+  uint64_t* mi = la + 3 * TS * NBP;    // [3][TS]
+  uint64_t* leaf = mi + 3 * TS;        // [3][NBP]
   const Keys& K = a.K;
   const uint64_t nfx = a.N * (uint64_t)nf;
 
   // is_leaf = eq(F_level, LEAF) (train.py:320); identical in every CTA
   for (int t = tid; t < nb; t += bd) {
     const B3 z = eqz<64>(K, a.op_leaf, 0, (uint64_t)(n0 + t), add_pub<64>(ld3s(a.f, a.n_h, n0 + t), 0ull - F_LEAF));
-    for (int c = 0; c < 3; ++c) leaf[c * NB + t] = z.v[c] & 1ull;
+    for (int c = 0; c < 3; ++c) leaf[c * NBP + t] = z.v[c] & 1ull;
   }
+  // mask / padding columns and the odd node slot stay zero for the whole kernel
+  for (int e = tid; e < 3 * TS * WC; e += bd) xs[e] = 0;
+  for (int e = tid; e < 3 * TS * NBP; e += bd) la[e] = 0;
 
-  const int P = nb * WP;
-  const int R = P >= bd ? 1 : bd / P;  // replicas split a tile's samples
+  const int CT = WC / CNT_CB, P = (NBP / CNT_NA) * CT;
+  const int R = max(1, bd / P);  // replicas split a tile's samples
   const bool active = tid < P * R;
   const int item = active ? tid % P : 0, q = tid / P;
-  const int n = item / WP, wp = item % WP;
-  const int w0 = 2 * wp, w1 = 2 * wp + 1;
-  const bool mask_col = w1 >= W;
-  // column w of sample s, component c: c_w[c * ccs_w + s * cst_w]  (sample_cols, train.py:231-233)
-  auto colptr = [&](int w, const uint64_t*& base, uint64_t& ccs, uint64_t& cst) {
-    if (w < nf) {
-      base = a.X + w, ccs = nfx, cst = (uint64_t)nf;
-    } else if (w < 2 * nf) {
-      base = a.P + (w - nf), ccs = nfx, cst = (uint64_t)nf;
-    } else {
-      base = a.Y, ccs = a.N, cst = 1;
-    }
-  };
-  const uint64_t *c0, *c1;
-  uint64_t ccs0, cst0, ccs1, cst1;
-  colptr(w0, c0, ccs0, cst0);
-  colptr(mask_col ? w0 : w1, c1, ccs1, cst1);
-  // acc[h][c]: local cross terms of column w0 + h, component c;
-  // zacc[h][i]: sum of key i's zero-share words (alpha_i = F_i - F_{i-1} is
-  // applied once at the end: sum_s alpha_i = zacc[i] - zacc[i-1]).
-  uint64_t acc[2][3] = {{0, 0, 0}, {0, 0, 0}}, zacc[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  const int nl = (item / CT) * CNT_NA, cl = (item % CT) * CNT_CB;
+  uint64_t mflag[CNT_CB];  // 1 on the mask column: u = x_i + x_{i+1} + 1 = 1 there
+#pragma unroll
+  for (int j = 0; j < CNT_CB; ++j) mflag[j] = (cl + j == W) ? 1ull : 0ull;
+  uint64_t acc[3][CNT_NA][CNT_CB];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int i = 0; i < CNT_NA; ++i)
+#pragma unroll
+      for (int j = 0; j < CNT_CB; ++j) acc[c][i][j] = 0;
 
   const uint64_t tile0 = (uint64_t)blockIdx.x * a.tiles_per_cta;
   for (int tt = 0; tt < a.tiles_per_cta; ++tt) {
@@ -182,99 +182,107 @@ __global__ void __launch_bounds__(CNT_TPB, CNT_MINB) k_count(CountArgs a) {
     if (s0 >= a.N) break;
     const int cnt = (int)min((uint64_t)TS, a.N - s0);
     __syncthreads();
+    // staging: X / prods rows are contiguous per component (sample_cols, train.py:231-233)
+    for (int e = tid; e < cnt * nf; e += bd) {
+      const int s = e / nf, f = e % nf;
+      const uint64_t g = (s0 + s) * (uint64_t)nf + f;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        xs[(c * TS + s) * WC + f] = __ldg(a.X + c * nfx + g);
+        xs[(c * TS + s) * WC + nf + f] = __ldg(a.P + c * nfx + g);
+      }
+    }
+    for (int s = tid; s < cnt; s += bd)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        xs[(c * TS + s) * WC + 2 * nf] = __ldg(a.Y + c * a.N + s0 + s);
+        mi[c * TS + s] = __ldg(a.midx + c * a.N + s0 + s);
+      }
+    __syncthreads();
     // phase A                                             train.py:328-331
     for (int e = tid; e < cnt * nb; e += bd) {
       const int s = e / nb, nn = e % nb;
       const uint64_t lane = (a.base + s0 + s) * (uint64_t)a.n_h + (uint64_t)(n0 + nn);
-      const A3 d = add_pub<64>(ld3s(a.midx, a.N, s0 + s), 0ull - (uint64_t)(a.off + n0 + nn));
+      const A3 d = add_pub<64>(a3(mi[s], mi[TS + s], mi[2 * TS + s]), 0ull - (uint64_t)(a.off + n0 + nn));
       const LaneRand Rr = lane_rand(K, a.op_cnt, 0, lane);
       const B3 hit = eq_arith<64>(d, Rr.r, Rr.Rb0, Rr.Rb1, Rr.Zw);
       B3 lf;
       uint64_t Z[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        lf.v[c] = leaf[c * NB + nn];
+        lf.v[c] = leaf[c * NBP + nn];
         Z[c] = Rr.F[c] & 1ull;
       }
       const B3 lcf = and_z(hit, lf, Z);
       const A3 l = b2a_arith<64>(lcf, Rr.A0, Rr.A1, Rr.bits);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) la[(c * TS + s) * NB + nn] = l.v[c];
+      for (int c = 0; c < 3; ++c) la[(c * TS + s) * NBP + nn] = l.v[c];
     }
     __syncthreads();
-    // phase B: contrib = mul(rows, la) summed over samples   train.py:332-335
+    // phase B: sum_s mul(cols, la) cross terms            train.py:332-335
     if (active) {
-      uint64_t lane = (a.base + s0 + q) * (uint64_t)a.n_h + (uint64_t)(n0 + n);
-      const uint64_t lstep = (uint64_t)R * a.n_h;
-      const uint64_t* p0 = c0 + (s0 + q) * cst0;
-      const uint64_t* p1 = c1 + (s0 + q) * cst1;
-      const uint64_t* lp = la + (uint64_t)q * NB + n;
-      const uint64_t pst0 = (uint64_t)R * cst0, pst1 = (uint64_t)R * cst1, lpst = (uint64_t)R * NB;
-      for (int s = q; s < cnt; s += R, lane += lstep, p0 += pst0, p1 += pst1, lp += lpst) {
-        const uint64_t l0 = lp[0], l1 = lp[(uint64_t)TS * NB], l2 = lp[2ull * TS * NB];
-        W2 F0 = {0, 0}, F1 = {0, 0}, F2 = {0, 0};
-        if (!a.dot) {  // per-element reshare (train.py:333); dot mode reshares the cell sums once
-          F0 = word2(K.pair[0], a.op_cnt, 3, wp, lane);
-          F1 = word2(K.pair[1], a.op_cnt, 3, wp, lane);
-          F2 = word2(K.pair[2], a.op_cnt, 3, wp, lane);
+#pragma unroll 2
+      for (int s = q; s < cnt; s += R) {
+        uint64_t l[3][CNT_NA], x[3][CNT_CB];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const ulonglong2 lv = *reinterpret_cast<const ulonglong2*>(la + (c * TS + s) * NBP + nl);
+          l[c][0] = lv.x;
+          l[c][1] = lv.y;
+          const ulonglong2 x01 = *reinterpret_cast<const ulonglong2*>(xs + (c * TS + s) * WC + cl);
+          const ulonglong2 x23 = *reinterpret_cast<const ulonglong2*>(xs + (c * TS + s) * WC + cl + 2);
+          x[c][0] = x01.x;
+          x[c][1] = x01.y;
+          x[c][2] = x23.x;
+          x[c][3] = x23.y;
         }
-        {
-          const uint64_t x0 = __ldg(p0), x1 = __ldg(p0 + ccs0), x2 = __ldg(p0 + 2 * ccs0);
-          // z_i = l_i (x_i + x_{i+1}) + x_i l_{i+1}   (rss.py:391-395, mul_z)
-          acc[0][0] += l0 * (x0 + x1) + x0 * l1;
-          acc[0][1] += l1 * (x1 + x2) + x1 * l2;
-          acc[0][2] += l2 * (x2 + x0) + x2 * l0;
-          zacc[0][0] += F0.a;
-          zacc[0][1] += F1.a;
-          zacc[0][2] += F2.a;
-        }
-        if (!mask_col) {
-          const uint64_t x0 = __ldg(p1), x1 = __ldg(p1 + ccs1), x2 = __ldg(p1 + 2 * ccs1);
-          acc[1][0] += l0 * (x0 + x1) + x0 * l1;
-          acc[1][1] += l1 * (x1 + x2) + x1 * l2;
-          acc[1][2] += l2 * (x2 + x0) + x2 * l0;
-          zacc[1][0] += F0.b;
-          zacc[1][1] += F1.b;
-          zacc[1][2] += F2.b;
-        } else {  // mask column: s_mask += la (local)
-          acc[1][0] += l0;
-          acc[1][1] += l1;
-          acc[1][2] += l2;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int cn = (c + 1) % 3;
+#pragma unroll
+          for (int j = 0; j < CNT_CB; ++j) {
+            const uint64_t u = x[c][j] + x[cn][j] + mflag[j];
+#pragma unroll
+            for (int i = 0; i < CNT_NA; ++i) acc[c][i][j] += l[c][i] * u + l[cn][i] * x[c][j];
+          }
         }
       }
     }
   }
-  // sum_s alpha_i = zacc[i] - zacc[i-1]; replicas of an item meet in shared
-  // memory so each CTA adds one word per (item, column, component)
-  uint64_t part[2][3];
-#pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) part[h][c] = acc[h][c] + zacc[h][c] - zacc[h][(c + 2) % 3];
+  // replicas of an item meet in shared memory; one atomic per (cell, component) per CTA
+  constexpr int NACC = 3 * CNT_NA * CNT_CB;
   if (R > 1) {
-    __syncthreads();  // la is dead: reuse it as [R][P][6] scratch
+    __syncthreads();  // xs is dead: reuse it as [R][P][NACC] scratch
     if (active)
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
+      for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) la[((uint64_t)q * P + item) * 6 + h * 3 + c] = part[h][c];
+        for (int i = 0; i < CNT_NA; ++i)
+#pragma unroll
+          for (int j = 0; j < CNT_CB; ++j) xs[((uint64_t)q * P + item) * NACC + (c * CNT_NA + i) * CNT_CB + j] = acc[c][i][j];
     __syncthreads();
     if (active && q == 0)
       for (int r = 1; r < R; ++r)
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+        for (int c = 0; c < 3; ++c)
 #pragma unroll
-          for (int c = 0; c < 3; ++c) part[h][c] += la[((uint64_t)r * P + item) * 6 + h * 3 + c];
+          for (int i = 0; i < CNT_NA; ++i)
+#pragma unroll
+            for (int j = 0; j < CNT_CB; ++j) acc[c][i][j] += xs[((uint64_t)r * P + item) * NACC + (c * CNT_NA + i) * CNT_CB + j];
   }
   if (!active || q != 0) return;
   const uint64_t Sstride = (uint64_t)a.n_h * (W + 1);
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int w = 2 * wp + h;
+  for (int i = 0; i < CNT_NA; ++i) {
+    if (nl + i >= nb) continue;
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
-      atomicAdd((unsigned long long*)&a.S[c * Sstride + (uint64_t)(n0 + n) * (W + 1) + w],
-                (unsigned long long)part[h][c]);
+    for (int j = 0; j < CNT_CB; ++j) {
+      if (cl + j > W) continue;
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        atomicAdd((unsigned long long*)&a.S[c * Sstride + (uint64_t)(n0 + nl + i) * (W + 1) + cl + j],
+                  (unsigned long long)acc[c][i][j]);
+    }
   }
 }
 
@@ -762,57 +770,72 @@ struct Prof {
   }
 };
 
-// Dot-product reshare of the counter cells (count_reshare = 1): ONE zero
-// share per (node, column) per level, added by the shard holding sample 0:
-// alpha_i = F(k_i) - F(k_{i-1}) at (op_cnt, sub 4, field w, lane n).
-__global__ void k_count_alpha(uint64_t* S, int n_h, int nf, Keys K, uint32_t op_cnt) {
-  const int W = 2 * nf + 1, n = blockIdx.x;
+// Zero shares of the count products, summed over this shard's samples, one
+// thread per (node, column):
+//  elementwise (count_reshare 0, train.py:333): the product at (sample t,
+//    node n, column w) is reshared with F_i(t) = H_i(t+1) - H_i(t),
+//    H_i(t) = pair_i word (op_cnt, sub 3, field w, lane t n_h + n), so
+//    sum_{t in [t0, t1)} F_i = H_i(t1) - H_i(t0) and sharded sums telescope;
+//  dot (count_reshare 1): ONE zero share per cell, F_i at (op_cnt, sub 4,
+//    field w, lane n), added by the shard holding sample 0.
+// alpha_i = F_i - F_{i-1} (rss.py:302-306).
+__global__ void k_count_alpha(uint64_t* S, int n_h, int nf, Keys K, uint32_t op_cnt, int dot, uint64_t t0,
+                              uint64_t t1) {
+  const int W = 2 * nf + 1;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n_h * W) return;
+  const int n = e / W, w = e % W;
   const uint64_t Sstride = (uint64_t)n_h * (W + 1);
-  for (int w = threadIdx.x; w < W; w += blockDim.x) {
-    uint64_t F[3];
-    for (int i = 0; i < 3; ++i) F[i] = word(K.pair[i], op_cnt, 4, (uint32_t)w, (uint64_t)n);
-    for (int c = 0; c < 3; ++c) S[c * Sstride + (uint64_t)n * (W + 1) + w] += F[c] - F[(c + 2) % 3];
-  }
+  uint64_t F[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    F[i] = dot ? word(K.pair[i], op_cnt, 4, (uint32_t)w, (uint64_t)n)
+               : word(K.pair[i], op_cnt, 3, (uint32_t)w, t1 * (uint64_t)n_h + n) -
+                     word(K.pair[i], op_cnt, 3, (uint32_t)w, t0 * (uint64_t)n_h + n);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) S[c * Sstride + (uint64_t)n * (W + 1) + w] += F[c] - F[(c + 2) % 3];
 }
 
-// Node block size: the (node, column-pair) items of a block should fill the
-// 256 threads (<= CNT_ITEMS each) with as little idle as possible.
-int choose_node_block(int n_h, int WP) {
-  int best = 1;
-  double best_eff = -1.0;
-  for (int nb = 1; nb <= std::min(n_h, 64); ++nb) {
-    const int P = nb * WP;
-    if (P > CNT_ITEMS * CNT_TPB) break;
-    double eff;
-    if (P >= CNT_TPB) {
-      const int per = (P + CNT_TPB - 1) / CNT_TPB;
-      eff = (double)P / (double)(per * CNT_TPB);
-    } else {
-      eff = (double)(P * (CNT_TPB / P)) / CNT_TPB;
-    }
-    if (eff > best_eff + 1e-9 || (eff > best_eff - 1e-9 && nb > best)) {
-      best_eff = eff;
-      best = nb;
-    }
-  }
-  return best;
-}
-
-int launch_count(CountArgs ca, cudaStream_t s, int num_sms) {
-  const int nf = ca.nf, W = 2 * nf + 1, WP = nf + 1;
-  ca.nb = choose_node_block(ca.n_h, WP);
-  ca.ts = std::max(32, std::min(256, ((CNT_TPB + ca.nb - 1) / ca.nb + 31) / 32 * 32));  // >= 256 phase-A lanes
-  const unsigned gy = (unsigned)((ca.n_h + ca.nb - 1) / ca.nb);
+template <int CNT_CB, int CNT_MINB>
+int launch_count_t(CountArgs ca, cudaStream_t s, int num_sms) {
+  const int nf = ca.nf, W = 2 * nf + 1;
+  ca.wc = (W + 1 + CNT_CB - 1) / CNT_CB * CNT_CB;
+  const int CT = ca.wc / CNT_CB;
+  // node block: as many nodes as keep the (node pair, column tile) items <= one CTA
+  const int nb_max = std::max(CNT_NA, (CNT_TPB / CT) * CNT_NA);
+  const int nblk = (ca.n_h + nb_max - 1) / nb_max;
+  ca.nb = (ca.n_h + nblk - 1) / nblk;
+  const int NBP = (ca.nb + 1) & ~1;
+  // tile: >= 256 phase-A lanes when the node block is small, within ~100 KB of smem
+  const int per_sample = 3 * (ca.wc + NBP + 1);
+  int ts = std::max(32, std::min(128, ((CNT_TPB + ca.nb - 1) / ca.nb + 15) / 16 * 16));
+  while (ts > 32 && ts * per_sample * 8 > 100 * 1024) ts -= 16;
+  ca.ts = ts;
+  const int P = (NBP / CNT_NA) * CT, R = std::max(1, CNT_TPB / P);
   const uint64_t tiles = (ca.N + ca.ts - 1) / ca.ts;
-  const uint64_t target = std::max<uint64_t>(1, (uint64_t)num_sms * CNT_MINB * 2 / gy);
+  const uint64_t target = std::max<uint64_t>(1, (uint64_t)num_sms * CNT_MINB / nblk);
   const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>(tiles, target));
   ca.tiles_per_cta = (int)((tiles + gx - 1) / gx);
   const unsigned gxx = (unsigned)((tiles + ca.tiles_per_cta - 1) / ca.tiles_per_cta);
-  const int smem = (int)sizeof(uint64_t) * (std::max(3 * ca.ts * ca.nb, 6 * CNT_TPB) + 3 * ca.nb);
-  if (smem > 48 * 1024) GT_CUDA_CHECK(cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_count<<<dim3(gxx, gy), CNT_TPB, smem, s>>>(ca);
+  const int words = std::max(3 * ca.ts * ca.wc, R * P * 3 * CNT_NA * CNT_CB) + 3 * ca.ts * NBP + 3 * ca.ts + 3 * NBP;
+  const int smem = (int)sizeof(uint64_t) * words;
+  if (smem > 48 * 1024) GT_CUDA_CHECK(cudaFuncSetAttribute(k_count<CNT_CB, CNT_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k_count<CNT_CB, CNT_MINB><<<dim3(gxx, (unsigned)nblk), CNT_TPB, smem, s>>>(ca);
   GT_LAUNCH_CHECK("k_count");
   return GT_OK;
+}
+
+// column tile x occupancy variant (GT_COUNT_VARIANT picks one for tuning runs)
+int launch_count(const CountArgs& ca, cudaStream_t s, int num_sms) {
+  static const int variant = [] {
+    const char* e = getenv("GT_COUNT_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  switch (variant) {
+    case 1: return launch_count_t<2, 2>(ca, s, num_sms);
+    case 2: return launch_count_t<4, 2>(ca, s, num_sms);
+    default: return launch_count_t<4, 1>(ca, s, num_sms);
+  }
 }
 
 int counter_shift(uint64_t n, int score_width, int tau) {  // train.py:189-192
@@ -924,14 +947,15 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
       ca.K = K;
       ca.op_leaf = op_id(level, SITE_ISLEAF);
       ca.op_cnt = op_id(level, SITE_COUNT);
-      ca.dot = c.count_reshare == 1;
       P.start();
       int rc = launch_count(ca, s, num_sms);
       if (rc) return rc;
       P.stop(Prof::COUNT);
     }
-    if (c.count_reshare == 1 && c.sample_base == 0) {
-      k_count_alpha<<<n_h, 64, 0, s>>>(S, n_h, c.nf, K, op_id(level, SITE_COUNT));
+    if (c.count_reshare == 0 ? N > 0 : c.sample_base == 0) {
+      const int cells = n_h * (int)W;
+      k_count_alpha<<<(cells + 127) / 128, 128, 0, s>>>(S, n_h, c.nf, K, op_id(level, SITE_COUNT), c.count_reshare,
+                                                       c.sample_base, c.sample_base + N);
       GT_LAUNCH_CHECK("k_count_alpha");
       P.count_launch();
     }

@@ -30,6 +30,14 @@ tr = DeviceTrainer(48842, 13, TrainConfig(depth=7))
 X = to_device(share(data[:, :-1], rng)); Y = to_device(share(data[:, -1], rng))
 fill = to_device(filler_values(setup.filler_seed, 127, 14))
 print("C2 train ms (min, med):", timed(lambda: tr.run(X, Y, fill, keys)), flush=True)
+from paper_2305_00645_b200 import _native as _nv
+pr = _nv.gt_train_profile()
+tr.run(X, Y, fill, keys, profile=pr); torch.cuda.synchronize()
+print("C2 per-kernel ms:", {k: round(getattr(pr, "ms_" + k), 4) for k in ("prods", "partition", "count", "node_hc", "node_finish")}, flush=True)
+tr_dot = DeviceTrainer(48842, 13, TrainConfig(depth=7, count_reshare="dot"))
+print("C2 dot ms (min, med):", timed(lambda: tr_dot.run(X, Y, fill, keys)), flush=True)
+if os.environ.get("QT_TRAIN_ONLY"):
+    sys.exit(0)
 for depth, nf, n in ((7, 13, 10_000), (10, 32, 1_000_000)):
     T = to_device(share(rng.integers(0, nf, (1 << depth) - 1), rng)); Q = to_device(share(rng.integers(0, 2, (n, nf)), rng))
     ms = timed(lambda: infer_device(T, depth, Q, keys))
