@@ -62,15 +62,26 @@ __global__ void k_init(uint64_t* f, uint64_t* gam, uint64_t* cst, uint64_t fstri
     for (int c = 0; c < 3; ++c) cst[c * cstride + e] = 0;
 }
 
-__global__ void k_prods(const uint64_t* X, const uint64_t* Y, uint64_t* P, uint64_t N, int nf, uint64_t base, Keys K,
-                        uint32_t op) {
-  // prods = mul(features, labels[:, None])                     train.py:229-230
-  uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  uint64_t total = N * (uint64_t)nf;
+// count:0 prods = mul(features, labels[:, None])               train.py:229-230
+// written straight into the level-invariant sample-column matrix the count
+// contraction streams: cols[c][s][0..WC) = x | x*y | y | 0 (mask) | 0 (pad)
+// (sample_cols, train.py:231-233).  One thread per (sample, column slot).
+__global__ void k_prods(const uint64_t* X, const uint64_t* Y, uint64_t* cols, uint64_t N, int nf, int WC,
+                        uint64_t base, Keys K, uint32_t op) {
+  const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t total = N * (uint64_t)WC, nfx = N * (uint64_t)nf;
   if (e >= total) return;
-  uint64_t s = e / nf;
-  uint32_t f = (uint32_t)(e % nf);
-  st3s(P, total, e, mul<64>(K, op, 0, f, base + s, ld3s(X, total, e), ld3s(Y, N, s)));
+  const uint64_t s = e / WC;
+  const int w = (int)(e % WC);
+  A3 v = a3(0, 0, 0);
+  if (w < nf) {
+    v = ld3s(X, nfx, s * nf + w);
+  } else if (w < 2 * nf) {
+    v = mul<64>(K, op, 0, (uint32_t)(w - nf), base + s, ld3s(X, nfx, s * nf + (w - nf)), ld3s(Y, N, s));
+  } else if (w == 2 * nf) {
+    v = ld3s(Y, N, s);
+  }
+  st3s(cols, total, e, v);
 }
 
 // ---------------------------------------------------------------------------
@@ -110,58 +121,149 @@ __global__ void k_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T
 // ---------------------------------------------------------------------------
 
 constexpr int CNT_TPB = 256;
-constexpr int CNT_NA = 2;  // nodes per phase-B thread tile
+constexpr int CNT_NA = 2;  // nodes per contraction thread tile
+constexpr int CNT_CB = 4;  // columns per contraction thread tile
 
-struct CountArgs {
-  const uint64_t *X, *P, *Y, *midx, *f;
-  uint64_t* S;  // [3][n_h][W+1]
-  uint64_t N, base;
-  int nf, n_h, off, nb, ts, tiles_per_cta, wc;
+// is_leaf = eq(F_level, LEAF) per node (train.py:320) -> leaf[3][n_h] bits
+__global__ void k_count_leaf(const uint64_t* f, uint64_t* leaf, int n_h, Keys K, uint32_t op_leaf) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= n_h) return;
+  const B3 z = eqz<64>(K, op_leaf, 0, (uint64_t)n, add_pub<64>(ld3s(f, n_h, n), 0ull - F_LEAF));
+#pragma unroll
+  for (int c = 0; c < 3; ++c) leaf[c * n_h + n] = z.v[c] & 1ull;
+}
+
+struct LaneArgs {
+  const uint64_t *midx, *leaf;
+  uint64_t* la;                   // [3][nblk][cap][nbp]: node-block-major, so a contraction tile is contiguous
+  uint64_t N, s0, cn, cap, base;  // shard samples, chunk start, chunk samples, chunk capacity, shard base
+  int n_h, off, nb, nbp, nblk;
   Keys K;
-  uint32_t op_leaf, op_cnt;
+  uint32_t op_cnt;
 };
 
-// One CTA = (sample range, node block of nb nodes).  Per tile of TS samples:
-//  staging  the tile's sample columns x[c][s][w] (features, prods, label;
-//           the mask column and the padding stay 0) and node indices -> smem
-//           with coalesced row loads;
-//  phase A  one lane per (sample, node):  la = b2a(eq(m_idx, off+n) & leaf[n])
-//           from the six Philox blocks of LaneRand at sub 0 (pair block half b
-//           bit 0 = the AND gate's zero bit)                train.py:328-331
-//  phase B  a register-tiled ring contraction: each thread owns NA nodes x CB
-//           columns x 3 components and accumulates the party-local cross
-//           terms of mul(cols, la) (rss.py:391-395)
-//              acc_i += la_i (x_i + x_{i+1}) + la_{i+1} x_i
-//           over the samples; the mask column (x = 0, u = 1) accumulates la_i
-//           itself (s_mask, train.py:334).                  train.py:332-335
-// The products' reshare zero shares are not drawn here: their per-sample
-// stream telescopes (F(s) = H(s+1) - H(s)), so their sum
-// over the shard is added once per cell by k_count_alpha.
-template <int CNT_CB, int CNT_MINB>
-__global__ void __launch_bounds__(CNT_TPB, CNT_MINB) k_count(CountArgs a) {
-  extern __shared__ __align__(16) uint64_t sm[];
-  const int nf = a.nf, W = 2 * nf + 1, WC = a.wc, NB = a.nb, NBP = (NB + 1) & ~1, TS = a.ts;
-  const int tid = threadIdx.x, bd = blockDim.x;
-  const int n0 = blockIdx.y * NB;
-  const int nb = min(NB, a.n_h - n0);
-  uint64_t* xs = sm;                   // [3][TS][WC]
-  uint64_t* la = xs + 3 * TS * WC;     // [3][TS][NBP]
-  uint64_t* mi = la + 3 * TS * NBP;    // [3][TS]
-  uint64_t* leaf = mi + 3 * TS;        // [3][NBP]
-  const Keys& K = a.K;
-  const uint64_t nfx = a.N * (uint64_t)nf;
-
-  // is_leaf = eq(F_level, LEAF) (train.py:320); identical in every CTA
-  for (int t = tid; t < nb; t += bd) {
-    const B3 z = eqz<64>(K, a.op_leaf, 0, (uint64_t)(n0 + t), add_pub<64>(ld3s(a.f, a.n_h, n0 + t), 0ull - F_LEAF));
-    for (int c = 0; c < 3; ++c) leaf[c * NBP + t] = z.v[c] & 1ull;
+// One thread per (sample, node) lane of a sample chunk:
+//   la = b2a(eq(m_idx, off+n) & is_leaf[n])                 train.py:328-331
+// from the six Philox blocks of LaneRand at sub 0 (pair block half b bit 0 =
+// the AND gate's zero bit).  Padding node slots are written as zero shares.
+__global__ void __launch_bounds__(256) k_count_lanes(LaneArgs a) {
+  const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t per = (uint64_t)a.nblk * a.nbp;
+  if (e >= a.cn * per) return;
+  const uint64_t s = e / per;
+  const int r = (int)(e % per), blk = r / a.nbp, nn = r % a.nbp, n = blk * a.nb + nn;
+  const uint64_t cs = (uint64_t)a.nblk * a.cap * a.nbp;
+  uint64_t* out = a.la + ((uint64_t)blk * a.cap + s) * a.nbp + nn;
+  if (nn >= a.nb || n >= a.n_h) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) out[c * cs] = 0;
+    return;
   }
-  // mask / padding columns and the odd node slot stay zero for the whole kernel
-  for (int e = tid; e < 3 * TS * WC; e += bd) xs[e] = 0;
-  for (int e = tid; e < 3 * TS * NBP; e += bd) la[e] = 0;
+  const uint64_t gs = a.s0 + s;
+  const uint64_t lane = (a.base + gs) * (uint64_t)a.n_h + (uint64_t)n;
+  const A3 d = add_pub<64>(a3(__ldg(a.midx + gs), __ldg(a.midx + a.N + gs), __ldg(a.midx + 2 * a.N + gs)),
+                           0ull - (uint64_t)(a.off + n));
+  const LaneRand Rr = lane_rand(a.K, a.op_cnt, 0, lane);
+  const B3 hit = eq_arith<64>(d, Rr.r, Rr.Rb0, Rr.Rb1, Rr.Zw);
+  B3 lf;
+  uint64_t Z[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    lf.v[c] = __ldg(a.leaf + c * a.n_h + n);
+    Z[c] = Rr.F[c] & 1ull;
+  }
+  const A3 l = b2a_arith<64>(and_z(hit, lf, Z), Rr.A0, Rr.A1, Rr.bits);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) out[c * cs] = l.v[c];
+}
+
+// --- TMA bulk copies (cp.async.bulk) into shared memory, mbarrier completion
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// acc + (x << 32) += a * b (mod 2^64): the low-half product accumulates in
+// 64 bits (IMAD.WIDE.U32 with the accumulator as addend), the two cross
+// products in a separate 32-bit word (the high x high product vanishes mod
+// 2^64); the two are combined once after the sample loop.
+__device__ __forceinline__ void mac64(uint64_t& acc, uint32_t& x, uint64_t a, uint64_t b) {
+  acc += (uint64_t)(uint32_t)a * (uint32_t)b;
+  x += (uint32_t)a * (uint32_t)(b >> 32) + (uint32_t)(a >> 32) * (uint32_t)b;
+}
+
+struct MacArgs {
+  const uint64_t *la, *cols;  // la [3][nblk][cap][nbp] (chunk), cols [3][N][WC] (shard)
+  uint64_t* S;                // [3][n_h][W+1]
+  uint64_t N, s0, cn, cap;
+  int n_h, W, WC, nb, nbp, nblk, ts, tiles_per_cta;
+};
+
+// Count contraction of one sample chunk: each thread owns NA nodes x CB
+// columns x 3 components and accumulates the party-local cross terms of
+// mul(cols, la) (rss.py:391-395)
+//     acc_i += la_i (x_i + x_{i+1}) + la_{i+1} x_i
+// over its samples; the mask column (x = 0, u = 1) accumulates la_i itself
+// (s_mask, train.py:334).  Tiles of TS samples (la rows of the node block and
+// column rows) arrive by cp.async.bulk into a 2-stage ring.  The products'
+// reshare zero shares are not drawn here: their per-sample stream telescopes
+// (F(t) = H(t+1) - H(t)) and k_count_alpha adds the
+// shard's sum once per cell.
+__global__ void __launch_bounds__(CNT_TPB, 1) k_count_mac(MacArgs a) {
+  extern __shared__ __align__(128) uint64_t sm[];
+  __shared__ __align__(8) uint64_t full[2];
+  const int W = a.W, WC = a.WC, NBP = a.nbp, TS = a.ts;
+  const int tid = threadIdx.x;
+  const int blk = blockIdx.y, n0 = blk * a.nb, nb = min(a.nb, a.n_h - n0);
+  const int stage_words = 3 * TS * (NBP + WC);
+  const uint64_t cs_la = (uint64_t)a.nblk * a.cap * NBP, cs_col = a.N * (uint64_t)WC;
+  const uint64_t tile0 = (uint64_t)blockIdx.x * a.tiles_per_cta;
+  const uint64_t ntiles = (a.cn + TS - 1) / TS;
+  const int my_tiles = (int)min((uint64_t)a.tiles_per_cta, ntiles > tile0 ? ntiles - tile0 : 0);
+
+  auto issue = [&](int t) {  // one elected thread: 6 bulk copies of tile t into stage t & 1
+    const uint64_t s0 = (tile0 + t) * (uint64_t)TS;
+    const int cnt = (int)min((uint64_t)TS, a.cn - s0);
+    uint64_t* st = sm + (t & 1) * stage_words;
+    const uint32_t lb = (uint32_t)(cnt * NBP * 8), cb = (uint32_t)(cnt * WC * 8);
+    mbar_expect_tx(&full[t & 1], 3 * (lb + cb));
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      bulk_g2s(st + c * TS * NBP, a.la + c * cs_la + ((uint64_t)blk * a.cap + s0) * NBP, lb, &full[t & 1]);
+      bulk_g2s(st + 3 * TS * NBP + c * TS * WC, a.cols + c * cs_col + (a.s0 + s0) * WC, cb, &full[t & 1]);
+    }
+  };
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (my_tiles > 0) issue(0);
+    if (my_tiles > 1) issue(1);
+  }
 
   const int CT = WC / CNT_CB, P = (NBP / CNT_NA) * CT;
-  const int R = max(1, bd / P);  // replicas split a tile's samples
+  const int R = max(1, CNT_TPB / P);  // replicas split a tile's samples
   const bool active = tid < P * R;
   const int item = active ? tid % P : 0, q = tid / P;
   const int nl = (item / CT) * CNT_NA, cl = (item % CT) * CNT_CB;
@@ -169,72 +271,34 @@ __global__ void __launch_bounds__(CNT_TPB, CNT_MINB) k_count(CountArgs a) {
 #pragma unroll
   for (int j = 0; j < CNT_CB; ++j) mflag[j] = (cl + j == W) ? 1ull : 0ull;
   uint64_t acc[3][CNT_NA][CNT_CB];
+  uint32_t accx[3][CNT_NA][CNT_CB];
 #pragma unroll
   for (int c = 0; c < 3; ++c)
 #pragma unroll
     for (int i = 0; i < CNT_NA; ++i)
 #pragma unroll
-      for (int j = 0; j < CNT_CB; ++j) acc[c][i][j] = 0;
+      for (int j = 0; j < CNT_CB; ++j) acc[c][i][j] = 0, accx[c][i][j] = 0;
 
-  const uint64_t tile0 = (uint64_t)blockIdx.x * a.tiles_per_cta;
-  for (int tt = 0; tt < a.tiles_per_cta; ++tt) {
-    const uint64_t s0 = (tile0 + tt) * (uint64_t)TS;
-    if (s0 >= a.N) break;
-    const int cnt = (int)min((uint64_t)TS, a.N - s0);
-    __syncthreads();
-    // staging: X / prods rows are contiguous per component (sample_cols, train.py:231-233)
-    for (int e = tid; e < cnt * nf; e += bd) {
-      const int s = e / nf, f = e % nf;
-      const uint64_t g = (s0 + s) * (uint64_t)nf + f;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        xs[(c * TS + s) * WC + f] = __ldg(a.X + c * nfx + g);
-        xs[(c * TS + s) * WC + nf + f] = __ldg(a.P + c * nfx + g);
-      }
-    }
-    for (int s = tid; s < cnt; s += bd)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        xs[(c * TS + s) * WC + 2 * nf] = __ldg(a.Y + c * a.N + s0 + s);
-        mi[c * TS + s] = __ldg(a.midx + c * a.N + s0 + s);
-      }
-    __syncthreads();
-    // phase A                                             train.py:328-331
-    for (int e = tid; e < cnt * nb; e += bd) {
-      const int s = e / nb, nn = e % nb;
-      const uint64_t lane = (a.base + s0 + s) * (uint64_t)a.n_h + (uint64_t)(n0 + nn);
-      const A3 d = add_pub<64>(a3(mi[s], mi[TS + s], mi[2 * TS + s]), 0ull - (uint64_t)(a.off + n0 + nn));
-      const LaneRand Rr = lane_rand(K, a.op_cnt, 0, lane);
-      const B3 hit = eq_arith<64>(d, Rr.r, Rr.Rb0, Rr.Rb1, Rr.Zw);
-      B3 lf;
-      uint64_t Z[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        lf.v[c] = leaf[c * NBP + nn];
-        Z[c] = Rr.F[c] & 1ull;
-      }
-      const B3 lcf = and_z(hit, lf, Z);
-      const A3 l = b2a_arith<64>(lcf, Rr.A0, Rr.A1, Rr.bits);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) la[(c * TS + s) * NBP + nn] = l.v[c];
-    }
-    __syncthreads();
-    // phase B: sum_s mul(cols, la) cross terms            train.py:332-335
+  for (int t = 0; t < my_tiles; ++t) {
+    const int cnt = (int)min((uint64_t)TS, a.cn - (tile0 + t) * (uint64_t)TS);
+    mbar_wait(&full[t & 1], (uint32_t)((t >> 1) & 1));
+    const uint64_t* lat = sm + (t & 1) * stage_words;
+    const uint64_t* xst = lat + 3 * TS * NBP;
     if (active) {
 #pragma unroll 2
       for (int s = q; s < cnt; s += R) {
         uint64_t l[3][CNT_NA], x[3][CNT_CB];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const ulonglong2 lv = *reinterpret_cast<const ulonglong2*>(la + (c * TS + s) * NBP + nl);
+          const ulonglong2 lv = *reinterpret_cast<const ulonglong2*>(lat + (c * TS + s) * NBP + nl);
           l[c][0] = lv.x;
           l[c][1] = lv.y;
-          const ulonglong2 x01 = *reinterpret_cast<const ulonglong2*>(xs + (c * TS + s) * WC + cl);
-          const ulonglong2 x23 = *reinterpret_cast<const ulonglong2*>(xs + (c * TS + s) * WC + cl + 2);
-          x[c][0] = x01.x;
-          x[c][1] = x01.y;
-          x[c][2] = x23.x;
-          x[c][3] = x23.y;
+#pragma unroll
+          for (int j = 0; j < CNT_CB; j += 2) {
+            const ulonglong2 xv = *reinterpret_cast<const ulonglong2*>(xst + (c * TS + s) * WC + cl + j);
+            x[c][j] = xv.x;
+            x[c][j + 1] = xv.y;
+          }
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -243,23 +307,33 @@ __global__ void __launch_bounds__(CNT_TPB, CNT_MINB) k_count(CountArgs a) {
           for (int j = 0; j < CNT_CB; ++j) {
             const uint64_t u = x[c][j] + x[cn][j] + mflag[j];
 #pragma unroll
-            for (int i = 0; i < CNT_NA; ++i) acc[c][i][j] += l[c][i] * u + l[cn][i] * x[c][j];
+            for (int i = 0; i < CNT_NA; ++i) {
+              mac64(acc[c][i][j], accx[c][i][j], l[c][i], u);
+              mac64(acc[c][i][j], accx[c][i][j], l[cn][i], x[c][j]);
+            }
           }
         }
       }
     }
+    __syncthreads();  // stage t & 1 consumed
+    if (tid == 0 && t + 2 < my_tiles) issue(t + 2);
   }
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int i = 0; i < CNT_NA; ++i)
+#pragma unroll
+      for (int j = 0; j < CNT_CB; ++j) acc[c][i][j] += (uint64_t)accx[c][i][j] << 32;
   // replicas of an item meet in shared memory; one atomic per (cell, component) per CTA
   constexpr int NACC = 3 * CNT_NA * CNT_CB;
   if (R > 1) {
-    __syncthreads();  // xs is dead: reuse it as [R][P][NACC] scratch
     if (active)
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int i = 0; i < CNT_NA; ++i)
 #pragma unroll
-          for (int j = 0; j < CNT_CB; ++j) xs[((uint64_t)q * P + item) * NACC + (c * CNT_NA + i) * CNT_CB + j] = acc[c][i][j];
+          for (int j = 0; j < CNT_CB; ++j) sm[((uint64_t)q * P + item) * NACC + (c * CNT_NA + i) * CNT_CB + j] = acc[c][i][j];
     __syncthreads();
     if (active && q == 0)
       for (int r = 1; r < R; ++r)
@@ -268,9 +342,9 @@ __global__ void __launch_bounds__(CNT_TPB, CNT_MINB) k_count(CountArgs a) {
 #pragma unroll
           for (int i = 0; i < CNT_NA; ++i)
 #pragma unroll
-            for (int j = 0; j < CNT_CB; ++j) acc[c][i][j] += xs[((uint64_t)r * P + item) * NACC + (c * CNT_NA + i) * CNT_CB + j];
+            for (int j = 0; j < CNT_CB; ++j) acc[c][i][j] += sm[((uint64_t)r * P + item) * NACC + (c * CNT_NA + i) * CNT_CB + j];
   }
-  if (!active || q != 0) return;
+  if (!active || q != 0 || my_tiles == 0) return;
   const uint64_t Sstride = (uint64_t)a.n_h * (W + 1);
 #pragma unroll
   for (int i = 0; i < CNT_NA; ++i) {
@@ -623,8 +697,40 @@ __global__ void __launch_bounds__(128) k_node_finish(FinishArgs a) {
 // workspace
 // ---------------------------------------------------------------------------
 
+// Node blocking, chunking and tiling of one level's count (shared by the
+// workspace layout and the launches).
+struct CountPlan {
+  int W, WC, CT, nb, nbp, nblk, ts, R, P;
+};
+CountPlan count_plan(int nf, int n_h) {
+  CountPlan p;
+  p.W = 2 * nf + 1;
+  p.WC = (p.W + 1 + CNT_CB - 1) / CNT_CB * CNT_CB;
+  p.CT = p.WC / CNT_CB;
+  // node block: as many nodes as keep the (node pair, column tile) items <= one CTA
+  const int nb_max = std::max(CNT_NA, (CNT_TPB / p.CT) * CNT_NA);
+  p.nblk = (n_h + nb_max - 1) / nb_max;
+  p.nb = (n_h + p.nblk - 1) / p.nblk;
+  p.nbp = (p.nb + 1) & ~1;
+  p.P = (p.nbp / CNT_NA) * p.CT;
+  p.R = std::max(1, CNT_TPB / p.P);
+  // tile: ~8 samples per replica, two stages within ~200 KB of shared memory
+  int ts = std::max(32, std::min(256, (8 * p.R + 7) / 8 * 8));
+  while (ts > 8 && 2 * 3 * ts * (p.nbp + p.WC) * 8 > 200 * 1024) ts -= 8;
+  p.ts = ts;
+  return p;
+}
+// la chunk capacity (words): keeps a chunk's lanes L2-resident between the
+// lane and contraction kernels, but never below 4096 samples per chunk
+uint64_t la_words(uint64_t N, int nf, int depth) {
+  const CountPlan p = count_plan(nf, 1 << (depth - 1));
+  const uint64_t per = 3ull * p.nblk * p.nbp;
+  const uint64_t want = std::max<uint64_t>(8ull << 20, per * 4096);
+  return std::min<uint64_t>(want, per * std::max<uint64_t>(N, 1));
+}
+
 struct Layout {
-  uint64_t prods, midx, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
+  uint64_t cols, la, leaf, midx, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
 };
 
 Layout layout(const gt_train_cfg& c) {
@@ -637,7 +743,9 @@ Layout layout(const gt_train_cfg& c) {
     o += (words + 31) & ~31ull;  // 256-byte alignment
     return r;
   };
-  L.prods = take(3 * N * nf);
+  L.cols = take(3 * N * (uint64_t)count_plan(c.nf, 1).WC);
+  L.la = take(la_words(N, c.nf, c.depth));
+  L.leaf = take(3 * nmax);
   L.midx = take(3 * N);
   L.S = take(3 * nmax * (W + 1));
   for (int i = 0; i < 2; ++i) {
@@ -796,46 +904,73 @@ __global__ void k_count_alpha(uint64_t* S, int n_h, int nf, Keys K, uint32_t op_
   for (int c = 0; c < 3; ++c) S[c * Sstride + (uint64_t)n * (W + 1) + w] += F[c] - F[(c + 2) % 3];
 }
 
-template <int CNT_CB, int CNT_MINB>
-int launch_count_t(CountArgs ca, cudaStream_t s, int num_sms) {
-  const int nf = ca.nf, W = 2 * nf + 1;
-  ca.wc = (W + 1 + CNT_CB - 1) / CNT_CB * CNT_CB;
-  const int CT = ca.wc / CNT_CB;
-  // node block: as many nodes as keep the (node pair, column tile) items <= one CTA
-  const int nb_max = std::max(CNT_NA, (CNT_TPB / CT) * CNT_NA);
-  const int nblk = (ca.n_h + nb_max - 1) / nb_max;
-  ca.nb = (ca.n_h + nblk - 1) / nblk;
-  const int NBP = (ca.nb + 1) & ~1;
-  // tile: >= 256 phase-A lanes when the node block is small, within ~100 KB of smem
-  const int per_sample = 3 * (ca.wc + NBP + 1);
-  int ts = std::max(32, std::min(128, ((CNT_TPB + ca.nb - 1) / ca.nb + 15) / 16 * 16));
-  while (ts > 32 && ts * per_sample * 8 > 100 * 1024) ts -= 16;
-  ca.ts = ts;
-  const int P = (NBP / CNT_NA) * CT, R = std::max(1, CNT_TPB / P);
-  const uint64_t tiles = (ca.N + ca.ts - 1) / ca.ts;
-  const uint64_t target = std::max<uint64_t>(1, (uint64_t)num_sms * CNT_MINB / nblk);
-  const uint64_t gx = std::max<uint64_t>(1, std::min<uint64_t>(tiles, target));
-  ca.tiles_per_cta = (int)((tiles + gx - 1) / gx);
-  const unsigned gxx = (unsigned)((tiles + ca.tiles_per_cta - 1) / ca.tiles_per_cta);
-  const int words = std::max(3 * ca.ts * ca.wc, R * P * 3 * CNT_NA * CNT_CB) + 3 * ca.ts * NBP + 3 * ca.ts + 3 * NBP;
-  const int smem = (int)sizeof(uint64_t) * words;
-  if (smem > 48 * 1024) GT_CUDA_CHECK(cudaFuncSetAttribute(k_count<CNT_CB, CNT_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_count<CNT_CB, CNT_MINB><<<dim3(gxx, (unsigned)nblk), CNT_TPB, smem, s>>>(ca);
-  GT_LAUNCH_CHECK("k_count");
-  return GT_OK;
-}
+struct CountLaunch {
+  const uint64_t *midx, *f, *cols;
+  uint64_t *la, *leaf, *S;
+  uint64_t la_cap_words, N, base;
+  int nf, n_h;
+  Keys K;
+  int level;
+};
 
-// column tile x occupancy variant (GT_COUNT_VARIANT picks one for tuning runs)
-int launch_count(const CountArgs& ca, cudaStream_t s, int num_sms) {
-  static const int variant = [] {
-    const char* e = getenv("GT_COUNT_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  switch (variant) {
-    case 1: return launch_count_t<2, 2>(ca, s, num_sms);
-    case 2: return launch_count_t<4, 2>(ca, s, num_sms);
-    default: return launch_count_t<4, 1>(ca, s, num_sms);
+// leaf + per chunk (lanes, contraction); returns the number of launches
+int launch_count(const CountLaunch& c, cudaStream_t s, int num_sms, int* launches) {
+  const CountPlan p = count_plan(c.nf, c.n_h);
+  k_count_leaf<<<(c.n_h + 127) / 128, 128, 0, s>>>(c.f, c.leaf, c.n_h, c.K, op_id(c.level, SITE_ISLEAF));
+  GT_LAUNCH_CHECK("k_count_leaf");
+  int nl = 1;
+  const uint64_t per = 3ull * p.nblk * p.nbp;
+  const uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(c.N, c.la_cap_words / per));
+  const int stage_words = 3 * p.ts * (p.nbp + p.WC);
+  const int smem = (int)sizeof(uint64_t) * std::max(2 * stage_words, p.R * p.P * 3 * CNT_NA * CNT_CB);
+  if (smem > 48 * 1024)
+    GT_CUDA_CHECK(cudaFuncSetAttribute(k_count_mac, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  for (uint64_t s0 = 0; s0 < c.N; s0 += cap) {
+    const uint64_t cn = std::min<uint64_t>(cap, c.N - s0);
+    LaneArgs la{};
+    la.midx = c.midx;
+    la.leaf = c.leaf;
+    la.la = c.la;
+    la.N = c.N;
+    la.s0 = s0;
+    la.cn = cn;
+    la.cap = cap;
+    la.base = c.base;
+    la.n_h = c.n_h;
+    la.off = c.n_h - 1;
+    la.nb = p.nb;
+    la.nbp = p.nbp;
+    la.nblk = p.nblk;
+    la.K = c.K;
+    la.op_cnt = op_id(c.level, SITE_COUNT);
+    const uint64_t lanes = cn * p.nblk * p.nbp;
+    k_count_lanes<<<(unsigned)((lanes + 255) / 256), 256, 0, s>>>(la);
+    GT_LAUNCH_CHECK("k_count_lanes");
+    MacArgs ma{};
+    ma.la = c.la;
+    ma.cols = c.cols;
+    ma.S = c.S;
+    ma.N = c.N;
+    ma.s0 = s0;
+    ma.cn = cn;
+    ma.cap = cap;
+    ma.n_h = c.n_h;
+    ma.W = p.W;
+    ma.WC = p.WC;
+    ma.nb = p.nb;
+    ma.nbp = p.nbp;
+    ma.nblk = p.nblk;
+    ma.ts = p.ts;
+    const uint64_t tiles = (cn + p.ts - 1) / p.ts;
+    const uint64_t gx0 = std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)std::max(1, num_sms / p.nblk)));
+    ma.tiles_per_cta = (int)((tiles + gx0 - 1) / gx0);
+    const unsigned gx = (unsigned)((tiles + ma.tiles_per_cta - 1) / ma.tiles_per_cta);
+    k_count_mac<<<dim3(gx, (unsigned)p.nblk), CNT_TPB, smem, s>>>(ma);
+    GT_LAUNCH_CHECK("k_count_mac");
+    nl += 2;
   }
+  *launches = nl;
+  return GT_OK;
 }
 
 int counter_shift(uint64_t n, int score_width, int tau) {  // train.py:189-192
@@ -900,7 +1035,7 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
   const uint64_t N = c.n_local, nf = (uint64_t)c.nf, cols = 2 * nf, W = cols + 1;
   const uint64_t slots = (1ull << c.depth) - 1;
   const int shift = counter_shift(c.n_total, c.score_width, c.tau);
-  uint64_t *prods = ws + L.prods, *midx = ws + L.midx, *S = ws + L.S, *hc = ws + L.hc;
+  uint64_t *colm = ws + L.cols, *midx = ws + L.midx, *S = ws + L.S, *hc = ws + L.hc;
   uint64_t *f[2] = {ws + L.f[0], ws + L.f[1]}, *gam[2] = {ws + L.gam[0], ws + L.gam[1]};
   uint64_t *cst[2] = {ws + L.cst[0], ws + L.cst[1]}, *ceff[2] = {ws + L.ceff[0], ws + L.ceff[1]};
   int cur = 0;
@@ -913,9 +1048,10 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
   GT_LAUNCH_CHECK("k_init");
   P.count_launch();
   if (N) {
-    const uint64_t tot = N * nf;
+    const int WC = count_plan(c.nf, 1).WC;
+    const uint64_t tot = N * (uint64_t)WC;
     P.start();
-    k_prods<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(features, labels, prods, N, c.nf, c.sample_base, K,
+    k_prods<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(features, labels, colm, N, c.nf, WC, c.sample_base, K,
                                                           op_id(0, SITE_PRODS));
     GT_LAUNCH_CHECK("k_prods");
     P.stop(Prof::PRODS);
@@ -932,25 +1068,26 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
     const uint64_t swords = 3ull * n_h * (W + 1);
     GT_CUDA_CHECK(cudaMemsetAsync(S, 0, swords * sizeof(uint64_t), s));
     if (N) {
-      CountArgs ca{};
-      ca.X = features;
-      ca.P = prods;
-      ca.Y = labels;
-      ca.midx = midx;
-      ca.f = f[cur];
-      ca.S = S;
-      ca.N = N;
-      ca.base = c.sample_base;
-      ca.nf = c.nf;
-      ca.n_h = n_h;
-      ca.off = n_h - 1;
-      ca.K = K;
-      ca.op_leaf = op_id(level, SITE_ISLEAF);
-      ca.op_cnt = op_id(level, SITE_COUNT);
+      CountLaunch cl{};
+      cl.midx = midx;
+      cl.f = f[cur];
+      cl.cols = colm;
+      cl.la = ws + L.la;
+      cl.leaf = ws + L.leaf;
+      cl.S = S;
+      cl.la_cap_words = la_words(N, c.nf, c.depth);
+      cl.N = N;
+      cl.base = c.sample_base;
+      cl.nf = c.nf;
+      cl.n_h = n_h;
+      cl.K = K;
+      cl.level = level;
+      int nl = 0;
       P.start();
-      int rc = launch_count(ca, s, num_sms);
+      int rc = launch_count(cl, s, num_sms, &nl);
       if (rc) return rc;
       P.stop(Prof::COUNT);
+      for (int i = 1; i < nl; ++i) P.count_launch();
     }
     if (c.count_reshare == 0 ? N > 0 : c.sample_base == 0) {
       const int cells = n_h * (int)W;
