@@ -105,7 +105,9 @@ typedef struct {
                             local products are summed over samples first and each counter
                             cell is reshared once (same revealed tree, n_h*W instead of
                             N*n_h*W reshared words per level) */
-  int32_t reserved;
+  int32_t count_engine;  /* count contraction: 0 = tensor cores (tcgen05.mma kind::i8 over
+                            INT8 limbs of the Z_2^64 shares), 1 = CUDA cores (64-bit IMAD) --
+                            identical shares */
 } gt_train_cfg;
 
 /* Sum-allreduce of `count` uint64 words in place (count partials of one

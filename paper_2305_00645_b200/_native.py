@@ -44,7 +44,7 @@ class gt_train_cfg(ctypes.Structure):
         ("n_local", ctypes.c_uint64),
         ("sample_base", ctypes.c_uint64),
         ("count_reshare", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("count_engine", ctypes.c_int32),
     ]
 
 

@@ -1,0 +1,300 @@
+// Tensor-core count contraction (count_engine 0): tcgen05.mma kind::i8 over
+// an INT8 limb decomposition of the Z_2^64 share products.
+//
+// The count contraction of one level (_count_level, reference
+// pkg/src/obtree/train.py:315-343) is, per share component i, the ring GEMM
+//     S_i[n][w] = sum_s la_i[s][n] u_i[s][w] + la_{i+1}[s][n] x_i[s][w]
+// (the party-local cross terms of mul(cols, la), rss.py:391-395, with
+// u_i = x_i + x_{i+1}; the mask column has u = 1, x = 0).  Writing every u64
+// as 8 unsigned bytes, a * b mod 2^64 = sum_{p+q<=7} a_p b_q 2^{8(p+q)}, so
+// with rows (node n, limb p) and columns (column w, limb q)
+//     D[(n,p)][(w,q)] = sum_s la_p u_q + la'_p x_q         (u8 x u8 -> s32)
+//     S[n][w]         = sum_{p+q<=7} D[(n,p)][(w,q)] << 8(p+q)   (mod 2^64)
+// D is one UMMA accumulator (M = 128 rows = 16 nodes x 8 limbs, N = 8 x
+// columns of the block, K = 2 x samples: the two terms are consecutive K
+// blocks).  Each CTA sums at most 2 x 16 512 samples, so every D entry stays
+// below 2^31 (exact in the s32 accumulator whether it wraps or saturates).
+//
+// Operands are staged by cp.async.bulk in the canonical K-major
+// SWIZZLE_NONE core-matrix layout (8 rows x 16 bytes = 128 contiguous bytes;
+// SBO = 128 B between 8-row groups, LBO between the 16-byte K chunks), which
+// the producer kernels write directly, so one block of 128 samples of an
+// operand is one contiguous bulk copy.
+#pragma once
+
+namespace gt {
+namespace {
+
+constexpr int TC_KB = 128;                // samples per K block
+constexpr int TC_STAGES = 4;              // smem ring depth
+constexpr int TC_ABLK = TC_KB * 128;      // bytes of an A block: 128 rows (16 nodes x 8 limbs) x 128 samples
+constexpr int TC_MAX_KB_PER_CTA = 64;     // 2 x 64 x 128 x 255^2 < 2^31
+constexpr int TC_TMEM_COLS = 256;
+
+struct TcPlan {
+  int CW;      // sample columns incl. the mask column (W + 1)
+  int nbn;     // column blocks
+  int cpb;     // columns per block (even)
+  int N;       // UMMA N = 8 * cpb (multiple of 16, <= 256)
+  int mtiles;  // 16-node M tiles
+  int BB;      // bytes of a B block (N rows x 128 samples)
+};
+inline TcPlan tc_plan(int nf, int n_h) {
+  TcPlan p;
+  p.CW = 2 * nf + 2;
+  p.nbn = (p.CW + 31) / 32;
+  p.cpb = (p.CW + p.nbn - 1) / p.nbn;
+  p.cpb += p.cpb & 1;
+  p.N = 8 * p.cpb;
+  p.mtiles = (n_h + 15) / 16;
+  p.BB = p.N * TC_KB;
+  return p;
+}
+
+// --- B operand: the level-invariant sample columns as byte planes
+// B8[c][term][nb][kb][kc 8][g cpb][q 8][16 samples]; term 0 = u_c, term 1 = x_c.
+struct Cols8Args {
+  const uint64_t* cols;  // [3][N][WC] u64 (x | prods | y | 0 ...)
+  uint8_t* B8;
+  uint64_t N, nkb;
+  int WC, W, cpb, nbn;
+};
+__global__ void __launch_bounds__(256) k_cols8(Cols8Args a) {
+  const int WG = a.nbn * a.cpb;
+  const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t total = 6ull * a.nkb * 8 * WG;
+  if (e >= total) return;
+  const int wg = (int)(e % WG);
+  uint64_t r = e / WG;
+  const int kc = (int)(r % 8);
+  r /= 8;
+  const uint64_t kb = r % a.nkb;
+  r /= a.nkb;
+  const int term = (int)(r % 2), c = (int)(r / 2);
+  const int nb = wg / a.cpb, g = wg % a.cpb, w = wg;
+  const uint64_t cs = a.N * (uint64_t)a.WC;
+  uint32_t pk[8][4];
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) pk[q][k] = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint64_t s = kb * TC_KB + kc * 16 + i;
+    uint64_t v = 0;
+    if (s < a.N) {
+      if (w < a.W) {
+        const uint64_t xc = __ldg(a.cols + c * cs + s * a.WC + w);
+        v = term ? xc : xc + __ldg(a.cols + ((c + 1) % 3) * cs + s * a.WC + w);
+      } else if (w == a.W) {
+        v = term ? 0ull : 1ull;  // mask column: s_mask += la (train.py:334)
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) pk[q][i >> 2] |= (uint32_t)((v >> (8 * q)) & 0xffu) << (8 * (i & 3));
+  }
+  uint8_t* dst = a.B8 + ((((uint64_t)(c * 2 + term) * a.nbn + nb) * a.nkb + kb) * (uint64_t)(8 * a.cpb * TC_KB)) +
+                 ((uint64_t)kc * a.cpb + g) * 128;
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    *reinterpret_cast<uint4*>(dst + q * 16) = make_uint4(pk[q][0], pk[q][1], pk[q][2], pk[q][3]);
+}
+
+// --- A operand: one CTA per (128-sample block, 16-node M tile) of a chunk;
+// lanes la = b2a(eq(m_idx, off+n) & is_leaf[n]) as in k_count_lanes, written
+// as byte planes la8[c][mt][kbc][kc 8][g 16][p 8][16] through shared memory
+// and a bulk store.
+struct Lanes8Args {
+  const uint64_t *midx, *leaf;
+  uint8_t* la8;
+  uint64_t N, s0, cn, base, nkbc;  // nkbc = chunk capacity in K blocks
+  int n_h, off, mtiles;
+  Keys K;
+  uint32_t op_cnt;
+};
+__global__ void __launch_bounds__(256) k_count_lanes8(Lanes8Args a) {
+  __shared__ __align__(128) uint8_t sb[3 * TC_ABLK];
+  const int kb = blockIdx.x, mt = blockIdx.y, tid = threadIdx.x;
+  for (int e = tid; e < 16 * TC_KB; e += blockDim.x) {
+    const int nn = e / TC_KB, ss = e % TC_KB;
+    const int n = mt * 16 + nn;
+    const uint64_t s = (uint64_t)kb * TC_KB + ss;
+    A3 l = a3(0, 0, 0);
+    if (n < a.n_h && s < a.cn) {
+      const uint64_t gs = a.s0 + s;
+      const uint64_t lane = (a.base + gs) * (uint64_t)a.n_h + (uint64_t)n;
+      const A3 d = add_pub<64>(a3(__ldg(a.midx + gs), __ldg(a.midx + a.N + gs), __ldg(a.midx + 2 * a.N + gs)),
+                               0ull - (uint64_t)(a.off + n));
+      const LaneRand Rr = lane_rand(a.K, a.op_cnt, 0, lane);
+      const B3 hit = eq_arith<64>(d, Rr.r, Rr.Rb0, Rr.Rb1, Rr.Zw);
+      B3 lf;
+      uint64_t Z[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        lf.v[c] = __ldg(a.leaf + c * a.n_h + n);
+        Z[c] = Rr.F[c] & 1ull;
+      }
+      l = b2a_arith<64>(and_z(hit, lf, Z), Rr.A0, Rr.A1, Rr.bits);
+    }
+    const int o = (((ss >> 4) * 16 + nn) * 8) * 16 + (ss & 15);
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int p = 0; p < 8; ++p) sb[c * TC_ABLK + o + p * 16] = (uint8_t)(l.v[c] >> (8 * p));
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (tid == 0) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      uint8_t* dst = a.la8 + (((uint64_t)c * a.mtiles + mt) * a.nkbc + kb) * (uint64_t)TC_ABLK;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                   "r"(smem_u32(sb + c * TC_ABLK)), "r"(TC_ABLK)
+                   : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
+// --- UMMA plumbing
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  // K-major SWIZZLE_NONE: start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46),
+  // version 1 [46,48), base offset 0, layout type 0 [61,64)
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(0), "r"(0), "r"(0), "r"(0)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+struct MmaArgs {
+  const uint8_t *la8, *B8;
+  uint64_t* S;  // [3][n_h][W+1]
+  uint64_t nkbc, nkb_total, kb_base;  // chunk capacity (blocks), shard blocks, chunk's first global block
+  uint32_t nkb;                       // blocks in this chunk
+  int n_h, W, cpb, nbn, mtiles, N, nkr;
+};
+
+// grid (K ranges, M tiles x column blocks, component).  Thread 0 drives the
+// bulk-copy ring and issues the MMAs; all four warps read the accumulator
+// back (warp w owns TMEM lanes 32w..32w+31), fold the limbs, reduce the 8
+// limb rows of a node by shuffles and add into S.
+__global__ void __launch_bounds__(128, 1) k_count_mma(MmaArgs a) {
+  extern __shared__ __align__(1024) uint8_t smt[];
+  __shared__ __align__(8) uint64_t full[TC_STAGES], empty[TC_STAGES], done;
+  __shared__ uint32_t tmem_slot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int c = blockIdx.z, mt = blockIdx.y / a.nbn, nb = blockIdx.y % a.nbn;
+  const uint32_t per = (a.nkb + a.nkr - 1) / a.nkr;
+  const uint32_t kb0 = blockIdx.x * per, kb1 = min(a.nkb, kb0 + per);
+  const int T = kb1 > kb0 ? 2 * (int)(kb1 - kb0) : 0;
+  const int BB = a.N * TC_KB, stage = TC_ABLK + BB;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                 "r"(TC_TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 32) {
+    for (int i = 0; i < TC_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+
+  if (tid == 0 && T > 0) {
+    // idesc: S32 accumulator [4,6) = 2, A/B unsigned 8-bit, K-major, N>>3 at 17, M>>4 at 24
+    const uint32_t idesc = (2u << 4) | ((uint32_t)(a.N >> 3) << 17) | ((128u >> 4) << 24);
+    auto load = [&](int t) {
+      const int st = t % TC_STAGES, term = t & 1;
+      const uint64_t kb = kb0 + (uint32_t)(t >> 1);
+      uint8_t* sA = smt + st * stage;
+      const int ca = term ? (c + 1) % 3 : c;
+      mbar_expect_tx(&full[st], (uint32_t)stage);
+      bulk_g2s(sA, a.la8 + (((uint64_t)ca * a.mtiles + mt) * a.nkbc + kb) * (uint64_t)TC_ABLK, TC_ABLK, &full[st]);
+      bulk_g2s(sA + TC_ABLK,
+               a.B8 + ((((uint64_t)(c * 2 + term) * a.nbn + nb) * a.nkb_total + a.kb_base + kb) * (uint64_t)BB),
+               (uint32_t)BB, &full[st]);
+    };
+    for (int t = 0; t < min(TC_STAGES, T); ++t) load(t);
+    for (int t = 0; t < T; ++t) {
+      const int st = t % TC_STAGES;
+      mbar_wait(&full[st], (uint32_t)((t / TC_STAGES) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t sA = smem_u32(smt + st * stage), sB = sA + TC_ABLK;
+#pragma unroll
+      for (int j = 0; j < TC_KB / 32; ++j) {
+        const uint64_t ad = umma_desc(sA + j * 2 * (16 * 128), 16 * 128, 128);
+        const uint64_t bd = umma_desc(sB + j * 2 * (a.cpb * 128), a.cpb * 128, 128);
+        umma_i8(tmem, ad, bd, idesc, (t > 0 || j > 0) ? 1u : 0u);
+      }
+      umma_commit(&empty[st]);
+      if (t >= 1 && t - 1 + TC_STAGES < T) {
+        const int p = (t - 1) % TC_STAGES;
+        mbar_wait(&empty[p], (uint32_t)(((t - 1) / TC_STAGES) & 1));
+        load(t - 1 + TC_STAGES);
+      }
+    }
+    umma_commit(&done);
+  }
+  __syncwarp();
+  if (T > 0) {
+    mbar_wait(&done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int r = warp * 32 + lane, nn = r >> 3, p = r & 7;
+    const int n = mt * 16 + nn;
+    const uint64_t Sstride = (uint64_t)a.n_h * (a.W + 1);
+    for (int k = 0; k < a.N / 16; ++k) {
+      uint32_t d[16];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+          "%15}, [%16];"
+          : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
+            "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
+          : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(k * 16)));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint64_t v = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int sh = 8 * (p + q);
+          if (sh < 64) v += (uint64_t)d[8 * h + q] << sh;
+        }
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        const int w = nb * a.cpb + 2 * k + h;
+        if (p == 0 && n < a.n_h && w <= a.W)
+          atomicAdd((unsigned long long*)&a.S[c * Sstride + (uint64_t)n * (a.W + 1) + w], (unsigned long long)v);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS) : "memory");
+  }
+}
+
+}  // namespace
+}  // namespace gt

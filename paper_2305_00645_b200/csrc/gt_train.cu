@@ -360,6 +360,12 @@ __global__ void __launch_bounds__(CNT_TPB, 1) k_count_mac(MacArgs a) {
   }
 }
 
+}  // namespace
+}  // namespace gt
+#include "gt_count_tc.cuh"
+namespace gt {
+namespace {
+
 // ---------------------------------------------------------------------------
 // per-node heuristic (_heuristic_mpc, train.py:346-388) + replace, in three
 // kernels so no thread waits on another's serial chain:
@@ -729,8 +735,17 @@ uint64_t la_words(uint64_t N, int nf, int depth) {
   return std::min<uint64_t>(want, per * std::max<uint64_t>(N, 1));
 }
 
+// la8 chunk capacity in 128-sample blocks (tensor engine): ~64 MB of byte
+// planes at the deepest level, at least one block, at most the shard
+uint64_t tc_la8_blocks(uint64_t N, int nf, int depth) {
+  const TcPlan tp = tc_plan(nf, 1 << (depth - 1));
+  const uint64_t per_blk = 3ull * tp.mtiles * TC_ABLK;
+  const uint64_t nkb = std::max<uint64_t>(1, (N + TC_KB - 1) / TC_KB);
+  return std::max<uint64_t>(1, std::min<uint64_t>(nkb, (64ull << 20) / per_blk));
+}
+
 struct Layout {
-  uint64_t cols, la, leaf, midx, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
+  uint64_t cols, la, cols8, leaf, midx, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
 };
 
 Layout layout(const gt_train_cfg& c) {
@@ -744,7 +759,15 @@ Layout layout(const gt_train_cfg& c) {
     return r;
   };
   L.cols = take(3 * N * (uint64_t)count_plan(c.nf, 1).WC);
-  L.la = take(la_words(N, c.nf, c.depth));
+  if (c.count_engine == 0) {
+    const TcPlan tp = tc_plan(c.nf, (int)nmax);
+    const uint64_t nkb = (N + TC_KB - 1) / TC_KB;
+    L.la = take(tc_la8_blocks(N, c.nf, c.depth) * 3ull * tp.mtiles * TC_ABLK / 8);
+    L.cols8 = take(6ull * tp.nbn * nkb * tp.BB / 8);
+  } else {
+    L.la = take(la_words(N, c.nf, c.depth));
+    L.cols8 = take(0);
+  }
   L.leaf = take(3 * nmax);
   L.midx = take(3 * N);
   L.S = take(3 * nmax * (W + 1));
@@ -973,6 +996,63 @@ int launch_count(const CountLaunch& c, cudaStream_t s, int num_sms, int* launche
   return GT_OK;
 }
 
+// tensor engine: leaf + per chunk (byte-plane lanes, tcgen05 contraction)
+int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks, cudaStream_t s, int num_sms,
+                    int* launches) {
+  const TcPlan tp = tc_plan(c.nf, c.n_h);
+  k_count_leaf<<<(c.n_h + 127) / 128, 128, 0, s>>>(c.f, c.leaf, c.n_h, c.K, op_id(c.level, SITE_ISLEAF));
+  GT_LAUNCH_CHECK("k_count_leaf");
+  int nl = 1;
+  const uint64_t cap = la8_blocks * TC_KB;
+  const uint64_t nkb_total = (c.N + TC_KB - 1) / TC_KB;
+  const int smem = TC_STAGES * (TC_ABLK + tp.BB);
+  GT_CUDA_CHECK(cudaFuncSetAttribute(k_count_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  for (uint64_t s0 = 0; s0 < c.N; s0 += cap) {
+    const uint64_t cn = std::min<uint64_t>(cap, c.N - s0);
+    const uint32_t nkb = (uint32_t)((cn + TC_KB - 1) / TC_KB);
+    Lanes8Args la{};
+    la.midx = c.midx;
+    la.leaf = c.leaf;
+    la.la8 = (uint8_t*)c.la;
+    la.N = c.N;
+    la.s0 = s0;
+    la.cn = cn;
+    la.base = c.base;
+    la.nkbc = la8_blocks;
+    la.n_h = c.n_h;
+    la.off = c.n_h - 1;
+    la.mtiles = tp.mtiles;
+    la.K = c.K;
+    la.op_cnt = op_id(c.level, SITE_COUNT);
+    k_count_lanes8<<<dim3(nkb, (unsigned)tp.mtiles), 256, 0, s>>>(la);
+    GT_LAUNCH_CHECK("k_count_lanes8");
+    MmaArgs ma{};
+    ma.la8 = (const uint8_t*)c.la;
+    ma.B8 = B8;
+    ma.S = c.S;
+    ma.nkbc = la8_blocks;
+    ma.nkb_total = nkb_total;
+    ma.kb_base = s0 / TC_KB;
+    ma.nkb = nkb;
+    ma.n_h = c.n_h;
+    ma.W = 2 * c.nf + 1;
+    ma.cpb = tp.cpb;
+    ma.nbn = tp.nbn;
+    ma.mtiles = tp.mtiles;
+    ma.N = tp.N;
+    const int tiles = 3 * tp.mtiles * tp.nbn;
+    int nkr = std::max<int>((int)((nkb + TC_MAX_KB_PER_CTA - 1) / TC_MAX_KB_PER_CTA), (num_sms + tiles - 1) / tiles);
+    nkr = std::min<int>(nkr, (int)nkb);
+    const int per = (int)((nkb + nkr - 1) / nkr);
+    ma.nkr = (int)((nkb + per - 1) / per);
+    k_count_mma<<<dim3((unsigned)ma.nkr, (unsigned)(tp.mtiles * tp.nbn), 3), 128, smem, s>>>(ma);
+    GT_LAUNCH_CHECK("k_count_mma");
+    nl += 2;
+  }
+  *launches = nl;
+  return GT_OK;
+}
+
 int counter_shift(uint64_t n, int score_width, int tau) {  // train.py:189-192
   int headroom = (score_width - tau - 2) / 2;
   int bl = 0;
@@ -1015,6 +1095,7 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
   if (c.policy == 1 && c.depth > 8) return fail_inval("grow policy supports depth <= 8");
   if (c.heuristic != 0 && c.heuristic != 1) return fail_inval("heuristic must be mpc (0) or tee (1)");
   if (c.count_reshare != 0 && c.count_reshare != 1) return fail_inval("count_reshare must be 0 or 1");
+  if (c.count_engine != 0 && c.count_engine != 1) return fail_inval("count_engine must be 0 (tensor) or 1 (cuda)");
   if (c.heuristic == 1 && !heuristic) return fail_inval("heuristic tee needs the trusted-helper callback");
   const bool tee = c.heuristic == 1;
   bool ok = false;
@@ -1054,6 +1135,22 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
     k_prods<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(features, labels, colm, N, c.nf, WC, c.sample_base, K,
                                                           op_id(0, SITE_PRODS));
     GT_LAUNCH_CHECK("k_prods");
+    if (c.count_engine == 0) {
+      const TcPlan tp = tc_plan(c.nf, 1);
+      Cols8Args ca{};
+      ca.cols = colm;
+      ca.B8 = (uint8_t*)(ws + L.cols8);
+      ca.N = N;
+      ca.nkb = (N + TC_KB - 1) / TC_KB;
+      ca.WC = WC;
+      ca.W = 2 * c.nf + 1;
+      ca.cpb = tp.cpb;
+      ca.nbn = tp.nbn;
+      const uint64_t thr = 6ull * ca.nkb * 8 * tp.nbn * tp.cpb;
+      k_cols8<<<(unsigned)((thr + 255) / 256), 256, 0, s>>>(ca);
+      GT_LAUNCH_CHECK("k_cols8");
+      P.count_launch();
+    }
     P.stop(Prof::PRODS);
   }
   int32_t trained = c.depth;
@@ -1084,7 +1181,9 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
       cl.level = level;
       int nl = 0;
       P.start();
-      int rc = launch_count(cl, s, num_sms, &nl);
+      int rc = c.count_engine == 0
+                   ? launch_count_tc(cl, (const uint8_t*)(ws + L.cols8), tc_la8_blocks(N, c.nf, c.depth), s, num_sms, &nl)
+                   : launch_count(cl, s, num_sms, &nl);
       if (rc) return rc;
       P.stop(Prof::COUNT);
       for (int i = 1; i < nl; ++i) P.count_launch();

@@ -37,6 +37,10 @@ class TrainConfig:
     # first and reshares each counter cell once (ABY3-style dot product) --
     # same revealed tree, a fraction of the reshared words.
     count_reshare: str = "elementwise"
+    # B200 extension: which unit runs the count contraction -- "tensor"
+    # (tcgen05.mma kind::i8 over INT8 limbs of the Z_2^64 shares) or "cuda"
+    # (64-bit IMAD on the CUDA cores).  Both produce identical shares.
+    count_engine: str = "tensor"
 
 
 @dataclass
@@ -75,6 +79,8 @@ def _validate(cfg: TrainConfig, nf: int) -> int:
         raise ValueError(f"unknown depth policy {cfg.policy!r}")
     if cfg.count_reshare not in ("elementwise", "dot"):
         raise ValueError(f"unknown count_reshare {cfg.count_reshare!r}")
+    if cfg.count_engine not in ("tensor", "cuda"):
+        raise ValueError(f"unknown count_engine {cfg.count_engine!r}")
     if cfg.count_ring.width != 64:
         raise ValueError("counters live in Z_2^64 on the B200 path")
     depth = resolved_depth(cfg, nf + 1)
@@ -109,6 +115,7 @@ class DeviceTrainer:
         c.policy = 1 if cfg.policy == "grow" else 0
         c.heuristic = 1 if cfg.heuristic == "tee" else 0
         c.count_reshare = 1 if cfg.count_reshare == "dot" else 0
+        c.count_engine = 1 if cfg.count_engine == "cuda" else 0
         c.n_total = self.n_total
         c.n_local = self.n_local
         c.sample_base = int(sample_base)

@@ -300,3 +300,24 @@ def test_score_ring64_and_tau_variants_match_reference_and_oracle():
         fill = filler_values(setup.filler_seed, (1 << m["depth"]) - 1, data.shape[1])
         To, Fo, _ = oracle.train(X, Y, fill, m["depth"], keys, tau=m["tau"], score_width=m["width"])
         assert np.array_equal(T, To) and np.array_equal(F, Fo), m
+
+
+@pytest.mark.parametrize("nf,n,depth", [(13, 4000, 5), (20, 3001, 4), (33, 1500, 3), (64, 700, 2)])
+def test_count_engines_share_exact_vs_oracle(nf, n, depth):
+    """Tensor-core (tcgen05 kind::i8 limb) and CUDA-core count contractions
+    give the oracle's shares, including several column blocks (nf > 15) and
+    partial sample blocks; the revealed tree equals the plain-integer shadow."""
+    from paper_2305_00645_b200.seeds import derive_seed
+
+    rng = np.random.default_rng(nf * 1000 + n)
+    data = rng.integers(0, 2, size=(n, nf + 1), dtype=np.uint8)
+    seed = (nf * 7 + n).to_bytes(16, "little")
+    setup, k, keys = run_keys(seed)
+    fill = filler_values(setup.filler_seed, (1 << depth) - 1, nf + 1)
+    X, Y = share(data[:, :-1], rng), share(data[:, -1], rng)
+    To, Fo, _ = oracle.train(X, Y, fill, depth, keys)
+    from paper_2305_00645_b200.train import TrainConfig, train_components
+
+    for engine in ("tensor", "cuda"):
+        T, F, d = train_components(X, Y, TrainConfig(depth=depth, count_engine=engine), setup, derive_seed(seed, "deal"))
+        assert np.array_equal(T, To) and np.array_equal(F, Fo), engine
