@@ -30,6 +30,7 @@ constexpr int TC_STAGES = 4;              // smem ring depth
 constexpr int TC_ABLK = TC_KB * 128;      // bytes of an A block: 128 rows (16 nodes x 8 limbs) x 128 samples
 constexpr int TC_MAX_KB_PER_CTA = 64;     // 2 x 64 x 128 x 255^2 < 2^31
 constexpr int TC_TMEM_COLS = 256;
+constexpr int TC_LANES_SMEM = 3 * TC_ABLK + 3 * 16 * 8;
 
 struct TcPlan {
   int CW;      // sample columns incl. the mask column (W + 1)
@@ -101,20 +102,38 @@ __global__ void __launch_bounds__(256) k_cols8(Cols8Args a) {
 }
 
 // --- A operand: one CTA per (128-sample block, 16-node M tile) of a chunk;
-// lanes la = b2a(eq(m_idx, off+n) & is_leaf[n]) as in k_count_lanes, written
-// as byte planes la8[c][mt][kbc][kc 8][g 16][p 8][16] through shared memory
-// and a bulk store.
+// lanes la = b2a(eq(m_idx, off+n) & is_leaf[n]) (train.py:328-331, the same
+// LaneRand schedule as k_count_lanes), four consecutive samples of one node
+// per work item so each limb row leaves as one packed 32-bit word; the byte
+// planes la8[c][mt][kbc][kc 8][g 16][p 8][16] go out through shared memory
+// and a bulk store.  is_leaf of the tile's 16 nodes (train.py:320) is drawn
+// in the CTA (it is keyed by node only).
 struct Lanes8Args {
-  const uint64_t *midx, *leaf;
+  const uint64_t *midx, *f;
   uint8_t* la8;
   uint64_t N, s0, cn, base, nkbc;  // nkbc = chunk capacity in K blocks
   int n_h, off, mtiles;
   Keys K;
-  uint32_t op_cnt;
+  uint32_t op_cnt, op_leaf;
 };
 __global__ void __launch_bounds__(256) k_count_lanes8(Lanes8Args a) {
-  __shared__ __align__(128) uint8_t sb[3 * TC_ABLK];
+  extern __shared__ __align__(1024) uint8_t sb[];  // [3][TC_ABLK] + leaf [3][16] u64
+  uint64_t(*leaf)[16] = reinterpret_cast<uint64_t(*)[16]>(sb + 3 * TC_ABLK);
   const int kb = blockIdx.x, mt = blockIdx.y, tid = threadIdx.x;
+  if (tid < 16) {
+    const int n = mt * 16 + tid;
+    B3 z = {{0, 0, 0}};
+    if (n < a.n_h) z = eqz<64>(a.K, a.op_leaf, 0, (uint64_t)n, add_pub<64>(ld3s(a.f, a.n_h, n), 0ull - F_LEAF));
+#pragma unroll
+    for (int c = 0; c < 3; ++c) leaf[c][tid] = z.v[c] & 1ull;
+  }
+  __syncthreads();
+  // one lane per thread; a warp = 32 consecutive samples of one node, a quad
+  // = 4 consecutive samples whose limb bytes are transposed in registers
+  // (3 shuffles + 3 byte permutes per 32-bit half) so lane j of the quad
+  // stores limbs j and j+4 of its 4 samples as two packed words.
+  const int qj = threadIdx.x & 3;
+  const uint32_t sel = (uint32_t)qj | ((uint32_t)(4 + qj) << 4);
   for (int e = tid; e < 16 * TC_KB; e += blockDim.x) {
     const int nn = e / TC_KB, ss = e % TC_KB;
     const int n = mt * 16 + nn;
@@ -131,16 +150,25 @@ __global__ void __launch_bounds__(256) k_count_lanes8(Lanes8Args a) {
       uint64_t Z[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        lf.v[c] = __ldg(a.leaf + c * a.n_h + n);
+        lf.v[c] = leaf[c][nn];
         Z[c] = Rr.F[c] & 1ull;
       }
       l = b2a_arith<64>(and_z(hit, lf, Z), Rr.A0, Rr.A1, Rr.bits);
     }
-    const int o = (((ss >> 4) * 16 + nn) * 8) * 16 + (ss & 15);
+    const int qb = threadIdx.x & ~3;  // quad base lane
+    const int o = (((ss >> 4) * 16 + nn) * 8) * 16 + ((ss & ~3) & 15);
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
-      for (int p = 0; p < 8; ++p) sb[c * TC_ABLK + o + p * 16] = (uint8_t)(l.v[c] >> (8 * p));
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t wv = (uint32_t)(l.v[c] >> (32 * h));
+        const uint32_t w0 = __shfl_sync(0xffffffffu, wv, qb + 0);
+        const uint32_t w1 = __shfl_sync(0xffffffffu, wv, qb + 1);
+        const uint32_t w2 = __shfl_sync(0xffffffffu, wv, qb + 2);
+        const uint32_t w3 = __shfl_sync(0xffffffffu, wv, qb + 3);
+        const uint32_t x = __byte_perm(w0, w1, sel), y = __byte_perm(w2, w3, sel);
+        *reinterpret_cast<uint32_t*>(sb + c * TC_ABLK + o + (4 * h + qj) * 16) = __byte_perm(x, y, 0x5410);
+      }
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
@@ -181,6 +209,10 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 struct MmaArgs {
   const uint8_t *la8, *B8;
   uint64_t* S;  // [3][n_h][W+1]
+  Keys K;
+  uint32_t op_cnt;
+  int alpha;            // 0: none, 1: telescoped elementwise reshare sums, 2: dot-product reshare
+  uint64_t t0, t1;      // shard sample range for the telescoped sums
   uint64_t nkbc, nkb_total, kb_base;  // chunk capacity (blocks), shard blocks, chunk's first global block
   uint32_t nkb;                       // blocks in this chunk
   int n_h, W, cpb, nbn, mtiles, N, nkr;
@@ -283,8 +315,22 @@ __global__ void __launch_bounds__(128, 1) k_count_mma(MmaArgs a) {
         v += __shfl_xor_sync(0xffffffffu, v, 2);
         v += __shfl_xor_sync(0xffffffffu, v, 4);
         const int w = nb * a.cpb + 2 * k + h;
-        if (p == 0 && n < a.n_h && w <= a.W)
+        if (p == 0 && n < a.n_h && w <= a.W) {
+          if (a.alpha && blockIdx.x == 0 && w < a.W) {
+            // zero shares of the count products summed over the shard (see
+            // k_count_alpha): alpha_c = F_c - F_{c-1}
+            uint64_t F[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const Key& key = a.K.pair[q == 0 ? c : (c + 2) % 3];
+              F[q] = a.alpha == 2 ? word(key, a.op_cnt, 4, (uint32_t)w, (uint64_t)n)
+                                  : word(key, a.op_cnt, 3, (uint32_t)w, a.t1 * (uint64_t)a.n_h + n) -
+                                        word(key, a.op_cnt, 3, (uint32_t)w, a.t0 * (uint64_t)a.n_h + n);
+            }
+            v += F[0] - F[1];
+          }
           atomicAdd((unsigned long long*)&a.S[c * Sstride + (uint64_t)n * (a.W + 1) + w], (unsigned long long)v);
+        }
       }
     }
   }

@@ -931,7 +931,7 @@ struct CountLaunch {
   const uint64_t *midx, *f, *cols;
   uint64_t *la, *leaf, *S;
   uint64_t la_cap_words, N, base;
-  int nf, n_h;
+  int nf, n_h, n_h_max;
   Keys K;
   int level;
 };
@@ -997,22 +997,26 @@ int launch_count(const CountLaunch& c, cudaStream_t s, int num_sms, int* launche
 }
 
 // tensor engine: leaf + per chunk (byte-plane lanes, tcgen05 contraction)
-int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks, cudaStream_t s, int num_sms,
-                    int* launches) {
+int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks, int alpha, uint64_t t0,
+                    uint64_t t1, cudaStream_t s, int num_sms, int* launches) {
   const TcPlan tp = tc_plan(c.nf, c.n_h);
-  k_count_leaf<<<(c.n_h + 127) / 128, 128, 0, s>>>(c.f, c.leaf, c.n_h, c.K, op_id(c.level, SITE_ISLEAF));
-  GT_LAUNCH_CHECK("k_count_leaf");
-  int nl = 1;
+  int nl = 0;
+  // the buffer holds la8_blocks K blocks at the deepest level: shallower
+  // levels (fewer M tiles) fit proportionally more samples per chunk
+  const int mt_max = tc_plan(c.nf, c.n_h_max).mtiles;
+  la8_blocks = std::min<uint64_t>(la8_blocks * mt_max / tp.mtiles, (c.N + TC_KB - 1) / TC_KB);
   const uint64_t cap = la8_blocks * TC_KB;
   const uint64_t nkb_total = (c.N + TC_KB - 1) / TC_KB;
   const int smem = TC_STAGES * (TC_ABLK + tp.BB);
   GT_CUDA_CHECK(cudaFuncSetAttribute(k_count_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  GT_CUDA_CHECK(cudaFuncSetAttribute(k_count_lanes8, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_LANES_SMEM));
   for (uint64_t s0 = 0; s0 < c.N; s0 += cap) {
     const uint64_t cn = std::min<uint64_t>(cap, c.N - s0);
     const uint32_t nkb = (uint32_t)((cn + TC_KB - 1) / TC_KB);
     Lanes8Args la{};
     la.midx = c.midx;
-    la.leaf = c.leaf;
+    la.f = c.f;
+    la.op_leaf = op_id(c.level, SITE_ISLEAF);
     la.la8 = (uint8_t*)c.la;
     la.N = c.N;
     la.s0 = s0;
@@ -1024,7 +1028,7 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
     la.mtiles = tp.mtiles;
     la.K = c.K;
     la.op_cnt = op_id(c.level, SITE_COUNT);
-    k_count_lanes8<<<dim3(nkb, (unsigned)tp.mtiles), 256, 0, s>>>(la);
+    k_count_lanes8<<<dim3(nkb, (unsigned)tp.mtiles), 256, TC_LANES_SMEM, s>>>(la);
     GT_LAUNCH_CHECK("k_count_lanes8");
     MmaArgs ma{};
     ma.la8 = (const uint8_t*)c.la;
@@ -1040,6 +1044,11 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
     ma.nbn = tp.nbn;
     ma.mtiles = tp.mtiles;
     ma.N = tp.N;
+    ma.K = c.K;
+    ma.op_cnt = op_id(c.level, SITE_COUNT);
+    ma.alpha = s0 == 0 ? alpha : 0;
+    ma.t0 = t0;
+    ma.t1 = t1;
     const int tiles = 3 * tp.mtiles * tp.nbn;
     int nkr = std::max<int>((int)((nkb + TC_MAX_KB_PER_CTA - 1) / TC_MAX_KB_PER_CTA), (num_sms + tiles - 1) / tiles);
     nkr = std::min<int>(nkr, (int)nkb);
@@ -1177,18 +1186,21 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
       cl.base = c.sample_base;
       cl.nf = c.nf;
       cl.n_h = n_h;
+      cl.n_h_max = 1 << (c.depth - 1);
       cl.K = K;
       cl.level = level;
       int nl = 0;
       P.start();
       int rc = c.count_engine == 0
-                   ? launch_count_tc(cl, (const uint8_t*)(ws + L.cols8), tc_la8_blocks(N, c.nf, c.depth), s, num_sms, &nl)
+                   ? launch_count_tc(cl, (const uint8_t*)(ws + L.cols8), tc_la8_blocks(N, c.nf, c.depth),
+                                     c.count_reshare == 0 ? 1 : (c.sample_base == 0 ? 2 : 0), c.sample_base,
+                                     c.sample_base + N, s, num_sms, &nl)
                    : launch_count(cl, s, num_sms, &nl);
       if (rc) return rc;
       P.stop(Prof::COUNT);
       for (int i = 1; i < nl; ++i) P.count_launch();
     }
-    if (c.count_reshare == 0 ? N > 0 : c.sample_base == 0) {
+    if (c.count_engine == 1 && (c.count_reshare == 0 ? N > 0 : c.sample_base == 0)) {  // tensor engine: in k_count_mma
       const int cells = n_h * (int)W;
       k_count_alpha<<<(cells + 127) / 128, 128, 0, s>>>(S, n_h, c.nf, K, op_id(level, SITE_COUNT), c.count_reshare,
                                                        c.sample_base, c.sample_base + N);
