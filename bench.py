@@ -136,6 +136,22 @@ def count_bytes(n, nf, depth):
     return sum(n * (24 + 24 * W) + 24 * (1 << h) * (W + 1) for h in range(depth))
 
 
+def count_lanes_bytes(n, nf, depth):
+    # node indices in (3 x 8 B per sample), la byte planes out (3 components x 8 limbs per (sample, node))
+    return sum(n * 24 + n * 24 * (1 << h) for h in range(depth))
+
+
+def count_contract_bytes(n, nf, depth):
+    # tcgen05 operands, each read once per level: la byte planes of the level's 16-node M tiles
+    # (3 x 128 B per sample per tile) + the sample-column planes (u and x terms, 3 components,
+    # 8 limb rows per column incl. the mask column, padded to the column block)
+    cw = 2 * nf + 2
+    nbn = (cw + 31) // 32
+    cpb = -(-cw // nbn)
+    cpb += cpb & 1
+    return sum(n * (3 * 128 * (((1 << h) + 15) // 16) + 6 * 8 * nbn * cpb) for h in range(depth))
+
+
 def partition_bytes(n, nf, depth):
     return sum(n * (48 + 24 * nf) + 24 * (1 << (h - 1)) for h in range(1, depth))
 
@@ -382,7 +398,7 @@ def main():
     clocks = clk.summary()
 
     # ---- per-kernel CUDA-event durations: a second pass of K profiled steps ----
-    prof_tot = {k: 0.0 for k in ("prods", "partition", "count", "node_hc", "node_finish")}
+    prof_tot = {k: 0.0 for k in ("prods", "partition", "count_lanes", "count_contract", "node_hc", "node_finish")}
     prof_n = {k: 0 for k in prof_tot}
     launches = 0
     for _ in range(args.steps):
@@ -470,22 +486,34 @@ def main():
 
     # ---- roofline of the dominant kernel class ----
     peak, peak_kind = _peaks()
-    dom = max(prof_tot, key=lambda k: prof_tot[k])
-    bytes_of = {"count": count_bytes(cnt, NF_C2, DEPTH_C2), "partition": partition_bytes(cnt, NF_C2, DEPTH_C2),
+    # dominant single kernel: node_hc (k_hc_pre + k_hc_div + k_hc_post per level) and node_finish are
+    # multi-kernel latency chains with no bulk data; their times are in kernel_ms_per_step
+    dom = max((k for k in prof_tot if k not in ("node_hc", "node_finish")), key=lambda k: prof_tot[k])
+    bytes_of = {"count_lanes": count_lanes_bytes(cnt, NF_C2, DEPTH_C2),
+                "count_contract": count_contract_bytes(cnt, NF_C2, DEPTH_C2),
+                "partition": partition_bytes(cnt, NF_C2, DEPTH_C2),
                 "prods": cnt * (24 * NF_C2 + 24 + 24 * NF_C2), "node_hc": 0, "node_finish": 0}
+    kname = {"count_lanes": "k_count_lanes8", "count_contract": "k_count_mma", "partition": "k_partition",
+             "node_hc": "k_hc_div", "prods": "k_cols8", "node_finish": "k_node_finish"}
     alg = bytes_of[dom] * args.steps
     achieved = alg / (prof_tot[dom] / 1e3) / 1e9 if prof_tot[dom] > 0 else 0.0
     nlaunch = max(1, prof_n[dom])
-    traffic = _traffic({"count": "k_count", "partition": "k_partition", "node_hc": "k_hc_div"}.get(dom, dom))
+    traffic = _traffic(kname.get(dom, dom))
     # integer-ALU roof: Philox blocks the dominant kernel draws vs the measured Philox peak
-    W = 2 * NF_C2 + 1
-    blocks = {"count": sum(cnt * (1 << h) * (6 + 3 * (NF_C2 + 1)) for h in range(DEPTH_C2)),
+    blocks = {"count_lanes": sum(cnt * (1 << h) * 6 for h in range(DEPTH_C2)),
               "partition": sum(cnt * ((1 << (h - 1)) + NF_C2) * 6 for h in range(1, DEPTH_C2))}.get(dom)
     alu = None
     if blocks:
         alu = {"bound": "int-alu (Philox4x32-10 blocks)", "achieved_blocks_per_s": blocks * args.steps / (prof_tot[dom] / 1e3),
                "peak_blocks_per_s": _philox_peak(), "note": "peak measured by gt_diag_philox on this GPU"}
         alu["frac"] = alu["achieved_blocks_per_s"] / alu["peak_blocks_per_s"] if alu["peak_blocks_per_s"] else None
+    # every kernel class against the HBM roof (same definitions), for the record
+    classes = {}
+    for k in prof_tot:
+        if prof_tot[k] > 0 and bytes_of.get(k):
+            gbs = bytes_of[k] * args.steps / (prof_tot[k] / 1e3) / 1e9
+            classes[k] = {"kernel": kname.get(k, k), "ms_per_step": prof_tot[k] / args.steps,
+                          "achieved_gbs": gbs, "frac": gbs / peak}
     cpu_base = None
     if world == 1 and not args.no_cpu_baseline:
         import oracle
@@ -509,10 +537,10 @@ def main():
         "parity": {"tree_equals_reference": parity, "c3_predictions_equal_reference": preds_ok},
         "e2e": {"value": e2e_s, "unit": "s/tree", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+        "roofline": {"bound": "hbm", "kernel": kname.get(dom, dom), "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": bytes_of[dom] / max(1, prof_n[dom] // args.steps),
-                     "avg_launch_ms": prof_tot[dom] / nlaunch, "alu": alu},
+                     "avg_launch_ms": prof_tot[dom] / nlaunch, "alu": alu, "classes": classes},
         "kernel_ms_per_step": {k: v / args.steps for k, v in prof_tot.items()},
         "timing": ("value: CUDA-graph replay of the whole tree (1 GPU) / stream launches (N>1); "
                    "kernel_ms_per_step + roofline: separate pass of K steps with per-launch CUDA events"),

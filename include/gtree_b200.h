@@ -144,6 +144,10 @@ typedef struct {
   uint32_t n_prods, n_partition, n_count, n_node_hc, n_node_finish;
   float ms_prods, ms_partition, ms_count, ms_node_hc, ms_node_finish;
   float ms_total; /* first to last event */
+  /* count split: lane kernels (eq/and/b2a per (sample, node)) and the
+     contraction (tcgen05 MMA or CUDA-core MAC); ms_count = their sum */
+  uint32_t n_count_lanes, n_count_contract;
+  float ms_count_lanes, ms_count_contract;
 } gt_train_profile;
 
 /* gt_train plus the tee helper callback (required when cfg->heuristic = 1)

@@ -52,7 +52,9 @@ class gt_train_profile(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_uint32), ("n_prods", ctypes.c_uint32), ("n_partition", ctypes.c_uint32),
                 ("n_count", ctypes.c_uint32), ("n_node_hc", ctypes.c_uint32), ("n_node_finish", ctypes.c_uint32),
                 ("ms_prods", ctypes.c_float), ("ms_partition", ctypes.c_float), ("ms_count", ctypes.c_float),
-                ("ms_node_hc", ctypes.c_float), ("ms_node_finish", ctypes.c_float), ("ms_total", ctypes.c_float)]
+                ("ms_node_hc", ctypes.c_float), ("ms_node_finish", ctypes.c_float), ("ms_total", ctypes.c_float),
+                ("n_count_lanes", ctypes.c_uint32), ("n_count_contract", ctypes.c_uint32),
+                ("ms_count_lanes", ctypes.c_float), ("ms_count_contract", ctypes.c_float)]
 
 
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p)

@@ -26,11 +26,10 @@ namespace gt {
 namespace {
 
 constexpr int TC_KB = 128;                // samples per K block
-constexpr int TC_STAGES = 4;              // smem ring depth
+constexpr int TC_STAGES = 5;              // smem ring depth
 constexpr int TC_ABLK = TC_KB * 128;      // bytes of an A block: 128 rows (16 nodes x 8 limbs) x 128 samples
 constexpr int TC_MAX_KB_PER_CTA = 64;     // 2 x 64 x 128 x 255^2 < 2^31
 constexpr int TC_TMEM_COLS = 256;
-constexpr int TC_LANES_SMEM = 3 * TC_ABLK + 3 * 16 * 8;
 
 struct TcPlan {
   int CW;      // sample columns incl. the mask column (W + 1)
@@ -105,8 +104,8 @@ __global__ void __launch_bounds__(256) k_cols8(Cols8Args a) {
 // lanes la = b2a(eq(m_idx, off+n) & is_leaf[n]) (train.py:328-331, the same
 // LaneRand schedule as k_count_lanes), four consecutive samples of one node
 // per work item so each limb row leaves as one packed 32-bit word; the byte
-// planes la8[c][mt][kbc][kc 8][g 16][p 8][16] go out through shared memory
-// and a bulk store.  is_leaf of the tile's 16 nodes (train.py:320) is drawn
+// planes la8[c][mt][kbc][kc 8][g 16][p 8][16] are stored straight from
+// registers (each warp store covers whole 32-byte sectors).  is_leaf of the tile's 16 nodes (train.py:320) is drawn
 // in the CTA (it is keyed by node only).
 struct Lanes8Args {
   const uint64_t *midx, *f;
@@ -117,9 +116,10 @@ struct Lanes8Args {
   uint32_t op_cnt, op_leaf;
 };
 __global__ void __launch_bounds__(256) k_count_lanes8(Lanes8Args a) {
-  extern __shared__ __align__(1024) uint8_t sb[];  // [3][TC_ABLK] + leaf [3][16] u64
-  uint64_t(*leaf)[16] = reinterpret_cast<uint64_t(*)[16]>(sb + 3 * TC_ABLK);
+  __shared__ uint64_t leaf[3][16];
   const int kb = blockIdx.x, mt = blockIdx.y, tid = threadIdx.x;
+  uint8_t* blk = a.la8 + ((uint64_t)mt * a.nkbc + kb) * (uint64_t)TC_ABLK;
+  const uint64_t cstride = (uint64_t)a.mtiles * a.nkbc * TC_ABLK;
   if (tid < 16) {
     const int n = mt * 16 + tid;
     B3 z = {{0, 0, 0}};
@@ -167,21 +167,9 @@ __global__ void __launch_bounds__(256) k_count_lanes8(Lanes8Args a) {
         const uint32_t w2 = __shfl_sync(0xffffffffu, wv, qb + 2);
         const uint32_t w3 = __shfl_sync(0xffffffffu, wv, qb + 3);
         const uint32_t x = __byte_perm(w0, w1, sel), y = __byte_perm(w2, w3, sel);
-        *reinterpret_cast<uint32_t*>(sb + c * TC_ABLK + o + (4 * h + qj) * 16) = __byte_perm(x, y, 0x5410);
+        // a warp's store = two contiguous 64-byte runs (4 limb rows x 16 samples)
+        *reinterpret_cast<uint32_t*>(blk + c * cstride + o + (4 * h + qj) * 16) = __byte_perm(x, y, 0x5410);
       }
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  __syncthreads();
-  if (tid == 0) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      uint8_t* dst = a.la8 + (((uint64_t)c * a.mtiles + mt) * a.nkbc + kb) * (uint64_t)TC_ABLK;
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-                   "r"(smem_u32(sb + c * TC_ABLK)), "r"(TC_ABLK)
-                   : "memory");
-    }
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
 }
 

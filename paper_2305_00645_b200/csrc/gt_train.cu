@@ -847,7 +847,7 @@ int launch_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint6
 
 // CUDA-event timing of each launch (gt_train_ex with a profile struct).
 struct Prof {
-  enum Kind { PRODS, PARTITION, COUNT, NODE_HC, NODE_FINISH, NKIND };
+  enum Kind { PRODS, PARTITION, COUNT_LANES, COUNT_CONTRACT, NODE_HC, NODE_FINISH, NKIND };
   gt_train_profile* out;
   cudaStream_t s;
   cudaEvent_t first = nullptr, a = nullptr;
@@ -885,8 +885,10 @@ struct Prof {
     GT_CUDA_CHECK(cudaStreamSynchronize(s));
     gt_train_profile p{};
     p.launches = launches;
-    float* ms[NKIND] = {&p.ms_prods, &p.ms_partition, &p.ms_count, &p.ms_node_hc, &p.ms_node_finish};
-    uint32_t* cnt[NKIND] = {&p.n_prods, &p.n_partition, &p.n_count, &p.n_node_hc, &p.n_node_finish};
+    float* ms[NKIND] = {&p.ms_prods,     &p.ms_partition, &p.ms_count_lanes, &p.ms_count_contract,
+                        &p.ms_node_hc,   &p.ms_node_finish};
+    uint32_t* cnt[NKIND] = {&p.n_prods,   &p.n_partition, &p.n_count_lanes, &p.n_count_contract,
+                            &p.n_node_hc, &p.n_node_finish};
     cudaEvent_t last = first;
     for (auto& e : spans) {
       float t = 0.f;
@@ -896,6 +898,8 @@ struct Prof {
       last = e.second.second;
     }
     GT_CUDA_CHECK(cudaEventElapsedTime(&p.ms_total, first, last));
+    p.ms_count = p.ms_count_lanes + p.ms_count_contract;
+    p.n_count = p.n_count_lanes + p.n_count_contract;
     *out = p;
     return GT_OK;
   }
@@ -937,11 +941,12 @@ struct CountLaunch {
 };
 
 // leaf + per chunk (lanes, contraction); returns the number of launches
-int launch_count(const CountLaunch& c, cudaStream_t s, int num_sms, int* launches) {
+int launch_count(const CountLaunch& c, cudaStream_t s, int num_sms, Prof& P) {
   const CountPlan p = count_plan(c.nf, c.n_h);
+  P.start();
   k_count_leaf<<<(c.n_h + 127) / 128, 128, 0, s>>>(c.f, c.leaf, c.n_h, c.K, op_id(c.level, SITE_ISLEAF));
   GT_LAUNCH_CHECK("k_count_leaf");
-  int nl = 1;
+  P.stop(Prof::COUNT_LANES);
   const uint64_t per = 3ull * p.nblk * p.nbp;
   const uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(c.N, c.la_cap_words / per));
   const int stage_words = 3 * p.ts * (p.nbp + p.WC);
@@ -967,8 +972,10 @@ int launch_count(const CountLaunch& c, cudaStream_t s, int num_sms, int* launche
     la.K = c.K;
     la.op_cnt = op_id(c.level, SITE_COUNT);
     const uint64_t lanes = cn * p.nblk * p.nbp;
+    P.start();
     k_count_lanes<<<(unsigned)((lanes + 255) / 256), 256, 0, s>>>(la);
     GT_LAUNCH_CHECK("k_count_lanes");
+    P.stop(Prof::COUNT_LANES);
     MacArgs ma{};
     ma.la = c.la;
     ma.cols = c.cols;
@@ -988,19 +995,44 @@ int launch_count(const CountLaunch& c, cudaStream_t s, int num_sms, int* launche
     const uint64_t gx0 = std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)std::max(1, num_sms / p.nblk)));
     ma.tiles_per_cta = (int)((tiles + gx0 - 1) / gx0);
     const unsigned gx = (unsigned)((tiles + ma.tiles_per_cta - 1) / ma.tiles_per_cta);
+    P.start();
     k_count_mac<<<dim3(gx, (unsigned)p.nblk), CNT_TPB, smem, s>>>(ma);
     GT_LAUNCH_CHECK("k_count_mac");
-    nl += 2;
+    P.stop(Prof::COUNT_CONTRACT);
   }
-  *launches = nl;
   return GT_OK;
+}
+
+// Keep the level-invariant B operand (the byte-plane sample columns, read by
+// every level's contraction) resident in L2: a persisting access-policy
+// window over it on the launches that write and read it.  The persisting
+// carve-out is raised once per device to cover it (bounded by the device max).
+bool l2_window_attr(const void* base, uint64_t bytes, cudaLaunchAttribute* at) {
+  static int max_persist = -1, max_window = 0;
+  if (max_persist < 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev) != cudaSuccess)
+      max_persist = 0;
+    if (max_persist > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
+    cudaGetLastError();
+  }
+  if (max_persist <= 0 || max_window <= 0 || bytes == 0) return false;
+  const uint64_t win = std::min<uint64_t>(bytes, (uint64_t)max_window);
+  at->id = cudaLaunchAttributeAccessPolicyWindow;
+  at->val.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+  at->val.accessPolicyWindow.num_bytes = (size_t)win;
+  at->val.accessPolicyWindow.hitRatio = std::min(1.0f, (float)max_persist / (float)win);
+  at->val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  at->val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  return true;
 }
 
 // tensor engine: leaf + per chunk (byte-plane lanes, tcgen05 contraction)
 int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks, int alpha, uint64_t t0,
-                    uint64_t t1, cudaStream_t s, int num_sms, int* launches) {
+                    uint64_t t1, cudaStream_t s, int num_sms, Prof& P) {
   const TcPlan tp = tc_plan(c.nf, c.n_h);
-  int nl = 0;
   // the buffer holds la8_blocks K blocks at the deepest level: shallower
   // levels (fewer M tiles) fit proportionally more samples per chunk
   const int mt_max = tc_plan(c.nf, c.n_h_max).mtiles;
@@ -1009,7 +1041,6 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
   const uint64_t nkb_total = (c.N + TC_KB - 1) / TC_KB;
   const int smem = TC_STAGES * (TC_ABLK + tp.BB);
   GT_CUDA_CHECK(cudaFuncSetAttribute(k_count_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  GT_CUDA_CHECK(cudaFuncSetAttribute(k_count_lanes8, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_LANES_SMEM));
   for (uint64_t s0 = 0; s0 < c.N; s0 += cap) {
     const uint64_t cn = std::min<uint64_t>(cap, c.N - s0);
     const uint32_t nkb = (uint32_t)((cn + TC_KB - 1) / TC_KB);
@@ -1028,8 +1059,10 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
     la.mtiles = tp.mtiles;
     la.K = c.K;
     la.op_cnt = op_id(c.level, SITE_COUNT);
-    k_count_lanes8<<<dim3(nkb, (unsigned)tp.mtiles), 256, TC_LANES_SMEM, s>>>(la);
+    P.start();
+    k_count_lanes8<<<dim3(nkb, (unsigned)tp.mtiles), 256, 0, s>>>(la);
     GT_LAUNCH_CHECK("k_count_lanes8");
+    P.stop(Prof::COUNT_LANES);
     MmaArgs ma{};
     ma.la8 = (const uint8_t*)c.la;
     ma.B8 = B8;
@@ -1054,11 +1087,21 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
     nkr = std::min<int>(nkr, (int)nkb);
     const int per = (int)((nkb + nkr - 1) / nkr);
     ma.nkr = (int)((nkb + per - 1) / per);
-    k_count_mma<<<dim3((unsigned)ma.nkr, (unsigned)(tp.mtiles * tp.nbn), 3), 128, smem, s>>>(ma);
+    {
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3((unsigned)ma.nkr, (unsigned)(tp.mtiles * tp.nbn), 3);
+      lc.blockDim = dim3(128);
+      lc.dynamicSmemBytes = (size_t)smem;
+      lc.stream = s;
+      cudaLaunchAttribute at[1];
+      lc.attrs = at;
+      lc.numAttrs = l2_window_attr(B8, 6ull * tp.nbn * nkb_total * tp.BB, at) ? 1 : 0;
+      P.start();
+      GT_CUDA_CHECK(cudaLaunchKernelEx(&lc, k_count_mma, ma));
+      P.stop(Prof::COUNT_CONTRACT);
+    }
     GT_LAUNCH_CHECK("k_count_mma");
-    nl += 2;
   }
-  *launches = nl;
   return GT_OK;
 }
 
@@ -1156,7 +1199,14 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
       ca.cpb = tp.cpb;
       ca.nbn = tp.nbn;
       const uint64_t thr = 6ull * ca.nkb * 8 * tp.nbn * tp.cpb;
-      k_cols8<<<(unsigned)((thr + 255) / 256), 256, 0, s>>>(ca);
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3((unsigned)((thr + 255) / 256));
+      lc.blockDim = dim3(256);
+      lc.stream = s;
+      cudaLaunchAttribute at[1];
+      lc.attrs = at;
+      lc.numAttrs = l2_window_attr(ca.B8, 6ull * tp.nbn * ca.nkb * tp.BB, at) ? 1 : 0;
+      GT_CUDA_CHECK(cudaLaunchKernelEx(&lc, k_cols8, ca));
       GT_LAUNCH_CHECK("k_cols8");
       P.count_launch();
     }
@@ -1189,16 +1239,12 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
       cl.n_h_max = 1 << (c.depth - 1);
       cl.K = K;
       cl.level = level;
-      int nl = 0;
-      P.start();
       int rc = c.count_engine == 0
                    ? launch_count_tc(cl, (const uint8_t*)(ws + L.cols8), tc_la8_blocks(N, c.nf, c.depth),
                                      c.count_reshare == 0 ? 1 : (c.sample_base == 0 ? 2 : 0), c.sample_base,
-                                     c.sample_base + N, s, num_sms, &nl)
-                   : launch_count(cl, s, num_sms, &nl);
+                                     c.sample_base + N, s, num_sms, P)
+                   : launch_count(cl, s, num_sms, P);
       if (rc) return rc;
-      P.stop(Prof::COUNT);
-      for (int i = 1; i < nl; ++i) P.count_launch();
     }
     if (c.count_engine == 1 && (c.count_reshare == 0 ? N > 0 : c.sample_base == 0)) {  // tensor engine: in k_count_mma
       const int cells = n_h * (int)W;

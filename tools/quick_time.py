@@ -33,7 +33,7 @@ print("C2 train ms (min, med):", timed(lambda: tr.run(X, Y, fill, keys)), flush=
 from paper_2305_00645_b200 import _native as _nv
 pr = _nv.gt_train_profile()
 tr.run(X, Y, fill, keys, profile=pr); torch.cuda.synchronize()
-print("C2 per-kernel ms:", {k: round(getattr(pr, "ms_" + k), 4) for k in ("prods", "partition", "count", "node_hc", "node_finish")}, flush=True)
+print("C2 per-kernel ms:", {k: round(getattr(pr, "ms_" + k), 4) for k in ("prods", "partition", "count_lanes", "count_contract", "node_hc", "node_finish")}, flush=True)
 tr_dot = DeviceTrainer(48842, 13, TrainConfig(depth=7, count_reshare="dot"))
 print("C2 dot ms (min, med):", timed(lambda: tr_dot.run(X, Y, fill, keys)), flush=True)
 if os.environ.get("QT_TRAIN_ONLY"):
