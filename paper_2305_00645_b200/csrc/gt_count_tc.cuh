@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(256) k_cols8(Cols8Args a) {
 
 // --- A operand: one CTA per (128-sample block, 16-node M tile) of a chunk;
 // lanes la = b2a(eq(m_idx, off+n) & is_leaf[n]) (train.py:328-331, the same
-// LaneRand schedule as k_count_lanes), four consecutive samples of one node
+// randomness as k_count_lanes: count_lane_pair), two samples of one node
 // per work item so each limb row leaves as one packed 32-bit word; the byte
 // planes la8[c][mt][kbc][kc 8][g 16][p 8][16] are stored straight from
 // registers (each warp store covers whole 32-byte sectors).  is_leaf of the tile's 16 nodes (train.py:320) is drawn
@@ -128,48 +128,55 @@ __global__ void __launch_bounds__(256) k_count_lanes8(Lanes8Args a) {
     for (int c = 0; c < 3; ++c) leaf[c][tid] = z.v[c] & 1ull;
   }
   __syncthreads();
-  // one lane per thread; a warp = 32 consecutive samples of one node, a quad
-  // = 4 consecutive samples whose limb bytes are transposed in registers
-  // (3 shuffles + 3 byte permutes per 32-bit half) so lane j of the quad
-  // stores limbs j and j+4 of its 4 samples as two packed words.
-  const int qj = threadIdx.x & 3;
-  const uint32_t sel = (uint32_t)qj | ((uint32_t)(4 + qj) << 4);
-  for (int e = tid; e < 16 * TC_KB; e += blockDim.x) {
-    const int nn = e / TC_KB, ss = e % TC_KB;
+  // one PAIR of samples per thread (their zero words share a pair block); a
+  // warp = 64 consecutive samples of one node.  Threads t, t^1 hold samples
+  // 4k..4k+3: limb bytes are packed with byte permutes, one shuffle pair per
+  // component, and the even thread stores limbs 0..3 of the 4 samples, the
+  // odd thread limbs 4..7, one 32-bit word each.
+  const bool odd = threadIdx.x & 1;
+  for (int e = tid; e < 16 * (TC_KB / 2); e += blockDim.x) {
+    const int nn = e / (TC_KB / 2), s2 = (e % (TC_KB / 2)) * 2;
     const int n = mt * 16 + nn;
-    const uint64_t s = (uint64_t)kb * TC_KB + ss;
-    A3 l = a3(0, 0, 0);
+    const uint64_t s = (uint64_t)kb * TC_KB + s2;
+    A3 l0 = a3(0, 0, 0), l1 = a3(0, 0, 0);
     if (n < a.n_h && s < a.cn) {
       const uint64_t gs = a.s0 + s;
-      const uint64_t lane = (a.base + gs) * (uint64_t)a.n_h + (uint64_t)n;
-      const A3 d = add_pub<64>(a3(__ldg(a.midx + gs), __ldg(a.midx + a.N + gs), __ldg(a.midx + 2 * a.N + gs)),
-                               0ull - (uint64_t)(a.off + n));
-      const LaneRand Rr = lane_rand(a.K, a.op_cnt, 0, lane);
-      const B3 hit = eq_arith<64>(d, Rr.r, Rr.Rb0, Rr.Rb1, Rr.Zw);
+      const bool v1 = s + 1 < a.cn;
+      const uint64_t off = 0ull - (uint64_t)(a.off + n);
+      const A3 d0 = add_pub<64>(a3(__ldg(a.midx + gs), __ldg(a.midx + a.N + gs), __ldg(a.midx + 2 * a.N + gs)), off);
+      A3 d1 = a3(0, 0, 0);
+      if (v1)
+        d1 = add_pub<64>(a3(__ldg(a.midx + gs + 1), __ldg(a.midx + a.N + gs + 1), __ldg(a.midx + 2 * a.N + gs + 1)), off);
       B3 lf;
-      uint64_t Z[3];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        lf.v[c] = leaf[c][nn];
-        Z[c] = Rr.F[c] & 1ull;
-      }
-      l = b2a_arith<64>(and_z(hit, lf, Z), Rr.A0, Rr.A1, Rr.bits);
+      for (int c = 0; c < 3; ++c) lf.v[c] = leaf[c][nn];
+      count_lane_pair(a.K, a.op_cnt, a.base + gs, a.n_h, n, d0, d1, true, v1, lf, &l0, &l1);
     }
-    const int qb = threadIdx.x & ~3;  // quad base lane
-    const int o = (((ss >> 4) * 16 + nn) * 8) * 16 + ((ss & ~3) & 15);
+    const int o = (((s2 >> 4) * 16 + nn) * 8) * 16 + ((s2 & ~3) & 15);
+    const int p0 = odd ? 4 : 0;
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t wv = (uint32_t)(l.v[c] >> (32 * h));
-        const uint32_t w0 = __shfl_sync(0xffffffffu, wv, qb + 0);
-        const uint32_t w1 = __shfl_sync(0xffffffffu, wv, qb + 1);
-        const uint32_t w2 = __shfl_sync(0xffffffffu, wv, qb + 2);
-        const uint32_t w3 = __shfl_sync(0xffffffffu, wv, qb + 3);
-        const uint32_t x = __byte_perm(w0, w1, sel), y = __byte_perm(w2, w3, sel);
-        // a warp's store = two contiguous 64-byte runs (4 limb rows x 16 samples)
-        *reinterpret_cast<uint32_t*>(blk + c * cstride + o + (4 * h + qj) * 16) = __byte_perm(x, y, 0x5410);
+    for (int c = 0; c < 3; ++c) {
+      const uint32_t a_lo = (uint32_t)l0.v[c], a_hi = (uint32_t)(l0.v[c] >> 32);
+      const uint32_t b_lo = (uint32_t)l1.v[c], b_hi = (uint32_t)(l1.v[c] >> 32);
+      const uint32_t P01 = __byte_perm(a_lo, b_lo, 0x5140), P23 = __byte_perm(a_lo, b_lo, 0x7362);
+      const uint32_t P45 = __byte_perm(a_hi, b_hi, 0x5140), P67 = __byte_perm(a_hi, b_hi, 0x7362);
+      const uint32_t r0 = __shfl_xor_sync(0xffffffffu, odd ? P01 : P45, 1);
+      const uint32_t r1 = __shfl_xor_sync(0xffffffffu, odd ? P23 : P67, 1);
+      uint32_t w[4];
+      if (!odd) {
+        w[0] = __byte_perm(P01, r0, 0x5410);
+        w[1] = __byte_perm(P01, r0, 0x7632);
+        w[2] = __byte_perm(P23, r1, 0x5410);
+        w[3] = __byte_perm(P23, r1, 0x7632);
+      } else {
+        w[0] = __byte_perm(r0, P45, 0x5410);
+        w[1] = __byte_perm(r0, P45, 0x7632);
+        w[2] = __byte_perm(r1, P67, 0x5410);
+        w[3] = __byte_perm(r1, P67, 0x7632);
       }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) *reinterpret_cast<uint32_t*>(blk + c * cstride + o + (p0 + i) * 16) = w[i];
+    }
   }
 }
 

@@ -121,6 +121,91 @@ __host__ __device__ inline int division_tape_blocks(const DivParams& d) {
   return newton_blocks<L>(d);
 }
 
+// ---------------------------------------------------------------------------
+// Precomputed division randomness (the division's Philox blocks depend only
+// on the keys, the op, the subs and the lane, never on data): one wide
+// kernel draws every block of every division lane of a level into a global
+// tape before the heuristic runs, so the latency-bound division chain only
+// does arithmetic.  Per lane: ladder step j (1 <= j < bound) = the lt's
+// LtRand blocks at sub s0+j-1 then the b2a dabit blocks (s0+bound-1+j-1,
+// 0..1); then the Newton chain's blocks in newton_tape_fill order.  Same
+// blocks as the live schedule, so shares are unchanged.
+template <int L>
+struct DivTape {
+  static constexpr int LADDER_STEP = LtRand<L>::BLOCKS + 2;
+};
+template <int L>
+__host__ __device__ inline int div_tape_blocks(const DivParams& d) {
+  return (d.bound - 1) * DivTape<L>::LADDER_STEP + newton_blocks<L>(d);
+}
+
+template <int L>
+__device__ __forceinline__ W2 div_tape_block(const Keys& K, uint32_t op, uint32_t s0, uint64_t lane,
+                                             const DivParams& d, int b) {
+  constexpr int LS = DivTape<L>::LADDER_STEP, LB = LtRand<L>::BLOCKS;
+  const int lbt = (d.bound - 1) * LS;
+  if (b < lbt) {
+    const int j = b / LS + 1, w = b % LS;
+    if (w < LB) {
+      int key;
+      uint32_t pidx;
+      lt_block_id<L>(w, s0 + (j - 1), &key, &pidx);
+      return word2(key < 0 ? K.dealer : K.pair[key], op, s0 + (j - 1), pidx, lane);
+    }
+    return word2(K.dealer, op, s0 + (d.bound - 1) + (j - 1), (uint32_t)(w - LB), lane);
+  }
+  b -= lbt;
+  const uint32_t sn = s0 + 2 * (d.bound - 1);
+  const int steps = newton_steps<L>(d);
+  for (int i = 0; i < steps; ++i) {
+    const ChainStep c = newton_step<L>(i, d);
+    const int nb = step_blocks<L>(c);
+    if (b < nb) {
+      const uint32_t sub = sn + c.sub_off;
+      if (c.is_trunc) {
+        int key;
+        uint32_t s, pidx;
+        trunc_block_id<L>(b, sub, &key, &s, &pidx);
+        return block_of(K, key, op, s, pidx, lane);
+      }
+      return word2(K.pair[b], op, sub, 0, lane);
+    }
+    b -= nb;
+  }
+  return W2{0, 0};
+}
+
+// Division by one warp from a precomputed lane tape `gt` (global): the
+// ladder's lt + b2a per lane straight from the tape, the Newton blocks
+// copied into the warp's shared-memory tape, then the serial chain.
+template <int L>
+__device__ __forceinline__ A3 division_warp_tape(const W2* __restrict__ gt, const A3& p, const A3& q,
+                                                 const DivParams& d, W2* tape) {
+  constexpr uint64_t M = Ring<L>::M;
+  constexpr int LS = DivTape<L>::LADDER_STEP, LB = LtRand<L>::BLOCKS;
+  const int wl = threadIdx.x & 31;
+  const int nl = d.bound - 1;
+  const int nb = newton_blocks<L>(d);
+  const W2* gn = gt + nl * LS;
+  for (int i = wl; i < nb; i += 32) tape[i] = gn[i];
+  A3 acc = a3(0, 0, 0);
+  for (int j = wl + 1; j <= nl; j += 32) {
+    const W2* b = gt + (j - 1) * LS;
+    const B3 below = lt_arith<L>(b, q, a3_const((1ull << j) & M));
+    const A3 t = b2a_arith<L>(bnot(below, 1ull), b[LB].a, b[LB].b, b[LB + 1].a);
+    acc = add<L>(acc, mul_pub<L>(t, 1ull << (d.bound - 1 - j)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) acc.v[i] = (acc.v[i] + __shfl_xor_sync(0xffffffffu, acc.v[i], o)) & M;
+  const A3 v = rsub_pub<L>(1ull << (d.bound - 1), acc);
+  __syncwarp();
+  const A3 out = newton_from_tape<L>(p, q, v, d, tape);
+  __syncwarp();
+  return out;
+}
+
 // Whole division lane by one warp; every lane returns the result.  `tape`
 // points at this warp's division_tape_blocks() W2 slots of shared memory.
 // The ladder's steps run one per lane with in-register Philox (measured

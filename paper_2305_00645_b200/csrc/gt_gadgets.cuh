@@ -448,31 +448,72 @@ __device__ __forceinline__ A3 b2a(const Keys& K, uint32_t op, uint32_t sub, uint
 }
 
 // One fused lookup / count lane (oaa.py:28-34, train.py:328-333): eq + b2a
-// (+ the select's reshare) draw from SIX Philox blocks, all halves used:
+// draw the lane's dealer material from THREE Philox blocks
 //   dealer (sub,0) = (r, Rb0)   (sub,1) = (Rb1, A0)   (sub,2) = (A1, dabit bits)
-//   pair_i (sub,0) = (AND-tree zero word, mul zero-share word F_i)
-struct LaneRand {
+// while the AND-tree zero words of two neighbouring lanes share ONE pair
+// block per key (.a / .b halves; the caller picks the block, see
+// lookup_partial and the count lane kernels).  A count lane's leaf-AND zero
+// bit is bit 63 of its zero word (the l = 64 AND tree uses bits 0..62).
+// One count lane (train.py:328-331) from its dealer material and zero word:
+// la = b2a(eq(d, 0) & leaf), the AND gate's zero bit = bit 63 of Zw.
+__device__ __forceinline__ A3 count_lane_arith(const A3& d, uint64_t r, uint64_t Rb0, uint64_t Rb1, uint64_t A0,
+                                               uint64_t A1, uint64_t bits, const uint64_t Zw[3], const B3& leaf);
+
+struct DealerRand {
   uint64_t r, Rb0, Rb1, A0, A1, bits;
-  uint64_t Zw[3], F[3];
 };
-__device__ __forceinline__ LaneRand lane_rand(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane) {
-  LaneRand R;
-  const W2 d0 = word2(K.dealer, op, sub, 0, lane);
-  const W2 d1 = word2(K.dealer, op, sub, 1, lane);
-  const W2 d2 = word2(K.dealer, op, sub, 2, lane);
+__device__ __forceinline__ DealerRand dealer_rand(const Keys& K, uint32_t op, uint64_t lane) {
+  DealerRand R;
+  const W2 d0 = word2(K.dealer, op, 0, 0, lane);
+  const W2 d1 = word2(K.dealer, op, 0, 1, lane);
+  const W2 d2 = word2(K.dealer, op, 0, 2, lane);
   R.r = d0.a;
   R.Rb0 = d0.b;
   R.Rb1 = d1.a;
   R.A0 = d1.b;
   R.A1 = d2.a;
   R.bits = d2.b;
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const W2 p = word2(K.pair[i], op, sub, 0, lane);
-    R.Zw[i] = p.a;
-    R.F[i] = p.b;
-  }
   return R;
+}
+
+__device__ __forceinline__ A3 count_lane_arith(const A3& d, uint64_t r, uint64_t Rb0, uint64_t Rb1, uint64_t A0,
+                                               uint64_t A1, uint64_t bits, const uint64_t Zw[3], const B3& leaf) {
+  const B3 hit = eq_arith<64>(d, r, Rb0, Rb1, Zw);
+  const uint64_t Z[3] = {Zw[0] >> 63, Zw[1] >> 63, Zw[2] >> 63};
+  return b2a_arith<64>(and_z(hit, leaf, Z), A0, A1, bits);
+}
+
+// The two count lanes of samples gs, gs+1 (global) at node n: their zero
+// words come from pair block (g >> 1) * n_h + n, half g & 1, for g = gs, gs+1
+// (one shared block per key when gs is even).
+__device__ __forceinline__ void count_lane_pair(const Keys& K, uint32_t op, uint64_t gs, int n_h, int n,
+                                                const A3& d0, const A3& d1, bool v0, bool v1, const B3& leaf,
+                                                A3* l0, A3* l1) {
+  uint64_t Z0[3], Z1[3];
+  if ((gs & 1) == 0) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const W2 z = word2(K.pair[i], op, 0, 0, (gs >> 1) * (uint64_t)n_h + n);
+      Z0[i] = z.a;
+      Z1[i] = z.b;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      Z0[i] = word2(K.pair[i], op, 0, 0, (gs >> 1) * (uint64_t)n_h + n).b;
+      Z1[i] = word2(K.pair[i], op, 0, 0, ((gs + 1) >> 1) * (uint64_t)n_h + n).a;
+    }
+  }
+  *l0 = a3(0, 0, 0);
+  *l1 = a3(0, 0, 0);
+  if (v0) {
+    const DealerRand R = dealer_rand(K, op, gs * (uint64_t)n_h + n);
+    *l0 = count_lane_arith(d0, R.r, R.Rb0, R.Rb1, R.A0, R.A1, R.bits, Z0, leaf);
+  }
+  if (v1) {
+    const DealerRand R = dealer_rand(K, op, (gs + 1) * (uint64_t)n_h + n);
+    *l1 = count_lane_arith(d1, R.r, R.Rb0, R.Rb1, R.A0, R.A1, R.bits, Z1, leaf);
+  }
 }
 
 // select_share (gadgets.py:238-253) for one condition lane and one payload

@@ -92,7 +92,7 @@ extern "C" int gt_infer(int depth, const uint64_t* tree, const uint64_t* queries
   uint64_t best_work = ~0ull;
   for (int G = 4; G <= 32; G <<= 1) {
     uint64_t rounds = 0;
-    for (int t = 0; t < depth; ++t) rounds += ((1ull << t) + G - 1) / G + (nf + G - 1) / G;
+    for (int t = 0; t < depth; ++t) rounds += (((1ull << t) + 1) / 2 + G - 1) / G + ((nf + 1) / 2 + G - 1) / G;
     const uint64_t work = rounds * G;
     if (n * (uint64_t)G >= target && work < best_work) {
       best_work = work;

@@ -3,27 +3,51 @@
 // entry, the hit bit is converted (b2a) and multiplies the entry (select
 // against zero), and the picked shares are summed locally.  There is no
 // data-dependent addressing: every lane reads every entry.  Lane numbering
-// is (global index) * m + j; the lane's eq, b2a and reshare draw from the six
-// Philox blocks of LaneRand at sub 0.
+// is (global index) * m + j (randomness schedule: lookup_partial).
 #pragma once
 #include "gt_gadgets.cuh"
 
 namespace gt {
 
-// Partial sum over entries j = j0, j0 + js, ... < m of one lookup.
+// Partial sum of one lookup over the entry pairs q = q0, q0 + qs, ...
+// (entries 2q, 2q+1; lane = gidx * m + j).  The pair's AND-tree zero words
+// come from one pair block per key at lane gidx * ceil(m/2) + q (.a for the
+// even entry, .b for the odd one).  The selects' reshare zero shares follow
+// the telescoping stream F_i(lane) = H_i(lane + 1) - H_i(lane) (H_i = pair_i
+// word at sub 1), so their sum over the lookup's m entries is added once, by
+// the q0 == 0 part: H_i(gidx m + m) - H_i(gidx m) per key.
 // `entry(j)` returns the A3 shares of table entry j.
 template <int L, typename Entry>
-__device__ __forceinline__ A3 lookup_partial(const Keys& K, uint32_t op, uint64_t gidx, const A3& idx, int m, int j0,
-                                             int js, Entry entry) {
+__device__ __forceinline__ A3 lookup_partial(const Keys& K, uint32_t op, uint64_t gidx, const A3& idx, int m, int q0,
+                                             int qs, Entry entry) {
+  const int mh = (m + 1) >> 1;
   A3 acc = a3(0, 0, 0);
-  for (int j = j0; j < m; j += js) {
-    const uint64_t lane = gidx * (uint64_t)m + (uint64_t)j;
-    const A3 d = add_pub<L>(idx, (0ull - (uint64_t)j) & Ring<L>::M);
-    const LaneRand R = lane_rand(K, op, 0, lane);
-    const B3 hit = eq_arith<L>(d, R.r, R.Rb0, R.Rb1, R.Zw);
-    const A3 ca = b2a_arith<L>(hit, R.A0, R.A1, R.bits);
-    // select_share(zero, rows, hit): w2 - w1 = rows (oaa.py:33)
-    acc = add<L>(acc, mul_z<L>(entry(j), ca, R.F));
+  for (int q = q0; q < mh; q += qs) {
+    W2 Z[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) Z[i] = word2(K.pair[i], op, 0, 0, gidx * (uint64_t)mh + (uint64_t)q);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = 2 * q + h;
+      if (j >= m) break;
+      const uint64_t lane = gidx * (uint64_t)m + (uint64_t)j;
+      const A3 d = add_pub<L>(idx, (0ull - (uint64_t)j) & Ring<L>::M);
+      const DealerRand R = dealer_rand(K, op, lane);
+      const uint64_t Zw[3] = {h ? Z[0].b : Z[0].a, h ? Z[1].b : Z[1].a, h ? Z[2].b : Z[2].a};
+      const B3 hit = eq_arith<L>(d, R.r, R.Rb0, R.Rb1, Zw);
+      const A3 ca = b2a_arith<L>(hit, R.A0, R.A1, R.bits);
+      // select_share(zero, rows, hit): w2 - w1 = rows (oaa.py:33); local cross terms
+      const uint64_t F0[3] = {0, 0, 0};
+      acc = add<L>(acc, mul_z<L>(entry(j), ca, F0));
+    }
+  }
+  if (q0 == 0) {
+    uint64_t F[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      F[i] = word(K.pair[i], op, 1, 0, gidx * (uint64_t)m + (uint64_t)m) - word(K.pair[i], op, 1, 0, gidx * (uint64_t)m);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) acc.v[i] = (acc.v[i] + F[i] - F[(i + 2) % 3]) & Ring<L>::M;
   }
   return acc;
 }

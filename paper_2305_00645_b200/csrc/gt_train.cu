@@ -142,39 +142,43 @@ struct LaneArgs {
   uint32_t op_cnt;
 };
 
-// One thread per (sample, node) lane of a sample chunk:
+// One thread per (sample pair, node) of a sample chunk:
 //   la = b2a(eq(m_idx, off+n) & is_leaf[n])                 train.py:328-331
-// from the six Philox blocks of LaneRand at sub 0 (pair block half b bit 0 =
-// the AND gate's zero bit).  Padding node slots are written as zero shares.
+// (dealer material per lane, the two lanes' zero words from one pair block:
+// count_lane_pair).  Padding node slots are written as zero shares.
 __global__ void __launch_bounds__(256) k_count_lanes(LaneArgs a) {
   const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t per = (uint64_t)a.nblk * a.nbp;
-  if (e >= a.cn * per) return;
-  const uint64_t s = e / per;
+  const uint64_t pairs = (a.cn + 1) / 2;
+  if (e >= pairs * per) return;
+  const uint64_t s = 2 * (e / per);
   const int r = (int)(e % per), blk = r / a.nbp, nn = r % a.nbp, n = blk * a.nb + nn;
   const uint64_t cs = (uint64_t)a.nblk * a.cap * a.nbp;
   uint64_t* out = a.la + ((uint64_t)blk * a.cap + s) * a.nbp + nn;
+  const bool v1 = s + 1 < a.cn;
   if (nn >= a.nb || n >= a.n_h) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) out[c * cs] = 0;
+    for (int c = 0; c < 3; ++c) {
+      out[c * cs] = 0;
+      if (v1) out[c * cs + a.nbp] = 0;
+    }
     return;
   }
   const uint64_t gs = a.s0 + s;
-  const uint64_t lane = (a.base + gs) * (uint64_t)a.n_h + (uint64_t)n;
-  const A3 d = add_pub<64>(a3(__ldg(a.midx + gs), __ldg(a.midx + a.N + gs), __ldg(a.midx + 2 * a.N + gs)),
-                           0ull - (uint64_t)(a.off + n));
-  const LaneRand Rr = lane_rand(a.K, a.op_cnt, 0, lane);
-  const B3 hit = eq_arith<64>(d, Rr.r, Rr.Rb0, Rr.Rb1, Rr.Zw);
+  const uint64_t off = 0ull - (uint64_t)(a.off + n);
+  const A3 d0 = add_pub<64>(a3(__ldg(a.midx + gs), __ldg(a.midx + a.N + gs), __ldg(a.midx + 2 * a.N + gs)), off);
+  A3 d1 = a3(0, 0, 0);
+  if (v1) d1 = add_pub<64>(a3(__ldg(a.midx + gs + 1), __ldg(a.midx + a.N + gs + 1), __ldg(a.midx + 2 * a.N + gs + 1)), off);
   B3 lf;
-  uint64_t Z[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) lf.v[c] = __ldg(a.leaf + c * a.n_h + n);
+  A3 l0, l1;
+  count_lane_pair(a.K, a.op_cnt, a.base + gs, a.n_h, n, d0, d1, true, v1, lf, &l0, &l1);
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    lf.v[c] = __ldg(a.leaf + c * a.n_h + n);
-    Z[c] = Rr.F[c] & 1ull;
+    out[c * cs] = l0.v[c];
+    if (v1) out[c * cs + a.nbp] = l1.v[c];
   }
-  const A3 l = b2a_arith<64>(and_z(hit, lf, Z), Rr.A0, Rr.A1, Rr.bits);
-#pragma unroll
-  for (int c = 0; c < 3; ++c) out[c * cs] = l.v[c];
 }
 
 // --- TMA bulk copies (cp.async.bulk) into shared memory, mbarrier completion
@@ -389,6 +393,7 @@ struct NodeArgs {
   uint64_t* hc;               // [4][3][n_h]: should_split, sd, new_f, new_gam
   uint64_t* dv;               // [3][3][n_h*cols]: P, Q+[Q==0], division terms
   uint64_t* co_out;           // [3][n_h][3][cols] c_orig for the tee helper (or null)
+  const W2* divtape;          // precomputed division blocks of this level (or null: draw live)
   int n_h, nf, level, last, shift, tau;
   DivParams d;
   Keys K;
@@ -529,8 +534,69 @@ __global__ void __launch_bounds__(32 * DIV_WARPS) k_hc_div(NodeArgs a) {
   W2* tape = tape_sm + (size_t)warp * division_tape_blocks<SL>(a.d);
   const A3 p = ld3s(a.dv, lanes, li), q = ld3s(a.dv + 3 * lanes, lanes, li);
   // terms = division(P, qsafe)                              train.py:382
-  const A3 t = division_warp<SL>(a.K, op_id(a.level, SITE_HC), 13, li, p, q, a.d, tape);
+  const A3 t = a.divtape ? division_warp_tape<SL>(a.divtape + li * (uint64_t)div_tape_blocks<SL>(a.d), p, q, a.d, tape)
+                         : division_warp<SL>(a.K, op_id(a.level, SITE_HC), 13, li, p, q, a.d, tape);
   if ((threadIdx.x & 31) == 0) st3s(a.dv + 6 * lanes, lanes, li, t);
+}
+
+// All division blocks of every heuristic level (see DivTape).  A per-lane
+// schedule table (block -> key, sub, Philox block index; identical for every
+// lane) is built once, then one thread per (lane, block) draws its block;
+// level h's lanes start at (2^h - 1) * cols.
+template <int SL>
+__global__ void k_div_table(uint32_t* table, DivParams d) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= div_tape_blocks<SL>(d)) return;
+  constexpr int LS = DivTape<SL>::LADDER_STEP, LB = LtRand<SL>::BLOCKS;
+  const int nl = d.bound - 1;
+  int key = -1;
+  uint32_t sub = 0, pidx = 0;  // sub relative to the division's first sub
+  if (b < nl * LS) {
+    const int j = b / LS, w = b % LS;
+    if (w < LB) {
+      lt_block_id<SL>(w, 0, &key, &pidx);
+      sub = j;
+    } else {
+      sub = nl + j, pidx = w - LB;
+    }
+  } else {
+    int r = b - nl * LS;
+    for (int i = 0; i < newton_steps<SL>(d); ++i) {
+      const ChainStep c = newton_step<SL>(i, d);
+      const int nb = step_blocks<SL>(c);
+      if (r < nb) {
+        const uint32_t s0 = 2 * nl + c.sub_off;
+        if (c.is_trunc) {
+          trunc_block_id<SL>(r, s0, &key, &sub, &pidx);
+        } else {
+          key = r, sub = s0, pidx = 0;
+        }
+        break;
+      }
+      r -= nb;
+    }
+  }
+  table[b] = (sub << 16) | (pidx << 8) | (uint32_t)(key + 1);
+}
+
+template <int SL>
+__global__ void __launch_bounds__(256) k_div_tape(W2* tape, const uint32_t* __restrict__ table, uint64_t total,
+                                                   int cols, int TB, Keys K) {
+  // the lanes of a warp draw with different keys: index the round keys in
+  // shared memory (a dynamically indexed kernel parameter serialises)
+  __shared__ Keys ks;
+  for (int i = threadIdx.x; i < (int)(sizeof(Keys) / 4); i += blockDim.x)
+    reinterpret_cast<uint32_t*>(&ks)[i] = reinterpret_cast<const uint32_t*>(&K)[i];
+  __syncthreads();
+  // 32-bit index math: the tape is capped at 256 MB (< 2^24 blocks)
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  const uint32_t g = e / (uint32_t)TB, nodes = g / (uint32_t)cols;
+  const uint32_t t = __ldg(table + (e - g * (uint32_t)TB));
+  const int level = 31 - __clz(nodes + 1);  // nodes in [2^h - 1, 2^{h+1} - 1)
+  const uint64_t li = g - ((1u << level) - 1) * (uint32_t)cols;
+  const int key = (int)(t & 0xff) - 1;
+  tape[e] = word2(key < 0 ? ks.dealer : ks.pair[key], op_id(level, SITE_HC), 13 + (t >> 16), (t >> 8) & 0xff, li);
 }
 
 template <int SL>
@@ -744,8 +810,24 @@ uint64_t tc_la8_blocks(uint64_t N, int nf, int depth) {
   return std::max<uint64_t>(1, std::min<uint64_t>(nkb, (64ull << 20) / per_blk));
 }
 
+// Division tapes of every heuristic level (levels 0 .. depth-2, mpc only),
+// in W2 units; 0 when they would exceed 256 MB (then blocks are drawn live).
+uint64_t div_tape_words(const gt_train_cfg& c) {
+  if (c.heuristic != 0 || c.depth < 2) return 0;
+  bool ok = false;
+  const DivParams d = div_params(c.score_width, c.tau, &ok);
+  if (!ok) return 0;
+  const int TB = c.score_width == 32 ? div_tape_blocks<32>(d) : div_tape_blocks<64>(d);
+  const uint64_t lanes = ((1ull << (c.depth - 1)) - 1) * 2ull * c.nf;
+  const uint64_t w = lanes * (uint64_t)TB;
+  return w * 16 > (256ull << 20) ? 0 : w;
+}
+inline uint64_t div_tape_level_off(int level, int nf, int TB) {  // W2 offset of level's tape
+  return ((1ull << level) - 1) * 2ull * nf * (uint64_t)TB;
+}
+
 struct Layout {
-  uint64_t cols, la, cols8, leaf, midx, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
+  uint64_t cols, la, cols8, leaf, midx, divtape, divtable, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
 };
 
 Layout layout(const gt_train_cfg& c) {
@@ -770,6 +852,13 @@ Layout layout(const gt_train_cfg& c) {
   }
   L.leaf = take(3 * nmax);
   L.midx = take(3 * N);
+  L.divtape = take(2 * div_tape_words(c));
+  {
+    bool ok = false;
+    const DivParams d = div_params(c.score_width, c.tau, &ok);
+    const int TB = !ok ? 0 : c.score_width == 32 ? div_tape_blocks<32>(d) : div_tape_blocks<64>(d);
+    L.divtable = take((uint64_t)(TB + 1) / 2);  // TB u32 schedule entries
+  }
   L.S = take(3 * nmax * (W + 1));
   for (int i = 0; i < 2; ++i) {
     L.f[i] = take(3 * ch);
@@ -831,7 +920,7 @@ int launch_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint6
   int best = 16;
   uint64_t best_work = ~0ull;
   for (int G = 2; G <= 16; G <<= 1) {
-    const uint64_t work = (uint64_t)G * ((m + G - 1) / G + (nf + G - 1) / G);
+    const uint64_t work = (uint64_t)G * (((m + 1) / 2 + G - 1) / G + ((nf + 1) / 2 + G - 1) / G);
     if (N * (uint64_t)G >= target && work < best_work) {
       best_work = work;
       best = G;
@@ -971,7 +1060,7 @@ int launch_count(const CountLaunch& c, cudaStream_t s, int num_sms, Prof& P) {
     la.nblk = p.nblk;
     la.K = c.K;
     la.op_cnt = op_id(c.level, SITE_COUNT);
-    const uint64_t lanes = cn * p.nblk * p.nbp;
+    const uint64_t lanes = (cn + 1) / 2 * p.nblk * p.nbp;
     P.start();
     k_count_lanes<<<(unsigned)((lanes + 255) / 256), 256, 0, s>>>(la);
     GT_LAUNCH_CHECK("k_count_lanes");
@@ -1212,6 +1301,25 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
     }
     P.stop(Prof::PRODS);
   }
+  // the division randomness of every level is data-independent: draw it all now
+  const uint64_t tape_words = div_tape_words(c);
+  if (tape_words) {
+    const int cols_i = 2 * c.nf;
+    const int TB = c.score_width == 32 ? div_tape_blocks<32>(d) : div_tape_blocks<64>(d);
+    uint32_t* table = reinterpret_cast<uint32_t*>(ws + L.divtable);
+    W2* tape = reinterpret_cast<W2*>(ws + L.divtape);
+    P.start();
+    if (c.score_width == 32) {
+      k_div_table<32><<<(TB + 127) / 128, 128, 0, s>>>(table, d);
+      k_div_tape<32><<<(unsigned)((tape_words + 255) / 256), 256, 0, s>>>(tape, table, tape_words, cols_i, TB, K);
+    } else {
+      k_div_table<64><<<(TB + 127) / 128, 128, 0, s>>>(table, d);
+      k_div_tape<64><<<(unsigned)((tape_words + 255) / 256), 256, 0, s>>>(tape, table, tape_words, cols_i, TB, K);
+    }
+    P.count_launch();
+    GT_LAUNCH_CHECK("k_div_tape");
+    P.stop(Prof::NODE_HC);
+  }
   int32_t trained = c.depth;
   for (int level = 0; level < c.depth; ++level) {
     const int n_h = 1 << level;
@@ -1268,6 +1376,10 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
     na.hc = hc;
     na.dv = ws + L.dv;
     na.co_out = tee ? ws + L.co : nullptr;
+    na.divtape = tape_words ? reinterpret_cast<const W2*>(ws + L.divtape) +
+                                  div_tape_level_off(level, c.nf, c.score_width == 32 ? div_tape_blocks<32>(d)
+                                                                                      : div_tape_blocks<64>(d))
+                            : nullptr;
     na.n_h = n_h;
     na.nf = c.nf;
     na.level = level;
