@@ -26,9 +26,8 @@ namespace gt {
 namespace {
 
 constexpr int TC_KB = 128;                // samples per K block
-constexpr int TC_STAGES = 5;              // smem ring depth
 constexpr int TC_ABLK = TC_KB * 128;      // bytes of an A block: 128 rows (16 nodes x 8 limbs) x 128 samples
-constexpr int TC_MAX_KB_PER_CTA = 64;     // 2 x 64 x 128 x 255^2 < 2^31
+constexpr int TC_MAX_KB_PER_CTA = 64;     // 2 products x 64 x 128 x 255^2 < 2^31
 constexpr int TC_TMEM_COLS = 256;
 
 struct TcPlan {
@@ -52,7 +51,9 @@ inline TcPlan tc_plan(int nf, int n_h) {
 }
 
 // --- B operand: the level-invariant sample columns as byte planes
-// B8[c][term][nb][kb][kc 8][g cpb][q 8][16 samples]; term 0 = u_c, term 1 = x_c.
+// B8[c][nb][kb][half 2][term 2][kc 4][g cpb][q 8][16 samples]; term 0 =
+// u_c = x_c + x_{c+1} (1 on the mask column), term 1 = x_c (0 there): the
+// two terms of a 64-sample half block are one contiguous run (one copy).
 struct Cols8Args {
   const uint64_t* cols;  // [3][N][WC] u64 (x | prods | y | 0 ...)
   uint8_t* B8;
@@ -60,51 +61,62 @@ struct Cols8Args {
   int WC, W, cpb, nbn;
 };
 __global__ void __launch_bounds__(256) k_cols8(Cols8Args a) {
+  // one thread per (K block, 16-sample chunk, column): the three components
+  // of 16 samples are read once and all six (component, term) planes written
   const int WG = a.nbn * a.cpb;
   const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t total = 6ull * a.nkb * 8 * WG;
+  const uint64_t total = a.nkb * 8 * WG;
   if (e >= total) return;
   const int wg = (int)(e % WG);
-  uint64_t r = e / WG;
+  const uint64_t r = e / WG;
   const int kc = (int)(r % 8);
-  r /= 8;
-  const uint64_t kb = r % a.nkb;
-  r /= a.nkb;
-  const int term = (int)(r % 2), c = (int)(r / 2);
+  const uint64_t kb = r / 8;
   const int nb = wg / a.cpb, g = wg % a.cpb, w = wg;
   const uint64_t cs = a.N * (uint64_t)a.WC;
-  uint32_t pk[8][4];
+#pragma unroll 1
+  for (int c = 0; c < 3; ++c) {
+    uint32_t pk[2][8][4];
 #pragma unroll
-  for (int q = 0; q < 8; ++q)
+    for (int t = 0; t < 2; ++t)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) pk[q][k] = 0;
+      for (int q = 0; q < 8; ++q)
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const uint64_t s = kb * TC_KB + kc * 16 + i;
-    uint64_t v = 0;
-    if (s < a.N) {
-      if (w < a.W) {
-        const uint64_t xc = __ldg(a.cols + c * cs + s * a.WC + w);
-        v = term ? xc : xc + __ldg(a.cols + ((c + 1) % 3) * cs + s * a.WC + w);
-      } else if (w == a.W) {
-        v = term ? 0ull : 1ull;  // mask column: s_mask += la (train.py:334)
+        for (int k = 0; k < 4; ++k) pk[t][q][k] = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const uint64_t s = kb * TC_KB + kc * 16 + i;
+      uint64_t x = 0, u = 0;
+      if (s < a.N) {
+        if (w < a.W) {
+          x = __ldg(a.cols + c * cs + s * a.WC + w);
+          u = x + __ldg(a.cols + ((c + 1) % 3) * cs + s * a.WC + w);
+        } else if (w == a.W) {
+          u = 1;  // mask column: s_mask += la (train.py:334)
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        pk[0][q][i >> 2] |= (uint32_t)((u >> (8 * q)) & 0xffu) << (8 * (i & 3));
+        pk[1][q][i >> 2] |= (uint32_t)((x >> (8 * q)) & 0xffu) << (8 * (i & 3));
       }
     }
+    const uint64_t HB = (uint64_t)8 * a.cpb * (TC_KB / 2);  // one term of a half block
 #pragma unroll
-    for (int q = 0; q < 8; ++q) pk[q][i >> 2] |= (uint32_t)((v >> (8 * q)) & 0xffu) << (8 * (i & 3));
+    for (int t = 0; t < 2; ++t) {
+      uint8_t* dst = a.B8 + ((((uint64_t)c * a.nbn + nb) * a.nkb + kb) * 2 + (kc >> 2)) * 2 * HB + t * HB +
+                     ((uint64_t)(kc & 3) * a.cpb + g) * 128;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<uint4*>(dst + q * 16) = make_uint4(pk[t][q][0], pk[t][q][1], pk[t][q][2], pk[t][q][3]);
+    }
   }
-  uint8_t* dst = a.B8 + ((((uint64_t)(c * 2 + term) * a.nbn + nb) * a.nkb + kb) * (uint64_t)(8 * a.cpb * TC_KB)) +
-                 ((uint64_t)kc * a.cpb + g) * 128;
-#pragma unroll
-  for (int q = 0; q < 8; ++q)
-    *reinterpret_cast<uint4*>(dst + q * 16) = make_uint4(pk[q][0], pk[q][1], pk[q][2], pk[q][3]);
 }
 
 // --- A operand: one CTA per (128-sample block, 16-node M tile) of a chunk;
 // lanes la = b2a(eq(m_idx, off+n) & is_leaf[n]) (train.py:328-331, the same
 // randomness as k_count_lanes: count_lane_pair), two samples of one node
 // per work item so each limb row leaves as one packed 32-bit word; the byte
-// planes la8[c][mt][kbc][kc 8][g 16][p 8][16] are stored straight from
+// planes la8[mt][kbc][half][c][kc 4][g 16][p 8][16] are stored straight from
 // registers (each warp store covers whole 32-byte sectors).  is_leaf of the tile's 16 nodes (train.py:320) is drawn
 // in the CTA (it is keyed by node only).
 struct Lanes8Args {
@@ -118,8 +130,11 @@ struct Lanes8Args {
 __global__ void __launch_bounds__(256) k_count_lanes8(Lanes8Args a) {
   __shared__ uint64_t leaf[3][16];
   const int kb = blockIdx.x, mt = blockIdx.y, tid = threadIdx.x;
-  uint8_t* blk = a.la8 + ((uint64_t)mt * a.nkbc + kb) * (uint64_t)TC_ABLK;
-  const uint64_t cstride = (uint64_t)a.mtiles * a.nkbc * TC_ABLK;
+  // la8[mt][kbc][half 2][c 3][kc 4][g 16][p 8][16]: the three components of
+  // a 64-sample half block are one contiguous 24 KB run (one bulk copy for
+  // the contraction)
+  uint8_t* blk = a.la8 + ((uint64_t)mt * a.nkbc + kb) * (uint64_t)(3 * TC_ABLK);
+  const uint64_t cstride = TC_ABLK / 2;
   if (tid < 16) {
     const int n = mt * 16 + tid;
     B3 z = {{0, 0, 0}};
@@ -152,7 +167,7 @@ __global__ void __launch_bounds__(256) k_count_lanes8(Lanes8Args a) {
       for (int c = 0; c < 3; ++c) lf.v[c] = leaf[c][nn];
       count_lane_pair(a.K, a.op_cnt, a.base + gs, a.n_h, n, d0, d1, true, v1, lf, &l0, &l1);
     }
-    const int o = (((s2 >> 4) * 16 + nn) * 8) * 16 + ((s2 & ~3) & 15);
+    const int o = (s2 >> 6) * (3 * TC_ABLK / 2) + ((((s2 >> 4) & 3) * 16 + nn) * 8) * 16 + ((s2 & ~3) & 15);
     const int p0 = odd ? 4 : 0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -211,22 +226,31 @@ struct MmaArgs {
   uint64_t nkbc, nkb_total, kb_base;  // chunk capacity (blocks), shard blocks, chunk's first global block
   uint32_t nkb;                       // blocks in this chunk
   int n_h, W, cpb, nbn, mtiles, N, nkr;
+  int probe;  // diagnostics only (GT_MMA_PROBE): 1 = loads without MMAs, 2 = MMAs without loads
 };
 
-// grid (K ranges, M tiles x column blocks, component).  Thread 0 drives the
-// bulk-copy ring and issues the MMAs; all four warps read the accumulator
-// back (warp w owns TMEM lanes 32w..32w+31), fold the limbs, reduce the 8
-// limb rows of a node by shuffles and add into S.
+// One CTA per (K range, M tile, column block, component c): the party-local
+// cross terms of component c
+//     D_c = A_c U_c + A_{c+1} X_c        (U_c = x_c + x_{c+1}, rss.py:391-395)
+// A stage is one 64-sample half block brought by TWO contiguous bulk copies
+// (the three components' la planes, 24 KB, of which A_c and A_{c+1} are
+// used; the (U_c, X_c) planes, N x 128 B), four stages in flight: bulk
+// copies pay a fixed latency each, so few large requests with several in
+// flight keep the SM's copy engine streaming.
+constexpr int TC_MC_STAGES = 4;
+constexpr int TC_A_HB = 3 * TC_ABLK / 2;  // the 3 components' la planes of a half block
 __global__ void __launch_bounds__(128, 1) k_count_mma(MmaArgs a) {
   extern __shared__ __align__(1024) uint8_t smt[];
-  __shared__ __align__(8) uint64_t full[TC_STAGES], empty[TC_STAGES], done;
+  __shared__ __align__(8) uint64_t full[TC_MC_STAGES], empty[TC_MC_STAGES], done;
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int c = blockIdx.z, mt = blockIdx.y / a.nbn, nb = blockIdx.y % a.nbn;
+  const int cn = (c + 1) % 3, cp = (c + 2) % 3;
   const uint32_t per = (a.nkb + a.nkr - 1) / a.nkr;
   const uint32_t kb0 = blockIdx.x * per, kb1 = min(a.nkb, kb0 + per);
-  const int T = kb1 > kb0 ? 2 * (int)(kb1 - kb0) : 0;
-  const int BB = a.N * TC_KB, stage = TC_ABLK + BB;
+  const int T = kb1 > kb0 ? 2 * (int)(kb1 - kb0) : 0;  // half blocks
+  const int HB = a.N * (TC_KB / 2);                     // one term of a half block
+  const int stage = TC_A_HB + 2 * HB;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
@@ -235,7 +259,7 @@ __global__ void __launch_bounds__(128, 1) k_count_mma(MmaArgs a) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (tid == 32) {
-    for (int i = 0; i < TC_STAGES; ++i) {
+    for (int i = 0; i < TC_MC_STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
@@ -251,33 +275,41 @@ __global__ void __launch_bounds__(128, 1) k_count_mma(MmaArgs a) {
     // idesc: S32 accumulator [4,6) = 2, A/B unsigned 8-bit, K-major, N>>3 at 17, M>>4 at 24
     const uint32_t idesc = (2u << 4) | ((uint32_t)(a.N >> 3) << 17) | ((128u >> 4) << 24);
     auto load = [&](int t) {
-      const int st = t % TC_STAGES, term = t & 1;
-      const uint64_t kb = kb0 + (uint32_t)(t >> 1);
-      uint8_t* sA = smt + st * stage;
-      const int ca = term ? (c + 1) % 3 : c;
-      mbar_expect_tx(&full[st], (uint32_t)stage);
-      bulk_g2s(sA, a.la8 + (((uint64_t)ca * a.mtiles + mt) * a.nkbc + kb) * (uint64_t)TC_ABLK, TC_ABLK, &full[st]);
-      bulk_g2s(sA + TC_ABLK,
-               a.B8 + ((((uint64_t)(c * 2 + term) * a.nbn + nb) * a.nkb_total + a.kb_base + kb) * (uint64_t)BB),
-               (uint32_t)BB, &full[st]);
+      const int st = t % TC_MC_STAGES;
+      const uint64_t kb = kb0 + (uint32_t)(t >> 1), h = t & 1;
+      uint8_t* sb = smt + st * stage;
+      // A_c, A_{c+1} only: adjacent planes for c = 0, 1; component 2 needs
+      // planes 2 and 0, so it takes the whole 24 KB run
+      const uint32_t aoff = c < 2 ? (uint32_t)c * (TC_ABLK / 2) : 0u, alen = c < 2 ? (uint32_t)TC_ABLK : TC_A_HB;
+      mbar_expect_tx(&full[st], alen + 2u * HB);
+      bulk_g2s(sb + aoff, a.la8 + (((uint64_t)mt * a.nkbc + kb) * 2 + h) * (uint64_t)TC_A_HB + aoff, alen, &full[st]);
+      bulk_g2s(sb + TC_A_HB,
+               a.B8 + ((((uint64_t)c * a.nbn + nb) * a.nkb_total + a.kb_base + kb) * 2 + h) * (uint64_t)(2 * HB),
+               (uint32_t)(2 * HB), &full[st]);
     };
-    for (int t = 0; t < min(TC_STAGES, T); ++t) load(t);
+    if (a.probe != 2)
+      for (int t = 0; t < min(TC_MC_STAGES, T); ++t) load(t);
     for (int t = 0; t < T; ++t) {
-      const int st = t % TC_STAGES;
-      mbar_wait(&full[st], (uint32_t)((t / TC_STAGES) & 1));
+      const int st = t % TC_MC_STAGES;
+      if (a.probe != 2) mbar_wait(&full[st], (uint32_t)((t / TC_MC_STAGES) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t sA = smem_u32(smt + st * stage), sB = sA + TC_ABLK;
+      const uint32_t base = smem_u32(smt + st * stage);
+      const uint32_t Ac = base + c * (TC_ABLK / 2), An = base + cn * (TC_ABLK / 2);
+      const uint32_t Uc = base + TC_A_HB, Xc = Uc + HB;
+      if (a.probe != 1)
 #pragma unroll
-      for (int j = 0; j < TC_KB / 32; ++j) {
-        const uint64_t ad = umma_desc(sA + j * 2 * (16 * 128), 16 * 128, 128);
-        const uint64_t bd = umma_desc(sB + j * 2 * (a.cpb * 128), a.cpb * 128, 128);
-        umma_i8(tmem, ad, bd, idesc, (t > 0 || j > 0) ? 1u : 0u);
+      for (int j = 0; j < 2; ++j) {
+        const uint32_t ao = j * 2 * (16 * 128), xo = j * 2 * (a.cpb * 128);
+        umma_i8(tmem, umma_desc(Ac + ao, 16 * 128, 128), umma_desc(Uc + xo, a.cpb * 128, 128), idesc,
+                (t > 0 || j > 0) ? 1u : 0u);
+        umma_i8(tmem, umma_desc(An + ao, 16 * 128, 128), umma_desc(Xc + xo, a.cpb * 128, 128), idesc, 1u);
       }
       umma_commit(&empty[st]);
-      if (t >= 1 && t - 1 + TC_STAGES < T) {
-        const int p = (t - 1) % TC_STAGES;
-        mbar_wait(&empty[p], (uint32_t)(((t - 1) / TC_STAGES) & 1));
-        load(t - 1 + TC_STAGES);
+      // refill the previous stage (its MMAs were issued one step earlier)
+      if (a.probe != 2 && t >= 1 && t - 1 + TC_MC_STAGES < T) {
+        const int pst = (t - 1) % TC_MC_STAGES;
+        mbar_wait(&empty[pst], (uint32_t)(((t - 1) / TC_MC_STAGES) & 1));
+        load(t - 1 + TC_MC_STAGES);
       }
     }
     umma_commit(&done);
@@ -317,7 +349,7 @@ __global__ void __launch_bounds__(128, 1) k_count_mma(MmaArgs a) {
             uint64_t F[2];
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
-              const Key& key = a.K.pair[q == 0 ? c : (c + 2) % 3];
+              const Key& key = a.K.pair[q == 0 ? c : cp];
               F[q] = a.alpha == 2 ? word(key, a.op_cnt, 4, (uint32_t)w, (uint64_t)n)
                                   : word(key, a.op_cnt, 3, (uint32_t)w, a.t1 * (uint64_t)a.n_h + n) -
                                         word(key, a.op_cnt, 3, (uint32_t)w, a.t0 * (uint64_t)a.n_h + n);

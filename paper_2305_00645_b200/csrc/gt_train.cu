@@ -801,13 +801,13 @@ uint64_t la_words(uint64_t N, int nf, int depth) {
   return std::min<uint64_t>(want, per * std::max<uint64_t>(N, 1));
 }
 
-// la8 chunk capacity in 128-sample blocks (tensor engine): ~64 MB of byte
+// la8 chunk capacity in 128-sample blocks (tensor engine): ~48 MB of byte
 // planes at the deepest level, at least one block, at most the shard
 uint64_t tc_la8_blocks(uint64_t N, int nf, int depth) {
   const TcPlan tp = tc_plan(nf, 1 << (depth - 1));
   const uint64_t per_blk = 3ull * tp.mtiles * TC_ABLK;
   const uint64_t nkb = std::max<uint64_t>(1, (N + TC_KB - 1) / TC_KB);
-  return std::max<uint64_t>(1, std::min<uint64_t>(nkb, (64ull << 20) / per_blk));
+  return std::max<uint64_t>(1, std::min<uint64_t>(nkb, (48ull << 20) / per_blk));
 }
 
 // Division tapes of every heuristic level (levels 0 .. depth-2, mpc only),
@@ -1098,6 +1098,8 @@ int launch_count(const CountLaunch& c, cudaStream_t s, int num_sms, Prof& P) {
 // carve-out is raised once per device to cover it (bounded by the device max).
 bool l2_window_attr(const void* base, uint64_t bytes, cudaLaunchAttribute* at) {
   static int max_persist = -1, max_window = 0;
+  static const bool off = getenv("GT_NO_L2_WINDOW") != nullptr;  // A/B experiments
+  if (off) return false;
   if (max_persist < 0) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess ||
@@ -1128,7 +1130,7 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
   la8_blocks = std::min<uint64_t>(la8_blocks * mt_max / tp.mtiles, (c.N + TC_KB - 1) / TC_KB);
   const uint64_t cap = la8_blocks * TC_KB;
   const uint64_t nkb_total = (c.N + TC_KB - 1) / TC_KB;
-  const int smem = TC_STAGES * (TC_ABLK + tp.BB);
+  const int smem = TC_MC_STAGES * (TC_A_HB + tp.BB);
   GT_CUDA_CHECK(cudaFuncSetAttribute(k_count_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   for (uint64_t s0 = 0; s0 < c.N; s0 += cap) {
     const uint64_t cn = std::min<uint64_t>(cap, c.N - s0);
@@ -1168,6 +1170,10 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
     ma.N = tp.N;
     ma.K = c.K;
     ma.op_cnt = op_id(c.level, SITE_COUNT);
+    {
+      static const int probe = getenv("GT_MMA_PROBE") ? atoi(getenv("GT_MMA_PROBE")) : 0;
+      ma.probe = probe;
+    }
     ma.alpha = s0 == 0 ? alpha : 0;
     ma.t0 = t0;
     ma.t1 = t1;
@@ -1287,7 +1293,7 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
       ca.W = 2 * c.nf + 1;
       ca.cpb = tp.cpb;
       ca.nbn = tp.nbn;
-      const uint64_t thr = 6ull * ca.nkb * 8 * tp.nbn * tp.cpb;
+      const uint64_t thr = ca.nkb * 8 * tp.nbn * tp.cpb;
       cudaLaunchConfig_t lc{};
       lc.gridDim = dim3((unsigned)((thr + 255) / 256));
       lc.blockDim = dim3(256);
