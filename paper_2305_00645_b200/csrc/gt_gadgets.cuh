@@ -233,6 +233,79 @@ __device__ __forceinline__ B3 eq_arith<64>(const A3& d, uint64_t r, uint64_t Rb0
   return out;
 }
 
+// Two l = 64 eq lanes at once: the first AND level runs per lane on the
+// 32-bit halves; from the second level on both lanes share every 32-bit
+// register (lane A in the low half, lane B in the high half of each packed
+// field, packed with byte permutes), halving the AND-tree instructions.
+// Same gates, same zero bits as eq_arith<64> (levels at offsets 0, 32, 48,
+// 56, 60, 62 of each lane's zero words).  Returns lane A / lane B in bit 0 of
+// hA / hB.
+__device__ __forceinline__ void eq_arith64_x2(const A3& dA, uint64_t rA, uint64_t Rb0A, uint64_t Rb1A,
+                                              const uint64_t ZA[3], const A3& dB, uint64_t rB, uint64_t Rb0B,
+                                              uint64_t Rb1B, const uint64_t ZB[3], B3* hA, B3* hB) {
+  const uint64_t cA = open<64>(dA) + rA, cB = open<64>(dB) + rB;
+  const uint64_t PA[3] = {Rb0A ^ ~cA, Rb1A, rA ^ Rb0A ^ Rb1A};
+  const uint64_t PB[3] = {Rb0B ^ ~cB, Rb1B, rB ^ Rb0B ^ Rb1B};
+  uint32_t a[3], b[3], z[3], wA[3], wB[3];
+  // level 1 (64 -> 32) per lane
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    a[i] = (uint32_t)PA[i];
+    b[i] = (uint32_t)(PA[i] >> 32);
+    z[i] = (uint32_t)ZA[i];
+  }
+  and3_32(a, b, z, wA);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    a[i] = (uint32_t)PB[i];
+    b[i] = (uint32_t)(PB[i] >> 32);
+    z[i] = (uint32_t)ZB[i];
+  }
+  and3_32(a, b, z, wB);
+  uint32_t zhA[3], zhB[3], w[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    zhA[i] = (uint32_t)(ZA[i] >> 32);
+    zhB[i] = (uint32_t)(ZB[i] >> 32);
+  }
+  // level 2 (32 -> 16): halves 0..15 / 16..31 of each lane, packed A | B << 16
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    a[i] = __byte_perm(wA[i], wB[i], 0x5410);
+    b[i] = __byte_perm(wA[i], wB[i], 0x7632);
+    z[i] = __byte_perm(zhA[i], zhB[i], 0x5410);  // zero bits 0..15 of each lane's high word
+  }
+  and3_32(a, b, z, w);  // lane A bits 0..15, lane B bits 16..31
+  // level 3 (16 -> 8): bytes [A0 A1 B0 B1] -> a = [A0 B0], b = [A1 B1]
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    a[i] = __byte_perm(w[i], 0, 0x4420);
+    b[i] = __byte_perm(w[i], 0, 0x4431);
+    z[i] = __byte_perm(zhA[i], zhB[i], 0x4462);  // zero bits 16..23 of each lane
+  }
+  and3_32(a, b, z, w);  // lane A byte 0, lane B byte 1
+  // levels 4..6 (8 -> 4 -> 2 -> 1) within each lane's byte
+  uint32_t zz[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) zz[i] = __byte_perm(zhA[i], zhB[i], 0x4473);  // zero bits 24..31
+#pragma unroll
+  for (int lvl = 0, half = 4, off = 0; lvl < 3; ++lvl, off += half, half >>= 1) {
+    const uint32_t lm = ((1u << half) - 1u) * 0x0101u;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      a[i] = w[i] & lm;
+      b[i] = (w[i] >> half) & lm;
+      z[i] = (zz[i] >> off) & lm;
+    }
+    and3_32(a, b, z, w);
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    hA->v[i] = w[i] & 1u;
+    hB->v[i] = (w[i] >> 8) & 1u;
+  }
+}
+
 // standalone eq: dealer fields r=0 Rb0=1 Rb1=2; pair field 0 = AND-tree bits.
 template <int L>
 __device__ __forceinline__ B3 eqz(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const A3& d) {
@@ -504,16 +577,18 @@ __device__ __forceinline__ void count_lane_pair(const Keys& K, uint32_t op, uint
       Z1[i] = word2(K.pair[i], op, 0, 0, ((gs + 1) >> 1) * (uint64_t)n_h + n).a;
     }
   }
-  *l0 = a3(0, 0, 0);
-  *l1 = a3(0, 0, 0);
-  if (v0) {
-    const DealerRand R = dealer_rand(K, op, gs * (uint64_t)n_h + n);
-    *l0 = count_lane_arith(d0, R.r, R.Rb0, R.Rb1, R.A0, R.A1, R.bits, Z0, leaf);
-  }
-  if (v1) {
-    const DealerRand R = dealer_rand(K, op, (gs + 1) * (uint64_t)n_h + n);
-    *l1 = count_lane_arith(d1, R.r, R.Rb0, R.Rb1, R.A0, R.A1, R.bits, Z1, leaf);
-  }
+  // both lanes always computed (the second lane of a shard's odd tail is
+  // discarded by the caller)
+  (void)v0;
+  (void)v1;
+  const DealerRand R0 = dealer_rand(K, op, gs * (uint64_t)n_h + n);
+  const DealerRand R1 = dealer_rand(K, op, (gs + 1) * (uint64_t)n_h + n);
+  B3 h0, h1;
+  eq_arith64_x2(d0, R0.r, R0.Rb0, R0.Rb1, Z0, d1, R1.r, R1.Rb0, R1.Rb1, Z1, &h0, &h1);
+  const uint64_t Y0[3] = {Z0[0] >> 63, Z0[1] >> 63, Z0[2] >> 63};
+  const uint64_t Y1[3] = {Z1[0] >> 63, Z1[1] >> 63, Z1[2] >> 63};
+  *l0 = b2a_arith<64>(and_z(h0, leaf, Y0), R0.A0, R0.A1, R0.bits);
+  *l1 = b2a_arith<64>(and_z(h1, leaf, Y1), R1.A0, R1.A1, R1.bits);
 }
 
 // select_share (gadgets.py:238-253) for one condition lane and one payload

@@ -26,6 +26,20 @@ __device__ __forceinline__ A3 lookup_partial(const Keys& K, uint32_t op, uint64_
     W2 Z[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) Z[i] = word2(K.pair[i], op, 0, 0, gidx * (uint64_t)mh + (uint64_t)q);
+    const uint64_t F0[3] = {0, 0, 0};
+    if (L == 64) {  // both entries' eq trees packed together (eq_arith64_x2)
+      const int j0 = 2 * q, j1 = 2 * q + 1;
+      const uint64_t lane0 = gidx * (uint64_t)m + (uint64_t)j0;
+      const A3 d0 = add_pub<L>(idx, 0ull - (uint64_t)j0), d1 = add_pub<L>(idx, 0ull - (uint64_t)j1);
+      const DealerRand R0 = dealer_rand(K, op, lane0), R1 = dealer_rand(K, op, lane0 + 1);
+      const uint64_t Z0[3] = {Z[0].a, Z[1].a, Z[2].a}, Z1[3] = {Z[0].b, Z[1].b, Z[2].b};
+      B3 h0, h1;
+      eq_arith64_x2(d0, R0.r, R0.Rb0, R0.Rb1, Z0, d1, R1.r, R1.Rb0, R1.Rb1, Z1, &h0, &h1);
+      // select_share(zero, rows, hit): w2 - w1 = rows (oaa.py:33); local cross terms
+      acc = add<L>(acc, mul_z<L>(entry(j0), b2a_arith<L>(h0, R0.A0, R0.A1, R0.bits), F0));
+      if (j1 < m) acc = add<L>(acc, mul_z<L>(entry(j1), b2a_arith<L>(h1, R1.A0, R1.A1, R1.bits), F0));
+      continue;
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int j = 2 * q + h;
@@ -36,8 +50,6 @@ __device__ __forceinline__ A3 lookup_partial(const Keys& K, uint32_t op, uint64_
       const uint64_t Zw[3] = {h ? Z[0].b : Z[0].a, h ? Z[1].b : Z[1].a, h ? Z[2].b : Z[2].a};
       const B3 hit = eq_arith<L>(d, R.r, R.Rb0, R.Rb1, Zw);
       const A3 ca = b2a_arith<L>(hit, R.A0, R.A1, R.bits);
-      // select_share(zero, rows, hit): w2 - w1 = rows (oaa.py:33); local cross terms
-      const uint64_t F0[3] = {0, 0, 0};
       acc = add<L>(acc, mul_z<L>(entry(j), ca, F0));
     }
   }
