@@ -51,6 +51,9 @@ struct W2 {
 };
 
 __device__ __forceinline__ W2 philox(const Key& key, uint32_t op, uint32_t stream, uint64_t lane) {
+#ifdef GT_FAKE_PRG  // timing experiments only: a cheap non-random stand-in
+  { W2 w; w.a = lane * 0x9E3779B97F4A7C15ull + stream + key.k0[0]; w.b = w.a ^ ((uint64_t)op << 17); return w; }
+#endif
   uint32_t c0 = (uint32_t)lane, c1 = (uint32_t)(lane >> 32), c2 = stream, c3 = op;
 #pragma unroll
   for (int r = 0; r < 10; ++r) {

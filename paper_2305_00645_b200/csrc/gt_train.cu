@@ -401,30 +401,127 @@ struct NodeArgs {
 
 __device__ __forceinline__ void bar_workers() { asm volatile("bar.sync 1, 192;" ::: "memory"); }
 
-template <int SL>
-__global__ void __launch_bounds__(256) k_hc_pre(NodeArgs a) {
-  extern __shared__ uint64_t sm[];
-  constexpr uint64_t MS = Ring<SL>::M;
-  const int n = blockIdx.x, tid = threadIdx.x;
+// c_orig cell e = (row r, column k) of node n: c_start + the counters
+// assembled from the count partials (train.py:256, 336-343)
+__device__ __forceinline__ uint64_t co_cell(const NodeArgs& a, int c, int n, int e) {
   const int nf = a.nf, cols = 2 * nf, W = cols + 1, C3 = 3 * cols;
+  const uint64_t hs = (uint64_t)a.n_h;
+  const int r = e / cols, k = e % cols, i = k >> 1, j = k & 1;
+  const uint64_t* Sn = a.S + (uint64_t)c * hs * (W + 1) + (uint64_t)n * (W + 1);
+  const uint64_t s1 = Sn[W], sx = Sn[i], sp = Sn[nf + i], sy = Sn[2 * nf];
+  uint64_t v;
+  if (r == 0) v = j ? sx : s1 - sx;
+  else if (r == 1) v = j ? sx - sp : s1 - sx - sy + sp;
+  else v = j ? sp : sy - sp;
+  return a.cst[(uint64_t)c * hs * C3 + (uint64_t)n * C3 + e] + v;
+}
+
+// Heuristic prologue, grid (node, 1 + features):
+//  y = 0 (control CTA, 64 threads): counter assembly; warp 0 runs the short
+//     probe / featureless / should_split / new_f chain, warp 1 replace
+//  y = 1 + i (one warp per feature i): the six counter cells of feature i
+//     are truncated by the public shift and ring_down'ed, the squares and the
+//     a*tot products formed, then P, Q and the Q == 0 fix for its two
+//     columns (train.py:366-381).  The warp first draws every Philox block
+//     of the feature (truncations, products, eq, b2a: the live schedule's
+//     blocks) into shared memory in parallel, so the serial gadget chain
+//     only does arithmetic.
+template <int SL>
+__device__ __forceinline__ void hc_pre_feature(const NodeArgs& a, int n, int fi) {
+  constexpr uint64_t MS = Ring<SL>::M;
+  constexpr int TB = TruncRand<64>::BLOCKS;
+  constexpr int NB = 6 * TB + 8 * 3 + 2 * 7;
+  __shared__ W2 tape[NB];
+  __shared__ uint64_t c32[3][6], pr[3][8];
+  const int wl = threadIdx.x;
+  const int nf = a.nf, cols = 2 * nf, C3 = 3 * cols;
   const uint64_t hs = (uint64_t)a.n_h, lanes = hs * cols;
-  uint64_t* co = sm;            // [3][3*cols] c_orig
-  uint64_t* c32 = co + 3 * C3;  // [3][3*cols]
-  uint64_t* pr = c32 + 3 * C3;  // [3][4*cols]
+  const Keys& K = a.K;
+  const uint32_t opH = op_id(a.level, SITE_HC);
+  // cell q = r * 2 + j  <->  e = r * cols + 2 fi + j; product p < 6: cell p squared,
+  // p = 6 + j: a (row 0, column 2fi+j) times tot (row 0, columns 2fi, 2fi+1)
+  auto cell_e = [&](int q) { return (q >> 1) * cols + 2 * fi + (q & 1); };
+  auto prod_e = [&](int p) { return p < 6 ? cell_e(p) : C3 + 2 * fi + (p - 6); };
+  for (int b = wl; b < NB; b += 32) {
+    int key = -1;
+    uint32_t sub, pidx;
+    uint64_t lane;
+    if (b < 6 * TB) {
+      const int q = b / TB;
+      trunc_block_id<64>(b % TB, 7, &key, &sub, &pidx);
+      lane = (uint64_t)n * C3 + cell_e(q);
+      if (!a.shift) continue;
+    } else if (b < 6 * TB + 24) {
+      const int t = b - 6 * TB;
+      key = t % 3, sub = 10, pidx = 0;
+      lane = (uint64_t)n * 4 * cols + prod_e(t / 3);
+    } else {
+      const int t = b - 6 * TB - 24, j = t / 7, w = t % 7;
+      lane = (uint64_t)n * cols + 2 * fi + j;
+      if (w < 2) key = -1, sub = 11, pidx = w;            // eqz dealer (r, Rb0) (Rb1, -)
+      else if (w < 5) key = w - 2, sub = 11, pidx = 0;    // eqz zero words
+      else key = -1, sub = 12, pidx = w - 5;              // b2a dealer (A0, A1) (bits, -)
+    }
+    tape[b] = word2(key < 0 ? K.dealer : K.pair[key], opH, sub, pidx, lane);
+  }
+  __syncwarp();
+  // counters: truncate by the public shift, ring_down      train.py:366-370
+  if (wl < 6) {
+    const int e = cell_e(wl);
+    A3 x = a3(co_cell(a, 0, n, e), co_cell(a, 1, n, e), co_cell(a, 2, n, e));
+    if (a.shift) x = trunc_arith<64>(tape + wl * TB, x, a.shift);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) c32[c][wl] = x.v[c] & MS;
+  }
+  __syncwarp();
+  auto C32 = [&](int q) { return a3(c32[0][q], c32[1][q], c32[2][q]); };
+  // prods = mul([c32, a], [c32, tot_rep])                   train.py:371-376
+  if (wl < 8) {
+    A3 x, y;
+    if (wl < 6) {
+      x = C32(wl);
+      y = x;
+    } else {
+      x = C32(wl - 6);  // row 0, column 2fi + j
+      y = add<SL>(C32(0), C32(1));
+    }
+    const W2* t = tape + 6 * TB + 3 * wl;
+    const uint64_t F[3] = {t[0].a, t[1].a, t[2].a};
+    const A3 z = mul_z<SL>(x, y, F);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) pr[c][wl] = z.v[c];
+  }
+  __syncwarp();
+  // P = a^2 - m0^2 - m1^2, qsafe = Q + b2a(eq(Q, 0))       train.py:377-381
+  if (wl < 2) {
+    auto PR = [&](int p) { return a3(pr[0][p], pr[1][p], pr[2][p]); };
+    const A3 p = diff<SL>(diff<SL>(PR(wl), PR(2 + wl)), PR(4 + wl));
+    const A3 q = PR(6 + wl);
+    const W2* t = tape + 6 * TB + 24 + 7 * wl;
+    const uint64_t Zw[3] = {t[2].a, t[3].a, t[4].a};
+    const B3 qz = eq_arith<SL>(q, t[0].a, t[0].b, t[1].a, Zw);
+    const A3 qsv = add<SL>(q, b2a_arith<SL>(qz, t[5].a, t[5].b, t[6].a));
+    const uint64_t lane = (uint64_t)n * cols + 2 * fi + wl;
+    st3s(a.dv, lanes, lane, p);
+    st3s(a.dv + 3 * lanes, lanes, lane, qsv);
+  }
+}
+
+template <int SL>
+__global__ void __launch_bounds__(64) k_hc_pre(NodeArgs a) {
+  const int n = blockIdx.x;
+  if (blockIdx.y > 0) {
+    if (threadIdx.x < 32) hc_pre_feature<SL>(a, n, (int)blockIdx.y - 1);
+    return;
+  }
+  extern __shared__ uint64_t sm[];
+  const int tid = threadIdx.x;
+  const int nf = a.nf, cols = 2 * nf, C3 = 3 * cols;
+  const uint64_t hs = (uint64_t)a.n_h;
+  uint64_t* co = sm;  // [3][3*cols] c_orig
   const Keys& K = a.K;
   const uint32_t opH = op_id(a.level, SITE_HC), opR = op_id(a.level, SITE_REPLACE);
-
-  // c_orig = c_start + assembled counters (train.py:256, 336-343)
-  for (int e = tid; e < 3 * C3; e += blockDim.x) {
-    const int c = e / C3, rk = e % C3, r = rk / cols, k = rk % cols, i = k >> 1, j = k & 1;
-    const uint64_t* Sn = a.S + (uint64_t)c * hs * (W + 1) + (uint64_t)n * (W + 1);
-    const uint64_t s1 = Sn[W], sx = Sn[i], sp = Sn[nf + i], sy = Sn[2 * nf];
-    uint64_t v;
-    if (r == 0) v = j ? sx : s1 - sx;
-    else if (r == 1) v = j ? sx - sp : s1 - sx - sy + sp;
-    else v = j ? sp : sy - sp;
-    co[e] = a.cst[(uint64_t)c * hs * C3 + (uint64_t)n * C3 + rk] + v;
-  }
+  for (int e = tid; e < 3 * C3; e += blockDim.x) co[e] = co_cell(a, e / C3, n, e % C3);
   __syncthreads();
   auto CO = [&](int e) { return a3(co[e], co[C3 + e], co[2 * C3 + e]); };
   if (a.co_out)  // heuristic "tee": hand the counters to the trusted helper
@@ -466,59 +563,20 @@ __global__ void __launch_bounds__(256) k_hc_pre(NodeArgs a) {
     }
     return;
   }
-  if (tid < 64) {
-    const int wl = tid - 32;
-    // replace: empty nodes adopt the parent's effective counters  train.py:269-276
-    if (a.level > 0) {
-      A3 ca = a3(0, 0, 0);
-      if (wl == 0) ca = b2a<64>(K, opR, 1, n, eqz<64>(K, opR, 0, n, add<64>(CO(0), CO(1))));
+  const int wl = tid - 32;
+  // replace: empty nodes adopt the parent's effective counters  train.py:269-276
+  if (a.level > 0) {
+    A3 ca = a3(0, 0, 0);
+    if (wl == 0) ca = b2a<64>(K, opR, 1, n, eqz<64>(K, opR, 0, n, add<64>(CO(0), CO(1))));
 #pragma unroll
-      for (int c = 0; c < 3; ++c) ca.v[c] = __shfl_sync(0xffffffffu, ca.v[c], 0);
-      const uint64_t pn = (uint64_t)(n >> 1);
-      for (int e = wl; e < C3; e += 32) {
-        const A3 par = ld3s(a.ceff_prev, (hs / 2) * C3, pn * C3 + e);
-        st3s(a.ceff, hs * C3, (uint64_t)n * C3 + e, select_with<64>(K, opR, 1, (uint32_t)e, n, CO(e), par, ca));
-      }
-    } else {
-      for (int e = wl; e < C3; e += 32) st3s(a.ceff, hs * C3, (uint64_t)n * C3 + e, CO(e));
+    for (int c = 0; c < 3; ++c) ca.v[c] = __shfl_sync(0xffffffffu, ca.v[c], 0);
+    const uint64_t pn = (uint64_t)(n >> 1);
+    for (int e = wl; e < C3; e += 32) {
+      const A3 par = ld3s(a.ceff_prev, (hs / 2) * C3, pn * C3 + e);
+      st3s(a.ceff, hs * C3, (uint64_t)n * C3 + e, select_with<64>(K, opR, 1, (uint32_t)e, n, CO(e), par, ca));
     }
-    return;
-  }
-  if (a.last || a.co_out) return;
-  const int wt = tid - 64, wn = blockDim.x - 64;  // 192 worker threads (warps 2-7)
-  // counters: truncate by the public shift, ring_down      train.py:366-370
-  for (int e = wt; e < C3; e += wn) {
-    A3 x = CO(e);
-    if (a.shift) x = trunc<64>(K, opH, 7, (uint64_t)n * C3 + e, x, a.shift);
-    for (int c = 0; c < 3; ++c) c32[c * C3 + e] = x.v[c] & MS;
-  }
-  bar_workers();
-  auto C32 = [&](int e) { return a3(c32[e], c32[C3 + e], c32[2 * C3 + e]); };
-  // prods = mul([c32, a], [c32, tot_rep])                   train.py:371-376
-  for (int e = wt; e < 4 * cols; e += wn) {
-    A3 x, y;
-    if (e < C3) {
-      x = C32(e);
-      y = x;
-    } else {
-      const int k = e - C3, i = k >> 1;
-      x = C32(k);
-      y = add<SL>(C32(2 * i), C32(2 * i + 1));
-    }
-    const A3 z = mul<SL>(K, opH, 10, 0, (uint64_t)n * 4 * cols + e, x, y);
-    for (int c = 0; c < 3; ++c) pr[c * 4 * cols + e] = z.v[c];
-  }
-  bar_workers();
-  auto PR = [&](int e) { return a3(pr[e], pr[4 * cols + e], pr[8 * cols + e]); };
-  // P = a^2 - m0^2 - m1^2, qsafe = Q + b2a(eq(Q, 0))       train.py:377-381
-  for (int k = wt; k < cols; k += wn) {
-    const A3 p = diff<SL>(diff<SL>(PR(k), PR(cols + k)), PR(2 * cols + k));
-    const A3 q = PR(C3 + k);
-    const uint64_t lane = (uint64_t)n * cols + k;
-    const B3 qz = eqz<SL>(K, opH, 11, lane, q);
-    const A3 qsv = add<SL>(q, b2a<SL>(K, opH, 12, lane, qz));
-    st3s(a.dv, lanes, lane, p);
-    st3s(a.dv + 3 * lanes, lanes, lane, qsv);
+  } else {
+    for (int e = wl; e < C3; e += 32) st3s(a.ceff, hs * C3, (uint64_t)n * C3 + e, CO(e));
   }
 }
 
@@ -600,10 +658,10 @@ __global__ void __launch_bounds__(256) k_div_tape(W2* tape, const uint32_t* __re
 }
 
 template <int SL>
-__global__ void __launch_bounds__(256) k_hc_post(NodeArgs a) {
+__device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n) {
   extern __shared__ uint64_t sm[];
   constexpr uint64_t MS = Ring<SL>::M;
-  const int n = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
+  const int tid = threadIdx.x, bd = blockDim.x;
   const int nf = a.nf, cols = 2 * nf;
   const uint64_t hs = (uint64_t)a.n_h, lanes = hs * cols;
   uint64_t* vals = sm;  // [3][nf]
@@ -685,6 +743,11 @@ __global__ void __launch_bounds__(256) k_hc_post(NodeArgs a) {
   }
 }
 
+template <int SL>
+__global__ void __launch_bounds__(256) k_hc_post(NodeArgs a) {
+  hc_post_body<SL>(a, blockIdx.x);
+}
+
 // grow policy: all_declined = open(and_reduce(~is_int over nodes)) (train.py:279-282)
 __global__ void k_node_stop(const uint64_t* hc, int n_h, Keys K, uint32_t op, uint64_t* out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -711,9 +774,9 @@ struct FinishArgs {
   Keys K;
 };
 
-__global__ void __launch_bounds__(128) k_node_finish(FinishArgs a) {
+__device__ __forceinline__ void node_finish_body(const FinishArgs& a, int n) {
   __shared__ uint64_t ca[3];
-  const int n = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
+  const int tid = threadIdx.x, bd = blockDim.x;
   const int cols = 2 * a.nf, C3 = 3 * cols;
   const uint64_t hs = (uint64_t)a.n_h, slot = hs - 1 + n;
   const Keys& K = a.K;
@@ -763,6 +826,17 @@ __global__ void __launch_bounds__(128) k_node_finish(FinishArgs a) {
     const A3 cc = select_with<64>(K, op, 4, (uint32_t)e, n, CE(e), a3(0, 0, 0), cav);
     for (int ch = 0; ch < 2; ++ch) st3s(a.cst_nxt, cs * C3, (uint64_t)(2 * n + ch) * C3 + e, cc);
   }
+}
+
+__global__ void __launch_bounds__(128) k_node_finish(FinishArgs a) { node_finish_body(a, blockIdx.x); }
+
+// scores / argmin / budget clear, then split, in one launch per level (fixed
+// policy, mpc heuristic): the node's CTA continues from sd to its children
+template <int SL>
+__global__ void __launch_bounds__(256) k_hc_post_finish(NodeArgs na, FinishArgs fa) {
+  hc_post_body<SL>(na, blockIdx.x);
+  __syncthreads();  // hc[sd], hc[new_gam] of this node written by thread 0
+  node_finish_body(fa, blockIdx.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -876,12 +950,16 @@ Layout layout(const gt_train_cfg& c) {
 }
 
 template <int SL>
-int launch_node_hc(const NodeArgs& na, cudaStream_t s) {
+int post_smem_bytes(const NodeArgs& na) {
+  return (int)sizeof(uint64_t) * (12 * na.nf + 4) + (int)sizeof(W2) * 8 * ArgminPair<SL>::BLOCKS;
+}
+
+template <int SL>
+int launch_node_hc(const NodeArgs& na, cudaStream_t s, bool fuse_post) {
   const int cols = 2 * na.nf;
-  const int pre_smem = (int)sizeof(uint64_t) * (9 * cols + 9 * cols + 12 * cols);
-  if (pre_smem > 48 * 1024)
-    GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_pre<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, pre_smem));
-  k_hc_pre<SL><<<na.n_h, 256, pre_smem, s>>>(na);
+  const int pre_smem = (int)sizeof(uint64_t) * 9 * cols;
+  const unsigned gy = (na.last || na.co_out) ? 1u : (unsigned)(1 + na.nf);
+  k_hc_pre<SL><<<dim3(na.n_h, gy), 64, pre_smem, s>>>(na);
   GT_LAUNCH_CHECK("k_hc_pre");
   if (na.last || na.co_out) return GT_OK;
   const uint64_t lanes = (uint64_t)na.n_h * cols;
@@ -892,8 +970,8 @@ int launch_node_hc(const NodeArgs& na, cudaStream_t s) {
     GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_div<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, div_smem));
   k_hc_div<SL><<<(unsigned)((lanes + wpc - 1) / wpc), 32 * wpc, div_smem, s>>>(na);
   GT_LAUNCH_CHECK("k_hc_div");
-  const int post_smem = (int)sizeof(uint64_t) * (12 * na.nf + 4) + (int)sizeof(W2) * 8 * ArgminPair<SL>::BLOCKS;
-  k_hc_post<SL><<<na.n_h, 256, post_smem, s>>>(na);
+  if (fuse_post) return GT_OK;  // k_hc_post_finish runs it with the split
+  k_hc_post<SL><<<na.n_h, 256, post_smem_bytes<SL>(na), s>>>(na);
   GT_LAUNCH_CHECK("k_hc_post");
   return GT_OK;
 }
@@ -1395,12 +1473,13 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
     na.d = d;
     na.K = K;
     P.start();
-    int rc = c.score_width == 32 ? launch_node_hc<32>(na, s) : launch_node_hc<64>(na, s);
+    const bool fuse = !last && !tee && c.policy == 0;
+    int rc = c.score_width == 32 ? launch_node_hc<32>(na, s, fuse) : launch_node_hc<64>(na, s, fuse);
     if (rc) return rc;
     P.stop(Prof::NODE_HC);
-    if (!last && !tee) {  // k_hc_div + k_hc_post
+    if (!last && !tee) {  // k_hc_div (+ k_hc_post unless fused into the finish launch)
       P.count_launch();
-      P.count_launch();
+      if (!fuse) P.count_launch();
     }
     if (!last && tee) {
       int hrc = heuristic(1, level, n_h, c.nf, ws + L.co, gam[cur], f[cur], hc, stream, heuristic_user);
@@ -1438,7 +1517,14 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
     fa.labels = last;
     fa.K = K;
     P.start();
-    k_node_finish<<<n_h, 128, 0, s>>>(fa);
+    if (fuse) {
+      if (c.score_width == 32)
+        k_hc_post_finish<32><<<n_h, 256, post_smem_bytes<32>(na), s>>>(na, fa);
+      else
+        k_hc_post_finish<64><<<n_h, 256, post_smem_bytes<64>(na), s>>>(na, fa);
+    } else {
+      k_node_finish<<<n_h, 128, 0, s>>>(fa);
+    }
     GT_LAUNCH_CHECK("k_node_finish");
     P.stop(Prof::NODE_FINISH);
     cur ^= 1;
