@@ -875,13 +875,13 @@ uint64_t la_words(uint64_t N, int nf, int depth) {
   return std::min<uint64_t>(want, per * std::max<uint64_t>(N, 1));
 }
 
-// la8 chunk capacity in 128-sample blocks (tensor engine): ~48 MB of byte
+// la8 chunk capacity in 128-sample blocks (tensor engine): ~32 MB of byte
 // planes at the deepest level, at least one block, at most the shard
 uint64_t tc_la8_blocks(uint64_t N, int nf, int depth) {
   const TcPlan tp = tc_plan(nf, 1 << (depth - 1));
   const uint64_t per_blk = 3ull * tp.mtiles * TC_ABLK;
   const uint64_t nkb = std::max<uint64_t>(1, (N + TC_KB - 1) / TC_KB);
-  return std::max<uint64_t>(1, std::min<uint64_t>(nkb, (48ull << 20) / per_blk));
+  return std::max<uint64_t>(1, std::min<uint64_t>(nkb, (32ull << 20) / per_blk));
 }
 
 // Division tapes of every heuristic level (levels 0 .. depth-2, mpc only),
@@ -918,7 +918,7 @@ Layout layout(const gt_train_cfg& c) {
   if (c.count_engine == 0) {
     const TcPlan tp = tc_plan(c.nf, (int)nmax);
     const uint64_t nkb = (N + TC_KB - 1) / TC_KB;
-    L.la = take(tc_la8_blocks(N, c.nf, c.depth) * 3ull * tp.mtiles * TC_ABLK / 8);
+    L.la = take(2 * tc_la8_blocks(N, c.nf, c.depth) * 3ull * tp.mtiles * TC_ABLK / 8);  // two chunk buffers
     L.cols8 = take(6ull * tp.nbn * nkb * tp.BB / 8);
   } else {
     L.la = take(la_words(N, c.nf, c.depth));
@@ -1198,26 +1198,70 @@ bool l2_window_attr(const void* base, uint64_t bytes, cudaLaunchAttribute* at) {
   return true;
 }
 
+// A second (side) stream per device for work that can run beside the main
+// stream -- the division tapes beside the prologue, a chunk's contraction
+// beside the next chunk's lanes -- with reusable fork/join events.  Inside a
+// CUDA-graph capture the waits become graph edges.
+struct Side {
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[8] = {};
+};
+int side_of(int dev, Side** out) {
+  static Side sides[64];
+  if (dev < 0 || dev >= 64) return fail_inval("device index out of range");
+  Side& sd = sides[dev];
+  if (!sd.st) {
+    // highest priority: a contraction's CTAs are dispatched as soon as the
+    // lane kernel running beside it frees an SM slot
+    int lo = 0, hi = 0;
+    GT_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    GT_CUDA_CHECK(cudaStreamCreateWithPriority(&sd.st, cudaStreamNonBlocking, hi));
+    for (auto& e : sd.ev) GT_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  *out = &sd;
+  return GT_OK;
+}
+// `to` waits for everything issued so far on `from`
+int stream_after(cudaStream_t to, cudaStream_t from, cudaEvent_t ev) {
+  GT_CUDA_CHECK(cudaEventRecord(ev, from));
+  GT_CUDA_CHECK(cudaStreamWaitEvent(to, ev, 0));
+  return GT_OK;
+}
+
 // tensor engine: leaf + per chunk (byte-plane lanes, tcgen05 contraction)
+// Chunks alternate between two la8 buffers (each holds la8_blocks K blocks at
+// the deepest level): with a side stream, the contraction of chunk k runs
+// beside the lanes of chunk k+1 (ALU-bound lanes, copy-bound contraction),
+// and the lanes of chunk k+2 wait for the contraction of chunk k.
 int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks, int alpha, uint64_t t0,
-                    uint64_t t1, cudaStream_t s, int num_sms, Prof& P) {
+                    uint64_t t1, cudaStream_t s, Side* side, int num_sms, Prof& P) {
   const TcPlan tp = tc_plan(c.nf, c.n_h);
-  // the buffer holds la8_blocks K blocks at the deepest level: shallower
-  // levels (fewer M tiles) fit proportionally more samples per chunk
-  const int mt_max = tc_plan(c.nf, c.n_h_max).mtiles;
-  la8_blocks = std::min<uint64_t>(la8_blocks * mt_max / tp.mtiles, (c.N + TC_KB - 1) / TC_KB);
+  const uint64_t buf_bytes = la8_blocks * 3ull * tc_plan(c.nf, c.n_h_max).mtiles * TC_ABLK;
+  const uint64_t nkb_all = (c.N + TC_KB - 1) / TC_KB;
+  // shallower levels (fewer M tiles) fit proportionally more samples per buffer;
+  // with a side stream, at least two chunks so the pipeline has something to overlap
+  la8_blocks = std::min<uint64_t>(buf_bytes / (3ull * tp.mtiles * TC_ABLK), nkb_all);
+  if (side && nkb_all >= 2) la8_blocks = std::min<uint64_t>(la8_blocks, (nkb_all + 1) / 2);
   const uint64_t cap = la8_blocks * TC_KB;
+  cudaStream_t s2 = side ? side->st : s;
+  if (side) {
+    int rc = stream_after(s2, s, side->ev[0]);  // the side stream joins after the level's partition
+    if (rc) return rc;
+  }
+  int k = 0;
   const uint64_t nkb_total = (c.N + TC_KB - 1) / TC_KB;
   const int smem = TC_MC_STAGES * (TC_A_HB + tp.BB);
   GT_CUDA_CHECK(cudaFuncSetAttribute(k_count_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  for (uint64_t s0 = 0; s0 < c.N; s0 += cap) {
+  for (uint64_t s0 = 0; s0 < c.N; s0 += cap, ++k) {
     const uint64_t cn = std::min<uint64_t>(cap, c.N - s0);
     const uint32_t nkb = (uint32_t)((cn + TC_KB - 1) / TC_KB);
+    uint8_t* buf = (uint8_t*)c.la + (uint64_t)(k & 1) * buf_bytes;
+    if (side && k >= 2) GT_CUDA_CHECK(cudaStreamWaitEvent(s, side->ev[2 + (k & 1)], 0));  // buffer reuse
     Lanes8Args la{};
     la.midx = c.midx;
     la.f = c.f;
     la.op_leaf = op_id(c.level, SITE_ISLEAF);
-    la.la8 = (uint8_t*)c.la;
+    la.la8 = buf;
     la.N = c.N;
     la.s0 = s0;
     la.cn = cn;
@@ -1232,8 +1276,12 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
     k_count_lanes8<<<dim3(nkb, (unsigned)tp.mtiles), 256, 0, s>>>(la);
     GT_LAUNCH_CHECK("k_count_lanes8");
     P.stop(Prof::COUNT_LANES);
+    if (side) {
+      GT_CUDA_CHECK(cudaEventRecord(side->ev[4 + (k & 1)], s));
+      GT_CUDA_CHECK(cudaStreamWaitEvent(s2, side->ev[4 + (k & 1)], 0));
+    }
     MmaArgs ma{};
-    ma.la8 = (const uint8_t*)c.la;
+    ma.la8 = buf;
     ma.B8 = B8;
     ma.S = c.S;
     ma.nkbc = la8_blocks;
@@ -1265,7 +1313,7 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
       lc.gridDim = dim3((unsigned)ma.nkr, (unsigned)(tp.mtiles * tp.nbn), 3);
       lc.blockDim = dim3(128);
       lc.dynamicSmemBytes = (size_t)smem;
-      lc.stream = s;
+      lc.stream = s2;
       cudaLaunchAttribute at[1];
       lc.attrs = at;
       lc.numAttrs = l2_window_attr(B8, 6ull * tp.nbn * nkb_total * tp.BB, at) ? 1 : 0;
@@ -1274,6 +1322,11 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
       P.stop(Prof::COUNT_CONTRACT);
     }
     GT_LAUNCH_CHECK("k_count_mma");
+    if (side) GT_CUDA_CHECK(cudaEventRecord(side->ev[2 + (k & 1)], s2));
+  }
+  if (side) {  // join: the level's heuristic needs every chunk's counters
+    int rc = stream_after(s, s2, side->ev[1]);
+    if (rc) return rc;
   }
   return GT_OK;
 }
@@ -1338,6 +1391,17 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
   GT_CUDA_CHECK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
   const Keys K = to_keys(keys);
   uint64_t* ws = (uint64_t*)workspace;
+  Side* side = nullptr;
+  // A/B switches: GT_NO_SIDE keeps the division tapes on the main stream;
+  // GT_COUNT_OVERLAP=1 pipelines count chunks across the two streams (measured
+  // slower on C2: the lane kernel fills every SM's registers, so the
+  // contraction CTAs rarely co-reside, and the extra chunks cost more)
+  static const bool no_side = getenv("GT_NO_SIDE") != nullptr;
+  static const bool count_overlap = getenv("GT_COUNT_OVERLAP") != nullptr;
+  {
+    int rc = side_of(dev, &side);
+    if (rc) return rc;
+  }
   const uint64_t N = c.n_local, nf = (uint64_t)c.nf, cols = 2 * nf, W = cols + 1;
   const uint64_t slots = (1ull << c.depth) - 1;
   const int shift = counter_shift(c.n_total, c.score_width, c.tau);
@@ -1387,19 +1451,29 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
   }
   // the division randomness of every level is data-independent: draw it all now
   const uint64_t tape_words = div_tape_words(c);
+  bool tape_forked = false;  // joined before the first heuristic
   if (tape_words) {
     const int cols_i = 2 * c.nf;
     const int TB = c.score_width == 32 ? div_tape_blocks<32>(d) : div_tape_blocks<64>(d);
     uint32_t* table = reinterpret_cast<uint32_t*>(ws + L.divtable);
     W2* tape = reinterpret_cast<W2*>(ws + L.divtape);
+    // on the side stream beside the prologue (the first count join orders it
+    // before any heuristic); inline when profiling
+    cudaStream_t ts = s;
+    if (!prof && !no_side && N) {
+      int rc = stream_after(side->st, s, side->ev[6]);
+      if (rc) return rc;
+      ts = side->st;
+    }
     P.start();
     if (c.score_width == 32) {
-      k_div_table<32><<<(TB + 127) / 128, 128, 0, s>>>(table, d);
-      k_div_tape<32><<<(unsigned)((tape_words + 255) / 256), 256, 0, s>>>(tape, table, tape_words, cols_i, TB, K);
+      k_div_table<32><<<(TB + 127) / 128, 128, 0, ts>>>(table, d);
+      k_div_tape<32><<<(unsigned)((tape_words + 255) / 256), 256, 0, ts>>>(tape, table, tape_words, cols_i, TB, K);
     } else {
-      k_div_table<64><<<(TB + 127) / 128, 128, 0, s>>>(table, d);
-      k_div_tape<64><<<(unsigned)((tape_words + 255) / 256), 256, 0, s>>>(tape, table, tape_words, cols_i, TB, K);
+      k_div_table<64><<<(TB + 127) / 128, 128, 0, ts>>>(table, d);
+      k_div_tape<64><<<(unsigned)((tape_words + 255) / 256), 256, 0, ts>>>(tape, table, tape_words, cols_i, TB, K);
     }
+    tape_forked = ts != s;
     P.count_launch();
     GT_LAUNCH_CHECK("k_div_tape");
     P.stop(Prof::NODE_HC);
@@ -1434,7 +1508,7 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
       int rc = c.count_engine == 0
                    ? launch_count_tc(cl, (const uint8_t*)(ws + L.cols8), tc_la8_blocks(N, c.nf, c.depth),
                                      c.count_reshare == 0 ? 1 : (c.sample_base == 0 ? 2 : 0), c.sample_base,
-                                     c.sample_base + N, s, num_sms, P)
+                                     c.sample_base + N, s, (prof || !count_overlap) ? nullptr : side, num_sms, P)
                    : launch_count(cl, s, num_sms, P);
       if (rc) return rc;
     }
@@ -1473,6 +1547,11 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
     na.d = d;
     na.K = K;
     P.start();
+    if (tape_forked) {
+      int rc = stream_after(s, side->st, side->ev[7]);
+      if (rc) return rc;
+      tape_forked = false;
+    }
     const bool fuse = !last && !tee && c.policy == 0;
     int rc = c.score_width == 32 ? launch_node_hc<32>(na, s, fuse) : launch_node_hc<64>(na, s, fuse);
     if (rc) return rc;
