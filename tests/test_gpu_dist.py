@@ -54,21 +54,24 @@ def _worker(rank, world, port, X, Y, fill, depth, keys_t, out_dir):
     dist.destroy_process_group()
 
 
-def test_sharded_device_training_equals_single_device(tmp_path):
+@pytest.mark.parametrize("n,world", [(5003, 2), (4999, 3)])
+def test_sharded_device_training_equals_single_device(tmp_path, n, world):
+    """(4999, 3) gives odd shard bases (1667, 3333): the count lanes' zero
+    words then straddle shard boundaries (count_lane_pair's unaligned path)."""
     from paper_2305_00645_b200 import TrainConfig
     from paper_2305_00645_b200.seeds import derive_seed, filler_values
     from paper_2305_00645_b200.train import train_components
 
     rng = np.random.default_rng(31)
-    data = rng.integers(0, 2, (5003, 10), dtype=np.uint8)
+    data = rng.integers(0, 2, (n, 10), dtype=np.uint8)
     depth = 5
     seed = b"\x52" * 16
     setup, k, keys_t = run_keys(seed)
     fill = filler_values(setup.filler_seed, (1 << depth) - 1, 10)
     X, Y = share(data[:, :-1], rng), share(data[:, -1], rng)
     T1, F1, _ = train_components(X, Y, TrainConfig(depth=depth), setup, derive_seed(seed, "deal"))
-    mp.spawn(_worker, args=(2, _port(), X, Y, fill, depth, keys_t, str(tmp_path)), nprocs=2, join=True)
-    for r in range(2):
+    mp.spawn(_worker, args=(world, _port(), X, Y, fill, depth, keys_t, str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
         z = np.load(tmp_path / f"r{r}.npz")
         assert int(z["d"]) == depth
         assert np.array_equal(z["T"], T1) and np.array_equal(z["F"], F1)
