@@ -173,6 +173,9 @@ int gt_infer(int depth, const uint64_t* tree, const uint64_t* queries, uint64_t 
  * The caller times it; blocks/s is the integer-ALU roof of the share kernels,
  * whose correlated randomness is drawn the same way. */
 int gt_diag_philox(uint32_t grid, uint32_t iters, uint64_t* out, void* stream);
+/* diagnostics: per-level heuristic phase timestamps (%globaltimer, ns) of the
+   last training run made with GT_HC_TIMING=1; slot 8*level + phase. */
+int gt_diag_hc_timestamps(unsigned long long* out, int n);
 
 #ifdef __cplusplus
 }

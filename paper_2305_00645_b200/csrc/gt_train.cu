@@ -383,6 +383,27 @@ namespace {
 //              clear
 // ---------------------------------------------------------------------------
 
+// Phase timestamps of the heuristic kernels (diagnostics: GT_HC_TIMING=1
+// makes node 0's thread 0 record %globaltimer at each phase boundary).
+__device__ unsigned long long g_hc_ts[64];
+__device__ __forceinline__ void hc_ts(int slot, bool on) {
+  if (!on || blockIdx.x != 0 || threadIdx.x != 0) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_hc_ts[slot] = t;
+}
+
+// The heuristic kernels draw Philox blocks along long dependent chains and,
+// in warp-cooperative draws, with lane-dependent keys: stage the expanded
+// round keys in shared memory once per CTA (every thread of the CTA calls
+// this before diverging) instead of indexing the kernel parameters.
+__device__ __forceinline__ const Keys& keys_smem(const Keys& K, Keys& ks) {
+  for (int i = threadIdx.x; i < (int)(sizeof(Keys) / 4); i += blockDim.x)
+    reinterpret_cast<uint32_t*>(&ks)[i] = reinterpret_cast<const uint32_t*>(&K)[i];
+  __syncthreads();
+  return ks;
+}
+
 struct NodeArgs {
   const uint64_t* S;          // [3][n_h][W+1]
   const uint64_t* cst;        // [3][n_h][3][cols]
@@ -394,7 +415,7 @@ struct NodeArgs {
   uint64_t* dv;               // [3][3][n_h*cols]: P, Q+[Q==0], division terms
   uint64_t* co_out;           // [3][n_h][3][cols] c_orig for the tee helper (or null)
   const W2* divtape;          // precomputed division blocks of this level (or null: draw live)
-  int n_h, nf, level, last, shift, tau;
+  int n_h, nf, level, last, shift, tau, ts;
   DivParams d;
   Keys K;
 };
@@ -427,7 +448,7 @@ __device__ __forceinline__ uint64_t co_cell(const NodeArgs& a, int c, int n, int
 //     blocks) into shared memory in parallel, so the serial gadget chain
 //     only does arithmetic.
 template <int SL>
-__device__ __forceinline__ void hc_pre_feature(const NodeArgs& a, int n, int fi) {
+__device__ __forceinline__ void hc_pre_feature(const NodeArgs& a, int n, int fi, const Keys& K) {
   constexpr uint64_t MS = Ring<SL>::M;
   constexpr int TB = TruncRand<64>::BLOCKS;
   constexpr int NB = 6 * TB + 8 * 3 + 2 * 7;
@@ -436,7 +457,6 @@ __device__ __forceinline__ void hc_pre_feature(const NodeArgs& a, int n, int fi)
   const int wl = threadIdx.x;
   const int nf = a.nf, cols = 2 * nf, C3 = 3 * cols;
   const uint64_t hs = (uint64_t)a.n_h, lanes = hs * cols;
-  const Keys& K = a.K;
   const uint32_t opH = op_id(a.level, SITE_HC);
   // cell q = r * 2 + j  <->  e = r * cols + 2 fi + j; product p < 6: cell p squared,
   // p = 6 + j: a (row 0, column 2fi+j) times tot (row 0, columns 2fi, 2fi+1)
@@ -509,9 +529,11 @@ __device__ __forceinline__ void hc_pre_feature(const NodeArgs& a, int n, int fi)
 
 template <int SL>
 __global__ void __launch_bounds__(64) k_hc_pre(NodeArgs a) {
+  __shared__ Keys ks;
+  const Keys& K = keys_smem(a.K, ks);
   const int n = blockIdx.x;
   if (blockIdx.y > 0) {
-    if (threadIdx.x < 32) hc_pre_feature<SL>(a, n, (int)blockIdx.y - 1);
+    if (threadIdx.x < 32) hc_pre_feature<SL>(a, n, (int)blockIdx.y - 1, K);
     return;
   }
   extern __shared__ uint64_t sm[];
@@ -519,7 +541,6 @@ __global__ void __launch_bounds__(64) k_hc_pre(NodeArgs a) {
   const int nf = a.nf, cols = 2 * nf, C3 = 3 * cols;
   const uint64_t hs = (uint64_t)a.n_h;
   uint64_t* co = sm;  // [3][3*cols] c_orig
-  const Keys& K = a.K;
   const uint32_t opH = op_id(a.level, SITE_HC), opR = op_id(a.level, SITE_REPLACE);
   for (int e = tid; e < 3 * C3; e += blockDim.x) co[e] = co_cell(a, e / C3, n, e % C3);
   __syncthreads();
@@ -669,12 +690,14 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n) {
   uint64_t* nvals = idxs + 3 * nf;
   uint64_t* nidxs = nvals + 3 * nf;
   uint64_t* hitw = nidxs + 3 * nf;  // [3]
-  const Keys& K = a.K;
+  __shared__ Keys ks;
+  const Keys& K = keys_smem(a.K, ks);
   const uint32_t opH = op_id(a.level, SITE_HC);
   const B3 gam = ldb3s(a.gam, hs, n);
   const uint64_t* terms = a.dv + 6 * lanes;
   auto TM = [&](int k) { return ld3s(terms, lanes, (uint64_t)n * cols + k); };
   // scores + masked argmin (tournament)     train.py:383-385, gadgets.py:366-401
+  hc_ts(0 + 8 * a.level, a.ts);
   const uint32_t SA = 13 + div_subs(a.d);
   const uint64_t worst = (1ull << (a.tau + 1)) & MS;
   for (int i = tid; i < nf; i += bd) {
@@ -692,6 +715,7 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n) {
   int m = nf;
   const int warp = tid >> 5, nwarps = bd >> 5;
   W2* tape = reinterpret_cast<W2*>(hitw + 4) + warp * ArgminPair<SL>::BLOCKS;
+  hc_ts(1 + 8 * a.level, a.ts);
   for (int r = 0; m > 1; ++r) {
     const int pairs = m / 2;
     const uint32_t base = SA + 2 + 5 * r;
@@ -724,6 +748,7 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n) {
     __syncthreads();
     m = nm;
   }
+  hc_ts(2 + 8 * a.level, a.ts);
   const A3 sd = a3(idxs[0], idxs[nf], idxs[2 * nf]);
   // gamma &= ~[sd == k]                                     train.py:386-387
   const uint32_t SH = SA + 2 + 5 * 7;
@@ -779,7 +804,8 @@ __device__ __forceinline__ void node_finish_body(const FinishArgs& a, int n) {
   const int tid = threadIdx.x, bd = blockDim.x;
   const int cols = 2 * a.nf, C3 = 3 * cols;
   const uint64_t hs = (uint64_t)a.n_h, slot = hs - 1 + n;
-  const Keys& K = a.K;
+  __shared__ Keys ks;
+  const Keys& K = keys_smem(a.K, ks);
   auto CE = [&](int e) { return ld3s(a.ceff, hs * C3, (uint64_t)n * C3 + e); };
   if (a.labels && a.lab) {  // labels from the trusted helper (train.py:301-302)
     if (tid == 0) {
@@ -803,19 +829,19 @@ __device__ __forceinline__ void node_finish_body(const FinishArgs& a, int n) {
   B3 ss;
   for (int c = 0; c < 3; ++c) ss.v[c] = a.hc[(0 * 3 + c) * hs + n];
   const uint64_t cs = 2 * hs;  // children per level
-  // the three selects of split:h are independent chains: one lane each
+  // the three selects of split:h are independent chains: one per warp
   if (tid == 0) {  // payload T = is_int ? sd : filler        (train.py:287)
     const A3 sd = ld3s(a.hc + 3 * hs, hs, n);
     st3s(a.T, a.slots, slot, select_with<64>(K, op, 0, 0, n, a3_const(a.filler[slot]), sd, b2a<64>(K, op, 0, n, ss)));
     st3s(a.F, a.slots, slot, ld3s(a.hc + 6 * hs, hs, n));
-  } else if (tid == 1) {  // child type = is_int ? LEAF : DUMMY  (train.py:288-289)
+  } else if (tid == 32) {  // child type = is_int ? LEAF : DUMMY  (train.py:288-289)
     const A3 cf = select_with<64>(K, op, 2, 0, n, a3_const(F_DUMMY), a3_const(F_LEAF), b2a<64>(K, op, 2, n, ss));
     const A3 ng = ld3s(a.hc + 9 * hs, hs, n);
     for (int ch = 0; ch < 2; ++ch) {
       st3s(a.f_nxt, cs, 2 * n + ch, cf);
       st3s(a.gam_nxt, cs, 2 * n + ch, ng);
     }
-  } else if (tid == 2) {  // child counters' condition
+  } else if (tid == 64) {  // child counters' condition
     const A3 c2 = b2a<64>(K, op, 4, n, ss);
     for (int c = 0; c < 3; ++c) ca[c] = c2.v[c];
   }
@@ -835,8 +861,11 @@ __global__ void __launch_bounds__(128) k_node_finish(FinishArgs a) { node_finish
 template <int SL>
 __global__ void __launch_bounds__(256) k_hc_post_finish(NodeArgs na, FinishArgs fa) {
   hc_post_body<SL>(na, blockIdx.x);
+  hc_ts(3 + 8 * na.level, na.ts);
   __syncthreads();  // hc[sd], hc[new_gam] of this node written by thread 0
   node_finish_body(fa, blockIdx.x);
+  __syncthreads();
+  hc_ts(4 + 8 * na.level, na.ts);
 }
 
 // ---------------------------------------------------------------------------
@@ -1236,7 +1265,8 @@ int stream_after(cudaStream_t to, cudaStream_t from, cudaEvent_t ev) {
 int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks, int alpha, uint64_t t0,
                     uint64_t t1, cudaStream_t s, Side* side, int num_sms, Prof& P) {
   const TcPlan tp = tc_plan(c.nf, c.n_h);
-  const uint64_t buf_bytes = la8_blocks * 3ull * tc_plan(c.nf, c.n_h_max).mtiles * TC_ABLK;
+  // two chunk buffers when pipelining across streams, else one of twice the size
+  const uint64_t buf_bytes = (side ? 1ull : 2ull) * la8_blocks * 3ull * tc_plan(c.nf, c.n_h_max).mtiles * TC_ABLK;
   const uint64_t nkb_all = (c.N + TC_KB - 1) / TC_KB;
   // shallower levels (fewer M tiles) fit proportionally more samples per buffer;
   // with a side stream, at least two chunks so the pipeline has something to overlap
@@ -1546,6 +1576,10 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
     na.tau = c.tau;
     na.d = d;
     na.K = K;
+    {
+      static const int ts = getenv("GT_HC_TIMING") ? 1 : 0;
+      na.ts = ts;
+    }
     P.start();
     if (tape_forked) {
       int rc = stream_after(s, side->st, side->ev[7]);
@@ -1614,6 +1648,13 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
   }
   if (depth_out) *depth_out = trained;
   return P.finish();
+}
+
+// diagnostics: the heuristic phase timestamps of the last GT_HC_TIMING run (ns)
+int gt_diag_hc_timestamps(unsigned long long* out, int n) {
+  if (!out || n < 0 || n > 64) return fail_inval("gt_diag_hc_timestamps: bad output");
+  GT_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_hc_ts, sizeof(unsigned long long) * n));
+  return GT_OK;
 }
 
 }  // extern "C"

@@ -1,0 +1,25 @@
+"""Per-level heuristic phase timings (GT_HC_TIMING=1): post-finish kernel of
+node 0: scores, argmin rounds, budget clear, split."""
+import ctypes, os, sys
+os.environ["GT_HC_TIMING"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import bench
+from paper_2305_00645_b200 import TrainConfig, _native
+from paper_2305_00645_b200.train import DeviceTrainer
+setup, keys, fill = bench._keys_and_filler()
+dev = torch.device("cuda", 0)
+t = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).to(dev)
+data, X, Y = bench._c2_inputs()
+tr = DeviceTrainer(bench.N_C2, bench.NF_C2, TrainConfig(depth=bench.DEPTH_C2))
+X, Y, F = t(X), t(Y), t(fill)
+for _ in range(3):
+    tr.run(X, Y, F, keys)
+torch.cuda.synchronize()
+lib = _native.load()
+buf = (ctypes.c_ulonglong * 64)()
+_native.check(lib.gt_diag_hc_timestamps(buf, 64))
+for lv in range(bench.DEPTH_C2 - 1):
+    ts = [buf[8 * lv + k] for k in range(5)]
+    d = [(ts[k + 1] - ts[k]) / 1e3 for k in range(4)]
+    print(f"level {lv}: scores {d[0]:.2f} us, argmin {d[1]:.2f} us, budget {d[2]:.2f} us, split {d[3]:.2f} us")
