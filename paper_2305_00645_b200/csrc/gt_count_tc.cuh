@@ -112,6 +112,97 @@ __global__ void __launch_bounds__(256) k_cols8(Cols8Args a) {
   }
 }
 
+// Fused prologue for the tensor engine (replaces k_prods + k_cols8): one CTA
+// per 128-sample K block stages the block's features and labels in shared
+// memory (coalesced rows), forms count:0's prods = mul(features, labels)
+// (train.py:229-230, same Philox schedule as k_prods) next to them, and
+// writes the U / X byte planes straight from shared memory: the u64 column
+// matrix never goes through HBM.
+struct Prep8Args {
+  const uint64_t *X, *Y;  // [3][N][nf], [3][N]
+  uint8_t* B8;
+  uint64_t N, nkb, base;
+  int nf, W, cpb, nbn;
+  Keys K;
+  uint32_t op_prods;
+};
+__global__ void __launch_bounds__(256) k_prep8(Prep8Args a) {
+  // one CTA per 64-sample half block (smem 3 x 64 x W words <= 198 KB at nf = 64)
+  constexpr int HS = TC_KB / 2;
+  extern __shared__ __align__(16) uint64_t v[];  // [3][HS][W] (x | prods | y)
+  const int nf = a.nf, W = a.W, tid = threadIdx.x;
+  const uint64_t kb = blockIdx.x >> 1;
+  const int half = blockIdx.x & 1;
+  const uint64_t nfx = a.N * (uint64_t)nf;
+  const uint64_t s0 = kb * TC_KB + half * HS;
+  for (int e = tid; e < HS * nf; e += blockDim.x) {
+    const int sl = e / nf, f = e % nf;
+    const uint64_t gs = s0 + sl;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) v[(c * HS + sl) * W + f] = gs < a.N ? __ldg(a.X + c * nfx + gs * nf + f) : 0ull;
+  }
+  for (int sl = tid; sl < HS; sl += blockDim.x) {
+    const uint64_t gs = s0 + sl;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) v[(c * HS + sl) * W + 2 * nf] = gs < a.N ? __ldg(a.Y + c * a.N + gs) : 0ull;
+  }
+  __syncthreads();
+  for (int e = tid; e < HS * nf; e += blockDim.x) {
+    const int sl = e / nf, f = e % nf;
+    const uint64_t gs = s0 + sl;
+    A3 z = a3(0, 0, 0);
+    if (gs < a.N) {
+      auto at = [&](int c, int w) { return v[(c * HS + sl) * W + w]; };
+      z = mul<64>(a.K, a.op_prods, 0, (uint32_t)f, a.base + gs, a3(at(0, f), at(1, f), at(2, f)),
+                  a3(at(0, 2 * nf), at(1, 2 * nf), at(2, 2 * nf)));
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) v[(c * HS + sl) * W + nf + f] = z.v[c];
+  }
+  __syncthreads();
+  // planes: item = (component, 16-sample chunk, column); 8 limb rows of 16
+  // bytes for each of U and X
+  const int WG = a.nbn * a.cpb;
+  const uint64_t HB = (uint64_t)8 * a.cpb * HS;
+  for (int it = tid; it < 3 * 4 * WG; it += blockDim.x) {
+    const int w = it % WG, kc = (it / WG) % 4, c = it / (4 * WG);
+    const int nb = w / a.cpb, g = w % a.cpb;
+    uint32_t pk[2][8][4];
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pk[t][q][k] = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int sl = kc * 16 + i;
+      uint64_t x = 0, u = 0;
+      if (s0 + sl < a.N) {
+        if (w < W) {
+          x = v[(c * HS + sl) * W + w];
+          u = x + v[(((c + 1) % 3) * HS + sl) * W + w];
+        } else if (w == W) {
+          u = 1;  // mask column: s_mask += la (train.py:334)
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        pk[0][q][i >> 2] |= (uint32_t)((u >> (8 * q)) & 0xffu) << (8 * (i & 3));
+        pk[1][q][i >> 2] |= (uint32_t)((x >> (8 * q)) & 0xffu) << (8 * (i & 3));
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      uint8_t* dst = a.B8 + ((((uint64_t)c * a.nbn + nb) * a.nkb + kb) * 2 + half) * 2 * HB + t * HB +
+                     ((uint64_t)kc * a.cpb + g) * 128;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<uint4*>(dst + q * 16) = make_uint4(pk[t][q][0], pk[t][q][1], pk[t][q][2], pk[t][q][3]);
+    }
+  }
+}
+
 // --- A operand: one CTA per (128-sample block, 16-node M tile) of a chunk;
 // lanes la = b2a(eq(m_idx, off+n) & is_leaf[n]) (train.py:328-331, the same
 // randomness as k_count_lanes: count_lane_pair), two samples of one node

@@ -943,7 +943,7 @@ Layout layout(const gt_train_cfg& c) {
     o += (words + 31) & ~31ull;  // 256-byte alignment
     return r;
   };
-  L.cols = take(3 * N * (uint64_t)count_plan(c.nf, 1).WC);
+  L.cols = take(c.count_engine == 1 ? 3 * N * (uint64_t)count_plan(c.nf, 1).WC : 0);
   if (c.count_engine == 0) {
     const TcPlan tp = tc_plan(c.nf, (int)nmax);
     const uint64_t nkb = (N + TC_KB - 1) / TC_KB;
@@ -1451,31 +1451,37 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
     const int WC = count_plan(c.nf, 1).WC;
     const uint64_t tot = N * (uint64_t)WC;
     P.start();
-    k_prods<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(features, labels, colm, N, c.nf, WC, c.sample_base, K,
-                                                          op_id(0, SITE_PRODS));
-    GT_LAUNCH_CHECK("k_prods");
-    if (c.count_engine == 0) {
+    if (c.count_engine == 0) {  // tensor engine: prods and byte planes in one pass
       const TcPlan tp = tc_plan(c.nf, 1);
-      Cols8Args ca{};
-      ca.cols = colm;
-      ca.B8 = (uint8_t*)(ws + L.cols8);
-      ca.N = N;
-      ca.nkb = (N + TC_KB - 1) / TC_KB;
-      ca.WC = WC;
-      ca.W = 2 * c.nf + 1;
-      ca.cpb = tp.cpb;
-      ca.nbn = tp.nbn;
-      const uint64_t thr = ca.nkb * 8 * tp.nbn * tp.cpb;
+      Prep8Args pa{};
+      pa.X = features;
+      pa.Y = labels;
+      pa.B8 = (uint8_t*)(ws + L.cols8);
+      pa.N = N;
+      pa.nkb = (N + TC_KB - 1) / TC_KB;
+      pa.base = c.sample_base;
+      pa.nf = c.nf;
+      pa.W = 2 * c.nf + 1;
+      pa.cpb = tp.cpb;
+      pa.nbn = tp.nbn;
+      pa.K = K;
+      pa.op_prods = op_id(0, SITE_PRODS);
+      const int smem = 3 * (TC_KB / 2) * pa.W * (int)sizeof(uint64_t);
+      GT_CUDA_CHECK(cudaFuncSetAttribute(k_prep8, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       cudaLaunchConfig_t lc{};
-      lc.gridDim = dim3((unsigned)((thr + 255) / 256));
+      lc.gridDim = dim3((unsigned)(2 * pa.nkb));
       lc.blockDim = dim3(256);
+      lc.dynamicSmemBytes = (size_t)smem;
       lc.stream = s;
       cudaLaunchAttribute at[1];
       lc.attrs = at;
-      lc.numAttrs = l2_window_attr(ca.B8, 6ull * tp.nbn * ca.nkb * tp.BB, at) ? 1 : 0;
-      GT_CUDA_CHECK(cudaLaunchKernelEx(&lc, k_cols8, ca));
-      GT_LAUNCH_CHECK("k_cols8");
-      P.count_launch();
+      lc.numAttrs = l2_window_attr(pa.B8, 6ull * tp.nbn * pa.nkb * tp.BB, at) ? 1 : 0;
+      GT_CUDA_CHECK(cudaLaunchKernelEx(&lc, k_prep8, pa));
+      GT_LAUNCH_CHECK("k_prep8");
+    } else {
+      k_prods<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(features, labels, colm, N, c.nf, WC, c.sample_base, K,
+                                                            op_id(0, SITE_PRODS));
+      GT_LAUNCH_CHECK("k_prods");
     }
     P.stop(Prof::PRODS);
   }
