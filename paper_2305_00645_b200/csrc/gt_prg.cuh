@@ -55,7 +55,11 @@ __device__ __forceinline__ W2 philox(const Key& key, uint32_t op, uint32_t strea
   { W2 w; w.a = lane * 0x9E3779B97F4A7C15ull + stream + key.k0[0]; w.b = w.a ^ ((uint64_t)op << 17); return w; }
 #endif
   uint32_t c0 = (uint32_t)lane, c1 = (uint32_t)(lane >> 32), c2 = stream, c3 = op;
+#ifdef GT_PHILOX_ROLLED  // latency kernels: a rolled round loop keeps the code hot in the instruction cache
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
   for (int r = 0; r < 10; ++r) {
     uint64_t p0 = (uint64_t)0xD2511F53u * c0;  // IMAD.WIDE.U32
     uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;

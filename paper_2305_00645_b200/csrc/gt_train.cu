@@ -529,13 +529,15 @@ __device__ __forceinline__ void hc_pre_feature(const NodeArgs& a, int n, int fi,
 
 template <int SL>
 __global__ void __launch_bounds__(64) k_hc_pre(NodeArgs a) {
-  __shared__ Keys ks;
-  const Keys& K = keys_smem(a.K, ks);
   const int n = blockIdx.x;
-  if (blockIdx.y > 0) {
-    if (threadIdx.x < 32) hc_pre_feature<SL>(a, n, (int)blockIdx.y - 1, K);
+  if (blockIdx.y > 0) {  // the feature warp draws with lane-dependent keys: stage them in smem
+    __shared__ Keys ks;
+    const Keys& Ks = keys_smem(a.K, ks);
+    if (threadIdx.x < 32) hc_pre_feature<SL>(a, n, (int)blockIdx.y - 1, Ks);
     return;
   }
+  // uniform-key chains read the round keys as constant-bank operands
+  const Keys& K = a.K;
   extern __shared__ uint64_t sm[];
   const int tid = threadIdx.x;
   const int nf = a.nf, cols = 2 * nf, C3 = 3 * cols;
@@ -691,7 +693,8 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n) {
   uint64_t* nidxs = nvals + 3 * nf;
   uint64_t* hitw = nidxs + 3 * nf;  // [3]
   __shared__ Keys ks;
-  const Keys& K = keys_smem(a.K, ks);
+  const Keys& Ks = keys_smem(a.K, ks);  // lane-dependent keys of the tournament tapes
+  const Keys& K = a.K;                  // uniform-key gadgets: constant-bank operands
   const uint32_t opH = op_id(a.level, SITE_HC);
   const B3 gam = ldb3s(a.gam, hs, n);
   const uint64_t* terms = a.dv + 6 * lanes;
@@ -726,7 +729,7 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n) {
       const A3 ai = a3(idxs[2 * p], idxs[nf + 2 * p], idxs[2 * nf + 2 * p]);
       const A3 bi = a3(idxs[2 * p + 1], idxs[nf + 2 * p + 1], idxs[2 * nf + 2 * p + 1]);
       A3 nv, ni;
-      argmin_pair_warp<SL>(K, opH, base, lane, av, bv, ai, bi, tape, &nv, &ni);
+      argmin_pair_warp<SL>(Ks, opH, base, lane, av, bv, ai, bi, tape, &nv, &ni);
       if ((tid & 31) == 0)
         for (int c = 0; c < 3; ++c) {
           nvals[c * nf + p] = nv.v[c];
@@ -795,7 +798,7 @@ struct FinishArgs {
   uint64_t *f_nxt, *gam_nxt, *cst_nxt;  // children
   const uint64_t* lab;                  // [3][n_h] helper labels (heuristic tee) or null
   uint64_t slots;
-  int n_h, nf, level, labels;
+  int n_h, nf, level, labels, ts;
   Keys K;
 };
 
@@ -804,8 +807,8 @@ __device__ __forceinline__ void node_finish_body(const FinishArgs& a, int n) {
   const int tid = threadIdx.x, bd = blockDim.x;
   const int cols = 2 * a.nf, C3 = 3 * cols;
   const uint64_t hs = (uint64_t)a.n_h, slot = hs - 1 + n;
-  __shared__ Keys ks;
-  const Keys& K = keys_smem(a.K, ks);
+  const Keys& K = a.K;
+  hc_ts(5 + 8 * a.level, a.ts);
   auto CE = [&](int e) { return ld3s(a.ceff, hs * C3, (uint64_t)n * C3 + e); };
   if (a.labels && a.lab) {  // labels from the trusted helper (train.py:301-302)
     if (tid == 0) {
@@ -832,7 +835,9 @@ __device__ __forceinline__ void node_finish_body(const FinishArgs& a, int n) {
   // the three selects of split:h are independent chains: one per warp
   if (tid == 0) {  // payload T = is_int ? sd : filler        (train.py:287)
     const A3 sd = ld3s(a.hc + 3 * hs, hs, n);
-    st3s(a.T, a.slots, slot, select_with<64>(K, op, 0, 0, n, a3_const(a.filler[slot]), sd, b2a<64>(K, op, 0, n, ss)));
+    const uint64_t fl = a.filler[slot];
+    const A3 cb = b2a<64>(K, op, 0, n, ss);
+    st3s(a.T, a.slots, slot, select_with<64>(K, op, 0, 0, n, a3_const(fl), sd, cb));
     st3s(a.F, a.slots, slot, ld3s(a.hc + 6 * hs, hs, n));
   } else if (tid == 32) {  // child type = is_int ? LEAF : DUMMY  (train.py:288-289)
     const A3 cf = select_with<64>(K, op, 2, 0, n, a3_const(F_DUMMY), a3_const(F_LEAF), b2a<64>(K, op, 2, n, ss));
@@ -846,6 +851,7 @@ __device__ __forceinline__ void node_finish_body(const FinishArgs& a, int n) {
     for (int c = 0; c < 3; ++c) ca[c] = c2.v[c];
   }
   __syncthreads();
+  hc_ts(6 + 8 * a.level, a.ts);
   // child counters = select(c_eff, 0, is_int)                 train.py:290
   const A3 cav = a3(ca[0], ca[1], ca[2]);
   for (int e = tid; e < C3; e += bd) {
@@ -1630,6 +1636,7 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
       fa.lab = ws + L.lab;
     }
     fa.slots = slots;
+    fa.ts = na.ts;
     fa.n_h = n_h;
     fa.nf = c.nf;
     fa.level = level;

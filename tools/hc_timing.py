@@ -20,6 +20,7 @@ lib = _native.load()
 buf = (ctypes.c_ulonglong * 64)()
 _native.check(lib.gt_diag_hc_timestamps(buf, 64))
 for lv in range(bench.DEPTH_C2 - 1):
-    ts = [buf[8 * lv + k] for k in range(5)]
-    d = [(ts[k + 1] - ts[k]) / 1e3 for k in range(4)]
-    print(f"level {lv}: scores {d[0]:.2f} us, argmin {d[1]:.2f} us, budget {d[2]:.2f} us, split {d[3]:.2f} us")
+    ts = [buf[8 * lv + k] for k in range(7)]
+    d = lambda a, b: (ts[b] - ts[a]) / 1e3
+    print(f"level {lv}: scores {d(0, 1):.2f} us, argmin {d(1, 2):.2f} us, budget {d(2, 3):.2f} us, "
+          f"split: keys {d(3, 5):.2f} chains {d(5, 6):.2f} counters {d(6, 4):.2f} us)
