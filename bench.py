@@ -419,26 +419,31 @@ def main():
     parity = bool(np.array_equal(Tc.sum(axis=0), z["T"]) and np.array_equal(Fc.sum(axis=0), z["F"]))
 
     # ---- e2e through the public API with host buffers ----
+    # gt_train_host: pinned host shares in, the tree shares out; the sample
+    # shares go up in chunks while the prologue of the resident chunks runs
+    # (one GPU: the whole call is a CUDA graph, like `value`)
     e2e_ms = []
     Th = torch.empty((3, tr.T.shape[1]), dtype=torch.int64).pin_memory()
     Fh = torch.empty((3, tr.F.shape[1]), dtype=torch.int64).pin_memory()
+    tr_h = DeviceTrainer(cnt, NF_C2, TrainConfig(depth=DEPTH_C2), n_total=N_C2, sample_base=start, device=dev,
+                         host_io=True)
+    cb_h = make_allreduce(tr_h) if world > 1 else None
+    run_h = (tr_h.capture_host(Xp, Yp, Fp, Th, Fh, keys) if world == 1
+             else (lambda: tr_h.run_host(Xp, Yp, Fp, Th, Fh, keys, allreduce=cb_h)))
     for i in range(args.warmup + args.steps):
         flush.zero_()
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        X.copy_(Xp, non_blocking=True)
-        Y.copy_(Yp, non_blocking=True)
-        FL.copy_(Fp, non_blocking=True)
-        step()
-        Th.copy_(tr.T, non_blocking=True)
-        Fh.copy_(tr.F, non_blocking=True)
+        run_h()
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
         if i >= args.warmup:
             e2e_ms.append(e0.elapsed_time(e1))
+    e2e_parity = bool(np.array_equal(Th.numpy().view(np.uint64).sum(axis=0), z["T"]) and
+                      np.array_equal(Fh.numpy().view(np.uint64).sum(axis=0), z["F"]))
     e2e_s = max_over_ranks(sum(e2e_ms)) / args.steps / 1e3
     h2d = int(Xp.numel() * 8 + Yp.numel() * 8 + Fp.numel() * 8)
     d2h = int(Th.numel() * 8 + Fh.numel() * 8)
@@ -534,7 +539,8 @@ def main():
                    "n_samples": N_C2, "n_features": NF_C2, "depth": DEPTH_C2, "parties": 3,
                    "parallelism": f"samples sharded x{world}" + (" + NCCL count allreduce" if world > 1 else ""),
                    "l2": "flushed (256 MiB write) between timed steps"},
-        "parity": {"tree_equals_reference": parity, "c3_predictions_equal_reference": preds_ok},
+        "parity": {"tree_equals_reference": parity, "e2e_tree_equals_reference": e2e_parity,
+                   "c3_predictions_equal_reference": preds_ok},
         "e2e": {"value": e2e_s, "unit": "s/tree", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": kname.get(dom, dom), "achieved": achieved, "peak": peak,

@@ -158,6 +158,17 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
                 const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user, gt_heuristic_fn heuristic,
                 void* heuristic_user, void* stream, gt_train_profile* prof);
 
+/* gt_train with HOST operands (the same arrays as gt_train, in pinned host
+ * memory): the sample shares go up in chunks on a copy stream while the
+ * prologue of the chunks already resident runs, T and F come back at the end;
+ * all work is ordered on `stream` (synchronise it before reading T_h / F_h).
+ * The workspace must hold gt_train_host_workspace_bytes(cfg) (device). */
+uint64_t gt_train_host_workspace_bytes(const gt_train_cfg* cfg);
+int gt_train_host(const gt_train_cfg* cfg, const uint64_t* features_h, const uint64_t* labels_h,
+                  const uint64_t* filler_h, uint64_t* T_h, uint64_t* F_h, int32_t* depth_out, void* workspace,
+                  uint64_t workspace_bytes, const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user,
+                  void* stream);
+
 /* ---- secure inference (infer_batch, infer.py:91-106) ---- */
 
 /* tree [3][2^depth-1] heap-ordered payload shares, queries [3][n][nf];

@@ -86,6 +86,10 @@ _SIGS = {
     "gt_row_lookup": (ctypes.c_int, [ctypes.c_int, _u64p, ctypes.c_uint64, _u64p, _u64p, ctypes.c_uint64,
                                      ctypes.POINTER(gt_keys), ctypes.c_uint32, ctypes.c_void_p]),
     "gt_train_workspace_bytes": (ctypes.c_uint64, [ctypes.POINTER(gt_train_cfg)]),
+    "gt_train_host_workspace_bytes": (ctypes.c_uint64, [ctypes.POINTER(gt_train_cfg)]),
+    "gt_train_host": (ctypes.c_int, [ctypes.POINTER(gt_train_cfg), _u64p, _u64p, _u64p, _u64p, _u64p,
+                                     ctypes.POINTER(ctypes.c_int32), _u64p, ctypes.c_uint64, ctypes.POINTER(gt_keys),
+                                     ALLREDUCE_FN, ctypes.c_void_p, ctypes.c_void_p]),
     "gt_train": (ctypes.c_int, [ctypes.POINTER(gt_train_cfg), _u64p, _u64p, _u64p, _u64p, _u64p,
                                 ctypes.POINTER(ctypes.c_int32), ctypes.c_void_p, ctypes.c_uint64,
                                 ctypes.POINTER(gt_keys), ALLREDUCE_FN, ctypes.c_void_p, ctypes.c_void_p]),

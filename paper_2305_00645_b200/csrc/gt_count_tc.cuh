@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(256) k_cols8(Cols8Args a) {
 struct Prep8Args {
   const uint64_t *X, *Y;  // [3][N][nf], [3][N]
   uint8_t* B8;
-  uint64_t N, nkb, base;
+  uint64_t N, nkb, base, hb0;  // hb0: first 64-sample half block of this launch
   int nf, W, cpb, nbn;
   Keys K;
   uint32_t op_prods;
@@ -131,8 +131,9 @@ __global__ void __launch_bounds__(256) k_prep8(Prep8Args a) {
   constexpr int HS = TC_KB / 2;
   extern __shared__ __align__(16) uint64_t v[];  // [3][HS][W] (x | prods | y)
   const int nf = a.nf, W = a.W, tid = threadIdx.x;
-  const uint64_t kb = blockIdx.x >> 1;
-  const int half = blockIdx.x & 1;
+  const uint64_t hb = a.hb0 + blockIdx.x;
+  const uint64_t kb = hb >> 1;
+  const int half = (int)(hb & 1);
   const uint64_t nfx = a.N * (uint64_t)nf;
   const uint64_t s0 = kb * TC_KB + half * HS;
   for (int e = tid; e < HS * nf; e += blockDim.x) {

@@ -936,10 +936,10 @@ inline uint64_t div_tape_level_off(int level, int nf, int TB) {  // W2 offset of
 }
 
 struct Layout {
-  uint64_t cols, la, cols8, leaf, midx, divtape, divtable, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
+  uint64_t xin, yin, fin, tout, fout, cols, la, cols8, leaf, midx, divtape, divtable, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
 };
 
-Layout layout(const gt_train_cfg& c) {
+Layout layout(const gt_train_cfg& c, bool host_io = false) {
   const uint64_t N = c.n_local, nf = (uint64_t)c.nf, cols = 2 * nf, W = cols + 1;
   const uint64_t nmax = 1ull << (c.depth - 1), ch = 2 * nmax;
   Layout L;
@@ -980,6 +980,13 @@ Layout layout(const gt_train_cfg& c) {
   L.co = take(3 * nmax * 3 * cols);
   L.lab = take(3 * nmax);
   L.stop = take(4);
+  // device staging of the host-input entry (gt_train_host)
+  const uint64_t slots = (1ull << c.depth) - 1;
+  L.xin = take(host_io ? 3 * N * nf : 0);
+  L.yin = take(host_io ? 3 * N : 0);
+  L.fin = take(host_io ? slots : 0);
+  L.tout = take(host_io ? 3 * slots : 0);
+  L.fout = take(host_io ? 3 * slots : 0);
   L.total = o;
   return L;
 }
@@ -1238,8 +1245,9 @@ bool l2_window_attr(const void* base, uint64_t bytes, cudaLaunchAttribute* at) {
 // beside the next chunk's lanes -- with reusable fork/join events.  Inside a
 // CUDA-graph capture the waits become graph edges.
 struct Side {
-  cudaStream_t st = nullptr;
-  cudaEvent_t ev[8] = {};
+  cudaStream_t st = nullptr;  // compute side stream (high priority)
+  cudaStream_t cp = nullptr;  // host <-> device copies of the host-input entry
+  cudaEvent_t ev[16] = {};
 };
 int side_of(int dev, Side** out) {
   static Side sides[64];
@@ -1251,6 +1259,7 @@ int side_of(int dev, Side** out) {
     int lo = 0, hi = 0;
     GT_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     GT_CUDA_CHECK(cudaStreamCreateWithPriority(&sd.st, cudaStreamNonBlocking, hi));
+    GT_CUDA_CHECK(cudaStreamCreateWithFlags(&sd.cp, cudaStreamNonBlocking));
     for (auto& e : sd.ev) GT_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   *out = &sd;
@@ -1269,7 +1278,9 @@ int stream_after(cudaStream_t to, cudaStream_t from, cudaEvent_t ev) {
 // beside the lanes of chunk k+1 (ALU-bound lanes, copy-bound contraction),
 // and the lanes of chunk k+2 wait for the contraction of chunk k.
 int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks, int alpha, uint64_t t0,
-                    uint64_t t1, cudaStream_t s, Side* side, int num_sms, Prof& P) {
+                    uint64_t t1, cudaStream_t s, Side* side, int num_sms, Prof& P, uint64_t lo = 0,
+                    uint64_t hi = ~0ull) {
+  hi = std::min<uint64_t>(hi, c.N);
   const TcPlan tp = tc_plan(c.nf, c.n_h);
   // two chunk buffers when pipelining across streams, else one of twice the size
   const uint64_t buf_bytes = (side ? 1ull : 2ull) * la8_blocks * 3ull * tc_plan(c.nf, c.n_h_max).mtiles * TC_ABLK;
@@ -1288,8 +1299,8 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
   const uint64_t nkb_total = (c.N + TC_KB - 1) / TC_KB;
   const int smem = TC_MC_STAGES * (TC_A_HB + tp.BB);
   GT_CUDA_CHECK(cudaFuncSetAttribute(k_count_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  for (uint64_t s0 = 0; s0 < c.N; s0 += cap, ++k) {
-    const uint64_t cn = std::min<uint64_t>(cap, c.N - s0);
+  for (uint64_t s0 = lo; s0 < hi; s0 += cap, ++k) {  // lo is a multiple of TC_KB
+    const uint64_t cn = std::min<uint64_t>(cap, hi - s0);
     const uint32_t nkb = (uint32_t)((cn + TC_KB - 1) / TC_KB);
     uint8_t* buf = (uint8_t*)c.la + (uint64_t)(k & 1) * buf_bytes;
     if (side && k >= 2) GT_CUDA_CHECK(cudaStreamWaitEvent(s, side->ev[2 + (k & 1)], 0));  // buffer reuse
@@ -1367,6 +1378,46 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
   return GT_OK;
 }
 
+// host-side operands of gt_train_host
+struct HostIn {
+  const uint64_t *X, *Y, *fill;
+  uint64_t *T, *F;
+};
+
+// tensor-engine prologue over the 64-sample half blocks [hb_lo, hb_hi)
+int launch_prep8(const gt_train_cfg& c, const uint64_t* features, const uint64_t* labels, uint64_t* ws,
+                 const Layout& L, const Keys& K, uint64_t hb_lo, uint64_t hb_hi, cudaStream_t s) {
+  if (hb_hi <= hb_lo) return GT_OK;
+  const TcPlan tp = tc_plan(c.nf, 1);
+  Prep8Args pa{};
+  pa.X = features;
+  pa.Y = labels;
+  pa.B8 = (uint8_t*)(ws + L.cols8);
+  pa.N = c.n_local;
+  pa.nkb = (c.n_local + TC_KB - 1) / TC_KB;
+  pa.base = c.sample_base;
+  pa.hb0 = hb_lo;
+  pa.nf = c.nf;
+  pa.W = 2 * c.nf + 1;
+  pa.cpb = tp.cpb;
+  pa.nbn = tp.nbn;
+  pa.K = K;
+  pa.op_prods = op_id(0, SITE_PRODS);
+  const int smem = 3 * (TC_KB / 2) * pa.W * (int)sizeof(uint64_t);
+  GT_CUDA_CHECK(cudaFuncSetAttribute(k_prep8, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((unsigned)(hb_hi - hb_lo));
+  lc.blockDim = dim3(256);
+  lc.dynamicSmemBytes = (size_t)smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  lc.attrs = at;
+  lc.numAttrs = l2_window_attr(pa.B8, 6ull * tp.nbn * pa.nkb * tp.BB, at) ? 1 : 0;
+  GT_CUDA_CHECK(cudaLaunchKernelEx(&lc, k_prep8, pa));
+  GT_LAUNCH_CHECK("k_prep8");
+  return GT_OK;
+}
+
 int counter_shift(uint64_t n, int score_width, int tau) {  // train.py:189-192
   int headroom = (score_width - tau - 2) / 2;
   int bl = 0;
@@ -1393,10 +1444,11 @@ int gt_train(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* 
                      allreduce_user, nullptr, nullptr, stream, nullptr);
 }
 
-int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* labels, const uint64_t* filler,
-                uint64_t* T, uint64_t* F, int32_t* depth_out, void* workspace, uint64_t workspace_bytes,
-                const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user, gt_heuristic_fn heuristic,
-                void* heuristic_user, void* stream, gt_train_profile* prof) {
+static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* labels,
+                      const uint64_t* filler, uint64_t* T, uint64_t* F, int32_t* depth_out, void* workspace,
+                      uint64_t workspace_bytes, const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user,
+                      gt_heuristic_fn heuristic, void* heuristic_user, void* stream, gt_train_profile* prof,
+                      const HostIn* hin) {
   if (!cfg || !keys) return fail_inval("gt_train: NULL cfg/keys");
   const gt_train_cfg c = *cfg;
   if (c.depth < 1 || c.depth > 16) return fail_inval("depth must be in 1..16");
@@ -1415,8 +1467,17 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
   bool ok = false;
   const DivParams d = div_params(c.score_width, c.tau, &ok);
   if (!ok) return fail_inval("division unsupported at this width/tau");
-  const Layout L = layout(c);
+  const Layout L = layout(c, hin != nullptr);
   if (!workspace || workspace_bytes < L.total * sizeof(uint64_t)) return fail_inval("workspace too small");
+  if (hin) {  // host operands: stage through the workspace
+    if (c.n_local && (!hin->X || !hin->Y)) return fail_inval("NULL features/labels");
+    if (!hin->fill || !hin->T || !hin->F) return fail_inval("NULL filler/T/F");
+    features = (const uint64_t*)workspace + L.xin;
+    labels = (const uint64_t*)workspace + L.yin;
+    filler = (const uint64_t*)workspace + L.fin;
+    T = (uint64_t*)workspace + L.tout;
+    F = (uint64_t*)workspace + L.fout;
+  }
   if (c.n_local && (!features || !labels)) return fail_inval("NULL features/labels");
   if (!filler || !T || !F) return fail_inval("NULL filler/T/F");
 
@@ -1446,6 +1507,8 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
   uint64_t *cst[2] = {ws + L.cst[0], ws + L.cst[1]}, *ceff[2] = {ws + L.ceff[0], ws + L.ceff[1]};
   int cur = 0;
 
+  if (hin)
+    GT_CUDA_CHECK(cudaMemcpyAsync((void*)filler, hin->fill, slots * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
   GT_CUDA_CHECK(cudaMemsetAsync(T, 0, 3 * slots * sizeof(uint64_t), s));
   GT_CUDA_CHECK(cudaMemsetAsync(F, 0, 3 * slots * sizeof(uint64_t), s));
   if (N) GT_CUDA_CHECK(cudaMemsetAsync(midx, 0, 3 * N * sizeof(uint64_t), s));  // m_idx = const(0)
@@ -1453,44 +1516,6 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
   k_init<<<1, 128, 0, s>>>(f[0], gam[0], cst[0], 1, 3 * cols, (int)cols, c.nf);
   GT_LAUNCH_CHECK("k_init");
   P.count_launch();
-  if (N) {
-    const int WC = count_plan(c.nf, 1).WC;
-    const uint64_t tot = N * (uint64_t)WC;
-    P.start();
-    if (c.count_engine == 0) {  // tensor engine: prods and byte planes in one pass
-      const TcPlan tp = tc_plan(c.nf, 1);
-      Prep8Args pa{};
-      pa.X = features;
-      pa.Y = labels;
-      pa.B8 = (uint8_t*)(ws + L.cols8);
-      pa.N = N;
-      pa.nkb = (N + TC_KB - 1) / TC_KB;
-      pa.base = c.sample_base;
-      pa.nf = c.nf;
-      pa.W = 2 * c.nf + 1;
-      pa.cpb = tp.cpb;
-      pa.nbn = tp.nbn;
-      pa.K = K;
-      pa.op_prods = op_id(0, SITE_PRODS);
-      const int smem = 3 * (TC_KB / 2) * pa.W * (int)sizeof(uint64_t);
-      GT_CUDA_CHECK(cudaFuncSetAttribute(k_prep8, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      cudaLaunchConfig_t lc{};
-      lc.gridDim = dim3((unsigned)(2 * pa.nkb));
-      lc.blockDim = dim3(256);
-      lc.dynamicSmemBytes = (size_t)smem;
-      lc.stream = s;
-      cudaLaunchAttribute at[1];
-      lc.attrs = at;
-      lc.numAttrs = l2_window_attr(pa.B8, 6ull * tp.nbn * pa.nkb * tp.BB, at) ? 1 : 0;
-      GT_CUDA_CHECK(cudaLaunchKernelEx(&lc, k_prep8, pa));
-      GT_LAUNCH_CHECK("k_prep8");
-    } else {
-      k_prods<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(features, labels, colm, N, c.nf, WC, c.sample_base, K,
-                                                            op_id(0, SITE_PRODS));
-      GT_LAUNCH_CHECK("k_prods");
-    }
-    P.stop(Prof::PRODS);
-  }
   // the division randomness of every level is data-independent: draw it all now
   const uint64_t tape_words = div_tape_words(c);
   bool tape_forked = false;  // joined before the first heuristic
@@ -1520,6 +1545,87 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
     GT_LAUNCH_CHECK("k_div_tape");
     P.stop(Prof::NODE_HC);
   }
+  // the count of one level over the samples [lo, hi)
+  auto count_range = [&](int level, int fcur, uint64_t lo, uint64_t hi) -> int {
+    CountLaunch cl{};
+    cl.midx = midx;
+    cl.f = f[fcur];
+    cl.cols = colm;
+    cl.la = ws + L.la;
+    cl.leaf = ws + L.leaf;
+    cl.S = S;
+    cl.la_cap_words = la_words(N, c.nf, c.depth);
+    cl.N = N;
+    cl.base = c.sample_base;
+    cl.nf = c.nf;
+    cl.n_h = 1 << level;
+    cl.n_h_max = 1 << (c.depth - 1);
+    cl.K = K;
+    cl.level = level;
+    return c.count_engine == 0
+               ? launch_count_tc(cl, (const uint8_t*)(ws + L.cols8), tc_la8_blocks(N, c.nf, c.depth),
+                                 c.count_reshare == 0 ? 1 : (c.sample_base == 0 ? 2 : 0), c.sample_base,
+                                 c.sample_base + N, s, (prof || !count_overlap) ? nullptr : side, num_sms, P, lo, hi)
+               : launch_count(cl, s, num_sms, P);
+  };
+  bool count0_done = false;
+  if (N) {
+    const int WC = count_plan(c.nf, 1).WC;
+    const uint64_t tot = N * (uint64_t)WC;
+    P.start();
+    if (c.count_engine == 0) {  // tensor engine: prods and byte planes in one pass
+      const uint64_t nhb = (N + TC_KB / 2 - 1) / (TC_KB / 2);
+      if (hin) {
+        // host inputs: Q sample chunks go up on the copy stream while the
+        // prologue of the chunks already resident runs on the main stream
+        // chunks on 128-sample K-block boundaries; the level-0 count (m_idx = 0)
+        // of a chunk runs as soon as its planes exist
+        const uint64_t nkb = (N + TC_KB - 1) / TC_KB;
+        const int Q = (int)std::min<uint64_t>(4, nkb);
+        int rc = stream_after(side->cp, s, side->ev[8]);
+        if (rc) return rc;
+        const bool count0 = !prof && c.heuristic == 0;
+        if (count0) GT_CUDA_CHECK(cudaMemsetAsync(S, 0, 3ull * 1 * (W + 1) * sizeof(uint64_t), s));
+        uint64_t hb_lo = 0;
+        for (int q = 0; q < Q; ++q) {
+          const uint64_t hb_hi = std::min<uint64_t>(nhb, 2 * (nkb * (q + 1) / Q));
+          const uint64_t lo = hb_lo * (TC_KB / 2), hi = std::min<uint64_t>(N, hb_hi * (TC_KB / 2));
+          for (int cc = 0; cc < 3; ++cc) {
+            GT_CUDA_CHECK(cudaMemcpyAsync((void*)(features + cc * N * nf + lo * nf), hin->X + cc * N * nf + lo * nf,
+                                          (hi - lo) * nf * sizeof(uint64_t), cudaMemcpyHostToDevice, side->cp));
+            GT_CUDA_CHECK(cudaMemcpyAsync((void*)(labels + cc * N + lo), hin->Y + cc * N + lo,
+                                          (hi - lo) * sizeof(uint64_t), cudaMemcpyHostToDevice, side->cp));
+          }
+          GT_CUDA_CHECK(cudaEventRecord(side->ev[9 + (q & 3)], side->cp));
+          GT_CUDA_CHECK(cudaStreamWaitEvent(s, side->ev[9 + (q & 3)], 0));
+          rc = launch_prep8(c, features, labels, ws, L, K, hb_lo, hb_hi, s);
+          if (rc) return rc;
+          if (count0) {
+            rc = count_range(0, 0, lo, hi);
+            if (rc) return rc;
+          }
+          hb_lo = hb_hi;
+        }
+        count0_done = count0;
+      } else {
+        int rc = launch_prep8(c, features, labels, ws, L, K, 0, nhb, s);
+        if (rc) return rc;
+      }
+    } else {
+      if (hin) {
+        for (int cc = 0; cc < 3; ++cc) {
+          GT_CUDA_CHECK(cudaMemcpyAsync((void*)(features + cc * N * nf), hin->X + cc * N * nf, N * nf * sizeof(uint64_t),
+                                        cudaMemcpyHostToDevice, s));
+          GT_CUDA_CHECK(cudaMemcpyAsync((void*)(labels + cc * N), hin->Y + cc * N, N * sizeof(uint64_t),
+                                        cudaMemcpyHostToDevice, s));
+        }
+      }
+      k_prods<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(features, labels, colm, N, c.nf, WC, c.sample_base, K,
+                                                            op_id(0, SITE_PRODS));
+      GT_LAUNCH_CHECK("k_prods");
+    }
+    P.stop(Prof::PRODS);
+  }
   int32_t trained = c.depth;
   for (int level = 0; level < c.depth; ++level) {
     const int n_h = 1 << level;
@@ -1530,29 +1636,12 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
       P.stop(Prof::PARTITION);
     }
     const uint64_t swords = 3ull * n_h * (W + 1);
-    GT_CUDA_CHECK(cudaMemsetAsync(S, 0, swords * sizeof(uint64_t), s));
-    if (N) {
-      CountLaunch cl{};
-      cl.midx = midx;
-      cl.f = f[cur];
-      cl.cols = colm;
-      cl.la = ws + L.la;
-      cl.leaf = ws + L.leaf;
-      cl.S = S;
-      cl.la_cap_words = la_words(N, c.nf, c.depth);
-      cl.N = N;
-      cl.base = c.sample_base;
-      cl.nf = c.nf;
-      cl.n_h = n_h;
-      cl.n_h_max = 1 << (c.depth - 1);
-      cl.K = K;
-      cl.level = level;
-      int rc = c.count_engine == 0
-                   ? launch_count_tc(cl, (const uint8_t*)(ws + L.cols8), tc_la8_blocks(N, c.nf, c.depth),
-                                     c.count_reshare == 0 ? 1 : (c.sample_base == 0 ? 2 : 0), c.sample_base,
-                                     c.sample_base + N, s, (prof || !count_overlap) ? nullptr : side, num_sms, P)
-                   : launch_count(cl, s, num_sms, P);
-      if (rc) return rc;
+    if (!(level == 0 && count0_done)) {  // level 0 may already be counted chunk by chunk (host operands)
+      GT_CUDA_CHECK(cudaMemsetAsync(S, 0, swords * sizeof(uint64_t), s));
+      if (N) {
+        int rc = count_range(level, cur, 0, N);
+        if (rc) return rc;
+      }
     }
     if (c.count_engine == 1 && (c.count_reshare == 0 ? N > 0 : c.sample_base == 0)) {  // tensor engine: in k_count_mma
       const int cells = n_h * (int)W;
@@ -1659,8 +1748,35 @@ int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_
       break;
     }
   }
+  if (hin) {
+    GT_CUDA_CHECK(cudaMemcpyAsync(hin->T, T, 3 * slots * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    GT_CUDA_CHECK(cudaMemcpyAsync(hin->F, F, 3 * slots * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  }
   if (depth_out) *depth_out = trained;
   return P.finish();
+}
+
+int gt_train_ex(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* labels, const uint64_t* filler,
+                uint64_t* T, uint64_t* F, int32_t* depth_out, void* workspace, uint64_t workspace_bytes,
+                const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user, gt_heuristic_fn heuristic,
+                void* heuristic_user, void* stream, gt_train_profile* prof) {
+  return train_impl(cfg, features, labels, filler, T, F, depth_out, workspace, workspace_bytes, keys, allreduce,
+                    allreduce_user, heuristic, heuristic_user, stream, prof, nullptr);
+}
+
+uint64_t gt_train_host_workspace_bytes(const gt_train_cfg* cfg) {
+  if (!cfg || cfg->depth < 1 || cfg->depth > 16 || cfg->nf < 1 || cfg->nf > 64) return 0;
+  return layout(*cfg, true).total * sizeof(uint64_t);
+}
+
+int gt_train_host(const gt_train_cfg* cfg, const uint64_t* features_h, const uint64_t* labels_h,
+                  const uint64_t* filler_h, uint64_t* T_h, uint64_t* F_h, int32_t* depth_out, void* workspace,
+                  uint64_t workspace_bytes, const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user,
+                  void* stream) {
+  if (cfg && cfg->heuristic != 0) return fail_inval("gt_train_host: heuristic mpc only (use gt_train_ex for tee)");
+  const HostIn hin{features_h, labels_h, filler_h, T_h, F_h};
+  return train_impl(cfg, nullptr, nullptr, nullptr, nullptr, nullptr, depth_out, workspace, workspace_bytes, keys,
+                    allreduce, allreduce_user, nullptr, nullptr, stream, nullptr, &hin);
 }
 
 // diagnostics: the heuristic phase timestamps of the last GT_HC_TIMING run (ns)

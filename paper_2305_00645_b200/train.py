@@ -98,7 +98,7 @@ class DeviceTrainer:
     device workspace; ``run`` can be called repeatedly (bench steps)."""
 
     def __init__(self, n_local: int, nf: int, cfg: TrainConfig, *, n_total: Optional[int] = None,
-                 sample_base: int = 0, device=None):
+                 sample_base: int = 0, device=None, host_io: bool = False):
         torch = _native.require_cuda()
         self.lib = _native.load()
         self.depth = _validate(cfg, nf)
@@ -120,7 +120,9 @@ class DeviceTrainer:
         c.n_local = self.n_local
         c.sample_base = int(sample_base)
         self.c = c
-        nbytes = self.lib.gt_train_workspace_bytes(ctypes.byref(c))
+        self.host_io = bool(host_io)
+        nbytes = (self.lib.gt_train_host_workspace_bytes if self.host_io else self.lib.gt_train_workspace_bytes)(
+            ctypes.byref(c))
         if nbytes == 0:
             raise ValueError("unsupported training shape (depth 1..16, 1..64 features)")
         self.workspace = torch.empty(nbytes // 8, dtype=torch.int64, device=self.device)
@@ -162,6 +164,42 @@ class DeviceTrainer:
         _native.check(rc)
         return int(d.value)
 
+
+    def run_host(self, Xh, Yh, filler_h, T_h, F_h, keys, *, allreduce=None, stream=None) -> int:
+        """Training from HOST operands (pinned int64 CPU tensors, same shapes as
+        `run`; results into the pinned host tensors T_h / F_h [3, 2^H - 1]):
+        gt_train_host uploads the sample shares in chunks beside the prologue
+        and reads the tree back, all ordered on `stream`.  Needs a trainer built
+        with host_io=True; synchronise the stream before reading T_h / F_h."""
+        torch = _native.require_cuda()
+        if not self.host_io:
+            raise ValueError("construct the DeviceTrainer with host_io=True for run_host")
+        if tuple(Xh.shape) != (3, self.n_local, self.nf) or tuple(Yh.shape) != (3, self.n_local):
+            raise ValueError("features must be [3, n, nf] and labels [3, n] component shares")
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        d = ctypes.c_int32(0)
+        cb = _native.ALLREDUCE_FN(0) if allreduce is None else allreduce
+        rc = self.lib.gt_train_host(ctypes.byref(self.c), Xh.data_ptr(), Yh.data_ptr(), filler_h.data_ptr(),
+                                    T_h.data_ptr(), F_h.data_ptr(), ctypes.byref(d), ptr(self.workspace),
+                                    self.workspace.numel() * 8, ctypes.byref(keys), cb, None,
+                                    ctypes.c_void_p(s.cuda_stream))
+        _native.check(rc)
+        return int(d.value)
+
+    def capture_host(self, Xh, Yh, filler_h, T_h, F_h, keys):
+        """CUDA graph of one whole host-operand run (uploads, kernels, readback)."""
+        torch = _native.require_cuda()
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self.run_host(Xh, Yh, filler_h, T_h, F_h, keys, stream=s)
+        s.synchronize()
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.run_host(Xh, Yh, filler_h, T_h, F_h, keys, stream=s)
+        self._graph_host_refs = (Xh, Yh, filler_h, T_h, F_h, keys)
+        return g.replay
 
     def capture(self, X, Y, filler, keys):
         """Capture one whole training run (every level's kernels) into a CUDA

@@ -321,3 +321,43 @@ def test_count_engines_share_exact_vs_oracle(nf, n, depth):
     for engine in ("tensor", "cuda"):
         T, F, d = train_components(X, Y, TrainConfig(depth=depth, count_engine=engine), setup, derive_seed(seed, "deal"))
         assert np.array_equal(T, To) and np.array_equal(F, Fo), engine
+
+
+@pytest.mark.parametrize("engine", ["tensor", "cuda"])
+def test_host_operand_entry_equals_device_entry(engine):
+    """gt_train_host (pinned host shares in, chunked uploads beside the
+    prologue, tree shares out) gives exactly the device entry's shares, also
+    when captured in a CUDA graph and replayed."""
+    from paper_2305_00645_b200._native import gt_keys
+    from paper_2305_00645_b200.seeds import derive_seed
+    from paper_2305_00645_b200.train import DeviceTrainer, TrainConfig, train_components
+
+    rng = np.random.default_rng(77)
+    n, nf, depth = 3001, 12, 5
+    data = rng.integers(0, 2, size=(n, nf + 1), dtype=np.uint8)
+    seed = b"\x77" * 16
+    setup, k, keys_t = run_keys(seed)
+    fill = filler_values(setup.filler_seed, (1 << depth) - 1, nf + 1)
+    X, Y = share(data[:, :-1], rng), share(data[:, -1], rng)
+    cfg = TrainConfig(depth=depth, count_engine=engine)
+    T1, F1, _ = train_components(X, Y, cfg, setup, derive_seed(seed, "deal"))
+    K = gt_keys()
+    K.dealer.k0, K.dealer.k1 = keys_t[0]
+    for i in range(3):
+        K.pair[i].k0, K.pair[i].k1 = keys_t[i + 1]
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).pin_memory()  # noqa: E731
+    Xh, Yh, Fh = pin(X), pin(Y), pin(fill)
+    Th = torch.empty((3, (1 << depth) - 1), dtype=torch.int64).pin_memory()
+    Fo = torch.empty_like(Th).pin_memory()
+    tr = DeviceTrainer(n, nf, cfg, host_io=True)
+    tr.run_host(Xh, Yh, Fh, Th, Fo, K)
+    torch.cuda.synchronize()
+    assert np.array_equal(Th.numpy().view(np.uint64), T1) and np.array_equal(Fo.numpy().view(np.uint64), F1)
+    Th.zero_()
+    Fo.zero_()
+    replay = tr.capture_host(Xh, Yh, Fh, Th, Fo, K)
+    Th.zero_()
+    Fo.zero_()
+    replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(Th.numpy().view(np.uint64), T1) and np.array_equal(Fo.numpy().view(np.uint64), F1)
