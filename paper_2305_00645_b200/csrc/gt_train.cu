@@ -1302,7 +1302,7 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
   for (uint64_t s0 = lo; s0 < hi; s0 += cap, ++k) {  // lo is a multiple of TC_KB
     const uint64_t cn = std::min<uint64_t>(cap, hi - s0);
     const uint32_t nkb = (uint32_t)((cn + TC_KB - 1) / TC_KB);
-    uint8_t* buf = (uint8_t*)c.la + (uint64_t)(k & 1) * buf_bytes;
+    uint8_t* buf = (uint8_t*)c.la + (side ? (uint64_t)(k & 1) * buf_bytes : 0ull);
     if (side && k >= 2) GT_CUDA_CHECK(cudaStreamWaitEvent(s, side->ev[2 + (k & 1)], 0));  // buffer reuse
     Lanes8Args la{};
     la.midx = c.midx;

@@ -302,11 +302,13 @@ def test_score_ring64_and_tau_variants_match_reference_and_oracle():
         assert np.array_equal(T, To) and np.array_equal(F, Fo), m
 
 
-@pytest.mark.parametrize("nf,n,depth", [(13, 4000, 5), (20, 3001, 4), (33, 1500, 3), (64, 700, 2)])
+@pytest.mark.parametrize("nf,n,depth", [(13, 4000, 5), (20, 3001, 4), (33, 1500, 3), (64, 700, 2),
+                                         (32, 60000, 8)])
 def test_count_engines_share_exact_vs_oracle(nf, n, depth):
     """Tensor-core (tcgen05 kind::i8 limb) and CUDA-core count contractions
-    give the oracle's shares, including several column blocks (nf > 15) and
-    partial sample blocks; the revealed tree equals the plain-integer shadow."""
+    give the oracle's shares, including several column blocks (nf > 15),
+    partial sample blocks, and (60000 x 32, depth 8) levels that take several
+    lane chunks and K ranges."""
     from paper_2305_00645_b200.seeds import derive_seed
 
     rng = np.random.default_rng(nf * 1000 + n)
