@@ -336,10 +336,14 @@ __global__ void __launch_bounds__(128, 1) k_count_mma(MmaArgs a) {
   __shared__ __align__(8) uint64_t full[TC_MC_STAGES], empty[TC_MC_STAGES], done;
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int c = blockIdx.z, mt = blockIdx.y / a.nbn, nb = blockIdx.y % a.nbn;
+  // grid (3 components x M tiles, column blocks x K ranges): the CTAs that
+  // share operand planes -- the M tiles of one (K range, column block) read
+  // the same U/X planes, the two components of an M tile the same la planes --
+  // are adjacent in launch order, so they run together and share them in L2
+  const int c = blockIdx.x % 3, mt = blockIdx.x / 3, nb = blockIdx.y % a.nbn, kr = blockIdx.y / a.nbn;
   const int cn = (c + 1) % 3, cp = (c + 2) % 3;
   const uint32_t per = (a.nkb + a.nkr - 1) / a.nkr;
-  const uint32_t kb0 = blockIdx.x * per, kb1 = min(a.nkb, kb0 + per);
+  const uint32_t kb0 = kr * per, kb1 = min(a.nkb, kb0 + per);
   const int T = kb1 > kb0 ? 2 * (int)(kb1 - kb0) : 0;  // half blocks
   const int HB = a.N * (TC_KB / 2);                     // one term of a half block
   const int stage = TC_A_HB + 2 * HB;
@@ -435,7 +439,7 @@ __global__ void __launch_bounds__(128, 1) k_count_mma(MmaArgs a) {
         v += __shfl_xor_sync(0xffffffffu, v, 4);
         const int w = nb * a.cpb + 2 * k + h;
         if (p == 0 && n < a.n_h && w <= a.W) {
-          if (a.alpha && blockIdx.x == 0 && w < a.W) {
+          if (a.alpha && kr == 0 && w < a.W) {
             // zero shares of the count products summed over the shard (see
             // k_count_alpha): alpha_c = F_c - F_{c-1}
             uint64_t F[2];

@@ -910,13 +910,17 @@ uint64_t la_words(uint64_t N, int nf, int depth) {
   return std::min<uint64_t>(want, per * std::max<uint64_t>(N, 1));
 }
 
-// la8 chunk capacity in 128-sample blocks (tensor engine): ~32 MB of byte
+// la8 chunk capacity in 128-sample blocks (tensor engine): ~256 MB of byte
 // planes at the deepest level, at least one block, at most the shard
 uint64_t tc_la8_blocks(uint64_t N, int nf, int depth) {
   const TcPlan tp = tc_plan(nf, 1 << (depth - 1));
   const uint64_t per_blk = 3ull * tp.mtiles * TC_ABLK;
   const uint64_t nkb = std::max<uint64_t>(1, (N + TC_KB - 1) / TC_KB);
-  return std::max<uint64_t>(1, std::min<uint64_t>(nkb, (32ull << 20) / per_blk));
+  // 256 MB per buffer: a C2 level is one chunk; at C4 fewer chunks beat L2
+  // residency of the lane planes (measured 32 / 64 / 128 / 256 MB: contraction
+  // 14.7 / 11.3 / 11.3 / 10.3 ms per C4 tree); GT_LA8_MB overrides
+  static const uint64_t mb = getenv("GT_LA8_MB") ? (uint64_t)atoi(getenv("GT_LA8_MB")) : 256ull;
+  return std::max<uint64_t>(1, std::min<uint64_t>(nkb, (mb << 20) / per_blk));
 }
 
 // Division tapes of every heuristic level (levels 0 .. depth-2, mpc only),
@@ -1357,7 +1361,7 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
     ma.nkr = (int)((nkb + per - 1) / per);
     {
       cudaLaunchConfig_t lc{};
-      lc.gridDim = dim3((unsigned)ma.nkr, (unsigned)(tp.mtiles * tp.nbn), 3);
+      lc.gridDim = dim3((unsigned)(3 * tp.mtiles), (unsigned)(ma.nkr * tp.nbn), 1);
       lc.blockDim = dim3(128);
       lc.dynamicSmemBytes = (size_t)smem;
       lc.stream = s2;
