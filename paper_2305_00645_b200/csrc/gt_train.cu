@@ -1585,7 +1585,10 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
         // chunks on 128-sample K-block boundaries; the level-0 count (m_idx = 0)
         // of a chunk runs as soon as its planes exist
         const uint64_t nkb = (N + TC_KB - 1) / TC_KB;
-        const int Q = (int)std::min<uint64_t>(4, nkb);
+        // two chunks measured best on C2 (1 / 2 / 3 / 4 / 8: e2e 1.242 / 1.221 / 1.231 / 1.257 / 1.338 ms):
+        // each chunk costs six copies and a count launch pair
+        static const int Qenv = getenv("GT_HOST_CHUNKS") ? atoi(getenv("GT_HOST_CHUNKS")) : 2;
+        const int Q = (int)std::min<uint64_t>((uint64_t)std::max(1, Qenv), nkb);
         int rc = stream_after(side->cp, s, side->ev[8]);
         if (rc) return rc;
         const bool count0 = !prof && c.heuristic == 0;
@@ -1600,8 +1603,8 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
             GT_CUDA_CHECK(cudaMemcpyAsync((void*)(labels + cc * N + lo), hin->Y + cc * N + lo,
                                           (hi - lo) * sizeof(uint64_t), cudaMemcpyHostToDevice, side->cp));
           }
-          GT_CUDA_CHECK(cudaEventRecord(side->ev[9 + (q & 3)], side->cp));
-          GT_CUDA_CHECK(cudaStreamWaitEvent(s, side->ev[9 + (q & 3)], 0));
+          GT_CUDA_CHECK(cudaEventRecord(side->ev[9 + (q % 6)], side->cp));
+          GT_CUDA_CHECK(cudaStreamWaitEvent(s, side->ev[9 + (q % 6)], 0));
           rc = launch_prep8(c, features, labels, ws, L, K, hb_lo, hb_hi, s);
           if (rc) return rc;
           if (count0) {
