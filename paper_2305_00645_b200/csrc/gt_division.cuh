@@ -206,6 +206,29 @@ __device__ __forceinline__ A3 division_warp_tape(const W2* __restrict__ gt, cons
   return out;
 }
 
+// Division by one warp from its lane tape already staged in shared memory
+// (`ts` = ladder blocks then Newton blocks, div_tape_blocks<L>(d) of them).
+template <int L>
+__device__ __forceinline__ A3 division_warp_staged(const W2* ts, const A3& p, const A3& q, const DivParams& d) {
+  constexpr uint64_t M = Ring<L>::M;
+  constexpr int LS = DivTape<L>::LADDER_STEP, LB = LtRand<L>::BLOCKS;
+  const int wl = threadIdx.x & 31;
+  const int nl = d.bound - 1;
+  A3 acc = a3(0, 0, 0);
+  for (int j = wl + 1; j <= nl; j += 32) {
+    const W2* b = ts + (j - 1) * LS;
+    const B3 below = lt_arith<L>(b, q, a3_const((1ull << j) & M));
+    const A3 t = b2a_arith<L>(bnot(below, 1ull), b[LB].a, b[LB].b, b[LB + 1].a);
+    acc = add<L>(acc, mul_pub<L>(t, 1ull << (d.bound - 1 - j)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) acc.v[i] = (acc.v[i] + __shfl_xor_sync(0xffffffffu, acc.v[i], o)) & M;
+  const A3 v = rsub_pub<L>(1ull << (d.bound - 1), acc);
+  return newton_from_tape<L>(p, q, v, d, ts + nl * LS);
+}
+
 // Whole division lane by one warp; every lane returns the result.  `tape`
 // points at this warp's division_tape_blocks() W2 slots of shared memory.
 // The ladder's steps run one per lane with in-register Philox (measured

@@ -607,16 +607,32 @@ constexpr int DIV_WARPS = 4;  // at most; fewer when the tape is large (score ri
 
 template <int SL>
 __global__ void __launch_bounds__(32 * DIV_WARPS) k_hc_div(NodeArgs a) {
-  extern __shared__ W2 tape_sm[];
+  extern __shared__ __align__(128) W2 tape_sm[];
   const int warp = threadIdx.x >> 5, wpc = blockDim.x >> 5;
   const uint64_t cols = 2 * (uint64_t)a.nf, lanes = (uint64_t)a.n_h * cols;
   const uint64_t li = (uint64_t)blockIdx.x * wpc + warp;
   if (li >= lanes) return;  // whole warp exits together
-  W2* tape = tape_sm + (size_t)warp * division_tape_blocks<SL>(a.d);
   const A3 p = ld3s(a.dv, lanes, li), q = ld3s(a.dv + 3 * lanes, lanes, li);
   // terms = division(P, qsafe)                              train.py:382
-  const A3 t = a.divtape ? division_warp_tape<SL>(a.divtape + li * (uint64_t)div_tape_blocks<SL>(a.d), p, q, a.d, tape)
-                         : division_warp<SL>(a.K, op_id(a.level, SITE_HC), 13, li, p, q, a.d, tape);
+  A3 t;
+  if (a.divtape) {
+    // the lane's whole precomputed tape (ladder + Newton) comes in by one bulk
+    // copy, so neither chain waits on global memory
+    __shared__ __align__(8) uint64_t bar[DIV_WARPS];
+    const int TB = div_tape_blocks<SL>(a.d);
+    W2* ts = tape_sm + (size_t)warp * TB;
+    if ((threadIdx.x & 31) == 0) {
+      mbar_init(&bar[warp], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&bar[warp], (uint32_t)(TB * sizeof(W2)));
+      bulk_g2s(ts, a.divtape + li * (uint64_t)TB, (uint32_t)(TB * sizeof(W2)), &bar[warp]);
+    }
+    __syncwarp();
+    mbar_wait(&bar[warp], 0);
+    t = division_warp_staged<SL>(ts, p, q, a.d);
+  } else {
+    t = division_warp<SL>(a.K, op_id(a.level, SITE_HC), 13, li, p, q, a.d, tape_sm + (size_t)warp * division_tape_blocks<SL>(a.d));
+  }
   if ((threadIdx.x & 31) == 0) st3s(a.dv + 6 * lanes, lanes, li, t);
 }
 
@@ -1009,7 +1025,7 @@ int launch_node_hc(const NodeArgs& na, cudaStream_t s, bool fuse_post) {
   GT_LAUNCH_CHECK("k_hc_pre");
   if (na.last || na.co_out) return GT_OK;
   const uint64_t lanes = (uint64_t)na.n_h * cols;
-  const int per_warp = (int)sizeof(W2) * division_tape_blocks<SL>(na.d);
+  const int per_warp = (int)sizeof(W2) * (na.divtape ? div_tape_blocks<SL>(na.d) : division_tape_blocks<SL>(na.d));
   const int wpc = std::max(1, std::min(DIV_WARPS, (200 * 1024) / per_warp));
   const int div_smem = per_warp * wpc;
   if (div_smem > 48 * 1024)
