@@ -415,6 +415,7 @@ struct NodeArgs {
   uint64_t* dv;               // [3][3][n_h*cols]: P, Q+[Q==0], division terms
   uint64_t* co_out;           // [3][n_h][3][cols] c_orig for the tee helper (or null)
   const W2* divtape;          // precomputed division blocks of this level (or null: draw live)
+  const W2* posttape;         // precomputed epilogue blocks of this level (or null: draw live)
   int n_h, nf, level, last, shift, tau, ts;
   DivParams d;
   Keys K;
@@ -696,6 +697,101 @@ __global__ void __launch_bounds__(256) k_div_tape(W2* tape, const uint32_t* __re
   tape[e] = word2(key < 0 ? ks.dealer : ks.pair[key], op_id(level, SITE_HC), 13 + (t >> 16), (t >> 8) & 0xff, li);
 }
 
+// hc_post_body's shared scratch in words: vals/idxs/nvals/nidxs [3][nf], hit
+// words, then the per-warp live-draw tapes (8 warps), 16-byte aligned
+__host__ __device__ inline int post_scratch_words(int nf) {
+  return ((12 * nf + 4) + 2 * 8 * (LtRand<64>::BLOCKS + 10) + 1) & ~1;
+}
+
+// ---------------------------------------------------------------------------
+// Precomputed randomness of the heuristic epilogue (scores' mask selects, the
+// argmin tournament, the budget-clear eqs and AND): one node's blocks, in the
+// order hc_post_body consumes them, are identical in structure for every
+// node (only the lanes move), so like the division tapes they are drawn for
+// every level up front and each node's CTA stages its run with one bulk copy.
+//   [scores: nf x (b2a 2 + mul 3)] [rounds r, pairs p: 62 = lt 52 + 2 selects]
+//   [budget: nf x eqz 5] [and: 3]
+// Entry: key+1 (8 bits) | pidx (8) | sub (16) | lane index (16) | lane kind (8:
+// 0 = n*nf + index, 1 = n).
+template <int SL>
+__host__ __device__ inline int post_rounds_blocks(int nf) {
+  int m = nf, b = 0;
+  while (m > 1) {
+    b += (m / 2) * ArgminPair<SL>::BLOCKS;
+    m = m / 2 + (m & 1);
+  }
+  return b;
+}
+template <int SL>
+__host__ __device__ inline int post_tape_blocks(int nf) { return 5 * nf + post_rounds_blocks<SL>(nf) + 5 * nf + 3; }
+__host__ __device__ inline int post_tape_blocks_w(int width, int nf) {
+  return width == 32 ? post_tape_blocks<32>(nf) : post_tape_blocks<64>(nf);
+}
+
+template <int SL>
+__global__ void k_post_table(uint64_t* table, int nf, uint32_t SA) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= post_tape_blocks<SL>(nf)) return;
+  constexpr int PB = ArgminPair<SL>::BLOCKS;
+  const uint32_t SH = SA + 2 + 5 * 7;
+  int key = -1, idx = 0, kind = 0;
+  uint32_t sub = 0, pidx = 0;
+  int b = e;
+  if (b < 5 * nf) {  // score mask select (select1 at SA)
+    idx = b / 5;
+    select_block_id(b % 5, SA, &key, &sub, &pidx);
+  } else if ((b -= 5 * nf) < post_rounds_blocks<SL>(nf)) {
+    int m = nf, r = 0;
+    while (b >= (m / 2) * PB) {
+      b -= (m / 2) * PB;
+      m = m / 2 + (m & 1);
+      ++r;
+    }
+    const uint32_t base = SA + 2 + 5 * r;
+    idx = b / PB;
+    const int j = b % PB;
+    constexpr int LB = LtRand<SL>::BLOCKS;
+    if (j < LB) {
+      lt_block_id<SL>(j, base, &key, &pidx);
+      sub = base;
+    } else if (j < LB + 5) {
+      select_block_id(j - LB, base + 1, &key, &sub, &pidx);
+    } else {
+      select_block_id(j - LB - 5, base + 3, &key, &sub, &pidx);
+    }
+  } else if ((b -= post_rounds_blocks<SL>(nf)) < 5 * nf) {  // budget eqz at SH
+    idx = b / 5;
+    const int w = b % 5;
+    sub = SH;
+    if (w < 2) key = -1, pidx = w;
+    else key = w - 2, pidx = 0;
+  } else {  // and_gate at SH+1, field 0, lane n
+    b -= 5 * nf;
+    key = b, sub = SH + 1, pidx = 0, kind = 1;
+  }
+  table[e] = (uint64_t)(uint32_t)(key + 1) | ((uint64_t)pidx << 8) | ((uint64_t)sub << 16) | ((uint64_t)idx << 32) |
+             ((uint64_t)kind << 48);
+}
+
+// every level's epilogue tape: [level][node][post_tape_blocks]; one thread per block
+__global__ void __launch_bounds__(256) k_post_tape(W2* tape, const uint64_t* __restrict__ table, uint32_t total,
+                                                   int nf, int E, Keys K) {
+  __shared__ Keys ks;
+  for (int i = threadIdx.x; i < (int)(sizeof(Keys) / 4); i += blockDim.x)
+    reinterpret_cast<uint32_t*>(&ks)[i] = reinterpret_cast<const uint32_t*>(&K)[i];
+  __syncthreads();
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  const uint32_t gn = e / (uint32_t)E;  // global node = (2^level - 1) + n
+  const uint64_t t = __ldg(table + (e - gn * (uint32_t)E));
+  const int level = 31 - __clz(gn + 1);
+  const uint32_t n = gn - ((1u << level) - 1);
+  const int key = (int)(t & 0xff) - 1, kind = (int)((t >> 48) & 0xff);
+  const uint32_t pidx = (uint32_t)((t >> 8) & 0xff), sub = (uint32_t)((t >> 16) & 0xffff);
+  const uint64_t lane = kind ? (uint64_t)n : (uint64_t)n * nf + (uint32_t)((t >> 32) & 0xffff);
+  tape[e] = word2(key < 0 ? ks.dealer : ks.pair[key], op_id(level, SITE_HC), sub, pidx, lane);
+}
+
 template <int SL>
 __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n) {
   extern __shared__ uint64_t sm[];
@@ -715,6 +811,22 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n) {
   const B3 gam = ldb3s(a.gam, hs, n);
   const uint64_t* terms = a.dv + 6 * lanes;
   auto TM = [&](int k) { return ld3s(terms, lanes, (uint64_t)n * cols + k); };
+  // staged epilogue tape (see k_post_table): one bulk copy of this node's run
+  const W2* pt = nullptr;
+  if (a.posttape) {
+    __shared__ __align__(8) uint64_t pbar;
+    W2* pts = reinterpret_cast<W2*>(sm + post_scratch_words(nf));
+    const int E = post_tape_blocks<SL>(nf);
+    if (tid == 0) {
+      mbar_init(&pbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&pbar, (uint32_t)(E * sizeof(W2)));
+      bulk_g2s(pts, a.posttape + (uint64_t)n * E, (uint32_t)(E * sizeof(W2)), &pbar);
+    }
+    __syncthreads();
+    mbar_wait(&pbar, 0);
+    pt = pts;
+  }
   // scores + masked argmin (tournament)     train.py:383-385, gadgets.py:366-401
   hc_ts(0 + 8 * a.level, a.ts);
   const uint32_t SA = 13 + div_subs(a.d);
@@ -723,7 +835,8 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n) {
     const A3 score = add<SL>(TM(2 * i), TM(2 * i + 1));
     B3 av;
     for (int c = 0; c < 3; ++c) av.v[c] = (gam.v[c] >> i) & 1ull;
-    const A3 v = select1<SL>(K, opH, SA, (uint64_t)n * nf + i, a3_const(worst), score, av);
+    const A3 v = pt ? select_arith<SL>(pt + 5 * i, a3_const(worst), score, av)
+                    : select1<SL>(K, opH, SA, (uint64_t)n * nf + i, a3_const(worst), score, av);
     for (int c = 0; c < 3; ++c) {
       vals[c * nf + i] = v.v[c];
       idxs[c * nf + i] = c == 0 ? (uint64_t)i : 0ull;
@@ -735,6 +848,7 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n) {
   const int warp = tid >> 5, nwarps = bd >> 5;
   W2* tape = reinterpret_cast<W2*>(hitw + 4) + warp * ArgminPair<SL>::BLOCKS;
   hc_ts(1 + 8 * a.level, a.ts);
+  int roff = 5 * nf;  // this round's first block in the staged tape
   for (int r = 0; m > 1; ++r) {
     const int pairs = m / 2;
     const uint32_t base = SA + 2 + 5 * r;
@@ -745,7 +859,15 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n) {
       const A3 ai = a3(idxs[2 * p], idxs[nf + 2 * p], idxs[2 * nf + 2 * p]);
       const A3 bi = a3(idxs[2 * p + 1], idxs[nf + 2 * p + 1], idxs[2 * nf + 2 * p + 1]);
       A3 nv, ni;
-      argmin_pair_warp<SL>(Ks, opH, base, lane, av, bv, ai, bi, tape, &nv, &ni);
+      if (pt) {
+        const W2* b = pt + roff + ArgminPair<SL>::BLOCKS * p;
+        constexpr int LB = LtRand<SL>::BLOCKS;
+        const B3 cw = lt_arith<SL>(b, bv, av);  // challenger wins iff b < a
+        nv = select_arith<SL>(b + LB, av, bv, cw);
+        ni = select_arith<64>(b + LB + 5, ai, bi, cw);
+      } else {
+        argmin_pair_warp<SL>(Ks, opH, base, lane, av, bv, ai, bi, tape, &nv, &ni);
+      }
       if ((tid & 31) == 0)
         for (int c = 0; c < 3; ++c) {
           nvals[c * nf + p] = nv.v[c];
@@ -765,21 +887,37 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n) {
         idxs[c * nf + p] = nidxs[c * nf + p];
       }
     __syncthreads();
+    roff += ArgminPair<SL>::BLOCKS * pairs;
     m = nm;
   }
   hc_ts(2 + 8 * a.level, a.ts);
   const A3 sd = a3(idxs[0], idxs[nf], idxs[2 * nf]);
   // gamma &= ~[sd == k]                                     train.py:386-387
   const uint32_t SH = SA + 2 + 5 * 7;
+  const W2* pb = pt ? pt + 5 * nf + post_rounds_blocks<SL>(nf) : nullptr;  // budget blocks
   for (int f = tid; f < nf; f += bd) {
-    const B3 h = eqz<64>(K, opH, SH, (uint64_t)n * nf + f, add_pub<64>(sd, 0ull - (uint64_t)f));
+    B3 h;
+    if (pb) {
+      const W2* b = pb + 5 * f;
+      const uint64_t Zw[3] = {b[2].a, b[3].a, b[4].a};
+      h = eq_arith<64>(add_pub<64>(sd, 0ull - (uint64_t)f), b[0].a, b[0].b, b[1].a, Zw);
+    } else {
+      h = eqz<64>(K, opH, SH, (uint64_t)n * nf + f, add_pub<64>(sd, 0ull - (uint64_t)f));
+    }
     for (int c = 0; c < 3; ++c) atomicOr((unsigned long long*)&hitw[c], (unsigned long long)((h.v[c] & 1ull) << f));
   }
   __syncthreads();
   if (tid == 0) {
     B3 hw;
     for (int c = 0; c < 3; ++c) hw.v[c] = hitw[c];
-    const B3 ng = and_gate(K, opH, SH + 1, 0, n, gam, bnot(hw, lowmask(nf)), lowmask(nf));
+    B3 ng;
+    if (pb) {
+      const W2* b = pb + 5 * nf;
+      const uint64_t Z[3] = {b[0].a & lowmask(nf), b[1].a & lowmask(nf), b[2].a & lowmask(nf)};
+      ng = and_z(gam, bnot(hw, lowmask(nf)), Z);
+    } else {
+      ng = and_gate(K, opH, SH + 1, 0, n, gam, bnot(hw, lowmask(nf)), lowmask(nf));
+    }
     for (int c = 0; c < 3; ++c) {
       a.hc[(1 * 3 + c) * hs + n] = sd.v[c];
       a.hc[(3 * 3 + c) * hs + n] = ng.v[c];
@@ -951,12 +1089,18 @@ uint64_t div_tape_words(const gt_train_cfg& c) {
   const uint64_t w = lanes * (uint64_t)TB;
   return w * 16 > (256ull << 20) ? 0 : w;
 }
+// Epilogue tapes of every heuristic level (W2 units); 0 when over 256 MB
+uint64_t post_tape_words(const gt_train_cfg& c) {
+  if (c.heuristic != 0 || c.depth < 2) return 0;
+  const uint64_t w = ((1ull << (c.depth - 1)) - 1) * (uint64_t)post_tape_blocks_w(c.score_width, c.nf);
+  return w * 16 > (256ull << 20) ? 0 : w;
+}
 inline uint64_t div_tape_level_off(int level, int nf, int TB) {  // W2 offset of level's tape
   return ((1ull << level) - 1) * 2ull * nf * (uint64_t)TB;
 }
 
 struct Layout {
-  uint64_t xin, yin, fin, tout, fout, cols, la, cols8, leaf, midx, divtape, divtable, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
+  uint64_t xin, yin, fin, tout, fout, cols, la, cols8, leaf, midx, divtape, divtable, posttape, posttable, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
 };
 
 Layout layout(const gt_train_cfg& c, bool host_io = false) {
@@ -982,6 +1126,8 @@ Layout layout(const gt_train_cfg& c, bool host_io = false) {
   L.leaf = take(3 * nmax);
   L.midx = take(3 * N);
   L.divtape = take(2 * div_tape_words(c));
+  L.posttape = take(2 * post_tape_words(c));
+  L.posttable = take(c.heuristic == 0 ? (uint64_t)post_tape_blocks_w(c.score_width, c.nf) : 0);
   {
     bool ok = false;
     const DivParams d = div_params(c.score_width, c.tau, &ok);
@@ -1013,7 +1159,7 @@ Layout layout(const gt_train_cfg& c, bool host_io = false) {
 
 template <int SL>
 int post_smem_bytes(const NodeArgs& na) {
-  return (int)sizeof(uint64_t) * (12 * na.nf + 4) + (int)sizeof(W2) * 8 * ArgminPair<SL>::BLOCKS;
+  return (int)sizeof(uint64_t) * post_scratch_words(na.nf) + (int)sizeof(W2) * post_tape_blocks<SL>(na.nf);
 }
 
 template <int SL>
@@ -1033,7 +1179,9 @@ int launch_node_hc(const NodeArgs& na, cudaStream_t s, bool fuse_post) {
   k_hc_div<SL><<<(unsigned)((lanes + wpc - 1) / wpc), 32 * wpc, div_smem, s>>>(na);
   GT_LAUNCH_CHECK("k_hc_div");
   if (fuse_post) return GT_OK;  // k_hc_post_finish runs it with the split
-  k_hc_post<SL><<<na.n_h, 256, post_smem_bytes<SL>(na), s>>>(na);
+  const int psm = post_smem_bytes<SL>(na);
+  if (psm > 48 * 1024) GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_post<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm));
+  k_hc_post<SL><<<na.n_h, 256, psm, s>>>(na);
   GT_LAUNCH_CHECK("k_hc_post");
   return GT_OK;
 }
@@ -1560,6 +1708,21 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
       k_div_table<64><<<(TB + 127) / 128, 128, 0, ts>>>(table, d);
       k_div_tape<64><<<(unsigned)((tape_words + 255) / 256), 256, 0, ts>>>(tape, table, tape_words, cols_i, TB, K);
     }
+    const uint64_t post_words = post_tape_words(c);
+    if (post_words) {
+      const int E = post_tape_blocks_w(c.score_width, c.nf);
+      const uint32_t SA = 13 + div_subs(d);
+      uint64_t* ptab = ws + L.posttable;
+      if (c.score_width == 32)
+        k_post_table<32><<<(E + 127) / 128, 128, 0, ts>>>(ptab, c.nf, SA);
+      else
+        k_post_table<64><<<(E + 127) / 128, 128, 0, ts>>>(ptab, c.nf, SA);
+      k_post_tape<<<(unsigned)((post_words + 255) / 256), 256, 0, ts>>>(reinterpret_cast<W2*>(ws + L.posttape), ptab,
+                                                                       (uint32_t)post_words, c.nf, E, K);
+      GT_LAUNCH_CHECK("k_post_tape");
+      P.count_launch();
+      P.count_launch();
+    }
     tape_forked = ts != s;
     P.count_launch();
     GT_LAUNCH_CHECK("k_div_tape");
@@ -1688,6 +1851,9 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
     na.hc = hc;
     na.dv = ws + L.dv;
     na.co_out = tee ? ws + L.co : nullptr;
+    na.posttape = post_tape_words(c) ? reinterpret_cast<const W2*>(ws + L.posttape) +
+                                           ((1ull << level) - 1) * (uint64_t)post_tape_blocks_w(c.score_width, c.nf)
+                                     : nullptr;
     na.divtape = tape_words ? reinterpret_cast<const W2*>(ws + L.divtape) +
                                   div_tape_level_off(level, c.nf, c.score_width == 32 ? div_tape_blocks<32>(d)
                                                                                       : div_tape_blocks<64>(d))
@@ -1756,10 +1922,17 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
     fa.K = K;
     P.start();
     if (fuse) {
+      const int psm = c.score_width == 32 ? post_smem_bytes<32>(na) : post_smem_bytes<64>(na);
+      if (psm > 48 * 1024) {
+        if (c.score_width == 32)
+          GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_post_finish<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm));
+        else
+          GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_post_finish<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm));
+      }
       if (c.score_width == 32)
-        k_hc_post_finish<32><<<n_h, 256, post_smem_bytes<32>(na), s>>>(na, fa);
+        k_hc_post_finish<32><<<n_h, 256, psm, s>>>(na, fa);
       else
-        k_hc_post_finish<64><<<n_h, 256, post_smem_bytes<64>(na), s>>>(na, fa);
+        k_hc_post_finish<64><<<n_h, 256, psm, s>>>(na, fa);
     } else {
       k_node_finish<<<n_h, 128, 0, s>>>(fa);
     }

@@ -23,4 +23,4 @@ for lv in range(bench.DEPTH_C2 - 1):
     ts = [buf[8 * lv + k] for k in range(7)]
     d = lambda a, b: (ts[b] - ts[a]) / 1e3
     print(f"level {lv}: scores {d(0, 1):.2f} us, argmin {d(1, 2):.2f} us, budget {d(2, 3):.2f} us, "
-          f"split: keys {d(3, 5):.2f} chains {d(5, 6):.2f} counters {d(6, 4):.2f} us)
+          f"split: keys {d(3, 5):.2f} chains {d(5, 6):.2f} counters {d(6, 4):.2f} us")
