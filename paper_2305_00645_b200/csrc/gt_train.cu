@@ -416,12 +416,117 @@ struct NodeArgs {
   uint64_t* co_out;           // [3][n_h][3][cols] c_orig for the tee helper (or null)
   const W2* divtape;          // precomputed division blocks of this level (or null: draw live)
   const W2* posttape;         // precomputed epilogue blocks of this level (or null: draw live)
+  const W2* nodetape;         // precomputed node-chain blocks of this level's nodes (or null)
   int n_h, nf, level, last, shift, tau, ts;
   DivParams d;
   Keys K;
 };
 
 __device__ __forceinline__ void bar_workers() { asm volatile("bar.sync 1, 192;" ::: "memory"); }
+
+// ---------------------------------------------------------------------------
+// Node tapes: the randomness of the per-node chains of every level (heuristic
+// prologue: probe eqs, featureless AND tree, ORs, should_split AND, new_f
+// select; replace: eq, b2a, counter selects; split: payload / child type /
+// condition selects, child counter selects; labels: lt + b2a), drawn for all
+// levels up front like the division tapes and staged per node by one bulk
+// copy.  Layout per node (blocks):
+//   PRE  [3 eqz x 5][and_reduce 3][or 3][or 3][and 3][select 5]        = 32
+//   REP  [eqz 5][b2a 2][select muls 3 x ceil(3 cols / 2)]
+//   SPL  [b2a 2 + mul 3][b2a 2 + mul 3][b2a 2][counter muls 3 x ceil(3 cols / 2)]
+//   LAB  [lt LtRand<64>][b2a 2]
+// Entry: site (8) | key+1 (8) | sub (8) | pidx (16) | lane kind (8: 0 = n,
+// 1 = 3n + idx) | idx (8).
+struct NodeTape {
+  int rep, spl, lab, total;  // segment offsets (PRE at 0)
+};
+__host__ __device__ inline NodeTape node_tape_plan(int nf) {
+  const int mh = (3 * 2 * nf + 1) / 2;  // counter-select blocks per key
+  NodeTape t;
+  t.rep = 32;
+  t.spl = t.rep + 7 + 3 * mh;
+  t.lab = t.spl + 12 + 3 * mh;
+  t.total = t.lab + LtRand<64>::BLOCKS + 2;
+  return t;
+}
+__device__ __forceinline__ uint64_t node_entry(uint32_t site, int key, uint32_t sub, uint32_t pidx, int kind, int idx) {
+  return (uint64_t)site | ((uint64_t)(uint32_t)(key + 1) << 8) | ((uint64_t)sub << 16) | ((uint64_t)pidx << 24) |
+         ((uint64_t)kind << 40) | ((uint64_t)idx << 48);
+}
+__global__ void k_node_table(uint64_t* table, int nf) {
+  const NodeTape t = node_tape_plan(nf);
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= t.total) return;
+  uint64_t v;
+  if (e < t.rep) {  // PRE (op HC)
+    if (e < 15) {  // eqz lane 3n + j at sub 0: dealer (0,0) (0,1), pair_i (0,0)
+      const int j = e / 5, w = e % 5;
+      v = w < 2 ? node_entry(SITE_HC, -1, 0, w, 1, j) : node_entry(SITE_HC, w - 2, 0, 0, 1, j);
+    } else if (e < 27) {  // and_reduce (sub 1), or (2), or (3), and (4): pair_i (sub, 0)
+      const int q = e - 15;
+      v = node_entry(SITE_HC, q % 3, 1 + q / 3, 0, 0, 0);
+    } else {  // select at 5: b2a dealer (5,0) (5,1), mul pair_i (6,0)
+      const int w = e - 27;
+      v = w < 2 ? node_entry(SITE_HC, -1, 5, w, 0, 0) : node_entry(SITE_HC, w - 2, 6, 0, 0, 0);
+    }
+  } else if (e < t.spl) {  // REP (op REPLACE): eqz at 0, b2a at 1, counter-select muls at 2
+    const int q = e - t.rep;
+    if (q < 5) v = q < 2 ? node_entry(SITE_REPLACE, -1, 0, q, 0, 0) : node_entry(SITE_REPLACE, q - 2, 0, 0, 0, 0);
+    else if (q < 7) v = node_entry(SITE_REPLACE, -1, 1, q - 5, 0, 0);
+    else v = node_entry(SITE_REPLACE, (q - 7) % 3, 2, (q - 7) / 3, 0, 0);
+  } else if (e < t.lab) {  // SPL (op SPLIT): selects at 0/1, 2/3, b2a at 4, counter-select muls at 5
+    const int q = e - t.spl;
+    if (q < 10) {
+      const int g = q / 5, w = q % 5;
+      v = w < 2 ? node_entry(SITE_SPLIT, -1, 2 * g, w, 0, 0) : node_entry(SITE_SPLIT, w - 2, 2 * g + 1, 0, 0, 0);
+    } else if (q < 12) {
+      v = node_entry(SITE_SPLIT, -1, 4, q - 10, 0, 0);
+    } else {
+      v = node_entry(SITE_SPLIT, (q - 12) % 3, 5, (q - 12) / 3, 0, 0);
+    }
+  } else {  // LAB (op LABELS): lt at 0, b2a at 1
+    const int q = e - t.lab;
+    if (q < LtRand<64>::BLOCKS) {
+      int key;
+      uint32_t pidx;
+      lt_block_id<64>(q, 0, &key, &pidx);
+      v = node_entry(SITE_LABELS, key, 0, pidx, 0, 0);
+    } else {
+      v = node_entry(SITE_LABELS, -1, 1, q - LtRand<64>::BLOCKS, 0, 0);
+    }
+  }
+  table[e] = v;
+}
+// [global node (2^level - 1 + n)][entry]; one thread per block
+__global__ void __launch_bounds__(256) k_node_tape(W2* tape, const uint64_t* __restrict__ table, uint32_t total, int E,
+                                                   Keys K) {
+  __shared__ Keys ks;
+  for (int i = threadIdx.x; i < (int)(sizeof(Keys) / 4); i += blockDim.x)
+    reinterpret_cast<uint32_t*>(&ks)[i] = reinterpret_cast<const uint32_t*>(&K)[i];
+  __syncthreads();
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  const uint32_t gn = e / (uint32_t)E;
+  const uint64_t t = __ldg(table + (e - gn * (uint32_t)E));
+  const int level = 31 - __clz(gn + 1);
+  const uint32_t n = gn - ((1u << level) - 1);
+  const uint32_t site = (uint32_t)(t & 0xff), sub = (uint32_t)((t >> 16) & 0xff), pidx = (uint32_t)((t >> 24) & 0xffff);
+  const int key = (int)((t >> 8) & 0xff) - 1, kind = (int)((t >> 40) & 0xff), idx = (int)((t >> 48) & 0xff);
+  const uint64_t lane = kind ? 3ull * n + idx : (uint64_t)n;
+  tape[e] = word2(key < 0 ? ks.dealer : ks.pair[key], op_id(level, site), sub, pidx, lane);
+}
+// stage a node's tape segment [off, off + len) into shared memory by one bulk copy (thread 0 issues; all wait)
+__device__ __forceinline__ const W2* stage_node_tape(const W2* g, int len, W2* dst, uint64_t* bar) {
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(bar, (uint32_t)(len * sizeof(W2)));
+    bulk_g2s(dst, g, (uint32_t)(len * sizeof(W2)), bar);
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  return dst;
+}
 
 // c_orig cell e = (row r, column k) of node n: c_start + the counters
 // assembled from the count partials (train.py:256, 336-343)
@@ -545,8 +650,22 @@ __global__ void __launch_bounds__(64) k_hc_pre(NodeArgs a) {
   const uint64_t hs = (uint64_t)a.n_h;
   uint64_t* co = sm;  // [3][3*cols] c_orig
   const uint32_t opH = op_id(a.level, SITE_HC), opR = op_id(a.level, SITE_REPLACE);
+  const NodeTape NT = node_tape_plan(nf);
+  __shared__ __align__(8) uint64_t nbar;
+  W2* ntb = reinterpret_cast<W2*>(co + ((3 * C3 + 1) & ~1));
+  if (a.nodetape && tid == 0) {  // the prologue + replace segments of this node's tape
+    mbar_init(&nbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&nbar, (uint32_t)(NT.spl * sizeof(W2)));
+    bulk_g2s(ntb, a.nodetape + (uint64_t)n * NT.total, (uint32_t)(NT.spl * sizeof(W2)), &nbar);
+  }
   for (int e = tid; e < 3 * C3; e += blockDim.x) co[e] = co_cell(a, e / C3, n, e % C3);
   __syncthreads();
+  const W2* nt = nullptr;
+  if (a.nodetape) {
+    mbar_wait(&nbar, 0);
+    nt = ntb;
+  }
   auto CO = [&](int e) { return a3(co[e], co[C3 + e], co[2 * C3 + e]); };
   if (a.co_out)  // heuristic "tee": hand the counters to the trusted helper
     for (int e = tid; e < C3; e += blockDim.x) st3s(a.co_out, hs * C3, (uint64_t)n * C3 + e, CO(e));
@@ -562,7 +681,13 @@ __global__ void __launch_bounds__(64) k_hc_pre(NodeArgs a) {
         if (wl == 0) v = add<64>(CO(cols + 0), CO(cols + 1));
         else if (wl == 1) v = add<64>(CO(2 * cols + 0), CO(2 * cols + 1));
         else v = add_pub<64>(fl, 0ull - F_LEAF);
-        z = eqz<64>(K, opH, 0, (uint64_t)n * 3 + wl, v);
+        if (nt) {
+          const W2* b = nt + 5 * wl;
+          const uint64_t Zw[3] = {b[2].a, b[3].a, b[4].a};
+          z = eq_arith<64>(v, b[0].a, b[0].b, b[1].a, Zw);
+        } else {
+          z = eqz<64>(K, opH, 0, (uint64_t)n * 3 + wl, v);
+        }
       }
       B3 p0, p1, act;
 #pragma unroll
@@ -574,11 +699,25 @@ __global__ void __launch_bounds__(64) k_hc_pre(NodeArgs a) {
       if (wl == 0) {
         // featureless = and_reduce(~gam), leafish, should_split   train.py:360-364
         const B3 gam = ldb3s(a.gam, hs, n);
-        const B3 fless = and_reduce(K, opH, 1, 0, n, bnot(gam, lowmask(nf)), nf);
-        const B3 o1 = or_gate(K, opH, 2, n, p0, p1, 1ull);
-        const B3 leafish = or_gate(K, opH, 3, n, o1, fless, 1ull);
-        const B3 ss = and_gate(K, opH, 4, 0, n, act, bnot(leafish, 1ull), 1ull);
-        const A3 nfv = select1<64>(K, opH, 5, n, fl, a3(0, 0, 0), ss);
+        B3 ss;
+        A3 nfv;
+        if (nt) {
+          const uint64_t Zr[3] = {nt[15].a, nt[16].a, nt[17].a};
+          const B3 fless = and_reduce_w(bnot(gam, lowmask(nf)), nf, Zr);
+          const uint64_t Z2[3] = {nt[18].a & 1ull, nt[19].a & 1ull, nt[20].a & 1ull};
+          const B3 o1 = bxor(bxor(p0, p1), and_z(p0, p1, Z2));
+          const uint64_t Z3[3] = {nt[21].a & 1ull, nt[22].a & 1ull, nt[23].a & 1ull};
+          const B3 leafish = bxor(bxor(o1, fless), and_z(o1, fless, Z3));
+          const uint64_t Z4[3] = {nt[24].a & 1ull, nt[25].a & 1ull, nt[26].a & 1ull};
+          ss = and_z(act, bnot(leafish, 1ull), Z4);
+          nfv = select_arith<64>(nt + 27, fl, a3(0, 0, 0), ss);
+        } else {
+          const B3 fless = and_reduce(K, opH, 1, 0, n, bnot(gam, lowmask(nf)), nf);
+          const B3 o1 = or_gate(K, opH, 2, n, p0, p1, 1ull);
+          const B3 leafish = or_gate(K, opH, 3, n, o1, fless, 1ull);
+          ss = and_gate(K, opH, 4, 0, n, act, bnot(leafish, 1ull), 1ull);
+          nfv = select1<64>(K, opH, 5, n, fl, a3(0, 0, 0), ss);
+        }
         for (int c = 0; c < 3; ++c) {
           a.hc[(0 * 3 + c) * hs + n] = ss.v[c] & 1ull;
           a.hc[(2 * 3 + c) * hs + n] = nfv.v[c];
@@ -591,13 +730,30 @@ __global__ void __launch_bounds__(64) k_hc_pre(NodeArgs a) {
   // replace: empty nodes adopt the parent's effective counters  train.py:269-276
   if (a.level > 0) {
     A3 ca = a3(0, 0, 0);
-    if (wl == 0) ca = b2a<64>(K, opR, 1, n, eqz<64>(K, opR, 0, n, add<64>(CO(0), CO(1))));
+    const W2* rb = nt ? nt + NT.rep : nullptr;
+    if (wl == 0) {
+      if (rb) {
+        const uint64_t Zw[3] = {rb[2].a, rb[3].a, rb[4].a};
+        const B3 hz = eq_arith<64>(add<64>(CO(0), CO(1)), rb[0].a, rb[0].b, rb[1].a, Zw);
+        ca = b2a_arith<64>(hz, rb[5].a, rb[5].b, rb[6].a);
+      } else {
+        ca = b2a<64>(K, opR, 1, n, eqz<64>(K, opR, 0, n, add<64>(CO(0), CO(1))));
+      }
+    }
 #pragma unroll
     for (int c = 0; c < 3; ++c) ca.v[c] = __shfl_sync(0xffffffffu, ca.v[c], 0);
     const uint64_t pn = (uint64_t)(n >> 1);
     for (int e = wl; e < C3; e += 32) {
       const A3 par = ld3s(a.ceff_prev, (hs / 2) * C3, pn * C3 + e);
-      st3s(a.ceff, hs * C3, (uint64_t)n * C3 + e, select_with<64>(K, opR, 1, (uint32_t)e, n, CO(e), par, ca));
+      A3 out;
+      if (rb) {
+        const W2* b = rb + 7 + 3 * (e >> 1);
+        const uint64_t F[3] = {(e & 1) ? b[0].b : b[0].a, (e & 1) ? b[1].b : b[1].a, (e & 1) ? b[2].b : b[2].a};
+        out = add<64>(CO(e), mul_z<64>(diff<64>(par, CO(e)), ca, F));
+      } else {
+        out = select_with<64>(K, opR, 1, (uint32_t)e, n, CO(e), par, ca);
+      }
+      st3s(a.ceff, hs * C3, (uint64_t)n * C3 + e, out);
     }
   } else {
     for (int e = wl; e < C3; e += 32) st3s(a.ceff, hs * C3, (uint64_t)n * C3 + e, CO(e));
@@ -953,6 +1109,7 @@ struct FinishArgs {
   const uint64_t* lab;                  // [3][n_h] helper labels (heuristic tee) or null
   uint64_t slots;
   int n_h, nf, level, labels, ts;
+  const W2* nodetape;  // precomputed node-chain blocks of this level's nodes (or null: draw live)
   Keys K;
 };
 
@@ -964,6 +1121,15 @@ __device__ __forceinline__ void node_finish_body(const FinishArgs& a, int n) {
   const Keys& K = a.K;
   hc_ts(5 + 8 * a.level, a.ts);
   auto CE = [&](int e) { return ld3s(a.ceff, hs * C3, (uint64_t)n * C3 + e); };
+  // this node's split (or labels) segment of the precomputed node tape
+  const NodeTape NT = node_tape_plan(a.nf);
+  __shared__ __align__(128) W2 nsb[16 + 12 + 3 * 64 * 3 + LtRand<64>::BLOCKS];  // >= max segment
+  __shared__ __align__(8) uint64_t nbar;
+  const W2* nt = nullptr;
+  if (a.nodetape && !(a.labels && a.lab)) {
+    const int off = a.labels ? NT.lab : NT.spl, len = a.labels ? NT.total - NT.lab : NT.lab - NT.spl;
+    nt = stage_node_tape(a.nodetape + (uint64_t)n * NT.total + off, len, nsb, &nbar);
+  }
   if (a.labels && a.lab) {  // labels from the trusted helper (train.py:301-302)
     if (tid == 0) {
       st3s(a.T, a.slots, slot, ld3s(a.lab, hs, n));
@@ -976,7 +1142,9 @@ __device__ __forceinline__ void node_finish_body(const FinishArgs& a, int n) {
     if (tid == 0) {
       const uint32_t op = op_id(a.level, SITE_LABELS);
       const A3 psi0 = add<64>(CE(cols), CE(cols + 1)), psi1 = add<64>(CE(2 * cols), CE(2 * cols + 1));
-      const A3 lab = b2a<64>(K, op, 1, n, lt<64>(K, op, 0, n, psi0, psi1));
+      constexpr int LB = LtRand<64>::BLOCKS;
+      const A3 lab = nt ? b2a_arith<64>(lt_arith<64>(nt, psi0, psi1), nt[LB].a, nt[LB].b, nt[LB + 1].a)
+                        : b2a<64>(K, op, 1, n, lt<64>(K, op, 0, n, psi0, psi1));
       st3s(a.T, a.slots, slot, lab);
       st3s(a.F, a.slots, slot, ld3s(a.f, hs, n));
     }
@@ -990,18 +1158,20 @@ __device__ __forceinline__ void node_finish_body(const FinishArgs& a, int n) {
   if (tid == 0) {  // payload T = is_int ? sd : filler        (train.py:287)
     const A3 sd = ld3s(a.hc + 3 * hs, hs, n);
     const uint64_t fl = a.filler[slot];
-    const A3 cb = b2a<64>(K, op, 0, n, ss);
-    st3s(a.T, a.slots, slot, select_with<64>(K, op, 0, 0, n, a3_const(fl), sd, cb));
+    const A3 cb = nt ? a3(0, 0, 0) : b2a<64>(K, op, 0, n, ss);
+    st3s(a.T, a.slots, slot, nt ? select_arith<64>(nt, a3_const(fl), sd, ss)
+                                : select_with<64>(K, op, 0, 0, n, a3_const(fl), sd, cb));
     st3s(a.F, a.slots, slot, ld3s(a.hc + 6 * hs, hs, n));
   } else if (tid == 32) {  // child type = is_int ? LEAF : DUMMY  (train.py:288-289)
-    const A3 cf = select_with<64>(K, op, 2, 0, n, a3_const(F_DUMMY), a3_const(F_LEAF), b2a<64>(K, op, 2, n, ss));
+    const A3 cf = nt ? select_arith<64>(nt + 5, a3_const(F_DUMMY), a3_const(F_LEAF), ss)
+                     : select_with<64>(K, op, 2, 0, n, a3_const(F_DUMMY), a3_const(F_LEAF), b2a<64>(K, op, 2, n, ss));
     const A3 ng = ld3s(a.hc + 9 * hs, hs, n);
     for (int ch = 0; ch < 2; ++ch) {
       st3s(a.f_nxt, cs, 2 * n + ch, cf);
       st3s(a.gam_nxt, cs, 2 * n + ch, ng);
     }
   } else if (tid == 64) {  // child counters' condition
-    const A3 c2 = b2a<64>(K, op, 4, n, ss);
+    const A3 c2 = nt ? b2a_arith<64>(ss, nt[10].a, nt[10].b, nt[11].a) : b2a<64>(K, op, 4, n, ss);
     for (int c = 0; c < 3; ++c) ca[c] = c2.v[c];
   }
   __syncthreads();
@@ -1009,7 +1179,14 @@ __device__ __forceinline__ void node_finish_body(const FinishArgs& a, int n) {
   // child counters = select(c_eff, 0, is_int)                 train.py:290
   const A3 cav = a3(ca[0], ca[1], ca[2]);
   for (int e = tid; e < C3; e += bd) {
-    const A3 cc = select_with<64>(K, op, 4, (uint32_t)e, n, CE(e), a3(0, 0, 0), cav);
+    A3 cc;
+    if (nt) {
+      const W2* b = nt + 12 + 3 * (e >> 1);
+      const uint64_t F[3] = {(e & 1) ? b[0].b : b[0].a, (e & 1) ? b[1].b : b[1].a, (e & 1) ? b[2].b : b[2].a};
+      cc = add<64>(CE(e), mul_z<64>(diff<64>(a3(0, 0, 0), CE(e)), cav, F));
+    } else {
+      cc = select_with<64>(K, op, 4, (uint32_t)e, n, CE(e), a3(0, 0, 0), cav);
+    }
     for (int ch = 0; ch < 2; ++ch) st3s(a.cst_nxt, cs * C3, (uint64_t)(2 * n + ch) * C3 + e, cc);
   }
 }
@@ -1100,7 +1277,7 @@ inline uint64_t div_tape_level_off(int level, int nf, int TB) {  // W2 offset of
 }
 
 struct Layout {
-  uint64_t xin, yin, fin, tout, fout, cols, la, cols8, leaf, midx, divtape, divtable, posttape, posttable, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
+  uint64_t xin, yin, fin, tout, fout, cols, la, cols8, leaf, midx, divtape, divtable, posttape, posttable, nodetape, nodetable, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
 };
 
 Layout layout(const gt_train_cfg& c, bool host_io = false) {
@@ -1127,6 +1304,8 @@ Layout layout(const gt_train_cfg& c, bool host_io = false) {
   L.midx = take(3 * N);
   L.divtape = take(2 * div_tape_words(c));
   L.posttape = take(2 * post_tape_words(c));
+  L.nodetape = take(c.heuristic == 0 ? 2 * ((1ull << c.depth) - 1) * (uint64_t)node_tape_plan(c.nf).total : 0);
+  L.nodetable = take(c.heuristic == 0 ? (uint64_t)node_tape_plan(c.nf).total : 0);
   L.posttable = take(c.heuristic == 0 ? (uint64_t)post_tape_blocks_w(c.score_width, c.nf) : 0);
   {
     bool ok = false;
@@ -1165,7 +1344,7 @@ int post_smem_bytes(const NodeArgs& na) {
 template <int SL>
 int launch_node_hc(const NodeArgs& na, cudaStream_t s, bool fuse_post) {
   const int cols = 2 * na.nf;
-  const int pre_smem = (int)sizeof(uint64_t) * 9 * cols;
+  const int pre_smem = (int)sizeof(uint64_t) * ((9 * cols + 1) & ~1) + (int)sizeof(W2) * node_tape_plan(na.nf).spl;
   const unsigned gy = (na.last || na.co_out) ? 1u : (unsigned)(1 + na.nf);
   k_hc_pre<SL><<<dim3(na.n_h, gy), 64, pre_smem, s>>>(na);
   GT_LAUNCH_CHECK("k_hc_pre");
@@ -1723,6 +1902,17 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
       P.count_launch();
       P.count_launch();
     }
+    {  // node tapes of every level (prologue chains, replace, split, labels)
+      const NodeTape NT = node_tape_plan(c.nf);
+      const uint64_t nwords = ((1ull << c.depth) - 1) * (uint64_t)NT.total;
+      uint64_t* ntab = ws + L.nodetable;
+      k_node_table<<<(NT.total + 127) / 128, 128, 0, ts>>>(ntab, c.nf);
+      k_node_tape<<<(unsigned)((nwords + 255) / 256), 256, 0, ts>>>(reinterpret_cast<W2*>(ws + L.nodetape), ntab,
+                                                                    (uint32_t)nwords, NT.total, K);
+      GT_LAUNCH_CHECK("k_node_tape");
+      P.count_launch();
+      P.count_launch();
+    }
     tape_forked = ts != s;
     P.count_launch();
     GT_LAUNCH_CHECK("k_div_tape");
@@ -1851,6 +2041,9 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
     na.hc = hc;
     na.dv = ws + L.dv;
     na.co_out = tee ? ws + L.co : nullptr;
+    na.nodetape = (!tee && tape_words) ? reinterpret_cast<const W2*>(ws + L.nodetape) +
+                                           ((1ull << level) - 1) * (uint64_t)node_tape_plan(c.nf).total
+                                     : nullptr;
     na.posttape = post_tape_words(c) ? reinterpret_cast<const W2*>(ws + L.posttape) +
                                            ((1ull << level) - 1) * (uint64_t)post_tape_blocks_w(c.score_width, c.nf)
                                      : nullptr;
@@ -1915,6 +2108,7 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
     }
     fa.slots = slots;
     fa.ts = na.ts;
+    fa.nodetape = na.nodetape;
     fa.n_h = n_h;
     fa.nf = c.nf;
     fa.level = level;
