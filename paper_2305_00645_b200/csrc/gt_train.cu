@@ -417,6 +417,7 @@ struct NodeArgs {
   const W2* divtape;          // precomputed division blocks of this level (or null: draw live)
   const W2* posttape;         // precomputed epilogue blocks of this level (or null: draw live)
   const W2* nodetape;         // precomputed node-chain blocks of this level's nodes (or null)
+  const W2* feattape;         // precomputed prologue feature blocks of this level (or null)
   int n_h, nf, level, last, shift, tau, ts;
   DivParams d;
   Keys K;
@@ -553,44 +554,85 @@ __device__ __forceinline__ uint64_t co_cell(const NodeArgs& a, int c, int n, int
 //     of the feature (truncations, products, eq, b2a: the live schedule's
 //     blocks) into shared memory in parallel, so the serial gadget chain
 //     only does arithmetic.
+// The Philox blocks of feature fi of node n in the prologue, in consumption
+// order: six truncations (cells q = r*2 + j <-> e = r*cols + 2fi + j, sub 7),
+// eight products (sub 10; p < 6: cell p squared, p = 6 + j: a * tot), two
+// (eqz sub 11, b2a sub 12) for the Q == 0 fix of columns 2fi, 2fi+1.
+constexpr int FEAT_BLOCKS = 6 * TruncRand<64>::BLOCKS + 8 * 3 + 2 * 7;
+__device__ __forceinline__ void feat_block(int b, int fi, int nf, uint32_t n, int* key, uint32_t* sub, uint32_t* pidx,
+                                           uint64_t* lane) {
+  constexpr int TB = TruncRand<64>::BLOCKS;
+  const int cols = 2 * nf, C3 = 3 * cols;
+  auto cell_e = [&](int q) { return (q >> 1) * cols + 2 * fi + (q & 1); };
+  auto prod_e = [&](int p) { return p < 6 ? cell_e(p) : C3 + 2 * fi + (p - 6); };
+  *key = -1;
+  if (b < 6 * TB) {
+    trunc_block_id<64>(b % TB, 7, key, sub, pidx);
+    *lane = (uint64_t)n * C3 + cell_e(b / TB);
+  } else if (b < 6 * TB + 24) {
+    const int t = b - 6 * TB;
+    *key = t % 3, *sub = 10, *pidx = 0;
+    *lane = (uint64_t)n * 4 * cols + prod_e(t / 3);
+  } else {
+    const int t = b - 6 * TB - 24, j = t / 7, w = t % 7;
+    *lane = (uint64_t)n * cols + 2 * fi + j;
+    if (w < 2) *key = -1, *sub = 11, *pidx = w;            // eqz dealer (r, Rb0) (Rb1, -)
+    else if (w < 5) *key = w - 2, *sub = 11, *pidx = 0;    // eqz zero words
+    else *key = -1, *sub = 12, *pidx = w - 5;              // b2a dealer (A0, A1) (bits, -)
+  }
+}
+// every heuristic level's feature tapes: [global node][feature][FEAT_BLOCKS]
+__global__ void __launch_bounds__(256) k_feat_tape(W2* tape, uint32_t total, int nf, Keys K) {
+  __shared__ Keys ks;
+  for (int i = threadIdx.x; i < (int)(sizeof(Keys) / 4); i += blockDim.x)
+    reinterpret_cast<uint32_t*>(&ks)[i] = reinterpret_cast<const uint32_t*>(&K)[i];
+  __syncthreads();
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  const uint32_t per = (uint32_t)nf * FEAT_BLOCKS;
+  const uint32_t gn = e / per, r = e - gn * per, fi = r / FEAT_BLOCKS, b = r - fi * FEAT_BLOCKS;
+  const int level = 31 - __clz(gn + 1);
+  const uint32_t n = gn - ((1u << level) - 1);
+  int key;
+  uint32_t sub, pidx;
+  uint64_t lane;
+  feat_block((int)b, (int)fi, nf, n, &key, &sub, &pidx, &lane);
+  tape[e] = word2(key < 0 ? ks.dealer : ks.pair[key], op_id(level, SITE_HC), sub, pidx, lane);
+}
+
 template <int SL>
 __device__ __forceinline__ void hc_pre_feature(const NodeArgs& a, int n, int fi, const Keys& K) {
   constexpr uint64_t MS = Ring<SL>::M;
   constexpr int TB = TruncRand<64>::BLOCKS;
-  constexpr int NB = 6 * TB + 8 * 3 + 2 * 7;
-  __shared__ W2 tape[NB];
+  constexpr int NB = FEAT_BLOCKS;
+  __shared__ __align__(128) W2 tape[NB];
+  __shared__ __align__(8) uint64_t fbar;
   __shared__ uint64_t c32[3][6], pr[3][8];
   const int wl = threadIdx.x;
   const int nf = a.nf, cols = 2 * nf, C3 = 3 * cols;
   const uint64_t hs = (uint64_t)a.n_h, lanes = hs * cols;
   const uint32_t opH = op_id(a.level, SITE_HC);
-  // cell q = r * 2 + j  <->  e = r * cols + 2 fi + j; product p < 6: cell p squared,
-  // p = 6 + j: a (row 0, column 2fi+j) times tot (row 0, columns 2fi, 2fi+1)
   auto cell_e = [&](int q) { return (q >> 1) * cols + 2 * fi + (q & 1); };
-  auto prod_e = [&](int p) { return p < 6 ? cell_e(p) : C3 + 2 * fi + (p - 6); };
-  for (int b = wl; b < NB; b += 32) {
-    int key = -1;
-    uint32_t sub, pidx;
-    uint64_t lane;
-    if (b < 6 * TB) {
-      const int q = b / TB;
-      trunc_block_id<64>(b % TB, 7, &key, &sub, &pidx);
-      lane = (uint64_t)n * C3 + cell_e(q);
-      if (!a.shift) continue;
-    } else if (b < 6 * TB + 24) {
-      const int t = b - 6 * TB;
-      key = t % 3, sub = 10, pidx = 0;
-      lane = (uint64_t)n * 4 * cols + prod_e(t / 3);
-    } else {
-      const int t = b - 6 * TB - 24, j = t / 7, w = t % 7;
-      lane = (uint64_t)n * cols + 2 * fi + j;
-      if (w < 2) key = -1, sub = 11, pidx = w;            // eqz dealer (r, Rb0) (Rb1, -)
-      else if (w < 5) key = w - 2, sub = 11, pidx = 0;    // eqz zero words
-      else key = -1, sub = 12, pidx = w - 5;              // b2a dealer (A0, A1) (bits, -)
+  if (a.feattape) {  // precomputed: one bulk copy
+    if (wl == 0) {
+      mbar_init(&fbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&fbar, (uint32_t)(NB * sizeof(W2)));
+      bulk_g2s(tape, a.feattape + ((uint64_t)n * nf + fi) * NB, (uint32_t)(NB * sizeof(W2)), &fbar);
     }
-    tape[b] = word2(key < 0 ? K.dealer : K.pair[key], opH, sub, pidx, lane);
+    __syncwarp();
+    mbar_wait(&fbar, 0);
+  } else {
+    for (int b = wl; b < NB; b += 32) {
+      if (b < 6 * TB && !a.shift) continue;
+      int key;
+      uint32_t sub, pidx;
+      uint64_t lane;
+      feat_block(b, fi, nf, (uint32_t)n, &key, &sub, &pidx, &lane);
+      tape[b] = word2(key < 0 ? K.dealer : K.pair[key], opH, sub, pidx, lane);
+    }
+    __syncwarp();
   }
-  __syncwarp();
   // counters: truncate by the public shift, ring_down      train.py:366-370
   if (wl < 6) {
     const int e = cell_e(wl);
@@ -1266,6 +1308,13 @@ uint64_t div_tape_words(const gt_train_cfg& c) {
   const uint64_t w = lanes * (uint64_t)TB;
   return w * 16 > (256ull << 20) ? 0 : w;
 }
+// Prologue feature tapes of every heuristic level (W2 units); 0 when over 256 MB
+uint64_t feat_tape_words(const gt_train_cfg& c) {
+  static const bool off = getenv("GT_NO_FEAT_TAPE") != nullptr;  // A/B experiments
+  if (off || c.heuristic != 0 || c.depth < 2) return 0;
+  const uint64_t w = ((1ull << (c.depth - 1)) - 1) * (uint64_t)c.nf * FEAT_BLOCKS;
+  return w * 16 > (256ull << 20) ? 0 : w;
+}
 // Epilogue tapes of every heuristic level (W2 units); 0 when over 256 MB
 uint64_t post_tape_words(const gt_train_cfg& c) {
   if (c.heuristic != 0 || c.depth < 2) return 0;
@@ -1277,7 +1326,7 @@ inline uint64_t div_tape_level_off(int level, int nf, int TB) {  // W2 offset of
 }
 
 struct Layout {
-  uint64_t xin, yin, fin, tout, fout, cols, la, cols8, leaf, midx, divtape, divtable, posttape, posttable, nodetape, nodetable, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
+  uint64_t xin, yin, fin, tout, fout, cols, la, cols8, leaf, midx, divtape, divtable, posttape, posttable, nodetape, nodetable, feattape, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
 };
 
 Layout layout(const gt_train_cfg& c, bool host_io = false) {
@@ -1306,6 +1355,7 @@ Layout layout(const gt_train_cfg& c, bool host_io = false) {
   L.posttape = take(2 * post_tape_words(c));
   L.nodetape = take(c.heuristic == 0 ? 2 * ((1ull << c.depth) - 1) * (uint64_t)node_tape_plan(c.nf).total : 0);
   L.nodetable = take(c.heuristic == 0 ? (uint64_t)node_tape_plan(c.nf).total : 0);
+  L.feattape = take(2 * feat_tape_words(c));
   L.posttable = take(c.heuristic == 0 ? (uint64_t)post_tape_blocks_w(c.score_width, c.nf) : 0);
   {
     bool ok = false;
@@ -1902,6 +1952,13 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
       P.count_launch();
       P.count_launch();
     }
+    if (feat_tape_words(c)) {  // prologue feature tapes
+      const uint64_t fw = feat_tape_words(c);
+      k_feat_tape<<<(unsigned)((fw + 255) / 256), 256, 0, ts>>>(reinterpret_cast<W2*>(ws + L.feattape), (uint32_t)fw,
+                                                                c.nf, K);
+      GT_LAUNCH_CHECK("k_feat_tape");
+      P.count_launch();
+    }
     {  // node tapes of every level (prologue chains, replace, split, labels)
       const NodeTape NT = node_tape_plan(c.nf);
       const uint64_t nwords = ((1ull << c.depth) - 1) * (uint64_t)NT.total;
@@ -2041,6 +2098,9 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
     na.hc = hc;
     na.dv = ws + L.dv;
     na.co_out = tee ? ws + L.co : nullptr;
+    na.feattape = (!tee && tape_words && feat_tape_words(c))
+                      ? reinterpret_cast<const W2*>(ws + L.feattape) + ((1ull << level) - 1) * (uint64_t)c.nf * FEAT_BLOCKS
+                      : nullptr;
     na.nodetape = (!tee && tape_words) ? reinterpret_cast<const W2*>(ws + L.nodetape) +
                                            ((1ull << level) - 1) * (uint64_t)node_tape_plan(c.nf).total
                                      : nullptr;
