@@ -127,79 +127,114 @@ struct Prep8Args {
   uint32_t op_prods;
 };
 __global__ void __launch_bounds__(256) k_prep8(Prep8Args a) {
-  // one CTA per 64-sample half block (smem 3 x 64 x W words <= 198 KB at nf = 64)
+  // one CTA per 64-sample half block; shared memory (<= 198 KB at nf = 64):
+  // xs[3][HS][nf] features, ps[3][HS][nf] prods, ys[3][HS] labels
   constexpr int HS = TC_KB / 2;
-  extern __shared__ __align__(16) uint64_t v[];  // [3][HS][W] (x | prods | y)
+  extern __shared__ __align__(16) uint64_t v[];
+  __shared__ __align__(8) uint64_t bar;
   const int nf = a.nf, W = a.W, tid = threadIdx.x;
+  uint64_t* xs = v;
+  uint64_t* ps = v + 3 * HS * nf;
+  uint64_t* ys = v + 6 * HS * nf;
   const uint64_t hb = a.hb0 + blockIdx.x;
   const uint64_t kb = hb >> 1;
   const int half = (int)(hb & 1);
   const uint64_t nfx = a.N * (uint64_t)nf;
   const uint64_t s0 = kb * TC_KB + half * HS;
-  for (int e = tid; e < HS * nf; e += blockDim.x) {
-    const int sl = e / nf, f = e % nf;
-    const uint64_t gs = s0 + sl;
+  const int cnt = (int)min((uint64_t)HS, a.N - s0);
+  // the block's feature rows and labels are contiguous runs: bulk copies when
+  // every run is 16-byte aligned, plain loads otherwise
+  const bool bulk = ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.Y)) & 15) == 0 &&
+                    ((nfx | a.N | (uint64_t)cnt * nf | (uint64_t)cnt) & 1) == 0;
+  if (bulk) {
+    if (tid == 0) {
+      mbar_init(&bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      const uint32_t xb = (uint32_t)(cnt * nf * 8), yb = (uint32_t)(cnt * 8);
+      mbar_expect_tx(&bar, 3 * (xb + yb));
 #pragma unroll
-    for (int c = 0; c < 3; ++c) v[(c * HS + sl) * W + f] = gs < a.N ? __ldg(a.X + c * nfx + gs * nf + f) : 0ull;
-  }
-  for (int sl = tid; sl < HS; sl += blockDim.x) {
-    const uint64_t gs = s0 + sl;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) v[(c * HS + sl) * W + 2 * nf] = gs < a.N ? __ldg(a.Y + c * a.N + gs) : 0ull;
-  }
-  __syncthreads();
-  for (int e = tid; e < HS * nf; e += blockDim.x) {
-    const int sl = e / nf, f = e % nf;
-    const uint64_t gs = s0 + sl;
-    A3 z = a3(0, 0, 0);
-    if (gs < a.N) {
-      auto at = [&](int c, int w) { return v[(c * HS + sl) * W + w]; };
-      z = mul<64>(a.K, a.op_prods, 0, (uint32_t)f, a.base + gs, a3(at(0, f), at(1, f), at(2, f)),
-                  a3(at(0, 2 * nf), at(1, 2 * nf), at(2, 2 * nf)));
+      for (int c = 0; c < 3; ++c) {
+        bulk_g2s(xs + c * HS * nf, a.X + c * nfx + s0 * nf, xb, &bar);
+        bulk_g2s(ys + c * HS, a.Y + c * a.N + s0, yb, &bar);
+      }
     }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+  } else {
+    for (int e = tid; e < cnt * nf; e += blockDim.x) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) v[(c * HS + sl) * W + nf + f] = z.v[c];
+      for (int c = 0; c < 3; ++c) xs[c * HS * nf + e] = __ldg(a.X + c * nfx + s0 * nf + e);
+    }
+    for (int sl = tid; sl < cnt; sl += blockDim.x) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) ys[c * HS + sl] = __ldg(a.Y + c * a.N + s0 + sl);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < cnt * nf; e += blockDim.x) {
+    const int sl = e / nf, f = e - sl * nf;
+    const A3 z = mul<64>(a.K, a.op_prods, 0, (uint32_t)f, a.base + s0 + sl,
+                         a3(xs[e], xs[HS * nf + e], xs[2 * HS * nf + e]),
+                         a3(ys[sl], ys[HS + sl], ys[2 * HS + sl]));
+#pragma unroll
+    for (int c = 0; c < 3; ++c) ps[c * HS * nf + e] = z.v[c];
   }
   __syncthreads();
-  // planes: item = (component, 16-sample chunk, column); 8 limb rows of 16
-  // bytes for each of U and X
-  const int WG = a.nbn * a.cpb;
+  // planes: item = (component, 16-sample chunk, column, 4-sample quad); the
+  // quad's u = x_c + x_{c+1} and x_c words are byte-transposed in registers
+  // (4x4 byte_perm transposes) into one 32-bit word of each of the 8 limb
+  // rows of both terms; the four quads of a row are adjacent threads
   const uint64_t HB = (uint64_t)8 * a.cpb * HS;
-  for (int it = tid; it < 3 * 4 * WG; it += blockDim.x) {
-    const int w = it % WG, kc = (it / WG) % 4, c = it / (4 * WG);
-    const int nb = w / a.cpb, g = w % a.cpb;
-    uint32_t pk[2][8][4];
+  const int items = 3 * 4 * a.nbn * a.cpb * 4;
+  for (int it = tid; it < items; it += blockDim.x) {
+    const int quad = it & 3;
+    int r = it >> 2;
+    const int g = r % a.cpb;
+    r /= a.cpb;
+    const int kc = r & 3;
+    r >>= 2;
+    const int nb = r % a.nbn, c = r / a.nbn, c1 = (c + 1) % 3;
+    const int w = nb * a.cpb + g;
+    const uint64_t *p0 = nullptr, *p1 = nullptr;
+    int stride = nf;
+    if (w < nf) {
+      p0 = xs + c * HS * nf + w, p1 = xs + c1 * HS * nf + w;
+    } else if (w < 2 * nf) {
+      p0 = ps + c * HS * nf + (w - nf), p1 = ps + c1 * HS * nf + (w - nf);
+    } else if (w == 2 * nf) {
+      p0 = ys + c * HS, p1 = ys + c1 * HS, stride = 1;
+    }
+    uint32_t wx[2][4], wu[2][4];
 #pragma unroll
-    for (int t = 0; t < 2; ++t)
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) pk[t][q][k] = 0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int sl = kc * 16 + i;
+    for (int i = 0; i < 4; ++i) {
+      const int sl = kc * 16 + quad * 4 + i;
       uint64_t x = 0, u = 0;
-      if (s0 + sl < a.N) {
-        if (w < W) {
-          x = v[(c * HS + sl) * W + w];
-          u = x + v[(((c + 1) % 3) * HS + sl) * W + w];
+      if (sl < cnt) {
+        if (p0) {
+          x = p0[sl * stride];
+          u = x + p1[sl * stride];
         } else if (w == W) {
           u = 1;  // mask column: s_mask += la (train.py:334)
         }
       }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        pk[0][q][i >> 2] |= (uint32_t)((u >> (8 * q)) & 0xffu) << (8 * (i & 3));
-        pk[1][q][i >> 2] |= (uint32_t)((x >> (8 * q)) & 0xffu) << (8 * (i & 3));
-      }
+      wx[0][i] = (uint32_t)x, wx[1][i] = (uint32_t)(x >> 32);
+      wu[0][i] = (uint32_t)u, wu[1][i] = (uint32_t)(u >> 32);
     }
+    uint8_t* dst = a.B8 + ((((uint64_t)c * a.nbn + nb) * a.nkb + kb) * 2 + half) * 2 * HB +
+                   ((uint64_t)kc * a.cpb + g) * 128 + quad * 4;
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
-      uint8_t* dst = a.B8 + ((((uint64_t)c * a.nbn + nb) * a.nkb + kb) * 2 + half) * 2 * HB + t * HB +
-                     ((uint64_t)kc * a.cpb + g) * 128;
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        *reinterpret_cast<uint4*>(dst + q * 16) = make_uint4(pk[t][q][0], pk[t][q][1], pk[t][q][2], pk[t][q][3]);
+      for (int hh = 0; hh < 2; ++hh) {
+        const uint32_t* q4 = t == 0 ? wu[hh] : wx[hh];
+        const uint32_t t0 = __byte_perm(q4[0], q4[1], 0x5140), t1 = __byte_perm(q4[0], q4[1], 0x7362);
+        const uint32_t t2 = __byte_perm(q4[2], q4[3], 0x5140), t3 = __byte_perm(q4[2], q4[3], 0x7362);
+        uint8_t* d = dst + t * HB + hh * 4 * 16;
+        *reinterpret_cast<uint32_t*>(d) = __byte_perm(t0, t2, 0x5410);
+        *reinterpret_cast<uint32_t*>(d + 16) = __byte_perm(t0, t2, 0x7632);
+        *reinterpret_cast<uint32_t*>(d + 32) = __byte_perm(t1, t3, 0x5410);
+        *reinterpret_cast<uint32_t*>(d + 48) = __byte_perm(t1, t3, 0x7632);
+      }
     }
   }
 }
