@@ -79,4 +79,13 @@ inline DivParams div_params(int width, int tau, bool* ok) {
     if (_e != cudaSuccess) return ::gt::fail_cuda(_e, where);  \
   } while (0)
 
+// Programmatic dependent launch: the level-chain kernels are launched with
+// programmatic stream serialization (launch_chain), so a kernel's CTAs start
+// -- and issue their precomputed-tape bulk copies -- while its predecessor's
+// last wave drains.  pdl_wait() blocks until the predecessor grid has
+// completed and its writes are visible (a no-op for normal launches): every
+// read of a predecessor's output and every global write comes after it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 }  // namespace gt

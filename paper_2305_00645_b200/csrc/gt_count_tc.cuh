@@ -257,6 +257,8 @@ struct Lanes8Args {
 __global__ void __launch_bounds__(256) k_count_lanes8(Lanes8Args a) {
   __shared__ uint64_t leaf[3][16];
   const int kb = blockIdx.x, mt = blockIdx.y, tid = threadIdx.x;
+  pdl_wait();
+  pdl_trigger();
   // la8[mt][kbc][half 2][c 3][kc 4][g 16][p 8][16]: the three components of
   // a 64-sample half block are one contiguous 24 KB run (one bulk copy for
   // the contraction)
@@ -401,6 +403,7 @@ __global__ void __launch_bounds__(128, 1) k_count_mma(MmaArgs a) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_slot;
+  pdl_wait();  // the lane planes of the lane kernel
 
   if (tid == 0 && T > 0) {
     // idesc: S32 accumulator [4,6) = 2, A/B unsigned 8-bit, K-major, N>>3 at 17, M>>4 at 24
@@ -446,8 +449,9 @@ __global__ void __launch_bounds__(128, 1) k_count_mma(MmaArgs a) {
     umma_commit(&done);
   }
   __syncwarp();
+  if (T > 0) mbar_wait(&done, 0);
+  pdl_trigger();  // the epilogue overlaps the next kernel's launch
   if (T > 0) {
-    mbar_wait(&done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int r = warp * 32 + lane, nn = r >> 3, p = r & 7;
     const int n = mt * 16 + nn;

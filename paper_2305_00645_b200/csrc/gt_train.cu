@@ -90,8 +90,14 @@ __global__ void k_prods(const uint64_t* X, const uint64_t* Y, uint64_t* cols, ui
 
 template <int G>
 __global__ void k_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint64_t slots, int m, int nf,
-                            uint64_t N, uint64_t base, Keys K, uint32_t op_oaa, uint32_t op_row) {
+                            uint64_t N, uint64_t base, Keys K, uint32_t op_oaa, uint32_t op_row, uint64_t* Sz,
+                            uint64_t swords) {
   extern __shared__ uint64_t tab[];  // [3][m] level h-1 payload table
+  pdl_wait();
+  pdl_trigger();
+  // zero this level's count sums (the previous level's heuristic has read them)
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < swords; i += (uint64_t)gridDim.x * blockDim.x)
+    Sz[i] = 0;
   for (int i = threadIdx.x; i < 3 * m; i += blockDim.x) tab[i] = T[(uint64_t)(i / m) * slots + (m - 1) + (i % m)];
   __syncthreads();
   const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -385,13 +391,17 @@ namespace {
 
 // Phase timestamps of the heuristic kernels (diagnostics: GT_HC_TIMING=1
 // makes node 0's thread 0 record %globaltimer at each phase boundary).
-__device__ unsigned long long g_hc_ts[64];
-__device__ __forceinline__ void hc_ts(int slot, bool on) {
-  if (!on || blockIdx.x != 0 || threadIdx.x != 0) return;
+// Slots 0..63: post/finish (8 per level); 64..127: pre/div (8 per level:
+// 0 control start, 1 control tapes in, 2 control end, 3 feature-warp start,
+// 4 feature tape in, 5 feature end, 6 div start, 7 div end).
+__device__ unsigned long long g_hc_ts[128];
+__device__ __forceinline__ void hc_ts_at(int slot, bool on) {
+  if (!on) return;
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   g_hc_ts[slot] = t;
 }
+__device__ __forceinline__ void hc_ts(int slot, bool on) { hc_ts_at(slot, on && blockIdx.x == 0 && threadIdx.x == 0); }
 
 // The heuristic kernels draw Philox blocks along long dependent chains and,
 // in warp-cooperative draws, with lane-dependent keys: stage the expanded
@@ -613,6 +623,8 @@ __device__ __forceinline__ void hc_pre_feature(const NodeArgs& a, int n, int fi,
   const uint64_t hs = (uint64_t)a.n_h, lanes = hs * cols;
   const uint32_t opH = op_id(a.level, SITE_HC);
   auto cell_e = [&](int q) { return (q >> 1) * cols + 2 * fi + (q & 1); };
+  const bool tsw = a.ts && n == 0 && fi == 0 && wl == 0;
+  hc_ts_at(64 + 8 * a.level + 3, tsw);
   if (a.feattape) {  // precomputed: one bulk copy
     if (wl == 0) {
       mbar_init(&fbar, 1);
@@ -621,8 +633,12 @@ __device__ __forceinline__ void hc_pre_feature(const NodeArgs& a, int n, int fi,
       bulk_g2s(tape, a.feattape + ((uint64_t)n * nf + fi) * NB, (uint32_t)(NB * sizeof(W2)), &fbar);
     }
     __syncwarp();
+    pdl_wait();
+    pdl_trigger();
     mbar_wait(&fbar, 0);
   } else {
+    pdl_wait();
+    pdl_trigger();
     for (int b = wl; b < NB; b += 32) {
       if (b < 6 * TB && !a.shift) continue;
       int key;
@@ -633,6 +649,7 @@ __device__ __forceinline__ void hc_pre_feature(const NodeArgs& a, int n, int fi,
     }
     __syncwarp();
   }
+  hc_ts_at(64 + 8 * a.level + 4, tsw);
   // counters: truncate by the public shift, ring_down      train.py:366-370
   if (wl < 6) {
     const int e = cell_e(wl);
@@ -673,6 +690,7 @@ __device__ __forceinline__ void hc_pre_feature(const NodeArgs& a, int n, int fi,
     st3s(a.dv, lanes, lane, p);
     st3s(a.dv + 3 * lanes, lanes, lane, qsv);
   }
+  hc_ts_at(64 + 8 * a.level + 5, tsw);
 }
 
 template <int SL>
@@ -693,6 +711,8 @@ __global__ void __launch_bounds__(64) k_hc_pre(NodeArgs a) {
   uint64_t* co = sm;  // [3][3*cols] c_orig
   const uint32_t opH = op_id(a.level, SITE_HC), opR = op_id(a.level, SITE_REPLACE);
   const NodeTape NT = node_tape_plan(nf);
+  const bool tsc = a.ts && n == 0 && tid == 0;
+  hc_ts_at(64 + 8 * a.level + 0, tsc);
   __shared__ __align__(8) uint64_t nbar;
   W2* ntb = reinterpret_cast<W2*>(co + ((3 * C3 + 1) & ~1));
   if (a.nodetape && tid == 0) {  // the prologue + replace segments of this node's tape
@@ -701,6 +721,8 @@ __global__ void __launch_bounds__(64) k_hc_pre(NodeArgs a) {
     mbar_expect_tx(&nbar, (uint32_t)(NT.spl * sizeof(W2)));
     bulk_g2s(ntb, a.nodetape + (uint64_t)n * NT.total, (uint32_t)(NT.spl * sizeof(W2)), &nbar);
   }
+  pdl_wait();
+  pdl_trigger();
   for (int e = tid; e < 3 * C3; e += blockDim.x) co[e] = co_cell(a, e / C3, n, e % C3);
   __syncthreads();
   const W2* nt = nullptr;
@@ -708,6 +730,7 @@ __global__ void __launch_bounds__(64) k_hc_pre(NodeArgs a) {
     mbar_wait(&nbar, 0);
     nt = ntb;
   }
+  hc_ts_at(64 + 8 * a.level + 1, tsc);
   auto CO = [&](int e) { return a3(co[e], co[C3 + e], co[2 * C3 + e]); };
   if (a.co_out)  // heuristic "tee": hand the counters to the trusted helper
     for (int e = tid; e < C3; e += blockDim.x) st3s(a.co_out, hs * C3, (uint64_t)n * C3 + e, CO(e));
@@ -764,6 +787,7 @@ __global__ void __launch_bounds__(64) k_hc_pre(NodeArgs a) {
           a.hc[(0 * 3 + c) * hs + n] = ss.v[c] & 1ull;
           a.hc[(2 * 3 + c) * hs + n] = nfv.v[c];
         }
+        hc_ts_at(64 + 8 * a.level + 2, tsc);
       }
     }
     return;
@@ -811,7 +835,7 @@ __global__ void __launch_bounds__(32 * DIV_WARPS) k_hc_div(NodeArgs a) {
   const uint64_t cols = 2 * (uint64_t)a.nf, lanes = (uint64_t)a.n_h * cols;
   const uint64_t li = (uint64_t)blockIdx.x * wpc + warp;
   if (li >= lanes) return;  // whole warp exits together
-  const A3 p = ld3s(a.dv, lanes, li), q = ld3s(a.dv + 3 * lanes, lanes, li);
+  hc_ts_at(64 + 8 * a.level + 6, a.ts && li == 0 && threadIdx.x == 0);
   // terms = division(P, qsafe)                              train.py:382
   A3 t;
   if (a.divtape) {
@@ -827,12 +851,19 @@ __global__ void __launch_bounds__(32 * DIV_WARPS) k_hc_div(NodeArgs a) {
       bulk_g2s(ts, a.divtape + li * (uint64_t)TB, (uint32_t)(TB * sizeof(W2)), &bar[warp]);
     }
     __syncwarp();
+    pdl_wait();
+    pdl_trigger();
+    const A3 p = ld3s(a.dv, lanes, li), q = ld3s(a.dv + 3 * lanes, lanes, li);
     mbar_wait(&bar[warp], 0);
     t = division_warp_staged<SL>(ts, p, q, a.d);
   } else {
+    pdl_wait();
+    pdl_trigger();
+    const A3 p = ld3s(a.dv, lanes, li), q = ld3s(a.dv + 3 * lanes, lanes, li);
     t = division_warp<SL>(a.K, op_id(a.level, SITE_HC), 13, li, p, q, a.d, tape_sm + (size_t)warp * division_tape_blocks<SL>(a.d));
   }
   if ((threadIdx.x & 31) == 0) st3s(a.dv + 6 * lanes, lanes, li, t);
+  hc_ts_at(64 + 8 * a.level + 7, a.ts && li == 0 && threadIdx.x == 0);
 }
 
 // All division blocks of every heuristic level (see DivTape).  A per-lane
@@ -1006,13 +1037,13 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n) {
   const Keys& Ks = keys_smem(a.K, ks);  // lane-dependent keys of the tournament tapes
   const Keys& K = a.K;                  // uniform-key gadgets: constant-bank operands
   const uint32_t opH = op_id(a.level, SITE_HC);
-  const B3 gam = ldb3s(a.gam, hs, n);
   const uint64_t* terms = a.dv + 6 * lanes;
   auto TM = [&](int k) { return ld3s(terms, lanes, (uint64_t)n * cols + k); };
-  // staged epilogue tape (see k_post_table): one bulk copy of this node's run
+  // staged epilogue tape (see k_post_table): one bulk copy of this node's run,
+  // issued before the wait for the division kernel
   const W2* pt = nullptr;
+  __shared__ __align__(8) uint64_t pbar;
   if (a.posttape) {
-    __shared__ __align__(8) uint64_t pbar;
     W2* pts = reinterpret_cast<W2*>(sm + post_scratch_words(nf));
     const int E = post_tape_blocks<SL>(nf);
     if (tid == 0) {
@@ -1021,9 +1052,14 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n) {
       mbar_expect_tx(&pbar, (uint32_t)(E * sizeof(W2)));
       bulk_g2s(pts, a.posttape + (uint64_t)n * E, (uint32_t)(E * sizeof(W2)), &pbar);
     }
+    pt = pts;
+  }
+  pdl_wait();
+  pdl_trigger();
+  const B3 gam = ldb3s(a.gam, hs, n);
+  if (pt) {
     __syncthreads();
     mbar_wait(&pbar, 0);
-    pt = pts;
   }
   // scores + masked argmin (tournament)     train.py:383-385, gadgets.py:366-401
   hc_ts(0 + 8 * a.level, a.ts);
@@ -1233,7 +1269,11 @@ __device__ __forceinline__ void node_finish_body(const FinishArgs& a, int n) {
   }
 }
 
-__global__ void __launch_bounds__(128) k_node_finish(FinishArgs a) { node_finish_body(a, blockIdx.x); }
+__global__ void __launch_bounds__(128) k_node_finish(FinishArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  node_finish_body(a, blockIdx.x);
+}
 
 // scores / argmin / budget clear, then split, in one launch per level (fixed
 // policy, mpc heuristic): the node's CTA continues from sd to its children
@@ -1386,6 +1426,31 @@ Layout layout(const gt_train_cfg& c, bool host_io = false) {
   return L;
 }
 
+// Launch of a level-chain kernel with programmatic stream serialization (see
+// pdl_wait); GT_NO_PDL=1 launches them normally (A/B experiments).
+template <typename... KArgs, typename... Args>
+int launch_chain(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                 const cudaLaunchAttribute* extra, Args... args) {
+  static const bool pdl = getenv("GT_NO_PDL") == nullptr;
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (extra) at[na++] = *extra;
+  if (pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  lc.attrs = at;
+  lc.numAttrs = (unsigned)na;
+  GT_CUDA_CHECK(cudaLaunchKernelEx(&lc, kern, args...));
+  return GT_OK;
+}
+
 template <int SL>
 int post_smem_bytes(const NodeArgs& na) {
   return (int)sizeof(uint64_t) * post_scratch_words(na.nf) + (int)sizeof(W2) * post_tape_blocks<SL>(na.nf);
@@ -1396,7 +1461,8 @@ int launch_node_hc(const NodeArgs& na, cudaStream_t s, bool fuse_post) {
   const int cols = 2 * na.nf;
   const int pre_smem = (int)sizeof(uint64_t) * ((9 * cols + 1) & ~1) + (int)sizeof(W2) * node_tape_plan(na.nf).spl;
   const unsigned gy = (na.last || na.co_out) ? 1u : (unsigned)(1 + na.nf);
-  k_hc_pre<SL><<<dim3(na.n_h, gy), 64, pre_smem, s>>>(na);
+  int rc = launch_chain(k_hc_pre<SL>, dim3(na.n_h, gy), dim3(64), (size_t)pre_smem, s, nullptr, na);
+  if (rc) return rc;
   GT_LAUNCH_CHECK("k_hc_pre");
   if (na.last || na.co_out) return GT_OK;
   const uint64_t lanes = (uint64_t)na.n_h * cols;
@@ -1405,7 +1471,9 @@ int launch_node_hc(const NodeArgs& na, cudaStream_t s, bool fuse_post) {
   const int div_smem = per_warp * wpc;
   if (div_smem > 48 * 1024)
     GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_div<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, div_smem));
-  k_hc_div<SL><<<(unsigned)((lanes + wpc - 1) / wpc), 32 * wpc, div_smem, s>>>(na);
+  rc = launch_chain(k_hc_div<SL>, dim3((unsigned)((lanes + wpc - 1) / wpc)), dim3(32 * wpc), (size_t)div_smem, s,
+                    nullptr, na);
+  if (rc) return rc;
   GT_LAUNCH_CHECK("k_hc_div");
   if (fuse_post) return GT_OK;  // k_hc_post_finish runs it with the split
   const int psm = post_smem_bytes<SL>(na);
@@ -1417,14 +1485,16 @@ int launch_node_hc(const NodeArgs& na, cudaStream_t s, bool fuse_post) {
 
 template <int G>
 int launch_partition_g(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint64_t slots, int m, int nf,
-                       uint64_t N, uint64_t base, const Keys& K, int level, cudaStream_t s) {
+                       uint64_t N, uint64_t base, const Keys& K, int level, cudaStream_t s, uint64_t* Sz,
+                       uint64_t swords) {
   constexpr int TPB = 256;
   const uint64_t threads = N * G;
   const unsigned grid = (unsigned)((threads + TPB - 1) / TPB);
   const int smem = 3 * m * (int)sizeof(uint64_t);
   if (smem > 48 * 1024) GT_CUDA_CHECK(cudaFuncSetAttribute(k_partition<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_partition<G><<<grid, TPB, smem, s>>>(X, midx, T, slots, m, nf, N, base, K, op_id(level, SITE_PART_OAA),
-                                         op_id(level, SITE_PART_ROW));
+  int rc = launch_chain(k_partition<G>, dim3(grid), dim3(TPB), (size_t)smem, s, nullptr, X, midx, T, slots, m, nf, N,
+                        base, K, op_id(level, SITE_PART_OAA), op_id(level, SITE_PART_ROW), Sz, swords);
+  if (rc) return rc;
   GT_LAUNCH_CHECK("k_partition");
   return GT_OK;
 }
@@ -1432,7 +1502,8 @@ int launch_partition_g(const uint64_t* X, uint64_t* midx, const uint64_t* T, uin
 // G threads per sample: the fewest idle lane-slots (ceil(m/G) + ceil(nf/G)
 // rounds of G lanes) among the G that keep >= 4 resident warps per SMSP.
 int launch_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint64_t slots, int m, int nf, uint64_t N,
-                     uint64_t base, const Keys& K, int level, cudaStream_t s, int num_sms) {
+                     uint64_t base, const Keys& K, int level, cudaStream_t s, int num_sms, uint64_t* Sz,
+                     uint64_t swords) {
   const uint64_t target = (uint64_t)num_sms * 512;
   int best = 16;
   uint64_t best_work = ~0ull;
@@ -1444,10 +1515,10 @@ int launch_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint6
     }
   }
   switch (best) {
-    case 2: return launch_partition_g<2>(X, midx, T, slots, m, nf, N, base, K, level, s);
-    case 4: return launch_partition_g<4>(X, midx, T, slots, m, nf, N, base, K, level, s);
-    case 8: return launch_partition_g<8>(X, midx, T, slots, m, nf, N, base, K, level, s);
-    default: return launch_partition_g<16>(X, midx, T, slots, m, nf, N, base, K, level, s);
+    case 2: return launch_partition_g<2>(X, midx, T, slots, m, nf, N, base, K, level, s, Sz, swords);
+    case 4: return launch_partition_g<4>(X, midx, T, slots, m, nf, N, base, K, level, s, Sz, swords);
+    case 8: return launch_partition_g<8>(X, midx, T, slots, m, nf, N, base, K, level, s, Sz, swords);
+    default: return launch_partition_g<16>(X, midx, T, slots, m, nf, N, base, K, level, s, Sz, swords);
   }
 }
 
@@ -1717,7 +1788,10 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
     la.K = c.K;
     la.op_cnt = op_id(c.level, SITE_COUNT);
     P.start();
-    k_count_lanes8<<<dim3(nkb, (unsigned)tp.mtiles), 256, 0, s>>>(la);
+    {
+      int rc = launch_chain(k_count_lanes8, dim3(nkb, (unsigned)tp.mtiles), dim3(256), 0, s, nullptr, la);
+      if (rc) return rc;
+    }
     GT_LAUNCH_CHECK("k_count_lanes8");
     P.stop(Prof::COUNT_LANES);
     if (side) {
@@ -1753,16 +1827,12 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
     const int per = (int)((nkb + nkr - 1) / nkr);
     ma.nkr = (int)((nkb + per - 1) / per);
     {
-      cudaLaunchConfig_t lc{};
-      lc.gridDim = dim3((unsigned)(3 * tp.mtiles), (unsigned)(ma.nkr * tp.nbn), 1);
-      lc.blockDim = dim3(128);
-      lc.dynamicSmemBytes = (size_t)smem;
-      lc.stream = s2;
       cudaLaunchAttribute at[1];
-      lc.attrs = at;
-      lc.numAttrs = l2_window_attr(B8, 6ull * tp.nbn * nkb_total * tp.BB, at) ? 1 : 0;
+      const bool win = l2_window_attr(B8, 6ull * tp.nbn * nkb_total * tp.BB, at);
       P.start();
-      GT_CUDA_CHECK(cudaLaunchKernelEx(&lc, k_count_mma, ma));
+      int rc = launch_chain(k_count_mma, dim3((unsigned)(3 * tp.mtiles), (unsigned)(ma.nkr * tp.nbn), 1), dim3(128),
+                            (size_t)smem, s2, win ? at : nullptr, ma);
+      if (rc) return rc;
       P.stop(Prof::COUNT_CONTRACT);
     }
     GT_LAUNCH_CHECK("k_count_mma");
@@ -2062,15 +2132,16 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
   int32_t trained = c.depth;
   for (int level = 0; level < c.depth; ++level) {
     const int n_h = 1 << level;
-    if (level > 0 && N) {
+    const uint64_t swords = 3ull * n_h * (W + 1);
+    if (level > 0 && N) {  // the partition also zeroes this level's count sums
       P.start();
-      int rc = launch_partition(features, midx, T, slots, n_h / 2, c.nf, N, c.sample_base, K, level, s, num_sms);
+      int rc = launch_partition(features, midx, T, slots, n_h / 2, c.nf, N, c.sample_base, K, level, s, num_sms, S,
+                                swords);
       if (rc) return rc;
       P.stop(Prof::PARTITION);
     }
-    const uint64_t swords = 3ull * n_h * (W + 1);
     if (!(level == 0 && count0_done)) {  // level 0 may already be counted chunk by chunk (host operands)
-      GT_CUDA_CHECK(cudaMemsetAsync(S, 0, swords * sizeof(uint64_t), s));
+      if (!(level > 0 && N)) GT_CUDA_CHECK(cudaMemsetAsync(S, 0, swords * sizeof(uint64_t), s));
       if (N) {
         int rc = count_range(level, cur, 0, N);
         if (rc) return rc;
@@ -2183,12 +2254,13 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
         else
           GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_post_finish<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm));
       }
-      if (c.score_width == 32)
-        k_hc_post_finish<32><<<n_h, 256, psm, s>>>(na, fa);
-      else
-        k_hc_post_finish<64><<<n_h, 256, psm, s>>>(na, fa);
+      const int rc = c.score_width == 32
+                         ? launch_chain(k_hc_post_finish<32>, dim3(n_h), dim3(256), (size_t)psm, s, nullptr, na, fa)
+                         : launch_chain(k_hc_post_finish<64>, dim3(n_h), dim3(256), (size_t)psm, s, nullptr, na, fa);
+      if (rc) return rc;
     } else {
-      k_node_finish<<<n_h, 128, 0, s>>>(fa);
+      const int rc = launch_chain(k_node_finish, dim3(n_h), dim3(128), 0, s, nullptr, fa);
+      if (rc) return rc;
     }
     GT_LAUNCH_CHECK("k_node_finish");
     P.stop(Prof::NODE_FINISH);
@@ -2231,7 +2303,7 @@ int gt_train_host(const gt_train_cfg* cfg, const uint64_t* features_h, const uin
 
 // diagnostics: the heuristic phase timestamps of the last GT_HC_TIMING run (ns)
 int gt_diag_hc_timestamps(unsigned long long* out, int n) {
-  if (!out || n < 0 || n > 64) return fail_inval("gt_diag_hc_timestamps: bad output");
+  if (!out || n < 0 || n > 128) return fail_inval("gt_diag_hc_timestamps: bad output");
   GT_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_hc_ts, sizeof(unsigned long long) * n));
   return GT_OK;
 }
