@@ -3,23 +3,25 @@
 //
 // The count contraction of one level (_count_level, reference
 // pkg/src/obtree/train.py:315-343) is, per share component i, the ring GEMM
-//     S_i[n][w] = sum_s la_i[s][n] u_i[s][w] + la_{i+1}[s][n] x_i[s][w]
-// (the party-local cross terms of mul(cols, la), rss.py:391-395, with
-// u_i = x_i + x_{i+1}; the mask column has u = 1, x = 0).  Writing every u64
-// as 8 unsigned bytes, a * b mod 2^64 = sum_{p+q<=7} a_p b_q 2^{8(p+q)}, so
-// with rows (node n, limb p) and columns (column w, limb q)
-//     D[(n,p)][(w,q)] = sum_s la_p u_q + la'_p x_q         (u8 x u8 -> s32)
-//     S[n][w]         = sum_{p+q<=7} D[(n,p)][(w,q)] << 8(p+q)   (mod 2^64)
-// D is one UMMA accumulator (M = 128 rows = 16 nodes x 8 limbs, N = 8 x
-// columns of the block, K = 2 x samples: the two terms are consecutive K
-// blocks).  Each CTA sums at most 2 x 16 512 samples, so every D entry stays
-// below 2^31 (exact in the s32 accumulator whether it wraps or saturates).
+//     S_i[n][w] = sum_s la_i x_i + la_i x_{i+1} + la_{i+1} x_i
+// (the party-local cross terms of mul(cols, la), rss.py:391-395).  Writing
+// every u64 as 8 unsigned bytes, a * b mod 2^64 = sum_{p+q<=7} a_p b_q
+// 2^{8(p+q)}, so with rows (node n, limb p) and columns (column w, limb q)
+//     D_i[(n,p)][(w,q)] = sum_s la_i,p x_i,q + la_i,p x_{i+1},q + la_{i+1},p x_i,q   (u8 x u8 -> s32)
+//     S_i[n][w]         = sum_{p+q<=7} D_i[(n,p)][(w,q)] << 8(p+q)   (mod 2^64)
+// One CTA holds the three components' accumulators D_0, D_1, D_2 in TMEM
+// (M = 128 rows = 16 nodes x 8 limbs, N = 8 x columns of the block each), so
+// every operand plane is streamed once per (M tile, column block): nine UMMAs
+// per 32-sample K step over three la planes and three x planes.  Each CTA
+// sums at most 64 x 128 samples, so every D entry stays below
+// 3 x 8192 x 255^2 < 2^31 (exact in the s32 accumulator).  The mask column
+// s_mask = sum_s la (train.py:334) is summed by the lane kernel.
 //
 // Operands are staged by cp.async.bulk in the canonical K-major
 // SWIZZLE_NONE core-matrix layout (8 rows x 16 bytes = 128 contiguous bytes;
 // SBO = 128 B between 8-row groups, LBO between the 16-byte K chunks), which
-// the producer kernels write directly, so one block of 128 samples of an
-// operand is one contiguous bulk copy.
+// the producer kernels write directly, so one half block (64 samples) of the
+// three components of an operand is one contiguous bulk copy.
 #pragma once
 
 namespace gt {
@@ -27,21 +29,21 @@ namespace {
 
 constexpr int TC_KB = 128;                // samples per K block
 constexpr int TC_ABLK = TC_KB * 128;      // bytes of an A block: 128 rows (16 nodes x 8 limbs) x 128 samples
-constexpr int TC_MAX_KB_PER_CTA = 64;     // 2 products x 64 x 128 x 255^2 < 2^31
-constexpr int TC_TMEM_COLS = 256;
+constexpr int TC_MAX_KB_PER_CTA = 64;     // 3 products x 64 x 128 x 255^2 < 2^31
+constexpr int TC_TMEM_COLS = 512;         // three accumulators of N <= 160 columns
 
 struct TcPlan {
-  int CW;      // sample columns incl. the mask column (W + 1)
+  int CW;      // sample columns W (the mask column is summed by the lane kernel)
   int nbn;     // column blocks
   int cpb;     // columns per block (even)
-  int N;       // UMMA N = 8 * cpb (multiple of 16, <= 256)
+  int N;       // UMMA N = 8 * cpb (multiple of 16, <= 160: three accumulators fit TMEM)
   int mtiles;  // 16-node M tiles
-  int BB;      // bytes of a B block (N rows x 128 samples)
+  int BB;      // bytes of one component's x plane of a K block (N rows x 128 samples)
 };
 inline TcPlan tc_plan(int nf, int n_h) {
   TcPlan p;
-  p.CW = 2 * nf + 2;
-  p.nbn = (p.CW + 31) / 32;
+  p.CW = 2 * nf + 1;
+  p.nbn = (p.CW + 19) / 20;
   p.cpb = (p.CW + p.nbn - 1) / p.nbn;
   p.cpb += p.cpb & 1;
   p.N = 8 * p.cpb;
@@ -51,68 +53,9 @@ inline TcPlan tc_plan(int nf, int n_h) {
 }
 
 // --- B operand: the level-invariant sample columns as byte planes
-// B8[c][nb][kb][half 2][term 2][kc 4][g cpb][q 8][16 samples]; term 0 =
-// u_c = x_c + x_{c+1} (1 on the mask column), term 1 = x_c (0 there): the
-// two terms of a 64-sample half block are one contiguous run (one copy).
-struct Cols8Args {
-  const uint64_t* cols;  // [3][N][WC] u64 (x | prods | y | 0 ...)
-  uint8_t* B8;
-  uint64_t N, nkb;
-  int WC, W, cpb, nbn;
-};
-__global__ void __launch_bounds__(256) k_cols8(Cols8Args a) {
-  // one thread per (K block, 16-sample chunk, column): the three components
-  // of 16 samples are read once and all six (component, term) planes written
-  const int WG = a.nbn * a.cpb;
-  const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t total = a.nkb * 8 * WG;
-  if (e >= total) return;
-  const int wg = (int)(e % WG);
-  const uint64_t r = e / WG;
-  const int kc = (int)(r % 8);
-  const uint64_t kb = r / 8;
-  const int nb = wg / a.cpb, g = wg % a.cpb, w = wg;
-  const uint64_t cs = a.N * (uint64_t)a.WC;
-#pragma unroll 1
-  for (int c = 0; c < 3; ++c) {
-    uint32_t pk[2][8][4];
-#pragma unroll
-    for (int t = 0; t < 2; ++t)
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) pk[t][q][k] = 0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const uint64_t s = kb * TC_KB + kc * 16 + i;
-      uint64_t x = 0, u = 0;
-      if (s < a.N) {
-        if (w < a.W) {
-          x = __ldg(a.cols + c * cs + s * a.WC + w);
-          u = x + __ldg(a.cols + ((c + 1) % 3) * cs + s * a.WC + w);
-        } else if (w == a.W) {
-          u = 1;  // mask column: s_mask += la (train.py:334)
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        pk[0][q][i >> 2] |= (uint32_t)((u >> (8 * q)) & 0xffu) << (8 * (i & 3));
-        pk[1][q][i >> 2] |= (uint32_t)((x >> (8 * q)) & 0xffu) << (8 * (i & 3));
-      }
-    }
-    const uint64_t HB = (uint64_t)8 * a.cpb * (TC_KB / 2);  // one term of a half block
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      uint8_t* dst = a.B8 + ((((uint64_t)c * a.nbn + nb) * a.nkb + kb) * 2 + (kc >> 2)) * 2 * HB + t * HB +
-                     ((uint64_t)(kc & 3) * a.cpb + g) * 128;
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        *reinterpret_cast<uint4*>(dst + q * 16) = make_uint4(pk[t][q][0], pk[t][q][1], pk[t][q][2], pk[t][q][3]);
-    }
-  }
-}
-
-// Fused prologue for the tensor engine (replaces k_prods + k_cols8): one CTA
+// X8[nb][kb][half 2][c 3][kc 4][g cpb][q 8][16 samples]: the three
+// components' x planes of a 64-sample half block are one contiguous run.
+// Fused prologue for the tensor engine (count:0 prods + the x planes): one CTA
 // per 128-sample K block stages the block's features and labels in shared
 // memory (coalesced rows), forms count:0's prods = mul(features, labels)
 // (train.py:229-230, same Philox schedule as k_prods) next to them, and
@@ -181,10 +124,10 @@ __global__ void __launch_bounds__(256) k_prep8(Prep8Args a) {
   }
   __syncthreads();
   // planes: item = (component, 16-sample chunk, column, 4-sample quad); the
-  // quad's u = x_c + x_{c+1} and x_c words are byte-transposed in registers
-  // (4x4 byte_perm transposes) into one 32-bit word of each of the 8 limb
-  // rows of both terms; the four quads of a row are adjacent threads
-  const uint64_t HB = (uint64_t)8 * a.cpb * HS;
+  // quad's x words are byte-transposed in registers (4x4 byte_perm
+  // transposes) into one 32-bit word of each of the 8 limb rows; the four
+  // quads of a row are adjacent threads
+  const uint64_t HBX = (uint64_t)8 * a.cpb * HS;
   const int items = 3 * 4 * a.nbn * a.cpb * 4;
   for (int it = tid; it < items; it += blockDim.x) {
     const int quad = it & 3;
@@ -193,48 +136,32 @@ __global__ void __launch_bounds__(256) k_prep8(Prep8Args a) {
     r /= a.cpb;
     const int kc = r & 3;
     r >>= 2;
-    const int nb = r % a.nbn, c = r / a.nbn, c1 = (c + 1) % 3;
+    const int nb = r % a.nbn, c = r / a.nbn;
     const int w = nb * a.cpb + g;
-    const uint64_t *p0 = nullptr, *p1 = nullptr;
+    const uint64_t* p0 = nullptr;
     int stride = nf;
-    if (w < nf) {
-      p0 = xs + c * HS * nf + w, p1 = xs + c1 * HS * nf + w;
-    } else if (w < 2 * nf) {
-      p0 = ps + c * HS * nf + (w - nf), p1 = ps + c1 * HS * nf + (w - nf);
-    } else if (w == 2 * nf) {
-      p0 = ys + c * HS, p1 = ys + c1 * HS, stride = 1;
-    }
-    uint32_t wx[2][4], wu[2][4];
+    if (w < nf) p0 = xs + c * HS * nf + w;
+    else if (w < 2 * nf) p0 = ps + c * HS * nf + (w - nf);
+    else if (w == 2 * nf) p0 = ys + c * HS, stride = 1;
+    uint32_t wx[2][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int sl = kc * 16 + quad * 4 + i;
-      uint64_t x = 0, u = 0;
-      if (sl < cnt) {
-        if (p0) {
-          x = p0[sl * stride];
-          u = x + p1[sl * stride];
-        } else if (w == W) {
-          u = 1;  // mask column: s_mask += la (train.py:334)
-        }
-      }
+      const uint64_t x = (p0 && sl < cnt) ? p0[sl * stride] : 0ull;
       wx[0][i] = (uint32_t)x, wx[1][i] = (uint32_t)(x >> 32);
-      wu[0][i] = (uint32_t)u, wu[1][i] = (uint32_t)(u >> 32);
     }
-    uint8_t* dst = a.B8 + ((((uint64_t)c * a.nbn + nb) * a.nkb + kb) * 2 + half) * 2 * HB +
+    uint8_t* dst = a.B8 + (((uint64_t)nb * a.nkb + kb) * 2 + half) * 3 * HBX + c * HBX +
                    ((uint64_t)kc * a.cpb + g) * 128 + quad * 4;
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const uint32_t* q4 = t == 0 ? wu[hh] : wx[hh];
-        const uint32_t t0 = __byte_perm(q4[0], q4[1], 0x5140), t1 = __byte_perm(q4[0], q4[1], 0x7362);
-        const uint32_t t2 = __byte_perm(q4[2], q4[3], 0x5140), t3 = __byte_perm(q4[2], q4[3], 0x7362);
-        uint8_t* d = dst + t * HB + hh * 4 * 16;
-        *reinterpret_cast<uint32_t*>(d) = __byte_perm(t0, t2, 0x5410);
-        *reinterpret_cast<uint32_t*>(d + 16) = __byte_perm(t0, t2, 0x7632);
-        *reinterpret_cast<uint32_t*>(d + 32) = __byte_perm(t1, t3, 0x5410);
-        *reinterpret_cast<uint32_t*>(d + 48) = __byte_perm(t1, t3, 0x7632);
-      }
+    for (int hh = 0; hh < 2; ++hh) {
+      const uint32_t* q4 = wx[hh];
+      const uint32_t t0 = __byte_perm(q4[0], q4[1], 0x5140), t1 = __byte_perm(q4[0], q4[1], 0x7362);
+      const uint32_t t2 = __byte_perm(q4[2], q4[3], 0x5140), t3 = __byte_perm(q4[2], q4[3], 0x7362);
+      uint8_t* d = dst + hh * 4 * 16;
+      *reinterpret_cast<uint32_t*>(d) = __byte_perm(t0, t2, 0x5410);
+      *reinterpret_cast<uint32_t*>(d + 16) = __byte_perm(t0, t2, 0x7632);
+      *reinterpret_cast<uint32_t*>(d + 32) = __byte_perm(t1, t3, 0x5410);
+      *reinterpret_cast<uint32_t*>(d + 48) = __byte_perm(t1, t3, 0x7632);
     }
   }
 }
@@ -249,6 +176,8 @@ __global__ void __launch_bounds__(256) k_prep8(Prep8Args a) {
 struct Lanes8Args {
   const uint64_t *midx, *f;
   uint8_t* la8;
+  uint64_t* S;  // [3][n_h][W+1]: the mask column s_mask[n] = sum_s la (train.py:334)
+  int W;
   uint64_t N, s0, cn, base, nkbc;  // nkbc = chunk capacity in K blocks
   int n_h, off, mtiles;
   Keys K;
@@ -295,6 +224,20 @@ __global__ void __launch_bounds__(256) k_count_lanes8(Lanes8Args a) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) lf.v[c] = leaf[c][nn];
       count_lane_pair(a.K, a.op_cnt, a.base + gs, a.n_h, n, d0, d1, true, v1, lf, &l0, &l1);
+    }
+    {  // s_mask: the warp's 64 samples of node n, one atomic per component
+      // (l1 of a pair past the chunk's end is padding: multiplied by zero
+      // columns in the contraction, left out here)
+      const bool has1 = (uint64_t)kb * TC_KB + s2 + 1 < a.cn;
+      A3 m = has1 ? add<64>(l0, l1) : l0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) m.v[c] += __shfl_xor_sync(0xffffffffu, m.v[c], o);
+      if ((tid & 31) == 0 && n < a.n_h)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          atomicAdd((unsigned long long*)&a.S[((uint64_t)c * a.n_h + n) * (a.W + 1) + a.W], (unsigned long long)m.v[c]);
     }
     const int o = (s2 >> 6) * (3 * TC_ABLK / 2) + ((((s2 >> 4) & 3) * 16 + nn) * 8) * 16 + ((s2 & ~3) & 15);
     const int p0 = odd ? 4 : 0;
@@ -351,39 +294,38 @@ struct MmaArgs {
   Keys K;
   uint32_t op_cnt;
   int alpha;            // 0: none, 1: telescoped elementwise reshare sums, 2: dot-product reshare
+  const uint64_t* alpha_tab;  // this level's precomputed sums [n][3][W] (k_alpha_tape) or null: draw them
   uint64_t t0, t1;      // shard sample range for the telescoped sums
   uint64_t nkbc, nkb_total, kb_base;  // chunk capacity (blocks), shard blocks, chunk's first global block
   uint32_t nkb;                       // blocks in this chunk
   int n_h, W, cpb, nbn, mtiles, N, nkr;
-  int probe;  // diagnostics only (GT_MMA_PROBE): 1 = loads without MMAs, 2 = MMAs without loads
+  int probe;  // diagnostics only (GT_MMA_PROBE): 1 = loads without MMAs, 2 = MMAs without loads, 3 = neither
 };
 
-// One CTA per (K range, M tile, column block, component c): the party-local
-// cross terms of component c
-//     D_c = A_c U_c + A_{c+1} X_c        (U_c = x_c + x_{c+1}, rss.py:391-395)
+// One CTA per (K range, M tile, column block): the party-local cross terms
+// of all three components
+//     D_c = A_c X_c + A_c X_{c+1} + A_{c+1} X_c        (rss.py:391-395)
 // A stage is one 64-sample half block brought by TWO contiguous bulk copies
-// (the three components' la planes, 24 KB, of which A_c and A_{c+1} are
-// used; the (U_c, X_c) planes, N x 128 B), four stages in flight: bulk
-// copies pay a fixed latency each, so few large requests with several in
-// flight keep the SM's copy engine streaming.
+// (the three components' la planes, 24 KB; the three components' x planes,
+// 3 x N x 64 B), four stages in flight: bulk copies pay a fixed latency each,
+// so few large requests with several in flight keep the SM's copy engine
+// streaming.
 constexpr int TC_MC_STAGES = 4;
 constexpr int TC_A_HB = 3 * TC_ABLK / 2;  // the 3 components' la planes of a half block
-__global__ void __launch_bounds__(128, 1) k_count_mma(MmaArgs a) {
+__global__ void __launch_bounds__(256, 1) k_count_mma(MmaArgs a) {
   extern __shared__ __align__(1024) uint8_t smt[];
   __shared__ __align__(8) uint64_t full[TC_MC_STAGES], empty[TC_MC_STAGES], done;
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // grid (3 components x M tiles, column blocks x K ranges): the CTAs that
-  // share operand planes -- the M tiles of one (K range, column block) read
-  // the same U/X planes, the two components of an M tile the same la planes --
-  // are adjacent in launch order, so they run together and share them in L2
-  const int c = blockIdx.x % 3, mt = blockIdx.x / 3, nb = blockIdx.y % a.nbn, kr = blockIdx.y / a.nbn;
-  const int cn = (c + 1) % 3, cp = (c + 2) % 3;
+  // grid (M tiles, column blocks x K ranges): the M tiles of one (K range,
+  // column block) read the same x planes and are adjacent in launch order
+  const int mt = blockIdx.x, nb = blockIdx.y % a.nbn, kr = blockIdx.y / a.nbn;
   const uint32_t per = (a.nkb + a.nkr - 1) / a.nkr;
   const uint32_t kb0 = kr * per, kb1 = min(a.nkb, kb0 + per);
   const int T = kb1 > kb0 ? 2 * (int)(kb1 - kb0) : 0;  // half blocks
-  const int HB = a.N * (TC_KB / 2);                     // one term of a half block
-  const int stage = TC_A_HB + 2 * HB;
+  const int HBX = a.N * (TC_KB / 2);                    // one component's x plane of a half block
+  const int stage = TC_A_HB + 3 * HBX;
+  const int NS = (a.N + 31) & ~31;                      // accumulator column stride in TMEM
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
@@ -405,21 +347,17 @@ __global__ void __launch_bounds__(128, 1) k_count_mma(MmaArgs a) {
   const uint32_t tmem = tmem_slot;
   pdl_wait();  // the lane planes of the lane kernel
 
-  if (tid == 0 && T > 0) {
+  if (tid == 0 && T > 0 && a.probe < 3) {
     // idesc: S32 accumulator [4,6) = 2, A/B unsigned 8-bit, K-major, N>>3 at 17, M>>4 at 24
     const uint32_t idesc = (2u << 4) | ((uint32_t)(a.N >> 3) << 17) | ((128u >> 4) << 24);
     auto load = [&](int t) {
       const int st = t % TC_MC_STAGES;
       const uint64_t kb = kb0 + (uint32_t)(t >> 1), h = t & 1;
       uint8_t* sb = smt + st * stage;
-      // A_c, A_{c+1} only: adjacent planes for c = 0, 1; component 2 needs
-      // planes 2 and 0, so it takes the whole 24 KB run
-      const uint32_t aoff = c < 2 ? (uint32_t)c * (TC_ABLK / 2) : 0u, alen = c < 2 ? (uint32_t)TC_ABLK : TC_A_HB;
-      mbar_expect_tx(&full[st], alen + 2u * HB);
-      bulk_g2s(sb + aoff, a.la8 + (((uint64_t)mt * a.nkbc + kb) * 2 + h) * (uint64_t)TC_A_HB + aoff, alen, &full[st]);
-      bulk_g2s(sb + TC_A_HB,
-               a.B8 + ((((uint64_t)c * a.nbn + nb) * a.nkb_total + a.kb_base + kb) * 2 + h) * (uint64_t)(2 * HB),
-               (uint32_t)(2 * HB), &full[st]);
+      mbar_expect_tx(&full[st], (uint32_t)stage);
+      bulk_g2s(sb, a.la8 + (((uint64_t)mt * a.nkbc + kb) * 2 + h) * (uint64_t)TC_A_HB, (uint32_t)TC_A_HB, &full[st]);
+      bulk_g2s(sb + TC_A_HB, a.B8 + (((uint64_t)nb * a.nkb_total + a.kb_base + kb) * 2 + h) * (uint64_t)(3 * HBX),
+               (uint32_t)(3 * HBX), &full[st]);
     };
     if (a.probe != 2)
       for (int t = 0; t < min(TC_MC_STAGES, T); ++t) load(t);
@@ -428,16 +366,22 @@ __global__ void __launch_bounds__(128, 1) k_count_mma(MmaArgs a) {
       if (a.probe != 2) mbar_wait(&full[st], (uint32_t)((t / TC_MC_STAGES) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t base = smem_u32(smt + st * stage);
-      const uint32_t Ac = base + c * (TC_ABLK / 2), An = base + cn * (TC_ABLK / 2);
-      const uint32_t Uc = base + TC_A_HB, Xc = Uc + HB;
       if (a.probe != 1)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const uint32_t ao = j * 2 * (16 * 128), xo = j * 2 * (a.cpb * 128);
-        umma_i8(tmem, umma_desc(Ac + ao, 16 * 128, 128), umma_desc(Uc + xo, a.cpb * 128, 128), idesc,
-                (t > 0 || j > 0) ? 1u : 0u);
-        umma_i8(tmem, umma_desc(An + ao, 16 * 128, 128), umma_desc(Xc + xo, a.cpb * 128, 128), idesc, 1u);
-      }
+        for (int j = 0; j < 2; ++j) {
+          const uint32_t ao = j * 2 * (16 * 128), xo = j * 2 * (a.cpb * 128);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const int cn = (c + 1) % 3;
+            const uint32_t Ac = base + c * (TC_ABLK / 2) + ao, An = base + cn * (TC_ABLK / 2) + ao;
+            const uint32_t Xc = base + TC_A_HB + c * HBX + xo, Xn = base + TC_A_HB + cn * HBX + xo;
+            const uint32_t D = tmem + (uint32_t)(c * NS);
+            umma_i8(D, umma_desc(Ac, 16 * 128, 128), umma_desc(Xc, a.cpb * 128, 128), idesc,
+                    (t > 0 || j > 0) ? 1u : 0u);
+            umma_i8(D, umma_desc(Ac, 16 * 128, 128), umma_desc(Xn, a.cpb * 128, 128), idesc, 1u);
+            umma_i8(D, umma_desc(An, 16 * 128, 128), umma_desc(Xc, a.cpb * 128, 128), idesc, 1u);
+          }
+        }
       umma_commit(&empty[st]);
       // refill the previous stage (its MMAs were issued one step earlier)
       if (a.probe != 2 && t >= 1 && t - 1 + TC_MC_STAGES < T) {
@@ -449,51 +393,70 @@ __global__ void __launch_bounds__(128, 1) k_count_mma(MmaArgs a) {
     umma_commit(&done);
   }
   __syncwarp();
-  if (T > 0) mbar_wait(&done, 0);
+  if (T > 0 && a.probe < 3) mbar_wait(&done, 0);
   pdl_trigger();  // the epilogue overlaps the next kernel's launch
-  if (T > 0) {
+  if (T > 0 && a.probe < 4) {
+    // epilogue: thread (node nn, limb p) = TMEM lane r forms, per column w,
+    // R_p[w] = sum_q D[(nn,p)][(w,q)] << 8(p+q) from 64-column TMEM loads (8
+    // columns each); the eight limb rows of a node are summed through shared
+    // memory (the operand ring is idle now), one atomic per (component, node,
+    // column)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int r = warp * 32 + lane, nn = r >> 3, p = r & 7;
-    const int n = mt * 16 + nn;
-    const uint64_t Sstride = (uint64_t)a.n_h * (a.W + 1);
-    for (int k = 0; k < a.N / 16; ++k) {
-      uint32_t d[16];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-          "%15}, [%16];"
-          : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
-            "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
-          : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(k * 16)));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    // warps w and w + 4 share TMEM lanes 32 (w % 4) ..: they split the loads
+    const int r = (warp & 3) * 32 + lane, nn = r >> 3, p = r & 7, grp = warp >> 2;
+    uint64_t* red = reinterpret_cast<uint64_t*>(smt);  // [3][cpb][16 nn][8 p]
+    const int cpb = a.cpb, nchunk = NS / 64 + (NS % 64 ? 1 : 0);
+    for (int it = grp; it < 3 * nchunk; it += 2) {
+      const int c = it / nchunk, cb = (it % nchunk) * 64;
+      {
+        uint32_t d[64];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63}, [%64];"
+            : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]), "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15]), "=r"(d[16]), "=r"(d[17]), "=r"(d[18]), "=r"(d[19]), "=r"(d[20]), "=r"(d[21]), "=r"(d[22]), "=r"(d[23]), "=r"(d[24]), "=r"(d[25]), "=r"(d[26]), "=r"(d[27]), "=r"(d[28]), "=r"(d[29]), "=r"(d[30]), "=r"(d[31]), "=r"(d[32]), "=r"(d[33]), "=r"(d[34]), "=r"(d[35]), "=r"(d[36]), "=r"(d[37]), "=r"(d[38]), "=r"(d[39]), "=r"(d[40]), "=r"(d[41]), "=r"(d[42]), "=r"(d[43]), "=r"(d[44]), "=r"(d[45]), "=r"(d[46]), "=r"(d[47]), "=r"(d[48]), "=r"(d[49]), "=r"(d[50]), "=r"(d[51]), "=r"(d[52]), "=r"(d[53]), "=r"(d[54]), "=r"(d[55]), "=r"(d[56]), "=r"(d[57]), "=r"(d[58]), "=r"(d[59]), "=r"(d[60]), "=r"(d[61]), "=r"(d[62]), "=r"(d[63])
+            : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * NS + cb)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint64_t v = 0;
+        for (int wl = 0; wl < 8; ++wl) {
+          // sum_q d_q << 8q with constant shifts, then << 8p (the terms with
+          // p + q >= 8 leave the ring)
+          uint64_t v = 0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int sh = 8 * (p + q);
-          if (sh < 64) v += (uint64_t)d[8 * h + q] << sh;
-        }
-        v += __shfl_xor_sync(0xffffffffu, v, 1);
-        v += __shfl_xor_sync(0xffffffffu, v, 2);
-        v += __shfl_xor_sync(0xffffffffu, v, 4);
-        const int w = nb * a.cpb + 2 * k + h;
-        if (p == 0 && n < a.n_h && w <= a.W) {
-          if (a.alpha && kr == 0 && w < a.W) {
-            // zero shares of the count products summed over the shard (see
-            // k_count_alpha): alpha_c = F_c - F_{c-1}
-            uint64_t F[2];
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const Key& key = a.K.pair[q == 0 ? c : cp];
-              F[q] = a.alpha == 2 ? word(key, a.op_cnt, 4, (uint32_t)w, (uint64_t)n)
-                                  : word(key, a.op_cnt, 3, (uint32_t)w, a.t1 * (uint64_t)a.n_h + n) -
-                                        word(key, a.op_cnt, 3, (uint32_t)w, a.t0 * (uint64_t)a.n_h + n);
-            }
-            v += F[0] - F[1];
-          }
-          atomicAdd((unsigned long long*)&a.S[c * Sstride + (uint64_t)n * (a.W + 1) + w], (unsigned long long)v);
+          for (int q = 0; q < 8; ++q) v += (uint64_t)d[8 * wl + q] << (8 * q);
+          v <<= 8 * p;
+          const int w = cb / 8 + wl;
+          if (w < cpb) red[((c * cpb + w) * 16 + nn) * 8 + p] = v;
         }
       }
+    }
+    __syncthreads();
+    const uint64_t Sstride = (uint64_t)a.n_h * (a.W + 1);
+    for (int cell = tid; cell < 3 * cpb * 16; cell += blockDim.x) {
+      const int nc = cell & 15, cw = cell >> 4, w = cw % cpb, c = cw / cpb;
+      const int n = mt * 16 + nc, wg = nb * cpb + w;
+      if (n >= a.n_h || wg >= a.W) continue;
+      const uint4* rp = reinterpret_cast<const uint4*>(red + (uint64_t)cell * 8);
+      uint64_t v = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint4 x = rp[i];
+        v += ((uint64_t)x.y << 32 | x.x) + ((uint64_t)x.w << 32 | x.z);
+      }
+      if (a.alpha && kr == 0 && a.alpha_tab) {
+        v += a.alpha_tab[((uint64_t)n * 3 + c) * a.W + wg];
+      } else if (a.alpha && kr == 0) {
+        // zero shares of the count products summed over the shard (see
+        // k_count_alpha): alpha_c = F_c - F_{c-1}
+        uint64_t F[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const Key& key = a.K.pair[q == 0 ? c : (c + 2) % 3];
+          F[q] = a.alpha == 2 ? word(key, a.op_cnt, 4, (uint32_t)wg, (uint64_t)n)
+                              : word(key, a.op_cnt, 3, (uint32_t)wg, a.t1 * (uint64_t)a.n_h + n) -
+                                    word(key, a.op_cnt, 3, (uint32_t)wg, a.t0 * (uint64_t)a.n_h + n);
+        }
+        v += F[0] - F[1];
+      }
+      atomicAdd((unsigned long long*)&a.S[c * Sstride + (uint64_t)n * (a.W + 1) + wg], (unsigned long long)v);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -1348,6 +1348,12 @@ uint64_t div_tape_words(const gt_train_cfg& c) {
   const uint64_t w = lanes * (uint64_t)TB;
   return w * 16 > (256ull << 20) ? 0 : w;
 }
+// Count reshare sums of every level (k_alpha_tape, tensor engine); 0 when over 64 MB
+uint64_t alpha_tab_words(const gt_train_cfg& c) {
+  if (c.count_engine != 0) return 0;
+  const uint64_t w = 3ull * ((1ull << c.depth) - 1) * (uint64_t)(2 * c.nf + 1);
+  return w * 8 > (64ull << 20) ? 0 : w;
+}
 // Prologue feature tapes of every heuristic level (W2 units); 0 when over 256 MB
 uint64_t feat_tape_words(const gt_train_cfg& c) {
   static const bool off = getenv("GT_NO_FEAT_TAPE") != nullptr;  // A/B experiments
@@ -1366,7 +1372,7 @@ inline uint64_t div_tape_level_off(int level, int nf, int TB) {  // W2 offset of
 }
 
 struct Layout {
-  uint64_t xin, yin, fin, tout, fout, cols, la, cols8, leaf, midx, divtape, divtable, posttape, posttable, nodetape, nodetable, feattape, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
+  uint64_t xin, yin, fin, tout, fout, cols, la, cols8, leaf, midx, divtape, divtable, posttape, posttable, nodetape, nodetable, feattape, alphatab, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
 };
 
 Layout layout(const gt_train_cfg& c, bool host_io = false) {
@@ -1384,7 +1390,7 @@ Layout layout(const gt_train_cfg& c, bool host_io = false) {
     const TcPlan tp = tc_plan(c.nf, (int)nmax);
     const uint64_t nkb = (N + TC_KB - 1) / TC_KB;
     L.la = take(2 * tc_la8_blocks(N, c.nf, c.depth) * 3ull * tp.mtiles * TC_ABLK / 8);  // two chunk buffers
-    L.cols8 = take(6ull * tp.nbn * nkb * tp.BB / 8);
+    L.cols8 = take(3ull * tp.nbn * nkb * tp.BB / 8);
   } else {
     L.la = take(la_words(N, c.nf, c.depth));
     L.cols8 = take(0);
@@ -1396,6 +1402,7 @@ Layout layout(const gt_train_cfg& c, bool host_io = false) {
   L.nodetape = take(c.heuristic == 0 ? 2 * ((1ull << c.depth) - 1) * (uint64_t)node_tape_plan(c.nf).total : 0);
   L.nodetable = take(c.heuristic == 0 ? (uint64_t)node_tape_plan(c.nf).total : 0);
   L.feattape = take(2 * feat_tape_words(c));
+  L.alphatab = take(alpha_tab_words(c));
   L.posttable = take(c.heuristic == 0 ? (uint64_t)post_tape_blocks_w(c.score_width, c.nf) : 0);
   {
     bool ok = false;
@@ -1591,6 +1598,28 @@ struct Prof {
 //  dot (count_reshare 1): ONE zero share per cell, F_i at (op_cnt, sub 4,
 //    field w, lane n), added by the shard holding sample 0.
 // alpha_i = F_i - F_{i-1} (rss.py:302-306).
+// The count products' reshare sums of every level, drawn up front (they depend
+// only on the keys and the shard's sample range): tab[(2^h - 1) + n][c][w] =
+// F_c - F_{c-1}, F as in k_count_alpha.  The contraction's epilogue adds them.
+__global__ void __launch_bounds__(256) k_alpha_tape(uint64_t* tab, uint32_t cells, int nf, Keys K, int dot,
+                                                    uint64_t t0, uint64_t t1) {
+  const int W = 2 * nf + 1;
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= cells) return;
+  const uint32_t gn = e / W;
+  const int w = (int)(e - gn * W);
+  const int level = 31 - __clz(gn + 1);
+  const uint64_t n = gn - ((1u << level) - 1), n_h = 1ull << level;
+  const uint32_t op = op_id(level, SITE_COUNT);
+  uint64_t F[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    F[i] = dot ? word(K.pair[i], op, 4, (uint32_t)w, n)
+               : word(K.pair[i], op, 3, (uint32_t)w, t1 * n_h + n) - word(K.pair[i], op, 3, (uint32_t)w, t0 * n_h + n);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) tab[((uint64_t)gn * 3 + c) * W + w] = F[c] - F[(c + 2) % 3];
+}
+
 __global__ void k_count_alpha(uint64_t* S, int n_h, int nf, Keys K, uint32_t op_cnt, int dot, uint64_t t0,
                               uint64_t t1) {
   const int W = 2 * nf + 1;
@@ -1615,6 +1644,7 @@ struct CountLaunch {
   int nf, n_h, n_h_max;
   Keys K;
   int level;
+  const uint64_t* alpha_tab;  // the level's precomputed count reshare sums (tensor engine) or null
 };
 
 // leaf + per chunk (lanes, contraction); returns the number of launches
@@ -1765,7 +1795,7 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
   }
   int k = 0;
   const uint64_t nkb_total = (c.N + TC_KB - 1) / TC_KB;
-  const int smem = TC_MC_STAGES * (TC_A_HB + tp.BB);
+  const int smem = TC_MC_STAGES * (TC_A_HB + 3 * tp.BB / 2);
   GT_CUDA_CHECK(cudaFuncSetAttribute(k_count_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   for (uint64_t s0 = lo; s0 < hi; s0 += cap, ++k) {  // lo is a multiple of TC_KB
     const uint64_t cn = std::min<uint64_t>(cap, hi - s0);
@@ -1787,6 +1817,8 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
     la.mtiles = tp.mtiles;
     la.K = c.K;
     la.op_cnt = op_id(c.level, SITE_COUNT);
+    la.S = c.S;
+    la.W = 2 * c.nf + 1;
     P.start();
     {
       int rc = launch_chain(k_count_lanes8, dim3(nkb, (unsigned)tp.mtiles), dim3(256), 0, s, nullptr, la);
@@ -1819,18 +1851,24 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
       ma.probe = probe;
     }
     ma.alpha = s0 == 0 ? alpha : 0;
+    ma.alpha_tab = c.alpha_tab;
     ma.t0 = t0;
     ma.t1 = t1;
-    const int tiles = 3 * tp.mtiles * tp.nbn;
-    int nkr = std::max<int>((int)((nkb + TC_MAX_KB_PER_CTA - 1) / TC_MAX_KB_PER_CTA), (num_sms + tiles - 1) / tiles);
+    // one CTA per SM (shared memory): the fewest waves the K-range bound
+    // allows, filled with as many K ranges as fit in them (a partial second
+    // wave would double the kernel's time)
+    const int tiles = tp.mtiles * tp.nbn;
+    const int nkr_min = (int)((nkb + TC_MAX_KB_PER_CTA - 1) / TC_MAX_KB_PER_CTA);
+    const int waves = std::max(1, (tiles * nkr_min + num_sms - 1) / num_sms);
+    int nkr = std::max(nkr_min, waves * num_sms / tiles);
     nkr = std::min<int>(nkr, (int)nkb);
     const int per = (int)((nkb + nkr - 1) / nkr);
     ma.nkr = (int)((nkb + per - 1) / per);
     {
       cudaLaunchAttribute at[1];
-      const bool win = l2_window_attr(B8, 6ull * tp.nbn * nkb_total * tp.BB, at);
+      const bool win = l2_window_attr(B8, 3ull * tp.nbn * nkb_total * tp.BB, at);
       P.start();
-      int rc = launch_chain(k_count_mma, dim3((unsigned)(3 * tp.mtiles), (unsigned)(ma.nkr * tp.nbn), 1), dim3(128),
+      int rc = launch_chain(k_count_mma, dim3((unsigned)tp.mtiles, (unsigned)(ma.nkr * tp.nbn), 1), dim3(256),
                             (size_t)smem, s2, win ? at : nullptr, ma);
       if (rc) return rc;
       P.stop(Prof::COUNT_CONTRACT);
@@ -1879,7 +1917,7 @@ int launch_prep8(const gt_train_cfg& c, const uint64_t* features, const uint64_t
   lc.stream = s;
   cudaLaunchAttribute at[1];
   lc.attrs = at;
-  lc.numAttrs = l2_window_attr(pa.B8, 6ull * tp.nbn * pa.nkb * tp.BB, at) ? 1 : 0;
+  lc.numAttrs = l2_window_attr(pa.B8, 3ull * tp.nbn * pa.nkb * tp.BB, at) ? 1 : 0;
   GT_CUDA_CHECK(cudaLaunchKernelEx(&lc, k_prep8, pa));
   GT_LAUNCH_CHECK("k_prep8");
   return GT_OK;
@@ -1983,6 +2021,25 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
   k_init<<<1, 128, 0, s>>>(f[0], gam[0], cst[0], 1, 3 * cols, (int)cols, c.nf);
   GT_LAUNCH_CHECK("k_init");
   P.count_launch();
+  // the count reshare sums of every level (data-independent): beside the
+  // prologue, joined before the first count
+  const int alpha_mode = c.count_reshare == 0 ? 1 : (c.sample_base == 0 ? 2 : 0);
+  bool alpha_forked = false;
+  if (alpha_tab_words(c) && alpha_mode && N) {
+    cudaStream_t as = s;
+    if (!prof && !no_side) {
+      int rc = stream_after(side->st, s, side->ev[15]);
+      if (rc) return rc;
+      as = side->st;
+      alpha_forked = true;
+    }
+    const uint32_t cells = (uint32_t)(alpha_tab_words(c) / 3);
+    k_alpha_tape<<<(cells + 255) / 256, 256, 0, as>>>(ws + L.alphatab, cells, c.nf, K, alpha_mode == 2 ? 1 : 0,
+                                                      c.sample_base, c.sample_base + N);
+    GT_LAUNCH_CHECK("k_alpha_tape");
+    P.count_launch();
+    if (alpha_forked) GT_CUDA_CHECK(cudaEventRecord(side->ev[15], side->st));
+  }
   // the division randomness of every level is data-independent: draw it all now
   const uint64_t tape_words = div_tape_words(c);
   bool tape_forked = false;  // joined before the first heuristic
@@ -2047,7 +2104,12 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
   }
   // the count of one level over the samples [lo, hi)
   auto count_range = [&](int level, int fcur, uint64_t lo, uint64_t hi) -> int {
+    if (alpha_forked) {
+      GT_CUDA_CHECK(cudaStreamWaitEvent(s, side->ev[15], 0));
+      alpha_forked = false;
+    }
     CountLaunch cl{};
+    cl.alpha_tab = alpha_tab_words(c) ? ws + L.alphatab + 3ull * ((1ull << level) - 1) * W : nullptr;
     cl.midx = midx;
     cl.f = f[fcur];
     cl.cols = colm;
@@ -2064,7 +2126,7 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
     cl.level = level;
     return c.count_engine == 0
                ? launch_count_tc(cl, (const uint8_t*)(ws + L.cols8), tc_la8_blocks(N, c.nf, c.depth),
-                                 c.count_reshare == 0 ? 1 : (c.sample_base == 0 ? 2 : 0), c.sample_base,
+                                 alpha_mode, c.sample_base,
                                  c.sample_base + N, s, (prof || !count_overlap) ? nullptr : side, num_sms, P, lo, hi)
                : launch_count(cl, s, num_sms, P);
   };
