@@ -1521,6 +1521,8 @@ int launch_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint6
       best = G;
     }
   }
+  static const int forced = getenv("GT_PART_G") ? atoi(getenv("GT_PART_G")) : 0;  // A/B experiments
+  if (forced == 2 || forced == 4 || forced == 8 || forced == 16) best = forced;
   switch (best) {
     case 2: return launch_partition_g<2>(X, midx, T, slots, m, nf, N, base, K, level, s, Sz, swords);
     case 4: return launch_partition_g<4>(X, midx, T, slots, m, nf, N, base, K, level, s, Sz, swords);
