@@ -499,14 +499,17 @@ def main():
                 "partition": partition_bytes(cnt, NF_C2, DEPTH_C2),
                 "prods": cnt * (24 * NF_C2 + 24 + 24 * NF_C2), "node_hc": 0, "node_finish": 0}
     kname = {"count_lanes": "k_count_lanes8", "count_contract": "k_count_mma", "partition": "k_partition",
-             "node_hc": "k_hc_div", "prods": "k_cols8", "node_finish": "k_node_finish"}
+             "node_hc": "k_hc_div", "prods": "k_prep8", "node_finish": "k_node_finish"}
     alg = bytes_of[dom] * args.steps
     achieved = alg / (prof_tot[dom] / 1e3) / 1e9 if prof_tot[dom] > 0 else 0.0
     nlaunch = max(1, prof_n[dom])
     traffic = _traffic(kname.get(dom, dom))
     # integer-ALU roof: Philox blocks the dominant kernel draws vs the measured Philox peak
-    blocks = {"count_lanes": sum(cnt * (1 << h) * 6 for h in range(DEPTH_C2)),
-              "partition": sum(cnt * ((1 << (h - 1)) + NF_C2) * 6 for h in range(1, DEPTH_C2))}.get(dom)
+    # (randomness schedule v2: a pair of eq lanes draws 2 x 3 dealer blocks + 3 shared pair blocks;
+    # each lookup adds 2 x 3 telescoped reshare words per index)
+    blocks = {"count_lanes": sum(((cnt + 1) // 2) * (1 << h) * 9 for h in range(DEPTH_C2)),
+              "partition": sum(cnt * ((((1 << (h - 1)) + 1) // 2 + (NF_C2 + 1) // 2) * 9 + 12)
+                               for h in range(1, DEPTH_C2))}.get(dom)
     alu = None
     if blocks:
         alu = {"bound": "int-alu (Philox4x32-10 blocks)", "achieved_blocks_per_s": blocks * args.steps / (prof_tot[dom] / 1e3),
