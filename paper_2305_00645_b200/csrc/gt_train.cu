@@ -17,6 +17,7 @@
 // Every lane's randomness is keyed by (op, sub, field, global lane), so the
 // shares produced are independent of sharding and of launch geometry.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <utility>
 #include <vector>
@@ -1454,7 +1455,12 @@ int launch_chain(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cud
   }
   lc.attrs = at;
   lc.numAttrs = (unsigned)na;
-  GT_CUDA_CHECK(cudaLaunchKernelEx(&lc, kern, args...));
+  const cudaError_t e = cudaLaunchKernelEx(&lc, kern, args...);
+  if (e != cudaSuccess) {
+    static thread_local char what[160];
+    snprintf(what, sizeof what, "chain launch grid (%u,%u) block %u smem %zu", grid.x, grid.y, block.x, smem);
+    return fail_cuda(e, what);
+  }
   return GT_OK;
 }
 
@@ -1468,6 +1474,7 @@ int launch_node_hc(const NodeArgs& na, cudaStream_t s, bool fuse_post) {
   const int cols = 2 * na.nf;
   const int pre_smem = (int)sizeof(uint64_t) * ((9 * cols + 1) & ~1) + (int)sizeof(W2) * node_tape_plan(na.nf).spl;
   const unsigned gy = (na.last || na.co_out) ? 1u : (unsigned)(1 + na.nf);
+  GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_pre<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, pre_smem));
   int rc = launch_chain(k_hc_pre<SL>, dim3(na.n_h, gy), dim3(64), (size_t)pre_smem, s, nullptr, na);
   if (rc) return rc;
   GT_LAUNCH_CHECK("k_hc_pre");
@@ -1476,15 +1483,14 @@ int launch_node_hc(const NodeArgs& na, cudaStream_t s, bool fuse_post) {
   const int per_warp = (int)sizeof(W2) * (na.divtape ? div_tape_blocks<SL>(na.d) : division_tape_blocks<SL>(na.d));
   const int wpc = std::max(1, std::min(DIV_WARPS, (200 * 1024) / per_warp));
   const int div_smem = per_warp * wpc;
-  if (div_smem > 48 * 1024)
-    GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_div<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, div_smem));
+  GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_div<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, div_smem));
   rc = launch_chain(k_hc_div<SL>, dim3((unsigned)((lanes + wpc - 1) / wpc)), dim3(32 * wpc), (size_t)div_smem, s,
                     nullptr, na);
   if (rc) return rc;
   GT_LAUNCH_CHECK("k_hc_div");
   if (fuse_post) return GT_OK;  // k_hc_post_finish runs it with the split
   const int psm = post_smem_bytes<SL>(na);
-  if (psm > 48 * 1024) GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_post<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm));
+  GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_post<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm));
   k_hc_post<SL><<<na.n_h, 256, psm, s>>>(na);
   GT_LAUNCH_CHECK("k_hc_post");
   return GT_OK;
@@ -2312,7 +2318,7 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
     P.start();
     if (fuse) {
       const int psm = c.score_width == 32 ? post_smem_bytes<32>(na) : post_smem_bytes<64>(na);
-      if (psm > 48 * 1024) {
+      {  // always opt in: the kernel's static shared memory counts against the 48 KB default
         if (c.score_width == 32)
           GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_post_finish<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm));
         else
