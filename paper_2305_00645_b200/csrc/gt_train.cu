@@ -430,6 +430,7 @@ struct NodeArgs {
   const W2* nodetape;         // precomputed node-chain blocks of this level's nodes (or null)
   const W2* feattape;         // precomputed prologue feature blocks of this level (or null)
   int n_h, nf, level, last, shift, tau, ts;
+  int fuse_div;               // the division runs in k_hc_pre's feature CTAs (needs divtape)
   DivParams d;
   Keys K;
 };
@@ -612,7 +613,7 @@ __global__ void __launch_bounds__(256) k_feat_tape(W2* tape, uint32_t total, int
 }
 
 template <int SL>
-__device__ __forceinline__ void hc_pre_feature(const NodeArgs& a, int n, int fi, const Keys& K) {
+__device__ __forceinline__ void hc_pre_feature(const NodeArgs& a, int n, int fi, const Keys& K, uint64_t (*pq)[2][3]) {
   constexpr uint64_t MS = Ring<SL>::M;
   constexpr int TB = TruncRand<64>::BLOCKS;
   constexpr int NB = FEAT_BLOCKS;
@@ -688,8 +689,13 @@ __device__ __forceinline__ void hc_pre_feature(const NodeArgs& a, int n, int fi,
     const B3 qz = eq_arith<SL>(q, t[0].a, t[0].b, t[1].a, Zw);
     const A3 qsv = add<SL>(q, b2a_arith<SL>(qz, t[5].a, t[5].b, t[6].a));
     const uint64_t lane = (uint64_t)n * cols + 2 * fi + wl;
-    st3s(a.dv, lanes, lane, p);
-    st3s(a.dv + 3 * lanes, lanes, lane, qsv);
+    if (pq) {  // the division runs in this CTA
+#pragma unroll
+      for (int c = 0; c < 3; ++c) pq[wl][0][c] = p.v[c], pq[wl][1][c] = qsv.v[c];
+    } else {
+      st3s(a.dv, lanes, lane, p);
+      st3s(a.dv + 3 * lanes, lanes, lane, qsv);
+    }
   }
   hc_ts_at(64 + 8 * a.level + 5, tsw);
 }
@@ -700,7 +706,35 @@ __global__ void __launch_bounds__(64) k_hc_pre(NodeArgs a) {
   if (blockIdx.y > 0) {  // the feature warp draws with lane-dependent keys: stage them in smem
     __shared__ Keys ks;
     const Keys& Ks = keys_smem(a.K, ks);
-    if (threadIdx.x < 32) hc_pre_feature<SL>(a, n, (int)blockIdx.y - 1, Ks);
+    const int fi = (int)blockIdx.y - 1, warp = threadIdx.x >> 5;
+    if (!a.fuse_div) {
+      if (warp == 0) hc_pre_feature<SL>(a, n, fi, Ks, nullptr);
+      return;
+    }
+    // fused division (train.py:382): warp j divides column 2fi + j from its
+    // precomputed lane tape, bulk-copied before the wait for the contraction
+    extern __shared__ __align__(128) W2 dts[];  // [2][div_tape_blocks]
+    __shared__ __align__(8) uint64_t dbar[2];
+    __shared__ uint64_t pq[2][2][3];
+    const int TB = div_tape_blocks<SL>(a.d);
+    const uint64_t cols = 2 * (uint64_t)a.nf, lanes = (uint64_t)a.n_h * cols;
+    const uint64_t li = (uint64_t)n * cols + 2 * fi + warp;
+    W2* ts = dts + (size_t)warp * TB;
+    if ((threadIdx.x & 31) == 0) {
+      mbar_init(&dbar[warp], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&dbar[warp], (uint32_t)(TB * sizeof(W2)));
+      bulk_g2s(ts, a.divtape + li * (uint64_t)TB, (uint32_t)(TB * sizeof(W2)), &dbar[warp]);
+    }
+    if (warp == 0) hc_pre_feature<SL>(a, n, fi, Ks, pq);
+    __syncthreads();  // P, qsafe of both columns (warp 0 waited for the predecessor)
+    const bool tsd = a.ts && li == 0 && (threadIdx.x & 31) == 0;
+    hc_ts_at(64 + 8 * a.level + 6, tsd);
+    mbar_wait(&dbar[warp], 0);
+    const A3 t = division_warp_staged<SL>(ts, a3(pq[warp][0][0], pq[warp][0][1], pq[warp][0][2]),
+                                          a3(pq[warp][1][0], pq[warp][1][1], pq[warp][1][2]), a.d);
+    if ((threadIdx.x & 31) == 0) st3s(a.dv + 6 * lanes, lanes, li, t);
+    hc_ts_at(64 + 8 * a.level + 7, tsd);
     return;
   }
   // uniform-key chains read the round keys as constant-bank operands
@@ -1469,25 +1503,37 @@ int post_smem_bytes(const NodeArgs& na) {
   return (int)sizeof(uint64_t) * post_scratch_words(na.nf) + (int)sizeof(W2) * post_tape_blocks<SL>(na.nf);
 }
 
+// The division runs inside k_hc_pre's feature CTAs when its lane tapes exist
+// (GT_NO_FUSED_DIV=1: separate k_hc_div launch, A/B experiments).
+bool hc_div_fused(const NodeArgs& na) {
+  static const bool no_fuse = getenv("GT_NO_FUSED_DIV") != nullptr;
+  return !no_fuse && !na.last && !na.co_out && na.divtape != nullptr;
+}
+
 template <int SL>
 int launch_node_hc(const NodeArgs& na, cudaStream_t s, bool fuse_post) {
   const int cols = 2 * na.nf;
   const int pre_smem = (int)sizeof(uint64_t) * ((9 * cols + 1) & ~1) + (int)sizeof(W2) * node_tape_plan(na.nf).spl;
   const unsigned gy = (na.last || na.co_out) ? 1u : (unsigned)(1 + na.nf);
-  GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_pre<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, pre_smem));
-  int rc = launch_chain(k_hc_pre<SL>, dim3(na.n_h, gy), dim3(64), (size_t)pre_smem, s, nullptr, na);
+  NodeArgs nf_args = na;
+  nf_args.fuse_div = hc_div_fused(na);
+  const int smem = nf_args.fuse_div ? std::max(pre_smem, 2 * (int)sizeof(W2) * div_tape_blocks<SL>(na.d)) : pre_smem;
+  GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_pre<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int rc = launch_chain(k_hc_pre<SL>, dim3(na.n_h, gy), dim3(64), (size_t)smem, s, nullptr, nf_args);
   if (rc) return rc;
   GT_LAUNCH_CHECK("k_hc_pre");
   if (na.last || na.co_out) return GT_OK;
-  const uint64_t lanes = (uint64_t)na.n_h * cols;
-  const int per_warp = (int)sizeof(W2) * (na.divtape ? div_tape_blocks<SL>(na.d) : division_tape_blocks<SL>(na.d));
-  const int wpc = std::max(1, std::min(DIV_WARPS, (200 * 1024) / per_warp));
-  const int div_smem = per_warp * wpc;
-  GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_div<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, div_smem));
-  rc = launch_chain(k_hc_div<SL>, dim3((unsigned)((lanes + wpc - 1) / wpc)), dim3(32 * wpc), (size_t)div_smem, s,
-                    nullptr, na);
-  if (rc) return rc;
-  GT_LAUNCH_CHECK("k_hc_div");
+  if (!nf_args.fuse_div) {
+    const uint64_t lanes = (uint64_t)na.n_h * cols;
+    const int per_warp = (int)sizeof(W2) * (na.divtape ? div_tape_blocks<SL>(na.d) : division_tape_blocks<SL>(na.d));
+    const int wpc = std::max(1, std::min(DIV_WARPS, (200 * 1024) / per_warp));
+    const int div_smem = per_warp * wpc;
+    GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_div<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, div_smem));
+    rc = launch_chain(k_hc_div<SL>, dim3((unsigned)((lanes + wpc - 1) / wpc)), dim3(32 * wpc), (size_t)div_smem, s,
+                      nullptr, na);
+    if (rc) return rc;
+    GT_LAUNCH_CHECK("k_hc_div");
+  }
   if (fuse_post) return GT_OK;  // k_hc_post_finish runs it with the split
   const int psm = post_smem_bytes<SL>(na);
   GT_CUDA_CHECK(cudaFuncSetAttribute(k_hc_post<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm));
@@ -2274,8 +2320,8 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
     int rc = c.score_width == 32 ? launch_node_hc<32>(na, s, fuse) : launch_node_hc<64>(na, s, fuse);
     if (rc) return rc;
     P.stop(Prof::NODE_HC);
-    if (!last && !tee) {  // k_hc_div (+ k_hc_post unless fused into the finish launch)
-      P.count_launch();
+    if (!last && !tee) {  // k_hc_div unless fused into k_hc_pre (+ k_hc_post unless fused into the finish launch)
+      if (!hc_div_fused(na)) P.count_launch();
       if (!fuse) P.count_launch();
     }
     if (!last && tee) {
