@@ -178,6 +178,7 @@ struct Lanes8Args {
   uint8_t* la8;
   uint64_t* S;  // [3][n_h][W+1]: the mask column s_mask[n] = sum_s la (train.py:334)
   int W;
+  const uint64_t* leafbits;  // is_leaf [3][n_h] precomputed by the partition launch, or null: draw per CTA
   uint64_t N, s0, cn, base, nkbc;  // nkbc = chunk capacity in K blocks
   int n_h, off, mtiles;
   Keys K;
@@ -196,7 +197,12 @@ __global__ void __launch_bounds__(256) k_count_lanes8(Lanes8Args a) {
   if (tid < 16) {
     const int n = mt * 16 + tid;
     B3 z = {{0, 0, 0}};
-    if (n < a.n_h) z = eqz<64>(a.K, a.op_leaf, 0, (uint64_t)n, add_pub<64>(ld3s(a.f, a.n_h, n), 0ull - F_LEAF));
+    if (n < a.n_h && a.leafbits) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) z.v[c] = a.leafbits[c * a.n_h + n];
+    } else if (n < a.n_h) {
+      z = eqz<64>(a.K, a.op_leaf, 0, (uint64_t)n, add_pub<64>(ld3s(a.f, a.n_h, n), 0ull - F_LEAF));
+    }
 #pragma unroll
     for (int c = 0; c < 3; ++c) leaf[c][tid] = z.v[c] & 1ull;
   }

@@ -89,16 +89,34 @@ __global__ void k_prods(const uint64_t* X, const uint64_t* Y, uint64_t* cols, ui
 // partition
 // ---------------------------------------------------------------------------
 
+// Level-start side work the partition launch carries (no extra launch on the
+// chain): zero the level's count sums, and is_leaf = eq(F, LEAF) of the
+// level's nodes (train.py:320) for the lane kernel.
+struct PartAux {
+  uint64_t* S;
+  uint64_t swords;
+  uint64_t* leaf;      // [3][n_h] bits, or null
+  const uint64_t* f;   // [3][n_h] node types of the level
+  int n_h;
+  uint32_t op_leaf;
+};
+
 template <int G>
 __global__ void k_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint64_t slots, int m, int nf,
-                            uint64_t N, uint64_t base, Keys K, uint32_t op_oaa, uint32_t op_row, uint64_t* Sz,
-                            uint64_t swords) {
+                            uint64_t N, uint64_t base, Keys K, uint32_t op_oaa, uint32_t op_row, PartAux aux) {
   extern __shared__ uint64_t tab[];  // [3][m] level h-1 payload table
   pdl_wait();
   pdl_trigger();
   // zero this level's count sums (the previous level's heuristic has read them)
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < swords; i += (uint64_t)gridDim.x * blockDim.x)
-    Sz[i] = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < aux.swords;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    aux.S[i] = 0;
+  if (aux.leaf && blockIdx.x == gridDim.x - 1)
+    for (int n = threadIdx.x; n < aux.n_h; n += blockDim.x) {
+      const B3 z = eqz<64>(K, aux.op_leaf, 0, (uint64_t)n, add_pub<64>(ld3s(aux.f, aux.n_h, n), 0ull - F_LEAF));
+#pragma unroll
+      for (int c = 0; c < 3; ++c) aux.leaf[c * aux.n_h + n] = z.v[c] & 1ull;
+    }
   for (int i = threadIdx.x; i < 3 * m; i += blockDim.x) tab[i] = T[(uint64_t)(i / m) * slots + (m - 1) + (i % m)];
   __syncthreads();
   const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1544,15 +1562,14 @@ int launch_node_hc(const NodeArgs& na, cudaStream_t s, bool fuse_post) {
 
 template <int G>
 int launch_partition_g(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint64_t slots, int m, int nf,
-                       uint64_t N, uint64_t base, const Keys& K, int level, cudaStream_t s, uint64_t* Sz,
-                       uint64_t swords) {
+                       uint64_t N, uint64_t base, const Keys& K, int level, cudaStream_t s, const PartAux& aux) {
   constexpr int TPB = 256;
   const uint64_t threads = N * G;
   const unsigned grid = (unsigned)((threads + TPB - 1) / TPB);
   const int smem = 3 * m * (int)sizeof(uint64_t);
   if (smem > 48 * 1024) GT_CUDA_CHECK(cudaFuncSetAttribute(k_partition<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int rc = launch_chain(k_partition<G>, dim3(grid), dim3(TPB), (size_t)smem, s, nullptr, X, midx, T, slots, m, nf, N,
-                        base, K, op_id(level, SITE_PART_OAA), op_id(level, SITE_PART_ROW), Sz, swords);
+                        base, K, op_id(level, SITE_PART_OAA), op_id(level, SITE_PART_ROW), aux);
   if (rc) return rc;
   GT_LAUNCH_CHECK("k_partition");
   return GT_OK;
@@ -1561,8 +1578,7 @@ int launch_partition_g(const uint64_t* X, uint64_t* midx, const uint64_t* T, uin
 // G threads per sample: the fewest idle lane-slots (ceil(m/G) + ceil(nf/G)
 // rounds of G lanes) among the G that keep >= 4 resident warps per SMSP.
 int launch_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint64_t slots, int m, int nf, uint64_t N,
-                     uint64_t base, const Keys& K, int level, cudaStream_t s, int num_sms, uint64_t* Sz,
-                     uint64_t swords) {
+                     uint64_t base, const Keys& K, int level, cudaStream_t s, int num_sms, const PartAux& aux) {
   const uint64_t target = (uint64_t)num_sms * 512;
   int best = 16;
   uint64_t best_work = ~0ull;
@@ -1576,10 +1592,10 @@ int launch_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint6
   static const int forced = getenv("GT_PART_G") ? atoi(getenv("GT_PART_G")) : 0;  // A/B experiments
   if (forced == 2 || forced == 4 || forced == 8 || forced == 16) best = forced;
   switch (best) {
-    case 2: return launch_partition_g<2>(X, midx, T, slots, m, nf, N, base, K, level, s, Sz, swords);
-    case 4: return launch_partition_g<4>(X, midx, T, slots, m, nf, N, base, K, level, s, Sz, swords);
-    case 8: return launch_partition_g<8>(X, midx, T, slots, m, nf, N, base, K, level, s, Sz, swords);
-    default: return launch_partition_g<16>(X, midx, T, slots, m, nf, N, base, K, level, s, Sz, swords);
+    case 2: return launch_partition_g<2>(X, midx, T, slots, m, nf, N, base, K, level, s, aux);
+    case 4: return launch_partition_g<4>(X, midx, T, slots, m, nf, N, base, K, level, s, aux);
+    case 8: return launch_partition_g<8>(X, midx, T, slots, m, nf, N, base, K, level, s, aux);
+    default: return launch_partition_g<16>(X, midx, T, slots, m, nf, N, base, K, level, s, aux);
   }
 }
 
@@ -1699,6 +1715,7 @@ struct CountLaunch {
   Keys K;
   int level;
   const uint64_t* alpha_tab;  // the level's precomputed count reshare sums (tensor engine) or null
+  const uint64_t* leafbits;   // is_leaf bits [3][n_h] drawn by the level's partition launch, or null
 };
 
 // leaf + per chunk (lanes, contraction); returns the number of launches
@@ -1873,6 +1890,7 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
     la.op_cnt = op_id(c.level, SITE_COUNT);
     la.S = c.S;
     la.W = 2 * c.nf + 1;
+    la.leafbits = c.leafbits;
     P.start();
     {
       int rc = launch_chain(k_count_lanes8, dim3(nkb, (unsigned)tp.mtiles), dim3(256), 0, s, nullptr, la);
@@ -2164,6 +2182,7 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
     }
     CountLaunch cl{};
     cl.alpha_tab = alpha_tab_words(c) ? ws + L.alphatab + 3ull * ((1ull << level) - 1) * W : nullptr;
+    cl.leafbits = (level > 0 && N && c.count_engine == 0) ? ws + L.leaf : nullptr;
     cl.midx = midx;
     cl.f = f[fcur];
     cl.cols = colm;
@@ -2251,8 +2270,8 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
     const uint64_t swords = 3ull * n_h * (W + 1);
     if (level > 0 && N) {  // the partition also zeroes this level's count sums
       P.start();
-      int rc = launch_partition(features, midx, T, slots, n_h / 2, c.nf, N, c.sample_base, K, level, s, num_sms, S,
-                                swords);
+      PartAux aux{S, swords, c.count_engine == 0 ? ws + L.leaf : nullptr, f[cur], n_h, op_id(level, SITE_ISLEAF)};
+      int rc = launch_partition(features, midx, T, slots, n_h / 2, c.nf, N, c.sample_base, K, level, s, num_sms, aux);
       if (rc) return rc;
       P.stop(Prof::PARTITION);
     }
