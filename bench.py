@@ -267,8 +267,8 @@ def scale_c4(ctx, steps, warmup):
     tr = DeviceTrainer(cnt, nf, TrainConfig(depth=depth), n_total=n, sample_base=start, device=dev)
     cb = make_allreduce(tr) if world > 1 else None
     fn = (lambda: tr.run(X, Y, FL, keys, allreduce=cb))
-    if world == 1:
-        fn = tr.capture(X, Y, FL, keys)
+    if ctx["graphed"]:
+        fn = tr.capture(X, Y, FL, keys, allreduce=cb)
     t = _events_time(fn, steps, warmup, ctx["flush"], ctx["barrier"], ctx["stream"], ctx["max"])
     T, F = from_device(tr.T).sum(axis=0), from_device(tr.F).sum(axis=0)
     want_T, want_F = shadow.mpc_train(data, depth, fill)
@@ -376,7 +376,10 @@ def main():
         return tr.run(X, Y, FL, keys, allreduce=cb, profile=profile)
 
     # ---- device-resident timed region (value): CUDA-graph replay of whole trees ----
-    replay = tr.capture(X, Y, FL, keys) if world == 1 else None
+    # (N > 1: the NCCL count allreduce is captured with the kernels; GT_BENCH_EAGER=1 launches eagerly)
+    graphed = world == 1 or (dist.get_backend() == "nccl" and not os.environ.get("GT_BENCH_EAGER"))
+    ctx["graphed"] = graphed
+    replay = tr.capture(X, Y, FL, keys, allreduce=cb) if graphed else None
     run_tree = replay if replay is not None else step
     for _ in range(args.warmup):
         run_tree()
@@ -428,7 +431,7 @@ def main():
     tr_h = DeviceTrainer(cnt, NF_C2, TrainConfig(depth=DEPTH_C2), n_total=N_C2, sample_base=start, device=dev,
                          host_io=True)
     cb_h = make_allreduce(tr_h) if world > 1 else None
-    run_h = (tr_h.capture_host(Xp, Yp, Fp, Th, Fh, keys) if world == 1
+    run_h = (tr_h.capture_host(Xp, Yp, Fp, Th, Fh, keys, allreduce=cb_h) if graphed
              else (lambda: tr_h.run_host(Xp, Yp, Fp, Th, Fh, keys, allreduce=cb_h)))
     for i in range(args.warmup + args.steps):
         flush.zero_()
@@ -474,7 +477,8 @@ def main():
     tr_dot = DeviceTrainer(cnt, NF_C2, TrainConfig(depth=DEPTH_C2, count_reshare="dot"), n_total=N_C2,
                            sample_base=start, device=dev)
     cb_dot = make_allreduce(tr_dot) if world > 1 else None
-    run_dot = tr_dot.capture(X, Y, FL, keys) if world == 1 else (lambda: tr_dot.run(X, Y, FL, keys, allreduce=cb_dot))
+    run_dot = (tr_dot.capture(X, Y, FL, keys, allreduce=cb_dot) if graphed
+               else (lambda: tr_dot.run(X, Y, FL, keys, allreduce=cb_dot)))
     dot_s = _events_time(run_dot, args.steps, args.warmup, flush, barrier, stream, max_over_ranks)
     dot_ok = bool(np.array_equal(from_device(tr_dot.T).sum(axis=0), z["T"]) and
                   np.array_equal(from_device(tr_dot.F).sum(axis=0), z["F"]))
@@ -551,7 +555,8 @@ def main():
                      "algorithmic_bytes_per_launch": bytes_of[dom] / max(1, prof_n[dom] // args.steps),
                      "avg_launch_ms": prof_tot[dom] / nlaunch, "alu": alu, "classes": classes},
         "kernel_ms_per_step": {k: v / args.steps for k, v in prof_tot.items()},
-        "timing": ("value: CUDA-graph replay of the whole tree (1 GPU) / stream launches (N>1); "
+        "timing": ("value: CUDA-graph replay of the whole tree" + (" incl. the NCCL count allreduce" if world > 1 else "")
+                   + ("" if graphed else " [eager stream launches: GT_BENCH_EAGER / non-NCCL backend]") + "; "
                    "kernel_ms_per_step + roofline: separate pass of K steps with per-launch CUDA events"),
         "clocks": clocks,
         "secondary": {"metric": METRIC2, "value": N_C3 / inf_s, "unit": "instances/s", "ms_per_step": inf_s * 1e3,

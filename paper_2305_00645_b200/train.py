@@ -186,37 +186,40 @@ class DeviceTrainer:
         _native.check(rc)
         return int(d.value)
 
-    def capture_host(self, Xh, Yh, filler_h, T_h, F_h, keys):
-        """CUDA graph of one whole host-operand run (uploads, kernels, readback)."""
+    def capture_host(self, Xh, Yh, filler_h, T_h, F_h, keys, allreduce=None):
+        """CUDA graph of one whole host-operand run (uploads, kernels, the
+        sharded run's count allreduce if capturable, readback)."""
         torch = _native.require_cuda()
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(s):
-            self.run_host(Xh, Yh, filler_h, T_h, F_h, keys, stream=s)
+            self.run_host(Xh, Yh, filler_h, T_h, F_h, keys, stream=s, allreduce=allreduce)
         s.synchronize()
         torch.cuda.current_stream(self.device).wait_stream(s)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
-            self.run_host(Xh, Yh, filler_h, T_h, F_h, keys, stream=s)
-        self._graph_host_refs = (Xh, Yh, filler_h, T_h, F_h, keys)
+            self.run_host(Xh, Yh, filler_h, T_h, F_h, keys, stream=s, allreduce=allreduce)
+        self._graph_host_refs = (Xh, Yh, filler_h, T_h, F_h, keys, allreduce)
         return g.replay
 
-    def capture(self, X, Y, filler, keys):
-        """Capture one whole training run (every level's kernels) into a CUDA
-        graph; returns a callable that replays it on the current stream.
-        Fixed policy only (grow opens a stop bit on the host mid-run)."""
+    def capture(self, X, Y, filler, keys, allreduce=None):
+        """Capture one whole training run (every level's kernels, and the
+        per-level count allreduce of a sharded run when `allreduce` enqueues
+        a graph-capturable collective such as NCCL's) into a CUDA graph;
+        returns a callable that replays it on the current stream.  Fixed
+        policy only (grow opens a stop bit on the host mid-run)."""
         torch = _native.require_cuda()
         if self.cfg.policy == "grow" or self.cfg.heuristic == "tee":
             raise ValueError("grow / tee synchronise with the host per level; they cannot be captured")
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(s):
-            self.run(X, Y, filler, keys, stream=s)  # warm: sets kernel attributes outside capture
+            self.run(X, Y, filler, keys, stream=s, allreduce=allreduce)  # warm: kernel attributes outside capture
         torch.cuda.current_stream(self.device).wait_stream(s)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
-            self.run(X, Y, filler, keys, stream=s)
-        self._graph_refs = (X, Y, filler, keys)  # keep the captured buffers alive
+            self.run(X, Y, filler, keys, stream=s, allreduce=allreduce)
+        self._graph_refs = (X, Y, filler, keys, allreduce)  # keep the captured buffers alive
         return g.replay
 
 

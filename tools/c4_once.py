@@ -5,7 +5,7 @@ sys.argv = ["bench.py"]
 import torch
 import bench
 ctx = {"dev": torch.device("cuda", 0), "world": 1, "rank": 0, "flush": lambda: None, "barrier": lambda: None,
-       "stream": torch.cuda.current_stream()}
+       "stream": torch.cuda.current_stream(), "graphed": True, "max": lambda x: x}
 try:
     print(bench.scale_c4(ctx, 1, 1))
 except Exception as e:  # noqa: BLE001
