@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Secure batch inference (reference infer_batch, pkg/src/obtree/infer.py:91-106)
 // as ONE fused kernel: every query walks all H levels; level t fetches the
 // current slot's payload with an oblivious lookup over the 2^t level entries
@@ -58,7 +59,10 @@ __global__ void __launch_bounds__(256) k_walk(const uint64_t* tree, int depth, c
 template <int G>
 int launch_walk(const uint64_t* tree, int depth, const uint64_t* Q, uint64_t n, int nf, uint64_t base, uint64_t* out,
                 uint64_t* slot_out, const Keys& K, cudaStream_t s) {
-  constexpr int TPB = 256;
+  // 128-thread CTAs: finer residency granularity (96 registers per thread
+  // leave room for 5 such CTAs per SM vs 2 of 256), so a grid just above one
+  // wave of 256-thread CTAs (C3: 313) does not spill into a second wave
+  static const int TPB = getenv("GT_WALK_TPB") ? atoi(getenv("GT_WALK_TPB")) : 128;  // A/B experiments
   const int smem = 3 * ((1 << depth) - 1) * (int)sizeof(uint64_t);
   if (smem > 48 * 1024) GT_CUDA_CHECK(cudaFuncSetAttribute(k_walk<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const uint64_t threads = n * G;

@@ -1563,7 +1563,9 @@ int launch_node_hc(const NodeArgs& na, cudaStream_t s, bool fuse_post) {
 template <int G>
 int launch_partition_g(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint64_t slots, int m, int nf,
                        uint64_t N, uint64_t base, const Keys& K, int level, cudaStream_t s, const PartAux& aux) {
-  constexpr int TPB = 256;
+  // 128-thread CTAs: 96 registers per thread fit 5 per SM (20 warps) where
+  // 256-thread CTAs fit 2 (16 warps)
+  static const int TPB = getenv("GT_PART_TPB") ? atoi(getenv("GT_PART_TPB")) : 128;  // A/B experiments
   const uint64_t threads = N * G;
   const unsigned grid = (unsigned)((threads + TPB - 1) / TPB);
   const int smem = 3 * m * (int)sizeof(uint64_t);
