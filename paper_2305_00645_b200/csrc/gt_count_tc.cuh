@@ -184,7 +184,10 @@ struct Lanes8Args {
   Keys K;
   uint32_t op_cnt, op_leaf;
 };
-__global__ void __launch_bounds__(256) k_count_lanes8(Lanes8Args a) {
+#ifndef GT_LANES8_MINB
+#define GT_LANES8_MINB 1
+#endif
+__global__ void __launch_bounds__(256, GT_LANES8_MINB) k_count_lanes8(Lanes8Args a) {
   __shared__ uint64_t leaf[3][16];
   const int kb = blockIdx.x, mt = blockIdx.y, tid = threadIdx.x;
   pdl_wait();

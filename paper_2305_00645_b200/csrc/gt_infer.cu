@@ -94,7 +94,7 @@ extern "C" int gt_infer(int depth, const uint64_t* tree, const uint64_t* queries
   const uint64_t target = (uint64_t)sms * 512;
   int best = 32;
   uint64_t best_work = ~0ull;
-  for (int G = 4; G <= 32; G <<= 1) {
+  for (int G = 1; G <= 32; G <<= 1) {
     uint64_t rounds = 0;
     for (int t = 0; t < depth; ++t) rounds += (((1ull << t) + 1) / 2 + G - 1) / G + ((nf + 1) / 2 + G - 1) / G;
     const uint64_t work = rounds * G;
@@ -103,7 +103,11 @@ extern "C" int gt_infer(int depth, const uint64_t* tree, const uint64_t* queries
       best = G;
     }
   }
+  static const int forced = getenv("GT_WALK_G") ? atoi(getenv("GT_WALK_G")) : 0;  // A/B experiments
+  if (forced >= 1 && forced <= 32 && (forced & (forced - 1)) == 0) best = forced;
   switch (best) {
+    case 1: return launch_walk<1>(tree, depth, queries, n, (int)nf, instance_base, out, slot_out, K, s);
+    case 2: return launch_walk<2>(tree, depth, queries, n, (int)nf, instance_base, out, slot_out, K, s);
     case 4: return launch_walk<4>(tree, depth, queries, n, (int)nf, instance_base, out, slot_out, K, s);
     case 8: return launch_walk<8>(tree, depth, queries, n, (int)nf, instance_base, out, slot_out, K, s);
     case 16: return launch_walk<16>(tree, depth, queries, n, (int)nf, instance_base, out, slot_out, K, s);
