@@ -32,6 +32,9 @@ constexpr int TC_ABLK = TC_KB * 128;      // bytes of an A block: 128 rows (16 n
 constexpr int TC_MAX_KB_PER_CTA = 64;     // 3 products x 64 x 128 x 255^2 < 2^31
 constexpr int TC_TMEM_COLS = 512;         // three accumulators of N <= 160 columns
 
+// node groups per 16-sample chunk of the la planes: min(16, n_h)
+__host__ __device__ inline int tc_groups(int n_h) { return n_h < 16 ? n_h : 16; }
+
 struct TcPlan {
   int CW;      // sample columns W (the mask column is summed by the lane kernel)
   int nbn;     // column blocks
@@ -189,14 +192,15 @@ struct Lanes8Args {
 #endif
 __global__ void __launch_bounds__(256, GT_LANES8_MINB) k_count_lanes8(Lanes8Args a) {
   __shared__ uint64_t leaf[3][16];
-  const int kb = blockIdx.x, mt = blockIdx.y, tid = threadIdx.x;
+  const int mt = blockIdx.y, tid = threadIdx.x;
   pdl_wait();
   pdl_trigger();
-  // la8[mt][kbc][half 2][c 3][kc 4][g 16][p 8][16]: the three components of
-  // a 64-sample half block are one contiguous 24 KB run (one bulk copy for
-  // the contraction)
-  uint8_t* blk = a.la8 + ((uint64_t)mt * a.nkbc + kb) * (uint64_t)(3 * TC_ABLK);
-  const uint64_t cstride = TC_ABLK / 2;
+  // la8[mt][kbc][half 2][c 3][kc 4][g NG][p 8][16], NG = min(16, n_h) node
+  // groups: the three components of a 64-sample half block are one
+  // contiguous 1.5 NG KB run (one bulk copy for the contraction).  With
+  // NG < 16 a CTA covers 16 / NG K blocks.
+  const int NG = tc_groups(a.n_h), KPB = 16 / NG;
+  const uint64_t cstride = 512ull * NG;
   if (tid < 16) {
     const int n = mt * 16 + tid;
     B3 z = {{0, 0, 0}};
@@ -217,9 +221,13 @@ __global__ void __launch_bounds__(256, GT_LANES8_MINB) k_count_lanes8(Lanes8Args
   // odd thread limbs 4..7, one 32-bit word each.
   const bool odd = threadIdx.x & 1;
   for (int e = tid; e < 16 * (TC_KB / 2); e += blockDim.x) {
-    const int nn = e / (TC_KB / 2), s2 = (e % (TC_KB / 2)) * 2;
+    const int kbl = e / (NG * (TC_KB / 2)), r = e - kbl * NG * (TC_KB / 2);
+    const int nn = r / (TC_KB / 2), s2 = (r % (TC_KB / 2)) * 2;
+    const uint64_t kb = (uint64_t)blockIdx.x * KPB + kbl;
+    if (kb >= a.nkbc) break;  // warp-uniform (a warp's items share kbl)
+    uint8_t* blk = a.la8 + ((uint64_t)mt * a.nkbc + kb) * (3072ull * NG);
     const int n = mt * 16 + nn;
-    const uint64_t s = (uint64_t)kb * TC_KB + s2;
+    const uint64_t s = kb * TC_KB + s2;
     A3 l0 = a3(0, 0, 0), l1 = a3(0, 0, 0);
     if (n < a.n_h && s < a.cn) {
       const uint64_t gs = a.s0 + s;
@@ -237,7 +245,7 @@ __global__ void __launch_bounds__(256, GT_LANES8_MINB) k_count_lanes8(Lanes8Args
     {  // s_mask: the warp's 64 samples of node n, one atomic per component
       // (l1 of a pair past the chunk's end is padding: multiplied by zero
       // columns in the contraction, left out here)
-      const bool has1 = (uint64_t)kb * TC_KB + s2 + 1 < a.cn;
+      const bool has1 = kb * TC_KB + s2 + 1 < a.cn;
       A3 m = has1 ? add<64>(l0, l1) : l0;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1)
@@ -248,7 +256,7 @@ __global__ void __launch_bounds__(256, GT_LANES8_MINB) k_count_lanes8(Lanes8Args
         for (int c = 0; c < 3; ++c)
           atomicAdd((unsigned long long*)&a.S[((uint64_t)c * a.n_h + n) * (a.W + 1) + a.W], (unsigned long long)m.v[c]);
     }
-    const int o = (s2 >> 6) * (3 * TC_ABLK / 2) + ((((s2 >> 4) & 3) * 16 + nn) * 8) * 16 + ((s2 & ~3) & 15);
+    const int o = (s2 >> 6) * (1536 * NG) + ((((s2 >> 4) & 3) * NG + nn) * 8) * 16 + ((s2 & ~3) & 15);
     const int p0 = odd ? 4 : 0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -334,6 +342,11 @@ __global__ void __launch_bounds__(256, 1) k_count_mma(MmaArgs a) {
   const int T = kb1 > kb0 ? 2 * (int)(kb1 - kb0) : 0;  // half blocks
   const int HBX = a.N * (TC_KB / 2);                    // one component's x plane of a half block
   const int stage = TC_A_HB + 3 * HBX;
+  // la planes with NG node groups per 16-sample chunk (see k_count_lanes8):
+  // the UMMA still reads 16 groups (M = 128); rows of absent nodes read
+  // other chunks' bytes inside the stage and are never folded
+  const int NG = tc_groups(a.n_h);
+  const uint32_t AHB = 1536u * NG, ACS = 512u * NG, ALBO = 128u * NG;
   const int NS = (a.N + 31) & ~31;                      // accumulator column stride in TMEM
 
   if (warp == 0) {
@@ -363,8 +376,8 @@ __global__ void __launch_bounds__(256, 1) k_count_mma(MmaArgs a) {
       const int st = t % TC_MC_STAGES;
       const uint64_t kb = kb0 + (uint32_t)(t >> 1), h = t & 1;
       uint8_t* sb = smt + st * stage;
-      mbar_expect_tx(&full[st], (uint32_t)stage);
-      bulk_g2s(sb, a.la8 + (((uint64_t)mt * a.nkbc + kb) * 2 + h) * (uint64_t)TC_A_HB, (uint32_t)TC_A_HB, &full[st]);
+      mbar_expect_tx(&full[st], AHB + (uint32_t)(3 * HBX));
+      bulk_g2s(sb, a.la8 + (((uint64_t)mt * a.nkbc + kb) * 2 + h) * (uint64_t)AHB, AHB, &full[st]);
       bulk_g2s(sb + TC_A_HB, a.B8 + (((uint64_t)nb * a.nkb_total + a.kb_base + kb) * 2 + h) * (uint64_t)(3 * HBX),
                (uint32_t)(3 * HBX), &full[st]);
     };
@@ -378,17 +391,16 @@ __global__ void __launch_bounds__(256, 1) k_count_mma(MmaArgs a) {
       if (a.probe != 1)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          const uint32_t ao = j * 2 * (16 * 128), xo = j * 2 * (a.cpb * 128);
+          const uint32_t ao = j * 2 * ALBO, xo = j * 2 * (a.cpb * 128);
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             const int cn = (c + 1) % 3;
-            const uint32_t Ac = base + c * (TC_ABLK / 2) + ao, An = base + cn * (TC_ABLK / 2) + ao;
+            const uint32_t Ac = base + c * ACS + ao, An = base + cn * ACS + ao;
             const uint32_t Xc = base + TC_A_HB + c * HBX + xo, Xn = base + TC_A_HB + cn * HBX + xo;
             const uint32_t D = tmem + (uint32_t)(c * NS);
-            umma_i8(D, umma_desc(Ac, 16 * 128, 128), umma_desc(Xc, a.cpb * 128, 128), idesc,
-                    (t > 0 || j > 0) ? 1u : 0u);
-            umma_i8(D, umma_desc(Ac, 16 * 128, 128), umma_desc(Xn, a.cpb * 128, 128), idesc, 1u);
-            umma_i8(D, umma_desc(An, 16 * 128, 128), umma_desc(Xc, a.cpb * 128, 128), idesc, 1u);
+            umma_i8(D, umma_desc(Ac, ALBO, 128), umma_desc(Xc, a.cpb * 128, 128), idesc, (t > 0 || j > 0) ? 1u : 0u);
+            umma_i8(D, umma_desc(Ac, ALBO, 128), umma_desc(Xn, a.cpb * 128, 128), idesc, 1u);
+            umma_i8(D, umma_desc(An, ALBO, 128), umma_desc(Xc, a.cpb * 128, 128), idesc, 1u);
           }
         }
       umma_commit(&empty[st]);
@@ -473,6 +485,164 @@ __global__ void __launch_bounds__(256, 1) k_count_mma(MmaArgs a) {
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS) : "memory");
+  }
+}
+
+// Shallow levels (n_h <= 8, at most 16 columns per block): the same contraction with the operand roles
+// swapped -- the x planes are the UMMA A operand (M = 128 rows = column x limb
+// of the block; rows past 8 cpb read neighbouring bytes and are never
+// folded) and the compact la planes the B operand (N = 8 n_h node x limb
+// columns, at least 16) -- so the UMMA floor max(M,128) N / 256 scales with
+// the level's nodes instead of a fixed 16-node tile:
+//     D_c[(w,q)][(n,p)] = sum_s x_c la_c + x_{c+1} la_c + x_c la_{c+1}
+// Epilogue: thread (column g, limb q) folds sum_p D << 8p per node, shifts by
+// 8q, and the 8 limb rows of a column are summed through shared memory.
+__global__ void __launch_bounds__(256, 1) k_count_mma_t(MmaArgs a) {
+  extern __shared__ __align__(1024) uint8_t smt[];
+  __shared__ __align__(8) uint64_t full[TC_MC_STAGES], empty[TC_MC_STAGES], done;
+  __shared__ uint32_t tmem_slot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nb = blockIdx.y % a.nbn, kr = blockIdx.y / a.nbn;
+  const uint32_t per = (a.nkb + a.nkr - 1) / a.nkr;
+  const uint32_t kb0 = kr * per, kb1 = min(a.nkb, kb0 + per);
+  const int T = kb1 > kb0 ? 2 * (int)(kb1 - kb0) : 0;
+  const int HBX = a.N * (TC_KB / 2);
+  const int stage = TC_A_HB + 3 * HBX;
+  const int NG = tc_groups(a.n_h);
+  const uint32_t AHB = 1536u * NG, ACS = 512u * NG, ALBO = 128u * NG;
+  const int NT = NG * 8 < 16 ? 16 : NG * 8;  // UMMA N
+  constexpr int TCOLS = 256;                  // three accumulators of <= 64 columns
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                 "r"(TCOLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 32) {
+    for (int i = 0; i < TC_MC_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+  pdl_wait();
+
+  if (tid == 0 && T > 0) {
+    const uint32_t idesc = (2u << 4) | ((uint32_t)(NT >> 3) << 17) | ((128u >> 4) << 24);
+    auto load = [&](int t) {
+      const int st = t % TC_MC_STAGES;
+      const uint64_t kb = kb0 + (uint32_t)(t >> 1), h = t & 1;
+      uint8_t* sb = smt + st * stage;
+      mbar_expect_tx(&full[st], AHB + (uint32_t)(3 * HBX));
+      bulk_g2s(sb, a.la8 + (kb * 2 + h) * (uint64_t)AHB, AHB, &full[st]);  // one M tile (n_h <= 8)
+      bulk_g2s(sb + TC_A_HB, a.B8 + (((uint64_t)nb * a.nkb_total + a.kb_base + kb) * 2 + h) * (uint64_t)(3 * HBX),
+               (uint32_t)(3 * HBX), &full[st]);
+    };
+    for (int t = 0; t < min(TC_MC_STAGES, T); ++t) load(t);
+    for (int t = 0; t < T; ++t) {
+      const int st = t % TC_MC_STAGES;
+      mbar_wait(&full[st], (uint32_t)((t / TC_MC_STAGES) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t base = smem_u32(smt + st * stage);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const uint32_t ao = j * 2 * ALBO, xo = j * 2 * (a.cpb * 128);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int cn = (c + 1) % 3;
+          const uint32_t Ac = base + c * ACS + ao, An = base + cn * ACS + ao;
+          const uint32_t Xc = base + TC_A_HB + c * HBX + xo, Xn = base + TC_A_HB + cn * HBX + xo;
+          const uint32_t D = tmem + (uint32_t)(c * 64);
+          umma_i8(D, umma_desc(Xc, a.cpb * 128, 128), umma_desc(Ac, ALBO, 128), idesc, (t > 0 || j > 0) ? 1u : 0u);
+          umma_i8(D, umma_desc(Xn, a.cpb * 128, 128), umma_desc(Ac, ALBO, 128), idesc, 1u);
+          umma_i8(D, umma_desc(Xc, a.cpb * 128, 128), umma_desc(An, ALBO, 128), idesc, 1u);
+        }
+      }
+      umma_commit(&empty[st]);
+      if (t >= 1 && t - 1 + TC_MC_STAGES < T) {
+        const int pst = (t - 1) % TC_MC_STAGES;
+        mbar_wait(&empty[pst], (uint32_t)(((t - 1) / TC_MC_STAGES) & 1));
+        load(t - 1 + TC_MC_STAGES);
+      }
+    }
+    umma_commit(&done);
+  }
+  __syncwarp();
+  if (T > 0) mbar_wait(&done, 0);
+  pdl_trigger();
+  if (T > 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    uint64_t* red = reinterpret_cast<uint64_t*>(smt);  // [3][NG][16 g][8 q]
+    if (warp < 4) {
+      const int r = warp * 32 + lane, g = r >> 3, q = r & 7;
+      for (int c = 0; c < 3; ++c) {
+        uint32_t d[64];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+            "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, "
+            "%36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, "
+            "%57, %58, %59, %60, %61, %62, %63}, [%64];"
+            : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
+              "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15]),
+              "=r"(d[16]), "=r"(d[17]), "=r"(d[18]), "=r"(d[19]), "=r"(d[20]), "=r"(d[21]), "=r"(d[22]),
+              "=r"(d[23]), "=r"(d[24]), "=r"(d[25]), "=r"(d[26]), "=r"(d[27]), "=r"(d[28]), "=r"(d[29]),
+              "=r"(d[30]), "=r"(d[31]), "=r"(d[32]), "=r"(d[33]), "=r"(d[34]), "=r"(d[35]), "=r"(d[36]),
+              "=r"(d[37]), "=r"(d[38]), "=r"(d[39]), "=r"(d[40]), "=r"(d[41]), "=r"(d[42]), "=r"(d[43]),
+              "=r"(d[44]), "=r"(d[45]), "=r"(d[46]), "=r"(d[47]), "=r"(d[48]), "=r"(d[49]), "=r"(d[50]),
+              "=r"(d[51]), "=r"(d[52]), "=r"(d[53]), "=r"(d[54]), "=r"(d[55]), "=r"(d[56]), "=r"(d[57]),
+              "=r"(d[58]), "=r"(d[59]), "=r"(d[60]), "=r"(d[61]), "=r"(d[62]), "=r"(d[63])
+            : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * 64)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+          if (n >= NG) break;
+          uint64_t v = 0;
+#pragma unroll
+          for (int p = 0; p < 8; ++p) v += (uint64_t)d[8 * n + p] << (8 * p);
+          red[((c * NG + n) * 16 + g) * 8 + q] = v << (8 * q);
+        }
+      }
+    }
+    __syncthreads();
+    const uint64_t Sstride = (uint64_t)a.n_h * (a.W + 1);
+    for (int cell = tid; cell < 3 * NG * 16; cell += blockDim.x) {
+      const int g = cell & 15, cn = cell >> 4, n = cn % NG, c = cn / NG;
+      const int wg = nb * a.cpb + g;
+      if (g >= a.cpb || n >= a.n_h || wg >= a.W) continue;
+      const uint4* rp = reinterpret_cast<const uint4*>(red + (uint64_t)cell * 8);
+      uint64_t v = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint4 x = rp[i];
+        v += ((uint64_t)x.y << 32 | x.x) + ((uint64_t)x.w << 32 | x.z);
+      }
+      if (a.alpha && kr == 0 && a.alpha_tab) {
+        v += a.alpha_tab[((uint64_t)n * 3 + c) * a.W + wg];
+      } else if (a.alpha && kr == 0) {
+        uint64_t F[2];
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {
+          const Key& key = a.K.pair[qq == 0 ? c : (c + 2) % 3];
+          F[qq] = a.alpha == 2 ? word(key, a.op_cnt, 4, (uint32_t)wg, (uint64_t)n)
+                               : word(key, a.op_cnt, 3, (uint32_t)wg, a.t1 * (uint64_t)a.n_h + n) -
+                                     word(key, a.op_cnt, 3, (uint32_t)wg, a.t0 * (uint64_t)a.n_h + n);
+        }
+        v += F[0] - F[1];
+      }
+      atomicAdd((unsigned long long*)&a.S[c * Sstride + (uint64_t)n * (a.W + 1) + wg], (unsigned long long)v);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS) : "memory");
   }
 }
 

@@ -1871,8 +1871,13 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
   }
   int k = 0;
   const uint64_t nkb_total = (c.N + TC_KB - 1) / TC_KB;
-  const int smem = TC_MC_STAGES * (TC_A_HB + 3 * tp.BB / 2);
-  GT_CUDA_CHECK(cudaFuncSetAttribute(k_count_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  // n_h <= 8: operand roles swapped (k_count_mma_t; its x-plane A operand
+  // reads up to 2 KB past a stage)
+  static const bool no_t = getenv("GT_NO_MMA_T") != nullptr;  // A/B experiments
+  const bool swapped = c.n_h <= 8 && tp.cpb <= 16 && !no_t;  // the x planes fill at most M = 128 rows
+  const int smem = TC_MC_STAGES * (TC_A_HB + 3 * tp.BB / 2) + (swapped ? 2048 : 0);
+  GT_CUDA_CHECK(cudaFuncSetAttribute(swapped ? k_count_mma_t : k_count_mma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     smem));
   for (uint64_t s0 = lo; s0 < hi; s0 += cap, ++k) {  // lo is a multiple of TC_KB
     const uint64_t cn = std::min<uint64_t>(cap, hi - s0);
     const uint32_t nkb = (uint32_t)((cn + TC_KB - 1) / TC_KB);
@@ -1898,7 +1903,9 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
     la.leafbits = c.leafbits;
     P.start();
     {
-      int rc = launch_chain(k_count_lanes8, dim3(nkb, (unsigned)tp.mtiles), dim3(256), 0, s, nullptr, la);
+      const unsigned kpb = 16u / (unsigned)tc_groups(c.n_h);  // K blocks per CTA (compact shallow levels)
+      int rc = launch_chain(k_count_lanes8, dim3((nkb + kpb - 1) / kpb, (unsigned)tp.mtiles), dim3(256), 0, s, nullptr,
+                            la);
       if (rc) return rc;
     }
     GT_LAUNCH_CHECK("k_count_lanes8");
@@ -1945,8 +1952,9 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
       cudaLaunchAttribute at[1];
       const bool win = l2_window_attr(B8, 3ull * tp.nbn * nkb_total * tp.BB, at);
       P.start();
-      int rc = launch_chain(k_count_mma, dim3((unsigned)tp.mtiles, (unsigned)(ma.nkr * tp.nbn), 1), dim3(256),
-                            (size_t)smem, s2, win ? at : nullptr, ma);
+      int rc = launch_chain(swapped ? k_count_mma_t : k_count_mma,
+                            dim3((unsigned)tp.mtiles, (unsigned)(ma.nkr * tp.nbn), 1), dim3(256), (size_t)smem, s2,
+                            win ? at : nullptr, ma);
       if (rc) return rc;
       P.stop(Prof::COUNT_CONTRACT);
     }
