@@ -75,3 +75,18 @@ def test_sharded_device_training_equals_single_device(tmp_path, n, world):
         z = np.load(tmp_path / f"r{r}.npz")
         assert int(z["d"]) == depth
         assert np.array_equal(z["T"], T1) and np.array_equal(z["F"], F1)
+
+
+def test_graph_captured_nccl_allreduce_equals_eager():
+    """The sharded run's count allreduce captured in the CUDA graph with the
+    level kernels (bench N > 1): a 1-rank NCCL group still issues real NCCL
+    calls; the replayed C2 tree must equal the eager one."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
+           "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tools", "capture_nccl_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "graph tree == eager tree: True" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
