@@ -1136,9 +1136,13 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n) {
   W2* tape = reinterpret_cast<W2*>(hitw + 4) + warp * ArgminPair<SL>::BLOCKS;
   hc_ts(1 + 8 * a.level, a.ts);
   int roff = 5 * nf;  // this round's first block in the staged tape
+  // ping-pong buffers: round r reads (vals, idxs) and writes (nvals, nidxs),
+  // then the two swap
+  uint64_t *cv = vals, *ci = idxs, *nv_ = nvals, *ni_ = nidxs;
   for (int r = 0; m > 1; ++r) {
     const int pairs = m / 2;
     const uint32_t base = SA + 2 + 5 * r;
+    uint64_t *vals = cv, *idxs = ci, *nvals = nv_, *nidxs = ni_;
     for (int p = warp; p < pairs; p += nwarps) {  // one warp per tournament pair
       const uint64_t lane = (uint64_t)n * nf + p;
       const A3 av = a3(vals[2 * p], vals[nf + 2 * p], vals[2 * nf + 2 * p]);
@@ -1167,18 +1171,12 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n) {
         nidxs[c * nf + pairs] = idxs[c * nf + m - 1];
       }
     __syncthreads();
-    const int nm = pairs + (m & 1);
-    for (int p = tid; p < nm; p += bd)
-      for (int c = 0; c < 3; ++c) {
-        vals[c * nf + p] = nvals[c * nf + p];
-        idxs[c * nf + p] = nidxs[c * nf + p];
-      }
-    __syncthreads();
     roff += ArgminPair<SL>::BLOCKS * pairs;
-    m = nm;
+    m = pairs + (m & 1);
+    cv = nvals, ci = nidxs, nv_ = vals, ni_ = idxs;
   }
   hc_ts(2 + 8 * a.level, a.ts);
-  const A3 sd = a3(idxs[0], idxs[nf], idxs[2 * nf]);
+  const A3 sd = a3(ci[0], ci[nf], ci[2 * nf]);
   // gamma &= ~[sd == k]                                     train.py:386-387
   const uint32_t SH = SA + 2 + 5 * 7;
   const W2* pb = pt ? pt + 5 * nf + post_rounds_blocks<SL>(nf) : nullptr;  // budget blocks
