@@ -468,7 +468,17 @@ def main():
         infer_device(Tt, DEPTH_C2, Q, keys, instance_base=qs, out=out)
         Oh.copy_(out, non_blocking=True)
 
-    inf_e2e_s = _events_time(inf_e2e, args.steps, args.warmup, flush, barrier, stream, max_over_ranks)
+    # one CUDA graph per e2e step (H2D of the queries, the walk, D2H of the
+    # predictions), as the training e2e: no host launch gaps inside the timed region
+    gs = torch.cuda.Stream(dev)
+    gs.wait_stream(stream)
+    with torch.cuda.stream(gs):
+        inf_e2e()
+    gs.synchronize()
+    g_inf = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_inf, stream=gs):
+        inf_e2e()
+    inf_e2e_s = _events_time(g_inf.replay, args.steps, args.warmup, flush, barrier, stream, max_over_ranks)
     preds_ok = True
     if world == 1:
         preds_ok = bool(np.array_equal(from_device(out).sum(axis=0), z["preds"]))
