@@ -547,6 +547,18 @@ def main():
         cpu_base = {"value": cs, "unit": "s/tree", "cores": oracle.num_threads(), "kind": "port",
                     "sample": "one full C2 tree (48842x13, depth 7) through oracle/gtree_oracle.c"}
     walk_alg = walk_bytes(qc, NF_C2, DEPTH_C2)
+    # inter-party messages of the protocol the kernels execute (the analytic
+    # transcript, ledger.py) beside the reference's (its lane_limit chunking)
+    from paper_2305_00645_b200 import ledger
+
+    def _msgs(ours, ref):
+        return {"rounds": ours.rounds, "bytes_per_party": ours.sent_by_party(1),
+                "reference_rounds": ref.rounds, "reference_bytes_per_party": ref.sent_by_party(1)}
+    messages = {"note": "3-party transcript per tree / per batch (party 1 sends; the parties are symmetric)",
+                "c2_train": _msgs(ledger.train_metrics(N_C2, NF_C2, DEPTH_C2, lane_limit=None),
+                                  ledger.train_metrics(N_C2, NF_C2, DEPTH_C2)),
+                "c3_infer": _msgs(ledger.infer_metrics(N_C3, NF_C2, DEPTH_C2, lane_limit=None),
+                                  ledger.infer_metrics(N_C3, NF_C2, DEPTH_C2))}
     line = {
         "metric": METRIC, "value": value_s, "unit": "s/tree", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": value_s * 1e3, "higher_is_better": False,
@@ -560,6 +572,7 @@ def main():
                    "c3_predictions_equal_reference": preds_ok},
         "e2e": {"value": e2e_s, "unit": "s/tree", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
+        "messages": messages,
         "roofline": {"bound": "hbm", "kernel": kname.get(dom, dom), "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": bytes_of[dom] / max(1, prof_n[dom] // args.steps),
