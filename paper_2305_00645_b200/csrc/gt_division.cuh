@@ -209,7 +209,8 @@ __device__ __forceinline__ A3 division_warp_tape(const W2* __restrict__ gt, cons
 // Division by one warp from its lane tape already staged in shared memory
 // (`ts` = ladder blocks then Newton blocks, div_tape_blocks<L>(d) of them).
 template <int L>
-__device__ __forceinline__ A3 division_warp_staged(const W2* ts, const A3& p, const A3& q, const DivParams& d) {
+__device__ __forceinline__ A3 division_warp_staged(const W2* ts, const A3& p, const A3& q, const DivParams& d,
+                                                   unsigned long long* ts_out = nullptr) {
   constexpr uint64_t M = Ring<L>::M;
   constexpr int LS = DivTape<L>::LADDER_STEP, LB = LtRand<L>::BLOCKS;
   const int wl = threadIdx.x & 31;
@@ -226,6 +227,11 @@ __device__ __forceinline__ A3 division_warp_staged(const W2* ts, const A3& p, co
 #pragma unroll
     for (int i = 0; i < 3; ++i) acc.v[i] = (acc.v[i] + __shfl_xor_sync(0xffffffffu, acc.v[i], o)) & M;
   const A3 v = rsub_pub<L>(1ull << (d.bound - 1), acc);
+  if (ts_out) {  // diagnostics (GT_HC_TIMING): ladder done
+    unsigned long long tt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+    *ts_out = tt;
+  }
   return newton_from_tape<L>(p, q, v, d, ts + nl * LS);
 }
 

@@ -750,7 +750,8 @@ __global__ void __launch_bounds__(64) k_hc_pre(NodeArgs a) {
     hc_ts_at(64 + 8 * a.level + 6, tsd);
     mbar_wait(&dbar[warp], 0);
     const A3 t = division_warp_staged<SL>(ts, a3(pq[warp][0][0], pq[warp][0][1], pq[warp][0][2]),
-                                          a3(pq[warp][1][0], pq[warp][1][1], pq[warp][1][2]), a.d);
+                                          a3(pq[warp][1][0], pq[warp][1][1], pq[warp][1][2]), a.d,
+                                          tsd ? &g_hc_ts[8 * a.level + 7] : nullptr);
     if ((threadIdx.x & 31) == 0) st3s(a.dv + 6 * lanes, lanes, li, t);
     hc_ts_at(64 + 8 * a.level + 7, tsd);
     return;

@@ -30,4 +30,4 @@ for lv in range(bench.DEPTH_C2 - 1):
     t0 = q[0]
     r = lambda v: (v - t0) / 1e3
     print(f"level {lv}: ctrl {r(q[1]):.2f}/{r(q[2]):.2f}  feat {r(q[3]):.2f}/{r(q[4]):.2f}/{r(q[5]):.2f}  "
-          f"div {r(q[6]):.2f}/{r(q[7]):.2f}  post {r(buf[8 * lv]):.2f}/{r(buf[8 * lv + 4]):.2f}")
+          f"div {r(q[6]):.2f}/ladder {r(buf[8 * lv + 7]):.2f}/{r(q[7]):.2f}  post {r(buf[8 * lv]):.2f}/{r(buf[8 * lv + 4]):.2f}")
