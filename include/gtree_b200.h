@@ -185,7 +185,10 @@ int gt_infer(int depth, const uint64_t* tree, const uint64_t* queries, uint64_t 
  * whose correlated randomness is drawn the same way. */
 int gt_diag_philox(uint32_t grid, uint32_t iters, uint64_t* out, void* stream);
 /* diagnostics: per-level heuristic phase timestamps (%globaltimer, ns) of the
-   last training run made with GT_HC_TIMING=1; slot 8*level + phase. */
+   last training run made with GT_HC_TIMING=1 (n <= 128): slots 8*level +
+   phase for the scores / argmin / budget / split phases and the division's
+   ladder end (phase 7), 64 + 8*level + phase for the prologue and the
+   division (tools/hc_timing.py). */
 int gt_diag_hc_timestamps(unsigned long long* out, int n);
 
 #ifdef __cplusplus
