@@ -175,37 +175,6 @@ __device__ __forceinline__ W2 div_tape_block(const Keys& K, uint32_t op, uint32_
   return W2{0, 0};
 }
 
-// Division by one warp from a precomputed lane tape `gt` (global): the
-// ladder's lt + b2a per lane straight from the tape, the Newton blocks
-// copied into the warp's shared-memory tape, then the serial chain.
-template <int L>
-__device__ __forceinline__ A3 division_warp_tape(const W2* __restrict__ gt, const A3& p, const A3& q,
-                                                 const DivParams& d, W2* tape) {
-  constexpr uint64_t M = Ring<L>::M;
-  constexpr int LS = DivTape<L>::LADDER_STEP, LB = LtRand<L>::BLOCKS;
-  const int wl = threadIdx.x & 31;
-  const int nl = d.bound - 1;
-  const int nb = newton_blocks<L>(d);
-  const W2* gn = gt + nl * LS;
-  for (int i = wl; i < nb; i += 32) tape[i] = gn[i];
-  A3 acc = a3(0, 0, 0);
-  for (int j = wl + 1; j <= nl; j += 32) {
-    const W2* b = gt + (j - 1) * LS;
-    const B3 below = lt_arith<L>(b, q, a3_const((1ull << j) & M));
-    const A3 t = b2a_arith<L>(bnot(below, 1ull), b[LB].a, b[LB].b, b[LB + 1].a);
-    acc = add<L>(acc, mul_pub<L>(t, 1ull << (d.bound - 1 - j)));
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int i = 0; i < 3; ++i) acc.v[i] = (acc.v[i] + __shfl_xor_sync(0xffffffffu, acc.v[i], o)) & M;
-  const A3 v = rsub_pub<L>(1ull << (d.bound - 1), acc);
-  __syncwarp();
-  const A3 out = newton_from_tape<L>(p, q, v, d, tape);
-  __syncwarp();
-  return out;
-}
-
 // Division by one warp from its lane tape already staged in shared memory
 // (`ts` = ladder blocks then Newton blocks, div_tape_blocks<L>(d) of them).
 template <int L>
