@@ -511,7 +511,8 @@ def main():
     bytes_of = {"count_lanes": count_lanes_bytes(cnt, NF_C2, DEPTH_C2),
                 "count_contract": count_contract_bytes(cnt, NF_C2, DEPTH_C2),
                 "partition": partition_bytes(cnt, NF_C2, DEPTH_C2),
-                "prods": cnt * (24 * NF_C2 + 24 + 24 * NF_C2), "node_hc": 0, "node_finish": 0}
+                # prologue: features + labels in, the W sample columns (x | x*y | y) out
+                "prods": cnt * (24 * (NF_C2 + 1) + 24 * (2 * NF_C2 + 1)), "node_hc": 0, "node_finish": 0}
     kname = {"count_lanes": "k_count_lanes8", "count_contract": "k_count_mma", "partition": "k_partition",
              "node_hc": "k_hc_div", "prods": "k_prep8", "node_finish": "k_node_finish"}
     alg = bytes_of[dom] * args.steps
