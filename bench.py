@@ -378,8 +378,21 @@ def main():
     # ---- device-resident timed region (value): CUDA-graph replay of whole trees ----
     # (N > 1: the NCCL count allreduce is captured with the kernels; GT_BENCH_EAGER=1 launches eagerly)
     graphed = world == 1 or (dist.get_backend() == "nccl" and not os.environ.get("GT_BENCH_EAGER"))
+    replay = None
+    if graphed:
+        try:
+            replay = tr.capture(X, Y, FL, keys, allreduce=cb)
+        except Exception as e:  # noqa: BLE001 - N > 1: fall back to eager launches on every rank
+            if world == 1:
+                raise
+            print(f"rank {rank}: graph capture with the NCCL allreduce failed ({e}); eager launches", file=sys.stderr)
+            graphed = False
+        if world > 1:  # every rank takes the same mode
+            flag = torch.tensor([1 if graphed else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if not bool(flag.item()):
+                graphed, replay = False, None
     ctx["graphed"] = graphed
-    replay = tr.capture(X, Y, FL, keys, allreduce=cb) if graphed else None
     run_tree = replay if replay is not None else step
     for _ in range(args.warmup):
         run_tree()
