@@ -2240,12 +2240,12 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
         for (int q = 0; q < Q; ++q) {
           const uint64_t hb_hi = std::min<uint64_t>(nhb, 2 * (nkb * (q + 1) / Q));
           const uint64_t lo = hb_lo * (TC_KB / 2), hi = std::min<uint64_t>(N, hb_hi * (TC_KB / 2));
-          for (int cc = 0; cc < 3; ++cc) {
-            GT_CUDA_CHECK(cudaMemcpyAsync((void*)(features + cc * N * nf + lo * nf), hin->X + cc * N * nf + lo * nf,
-                                          (hi - lo) * nf * sizeof(uint64_t), cudaMemcpyHostToDevice, side->cp));
-            GT_CUDA_CHECK(cudaMemcpyAsync((void*)(labels + cc * N + lo), hin->Y + cc * N + lo,
-                                          (hi - lo) * sizeof(uint64_t), cudaMemcpyHostToDevice, side->cp));
-          }
+          // the chunk's rows of the three components: one 2-D copy per operand
+          GT_CUDA_CHECK(cudaMemcpy2DAsync((void*)(features + lo * nf), N * nf * sizeof(uint64_t), hin->X + lo * nf,
+                                          N * nf * sizeof(uint64_t), (hi - lo) * nf * sizeof(uint64_t), 3,
+                                          cudaMemcpyHostToDevice, side->cp));
+          GT_CUDA_CHECK(cudaMemcpy2DAsync((void*)(labels + lo), N * sizeof(uint64_t), hin->Y + lo, N * sizeof(uint64_t),
+                                          (hi - lo) * sizeof(uint64_t), 3, cudaMemcpyHostToDevice, side->cp));
           GT_CUDA_CHECK(cudaEventRecord(side->ev[9 + (q % 6)], side->cp));
           GT_CUDA_CHECK(cudaStreamWaitEvent(s, side->ev[9 + (q % 6)], 0));
           rc = launch_prep8(c, features, labels, ws, L, K, hb_lo, hb_hi, s);

@@ -1,0 +1,3 @@
+for q in 2 3 4 2 3 4; do
+  GT_HOST_CHUNKS=$q timeout 300 python bench.py --no-cpu-baseline --no-scale --steps 20 2>/dev/null | tail -1 | python -c "import json,sys; l=json.loads(sys.stdin.read()); print('chunks $q', round(l['value']*1e3,4), 'e2e', round(l['e2e']['value']*1e3,4), l['parity']['e2e_tree_equals_reference'])"
+done
