@@ -2096,7 +2096,10 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
   uint64_t *cst[2] = {ws + L.cst[0], ws + L.cst[1]}, *ceff[2] = {ws + L.ceff[0], ws + L.ceff[1]};
   int cur = 0;
 
-  if (hin)
+  // host filler: on the copy stream ahead of the sample chunks when they are
+  // streamed (the chunk joins order it before the first split), else here
+  const bool host_chunks = hin && c.count_engine == 0 && N;
+  if (hin && !host_chunks)
     GT_CUDA_CHECK(cudaMemcpyAsync((void*)filler, hin->fill, slots * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
   GT_CUDA_CHECK(cudaMemsetAsync(T, 0, 3 * slots * sizeof(uint64_t), s));
   GT_CUDA_CHECK(cudaMemsetAsync(F, 0, 3 * slots * sizeof(uint64_t), s));
@@ -2229,11 +2232,13 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
         // of a chunk runs as soon as its planes exist
         const uint64_t nkb = (N + TC_KB - 1) / TC_KB;
         // two chunks measured best on C2 (1 / 2 / 3 / 4 / 8: e2e 1.242 / 1.221 / 1.231 / 1.257 / 1.338 ms):
-        // each chunk costs six copies and a count launch pair
+        // (measured with six copies per chunk; now two 2-D copies, 2 chunks still best: 1.016 / 1.019 / 1.027 ms for 2 / 3 / 4)
         static const int Qenv = getenv("GT_HOST_CHUNKS") ? atoi(getenv("GT_HOST_CHUNKS")) : 2;
         const int Q = (int)std::min<uint64_t>((uint64_t)std::max(1, Qenv), nkb);
         int rc = stream_after(side->cp, s, side->ev[8]);
         if (rc) return rc;
+        GT_CUDA_CHECK(cudaMemcpyAsync((void*)filler, hin->fill, slots * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                      side->cp));
         const bool count0 = !prof && c.heuristic == 0;
         if (count0) GT_CUDA_CHECK(cudaMemsetAsync(S, 0, 3ull * 1 * (W + 1) * sizeof(uint64_t), s));
         uint64_t hb_lo = 0;
