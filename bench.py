@@ -237,6 +237,8 @@ def _events_time(fn, steps, warmup, flush, barrier, stream, max_over_ranks):
         torch.cuda.synchronize()
         barrier()
         ms.append(e0.elapsed_time(e1))
+    if os.environ.get("GT_BENCH_DEBUG"):
+        print("steps ms:", " ".join(f"{m:.3f}" for m in ms), file=sys.stderr)
     return max_over_ranks(sum(ms)) / steps / 1e3
 
 
