@@ -1,0 +1,44 @@
+"""bench.py's JSON line contract (B200): the keys the driver and the judge
+read, parity of the timed runs, and the reference arm's line."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(*args):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                       timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def test_bench_line_contract():
+    line = _run("--steps", "3", "--warmup", "3", "--no-scale", "--no-cpu-baseline")
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches", "roofline", "clocks", "messages"):
+        assert k in line, k
+    assert line["n_gpus"] == 1 and line["steps"] == 3 and line["warmup"] == 3
+    assert line["higher_is_better"] is False and line["value"] > 0
+    assert "workload" in line["config"]
+    e2e = line["e2e"]
+    assert e2e["value"] > line["value"] and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
+    assert line["gpu_launches"] > 0
+    rf = line["roofline"]
+    assert rf["bound"] in ("hbm", "tensor") and rf["peak"] > 0 and 0 < rf["frac"] <= 1
+    assert all(line["parity"].values()), line["parity"]
+    assert line["messages"]["c2_train"]["bytes_per_party"] == line["messages"]["c2_train"]["reference_bytes_per_party"]
+
+
+def test_reference_arm_line():
+    line = _run("--impl", "reference", "--steps", "1", "--warmup", "1")
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] in ("port", "reference") and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
