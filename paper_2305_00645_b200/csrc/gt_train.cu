@@ -1075,8 +1075,18 @@ __global__ void __launch_bounds__(256) k_post_tape(W2* tape, const uint64_t* __r
   tape[e] = word2(key < 0 ? ks.dealer : ks.pair[key], op_id(level, SITE_HC), sub, pidx, lane);
 }
 
+// What the fused post/split kernel takes over after the argmin: the budget
+// clear then runs beside the split chains (see k_hc_post_finish).
+struct PostOut {
+  A3 sd;
+  B3 gam;
+  const W2* pb;     // staged budget blocks (or null: draw live)
+  uint64_t* hitw;   // [3] shared-memory hit words, zeroed
+  uint32_t opH, SH;
+};
+
 template <int SL>
-__device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n) {
+__device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n, PostOut* out = nullptr) {
   extern __shared__ uint64_t sm[];
   constexpr uint64_t MS = Ring<SL>::M;
   const int tid = threadIdx.x, bd = blockDim.x;
@@ -1181,6 +1191,10 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n) {
   // gamma &= ~[sd == k]                                     train.py:386-387
   const uint32_t SH = SA + 2 + 5 * 7;
   const W2* pb = pt ? pt + 5 * nf + post_rounds_blocks<SL>(nf) : nullptr;  // budget blocks
+  if (out) {  // the caller runs the budget clear beside the split
+    out->sd = sd, out->gam = gam, out->pb = pb, out->hitw = hitw, out->opH = opH, out->SH = SH;
+    return;
+  }
   for (int f = tid; f < nf; f += bd) {
     B3 h;
     if (pb) {
@@ -1329,8 +1343,103 @@ __global__ void __launch_bounds__(128) k_node_finish(FinishArgs a) {
 
 // scores / argmin / budget clear, then split, in one launch per level (fixed
 // policy, mpc heuristic): the node's CTA continues from sd to its children
+// Budget clear (gamma &= ~[sd == k], train.py:386-387) on warps 0-1 while
+// warps 4-6 run the split's three independent chains (payload, child type,
+// child-counter condition, train.py:287-290); the children's gamma is stored
+// after the join.  Same gadgets and blocks as the sequential path.
+template <int SL>
+__device__ __forceinline__ void post_split_fused(const NodeArgs& na, const FinishArgs& a, int n, const PostOut& po) {
+  __shared__ uint64_t ca[3], ngs[3];
+  const int tid = threadIdx.x, bd = blockDim.x, warp = tid >> 5;
+  const int nf = a.nf, cols = 2 * nf, C3 = 3 * cols;
+  const uint64_t hs = (uint64_t)a.n_h, slot = hs - 1 + n, cs = 2 * hs;
+  const Keys& K = a.K;
+  const uint32_t op = op_id(a.level, SITE_SPLIT);
+  auto CE = [&](int e) { return ld3s(a.ceff, hs * C3, (uint64_t)n * C3 + e); };
+  const NodeTape NT = node_tape_plan(nf);
+  __shared__ __align__(128) W2 nsb[16 + 12 + 3 * 64 * 3];  // >= the split segment
+  __shared__ __align__(8) uint64_t nbar;
+  const W2* nt = a.nodetape ? stage_node_tape(a.nodetape + (uint64_t)n * NT.total + NT.spl, NT.lab - NT.spl, nsb, &nbar)
+                            : nullptr;
+  B3 ss;
+  for (int c = 0; c < 3; ++c) ss.v[c] = a.hc[(0 * 3 + c) * hs + n];
+  hc_ts(3 + 8 * a.level, a.ts);  // budget and split start together (slots 3, 5)
+  hc_ts(5 + 8 * a.level, a.ts);
+  if (warp < 2) {
+    for (int f = tid; f < nf; f += 64) {
+      B3 h;
+      if (po.pb) {
+        const W2* b = po.pb + 5 * f;
+        const uint64_t Zw[3] = {b[2].a, b[3].a, b[4].a};
+        h = eq_arith<64>(add_pub<64>(po.sd, 0ull - (uint64_t)f), b[0].a, b[0].b, b[1].a, Zw);
+      } else {
+        h = eqz<64>(K, po.opH, po.SH, (uint64_t)n * nf + f, add_pub<64>(po.sd, 0ull - (uint64_t)f));
+      }
+      for (int c = 0; c < 3; ++c)
+        atomicOr((unsigned long long*)&po.hitw[c], (unsigned long long)((h.v[c] & 1ull) << f));
+    }
+    asm volatile("bar.sync 2, 64;" ::: "memory");
+    if (tid == 0) {
+      B3 hw;
+      for (int c = 0; c < 3; ++c) hw.v[c] = po.hitw[c];
+      B3 ng;
+      if (po.pb) {
+        const W2* b = po.pb + 5 * nf;
+        const uint64_t Z[3] = {b[0].a & lowmask(nf), b[1].a & lowmask(nf), b[2].a & lowmask(nf)};
+        ng = and_z(po.gam, bnot(hw, lowmask(nf)), Z);
+      } else {
+        ng = and_gate(K, po.opH, po.SH + 1, 0, n, po.gam, bnot(hw, lowmask(nf)), lowmask(nf));
+      }
+      for (int c = 0; c < 3; ++c) {
+        na.hc[(1 * 3 + c) * hs + n] = po.sd.v[c];
+        na.hc[(3 * 3 + c) * hs + n] = ng.v[c];
+        ngs[c] = ng.v[c];
+      }
+    }
+  } else if (tid == 128) {  // payload T = is_int ? sd : filler        (train.py:287)
+    const uint64_t fl = a.filler[slot];
+    const A3 cb = nt ? a3(0, 0, 0) : b2a<64>(K, op, 0, n, ss);
+    st3s(a.T, a.slots, slot, nt ? select_arith<64>(nt, a3_const(fl), po.sd, ss)
+                                : select_with<64>(K, op, 0, 0, n, a3_const(fl), po.sd, cb));
+    st3s(a.F, a.slots, slot, ld3s(a.hc + 6 * hs, hs, n));
+  } else if (tid == 160) {  // child type = is_int ? LEAF : DUMMY  (train.py:288-289)
+    const A3 cf = nt ? select_arith<64>(nt + 5, a3_const(F_DUMMY), a3_const(F_LEAF), ss)
+                     : select_with<64>(K, op, 2, 0, n, a3_const(F_DUMMY), a3_const(F_LEAF), b2a<64>(K, op, 2, n, ss));
+    for (int ch = 0; ch < 2; ++ch) st3s(a.f_nxt, cs, 2 * n + ch, cf);
+  } else if (tid == 192) {  // child counters' condition
+    const A3 c2 = nt ? b2a_arith<64>(ss, nt[10].a, nt[10].b, nt[11].a) : b2a<64>(K, op, 4, n, ss);
+    for (int c = 0; c < 3; ++c) ca[c] = c2.v[c];
+  }
+  __syncthreads();
+  hc_ts(6 + 8 * a.level, a.ts);
+  if (tid < 2)  // children's budget
+    st3s(a.gam_nxt, cs, 2 * n + tid, a3(ngs[0], ngs[1], ngs[2]));
+  // child counters = select(c_eff, 0, is_int)                 train.py:290
+  const A3 cav = a3(ca[0], ca[1], ca[2]);
+  for (int e = tid; e < C3; e += bd) {
+    A3 cc;
+    if (nt) {
+      const W2* b = nt + 12 + 3 * (e >> 1);
+      const uint64_t F[3] = {(e & 1) ? b[0].b : b[0].a, (e & 1) ? b[1].b : b[1].a, (e & 1) ? b[2].b : b[2].a};
+      cc = add<64>(CE(e), mul_z<64>(diff<64>(a3(0, 0, 0), CE(e)), cav, F));
+    } else {
+      cc = select_with<64>(K, op, 4, (uint32_t)e, n, CE(e), a3(0, 0, 0), cav);
+    }
+    for (int ch = 0; ch < 2; ++ch) st3s(a.cst_nxt, cs * C3, (uint64_t)(2 * n + ch) * C3 + e, cc);
+  }
+}
+
 template <int SL>
 __global__ void __launch_bounds__(256) k_hc_post_finish(NodeArgs na, FinishArgs fa) {
+  static constexpr bool kFusedBudget = true;
+  if (kFusedBudget && blockDim.x >= 256 && na.nf <= 64) {
+    PostOut po;
+    hc_post_body<SL>(na, blockIdx.x, &po);
+    post_split_fused<SL>(na, fa, blockIdx.x, po);
+    __syncthreads();
+    hc_ts(4 + 8 * na.level, na.ts);
+    return;
+  }
   hc_post_body<SL>(na, blockIdx.x);
   hc_ts(3 + 8 * na.level, na.ts);
   __syncthreads();  // hc[sd], hc[new_gam] of this node written by thread 0
