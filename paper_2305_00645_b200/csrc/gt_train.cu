@@ -1348,7 +1348,8 @@ __global__ void __launch_bounds__(128) k_node_finish(FinishArgs a) {
 // child-counter condition, train.py:287-290); the children's gamma is stored
 // after the join.  Same gadgets and blocks as the sequential path.
 template <int SL>
-__device__ __forceinline__ void post_split_fused(const NodeArgs& na, const FinishArgs& a, int n, const PostOut& po) {
+__device__ __forceinline__ void post_split_fused(const NodeArgs& na, const FinishArgs& a, int n, const PostOut& po,
+                                                 const W2* nt_staged, uint64_t* nbar) {
   __shared__ uint64_t ca[3], ngs[3];
   const int tid = threadIdx.x, bd = blockDim.x, warp = tid >> 5;
   const int nf = a.nf, cols = 2 * nf, C3 = 3 * cols;
@@ -1356,11 +1357,15 @@ __device__ __forceinline__ void post_split_fused(const NodeArgs& na, const Finis
   const Keys& K = a.K;
   const uint32_t op = op_id(a.level, SITE_SPLIT);
   auto CE = [&](int e) { return ld3s(a.ceff, hs * C3, (uint64_t)n * C3 + e); };
-  const NodeTape NT = node_tape_plan(nf);
-  __shared__ __align__(128) W2 nsb[16 + 12 + 3 * 64 * 3];  // >= the split segment
-  __shared__ __align__(8) uint64_t nbar;
-  const W2* nt = a.nodetape ? stage_node_tape(a.nodetape + (uint64_t)n * NT.total + NT.spl, NT.lab - NT.spl, nsb, &nbar)
-                            : nullptr;
+  // the split segment of the node tape was bulk-copied at kernel start
+  const W2* nt = nullptr;
+  if (nt_staged) {
+    mbar_wait(nbar, 0);
+    nt = nt_staged;
+  }
+  // this thread's effective counters, loaded while the chains run
+  A3 ce = a3(0, 0, 0);
+  if (tid < C3) ce = CE(tid);
   B3 ss;
   for (int c = 0; c < 3; ++c) ss.v[c] = a.hc[(0 * 3 + c) * hs + n];
   hc_ts(3 + 8 * a.level, a.ts);  // budget and split start together (slots 3, 5)
@@ -1417,13 +1422,14 @@ __device__ __forceinline__ void post_split_fused(const NodeArgs& na, const Finis
   // child counters = select(c_eff, 0, is_int)                 train.py:290
   const A3 cav = a3(ca[0], ca[1], ca[2]);
   for (int e = tid; e < C3; e += bd) {
+    const A3 cev = e == tid ? ce : CE(e);
     A3 cc;
     if (nt) {
       const W2* b = nt + 12 + 3 * (e >> 1);
       const uint64_t F[3] = {(e & 1) ? b[0].b : b[0].a, (e & 1) ? b[1].b : b[1].a, (e & 1) ? b[2].b : b[2].a};
-      cc = add<64>(CE(e), mul_z<64>(diff<64>(a3(0, 0, 0), CE(e)), cav, F));
+      cc = add<64>(cev, mul_z<64>(diff<64>(a3(0, 0, 0), cev), cav, F));
     } else {
-      cc = select_with<64>(K, op, 4, (uint32_t)e, n, CE(e), a3(0, 0, 0), cav);
+      cc = select_with<64>(K, op, 4, (uint32_t)e, n, cev, a3(0, 0, 0), cav);
     }
     for (int ch = 0; ch < 2; ++ch) st3s(a.cst_nxt, cs * C3, (uint64_t)(2 * n + ch) * C3 + e, cc);
   }
@@ -1433,9 +1439,21 @@ template <int SL>
 __global__ void __launch_bounds__(256) k_hc_post_finish(NodeArgs na, FinishArgs fa) {
   static constexpr bool kFusedBudget = true;
   if (kFusedBudget && blockDim.x >= 256 && na.nf <= 64) {
+    // the split segment of the node tape (data-independent) starts coming in
+    // now, beside the epilogue tape, before the wait for the division
+    __shared__ __align__(128) W2 nsb[16 + 12 + 3 * 64 * 3];  // >= the split segment
+    __shared__ __align__(8) uint64_t nbar;
+    const NodeTape NT = node_tape_plan(fa.nf);
+    if (fa.nodetape && threadIdx.x == 0) {
+      const int len = NT.lab - NT.spl;
+      mbar_init(&nbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&nbar, (uint32_t)(len * sizeof(W2)));
+      bulk_g2s(nsb, fa.nodetape + (uint64_t)blockIdx.x * NT.total + NT.spl, (uint32_t)(len * sizeof(W2)), &nbar);
+    }
     PostOut po;
-    hc_post_body<SL>(na, blockIdx.x, &po);
-    post_split_fused<SL>(na, fa, blockIdx.x, po);
+    hc_post_body<SL>(na, blockIdx.x, &po);  // its barriers order the mbarrier init before any wait
+    post_split_fused<SL>(na, fa, blockIdx.x, po, fa.nodetape ? nsb : nullptr, &nbar);
     __syncthreads();
     hc_ts(4 + 8 * na.level, na.ts);
     return;
