@@ -326,17 +326,18 @@ def test_count_engines_share_exact_vs_oracle(nf, n, depth):
         assert np.array_equal(T, To) and np.array_equal(F, Fo), engine
 
 
-@pytest.mark.parametrize("engine", ["tensor", "cuda"])
-def test_host_operand_entry_equals_device_entry(engine):
-    """gt_train_host (pinned host shares in, chunked uploads beside the
-    prologue, tree shares out) gives exactly the device entry's shares, also
-    when captured in a CUDA graph and replayed."""
+@pytest.mark.parametrize("engine,n,nf,depth", [("tensor", 3001, 12, 5), ("cuda", 3001, 12, 5),
+                                                ("tensor", 300, 64, 3), ("tensor", 129, 5, 4)])
+def test_host_operand_entry_equals_device_entry(engine, n, nf, depth):
+    """gt_train_host (pinned host shares in, chunked 2-D uploads beside the
+    prologue -- the last chunk small, down to one K block --, tree shares out)
+    gives exactly the device entry's shares, also when captured in a CUDA
+    graph and replayed; including the widest feature count."""
     from paper_2305_00645_b200._native import gt_keys
     from paper_2305_00645_b200.seeds import derive_seed
     from paper_2305_00645_b200.train import DeviceTrainer, TrainConfig, train_components
 
-    rng = np.random.default_rng(77)
-    n, nf, depth = 3001, 12, 5
+    rng = np.random.default_rng(77 + n + nf)
     data = rng.integers(0, 2, size=(n, nf + 1), dtype=np.uint8)
     seed = b"\x77" * 16
     setup, k, keys_t = run_keys(seed)
