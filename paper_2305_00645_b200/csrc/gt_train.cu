@@ -1371,8 +1371,12 @@ __device__ __forceinline__ void post_split_fused(const NodeArgs& na, const Finis
   hc_ts(3 + 8 * a.level, a.ts);  // budget and split start together (slots 3, 5)
   hc_ts(5 + 8 * a.level, a.ts);
   if (warp < 2) {
-    for (int f = tid; f < nf; f += 64) {
-      B3 h;
+    // lane f = tid (nf <= 64): the hit bits gather by warp ballots (no
+    // contended shared-memory atomics)
+    __shared__ uint32_t hb[2][3];
+    B3 h = {{0, 0, 0}};
+    const int f = tid;
+    if (f < nf) {
       if (po.pb) {
         const W2* b = po.pb + 5 * f;
         const uint64_t Zw[3] = {b[2].a, b[3].a, b[4].a};
@@ -1380,13 +1384,16 @@ __device__ __forceinline__ void post_split_fused(const NodeArgs& na, const Finis
       } else {
         h = eqz<64>(K, po.opH, po.SH, (uint64_t)n * nf + f, add_pub<64>(po.sd, 0ull - (uint64_t)f));
       }
-      for (int c = 0; c < 3; ++c)
-        atomicOr((unsigned long long*)&po.hitw[c], (unsigned long long)((h.v[c] & 1ull) << f));
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const uint32_t bits = __ballot_sync(0xffffffffu, (uint32_t)(h.v[c] & 1ull));
+      if ((tid & 31) == 0) hb[warp][c] = bits;
     }
     asm volatile("bar.sync 2, 64;" ::: "memory");
     if (tid == 0) {
       B3 hw;
-      for (int c = 0; c < 3; ++c) hw.v[c] = po.hitw[c];
+      for (int c = 0; c < 3; ++c) hw.v[c] = (uint64_t)hb[0][c] | ((uint64_t)hb[1][c] << 32);
       B3 ng;
       if (po.pb) {
         const W2* b = po.pb + 5 * nf;
