@@ -1195,21 +1195,30 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n, PostOut* 
     out->sd = sd, out->gam = gam, out->pb = pb, out->hitw = hitw, out->opH = opH, out->SH = SH;
     return;
   }
-  for (int f = tid; f < nf; f += bd) {
-    B3 h;
-    if (pb) {
-      const W2* b = pb + 5 * f;
-      const uint64_t Zw[3] = {b[2].a, b[3].a, b[4].a};
-      h = eq_arith<64>(add_pub<64>(sd, 0ull - (uint64_t)f), b[0].a, b[0].b, b[1].a, Zw);
-    } else {
-      h = eqz<64>(K, opH, SH, (uint64_t)n * nf + f, add_pub<64>(sd, 0ull - (uint64_t)f));
+  // lane f = tid (nf <= 64 <= blockDim): hit bits by warp ballots
+  __shared__ uint32_t hbw[2][3];
+  if (tid < 64) {
+    B3 h = {{0, 0, 0}};
+    const int f = tid;
+    if (f < nf) {
+      if (pb) {
+        const W2* b = pb + 5 * f;
+        const uint64_t Zw[3] = {b[2].a, b[3].a, b[4].a};
+        h = eq_arith<64>(add_pub<64>(sd, 0ull - (uint64_t)f), b[0].a, b[0].b, b[1].a, Zw);
+      } else {
+        h = eqz<64>(K, opH, SH, (uint64_t)n * nf + f, add_pub<64>(sd, 0ull - (uint64_t)f));
+      }
     }
-    for (int c = 0; c < 3; ++c) atomicOr((unsigned long long*)&hitw[c], (unsigned long long)((h.v[c] & 1ull) << f));
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const uint32_t bits = __ballot_sync(0xffffffffu, (uint32_t)(h.v[c] & 1ull));
+      if ((tid & 31) == 0) hbw[tid >> 5][c] = bits;
+    }
   }
   __syncthreads();
   if (tid == 0) {
     B3 hw;
-    for (int c = 0; c < 3; ++c) hw.v[c] = hitw[c];
+    for (int c = 0; c < 3; ++c) hw.v[c] = (uint64_t)hbw[0][c] | ((uint64_t)hbw[1][c] << 32);
     B3 ng;
     if (pb) {
       const W2* b = pb + 5 * nf;
