@@ -369,6 +369,18 @@ __global__ void __launch_bounds__(256, 1) k_count_mma(MmaArgs a) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_slot;
+  // the epilogue's precomputed reshare sums (drawn before the level chain):
+  // loaded now, so their latency hides behind the main loop
+  uint64_t apre[4] = {0, 0, 0, 0};
+  if (a.alpha && kr == 0 && a.alpha_tab) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int cell = tid + k * (int)blockDim.x;
+      const int nc = cell & 15, cw = cell >> 4, w = cw % a.cpb, c = cw / a.cpb;
+      const int n = mt * 16 + nc, wg = nb * a.cpb + w;
+      if (cell < 3 * a.cpb * 16 && n < a.n_h && wg < a.W) apre[k] = a.alpha_tab[((uint64_t)n * 3 + c) * a.W + wg];
+    }
+  }
   pdl_wait();  // the lane planes of the lane kernel
 
   if (tid == 0 && T > 0 && a.probe < 3) {
@@ -453,7 +465,10 @@ __global__ void __launch_bounds__(256, 1) k_count_mma(MmaArgs a) {
     }
     __syncthreads();
     const uint64_t Sstride = (uint64_t)a.n_h * (a.W + 1);
-    for (int cell = tid; cell < 3 * cpb * 16; cell += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int cell = tid + k * (int)blockDim.x;
+      if (cell >= 3 * cpb * 16) break;
       const int nc = cell & 15, cw = cell >> 4, w = cw % cpb, c = cw / cpb;
       const int n = mt * 16 + nc, wg = nb * cpb + w;
       if (n >= a.n_h || wg >= a.W) continue;
@@ -465,7 +480,7 @@ __global__ void __launch_bounds__(256, 1) k_count_mma(MmaArgs a) {
         v += ((uint64_t)x.y << 32 | x.x) + ((uint64_t)x.w << 32 | x.z);
       }
       if (a.alpha && kr == 0 && a.alpha_tab) {
-        v += a.alpha_tab[((uint64_t)n * 3 + c) * a.W + wg];
+        v += apre[k];
       } else if (a.alpha && kr == 0) {
         // zero shares of the count products summed over the shard (see
         // k_count_alpha): alpha_c = F_c - F_{c-1}
@@ -533,6 +548,17 @@ __global__ void __launch_bounds__(256, 1) k_count_mma_t(MmaArgs a) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_slot;
+  uint64_t apre[2] = {0, 0};  // the epilogue's reshare sums, loaded early (see k_count_mma)
+  if (a.alpha && kr == 0 && a.alpha_tab) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int cell = tid + k * (int)blockDim.x;
+      const int g = cell & 15, cn = cell >> 4, n = cn % NG, c = cn / NG;
+      const int wg = nb * a.cpb + g;
+      if (cell < 3 * NG * 16 && g < a.cpb && n < a.n_h && wg < a.W)
+        apre[k] = a.alpha_tab[((uint64_t)n * 3 + c) * a.W + wg];
+    }
+  }
   pdl_wait();
 
   if (tid == 0 && T > 0) {
@@ -613,7 +639,10 @@ __global__ void __launch_bounds__(256, 1) k_count_mma_t(MmaArgs a) {
     }
     __syncthreads();
     const uint64_t Sstride = (uint64_t)a.n_h * (a.W + 1);
-    for (int cell = tid; cell < 3 * NG * 16; cell += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int cell = tid + k * (int)blockDim.x;
+      if (cell >= 3 * NG * 16) break;
       const int g = cell & 15, cn = cell >> 4, n = cn % NG, c = cn / NG;
       const int wg = nb * a.cpb + g;
       if (g >= a.cpb || n >= a.n_h || wg >= a.W) continue;
@@ -625,7 +654,7 @@ __global__ void __launch_bounds__(256, 1) k_count_mma_t(MmaArgs a) {
         v += ((uint64_t)x.y << 32 | x.x) + ((uint64_t)x.w << 32 | x.z);
       }
       if (a.alpha && kr == 0 && a.alpha_tab) {
-        v += a.alpha_tab[((uint64_t)n * 3 + c) * a.W + wg];
+        v += apre[k];
       } else if (a.alpha && kr == 0) {
         uint64_t F[2];
 #pragma unroll
