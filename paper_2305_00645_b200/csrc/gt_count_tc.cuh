@@ -119,13 +119,25 @@ __global__ void __launch_bounds__(256) k_prep8(Prep8Args a) {
     }
     __syncthreads();
   }
-  for (int e = tid; e < cnt * nf; e += blockDim.x) {
-    const int sl = e / nf, f = e - sl * nf;
-    const A3 z = mul<64>(a.K, a.op_prods, 0, (uint32_t)f, a.base + s0 + sl,
-                         a3(xs[e], xs[HS * nf + e], xs[2 * HS * nf + e]),
-                         a3(ys[sl], ys[HS + sl], ys[2 * HS + sl]));
+  // one thread per (sample, feature pair): features 2j and 2j+1 take the two
+  // words of the same Philox block per key (mul's schedule), drawn once
+  const int nfp = (nf + 1) >> 1;
+  for (int e = tid; e < cnt * nfp; e += blockDim.x) {
+    const int sl = e / nfp, fp = e - sl * nfp, f0 = 2 * fp;
+    W2 Z[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) ps[c * HS * nf + e] = z.v[c];
+    for (int i = 0; i < 3; ++i) Z[i] = word2(a.K.pair[i], a.op_prods, 0, (uint32_t)fp, a.base + s0 + sl);
+    const A3 y = a3(ys[sl], ys[HS + sl], ys[2 * HS + sl]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int f = f0 + h;
+      if (f >= nf) break;
+      const int ef = sl * nf + f;
+      const uint64_t F[3] = {h ? Z[0].b : Z[0].a, h ? Z[1].b : Z[1].a, h ? Z[2].b : Z[2].a};
+      const A3 z = mul_z<64>(a3(xs[ef], xs[HS * nf + ef], xs[2 * HS * nf + ef]), y, F);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) ps[c * HS * nf + ef] = z.v[c];
+    }
   }
   __syncthreads();
   // planes: item = (component, 16-sample chunk, column, 4-sample quad); the
