@@ -75,24 +75,27 @@ struct Prep8Args {
   uint32_t op_prods;
 };
 __global__ void __launch_bounds__(256) k_prep8(Prep8Args a) {
-  // one CTA per 64-sample half block; shared memory (<= 198 KB at nf = 64):
-  // xs[3][HS][nf] features, ps[3][HS][nf] prods, ys[3][HS] labels
-  constexpr int HS = TC_KB / 2;
+  // one CTA per 32-sample quarter block (chunks kc = 2 sub, 2 sub + 1 of a
+  // 64-sample half block: a grid of many small CTAs leaves no near-empty
+  // second wave); shared memory (<= 99 KB at nf = 64): xs[3][HS][nf]
+  // features, ps[3][HS][nf] prods, ys[3][HS] labels
+  constexpr int HS = TC_KB / 4;
   extern __shared__ __align__(16) uint64_t v[];
   __shared__ __align__(8) uint64_t bar;
   const int nf = a.nf, W = a.W, tid = threadIdx.x;
   uint64_t* xs = v;
   uint64_t* ps = v + 3 * HS * nf;
   uint64_t* ys = v + 6 * HS * nf;
-  const uint64_t hb = a.hb0 + blockIdx.x;
+  const uint64_t qb = 2 * a.hb0 + blockIdx.x;
+  const uint64_t hb = qb >> 1;
   const uint64_t kb = hb >> 1;
-  const int half = (int)(hb & 1);
+  const int half = (int)(hb & 1), sub = (int)(qb & 1);
   const uint64_t nfx = a.N * (uint64_t)nf;
-  const uint64_t s0 = kb * TC_KB + half * HS;
-  const int cnt = (int)min((uint64_t)HS, a.N - s0);
+  const uint64_t s0 = kb * TC_KB + half * (TC_KB / 2) + sub * HS;
+  const int cnt = s0 < a.N ? (int)min((uint64_t)HS, a.N - s0) : 0;  // 0: a half block's empty tail quarter
   // the block's feature rows and labels are contiguous runs: bulk copies when
   // every run is 16-byte aligned, plain loads otherwise
-  const bool bulk = ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.Y)) & 15) == 0 &&
+  const bool bulk = cnt > 0 && ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.Y)) & 15) == 0 &&
                     ((nfx | a.N | (uint64_t)cnt * nf | (uint64_t)cnt) & 1) == 0;
   if (bulk) {
     if (tid == 0) {
@@ -144,15 +147,15 @@ __global__ void __launch_bounds__(256) k_prep8(Prep8Args a) {
   // quad's x words are byte-transposed in registers (4x4 byte_perm
   // transposes) into one 32-bit word of each of the 8 limb rows; the four
   // quads of a row are adjacent threads
-  const uint64_t HBX = (uint64_t)8 * a.cpb * HS;
-  const int items = 3 * 4 * a.nbn * a.cpb * 4;
+  const uint64_t HBX = (uint64_t)8 * a.cpb * (TC_KB / 2);
+  const int items = 3 * 2 * a.nbn * a.cpb * 4;
   for (int it = tid; it < items; it += blockDim.x) {
     const int quad = it & 3;
     int r = it >> 2;
     const int g = r % a.cpb;
     r /= a.cpb;
-    const int kc = r & 3;
-    r >>= 2;
+    const int kc = 2 * sub + (r & 1);
+    r >>= 1;
     const int nb = r % a.nbn, c = r / a.nbn;
     const int w = nb * a.cpb + g;
     const uint64_t* p0 = nullptr;
@@ -163,7 +166,7 @@ __global__ void __launch_bounds__(256) k_prep8(Prep8Args a) {
     uint32_t wx[2][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const int sl = kc * 16 + quad * 4 + i;
+      const int sl = (kc & 1) * 16 + quad * 4 + i;
       const uint64_t x = (p0 && sl < cnt) ? p0[sl * stride] : 0ull;
       wx[0][i] = (uint32_t)x, wx[1][i] = (uint32_t)(x >> 32);
     }

@@ -2135,10 +2135,10 @@ int launch_prep8(const gt_train_cfg& c, const uint64_t* features, const uint64_t
   pa.nbn = tp.nbn;
   pa.K = K;
   pa.op_prods = op_id(0, SITE_PRODS);
-  const int smem = 3 * (TC_KB / 2) * pa.W * (int)sizeof(uint64_t);
+  const int smem = 3 * (TC_KB / 4) * pa.W * (int)sizeof(uint64_t);  // one CTA per 32-sample quarter block
   GT_CUDA_CHECK(cudaFuncSetAttribute(k_prep8, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3((unsigned)(hb_hi - hb_lo));
+  lc.gridDim = dim3((unsigned)(2 * (hb_hi - hb_lo)));
   lc.blockDim = dim3(256);
   lc.dynamicSmemBytes = (size_t)smem;
   lc.stream = s;
