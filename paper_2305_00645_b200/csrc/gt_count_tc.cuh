@@ -34,8 +34,9 @@ constexpr int TC_TMEM_COLS = 512;         // three accumulators of N <= 160 colu
 
 // node groups per 16-sample chunk of the la planes: min(16, n_h)
 __host__ __device__ inline int tc_groups(int n_h) { return n_h < 16 ? n_h : 16; }
-// K blocks per lane-kernel CTA: enough (node, sample pair) items for its 256 threads
-__host__ __device__ inline int tc_lane_kpb(int n_h) { return tc_groups(n_h) < 4 ? 4 / tc_groups(n_h) : 1; }
+// 64-sample half blocks per lane-kernel CTA: 256-512 (node, sample pair)
+// items for its 256 threads -- small CTAs, so the last wave is short
+__host__ __device__ inline int tc_lane_hpc(int n_h) { return tc_groups(n_h) < 8 ? 8 / tc_groups(n_h) : 1; }
 
 struct TcPlan {
   int CW;      // sample columns W (the mask column is summed by the lane kernel)
@@ -214,9 +215,9 @@ __global__ void __launch_bounds__(256, GT_LANES8_MINB) k_count_lanes8(Lanes8Args
   pdl_trigger();
   // la8[mt][kbc][half 2][c 3][kc 4][g NG][p 8][16], NG = min(16, n_h) node
   // groups: the three components of a 64-sample half block are one
-  // contiguous 1.5 NG KB run (one bulk copy for the contraction).  With
-  // NG < 4 a CTA covers 4 / NG K blocks (one sample pair per thread).
-  const int NG = tc_groups(a.n_h), KPB = tc_lane_kpb(a.n_h);
+  // contiguous 1.5 NG KB run (one bulk copy for the contraction).  A CTA
+  // covers HPC half blocks (tc_lane_hpc).
+  const int NG = tc_groups(a.n_h), HPC = tc_lane_hpc(a.n_h);
   const uint64_t cstride = 512ull * NG;
   if (tid < 16) {
     const int n = mt * 16 + tid;
@@ -237,11 +238,12 @@ __global__ void __launch_bounds__(256, GT_LANES8_MINB) k_count_lanes8(Lanes8Args
   // component, and the even thread stores limbs 0..3 of the 4 samples, the
   // odd thread limbs 4..7, one 32-bit word each.
   const bool odd = threadIdx.x & 1;
-  for (int e = tid; e < KPB * NG * (TC_KB / 2); e += blockDim.x) {
-    const int kbl = e / (NG * (TC_KB / 2)), r = e - kbl * NG * (TC_KB / 2);
-    const int nn = r / (TC_KB / 2), s2 = (r % (TC_KB / 2)) * 2;
-    const uint64_t kb = (uint64_t)blockIdx.x * KPB + kbl;
-    if (kb >= a.nkbc) break;  // warp-uniform (a warp's items share kbl)
+  for (int e = tid; e < HPC * NG * (TC_KB / 4); e += blockDim.x) {
+    const int hbl = e / (NG * (TC_KB / 4)), r = e - hbl * NG * (TC_KB / 4);
+    const uint64_t hb = (uint64_t)blockIdx.x * HPC + hbl;
+    if (hb >= 2 * a.nkbc) break;  // warp-uniform (a warp's items share hbl)
+    const uint64_t kb = hb >> 1;
+    const int nn = r / (TC_KB / 4), s2 = (int)(hb & 1) * (TC_KB / 2) + (r % (TC_KB / 4)) * 2;
     uint8_t* blk = a.la8 + ((uint64_t)mt * a.nkbc + kb) * (3072ull * NG);
     const int n = mt * 16 + nn;
     const uint64_t s = kb * TC_KB + s2;

@@ -2045,9 +2045,9 @@ int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks
     la.leafbits = c.leafbits;
     P.start();
     {
-      const unsigned kpb = (unsigned)tc_lane_kpb(c.n_h);  // K blocks per CTA (compact shallow levels)
-      int rc = launch_chain(k_count_lanes8, dim3((nkb + kpb - 1) / kpb, (unsigned)tp.mtiles), dim3(256), 0, s, nullptr,
-                            la);
+      const unsigned hpc = (unsigned)tc_lane_hpc(c.n_h);  // half blocks per CTA
+      int rc = launch_chain(k_count_lanes8, dim3((2 * nkb + hpc - 1) / hpc, (unsigned)tp.mtiles), dim3(256), 0, s,
+                            nullptr, la);
       if (rc) return rc;
     }
     GT_LAUNCH_CHECK("k_count_lanes8");
