@@ -482,6 +482,40 @@ __device__ __forceinline__ B3 lt_arith(const W2* b, const A3& x, const A3& y) {
   return rows;
 }
 
+// lt_arith by a whole warp: even lanes recover the bits of x, odd lanes those
+// of y (the same instructions on two operands run side by side), one shuffle
+// pair exchanges them, then every lane finishes the comparison.  Same blocks
+// and result as lt_arith; all 32 lanes must call it.
+template <int L>
+__device__ __forceinline__ B3 lt_arith_warp(const W2* b, const A3& x, const A3& y) {
+  constexpr uint64_t M = Ring<L>::M;
+  constexpr int NL = Levels<L>::n;
+  const bool odd = threadIdx.x & 1;
+  const A3 v = odd ? y : x;
+  const uint64_t r = (odd ? b[2].b : b[0].a) & M;
+  B3 Rb;
+  Rb.v[0] = (odd ? b[3].a : b[0].b) & M;
+  Rb.v[1] = (odd ? b[3].b : b[1].a) & M;
+  Rb.v[2] = r ^ Rb.v[0] ^ Rb.v[1];
+  const uint64_t c = (open<L>(v) + r) & M;
+  const B3 sc = borrow_scan_blk<L>(c, Rb, b + 4 + (odd ? 3 * NL : 0));
+  B3 mine;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) mine.v[i] = Rb.v[i] ^ ((sc.v[i] << 1) & M);
+  mine.v[0] ^= c;
+  B3 other;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) other.v[i] = __shfl_xor_sync(0xffffffffu, mine.v[i], 1);
+  const B3 xb = odd ? other : mine, yb = odd ? mine : other;
+  const uint64_t Zg[3] = {b[4 + 6 * NL].a & M, b[5 + 6 * NL].a & M, b[6 + 6 * NL].a & M};
+  const B3 g = and_z(yb, bnot(xb, M), Zg);
+  const B3 p = bnot(bxor(xb, yb), M);
+  B3 rows = prefix_borrow_blk<L>(g, p, b + 7 + 6 * NL);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) rows.v[i] = (rows.v[i] >> (L - 1)) & 1ull;
+  return rows;
+}
+
 template <int L>
 __device__ __forceinline__ B3 lt(const Keys& K, uint32_t op, uint32_t sub, uint64_t lane, const A3& x, const A3& y) {
   W2 b[LtRand<L>::BLOCKS];

@@ -1164,7 +1164,7 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n, PostOut* 
       if (pt) {
         const W2* b = pt + roff + ArgminPair<SL>::BLOCKS * p;
         constexpr int LB = LtRand<SL>::BLOCKS;
-        const B3 cw = lt_arith<SL>(b, bv, av);  // challenger wins iff b < a
+        const B3 cw = lt_arith_warp<SL>(b, bv, av);  // challenger wins iff b < a
         nv = select_arith<SL>(b + LB, av, bv, cw);
         ni = select_arith<64>(b + LB + 5, ai, bi, cw);
       } else {
