@@ -1292,14 +1292,16 @@ __device__ __forceinline__ void node_finish_body(const FinishArgs& a, int n) {
   }
   if (a.labels) {
     // labels = b2a(lt(psi0, psi1)) on effective counters      train.py:300-306
-    if (tid == 0) {
+    if (tid < 32) {  // warp 0 (the staged lt pairs its operands on neighbouring lanes)
       const uint32_t op = op_id(a.level, SITE_LABELS);
       const A3 psi0 = add<64>(CE(cols), CE(cols + 1)), psi1 = add<64>(CE(2 * cols), CE(2 * cols + 1));
       constexpr int LB = LtRand<64>::BLOCKS;
-      const A3 lab = nt ? b2a_arith<64>(lt_arith<64>(nt, psi0, psi1), nt[LB].a, nt[LB].b, nt[LB + 1].a)
+      const A3 lab = nt ? b2a_arith<64>(lt_arith_warp<64>(nt, psi0, psi1), nt[LB].a, nt[LB].b, nt[LB + 1].a)
                         : b2a<64>(K, op, 1, n, lt<64>(K, op, 0, n, psi0, psi1));
-      st3s(a.T, a.slots, slot, lab);
-      st3s(a.F, a.slots, slot, ld3s(a.f, hs, n));
+      if (tid == 0) {
+        st3s(a.T, a.slots, slot, lab);
+        st3s(a.F, a.slots, slot, ld3s(a.f, hs, n));
+      }
     }
     return;
   }
