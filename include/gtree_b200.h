@@ -88,20 +88,20 @@ int gt_oaa(int width, const uint64_t* table, uint64_t m, const uint64_t* idx, ui
 int gt_row_lookup(int width, const uint64_t* rows, uint64_t m, const uint64_t* idx, uint64_t* out, uint64_t n,
                   const gt_keys* keys, uint32_t op, void* stream);
 
-/* ---- secure training (train_tree, train.py:222-311, heuristic "mpc") ---- */
+/* ---- secure training (train_tree, train.py:108-197, heuristic "mpc") ---- */
 
 typedef struct {
-  int32_t depth;       /* resolved depth H (train.py:195-200) */
+  int32_t depth;       /* resolved depth H (train.py:81-86) */
   int32_t tau;         /* fixed-point bits (TrainConfig.tau) */
   int32_t score_width; /* score ring width, 32 or 64 (TrainConfig.score_ring) */
   int32_t nf;          /* features = n_columns - 1, 1..64 */
   int32_t policy;      /* 0 = fixed, 1 = grow (one opened stop bit per level) */
   int32_t heuristic;   /* 0 = mpc (on device), 1 = tee (trusted helper via callback) */
-  uint64_t n_total;     /* global sample count (counter_shift, train.py:189-192) */
+  uint64_t n_total;     /* global sample count (counter_shift, train.py:75-78) */
   uint64_t n_local;     /* samples resident on this device */
   uint64_t sample_base; /* global index of the first local sample */
   int32_t count_reshare; /* 0 = reshare every (sample, node, column) product as the
-                            reference does (train.py:333); 1 = dot-product reshare: the
+                            reference does (train.py:219); 1 = dot-product reshare: the
                             local products are summed over samples first and each counter
                             cell is reshared once (same revealed tree, n_h*W instead of
                             N*n_h*W reshared words per level) */
@@ -125,7 +125,7 @@ int gt_train(const gt_train_cfg* cfg, const uint64_t* features, const uint64_t* 
              const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user, void* stream);
 
 /* Trusted split helper of heuristic "tee" (reference _heuristic_tee /
- * _labels_tee, train.py:391-415, EnclaveService enclave.py:94-185).  Called
+ * _labels_tee, train.py:277-301, EnclaveService enclave.py:94-185).  Called
  * synchronously with DEVICE pointers on `stream`:
  *   op 1 (split):  counters [3][n][3][2nf] (c_orig), gamma [3][n] bit words,
  *                  types [3][n]; writes out [4][3][n] = should_split bits,
@@ -169,7 +169,7 @@ int gt_train_host(const gt_train_cfg* cfg, const uint64_t* features_h, const uin
                   uint64_t workspace_bytes, const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user,
                   void* stream);
 
-/* ---- secure inference (infer_batch, infer.py:91-106) ---- */
+/* ---- secure inference (infer_batch, infer.py:20-35) ---- */
 
 /* tree [3][2^depth-1] heap-ordered payload shares, queries [3][n][nf];
  * instance_base = global index of query 0 (instance sharding); out [3][n]

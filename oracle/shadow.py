@@ -5,7 +5,7 @@ The reference MPC trainer's revealed tree is an exact function of the
 plaintext data: every gadget is exact (gadgets.py:3-10), so the opened tree
 equals ``plaintext_train`` (tree.py:272-326) with the rational impurity
 replaced by the fixed-point pipeline the MPC path evaluates on shares
-(train.py:346-388, gadgets.py:297-401).  This module restates that pipeline
+(train.py:232-274, gadgets.py:297-401).  This module restates that pipeline
 on plain integers so revealed trees can be checked at
 10^6 samples in seconds; it is pinned to reference runs by the golden
 fixtures (tests/golden/trees_mpc.npz, c2c3.npz).
@@ -22,7 +22,7 @@ M32 = np.uint64(0xFFFFFFFF)
 
 
 def counter_shift(n_samples: int, score_width: int = 32, tau: int = 10) -> int:
-    """train.py:189-192."""
+    """train.py:75-78."""
     return max(0, int(n_samples).bit_length() - (score_width - tau - 2) // 2)
 
 
@@ -55,7 +55,7 @@ def fx_div(p: np.ndarray, q: np.ndarray, tau: int = 10) -> np.ndarray:
 
 
 def fx_scores(C: np.ndarray, shift: int, tau: int = 10) -> np.ndarray:
-    """Per-feature fixed-point scores of one node (train.py:366-383).
+    """Per-feature fixed-point scores of one node (train.py:252-269).
     C: (3, 2nf) exact counters (python ints or uint64)."""
     c = (np.asarray(C, dtype=np.uint64) >> np.uint64(shift)) & M32
     nf = c.shape[1] // 2
@@ -128,7 +128,7 @@ def mpc_train(data: np.ndarray, depth: int, filler: np.ndarray, tau: int = 10, n
             sd = int(np.argmin(sc))  # leftmost minimum (gadgets.py:366-401)
             split = types[k] == F_LEAF and psi0 != 0 and psi1 != 0 and gammas[k].any()
             g = gammas[k].copy()
-            g[sd] = False  # cleared for every node (train.py:386-387)
+            g[sd] = False  # cleared for every node (train.py:272-273)
             new_g[2 * k] = new_g[2 * k + 1] = g
             if split:
                 T[off + k] = sd

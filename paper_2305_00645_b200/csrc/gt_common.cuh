@@ -13,20 +13,20 @@
 namespace gt {
 
 // Op ids: (level << 16) | site.  One site per gadget call site of the
-// reference level loop (train.py:222-311, infer.py:91-106).
+// reference level loop (train.py:108-197, infer.py:20-35).
 enum Site : uint32_t {
-  SITE_PRODS = 1,     // count:0 features x labels          train.py:229-230
-  SITE_PART_OAA = 2,  // partition oaa on level payloads    train.py:249-251
-  SITE_PART_ROW = 3,  // partition row_lookup on features   train.py:252
-  SITE_ISLEAF = 4,    // count is_leaf = eq(F, LEAF)        train.py:320
-  SITE_COUNT = 5,     // count lanes (eq, and, b2a, mul)    train.py:325-335
-  SITE_HC = 6,        // _heuristic_mpc                     train.py:346-388
-  SITE_REPLACE = 7,   // replace:h                          train.py:269-276
-  SITE_SPLIT = 8,     // split:h                            train.py:284-290
-  SITE_LABELS = 9,    // labels:h                           train.py:300-306
-  SITE_STOP = 10,     // grow-policy stop bit               train.py:279-282
-  SITE_WALK_OAA = 16, // walk:t oaa                         infer.py:101-102
-  SITE_WALK_ROW = 17, // walk:t row_lookup                  infer.py:103
+  SITE_PRODS = 1,     // count:0 features x labels          train.py:115-116
+  SITE_PART_OAA = 2,  // partition oaa on level payloads    train.py:135-137
+  SITE_PART_ROW = 3,  // partition row_lookup on features   train.py:138
+  SITE_ISLEAF = 4,    // count is_leaf = eq(F, LEAF)        train.py:206
+  SITE_COUNT = 5,     // count lanes (eq, and, b2a, mul)    train.py:211-221
+  SITE_HC = 6,        // _heuristic_mpc                     train.py:232-274
+  SITE_REPLACE = 7,   // replace:h                          train.py:155-162
+  SITE_SPLIT = 8,     // split:h                            train.py:170-176
+  SITE_LABELS = 9,    // labels:h                           train.py:186-192
+  SITE_STOP = 10,     // grow-policy stop bit               train.py:165-168
+  SITE_WALK_OAA = 16, // walk:t oaa                         infer.py:30-31
+  SITE_WALK_ROW = 17, // walk:t row_lookup                  infer.py:32
 };
 __host__ __device__ inline uint32_t op_id(int level, uint32_t site) { return ((uint32_t)level << 16) | site; }
 

@@ -2,7 +2,7 @@
 // an INT8 limb decomposition of the Z_2^64 share products.
 //
 // The count contraction of one level (_count_level, reference
-// pkg/src/obtree/train.py:315-343) is, per share component i, the ring GEMM
+// pkg/src/obtree/train.py:201-229) is, per share component i, the ring GEMM
 //     S_i[n][w] = sum_s la_i x_i + la_i x_{i+1} + la_{i+1} x_i
 // (the party-local cross terms of mul(cols, la), rss.py:391-395).  Writing
 // every u64 as 8 unsigned bytes, a * b mod 2^64 = sum_{p+q<=7} a_p b_q
@@ -15,7 +15,7 @@
 // per 32-sample K step over three la planes and three x planes.  Each CTA
 // sums at most 64 x 128 samples, so every D entry stays below
 // 3 x 8192 x 255^2 < 2^31 (exact in the s32 accumulator).  The mask column
-// s_mask = sum_s la (train.py:334) is summed by the lane kernel.
+// s_mask = sum_s la (train.py:220) is summed by the lane kernel.
 //
 // Operands are staged by cp.async.bulk in the canonical K-major
 // SWIZZLE_NONE core-matrix layout (8 rows x 16 bytes = 128 contiguous bytes;
@@ -64,7 +64,7 @@ inline TcPlan tc_plan(int nf, int n_h) {
 // Fused prologue for the tensor engine (count:0 prods + the x planes): one CTA
 // per 128-sample K block stages the block's features and labels in shared
 // memory (coalesced rows), forms count:0's prods = mul(features, labels)
-// (train.py:229-230, same Philox schedule as k_prods) next to them, and
+// (train.py:115-116, same Philox schedule as k_prods) next to them, and
 // writes the U / X byte planes straight from shared memory: the u64 column
 // matrix never goes through HBM.
 struct Prep8Args {
@@ -188,16 +188,16 @@ __global__ void __launch_bounds__(256) k_prep8(Prep8Args a) {
 }
 
 // --- A operand: one CTA per (128-sample block, 16-node M tile) of a chunk;
-// lanes la = b2a(eq(m_idx, off+n) & is_leaf[n]) (train.py:328-331, the same
+// lanes la = b2a(eq(m_idx, off+n) & is_leaf[n]) (train.py:214-217, the same
 // randomness as k_count_lanes: count_lane_pair), two samples of one node
 // per work item so each limb row leaves as one packed 32-bit word; the byte
 // planes la8[mt][kbc][half][c][kc 4][g 16][p 8][16] are stored straight from
-// registers (each warp store covers whole 32-byte sectors).  is_leaf of the tile's 16 nodes (train.py:320) is drawn
+// registers (each warp store covers whole 32-byte sectors).  is_leaf of the tile's 16 nodes (train.py:206) is drawn
 // in the CTA (it is keyed by node only).
 struct Lanes8Args {
   const uint64_t *midx, *f;
   uint8_t* la8;
-  uint64_t* S;  // [3][n_h][W+1]: the mask column s_mask[n] = sum_s la (train.py:334)
+  uint64_t* S;  // [3][n_h][W+1]: the mask column s_mask[n] = sum_s la (train.py:220)
   int W;
   const uint64_t* leafbits;  // is_leaf [3][n_h] precomputed by the partition launch, or null: draw per CTA
   uint64_t N, s0, cn, base, nkbc;  // nkbc = chunk capacity in K blocks

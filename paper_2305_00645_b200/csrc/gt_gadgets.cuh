@@ -183,7 +183,7 @@ __device__ __forceinline__ B3 eq_arith(const A3& d, uint64_t r, uint64_t Rb0, ui
   B3 P;
   P.v[0] = Rb0 ^ notc;  // xor_pub(planes, ~c)
   P.v[1] = Rb1;
-  P.v[2] = r ^ Rb0 ^ Rb1;  // _value_bit_words, dealer.py:411-417
+  P.v[2] = r ^ Rb0 ^ Rb1;  // _value_bit_words, dealer.py:51-57
   return and_reduce_w(P, L, Zw);
 }
 
@@ -531,7 +531,7 @@ __device__ __forceinline__ B3 lt(const Keys& K, uint32_t op, uint32_t sub, uint6
 
 // Boolean bit -> arithmetic share (b2a, gadgets.py:223-231) from a dabit:
 // arithmetic shares (A0, A1, beta - A0 - A1) and boolean shares of beta =
-// bit0 of `bits` with Bb0 = bit1, Bb1 = bit2 (_gen_dabits, dealer.py:420-424).
+// bit0 of `bits` with Bb0 = bit1, Bb1 = bit2 (_gen_dabits, dealer.py:60-64).
 template <int L>
 __device__ __forceinline__ A3 b2a_arith(const B3& b, uint64_t A0, uint64_t A1, uint64_t bits) {
   constexpr uint64_t M = Ring<L>::M;
@@ -554,14 +554,14 @@ __device__ __forceinline__ A3 b2a(const Keys& K, uint32_t op, uint32_t sub, uint
   return b2a_arith<L>(b, w.a, w.b, word(K.dealer, op, sub, 2, lane));
 }
 
-// One fused lookup / count lane (oaa.py:28-34, train.py:328-333): eq + b2a
+// One fused lookup / count lane (oaa.py:28-34, train.py:214-219): eq + b2a
 // draw the lane's dealer material from THREE Philox blocks
 //   dealer (sub,0) = (r, Rb0)   (sub,1) = (Rb1, A0)   (sub,2) = (A1, dabit bits)
 // while the AND-tree zero words of two neighbouring lanes share ONE pair
 // block per key (.a / .b halves; the caller picks the block, see
 // lookup_partial and the count lane kernels).  A count lane's leaf-AND zero
 // bit is bit 63 of its zero word (the l = 64 AND tree uses bits 0..62).
-// One count lane (train.py:328-331) from its dealer material and zero word:
+// One count lane (train.py:214-217) from its dealer material and zero word:
 // la = b2a(eq(d, 0) & leaf), the AND gate's zero bit = bit 63 of Zw.
 __device__ __forceinline__ A3 count_lane_arith(const A3& d, uint64_t r, uint64_t Rb0, uint64_t Rb1, uint64_t A0,
                                                uint64_t A1, uint64_t bits, const uint64_t Zw[3], const B3& leaf);
@@ -681,7 +681,7 @@ __device__ __forceinline__ A3 trunc_arith(const W2* b, const A3& x, int k) {
   Rb.v[1] = b[1].a & M;
   Rb.v[2] = r ^ Rb.v[0] ^ Rb.v[1];
   const uint64_t S0 = b[2].b & M, S1 = b[3].a & M;
-  const uint64_t S2 = ((r >> k) - S0 - S1) & M;  // _gen_truncpairs, dealer.py:427-432
+  const uint64_t S2 = ((r >> k) - S0 - S1) & M;  // _gen_truncpairs, dealer.py:67-72
   const uint64_t c = (open<L>(x) + r) & M;       // open_a(x + r)
   const B3 s = borrow_scan_blk<L>(c, Rb, b + 4);
   B3 wrap, lowb;

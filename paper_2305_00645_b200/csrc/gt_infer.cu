@@ -1,5 +1,5 @@
 #include <cstdlib>
-// Secure batch inference (reference infer_batch, pkg/src/obtree/infer.py:91-106)
+// Secure batch inference (reference infer_batch, pkg/src/obtree/infer.py:20-35)
 // as ONE fused kernel: every query walks all H levels; level t fetches the
 // current slot's payload with an oblivious lookup over the 2^t level entries
 // and then the query's bit for that feature with a row lookup over its nf
@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(256) k_walk(const uint64_t* tree, int depth, c
     const int m = 1 << lv, o = m - 1;
     A3 part = a3(0, 0, 0);
     if (valid) {
-      const A3 local = add_pub<64>(slot, 0ull - (uint64_t)o);  // infer.py:101
+      const A3 local = add_pub<64>(slot, 0ull - (uint64_t)o);  // infer.py:30
       auto entry = [&](int j) { return a3(tab[o + j], tab[slots + o + j], tab[2 * slots + o + j]); };
       part = lookup_partial<64>(K, op_id(lv, SITE_WALK_OAA), base + s, local, m, t, G, entry);
     }
@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(256) k_walk(const uint64_t* tree, int depth, c
       part2 = lookup_partial<64>(K, op_id(lv, SITE_WALK_ROW), base + s, payload, nf, t, G, entry);
     }
     const A3 branch = group_sum<G, 64>(part2);
-    slot = add_pub<64>(add<64>(mul_pub<64>(slot, 2), branch), 1);  // infer.py:104
+    slot = add_pub<64>(add<64>(mul_pub<64>(slot, 2), branch), 1);  // infer.py:33
   }
   if (valid && t == 0) {
     out[s] = payload.v[0];

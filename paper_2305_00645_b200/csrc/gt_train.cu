@@ -1,24 +1,25 @@
 // Secure level-wise training on device (reference train_tree,
-// pkg/src/obtree/train.py:222-311, heuristic "mpc", fixed/grow policies).
+// pkg/src/obtree/train.py:108-197, heuristic "mpc", fixed/grow policies).
 //
 // Per level h (n_h = 2^h nodes, W = 2nf+1 sample columns):
 //   k_partition   (h > 0)  oaa on level h-1 payloads + row_lookup on features,
-//                          m_idx = 2 m_idx + d + 1             train.py:248-253
+//                          m_idx = 2 m_idx + d + 1             train.py:134-139
 //   k_count                one lane per (sample, node): eq, and is_leaf, b2a,
 //                          W products with reshare, summed over samples
-//                          into S[n][w] (+ mask column)        train.py:315-335
+//                          into S[n][w] (+ mask column)        train.py:201-221
 //   allreduce(S)           sample-sharded runs only (linear in shares)
 //   k_node_hc              one CTA per node: counter assembly, _heuristic_mpc
 //                          (division ladder + Newton, masked argmin, budget
-//                          clear), replace                      train.py:256-276
-//   k_node_stop   (grow)   opened stop bit                     train.py:279-282
+//                          clear), replace                      train.py:142-162
+//   k_node_stop   (grow)   opened stop bit                     train.py:165-168
 //   k_node_finish          split (payload / child type / child counters) or
-//                          labels on the last level            train.py:284-306
+//                          labels on the last level            train.py:170-192
 // Every lane's randomness is keyed by (op, sub, field, global lane), so the
 // shares produced are independent of sharding and of launch geometry.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <utility>
 #include <vector>
 
@@ -53,7 +54,7 @@ __device__ __forceinline__ B3 ldb3s(const uint64_t* p, uint64_t stride, uint64_t
 
 __global__ void k_init(uint64_t* f, uint64_t* gam, uint64_t* cst, uint64_t fstride, uint64_t cstride, int cols,
                        int nf) {
-  // f_level = const(1), gam = const bits(ones), c_start = 0   (train.py:235-238)
+  // f_level = const(1), gam = const bits(ones), c_start = 0   (train.py:121-124)
   int t = threadIdx.x;
   if (t < 3) {
     f[t * fstride] = t == 0 ? F_LEAF : 0;
@@ -63,10 +64,10 @@ __global__ void k_init(uint64_t* f, uint64_t* gam, uint64_t* cst, uint64_t fstri
     for (int c = 0; c < 3; ++c) cst[c * cstride + e] = 0;
 }
 
-// count:0 prods = mul(features, labels[:, None])               train.py:229-230
+// count:0 prods = mul(features, labels[:, None])               train.py:115-116
 // written straight into the level-invariant sample-column matrix the count
 // contraction streams: cols[c][s][0..WC) = x | x*y | y | 0 (mask) | 0 (pad)
-// (sample_cols, train.py:231-233).  One thread per (sample, column slot).
+// (sample_cols, train.py:117-119).  One thread per (sample, column slot).
 __global__ void k_prods(const uint64_t* X, const uint64_t* Y, uint64_t* cols, uint64_t N, int nf, int WC,
                         uint64_t base, Keys K, uint32_t op) {
   const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -91,7 +92,7 @@ __global__ void k_prods(const uint64_t* X, const uint64_t* Y, uint64_t* cols, ui
 
 // Level-start side work the partition launch carries (no extra launch on the
 // chain): zero the level's count sums, and is_leaf = eq(F, LEAF) of the
-// level's nodes (train.py:320) for the lane kernel.
+// level's nodes (train.py:206) for the lane kernel.
 struct PartAux {
   uint64_t* S;
   uint64_t swords;
@@ -149,7 +150,7 @@ constexpr int CNT_TPB = 256;
 constexpr int CNT_NA = 2;  // nodes per contraction thread tile
 constexpr int CNT_CB = 4;  // columns per contraction thread tile
 
-// is_leaf = eq(F_level, LEAF) per node (train.py:320) -> leaf[3][n_h] bits
+// is_leaf = eq(F_level, LEAF) per node (train.py:206) -> leaf[3][n_h] bits
 __global__ void k_count_leaf(const uint64_t* f, uint64_t* leaf, int n_h, Keys K, uint32_t op_leaf) {
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= n_h) return;
@@ -168,7 +169,7 @@ struct LaneArgs {
 };
 
 // One thread per (sample pair, node) of a sample chunk:
-//   la = b2a(eq(m_idx, off+n) & is_leaf[n])                 train.py:328-331
+//   la = b2a(eq(m_idx, off+n) & is_leaf[n])                 train.py:214-217
 // (dealer material per lane, the two lanes' zero words from one pair block:
 // count_lane_pair).  Padding node slots are written as zero shares.
 __global__ void __launch_bounds__(256) k_count_lanes(LaneArgs a) {
@@ -251,7 +252,7 @@ struct MacArgs {
 // mul(cols, la) (rss.py:391-395)
 //     acc_i += la_i (x_i + x_{i+1}) + la_{i+1} x_i
 // over its samples; the mask column (x = 0, u = 1) accumulates la_i itself
-// (s_mask, train.py:334).  Tiles of TS samples (la rows of the node block and
+// (s_mask, train.py:220).  Tiles of TS samples (la rows of the node block and
 // column rows) arrive by cp.async.bulk into a 2-stage ring.  The products'
 // reshare zero shares are not drawn here: their per-sample stream telescopes
 // (F(t) = H(t+1) - H(t)) and k_count_alpha adds the
@@ -396,7 +397,7 @@ namespace gt {
 namespace {
 
 // ---------------------------------------------------------------------------
-// per-node heuristic (_heuristic_mpc, train.py:346-388) + replace, in three
+// per-node heuristic (_heuristic_mpc, train.py:232-274) + replace, in three
 // kernels so no thread waits on another's serial chain:
 //   k_hc_pre   one CTA per node: counter assembly; warp 0 runs the short
 //              probe/featureless/should_split/new_f chain, warp 1 replace;
@@ -560,7 +561,7 @@ __device__ __forceinline__ const W2* stage_node_tape(const W2* g, int len, W2* d
 }
 
 // c_orig cell e = (row r, column k) of node n: c_start + the counters
-// assembled from the count partials (train.py:256, 336-343)
+// assembled from the count partials (train.py:142, 336-343)
 __device__ __forceinline__ uint64_t co_cell(const NodeArgs& a, int c, int n, int e) {
   const int nf = a.nf, cols = 2 * nf, W = cols + 1, C3 = 3 * cols;
   const uint64_t hs = (uint64_t)a.n_h;
@@ -580,7 +581,7 @@ __device__ __forceinline__ uint64_t co_cell(const NodeArgs& a, int c, int n, int
 //  y = 1 + i (one warp per feature i): the six counter cells of feature i
 //     are truncated by the public shift and ring_down'ed, the squares and the
 //     a*tot products formed, then P, Q and the Q == 0 fix for its two
-//     columns (train.py:366-381).  The warp first draws every Philox block
+//     columns (train.py:252-267).  The warp first draws every Philox block
 //     of the feature (truncations, products, eq, b2a: the live schedule's
 //     blocks) into shared memory in parallel, so the serial gadget chain
 //     only does arithmetic.
@@ -670,7 +671,7 @@ __device__ __forceinline__ void hc_pre_feature(const NodeArgs& a, int n, int fi,
     __syncwarp();
   }
   hc_ts_at(64 + 8 * a.level + 4, tsw);
-  // counters: truncate by the public shift, ring_down      train.py:366-370
+  // counters: truncate by the public shift, ring_down      train.py:252-256
   if (wl < 6) {
     const int e = cell_e(wl);
     A3 x = a3(co_cell(a, 0, n, e), co_cell(a, 1, n, e), co_cell(a, 2, n, e));
@@ -680,7 +681,7 @@ __device__ __forceinline__ void hc_pre_feature(const NodeArgs& a, int n, int fi,
   }
   __syncwarp();
   auto C32 = [&](int q) { return a3(c32[0][q], c32[1][q], c32[2][q]); };
-  // prods = mul([c32, a], [c32, tot_rep])                   train.py:371-376
+  // prods = mul([c32, a], [c32, tot_rep])                   train.py:257-262
   if (wl < 8) {
     A3 x, y;
     if (wl < 6) {
@@ -697,7 +698,7 @@ __device__ __forceinline__ void hc_pre_feature(const NodeArgs& a, int n, int fi,
     for (int c = 0; c < 3; ++c) pr[c][wl] = z.v[c];
   }
   __syncwarp();
-  // P = a^2 - m0^2 - m1^2, qsafe = Q + b2a(eq(Q, 0))       train.py:377-381
+  // P = a^2 - m0^2 - m1^2, qsafe = Q + b2a(eq(Q, 0))       train.py:263-267
   if (wl < 2) {
     auto PR = [&](int p) { return a3(pr[0][p], pr[1][p], pr[2][p]); };
     const A3 p = diff<SL>(diff<SL>(PR(wl), PR(2 + wl)), PR(4 + wl));
@@ -729,7 +730,7 @@ __global__ void __launch_bounds__(64) k_hc_pre(NodeArgs a) {
       if (warp == 0) hc_pre_feature<SL>(a, n, fi, Ks, nullptr);
       return;
     }
-    // fused division (train.py:382): warp j divides column 2fi + j from its
+    // fused division (train.py:268): warp j divides column 2fi + j from its
     // precomputed lane tape, bulk-copied before the wait for the contraction
     extern __shared__ __align__(128) W2 dts[];  // [2][div_tape_blocks]
     __shared__ __align__(8) uint64_t dbar[2];
@@ -792,7 +793,7 @@ __global__ void __launch_bounds__(64) k_hc_pre(NodeArgs a) {
   if (tid < 32) {
     const int wl = tid;
     if (!a.last && !a.co_out) {
-      // zeros = eq([psi0, psi1, F - LEAF], 0)                 train.py:353-359
+      // zeros = eq([psi0, psi1, F - LEAF], 0)                 train.py:239-245
       const A3 fl = ld3s(a.f, hs, n);
       B3 z = {{0, 0, 0}};
       if (wl < 3) {
@@ -816,7 +817,7 @@ __global__ void __launch_bounds__(64) k_hc_pre(NodeArgs a) {
         act.v[c] = __shfl_sync(0xffffffffu, z.v[c], 2) & 1ull;
       }
       if (wl == 0) {
-        // featureless = and_reduce(~gam), leafish, should_split   train.py:360-364
+        // featureless = and_reduce(~gam), leafish, should_split   train.py:246-250
         const B3 gam = ldb3s(a.gam, hs, n);
         B3 ss;
         A3 nfv;
@@ -847,7 +848,7 @@ __global__ void __launch_bounds__(64) k_hc_pre(NodeArgs a) {
     return;
   }
   const int wl = tid - 32;
-  // replace: empty nodes adopt the parent's effective counters  train.py:269-276
+  // replace: empty nodes adopt the parent's effective counters  train.py:155-162
   if (a.level > 0) {
     A3 ca = a3(0, 0, 0);
     const W2* rb = nt ? nt + NT.rep : nullptr;
@@ -890,7 +891,7 @@ __global__ void __launch_bounds__(32 * DIV_WARPS) k_hc_div(NodeArgs a) {
   const uint64_t li = (uint64_t)blockIdx.x * wpc + warp;
   if (li >= lanes) return;  // whole warp exits together
   hc_ts_at(64 + 8 * a.level + 6, a.ts && li == 0 && threadIdx.x == 0);
-  // terms = division(P, qsafe)                              train.py:382
+  // terms = division(P, qsafe)                              train.py:268
   A3 t;
   if (a.divtape) {
     // the lane's whole precomputed tape (ladder + Newton) comes in by one bulk
@@ -1125,7 +1126,7 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n, PostOut* 
     __syncthreads();
     mbar_wait(&pbar, 0);
   }
-  // scores + masked argmin (tournament)     train.py:383-385, gadgets.py:366-401
+  // scores + masked argmin (tournament)     train.py:269-271, gadgets.py:366-401
   hc_ts(0 + 8 * a.level, a.ts);
   const uint32_t SA = 13 + div_subs(a.d);
   const uint64_t worst = (1ull << (a.tau + 1)) & MS;
@@ -1188,7 +1189,7 @@ __device__ __forceinline__ void hc_post_body(const NodeArgs& a, int n, PostOut* 
   }
   hc_ts(2 + 8 * a.level, a.ts);
   const A3 sd = a3(ci[0], ci[nf], ci[2 * nf]);
-  // gamma &= ~[sd == k]                                     train.py:386-387
+  // gamma &= ~[sd == k]                                     train.py:272-273
   const uint32_t SH = SA + 2 + 5 * 7;
   const W2* pb = pt ? pt + 5 * nf + post_rounds_blocks<SL>(nf) : nullptr;  // budget blocks
   if (out) {  // the caller runs the budget clear beside the split
@@ -1239,17 +1240,49 @@ __global__ void __launch_bounds__(256) k_hc_post(NodeArgs a) {
   hc_post_body<SL>(a, blockIdx.x);
 }
 
-// grow policy: all_declined = open(and_reduce(~is_int over nodes)) (train.py:279-282)
-__global__ void k_node_stop(const uint64_t* hc, int n_h, Keys K, uint32_t op, uint64_t* out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  B3 w;
-  for (int c = 0; c < 3; ++c) {
-    uint64_t x = 0;
-    for (int n = 0; n < n_h; ++n) x |= (hc[c * (uint64_t)n_h + n] & 1ull) << n;
-    w.v[c] = x;
+// grow policy: all_declined = open(and_reduce(~is_int over nodes)) (train.py:164-168,
+// and_reduce gadgets.py:94-109).  One CTA, the level's n_h bit planes per
+// component in shared memory; level with k planes ANDs plane j with plane
+// j + k/2 (odd last plane carried).  Gate g (counted over all levels) draws
+// zero bit g & 63 of pair word (sub 0, field g >> 6, lane 0) -- for n_h <= 64
+// exactly the in-word and_reduce schedule.
+__global__ void __launch_bounds__(256) k_node_stop(const uint64_t* hc, int n_h, Keys K, uint32_t op, uint64_t* out) {
+  extern __shared__ uint8_t planes[];  // [2][3][n_h]
+  uint8_t* cur = planes;
+  uint8_t* nxt = planes + 3 * n_h;
+  for (int n = threadIdx.x; n < n_h; n += blockDim.x)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) cur[c * n_h + n] = (uint8_t)((hc[c * (uint64_t)n_h + n] & 1ull) ^ (c == 0));  // bnot
+  __syncthreads();
+  int k = n_h, off = 0;
+  while (k > 1) {
+    const int half = k >> 1;
+    for (int j = threadIdx.x; j < half; j += blockDim.x) {
+      const int g = off + j;
+      uint8_t z[3], a[3], b[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        z[i] = (uint8_t)((word(K.pair[i], op, 0, (uint32_t)(g >> 6), 0) >> (g & 63)) & 1ull);
+        a[i] = cur[i * n_h + j];
+        b[i] = cur[i * n_h + j + half];
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int q = (i + 1) % 3, p = (i + 2) % 3;
+        nxt[i * n_h + j] = (a[i] & b[i]) ^ (a[q] & b[i]) ^ (a[i] & b[q]) ^ z[i] ^ z[p];
+      }
+    }
+    if ((k & 1) && threadIdx.x == 0)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) nxt[i * n_h + half] = cur[i * n_h + k - 1];
+    __syncthreads();
+    uint8_t* t = cur;
+    cur = nxt;
+    nxt = t;
+    off += half;
+    k = half + (k & 1);
   }
-  const B3 r = and_reduce(K, op, 0, 0, 0, bnot(w, lowmask(n_h)), n_h);
-  out[0] = (r.v[0] ^ r.v[1] ^ r.v[2]) & 1ull;  // open_bits
+  if (threadIdx.x == 0) out[0] = (cur[0] ^ cur[n_h] ^ cur[2 * n_h]) & 1;  // open_bits
 }
 
 struct FinishArgs {
@@ -1283,7 +1316,7 @@ __device__ __forceinline__ void node_finish_body(const FinishArgs& a, int n) {
     const int off = a.labels ? NT.lab : NT.spl, len = a.labels ? NT.total - NT.lab : NT.lab - NT.spl;
     nt = stage_node_tape(a.nodetape + (uint64_t)n * NT.total + off, len, nsb, &nbar);
   }
-  if (a.labels && a.lab) {  // labels from the trusted helper (train.py:301-302)
+  if (a.labels && a.lab) {  // labels from the trusted helper (train.py:187-188)
     if (tid == 0) {
       st3s(a.T, a.slots, slot, ld3s(a.lab, hs, n));
       st3s(a.F, a.slots, slot, ld3s(a.f, hs, n));
@@ -1291,7 +1324,7 @@ __device__ __forceinline__ void node_finish_body(const FinishArgs& a, int n) {
     return;
   }
   if (a.labels) {
-    // labels = b2a(lt(psi0, psi1)) on effective counters      train.py:300-306
+    // labels = b2a(lt(psi0, psi1)) on effective counters      train.py:186-192
     if (tid < 32) {  // warp 0 (the staged lt pairs its operands on neighbouring lanes)
       const uint32_t op = op_id(a.level, SITE_LABELS);
       const A3 psi0 = add<64>(CE(cols), CE(cols + 1)), psi1 = add<64>(CE(2 * cols), CE(2 * cols + 1));
@@ -1310,14 +1343,14 @@ __device__ __forceinline__ void node_finish_body(const FinishArgs& a, int n) {
   for (int c = 0; c < 3; ++c) ss.v[c] = a.hc[(0 * 3 + c) * hs + n];
   const uint64_t cs = 2 * hs;  // children per level
   // the three selects of split:h are independent chains: one per warp
-  if (tid == 0) {  // payload T = is_int ? sd : filler        (train.py:287)
+  if (tid == 0) {  // payload T = is_int ? sd : filler        (train.py:173)
     const A3 sd = ld3s(a.hc + 3 * hs, hs, n);
     const uint64_t fl = a.filler[slot];
     const A3 cb = nt ? a3(0, 0, 0) : b2a<64>(K, op, 0, n, ss);
     st3s(a.T, a.slots, slot, nt ? select_arith<64>(nt, a3_const(fl), sd, ss)
                                 : select_with<64>(K, op, 0, 0, n, a3_const(fl), sd, cb));
     st3s(a.F, a.slots, slot, ld3s(a.hc + 6 * hs, hs, n));
-  } else if (tid == 32) {  // child type = is_int ? LEAF : DUMMY  (train.py:288-289)
+  } else if (tid == 32) {  // child type = is_int ? LEAF : DUMMY  (train.py:174-175)
     const A3 cf = nt ? select_arith<64>(nt + 5, a3_const(F_DUMMY), a3_const(F_LEAF), ss)
                      : select_with<64>(K, op, 2, 0, n, a3_const(F_DUMMY), a3_const(F_LEAF), b2a<64>(K, op, 2, n, ss));
     const A3 ng = ld3s(a.hc + 9 * hs, hs, n);
@@ -1331,7 +1364,7 @@ __device__ __forceinline__ void node_finish_body(const FinishArgs& a, int n) {
   }
   __syncthreads();
   hc_ts(6 + 8 * a.level, a.ts);
-  // child counters = select(c_eff, 0, is_int)                 train.py:290
+  // child counters = select(c_eff, 0, is_int)                 train.py:176
   const A3 cav = a3(ca[0], ca[1], ca[2]);
   for (int e = tid; e < C3; e += bd) {
     A3 cc;
@@ -1354,9 +1387,9 @@ __global__ void __launch_bounds__(128) k_node_finish(FinishArgs a) {
 
 // scores / argmin / budget clear, then split, in one launch per level (fixed
 // policy, mpc heuristic): the node's CTA continues from sd to its children
-// Budget clear (gamma &= ~[sd == k], train.py:386-387) on warps 0-1 while
+// Budget clear (gamma &= ~[sd == k], train.py:272-273) on warps 0-1 while
 // warps 4-6 run the split's three independent chains (payload, child type,
-// child-counter condition, train.py:287-290); the children's gamma is stored
+// child-counter condition, train.py:173-176); the children's gamma is stored
 // after the join.  Same gadgets and blocks as the sequential path.
 template <int SL>
 __device__ __forceinline__ void post_split_fused(const NodeArgs& na, const FinishArgs& a, int n, const PostOut& po,
@@ -1419,13 +1452,13 @@ __device__ __forceinline__ void post_split_fused(const NodeArgs& na, const Finis
         ngs[c] = ng.v[c];
       }
     }
-  } else if (tid == 128) {  // payload T = is_int ? sd : filler        (train.py:287)
+  } else if (tid == 128) {  // payload T = is_int ? sd : filler        (train.py:173)
     const uint64_t fl = a.filler[slot];
     const A3 cb = nt ? a3(0, 0, 0) : b2a<64>(K, op, 0, n, ss);
     st3s(a.T, a.slots, slot, nt ? select_arith<64>(nt, a3_const(fl), po.sd, ss)
                                 : select_with<64>(K, op, 0, 0, n, a3_const(fl), po.sd, cb));
     st3s(a.F, a.slots, slot, ld3s(a.hc + 6 * hs, hs, n));
-  } else if (tid == 160) {  // child type = is_int ? LEAF : DUMMY  (train.py:288-289)
+  } else if (tid == 160) {  // child type = is_int ? LEAF : DUMMY  (train.py:174-175)
     const A3 cf = nt ? select_arith<64>(nt + 5, a3_const(F_DUMMY), a3_const(F_LEAF), ss)
                      : select_with<64>(K, op, 2, 0, n, a3_const(F_DUMMY), a3_const(F_LEAF), b2a<64>(K, op, 2, n, ss));
     for (int ch = 0; ch < 2; ++ch) st3s(a.f_nxt, cs, 2 * n + ch, cf);
@@ -1437,7 +1470,7 @@ __device__ __forceinline__ void post_split_fused(const NodeArgs& na, const Finis
   hc_ts(6 + 8 * a.level, a.ts);
   if (tid < 2)  // children's budget
     st3s(a.gam_nxt, cs, 2 * n + tid, a3(ngs[0], ngs[1], ngs[2]));
-  // child counters = select(c_eff, 0, is_int)                 train.py:290
+  // child counters = select(c_eff, 0, is_int)                 train.py:176
   const A3 cav = a3(ca[0], ca[1], ca[2]);
   for (int e = tid; e < C3; e += bd) {
     const A3 cev = e == tid ? ce : CE(e);
@@ -1810,7 +1843,7 @@ struct Prof {
 
 // Zero shares of the count products, summed over this shard's samples, one
 // thread per (node, column):
-//  elementwise (count_reshare 0, train.py:333): the product at (sample t,
+//  elementwise (count_reshare 0, train.py:219): the product at (sample t,
 //    node n, column w) is reshared with F_i(t) = H_i(t+1) - H_i(t),
 //    H_i(t) = pair_i word (op_cnt, sub 3, field w, lane t n_h + n), so
 //    sum_{t in [t0, t1)} F_i = H_i(t1) - H_i(t0) and sharded sums telescope;
@@ -1967,6 +2000,14 @@ struct Side {
   cudaStream_t cp = nullptr;  // host <-> device copies of the host-input entry
   cudaEvent_t ev[16] = {};
 };
+// One Side per device, shared by every trainer on that device: train_impl
+// holds the device's side lock for its whole host-side enqueue, so calls
+// from concurrent host threads never interleave their fork/join event
+// records (and the lazy creation below is race-free).
+std::recursive_mutex& side_lock(int dev) {
+  static std::recursive_mutex mu[64];
+  return mu[dev & 63];
+}
 int side_of(int dev, Side** out) {
   static Side sides[64];
   if (dev < 0 || dev >= 64) return fail_inval("device index out of range");
@@ -2152,7 +2193,7 @@ int launch_prep8(const gt_train_cfg& c, const uint64_t* features, const uint64_t
   return GT_OK;
 }
 
-int counter_shift(uint64_t n, int score_width, int tau) {  // train.py:189-192
+int counter_shift(uint64_t n, int score_width, int tau) {  // train.py:75-78
   int headroom = (score_width - tau - 2) / 2;
   int bl = 0;
   while (bl < 64 && (n >> bl)) ++bl;
@@ -2192,7 +2233,6 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
   if (c.n_total < 1) return fail_inval("dataset is empty");
   if (c.n_local > c.n_total || c.sample_base + c.n_local > c.n_total) return fail_inval("bad sample shard");
   if (c.policy != 0 && c.policy != 1) return fail_inval("policy must be fixed (0) or grow (1)");
-  if (c.policy == 1 && c.depth > 8) return fail_inval("grow policy supports depth <= 8");
   if (c.heuristic != 0 && c.heuristic != 1) return fail_inval("heuristic must be mpc (0) or tee (1)");
   if (c.count_reshare != 0 && c.count_reshare != 1) return fail_inval("count_reshare must be 0 or 1");
   if (c.count_engine != 0 && c.count_engine != 1) return fail_inval("count_engine must be 0 (tensor) or 1 (cuda)");
@@ -2229,6 +2269,8 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
   // contraction CTAs rarely co-reside, and the extra chunks cost more)
   static const bool no_side = getenv("GT_NO_SIDE") != nullptr;
   static const bool count_overlap = getenv("GT_COUNT_OVERLAP") != nullptr;
+  if (dev < 0 || dev >= 64) return fail_inval("device index out of range");
+  std::lock_guard<std::recursive_mutex> side_guard(side_lock(dev));
   {
     int rc = side_of(dev, &side);
     if (rc) return rc;
@@ -2517,7 +2559,10 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
       if (hrc) return fail_inval("trusted helper (split) failed");
     }
     if (!last && c.policy == 1) {
-      k_node_stop<<<1, 32, 0, s>>>(hc, n_h, K, op_id(level, SITE_STOP), ws + L.stop);
+      const int stop_smem = 6 * n_h;
+      if (stop_smem > 48 * 1024)
+        GT_CUDA_CHECK(cudaFuncSetAttribute(k_node_stop, cudaFuncAttributeMaxDynamicSharedMemorySize, stop_smem));
+      k_node_stop<<<1, 256, stop_smem, s>>>(hc, n_h, K, op_id(level, SITE_STOP), ws + L.stop);
       GT_LAUNCH_CHECK("k_node_stop");
       P.count_launch();
       uint64_t flag = 0;

@@ -60,7 +60,14 @@ def make_allreduce(trainer, group=None):
 
     def _cb(buf, count, stream, user):
         try:
-            allreduce_u64_(trainer.workspace_view(buf, int(count)), group)
+            import torch
+
+            # enqueue on the stream gt_train passes (its count kernels' stream), not
+            # torch's current one: the collective must be ordered after the partials
+            s = torch.cuda.ExternalStream(int(stream), device=trainer.device) if stream else \
+                torch.cuda.current_stream(trainer.device)
+            with torch.cuda.stream(s):
+                allreduce_u64_(trainer.workspace_view(buf, int(count)), group)
             return 0
         except Exception:  # noqa: BLE001 - reported to the C side as failure
             return 1
@@ -69,9 +76,10 @@ def make_allreduce(trainer, group=None):
 
 
 def train_sharded(X_local, Y_local, filler, cfg, keys, *, n_total: int, sample_base: int, group=None,
-                  trainer=None):
+                  trainer=None, stream=None):
     """Run one sample-sharded training step on this rank.  X_local
-    [3, n_local, nf], Y_local [3, n_local] device tensors.  Returns the
+    [3, n_local, nf], Y_local [3, n_local] device tensors; `stream` (default:
+    torch's current stream) orders the kernels and the allreduce.  Returns the
     trainer (T/F on trainer.T / trainer.F) and the trained depth."""
     from .train import DeviceTrainer
 
@@ -79,5 +87,5 @@ def train_sharded(X_local, Y_local, filler, cfg, keys, *, n_total: int, sample_b
         trainer = DeviceTrainer(int(X_local.shape[1]), int(X_local.shape[2]), cfg, n_total=n_total,
                                 sample_base=sample_base, device=X_local.device)
     cb = make_allreduce(trainer, group)
-    depth = trainer.run(X_local, Y_local, filler, keys, allreduce=cb)
+    depth = trainer.run(X_local, Y_local, filler, keys, allreduce=cb, stream=stream)
     return trainer, depth

@@ -1,88 +1,96 @@
 """Trusted split helper for heuristic "tee" (reference enclave.py:94-185,
-train.py:391-415).
+_heuristic_tee / _labels_tee train.py:277-301).
 
-The parties hand the helper their shares of the per-level node state; it
-reconstructs, picks every node's split EXACTLY (rational impurity, ties to
-the lower feature, tree.py:200-264), and hands back fresh shares of the
-decisions.  On B200 the three parties' shares already sit in one device
-buffer, so the "upload" is a device-to-host copy of the component arrays
-at the helper's call from ``gt_train`` (``gt_heuristic_fn``), and the
-"download" is a host-to-device copy of freshly drawn components.  The
-revealed tree therefore equals the exact plaintext trainer bit for bit
-(reference acceptance criterion 4, test_acceptance.py:180-193).
+The parties hand the helper their shares of a level's node state; it
+reconstructs them, decides every node's split exactly, and hands back fresh
+shares of the decisions.  On B200 the three parties' shares already sit in
+one device buffer, so the "upload" is a device-to-host copy of the component
+arrays at the helper's call from ``gt_train`` (``gt_heuristic_fn``) -- made
+on the stream ``gt_train`` passes -- and the "download" a host-to-device copy
+of freshly drawn components.
+
+The split rule is the reference's (tree.py:200-264: additive Gini
+sum_j (a_j^2 - m0_j^2 - m1_j^2) / (a_j * tot) over the non-empty branches,
+an empty node or a spent feature scores 2, leftmost strict minimum; split
+iff the node is a live leaf, impure and has features left; majority label
+with ties to 0) evaluated as whole-level integer arrays: every score is a
+fraction num/den with den > 0, and candidates are compared by exact
+cross-multiplication on Python integers (object arrays), so there is no
+rounding and no per-node loop.
 """
 
 from __future__ import annotations
 
 import hashlib
-from fractions import Fraction
-from typing import List, Sequence, Tuple
+from typing import Tuple
 
 import numpy as np
 
 from . import _native
 
-F_INTERNAL, F_LEAF, F_DUMMY = 0, 1, 2  # tree.py:40-42
-WORST_SCORE = Fraction(2)  # tree.py:44
+F_INTERNAL, F_LEAF, F_DUMMY = 0, 1, 2  # node types, tree.py:40-42
 
 
 class EnclaveError(RuntimeError):
     """enclave.py:43-44."""
 
 
-def plaintext_gini(c, feature: int) -> Fraction:
-    """Additive-form impurity of splitting on `feature` (tree.py:200-218)."""
-    a0, a1 = int(c[0][2 * feature]), int(c[0][2 * feature + 1])
-    total = a0 + a1
-    if total == 0:
-        return WORST_SCORE
-    score = Fraction(0)
-    for j, a in ((0, a0), (1, a1)):
-        if a == 0:
-            continue
-        m0 = int(c[1][2 * feature + j])
-        m1 = int(c[2][2 * feature + j])
-        score += Fraction(a * a - m0 * m0 - m1 * m1, a * total)
-    return score
+def score_fractions(C: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+    """Exact per-(node, feature) impurity as (numerator, denominator) object
+    arrays.  C: (n, 3, 2nf) exact counters, rows = all / label 0 / label 1,
+    columns (2i + j) = feature i takes value j."""
+    C = np.asarray(C).astype(object)
+    a, m0, m1 = C[:, 0, 0::2], C[:, 1, 0::2], C[:, 2, 0::2]  # branch j = 0
+    b, n0, n1 = C[:, 0, 1::2], C[:, 1, 1::2], C[:, 2, 1::2]  # branch j = 1
+    tot = a + b
+    pa = np.where(a > 0, a * a - m0 * m0 - m1 * m1, 0)
+    pb = np.where(b > 0, b * b - n0 * n0 - n1 * n1, 0)
+    da, db = np.where(a > 0, a, 1), np.where(b > 0, b, 1)
+    num, den = pa * db + pb * da, da * db * tot
+    empty = tot == 0
+    return np.where(empty, 2, num), np.where(empty, 1, den)
 
 
-def split_decisions(counters: Sequence, gammas: np.ndarray, types: np.ndarray
-                    ) -> Tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray]:
-    """Per-node split choice from exact counters (tree.py:221-254)."""
-    n = len(counters)
-    nf = gammas.shape[1]
-    sd = np.zeros(n, dtype=np.uint64)
-    new_f = np.array(types, dtype=np.uint64, copy=True)
-    is_int = np.zeros(n, dtype=bool)
-    new_g = np.array(gammas, dtype=bool, copy=True)
-    for k in range(n):
-        c = counters[k]
-        psi0 = int(c[1][0]) + int(c[1][1])
-        psi1 = int(c[2][0]) + int(c[2][1])
-        pure = psi0 == 0 or psi1 == 0
-        featureless = not gammas[k].any()
-        split = int(types[k]) == F_LEAF and not (pure or featureless)
-        best, best_score = 0, WORST_SCORE
-        for i in range(nf):
-            score = plaintext_gini(c, i) if gammas[k, i] else WORST_SCORE
-            if score < best_score:
-                best, best_score = i, score
-        sd[k] = best
-        if split:
-            is_int[k] = True
-            new_f[k] = F_INTERNAL
-            new_g[k, best] = False
-    return sd, new_f, is_int, new_g
+def best_features(C: np.ndarray, gammas: np.ndarray) -> np.ndarray:
+    """Leftmost strict argmin of the scores over the features still in each
+    node's budget (spent features score 2, like an empty node)."""
+    num, den = score_fractions(C)
+    gam = np.asarray(gammas, dtype=bool)
+    num, den = np.where(gam, num, 2), np.where(gam, den, 1)
+    n, nf = num.shape
+    best = np.zeros(n, dtype=np.int64)
+    bn, bd = np.full(n, 2, dtype=object), np.ones(n, dtype=object)
+    for i in range(nf):
+        win = (num[:, i] * bd) < (bn * den[:, i])
+        best = np.where(win, i, best)
+        bn, bd = np.where(win, num[:, i], bn), np.where(win, den[:, i], bd)
+    return best
 
 
-def majority_labels(counters: Sequence) -> np.ndarray:
-    """Majority class per node, ties to 0 (tree.py:257-264)."""
-    out = np.zeros(len(counters), dtype=np.uint64)
-    for k, c in enumerate(counters):
-        psi0 = int(c[1][0]) + int(c[1][1])
-        psi1 = int(c[2][0]) + int(c[2][1])
-        out[k] = 1 if psi1 > psi0 else 0
-    return out
+def label_totals(C: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+    """(psi0, psi1): samples of label 0 / label 1 at each node (feature 0's
+    two cells of rows 1 and 2 partition the node)."""
+    C = np.asarray(C).astype(object)
+    return C[:, 1, 0] + C[:, 1, 1], C[:, 2, 0] + C[:, 2, 1]
+
+
+def split_decisions(C: np.ndarray, gammas: np.ndarray, types: np.ndarray):
+    """Whole-level split decisions -> (sd, new_type, is_internal, new_gammas)."""
+    gam = np.array(gammas, dtype=bool)
+    kinds = np.asarray(types, dtype=np.uint64)
+    psi0, psi1 = label_totals(C)
+    sd = best_features(C, gam)
+    grow = (kinds == F_LEAF) & (psi0 != 0) & (psi1 != 0) & gam.any(axis=1)
+    rows = np.nonzero(grow)[0]
+    gam[rows, sd[rows]] = False
+    new_f = np.where(grow, np.uint64(F_INTERNAL), kinds).astype(np.uint64)
+    return sd.astype(np.uint64), new_f, grow, gam
+
+
+def majority_labels(C: np.ndarray) -> np.ndarray:
+    """1 where label-1 samples strictly outnumber label-0 samples, else 0."""
+    psi0, psi1 = label_totals(C)
+    return (psi1 > psi0).astype(np.uint64)
 
 
 class DeviceEnclave:
@@ -94,55 +102,65 @@ class DeviceEnclave:
         digest = hashlib.sha256(seed + b"/b200-enclave").digest()
         self.rng = np.random.Generator(np.random.PCG64(int.from_bytes(digest[:16], "little")))
         self.calls = 0
+        self.error = None
         self._fn = _native.HEURISTIC_FN(self._call)
 
     @property
     def fn(self):
         return self._fn
 
-    # -- plumbing ------------------------------------------------------------
-    def _words(self, shape) -> np.ndarray:
-        return self.rng.integers(0, 1 << 63, shape, dtype=np.uint64) * np.uint64(2) + \
+    def _random(self, shape, mask=None) -> np.ndarray:
+        w = self.rng.integers(0, 1 << 63, shape, dtype=np.uint64) * np.uint64(2) + \
             self.rng.integers(0, 2, shape, dtype=np.uint64)
+        return w if mask is None else w & np.uint64(mask)
 
-    def _share_words(self, values: np.ndarray) -> np.ndarray:
+    def _arith(self, values) -> np.ndarray:
         v = np.asarray(values, dtype=np.uint64)
-        s1, s2 = self._words(v.shape), self._words(v.shape)
-        return np.stack([s1, s2, v - s1 - s2])
+        r1, r2 = self._random(v.shape), self._random(v.shape)
+        return np.stack([r1, r2, v - r1 - r2])
 
-    def _share_bitwords(self, words: np.ndarray, mask: int) -> np.ndarray:
+    def _xor(self, words, mask: int) -> np.ndarray:
         w = np.asarray(words, dtype=np.uint64)
-        m = np.uint64(mask)
-        s1, s2 = self._words(w.shape) & m, self._words(w.shape) & m
-        return np.stack([s1, s2, w ^ s1 ^ s2])
+        r1, r2 = self._random(w.shape, mask), self._random(w.shape, mask)
+        return np.stack([r1, r2, w ^ r1 ^ r2])
 
-    def _view(self, addr: int, count: int):
-        return self.trainer.workspace_view(addr, count)
+    def _fetch(self, addr: int, count: int, stream) -> np.ndarray:
+        torch = _native.require_cuda()
+        with torch.cuda.stream(stream):
+            host = self.trainer.workspace_view(addr, count).to("cpu")  # synchronous on `stream`
+        return host.numpy().view(np.uint64)
 
-    # -- gt_heuristic_fn -----------------------------------------------------
+    def _store(self, addr: int, arr: np.ndarray, stream) -> None:
+        torch = _native.require_cuda()
+        src = torch.from_numpy(np.ascontiguousarray(arr.reshape(-1)).view(np.int64))
+        with torch.cuda.stream(stream):
+            self.trainer.workspace_view(addr, src.numel()).copy_(src)
+        stream.synchronize()
+
+    # gt_heuristic_fn(op, level, n, nf, counters, gamma, types, out, stream, user)
     def _call(self, op, level, n, nf, counters, gamma, types, out, stream, user):
         try:
+            torch = _native.require_cuda()
+            s = torch.cuda.ExternalStream(int(stream or 0), device=self.trainer.device) if stream else \
+                torch.cuda.current_stream(self.trainer.device)
             self.calls += 1
             cells = n * 3 * 2 * nf
-            comp = self._view(counters, 3 * cells).cpu().numpy().view(np.uint64).reshape(3, n, 3, 2 * nf)
-            C = comp.sum(axis=0, dtype=np.uint64)  # reconstruct (enclave.py:104-114)
-            rows = [[[int(v) for v in C[k, r]] for r in range(3)] for k in range(n)]
-            if op == 1:
-                gw = self._view(gamma, 3 * n).cpu().numpy().view(np.uint64).reshape(3, n)
-                tw = self._view(types, 3 * n).cpu().numpy().view(np.uint64).reshape(3, n)
-                gwords = gw[0] ^ gw[1] ^ gw[2]
-                gammas = ((gwords[:, None] >> np.arange(nf, dtype=np.uint64)[None, :]) & np.uint64(1)).astype(bool)
-                kinds = tw.sum(axis=0, dtype=np.uint64)
-                sd, new_f, is_int, new_g = split_decisions(rows, gammas, kinds)
-                gword = (new_g.astype(np.uint64) << np.arange(nf, dtype=np.uint64)[None, :]).sum(axis=1, dtype=np.uint64)
-                res = np.stack([self._share_bitwords(is_int.astype(np.uint64), 1), self._share_words(sd),
-                                self._share_words(new_f), self._share_bitwords(gword, (1 << nf) - 1)])
-                self._view(out, 12 * n).copy_(_native.require_cuda().from_numpy(res.reshape(-1).view(np.int64)))
-            elif op == 2:
-                res = self._share_words(majority_labels(rows))
-                self._view(out, 3 * n).copy_(_native.require_cuda().from_numpy(res.reshape(-1).view(np.int64)))
+            C = self._fetch(counters, 3 * cells, s).reshape(3, n, 3, 2 * nf).sum(axis=0, dtype=np.uint64)
+            if op == 1:  # split decisions (enclave.py:161-180)
+                gw = np.bitwise_xor.reduce(self._fetch(gamma, 3 * n, s).reshape(3, n), axis=0)
+                kinds = self._fetch(types, 3 * n, s).reshape(3, n).sum(axis=0, dtype=np.uint64)
+                bits = np.arange(nf, dtype=np.uint64)
+                gammas = ((gw[:, None] >> bits[None, :]) & np.uint64(1)).astype(bool)
+                sd, new_f, is_int, new_g = split_decisions(C, gammas, kinds)
+                gword = np.bitwise_or.reduce(new_g.astype(np.uint64) << bits[None, :], axis=1) if nf else \
+                    np.zeros(n, dtype=np.uint64)
+                res = np.stack([self._xor(is_int.astype(np.uint64), 1), self._arith(sd), self._arith(new_f),
+                                self._xor(gword, (1 << nf) - 1)])
+            elif op == 2:  # leaf labels (enclave.py:182-186)
+                res = self._arith(majority_labels(C))
             else:
                 raise EnclaveError(f"unknown enclave op {op}")
+            self._store(out, res, s)
             return 0
         except Exception as e:  # noqa: BLE001 - surfaced as a failed call
             self.error = e

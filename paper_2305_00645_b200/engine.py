@@ -2,8 +2,8 @@
 
 The reference runs the same protocol body on three party threads
 (``run_local``, rss.py:496-542) and each body calls ``train_tree(eng, X, y,
-cfg)`` (train.py:222) or ``infer_batch(eng, levels, queries)``
-(infer.py:91) on its own share pair.  Here the three co-resident parties meet
+cfg)`` (train.py:108) or ``infer_batch(eng, levels, queries)``
+(infer.py:20) on its own share pair.  Here the three co-resident parties meet
 at a rendezvous -- the pattern of the reference's ``EnclaveBridge``
 (transport.py:304-342): the three engines hand in their pairs, the last one
 to arrive checks replication consistency, runs ONE device call for all three
@@ -24,7 +24,7 @@ import numpy as np
 from .ledger import REF_LANE_LIMIT, Ledger, Metrics, Transcript
 from .seeds import PARTIES, SeedSetup, derive_seed, filler_values, make_keys
 from .shares import RING64, AVec, ShareError, avecs_from_components, components_from_avecs, ring_of
-from .train import TrainConfig, TrainResult, resolved_depth, train_components
+from .train import TrainConfig, TrainResult, as_config, resolved_depth, train_components
 
 
 class TransportError(RuntimeError):
@@ -120,6 +120,14 @@ class _Phase:
         return False
 
 
+def _own(eng) -> "PartyEngine":
+    if not isinstance(eng, PartyEngine):
+        raise TransportError("the B200 drop-ins run the three parties co-resident on the device: call them "
+                             "from a body executed by this package's run_local (the reference's TCP seats "
+                             "are not a B200 transport)")
+    return eng
+
+
 @dataclass
 class LocalRun:
     results: List
@@ -170,8 +178,11 @@ def run_local(fn: Callable[[PartyEngine], object], *, seeds: Union[SeedSetup, in
 
 
 def train_tree(eng: PartyEngine, features, labels, cfg: TrainConfig) -> TrainResult:
-    """Per-party drop-in for train.py:222 (SPMD; all three parties call it)."""
+    """Per-party drop-in for train.py:108 (SPMD; all three parties call it).
+    `cfg` may be this package's TrainConfig or the reference's own."""
+    _own(eng)
     n_samples, nf = features.shape
+    cfg = as_config(cfg)
 
     def compute(payloads):
         X = components_from_avecs([p[0] for p in payloads])
@@ -187,7 +198,8 @@ def train_tree(eng: PartyEngine, features, labels, cfg: TrainConfig) -> TrainRes
 
 
 def infer_batch(eng: PartyEngine, levels: List, queries) -> AVec:
-    """Per-party drop-in for infer.py:91 (levels sizes 1, 2, 4, ...)."""
+    """Per-party drop-in for infer.py:20 (levels sizes 1, 2, 4, ...)."""
+    _own(eng)
     n_queries, nf = queries.shape
     depth = len(levels)
 
@@ -202,6 +214,53 @@ def infer_batch(eng: PartyEngine, levels: List, queries) -> AVec:
         return avecs_from_components(out, ring_of(levels[0]))
 
     return eng._bridge.call(eng.party, "infer_batch", (levels, queries), compute)
+
+
+def _lookup(eng: PartyEngine, name: str, table, idx, per_row: bool):
+    _own(eng)
+    ring = ring_of(table)
+    shape = tuple(idx.shape)
+
+    def compute(payloads):
+        from . import gadgets as G
+        from .shares import from_device, to_device
+
+        tab = components_from_avecs([p[0] for p in payloads])
+        ix = components_from_avecs([p[1] for p in payloads]).reshape(3, -1)
+        keys = make_keys(eng.seeds, eng.dealer_seed)
+        op = 0x40000000 | eng._ledger.round_no  # fresh randomness per call site
+        dev = eng.device if eng.device is not None else "cuda"
+        if per_row:
+            out = G.row_lookup(ring.width, to_device(tab, dev), to_device(ix, dev), keys=keys, op=op)
+        else:
+            out = G.oaa(ring.width, to_device(tab.reshape(3, -1), dev), to_device(ix, dev), keys=keys, op=op)
+        if eng._phase:  # the caller's phase tags the records, as in the reference transcript
+            with eng._ledger.phase(eng._phase[-1]):
+                eng._ledger.oaa(ix.shape[1], tab.shape[-1], ring.width)
+        else:
+            eng._ledger.oaa(ix.shape[1], tab.shape[-1], ring.width)
+        return avecs_from_components(from_device(out).reshape((3,) + shape), ring)
+
+    return eng._bridge.call(eng.party, name, (table, idx), compute)
+
+
+def oaa(eng: PartyEngine, table, idx) -> AVec:
+    """Per-party drop-in for oaa.py:20-35: shares of table[idx], zero where
+    idx is out of range (ValueError unless `table` is one-dimensional)."""
+    _own(eng)
+    if len(table.shape) != 1:
+        raise ValueError("table must be one-dimensional")
+    return _lookup(eng, "oaa", table, idx, per_row=False)
+
+
+def row_lookup(eng: PartyEngine, rows, idx) -> AVec:
+    """Per-party drop-in for oaa.py:38-55: out[i] = rows[i][idx[i]]."""
+    _own(eng)
+    if len(rows.shape) != 2:
+        raise ValueError("rows must be two-dimensional")
+    if idx.size != rows.shape[0]:
+        raise ValueError("one index per row required")
+    return _lookup(eng, "row_lookup", rows, idx, per_row=True)
 
 
 def open_results(run: LocalRun, pick=lambda r: r) -> np.ndarray:

@@ -1,6 +1,6 @@
 """Secure batch inference on B200 (reference pkg/src/obtree/infer.py).
 
-The whole always-descend walk (``infer_batch``, infer.py:91-106) is one fused
+The whole always-descend walk (``infer_batch``, infer.py:20-35) is one fused
 sm_100a kernel (``gt_infer``): the encoded tree stays in shared memory, each
 query's level payload and feature bit are fetched with oblivious full-scan
 lookups, and no collective is needed -- instances are independent, so a
@@ -19,7 +19,7 @@ from .shares import RING64, components_from_pairs, from_device, pairs_from_compo
 
 
 def inference_needs(n_queries: int, depth: int, n_columns: int) -> dict:
-    """Lane counts of the walk per gadget (infer.py:109-114): eq / select
+    """Lane counts of the walk per gadget (infer.py:38-43): eq / select
     lanes of the oblivious lookups, for reporting."""
     lanes = n_queries * (((1 << depth) - 1) + depth * (n_columns - 1))
     return {("edabit", 64): lanes, ("dabit", 64): lanes}

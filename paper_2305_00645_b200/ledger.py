@@ -11,7 +11,7 @@ same (round, sender, receiver, nbytes, tag) records the reference's
 B200 run reports sit next to the reference's like for like.
 
 ``lane_limit`` reproduces the reference's chunking of wide lane batches
-(oaa.py:58-63, train.py:321-335); ``lane_limit=None`` is the device schedule
+(oaa.py:58-63, train.py:207-221); ``lane_limit=None`` is the device schedule
 (every gadget call is a single batch, so fewer rounds, same bytes up to the
 bit-packing of partial bytes).
 """
@@ -238,7 +238,7 @@ class Ledger:
     row_lookup = oaa  # oaa.py:38-55 has the identical message pattern
 
     # -- protocols ------------------------------------------------------------
-    def count_level(self, n: int, n_nodes: int, nf: int, dot: bool = False) -> None:  # train.py:315-343
+    def count_level(self, n: int, n_nodes: int, nf: int, dot: bool = False) -> None:  # train.py:201-229
         width = 2 * nf + 1
         self.eq(n_nodes, 64)
         if self.lane_limit is None:
@@ -256,7 +256,7 @@ class Ledger:
             self.mul(n_nodes * width, 64, "count.mul")
 
     def heuristic_mpc(self, n_nodes: int, nf: int, n_samples: int, tau: int, score_width: int) -> None:
-        cols = 2 * nf  # train.py:346-388
+        cols = 2 * nf  # train.py:232-274
         self.eq(3 * n_nodes, 64)
         self.and_reduce(nf, n_nodes)
         self.or_bits(n_nodes)
@@ -274,19 +274,19 @@ class Ledger:
         self.eq(n_nodes * nf, 64)
         self.and_bits(n_nodes * nf)
 
-    def heuristic_tee(self, n_nodes: int, nf: int) -> None:  # train.py:391-406, enclave.py:60-86
+    def heuristic_tee(self, n_nodes: int, nf: int) -> None:  # train.py:277-292, enclave.py:60-86
         cells = n_nodes * 3 * 2 * nf
         up = 16 + 16 * cells + 2 * n_nodes * nf + 16 * n_nodes
         down = 16 * n_nodes + 16 * n_nodes + 2 * n_nodes + 2 * n_nodes * nf
         self.enclave_call(up, down, "hc_tee")
 
-    def labels_tee(self, n_nodes: int, nf: int) -> None:  # train.py:409-415
+    def labels_tee(self, n_nodes: int, nf: int) -> None:  # train.py:295-301
         self.enclave_call(16 + 16 * n_nodes * 3 * 2 * nf, 16 * n_nodes, "labels_tee")
 
     def train(self, n: int, nf: int, depth: int, tau: int = 10, score_width: int = 32,
               grow_stop_level: Optional[int] = None, policy: str = "fixed", heuristic: str = "mpc",
               count_reshare: str = "elementwise") -> int:
-        """train_tree (train.py:222-311).  Under the grow policy the opened
+        """train_tree (train.py:108-197).  Under the grow policy the opened
         stop bit is data dependent; pass the level the run stopped at."""
         with self.phase("count:0"):
             self.mul(n * nf, 64, "count.mul")
@@ -331,7 +331,7 @@ class Ledger:
             return level + 1
         raise AssertionError("unreachable")
 
-    def infer(self, n: int, nf: int, depth: int) -> None:  # infer.py:91-106
+    def infer(self, n: int, nf: int, depth: int) -> None:  # infer.py:20-35
         for t in range(depth):
             with self.phase(f"walk:{t}"):
                 self.oaa(n, 1 << t, 64)
@@ -352,7 +352,7 @@ def div_params(width: int, tau: int) -> Dict[str, int]:
 
 
 def counter_shift(n_samples: int, score_width: int = 32, tau: int = 10) -> int:
-    """train.py:189-192."""
+    """train.py:75-78."""
     headroom = (score_width - tau - 2) // 2
     return max(0, int(n_samples).bit_length() - headroom)
 

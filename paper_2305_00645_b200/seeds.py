@@ -101,7 +101,7 @@ def filler_values(seed: bytes, total: int, n_columns: int) -> np.ndarray:
 
 
 def share_values(values: np.ndarray, width: int, seed: bytes):
-    """The reference dealer's input split (dealer.py:619-623): AES-CTR stream
+    """The reference dealer's input split (dealer.py:259-263): AES-CTR stream
     of derive_seed(seed, "input"); s1, s2 = next n words each, s3 = v - s1 - s2.
     Returns the three parties' (lo, hi) pairs."""
     mask = np.uint64((1 << width) - 1) if width < 64 else np.uint64(0xFFFFFFFFFFFFFFFF)

@@ -1,9 +1,9 @@
 """Secure level-wise training on B200 (reference pkg/src/obtree/train.py).
 
 ``TrainConfig`` / ``TrainResult`` / ``counter_shift`` / ``resolved_depth`` /
-``levels_of`` keep the reference's names and meaning (train.py:171-204).
+``levels_of`` keep the reference's names and meaning (train.py:57-90).
 The level loop itself (partition -> count -> heuristic -> replace -> split /
-labels, train.py:222-311) runs natively: ``gt_train`` in the C ABI drives the
+labels, train.py:108-197) runs natively: ``gt_train`` in the C ABI drives the
 sm_100a kernels level by level on one CUDA stream, calling back only for the
 per-level count allreduce of a sample-sharded run.
 """
@@ -23,7 +23,7 @@ from .shares import RING32, RING64, AVec, Ring, components_from_pairs, from_devi
 
 @dataclass
 class TrainConfig:
-    """train.py:171-179."""
+    """train.py:57-65."""
 
     depth: int = 4
     tau: int = 10
@@ -33,7 +33,7 @@ class TrainConfig:
     score_ring: Ring = RING32
     count_ring: Ring = RING64
     # B200 extension: "elementwise" reshares every count product like the
-    # reference (train.py:333); "dot" sums the local products over samples
+    # reference (train.py:219); "dot" sums the local products over samples
     # first and reshares each counter cell once (ABY3-style dot product) --
     # same revealed tree, a fraction of the reshared words.
     count_reshare: str = "elementwise"
@@ -45,21 +45,37 @@ class TrainConfig:
 
 @dataclass
 class TrainResult:
-    """train.py:182-186 (T, F per party as AVec in the drop-in path)."""
+    """train.py:68-72 (T, F per party as AVec in the drop-in path)."""
 
     T: object
     F: object
     depth: int
 
 
+def as_config(cfg) -> TrainConfig:
+    """Accept the reference's own TrainConfig (train.py:57-65) -- or any
+    object with its fields -- where a TrainConfig is expected; the B200-only
+    knobs take their defaults."""
+    if isinstance(cfg, TrainConfig):
+        return cfg
+    out = TrainConfig()
+    for name in ("depth", "tau", "heuristic", "policy", "max_depth", "count_reshare", "count_engine"):
+        if hasattr(cfg, name):
+            setattr(out, name, getattr(cfg, name))
+    for name in ("score_ring", "count_ring"):
+        if hasattr(cfg, name):
+            setattr(out, name, Ring(int(getattr(cfg, name).width)))
+    return out
+
+
 def counter_shift(n_samples: int, cfg: TrainConfig) -> int:
-    """Public scale-down so squared counters fit the division domain (train.py:189-192)."""
+    """Public scale-down so squared counters fit the division domain (train.py:75-78)."""
     headroom = (cfg.score_ring.width - cfg.tau - 2) // 2
     return max(0, int(n_samples).bit_length() - headroom)
 
 
 def resolved_depth(cfg: TrainConfig, n_columns: int) -> int:
-    """train.py:195-200."""
+    """train.py:81-86."""
     if cfg.policy == "feature_cap":
         return n_columns
     if cfg.policy == "grow":
@@ -68,7 +84,7 @@ def resolved_depth(cfg: TrainConfig, n_columns: int) -> int:
 
 
 def levels_of(vec, depth: int) -> List:
-    """Heap-level slices of a payload vector (train.py:203-204)."""
+    """Heap-level slices of a payload vector (train.py:89-90)."""
     return [vec.take(slice((1 << t) - 1, (1 << (t + 1)) - 1)) for t in range(depth)]
 
 
@@ -86,6 +102,12 @@ def _validate(cfg: TrainConfig, nf: int) -> int:
     depth = resolved_depth(cfg, nf + 1)
     if depth < 1:
         raise ValueError("depth must be at least 1")
+    if depth > 16:
+        raise ValueError(f"depth {depth} exceeds the B200 trainer's 16 levels (heap slots and node "
+                         "indices are sized for 2^16 - 1); pass an explicit depth / max_depth")
+    if not 1 <= nf <= 64:
+        raise ValueError(f"{nf} features: the B200 trainer supports 1..64 (a node's feature budget "
+                         "gamma is one 64-bit word of bit shares)")
     if cfg.score_ring.width not in (32, 64):
         raise ValueError("score ring must be Z_2^32 or Z_2^64")
     if not 0 <= cfg.tau < cfg.score_ring.width - 2:
@@ -188,8 +210,11 @@ class DeviceTrainer:
 
     def capture_host(self, Xh, Yh, filler_h, T_h, F_h, keys, allreduce=None):
         """CUDA graph of one whole host-operand run (uploads, kernels, the
-        sharded run's count allreduce if capturable, readback)."""
+        sharded run's count allreduce if capturable, readback).  Fixed policy,
+        mpc heuristic only (as ``capture``)."""
         torch = _native.require_cuda()
+        if self.cfg.policy == "grow" or self.cfg.heuristic == "tee":
+            raise ValueError("grow / tee synchronise with the host per level; they cannot be captured")
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(s):
@@ -234,6 +259,7 @@ def train_components(X: np.ndarray, Y: np.ndarray, cfg: TrainConfig, seeds: Seed
     n, nf = X.shape[1], X.shape[2]
     if n == 0:
         raise ValueError("dataset is empty")
+    cfg = as_config(cfg)
     tr = DeviceTrainer(n, nf, cfg, device=device)
     fill = filler_values(seeds.filler_seed, (1 << tr.depth) - 1, nf + 1)
     keys = make_keys(seeds, dealer_seed)
@@ -246,7 +272,7 @@ def train_components(X: np.ndarray, Y: np.ndarray, cfg: TrainConfig, seeds: Seed
 def train_3pc(x_pairs: Sequence, y_pairs: Sequence, cfg: TrainConfig, seeds: SeedSetup, dealer_seed: bytes,
               *, device=None, check: bool = True):
     """Whole-run entry on the three parties' replicated pairs (the form
-    ``share_values`` returns, dealer.py:619-623): x_pairs[i] = (lo, hi) of
+    ``share_values`` returns, dealer.py:259-263): x_pairs[i] = (lo, hi) of
     party i+1, lo/hi shaped (N, nf); y_pairs[i] shaped (N,).  Returns
     (T_pairs, F_pairs, depth) in the same per-party form."""
     X = components_from_pairs(x_pairs, RING64, check)

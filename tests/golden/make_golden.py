@@ -162,21 +162,21 @@ def make_trees():
     cases = []
     # test_train.py:47-51 depth-1 majority
     cases.append((np.array([[0, 1], [1, 1], [0, 1], [1, 0]], dtype=np.uint8), 1, b"\x0a" * 16, "majority"))
-    rng = np.random.default_rng(42)   # test_train.py:109-121
+    rng = np.random.default_rng(42)   # test_train.py:16-28
     for trial in range(10):
         n = int(rng.integers(4, 150))
         d = int(rng.integers(2, 8))
         depth = int(rng.integers(1, 5))
         data = rng.integers(0, 2, (n, d), dtype=np.uint8)
         cases.append((data, depth, bytes([trial + 1]) * 16, f"random{trial}"))
-    rng = np.random.default_rng(9)    # test_train.py:124-137 skewed
+    rng = np.random.default_rng(9)    # test_train.py:31-44 skewed
     for trial in range(5):
         n = int(rng.integers(4, 60))
         d = int(rng.integers(2, 6))
         data = np.zeros((n, d), dtype=np.uint8)
         data[:, int(rng.integers(0, d))] = rng.integers(0, 2, n)
         cases.append((data, 3, bytes([trial + 50]) * 16, f"skewed{trial}"))
-    rng = np.random.default_rng(4)    # test_train.py:147-155 counter shift 1
+    rng = np.random.default_rng(4)    # test_train.py:54-62 counter shift 1
     cases.append((rng.integers(0, 2, (1500, 5), dtype=np.uint8), 3, b"\x0b" * 16, "shift1500"))
     for i in range(24):               # acceptance battery (C5 shape)
         data, depth = _battery_dataset(i)
@@ -351,7 +351,7 @@ def make_c2c3():
 
 def make_variants():
     """MPC trees with a Z_2^64 score ring and other tau (TrainConfig.score_ring /
-    tau, train.py:171-179; cli --width / --tau)."""
+    tau, train.py:57-65; cli --width / --tau)."""
     from obtree.ring import Ring
     arrays, meta = {}, []
     cases = []
@@ -388,6 +388,29 @@ def make_tee():
     with open(os.path.join(OUT, "transcripts_tee.json"), "w") as fh:
         json.dump(out, fh)
     print("tee done")
+
+
+def make_policies():
+    """Depth policies on the MPC path (train.py:81-86): feature_cap as the
+    reference's test_feature_cap_policy_uses_column_count (test_train.py:85-94,
+    heuristic mpc here), and grow with the default cap (= column count) deep
+    enough that the opened stop bit is AND-reduced over > 64 nodes."""
+    arrays, meta = {}, []
+    cases = [
+        ("feature_cap_80x4", np.random.default_rng(6).integers(0, 2, (80, 4), dtype=np.uint8),
+         TrainConfig(depth=1, policy="feature_cap"), b"\x0e" * 16),
+        ("grow_default_cap_3000x10", np.random.default_rng(31).integers(0, 2, (3000, 10), dtype=np.uint8),
+         TrainConfig(depth=1, policy="grow"), b"\x21" * 16),
+    ]
+    for k, (name, data, cfg, seed) in enumerate(cases):
+        t0 = time.time()
+        T, F, dep, _ = secure_train(data, cfg, seed)
+        arrays[f"data{k}"], arrays[f"T{k}"], arrays[f"F{k}"] = data, T, F
+        meta.append({"name": name, "policy": cfg.policy, "depth_arg": cfg.depth, "trained_depth": dep,
+                     "seed": seed.hex()})
+        print("policy", name, dep, f"{time.time() - t0:.1f}s")
+    arrays["meta"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(OUT, "trees_policy.npz"), **arrays)
 
 
 def make_cli():
@@ -473,7 +496,7 @@ if __name__ == "__main__":
     ap.add_argument("--skip-c2", action="store_true")
     ap.add_argument("--only", default=None)
     a = ap.parse_args()
-    steps = {"cli": make_cli, "variants": make_variants,
+    steps = {"policies": make_policies, "cli": make_cli, "variants": make_variants,
              "tee": make_tee,
              "kats": make_kats, "trees": make_trees, "infer": make_infer,
              "transcripts": make_transcripts, "c2c3": make_c2c3}

@@ -143,7 +143,7 @@ def test_training_c2_adult_depth7():
 def test_grow_policy_matches_oracle():
     rng = np.random.default_rng(12)
     data = np.zeros((40, 4), dtype=np.uint8)
-    data[:, 0] = np.arange(40) % 2  # features vary, label constant (test_train.py:158-164)
+    data[:, 0] = np.arange(40) % 2  # features vary, label constant (test_train.py:65-71)
     X, Y, T, F, d, setup, keys = _device_train(data, 1, b"\x0c" * 16, rng, policy="grow", max_depth=3)
     assert d == 1 and opened(F).tolist() == [1] and opened(T).tolist() == [0]
     data = rng.integers(0, 2, (80, 4), dtype=np.uint8)

@@ -26,7 +26,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, X, Y, fill, depth, keys_t, out_dir):
+def _worker(rank, world, port, X, Y, fill, depth, keys_t, out_dir, side_stream=False):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -46,18 +46,28 @@ def _worker(rank, world, port, X, Y, fill, depth, keys_t, out_dir):
         k.pair[i].k0, k.pair[i].k1 = keys_t[i + 1]
     n = X.shape[1]
     start, cnt = shard_range(n, world, rank)
-    tr, d = train_sharded(to_device(np.ascontiguousarray(X[:, start:start + cnt])),
-                          to_device(np.ascontiguousarray(Y[:, start:start + cnt])), to_device(fill),
-                          TrainConfig(depth=depth), k, n_total=n, sample_base=start)
+    Xd = to_device(np.ascontiguousarray(X[:, start:start + cnt]))
+    Yd = to_device(np.ascontiguousarray(Y[:, start:start + cnt]))
+    Fd = to_device(fill)
+    s = None
+    if side_stream:  # a stream that is NOT torch's current one: the allreduce must follow it
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        torch.cuda.current_stream().synchronize()
+    tr, d = train_sharded(Xd, Yd, Fd, TrainConfig(depth=depth), k, n_total=n, sample_base=start, stream=s)
+    if s is not None:
+        s.synchronize()
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), T=from_device(tr.T), F=from_device(tr.F), d=d)
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,world", [(5003, 2), (4999, 3)])
-def test_sharded_device_training_equals_single_device(tmp_path, n, world):
+@pytest.mark.parametrize("n,world,side", [(5003, 2, False), (4999, 3, False), (5003, 2, True)])
+def test_sharded_device_training_equals_single_device(tmp_path, n, world, side):
     """(4999, 3) gives odd shard bases (1667, 3333): the count lanes' zero
-    words then straddle shard boundaries (count_lane_pair's unaligned path)."""
+    words then straddle shard boundaries (count_lane_pair's unaligned path).
+    side=True runs every rank on a non-current stream: the allreduce callback
+    must enqueue on the stream gt_train hands it."""
     from paper_2305_00645_b200 import TrainConfig
     from paper_2305_00645_b200.seeds import derive_seed, filler_values
     from paper_2305_00645_b200.train import train_components
@@ -70,7 +80,8 @@ def test_sharded_device_training_equals_single_device(tmp_path, n, world):
     fill = filler_values(setup.filler_seed, (1 << depth) - 1, 10)
     X, Y = share(data[:, :-1], rng), share(data[:, -1], rng)
     T1, F1, _ = train_components(X, Y, TrainConfig(depth=depth), setup, derive_seed(seed, "deal"))
-    mp.spawn(_worker, args=(world, _port(), X, Y, fill, depth, keys_t, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _port(), X, Y, fill, depth, keys_t, str(tmp_path), side), nprocs=world,
+             join=True)
     for r in range(world):
         z = np.load(tmp_path / f"r{r}.npz")
         assert int(z["d"]) == depth

@@ -95,7 +95,7 @@ def test_counter_shift_and_config_helpers():
     from paper_2305_00645_b200.shares import AVec
 
     vec = AVec(RING64, np.arange(7, dtype=np.uint64), np.zeros(7, dtype=np.uint64))
-    assert [p.size for p in levels_of(vec, 3)] == [1, 2, 4]  # test_train.py:203-206
+    assert [p.size for p in levels_of(vec, 3)] == [1, 2, 4]  # test_train.py:110-113
 
 
 def test_share_conversion_and_consistency_check():
