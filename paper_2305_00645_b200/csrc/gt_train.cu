@@ -142,6 +142,81 @@ __global__ void k_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T
   if (valid && t == 0) st3s(midx, N, s, add_pub<64>(add<64>(mul_pub<64>(idx, 2), dval), 1));
 }
 
+// Split partition: B threads per sample, placed in DIFFERENT warps (thread t
+// of the 256-thread CTA serves sample t % S of the CTA's S = 256 / B samples
+// as member r = t / S), so every lane of a warp runs the same entry pair q
+// at the same time -- uniform trip counts, warp-uniform table entries --
+// while the level's lookups get B times the threads of one-thread-per-sample.
+// Member r draws the telescope words e = r, r + B, ... and the entry pairs
+// q = r, r + B, ...; the B partial sums meet in shared memory.  Same lanes,
+// same randomness as lookup_partial (identical shares).
+constexpr int PS_TPB = 256;
+template <int B>
+__global__ void __launch_bounds__(PS_TPB, 3)
+    k_partition_split(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint64_t slots, int m, int nf, uint64_t N,
+                      uint64_t base, Keys K, uint32_t op_oaa, uint32_t op_row, PartAux aux, int tab_smem) {
+  constexpr int S = PS_TPB / B;
+  __shared__ uint64_t part[B][3][S];  // members' partial sums
+  __shared__ uint64_t feat[3][S];     // the sample's fetched feature index (shares)
+  extern __shared__ uint64_t tab[];   // [3][m] level payloads (if staged)
+  pdl_wait();
+  pdl_trigger();
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < aux.swords;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    aux.S[i] = 0;
+  if (aux.leaf && blockIdx.x == gridDim.x - 1)
+    for (int n = threadIdx.x; n < aux.n_h; n += blockDim.x) {
+      const B3 z = eqz<64>(K, aux.op_leaf, 0, (uint64_t)n, add_pub<64>(ld3s(aux.f, aux.n_h, n), 0ull - F_LEAF));
+#pragma unroll
+      for (int c = 0; c < 3; ++c) aux.leaf[c * aux.n_h + n] = z.v[c] & 1ull;
+    }
+  if (tab_smem)
+    for (int i = threadIdx.x; i < 3 * m; i += blockDim.x) tab[i] = T[(uint64_t)(i / m) * slots + (m - 1) + (i % m)];
+  __syncthreads();
+  const uint64_t* tg = T + (m - 1);
+  auto entryT = [&](int j) {
+    return tab_smem ? a3(tab[j], tab[m + j], tab[2 * m + j])
+                    : a3(__ldg(tg + j), __ldg(tg + slots + j), __ldg(tg + 2 * slots + j));
+  };
+  const int ls = threadIdx.x % S, r = threadIdx.x / S;  // r is warp-uniform
+  const uint64_t s = (uint64_t)blockIdx.x * S + ls;
+  const bool valid = s < N;
+  const uint64_t nfx = N * (uint64_t)nf, g = base + s;
+  A3 idx = a3(0, 0, 0), acc = a3(0, 0, 0);
+  if (valid) {  // oaa on the level-(h-1) payloads at local = m_idx - (m - 1)   (train.py:135-137)
+    idx = ld3s(midx, N, s);
+    acc = lookup_partial<64>(K, op_oaa, g, add_pub<64>(idx, 0ull - (uint64_t)(m - 1)), m, r, B, entryT);
+  }
+  if (B > 1) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) part[r][c][ls] = acc.v[c];
+    __syncthreads();
+    if (r == 0) {
+#pragma unroll
+      for (int q = 1; q < B; ++q) acc = add<64>(acc, a3(part[q][0][ls], part[q][1][ls], part[q][2][ls]));
+#pragma unroll
+      for (int c = 0; c < 3; ++c) feat[c][ls] = acc.v[c];
+    }
+    __syncthreads();
+    acc = a3(feat[0][ls], feat[1][ls], feat[2][ls]);
+  }
+  A3 d = a3(0, 0, 0);
+  if (valid) {  // row_lookup of the sample's features at the fetched index   (train.py:138)
+    auto entryX = [&](int f) { return ld3s(X, nfx, s * nf + f); };
+    d = lookup_partial<64>(K, op_row, g, acc, nf, r, B, entryX);
+  }
+  if (B > 1) {
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 3; ++c) part[r][c][ls] = d.v[c];
+    __syncthreads();
+    if (r == 0)
+#pragma unroll
+      for (int q = 1; q < B; ++q) d = add<64>(d, a3(part[q][0][ls], part[q][1][ls], part[q][2][ls]));
+  }
+  if (valid && r == 0) st3s(midx, N, s, add_pub<64>(add<64>(mul_pub<64>(idx, 2), d), 1));  // train.py:139
+}
+
 // ---------------------------------------------------------------------------
 // count
 // ---------------------------------------------------------------------------
@@ -1760,6 +1835,28 @@ int launch_partition_g(const uint64_t* X, uint64_t* midx, const uint64_t* T, uin
 // 181 vs 204 us per C2 tree against G = 2).
 int launch_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint64_t slots, int m, int nf, uint64_t N,
                      uint64_t base, const Keys& K, int level, cudaStream_t s, int num_sms, const PartAux& aux) {
+  // A/B: GT_PART_SPLIT=B (1, 2, 4) forces the split kernel, 0 the group kernel.
+  // Default (measured, C2 / C4): the split kernel with B = 2 while the level
+  // has fewer than ~700 samples per SM (C2: 0.657 vs 0.669 ms per tree), the
+  // one-thread-per-sample group kernel above that (C4: 20.95 vs 21.28 ms).
+  static const int forced_split = getenv("GT_PART_SPLIT") ? atoi(getenv("GT_PART_SPLIT")) : -1;
+  const int split = forced_split >= 0 ? forced_split : (N <= (uint64_t)num_sms * 700 ? 2 : 0);
+  if ((split == 1 || split == 2 || split == 4) && N) {
+    const int S = PS_TPB / split;
+    const unsigned grid = (unsigned)((N + S - 1) / S);
+    const int tab_smem = 3 * m * 8 <= 24 * 1024;
+    const size_t smem = tab_smem ? (size_t)3 * m * sizeof(uint64_t) : 0;
+    const uint32_t oo = op_id(level, SITE_PART_OAA), orow = op_id(level, SITE_PART_ROW);
+    int rc = split == 1 ? launch_chain(k_partition_split<1>, dim3(grid), dim3(PS_TPB), smem, s, nullptr, X, midx, T,
+                                       slots, m, nf, N, base, K, oo, orow, aux, tab_smem)
+           : split == 2 ? launch_chain(k_partition_split<2>, dim3(grid), dim3(PS_TPB), smem, s, nullptr, X, midx, T,
+                                       slots, m, nf, N, base, K, oo, orow, aux, tab_smem)
+                        : launch_chain(k_partition_split<4>, dim3(grid), dim3(PS_TPB), smem, s, nullptr, X, midx, T,
+                                       slots, m, nf, N, base, K, oo, orow, aux, tab_smem);
+    if (rc) return rc;
+    GT_LAUNCH_CHECK("k_partition_split");
+    return GT_OK;
+  }
   const uint64_t target = (uint64_t)num_sms * 256;
   int best = 16;
   uint64_t best_work = ~0ull;

@@ -1,0 +1,75 @@
+"""Dev timing probe (A/B experiments; not a bench number).
+
+  python tools/probe.py c2      C2 tree: CUDA-graph replay median ms + per-kernel-class ms
+  python tools/probe.py walk    C3 (10^4 x 13, 7 levels) and a C5 slice (2*10^6 x 32, 10 levels) inst/s
+  python tools/probe.py c4      C4 tree (10^6 x 32, depth 8) graph replay median ms
+Launch switches (GT_PART_G, GT_WALK_G, ...) come from the environment.
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2305_00645_b200 import TrainConfig, _native  # noqa: E402
+from paper_2305_00645_b200.infer import infer_device  # noqa: E402
+from paper_2305_00645_b200.train import DeviceTrainer  # noqa: E402
+
+
+def timed(fn, reps=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def main():
+    what = sys.argv[1]
+    tag = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("GT_"))
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).to(dev)  # noqa: E731
+    setup, keys, fill = bench._keys_and_filler()
+    if what == "c2":
+        data, X, Y = bench._c2_inputs()
+        tr = DeviceTrainer(bench.N_C2, bench.NF_C2, TrainConfig(depth=bench.DEPTH_C2))
+        X, Y, F = t(X), t(Y), t(fill)
+        g = tr.capture(X, Y, F, keys)
+        ms = timed(g)
+        z = np.load(os.path.join(bench.ROOT, "tests", "golden", "c2c3.npz"))
+        ok = np.array_equal(tr.T.sum(0).cpu().numpy().view(np.uint64), z["T"])
+        p = _native.gt_train_profile()
+        tr.run(X, Y, F, keys, profile=p)
+        torch.cuda.synchronize()
+        ks = ("prods", "partition", "count_lanes", "count_contract", "node_hc", "node_finish")
+        print(f"[{tag}] C2 {ms:.4f} ms tree_ok={ok} |", " ".join(f"{k}={getattr(p, 'ms_' + k) * 1e3:.1f}us"
+                                                              for k in ks), flush=True)
+    elif what == "c4":
+        n, nf, depth = 10 ** 6, 32, 8
+        rng = np.random.default_rng(3)
+        X = t(bench._share(rng.integers(0, 2, (n, nf)), rng))
+        Y = t(bench._share(rng.integers(0, 2, n), rng))
+        F = t(np.zeros((1 << depth) - 1, dtype=np.uint64))
+        tr = DeviceTrainer(n, nf, TrainConfig(depth=depth))
+        print(f"[{tag}] C4 {timed(tr.capture(X, Y, F, keys), 10):.3f} ms", flush=True)
+    elif what == "walk":
+        rng = np.random.default_rng(1)
+        for depth, nf, n in ((7, 13, 10_000), (10, 32, 2_000_000)):
+            T = t(bench._share(rng.integers(0, nf, (1 << depth) - 1), rng))
+            Q = t(bench._share(rng.integers(0, 2, (n, nf)), rng))
+            out = torch.empty((3, n), dtype=torch.int64, device=dev)
+            ms = timed(lambda: infer_device(T, depth, Q, keys, out=out))
+            print(f"[{tag}] walk d{depth} nf{nf} n{n}: {ms * 1e3:.1f} us  {n / ms / 1e3:.1f} M inst/s", flush=True)
+
+
+if __name__ == "__main__":
+    main()
