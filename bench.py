@@ -60,6 +60,14 @@ def _c2_inputs():
     return data, _share(data[:, :-1], rng), _share(data[:, -1], rng)
 
 
+def _c2_config():
+    """The workload dict both arms print (the driver compares them)."""
+    return {"workload": "C2 Adult-shaped 48842x13+label secure MPC training, depth 7, heuristic mpc",
+            "n_samples": N_C2, "n_features": NF_C2, "depth": DEPTH_C2, "heuristic": "mpc", "parties": 3,
+            "data": "default_rng(1011) binary matrix, seed (11000).to_bytes(16, 'little')",
+            "l2": "flushed (256 MiB write) between timed steps"}
+
+
 def _keys_and_filler():
     from paper_2305_00645_b200.seeds import SeedSetup, derive_seed, filler_values, make_keys
 
@@ -160,6 +168,49 @@ def walk_bytes(n, nf, depth):
     return n * (24 * nf + 24) + 24 * ((1 << depth) - 1) + n * 48  # queries + tree in, labels + slots out
 
 
+def tree_bytes(n, nf, depth):
+    """algorithmic bytes of one fused training tree -- prods
+    N(24 + 48 nf), level 0 N(48 + 48 nf), every deeper level N(96 + 72 nf)
+    (C2: 367 MB, C4: 19.9 GB)."""
+    return n * (24 + 48 * nf) + n * (48 + 48 * nf) + (depth - 1) * n * (96 + 72 * nf)
+
+
+# Philox4x32-10 blocks (randomness schedule v2, DESIGN.md section 4): one
+# lookup over m entries draws 9 blocks per entry pair (two lanes' 3 dealer
+# blocks + 3 shared pair blocks) and 6 telescoped reshare words; a pair of
+# count lanes draws 9 blocks; count:0's prods one pair block per key per
+# feature pair.
+def lookup_blocks(m):
+    return ((m + 1) // 2) * 9 + 6
+
+
+def partition_blocks(n, nf, depth):
+    return sum(n * (lookup_blocks(1 << (h - 1)) + lookup_blocks(nf)) for h in range(1, depth))
+
+
+def count_lane_blocks(n, depth):
+    return sum(((n + 1) // 2) * (1 << h) * 9 for h in range(depth))
+
+
+def tree_blocks(n, nf, depth):
+    return n * ((nf + 1) // 2) * 3 + partition_blocks(n, nf, depth) + count_lane_blocks(n, depth)
+
+
+def walk_blocks(n, nf, depth):
+    return n * sum(lookup_blocks(1 << t) + lookup_blocks(nf) for t in range(depth))
+
+
+def _roof(alg_bytes, blocks, seconds, peak, peak_kind, philox_peak, what):
+    """HBM roof on algorithmic bytes and the integer-ALU roof on Philox blocks
+    (the lane work is ALU bound) for one timed unit of work."""
+    gbs = alg_bytes / seconds / 1e9
+    bps = blocks / seconds
+    return {"bound": "hbm", "kernel": what, "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+            "peak_source": peak_kind, "algorithmic_bytes": alg_bytes, "traffic": None,
+            "alu": {"bound": "int-alu (Philox4x32-10 blocks)", "blocks": blocks, "achieved_blocks_per_s": bps,
+                    "peak_blocks_per_s": philox_peak, "frac": bps / philox_peak if philox_peak else None}}
+
+
 def _traffic(kernel: str):
     """DRAM bytes/launch of `kernel` from the committed ncu capture, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -196,8 +247,7 @@ def reference_arm(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s/tree", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": "C2 Adult-shaped 48842x13+label secure MPC training, depth 7",
-                       "n_samples": N_C2, "n_features": NF_C2, "depth": DEPTH_C2, "heuristic": "mpc"},
+            "config": _c2_config(), "parallelism": "host threads (OpenMP), rank 0 only",
             "cpu_baseline": {"value": v, "unit": "s/tree", "cores": cores, "kind": "port",
                              "sample": "full C2 tree per step (oracle/gtree_oracle.c, OpenMP)"},
             "e2e": {"value": v, "unit": "s/tree", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -274,9 +324,27 @@ def scale_c4(ctx, steps, warmup):
     t = _events_time(fn, steps, warmup, ctx["flush"], ctx["barrier"], ctx["stream"], ctx["max"])
     T, F = from_device(tr.T).sum(axis=0), from_device(tr.F).sum(axis=0)
     want_T, want_F = shadow.mpc_train(data, depth, fill)
-    return {"metric": "secure train s/tree (10^6 x 32, depth 8)", "value": t, "unit": "s/tree",
+    line = {"metric": "secure train s/tree (10^6 x 32, depth 8)", "value": t, "unit": "s/tree",
             "scaling": "strong", "config": "C4: default_rng(10**6) 10^6 x 33 binary, depth 8, mpc; samples sharded",
-            "parity_tree_equals_shadow_oracle": bool(np.array_equal(T, want_T) and np.array_equal(F, want_F))}
+            "parity_tree_equals_shadow_oracle": bool(np.array_equal(T, want_T) and np.array_equal(F, want_F)),
+            "roofline": _roof(tree_bytes(n, nf, depth), tree_blocks(n, nf, depth), t, ctx["peak"], ctx["peak_kind"],
+                              ctx["philox"], "whole tree (all kernels, serial chain)")}
+    if ctx["cpu"]:
+        # a 4*10^4-sample subsample of the same matrix through the
+        # C oracle port (all host threads), scaled x25 (the tree is linear in N)
+        import oracle
+        from paper_2305_00645_b200.seeds import keys_tuple
+
+        sub = 40_000
+        rng = np.random.default_rng(5)
+        Xs, Ys = _share(data[:sub, :-1], rng), _share(data[:sub, -1], rng)
+        t0 = time.perf_counter()
+        oracle.train(Xs, Ys, fill, depth, keys_tuple(keys))
+        cs = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": cs * (n / sub), "unit": "s/tree", "cores": oracle.num_threads(),
+                                "kind": "port", "measured_s": cs,
+                                "sample": "4*10^4 x 32 depth-8 tree through oracle/gtree_oracle.c, x25"}
+    return line
 
 
 def scale_c5(ctx, steps, warmup):
@@ -301,13 +369,123 @@ def scale_c5(ctx, steps, warmup):
     out = torch.empty((3, cnt), dtype=torch.int64, device=dev)
     t = _events_time(lambda: infer_device(T, depth, Q, ctx["keys"], instance_base=start, out=out), steps, warmup,
                      ctx["flush"], ctx["barrier"], ctx["stream"], ctx["max"])
-    sub = min(cnt, 200_000)
-    got = from_device(out[:, :sub]).sum(axis=0)
-    want = shadow.plaintext_infer(Tv, depth, qbits[:sub].cpu().numpy())
-    return {"metric": "secure inference instances/s (10^7 x 32, 10 levels)", "value": n / t, "unit": "instances/s",
+    got = from_device(out).sum(axis=0)
+    want = shadow.plaintext_infer(Tv, depth, qbits.cpu().numpy())
+    line = {"metric": "secure inference instances/s (10^7 x 32, 10 levels)", "value": n / t, "unit": "instances/s",
             "ms_per_step": t * 1e3, "scaling": "strong",
             "config": "C5: random_tree(default_rng(10), 10, 33), 10^7 random queries; instances sharded",
-            "parity_predictions_equal_plaintext_first_2e5": bool(np.array_equal(got, want))}
+            "parity_predictions_equal_plaintext_all": bool(np.array_equal(got, want)),
+            "roofline": _roof(walk_bytes(cnt, nf, depth), walk_blocks(cnt, nf, depth), t, ctx["peak"],
+                              ctx["peak_kind"], ctx["philox"], "k_walk")}
+    if ctx["cpu"]:
+        # 2*10^4 instances through the C oracle port, scaled x500
+        import oracle
+        from paper_2305_00645_b200.seeds import keys_tuple
+
+        sub = 20_000
+        rng = np.random.default_rng(6)
+        qs = qbits[:sub].cpu().numpy()
+        Tsh = _share(Tv, rng)
+        t0 = time.perf_counter()
+        oracle.infer(Tsh, depth, _share(qs, rng), keys_tuple(ctx["keys"]))
+        cs = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": sub / cs, "unit": "instances/s", "cores": oracle.num_threads(),
+                                "kind": "port", "measured_s": cs,
+                                "sample": "2*10^4 queries x 32 features on the 10-level tree through "
+                                          "oracle/gtree_oracle.c (rate of the full 10^7 = x500 the time)"}
+    return line
+
+
+def e2e_api(Xh, Yh, z, steps, warmup):
+    """C2 through the reference-facing drop-in exactly as a reference caller
+    runs it (tests/helpers.py:79-99 shape): run_local with three party
+    threads, each body hands its own host AVec pair to engine.train_tree, the
+    rendezvous checks replication consistency and makes one device call.
+    Wall clock per call (host threads, staging copies and sync included)."""
+    from paper_2305_00645_b200 import TrainConfig, engine
+    from paper_2305_00645_b200.seeds import SeedSetup, derive_seed
+    from paper_2305_00645_b200.shares import RING64, AVec
+
+    setup = SeedSetup.from_master(derive_seed(SEED_C2, "run"))
+    dseed = derive_seed(SEED_C2, "deal")
+    cfg = TrainConfig(depth=DEPTH_C2)
+
+    def body(eng):
+        p = eng.party
+        X = AVec(RING64, Xh[p - 1], Xh[p % 3])
+        Y = AVec(RING64, Yh[p - 1], Yh[p % 3])
+        r = engine.train_tree(eng, X, Y, cfg)
+        return r.T, r.F
+
+    ts, run = [], None
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        run = engine.run_local(body, seeds=setup, dealer_seed=dseed)
+        if i >= warmup:
+            ts.append(time.perf_counter() - t0)
+    T = engine.open_results(run, pick=lambda r: r[0])
+    F = engine.open_results(run, pick=lambda r: r[1])
+    v = statistics.median(ts)
+    return {"value": v, "unit": "s/tree", "timing": "wall clock per run_local call, median of the timed steps",
+            "path": "engine.run_local + engine.train_tree on per-party host AVecs (cached pinned-staging trainer)",
+            "h2d_bytes_per_step": int(Xh.nbytes + Yh.nbytes + 8 * ((1 << DEPTH_C2) - 1)),
+            "d2h_bytes_per_step": int(2 * 3 * 8 * ((1 << DEPTH_C2) - 1)),
+            "tree_equals_reference": bool(np.array_equal(T, z["T"]) and np.array_equal(F, z["F"]))}
+
+
+def python_reference(data, Xh, Yh, Tc, q, z):
+    """The UNMODIFIED Python reference (obtree, pip-installed into
+    baseline/_ref) timed on this host: run_local + train_tree on the C2 shares
+    (LiveDealer material, as tests/helpers.py:79-99) and run_local +
+    infer_batch on the C3 batch (helpers.py:50-61).  Three party threads;
+    numpy runs each op single-threaded.  None if baseline/_ref is absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "obtree")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    from obtree.dealer import LiveDealer
+    from obtree.enclave import EnclaveService
+    from obtree.infer import infer_batch
+    from obtree.ring import RING64
+    from obtree.rss import AVec, run_local
+    from obtree.train import TrainConfig, levels_of, train_tree
+    from obtree.transport import SeedSetup, derive_seed
+
+    setup = SeedSetup.from_master(derive_seed(SEED_C2, "run"))
+
+    def pair(comp, p):
+        return AVec(RING64, comp[p - 1].copy(), comp[p % 3].copy())
+
+    def tbody(eng):
+        r = train_tree(eng, pair(Xh, eng.party), pair(Yh, eng.party), TrainConfig(depth=DEPTH_C2, heuristic="mpc"))
+        return r.T, r.F
+
+    dealer = LiveDealer(derive_seed(SEED_C2, "deal"))
+    t0 = time.perf_counter()
+    run = run_local(tbody, seeds=setup, materials=[dealer.view(i) for i in (1, 2, 3)],
+                    enclave_handler=EnclaveService(setup.enclave_seed).handler)
+    t_train = time.perf_counter() - t0
+    opened = lambda k: sum((np.asarray(r[k].lo, dtype=np.uint64) for r in run.results), np.uint64(0))  # noqa: E731
+    train_ok = bool(np.array_equal(opened(0), z["T"]) and np.array_equal(opened(1), z["F"]))
+    rng = np.random.default_rng(3)
+    Qs = _share(q, rng)
+
+    def ibody(eng):
+        return infer_batch(eng, levels_of(pair(Tc, eng.party), DEPTH_C2), pair(Qs, eng.party))
+
+    dealer = LiveDealer(derive_seed(SEED_C2, "deal-infer"))
+    t0 = time.perf_counter()
+    irun = run_local(ibody, seeds=setup, materials=[dealer.view(i) for i in (1, 2, 3)])
+    t_inf = time.perf_counter() - t0
+    preds = sum((np.asarray(r.lo, dtype=np.uint64) for r in irun.results), np.uint64(0))
+    return {"kind": "reference", "cores": 3, "threads_note": "3 party threads, numpy single-threaded per op",
+            "host_cpus": os.cpu_count(),
+            "c2_train": {"value": t_train, "unit": "s/tree", "sample": "one full C2 tree (run_local + train_tree)",
+                         "tree_equals_golden": train_ok},
+            "c3_infer": {"value": N_C3 / t_inf, "unit": "instances/s", "sample": "the full C3 batch (run_local + "
+                         "infer_batch, 10^4 queries, 7 levels)", "predictions_equal_golden":
+                         bool(np.array_equal(preds, z["preds"]))}}
 
 
 def main():
@@ -318,6 +496,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-scale", action="store_true", help="skip the C4/C5 10^6-scale secondaries")
+    ap.add_argument("--no-python-reference", action="store_true",
+                    help="skip timing the unmodified Python reference (baseline/_ref) on C2/C3")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -342,6 +522,7 @@ def main():
     torch.cuda.set_device(local_dev)
     dev = torch.device("cuda", local_dev)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (nranks) on stderr
         backend = os.environ.get("GT_BENCH_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
@@ -371,8 +552,10 @@ def main():
     cb = make_allreduce(tr) if world > 1 else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
+    peak, peak_kind = _peaks()
     ctx = {"dev": dev, "world": world, "rank": rank, "flush": flush, "barrier": barrier, "stream": stream,
-           "max": max_over_ranks, "keys": keys}
+           "max": max_over_ranks, "keys": keys, "peak": peak, "peak_kind": peak_kind, "philox": _philox_peak(),
+           "cpu": world == 1 and not args.no_cpu_baseline}
 
     def step(profile=None):
         return tr.run(X, Y, FL, keys, allreduce=cb, profile=profile)
@@ -498,15 +681,10 @@ def main():
     if world == 1:
         preds_ok = bool(np.array_equal(from_device(out).sum(axis=0), z["preds"]))
 
-    # ---- protocol option: dot-product reshare of the count cells (same tree) ----
-    tr_dot = DeviceTrainer(cnt, NF_C2, TrainConfig(depth=DEPTH_C2, count_reshare="dot"), n_total=N_C2,
-                           sample_base=start, device=dev)
-    cb_dot = make_allreduce(tr_dot) if world > 1 else None
-    run_dot = (tr_dot.capture(X, Y, FL, keys, allreduce=cb_dot) if graphed
-               else (lambda: tr_dot.run(X, Y, FL, keys, allreduce=cb_dot)))
-    dot_s = _events_time(run_dot, args.steps, args.warmup, flush, barrier, stream, max_over_ranks)
-    dot_ok = bool(np.array_equal(from_device(tr_dot.T).sum(axis=0), z["T"]) and
-                  np.array_equal(from_device(tr_dot.F).sum(axis=0), z["F"]))
+    # ---- e2e through the reference-facing drop-in API (what a reference caller runs) ----
+    # run_local + train_tree with host AVecs per party (rss.py:496-542, train.py:108): three party
+    # threads, the rendezvous, consistency check, pinned staging, one gt_train_host call, scatter
+    api = e2e_api(Xh, Yh, z, args.steps, args.warmup) if world == 1 else None
 
     scale = {}
     if not args.no_scale:
@@ -519,7 +697,6 @@ def main():
         return
 
     # ---- roofline of the dominant kernel class ----
-    peak, peak_kind = _peaks()
     # dominant single kernel: node_hc (k_hc_pre + k_hc_div + k_hc_post per level) and node_finish are
     # multi-kernel latency chains with no bulk data; their times are in kernel_ms_per_step
     dom = max((k for k in prof_tot if k not in ("node_hc", "node_finish")), key=lambda k: prof_tot[k])
@@ -537,13 +714,12 @@ def main():
     # integer-ALU roof: Philox blocks the dominant kernel draws vs the measured Philox peak
     # (randomness schedule v2: a pair of eq lanes draws 2 x 3 dealer blocks + 3 shared pair blocks;
     # each lookup adds 2 x 3 telescoped reshare words per index)
-    blocks = {"count_lanes": sum(((cnt + 1) // 2) * (1 << h) * 9 for h in range(DEPTH_C2)),
-              "partition": sum(cnt * ((((1 << (h - 1)) + 1) // 2 + (NF_C2 + 1) // 2) * 9 + 12)
-                               for h in range(1, DEPTH_C2))}.get(dom)
+    blocks = {"count_lanes": count_lane_blocks(cnt, DEPTH_C2),
+              "partition": partition_blocks(cnt, NF_C2, DEPTH_C2)}.get(dom)
     alu = None
     if blocks:
         alu = {"bound": "int-alu (Philox4x32-10 blocks)", "achieved_blocks_per_s": blocks * args.steps / (prof_tot[dom] / 1e3),
-               "peak_blocks_per_s": _philox_peak(), "note": "peak measured by gt_diag_philox on this GPU"}
+               "peak_blocks_per_s": ctx["philox"], "note": "peak measured by gt_diag_philox on this GPU"}
         alu["frac"] = alu["achieved_blocks_per_s"] / alu["peak_blocks_per_s"] if alu["peak_blocks_per_s"] else None
     # every kernel class against the HBM roof (same definitions), for the record
     classes = {}
@@ -552,8 +728,8 @@ def main():
             gbs = bytes_of[k] * args.steps / (prof_tot[k] / 1e3) / 1e9
             classes[k] = {"kernel": kname.get(k, k), "ms_per_step": prof_tot[k] / args.steps,
                           "achieved_gbs": gbs, "frac": gbs / peak}
-    cpu_base = None
-    if world == 1 and not args.no_cpu_baseline:
+    cpu_base = cpu_c3 = py_ref = None
+    if ctx["cpu"]:
         import oracle
         from paper_2305_00645_b200.seeds import keys_tuple
 
@@ -562,6 +738,13 @@ def main():
         cs = time.perf_counter() - t0
         cpu_base = {"value": cs, "unit": "s/tree", "cores": oracle.num_threads(), "kind": "port",
                     "sample": "one full C2 tree (48842x13, depth 7) through oracle/gtree_oracle.c"}
+        t0 = time.perf_counter()
+        oracle.infer(Tc, DEPTH_C2, Qp.numpy().view(np.uint64), keys_tuple(keys))
+        cs = time.perf_counter() - t0
+        cpu_c3 = {"value": N_C3 / cs, "unit": "instances/s", "cores": oracle.num_threads(), "kind": "port",
+                  "sample": "the full C3 batch (10^4 queries, 7 levels) through oracle/gtree_oracle.c"}
+        if not args.no_python_reference:
+            py_ref = python_reference(data, Xh, Yh, Tc, q, z)
     walk_alg = walk_bytes(qc, NF_C2, DEPTH_C2)
     # inter-party messages of the protocol the kernels execute (the analytic
     # transcript, ledger.py) beside the reference's (its lane_limit chunking)
@@ -578,12 +761,10 @@ def main():
     line = {
         "metric": METRIC, "value": value_s, "unit": "s/tree", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": value_s * 1e3, "higher_is_better": False,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "u64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (Adult-shaped binary matrix, default_rng(1011); random 3-party shares)",
-        "config": {"workload": "C2 Adult-shaped 48842x13+label secure MPC training, depth 7, heuristic mpc",
-                   "n_samples": N_C2, "n_features": NF_C2, "depth": DEPTH_C2, "parties": 3,
-                   "parallelism": f"samples sharded x{world}" + (" + NCCL count allreduce" if world > 1 else ""),
-                   "l2": "flushed (256 MiB write) between timed steps"},
+        "config": _c2_config(),
+        "parallelism": f"samples sharded x{world}" + (" + NCCL count allreduce" if world > 1 else ""),
         "parity": {"tree_equals_reference": parity, "e2e_tree_equals_reference": e2e_parity,
                    "c3_predictions_equal_reference": preds_ok},
         "e2e": {"value": e2e_s, "unit": "s/tree", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -602,16 +783,19 @@ def main():
                       "config": "C3: 10^4 queries x 13 features on the C2 tree (7 levels)",
                       "e2e": {"value": N_C3 / inf_e2e_s, "unit": "instances/s",
                               "h2d_bytes_per_step": int(Qp.numel() * 8), "d2h_bytes_per_step": int(Oh.numel() * 8)},
-                      "roofline": {"bound": "hbm", "kernel": "k_walk", "achieved": walk_alg / inf_s / 1e9,
-                                   "peak": peak, "unit": "GB/s", "frac": walk_alg / inf_s / 1e9 / peak}},
+                      "roofline": _roof(walk_alg, walk_blocks(qc, NF_C2, DEPTH_C2), inf_s, peak, peak_kind,
+                                        ctx["philox"], "k_walk")},
+        "tree_roofline": _roof(tree_bytes(cnt, NF_C2, DEPTH_C2), tree_blocks(cnt, NF_C2, DEPTH_C2), value_s, peak,
+                               peak_kind, ctx["philox"], "whole C2 tree (all kernels, serial chain)"),
         "scale": scale,
-        "option_dot_reshare": {"metric": METRIC, "value": dot_s, "unit": "s/tree",
-                               "config": "C2 with TrainConfig(count_reshare='dot'): count cells reshared once "
-                                         "(ABY3 dot product) instead of per (sample, node, column) product",
-                               "tree_equals_reference": dot_ok},
     }
+    if api is not None:
+        line["e2e_api"] = api
     if cpu_base is not None:
         line["cpu_baseline"] = cpu_base
+        line["secondary"]["cpu_baseline"] = cpu_c3
+    if py_ref is not None:
+        line["cpu_baseline_python_reference"] = py_ref
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -11,6 +11,8 @@ per-level count allreduce of a sample-sharded run.
 from __future__ import annotations
 
 import ctypes
+import threading
+from collections import OrderedDict
 from dataclasses import dataclass
 from typing import List, Optional, Sequence, Tuple
 
@@ -248,10 +250,39 @@ class DeviceTrainer:
         return g.replay
 
 
+# Host-operand entry points reuse one trainer (workspace + pinned staging) per
+# training shape: repeated calls of the drop-in API (bench steps, CLI runs,
+# cross-validation loops) pay no allocation.  A lock serialises the cached
+# trainers' use across host threads (one rendezvous thread per run_local).
+_TRAINERS: "OrderedDict" = OrderedDict()
+_TRAINER_CACHE_MAX = 2
+_TRAIN_LOCK = threading.Lock()
+
+
+def _cached_trainer(n: int, nf: int, cfg: TrainConfig, device, host_io: bool) -> "DeviceTrainer":
+    torch = _native.require_cuda()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    key = (n, nf, repr(cfg), str(dev), host_io)
+    tr = _TRAINERS.pop(key, None)
+    if tr is None:
+        while len(_TRAINERS) >= _TRAINER_CACHE_MAX:
+            _TRAINERS.popitem(last=False)
+        tr = DeviceTrainer(n, nf, cfg, device=dev, host_io=host_io)
+        if host_io:
+            slots = (1 << tr.depth) - 1
+            pin = lambda *shape: torch.empty(shape, dtype=torch.int64).pin_memory()  # noqa: E731
+            tr.staging = {"X": pin(3, n, nf), "Y": pin(3, n), "fill": pin(slots), "T": pin(3, slots),
+                          "F": pin(3, slots)}
+    _TRAINERS[key] = tr
+    return tr
+
+
 def train_components(X: np.ndarray, Y: np.ndarray, cfg: TrainConfig, seeds: SeedSetup, dealer_seed: bytes,
                      *, device=None) -> Tuple[np.ndarray, np.ndarray, int]:
     """Whole-run entry on component-major shares: X [3, N, nf], Y [3, N]
-    uint64 -> (T [3, slots], F [3, slots], depth) component shares."""
+    uint64 -> (T [3, slots], F [3, slots], depth) component shares.
+    Heuristic mpc goes through gt_train_host (pinned staging, chunked upload
+    beside the prologue); tee through gt_train_ex (its helper callback)."""
     X = np.asarray(X, dtype=np.uint64)
     Y = np.asarray(Y, dtype=np.uint64)
     if X.ndim != 3 or X.shape[0] != 3 or Y.shape != (3, X.shape[1]):
@@ -260,13 +291,27 @@ def train_components(X: np.ndarray, Y: np.ndarray, cfg: TrainConfig, seeds: Seed
     if n == 0:
         raise ValueError("dataset is empty")
     cfg = as_config(cfg)
-    tr = DeviceTrainer(n, nf, cfg, device=device)
-    fill = filler_values(seeds.filler_seed, (1 << tr.depth) - 1, nf + 1)
     keys = make_keys(seeds, dealer_seed)
-    depth = tr.run(to_device(X, tr.device), to_device(Y, tr.device), to_device(fill, tr.device), keys,
-                   enclave_seed=seeds.enclave_seed)
-    slots = (1 << depth) - 1
-    return from_device(tr.T)[:, :slots].copy(), from_device(tr.F)[:, :slots].copy(), depth
+    with _TRAIN_LOCK:
+        if cfg.heuristic == "mpc":
+            torch = _native.require_cuda()
+            tr = _cached_trainer(n, nf, cfg, device, True)
+            st = tr.staging
+            np.copyto(st["X"].numpy().view(np.uint64), X)
+            np.copyto(st["Y"].numpy().view(np.uint64), Y)
+            st["fill"].numpy().view(np.uint64)[:] = filler_values(seeds.filler_seed, (1 << tr.depth) - 1, nf + 1)
+            s = torch.cuda.current_stream(tr.device)
+            depth = tr.run_host(st["X"], st["Y"], st["fill"], st["T"], st["F"], keys, stream=s)
+            s.synchronize()
+            slots = (1 << depth) - 1
+            return (st["T"].numpy().view(np.uint64)[:, :slots].copy(),
+                    st["F"].numpy().view(np.uint64)[:, :slots].copy(), depth)
+        tr = _cached_trainer(n, nf, cfg, device, False)
+        fill = filler_values(seeds.filler_seed, (1 << tr.depth) - 1, nf + 1)
+        depth = tr.run(to_device(X, tr.device), to_device(Y, tr.device), to_device(fill, tr.device), keys,
+                       enclave_seed=seeds.enclave_seed)
+        slots = (1 << depth) - 1
+        return from_device(tr.T)[:, :slots].copy(), from_device(tr.F)[:, :slots].copy(), depth
 
 
 def train_3pc(x_pairs: Sequence, y_pairs: Sequence, cfg: TrainConfig, seeds: SeedSetup, dealer_seed: bytes,

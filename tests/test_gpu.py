@@ -230,6 +230,33 @@ def test_dropin_run_local_train_and_infer():
     assert np.array_equal(got, shadow.plaintext_infer(want_T, 3, q))
 
 
+def test_dropin_run_local_c2_twice_equals_reference_tree():
+    """The drop-in API at the C2 shape (48 842 x 13, depth 7): per-party host
+    AVecs through run_local + train_tree, twice (the second call reuses the
+    cached trainer and its pinned staging), both equal to the reference's C2
+    tree (tests/golden/c2c3.npz)."""
+    from paper_2305_00645_b200 import TrainConfig, run_local, train_tree
+    from paper_2305_00645_b200.seeds import SeedSetup, derive_seed
+    from paper_2305_00645_b200.shares import AVec, RING64
+
+    z, _ = golden_npz("c2c3.npz")
+    data = np.random.default_rng(1011).integers(0, 2, size=(48842, 14), dtype=np.uint8)
+    seed = (11_000).to_bytes(16, "little")
+    setup = SeedSetup.from_master(derive_seed(seed, "run"))
+    for it in range(2):
+        rng = np.random.default_rng(70 + it)
+        X, Y = share(data[:, :-1], rng), share(data[:, -1], rng)
+
+        def body(eng):
+            p = eng.party
+            return train_tree(eng, AVec(RING64, X[p - 1], X[p % 3]), AVec(RING64, Y[p - 1], Y[p % 3]),
+                              TrainConfig(depth=7))
+
+        run = run_local(body, seeds=setup, dealer_seed=derive_seed(seed, "deal"))
+        assert np.array_equal(sum(r.T.lo for r in run.results), z["T"])
+        assert np.array_equal(sum(r.F.lo for r in run.results), z["F"])
+
+
 def test_tee_heuristic_bit_identical_to_plaintext_trainer():
     # reference acceptance criterion 4 (test_acceptance.py:180-193): the trusted
     # path equals plaintext_train exactly; golden oT/oF are the reference's own

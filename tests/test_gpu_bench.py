@@ -35,6 +35,11 @@ def test_bench_line_contract():
     assert rf["bound"] in ("hbm", "tensor") and rf["peak"] > 0 and 0 < rf["frac"] <= 1
     assert all(line["parity"].values()), line["parity"]
     assert line["messages"]["c2_train"]["bytes_per_party"] == line["messages"]["c2_train"]["reference_bytes_per_party"]
+    assert line["e2e_api"]["tree_equals_reference"] and line["e2e_api"]["value"] > 0
+    for rf in (line["tree_roofline"], line["secondary"]["roofline"]):
+        assert 0 < rf["frac"] <= 1 and 0 < rf["alu"]["frac"] <= 1
+    ref = _run("--impl", "reference", "--steps", "1", "--warmup", "0")
+    assert ref["config"] == line["config"] and ref["scaling"] == line["scaling"]
 
 
 def test_reference_arm_line():

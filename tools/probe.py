@@ -3,7 +3,8 @@
   python tools/probe.py c2      C2 tree: CUDA-graph replay median ms + per-kernel-class ms
   python tools/probe.py walk    C3 (10^4 x 13, 7 levels) and a C5 slice (2*10^6 x 32, 10 levels) inst/s
   python tools/probe.py c4      C4 tree (10^6 x 32, depth 8) graph replay median ms
-Launch switches (GT_PART_G, GT_WALK_G, ...) come from the environment.
+Launch switches (GT_PART_G, GT_WALK_G, ...) come from the environment;
+GT_PROBE_ENGINE=cuda runs the count contraction on the CUDA cores (A/B).
 """
 import os
 import sys
@@ -41,7 +42,8 @@ def main():
     setup, keys, fill = bench._keys_and_filler()
     if what == "c2":
         data, X, Y = bench._c2_inputs()
-        tr = DeviceTrainer(bench.N_C2, bench.NF_C2, TrainConfig(depth=bench.DEPTH_C2))
+        eng = os.environ.get("GT_PROBE_ENGINE", "tensor")  # count engine A/B: tensor | cuda
+        tr = DeviceTrainer(bench.N_C2, bench.NF_C2, TrainConfig(depth=bench.DEPTH_C2, count_engine=eng))
         X, Y, F = t(X), t(Y), t(fill)
         g = tr.capture(X, Y, F, keys)
         ms = timed(g)
@@ -59,7 +61,7 @@ def main():
         X = t(bench._share(rng.integers(0, 2, (n, nf)), rng))
         Y = t(bench._share(rng.integers(0, 2, n), rng))
         F = t(np.zeros((1 << depth) - 1, dtype=np.uint64))
-        tr = DeviceTrainer(n, nf, TrainConfig(depth=depth))
+        tr = DeviceTrainer(n, nf, TrainConfig(depth=depth, count_engine=os.environ.get("GT_PROBE_ENGINE", "tensor")))
         print(f"[{tag}] C4 {timed(tr.capture(X, Y, F, keys), 10):.3f} ms", flush=True)
     elif what == "walk":
         rng = np.random.default_rng(1)
