@@ -190,6 +190,9 @@ int gt_diag_philox(uint32_t grid, uint32_t iters, uint64_t* out, void* stream);
    ladder end (phase 7), 64 + 8*level + phase for the prologue and the
    division (tools/hc_timing.py). */
 int gt_diag_hc_timestamps(unsigned long long* out, int n);
+/* diagnostics: phase timestamps (ns, globaltimer) of the fused count's first
+ * cluster per level, 8 slots per level, filled when GT_COUNT_TS is set */
+int gt_diag_count_timestamps(unsigned long long* out, int n);
 
 #ifdef __cplusplus
 }

@@ -101,6 +101,7 @@ _SIGS = {
                                 _u64p, _u64p, ctypes.POINTER(gt_keys), ctypes.c_void_p]),
     "gt_diag_philox": (ctypes.c_int, [ctypes.c_uint32, ctypes.c_uint32, _u64p, ctypes.c_void_p]),
     "gt_diag_hc_timestamps": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "gt_diag_count_timestamps": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
 }
 EXPORTS = tuple(_SIGS)
 

@@ -52,6 +52,7 @@ inline TcPlan tc_plan(int nf, int n_h) {
   p.nbn = (p.CW + 19) / 20;
   p.cpb = (p.CW + p.nbn - 1) / p.nbn;
   p.cpb += p.cpb & 1;
+  if (p.nbn == 2) p.cpb = 16;  // 21..32 columns: two 16-column blocks, the A halves of the fused CTA pair
   p.N = 8 * p.cpb;
   p.mtiles = (n_h + 15) / 16;
   p.BB = p.N * TC_KB;
@@ -691,6 +692,403 @@ __global__ void __launch_bounds__(256, 1) k_count_mma_t(MmaArgs a) {
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused count (lanes + contraction in one CTA pair, 21..32 sample columns)
+// ---------------------------------------------------------------------------
+//
+// The count of one level without the la planes ever leaving shared memory:
+// a cluster of two CTAs (one per SM of a TPC) runs ONE tcgen05.mma.cta_group::2
+// stream with the operand roles of k_count_mma_t,
+//     D_c[(w,q)][(n,p)] = sum_s X_c[(w,q)][s] la_c[(n,p)][s] + X_{c+1} la_c + X_c la_{c+1},
+// M = 256 = 32 sample columns x 8 limbs (CTA r holds the x planes of column
+// block r: its own M half), N = 16 NBn = 2 NBn nodes x 8 limbs where CTA r
+// holds the la rows of ITS NBn nodes (the B operand of a CTA pair is split
+// along N: tools/umma2_probe.cu, profiles/r02c_umma2_probe.txt).  So every
+// lane la = b2a(eq(m_idx, off+n) & is_leaf[n]) (train.py:211-217) is computed
+// exactly once, by the producer warps of the CTA that owns node n, straight
+// into the shared-memory B stage; the MMA reads both CTAs' stages; the
+// contraction runs on the tensor pipe under the producers' ALU work.
+// Pipeline per CTA: stages of 64 samples; x planes in a 3-deep ring by one
+// bulk copy each (xfull / xempty), la bytes by the producer warps in a deep
+// ring (full[s] = NBn producer arrivals / empty[s]); the peer relays its
+// full[s] to the leader's pfull[s]; the leader's commits multicast empty[s]
+// and xempty to both CTAs.  Same lanes, same
+// randomness and the same epilogue sums as lanes8 + k_count_mma_t: the
+// shares are identical.
+constexpr int TCF_MAXS = 16;                      // la stages (the x-plane ring has XS)
+constexpr int TCF_MAXXS = 8;                      // x-plane stages (at most)
+constexpr int TCF_XB = 3 * 128 * (TC_KB / 2);     // x planes of a stage: 3 components x 128 rows x 64 samples
+__host__ __device__ inline int tcf_la_bytes(int nbn_nodes) { return 3 * 512 * nbn_nodes; }
+// x-plane stages: deep where the level has few nodes (the contraction then
+// streams the x planes; lane work is small), 3 at 16-node tiles
+__host__ __device__ inline int tcf_xstages(int nbn_nodes) { return nbn_nodes <= 2 ? 6 : nbn_nodes <= 4 ? 4 : 3; }
+// la stages: a deep ring, so a producer warp that runs ahead of the slowest
+// one rarely waits for a slot (each stage needs all NBn node items)
+__host__ __device__ inline int tcf_stages(int nbn_nodes) {
+  const int s = (200 * 1024 - tcf_xstages(nbn_nodes) * TCF_XB) / tcf_la_bytes(nbn_nodes);
+  return s > TCF_MAXS ? TCF_MAXS : s;
+}
+__host__ __device__ inline int tcf_smem(int nbn_nodes) {
+  return tcf_xstages(nbn_nodes) * TCF_XB + tcf_stages(nbn_nodes) * tcf_la_bytes(nbn_nodes);
+}
+
+struct FusedArgs {
+  const uint64_t *midx, *f, *leafbits;  // leafbits: is_leaf [3][n_h] from the partition launch, or null
+  const uint8_t* B8;                    // x planes (tc_plan nbn = 2, cpb = 16)
+  uint64_t* S;                          // [3][n_h][W+1]
+  const uint64_t* alpha_tab;            // the level's reshare sums [n][3][W] or null (drawn)
+  Keys K;
+  uint32_t op_cnt, op_leaf;
+  int alpha;                            // 0 none, 1 telescoped, 2 dot
+  uint64_t t0, t1;                      // shard sample range (telescoped sums)
+  uint64_t N, base;                     // shard samples, global index of shard sample 0
+  uint64_t nkb_total, kb_lo;            // shard K blocks; first K block of this launch's range
+  uint32_t nkb;                         // K blocks of the range
+  int n_h, W, nkr, NBn, stages;
+  int ts_level;  // diagnostics (GT_COUNT_TS): phase timestamps of cluster 0 into g_cnt_ts[8 level ..], -1 off
+};
+
+__device__ unsigned long long g_cnt_ts[128];
+__device__ __forceinline__ void cnt_ts(const FusedArgs& a, int slot, bool on) {
+  if (a.ts_level < 0 || !on || blockIdx.y != 0 || blockIdx.z != 0 || blockIdx.x != 0) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_cnt_ts[8 * a.ts_level + slot] = t;
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_local(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_rank0(uint64_t* bar) {  // the same barrier in cluster CTA 0
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void umma2_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {  // arrive on `bar` in both CTAs of the pair
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+// PW producer warps + one copy / MMA warp; PF: each producer loads its next
+// item's node indices before computing the current one (the lane math hides
+// their L2 latency)
+template <int PW, bool PF>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 1), 1) k_count_fused(FusedArgs a) {
+  constexpr int TCF_PW = PW, TCF_THREADS = 32 * (PW + 1);
+  extern __shared__ __align__(1024) uint8_t smt[];
+  __shared__ __align__(8) uint64_t full[TCF_MAXS], empty[TCF_MAXS], pfull[TCF_MAXS], xfull[TCF_MAXXS], xempty[TCF_MAXXS],
+      done;
+  __shared__ uint32_t tmem_slot;
+  __shared__ uint64_t leaf[3][8];
+  const uint32_t rank = cluster_rank();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nt = blockIdx.y, kr = blockIdx.z;
+  const int NBn = a.NBn, NU = 16 * NBn, NS = a.stages;  // NU: the pair's UMMA N (2 NBn nodes x 8 limbs)
+  const int LB = tcf_la_bytes(NBn);
+  const int XS = tcf_xstages(NBn);
+  uint8_t* lring = smt + XS * TCF_XB;  // la stages after the x-plane stages
+  const uint32_t ACS = 512u * NBn, ALBO = 128u * NBn;  // la: [c][kc 4][g NBn][p 8][16 samples] per stage
+  const uint32_t per = (a.nkb + a.nkr - 1) / a.nkr;
+  const uint32_t kb0 = kr * per, kb1 = min(a.nkb, kb0 + per);
+  const int T = kb1 > kb0 ? 2 * (int)(kb1 - kb0) : 0;  // 64-sample stages
+  const int node0 = nt * 16 + (int)rank * NBn;          // this CTA's first node
+  const uint32_t tcols = NU * 3 <= 256 ? 256u : 512u;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                 "r"(tcols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  if (tid == 32) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], NBn);
+      mbar_init(&empty[i], 1);
+      mbar_init(&pfull[i], 1);
+    }
+    for (int i = 0; i < XS; ++i) {
+      mbar_init(&xfull[i], 1);
+      mbar_init(&xempty[i], 1);
+    }
+    mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // both CTAs' barriers exist before any remote arrive / multicast commit
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+  // the epilogue's precomputed reshare sums: loaded before the wait
+  uint64_t apre[4] = {0, 0, 0, 0};
+  const int NNt = 2 * NBn, cells = 3 * NNt * 16;
+  if (a.alpha && kr == 0 && a.alpha_tab) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int cell = tid + k * TCF_THREADS;
+      const int w = cell & 15, cn = cell >> 4, ni = cn % NNt, c = cn / NNt;
+      const int n = nt * 16 + ni, wg = (int)rank * 16 + w;
+      if (cell < cells && n < a.n_h && wg < a.W) apre[k] = a.alpha_tab[((uint64_t)n * 3 + c) * a.W + wg];
+    }
+  }
+  cnt_ts(a, 0, tid == 0);
+  pdl_wait();  // m_idx, is_leaf, the zeroed sums (partition) and the x planes (prologue)
+  cnt_ts(a, 1, tid == 0);
+  if (tid < NBn) {
+    const int n = node0 + tid;
+    B3 z = {{0, 0, 0}};
+    if (n < a.n_h && a.leafbits) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) z.v[c] = a.leafbits[c * a.n_h + n];
+    } else if (n < a.n_h) {
+      z = eqz<64>(a.K, a.op_leaf, 0, (uint64_t)n, add_pub<64>(ld3s(a.f, a.n_h, n), 0ull - F_LEAF));
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) leaf[c][tid] = z.v[c] & 1ull;
+  }
+  __syncthreads();
+
+  if (warp < TCF_PW) {
+    // producers: warp item (stage t, node g) = the 64 samples of stage t at
+    // node node0 + g, one sample pair per lane (count_lane_pair); bytes as in
+    // k_count_lanes8 (pairs of lanes swap limb halves with one shuffle pair)
+    const bool odd = lane & 1;
+    const int s2 = 2 * lane, items = T * NBn;
+    auto sample_of = [&](int i) {
+      const int t = i / NBn;
+      return ((uint64_t)a.kb_lo + kb0 + (uint32_t)(t >> 1)) * TC_KB + (t & 1) * (TC_KB / 2) + s2;
+    };
+    auto load_idx = [&](int i, uint64_t (&m)[6]) {
+      const uint64_t s = sample_of(i);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) m[k] = 0;
+      if (i < items && s < a.N) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) m[c] = __ldg(a.midx + c * a.N + s);
+        if (s + 1 < a.N)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) m[3 + c] = __ldg(a.midx + c * a.N + s + 1);
+      }
+    };
+    uint64_t mnext[6];
+    if (PF) load_idx(warp, mnext);
+    for (int i = warp; i < items; i += TCF_PW) {
+      const int t = i / NBn, g = i - t * NBn, st = t % NS;
+      uint64_t mc[6];
+      if (PF) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) mc[k] = mnext[k];
+        load_idx(i + TCF_PW, mnext);
+      } else {
+        load_idx(i, mc);
+      }
+      if (t >= NS) mbar_wait(&empty[st], (uint32_t)(((t / NS) - 1) & 1));
+      const int n = node0 + g;
+      const uint64_t s = sample_of(i);
+      A3 l0 = a3(0, 0, 0), l1 = a3(0, 0, 0);
+      const bool v0 = n < a.n_h && s < a.N, v1 = v0 && s + 1 < a.N;
+      if (v0) {
+        const uint64_t off = 0ull - (uint64_t)(a.n_h - 1 + n);
+        const A3 d0 = add_pub<64>(a3(mc[0], mc[1], mc[2]), off);
+        A3 d1 = a3(0, 0, 0);
+        if (v1) d1 = add_pub<64>(a3(mc[3], mc[4], mc[5]), off);
+        B3 lf;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) lf.v[c] = leaf[c][g];
+        count_lane_pair(a.K, a.op_cnt, a.base + s, a.n_h, n, d0, d1, true, v1, lf, &l0, &l1);
+      }
+      {  // s_mask (train.py:220): the warp's 64 samples of node n, one atomic per component
+        A3 m = v1 ? add<64>(l0, l1) : l0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) m.v[c] += __shfl_xor_sync(0xffffffffu, m.v[c], o);
+        if (lane == 0 && n < a.n_h)
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            atomicAdd((unsigned long long*)&a.S[((uint64_t)c * a.n_h + n) * (a.W + 1) + a.W], (unsigned long long)m.v[c]);
+      }
+      uint8_t* lb = lring + st * LB;
+      const int o = ((((s2 >> 4) & 3) * NBn + g) * 8) * 16 + ((s2 & ~3) & 15);
+      const int p0 = odd ? 4 : 0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const uint32_t a_lo = (uint32_t)l0.v[c], a_hi = (uint32_t)(l0.v[c] >> 32);
+        const uint32_t b_lo = (uint32_t)l1.v[c], b_hi = (uint32_t)(l1.v[c] >> 32);
+        const uint32_t P01 = __byte_perm(a_lo, b_lo, 0x5140), P23 = __byte_perm(a_lo, b_lo, 0x7362);
+        const uint32_t P45 = __byte_perm(a_hi, b_hi, 0x5140), P67 = __byte_perm(a_hi, b_hi, 0x7362);
+        const uint32_t r0 = __shfl_xor_sync(0xffffffffu, odd ? P01 : P45, 1);
+        const uint32_t r1 = __shfl_xor_sync(0xffffffffu, odd ? P23 : P67, 1);
+        uint32_t w[4];
+        if (!odd) {
+          w[0] = __byte_perm(P01, r0, 0x5410);
+          w[1] = __byte_perm(P01, r0, 0x7632);
+          w[2] = __byte_perm(P23, r1, 0x5410);
+          w[3] = __byte_perm(P23, r1, 0x7632);
+        } else {
+          w[0] = __byte_perm(r0, P45, 0x5410);
+          w[1] = __byte_perm(r0, P45, 0x7632);
+          w[2] = __byte_perm(r1, P67, 0x5410);
+          w[3] = __byte_perm(r1, P67, 0x7632);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) *reinterpret_cast<uint32_t*>(lb + c * ACS + o + (p0 + k) * 16) = w[k];
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> the tensor pipe's view
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(&full[st]);
+      cnt_ts(a, 2, lane == 0 && i == 0);
+      cnt_ts(a, 3, lane == 0 && i + TCF_PW >= items);
+    }
+  } else if (lane == 0 && T > 0) {
+    // copy + MMA thread: x planes of column block `rank` by bulk copy; the
+    // leader issues the pair's UMMAs once both CTAs' stage is full
+    const uint32_t idesc = (2u << 4) | ((uint32_t)(NU >> 3) << 17) | ((256u >> 4) << 24);
+    auto load = [&](int t) {
+      const int xs = t % XS;
+      const uint64_t kb = a.kb_lo + kb0 + (uint32_t)(t >> 1), h = t & 1;
+      mbar_expect_tx(&xfull[xs], (uint32_t)TCF_XB);
+      bulk_g2s(smt + xs * TCF_XB, a.B8 + (((uint64_t)rank * a.nkb_total + kb) * 2 + h) * (uint64_t)TCF_XB,
+               (uint32_t)TCF_XB, &xfull[xs]);
+    };
+    for (int t = 0; t < min(XS, T); ++t) load(t);
+    for (int t = 0; t < T; ++t) {
+      const int st = t % NS, xs = t % XS;
+      const uint32_t ph = (uint32_t)((t / NS) & 1);
+      mbar_wait(&xfull[xs], (uint32_t)((t / XS) & 1));
+      mbar_wait(&full[st], ph);
+      if (rank == 0) {
+        mbar_wait_cluster(&pfull[st], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t base = smem_u32(smt + xs * TCF_XB), lbase = smem_u32(lring + st * LB);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const uint32_t xo = j * 2 * 2048, ao = j * 2 * ALBO;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const int cn = (c + 1) % 3;
+            const uint32_t Xc = base + c * 8192 + xo, Xn = base + cn * 8192 + xo;
+            const uint32_t Ac = lbase + c * ACS + ao, An = lbase + cn * ACS + ao;
+            const uint32_t D = tmem + (uint32_t)(c * NU);
+            umma2_i8(D, umma_desc(Xc, 2048, 128), umma_desc(Ac, ALBO, 128), idesc, (t > 0 || j > 0) ? 1u : 0u);
+            umma2_i8(D, umma_desc(Xn, 2048, 128), umma_desc(Ac, ALBO, 128), idesc, 1u);
+            umma2_i8(D, umma_desc(Xc, 2048, 128), umma_desc(An, ALBO, 128), idesc, 1u);
+          }
+        }
+        umma2_commit_both(&empty[st]);
+        umma2_commit_both(&xempty[xs]);
+      } else {
+        mbar_arrive_rank0(&pfull[st]);
+      }
+      // refill the x-plane stage of the previous step (its MMAs were issued a step earlier)
+      if (t >= 1 && t - 1 + XS < T) {
+        const int pxs = (t - 1) % XS;
+        mbar_wait(&xempty[pxs], (uint32_t)(((t - 1) / XS) & 1));
+        load(t - 1 + XS);
+      }
+    }
+    if (rank == 0) umma2_commit_both(&done);
+    cnt_ts(a, 4, true);
+  }
+  __syncwarp();
+  if (T > 0) mbar_wait(&done, 0);
+  cnt_ts(a, 5, tid == 0);
+  pdl_trigger();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  uint64_t* red = reinterpret_cast<uint64_t*>(smt);  // [3][NNt nodes][16 w][8 q] (the stages are idle now)
+  if (T > 0) {
+    if (warp < 4) {
+      // TMEM lane r = warp 32 + lane = (column w, limb q) of this CTA's block;
+      // accumulator columns j = node index x 8 + p (node index over the pair)
+      const int r = warp * 32 + lane, w = r >> 3, q = r & 7;
+      for (int c = 0; c < 3; ++c)
+        for (int j0 = 0; j0 < NU; j0 += 16) {
+          uint32_t d[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+              "%14, %15}, [%16];"
+              : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
+                "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
+              : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * NU + j0)));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            uint64_t v = 0;
+#pragma unroll
+            for (int p = 0; p < 8; ++p) v += (uint64_t)d[8 * k + p] << (8 * p);
+            const int ni = j0 / 8 + k;
+            red[((c * NNt + ni) * 16 + w) * 8 + q] = v << (8 * q);
+          }
+        }
+    }
+    __syncthreads();
+    const uint64_t Sstride = (uint64_t)a.n_h * (a.W + 1);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int cell = tid + k * TCF_THREADS;
+      if (cell >= cells) break;
+      const int w = cell & 15, cn = cell >> 4, ni = cn % NNt, c = cn / NNt;
+      const int n = nt * 16 + ni, wg = (int)rank * 16 + w;
+      if (n >= a.n_h || wg >= a.W) continue;
+      const uint4* rp = reinterpret_cast<const uint4*>(red + (uint64_t)cell * 8);
+      uint64_t v = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint4 x = rp[i];
+        v += ((uint64_t)x.y << 32 | x.x) + ((uint64_t)x.w << 32 | x.z);
+      }
+      if (a.alpha && kr == 0 && a.alpha_tab) {
+        v += apre[k];
+      } else if (a.alpha && kr == 0) {
+        uint64_t F[2];
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {
+          const Key& key = a.K.pair[qq == 0 ? c : (c + 2) % 3];
+          F[qq] = a.alpha == 2 ? word(key, a.op_cnt, 4, (uint32_t)wg, (uint64_t)n)
+                               : word(key, a.op_cnt, 3, (uint32_t)wg, a.t1 * (uint64_t)a.n_h + n) -
+                                     word(key, a.op_cnt, 3, (uint32_t)wg, a.t0 * (uint64_t)a.n_h + n);
+        }
+        v += F[0] - F[1];
+      }
+      atomicAdd((unsigned long long*)&a.S[c * Sstride + (uint64_t)n * (a.W + 1) + wg], (unsigned long long)v);
+    }
+  }
+  cnt_ts(a, 6, tid == 0);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // both CTAs are past their TMEM reads before the pair's columns are freed
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols) : "memory");
   }
 }
 

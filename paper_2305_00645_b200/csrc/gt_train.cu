@@ -1676,6 +1676,8 @@ inline uint64_t div_tape_level_off(int level, int nf, int TB) {  // W2 offset of
   return ((1ull << level) - 1) * 2ull * nf * (uint64_t)TB;
 }
 
+bool count_fused_ok(int nf);
+
 struct Layout {
   uint64_t xin, yin, fin, tout, fout, cols, la, cols8, leaf, midx, divtape, divtable, posttape, posttable, nodetape, nodetable, feattape, alphatab, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
 };
@@ -1694,7 +1696,8 @@ Layout layout(const gt_train_cfg& c, bool host_io = false) {
   if (c.count_engine == 0) {
     const TcPlan tp = tc_plan(c.nf, (int)nmax);
     const uint64_t nkb = (N + TC_KB - 1) / TC_KB;
-    L.la = take(2 * tc_la8_blocks(N, c.nf, c.depth) * 3ull * tp.mtiles * TC_ABLK / 8);  // two chunk buffers
+    // two chunk buffers (none for the fused count: its lanes never leave shared memory)
+    L.la = take(count_fused_ok(c.nf) ? 0 : 2 * tc_la8_blocks(N, c.nf, c.depth) * 3ull * tp.mtiles * TC_ABLK / 8);
     L.cols8 = take(3ull * tp.nbn * nkb * tp.BB / 8);
   } else {
     L.la = take(la_words(N, c.nf, c.depth));
@@ -2128,6 +2131,80 @@ int stream_after(cudaStream_t to, cudaStream_t from, cudaEvent_t ev) {
   return GT_OK;
 }
 
+// Fused count (21..32 sample columns): one launch per level range, CTA pairs
+// of (16-node tile, K range) produce the lanes straight into the tcgen05
+// B stages (k_count_fused); no la planes, no chunking.
+int launch_count_fused(const CountLaunch& c, const uint8_t* B8, int alpha, uint64_t t0, uint64_t t1, cudaStream_t s,
+                       int num_sms, Prof& P, uint64_t lo, uint64_t hi) {
+  hi = std::min<uint64_t>(hi, c.N);
+  if (hi <= lo) return GT_OK;
+  const int NN = std::min(16, c.n_h), NBn = std::max(1, NN / 2), ntiles = (c.n_h + 15) / 16;
+  const uint64_t nkb_total = (c.N + TC_KB - 1) / TC_KB;
+  const uint32_t kb_lo = (uint32_t)(lo / TC_KB);  // lo is a K-block boundary
+  const uint32_t nkb = (uint32_t)((hi - lo + TC_KB - 1) / TC_KB);
+  // one CTA per SM: the fewest waves of pairs the K-range bound allows, filled
+  // with as many K ranges as fit in them
+  const int pairs = std::max(1, num_sms / 2);
+  const int nkr_min = (int)((nkb + TC_MAX_KB_PER_CTA - 1) / TC_MAX_KB_PER_CTA);
+  const int waves = std::max(1, (ntiles * nkr_min + pairs - 1) / pairs);
+  int nkr = std::max(nkr_min, waves * pairs / ntiles);
+  nkr = std::min<int>(nkr, (int)nkb);
+  const int per = (int)((nkb + nkr - 1) / nkr);
+  nkr = (int)((nkb + per - 1) / per);
+  FusedArgs fa{};
+  fa.midx = c.midx;
+  fa.f = c.f;
+  fa.leafbits = c.leafbits;
+  fa.B8 = B8;
+  fa.S = c.S;
+  fa.alpha_tab = c.alpha_tab;
+  fa.K = c.K;
+  fa.op_cnt = op_id(c.level, SITE_COUNT);
+  fa.op_leaf = op_id(c.level, SITE_ISLEAF);
+  fa.alpha = lo == 0 ? alpha : 0;
+  fa.t0 = t0;
+  fa.t1 = t1;
+  fa.N = c.N;
+  fa.base = c.base;
+  fa.nkb_total = nkb_total;
+  fa.kb_lo = kb_lo;
+  fa.nkb = nkb;
+  fa.n_h = c.n_h;
+  fa.W = 2 * c.nf + 1;
+  fa.nkr = nkr;
+  fa.NBn = NBn;
+  fa.stages = tcf_stages(NBn);
+  {
+    static const bool ts = getenv("GT_COUNT_TS") != nullptr;
+    fa.ts_level = ts ? c.level : -1;
+  }
+  const int smem = tcf_smem(NBn);
+  cudaLaunchAttribute at[1];
+  const TcPlan tp = tc_plan(c.nf, c.n_h);
+  const bool win = l2_window_attr(B8, 3ull * tp.nbn * nkb_total * tp.BB, at);
+  // A/B: GT_FUSED_PW = producer warps (12 or 15), GT_FUSED_PF = 0/1 index prefetch
+  static const int pw = getenv("GT_FUSED_PW") ? atoi(getenv("GT_FUSED_PW")) : 15;
+  static const int pf = getenv("GT_FUSED_PF") ? atoi(getenv("GT_FUSED_PF")) : 0;
+  auto go = [&](auto kern, int threads) {
+    GT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    return launch_chain(kern, dim3(2, (unsigned)ntiles, (unsigned)nkr), dim3(threads), (size_t)smem, s,
+                        win ? at : nullptr, fa);
+  };
+  P.start();
+  int rc = pw == 15 ? (pf ? go(k_count_fused<15, true>, 512) : go(k_count_fused<15, false>, 512))
+                    : (pf ? go(k_count_fused<12, true>, 416) : go(k_count_fused<12, false>, 416));
+  if (rc) return rc;
+  P.stop(Prof::COUNT_CONTRACT);
+  GT_LAUNCH_CHECK("k_count_fused");
+  return GT_OK;
+}
+
+bool count_fused_ok(int nf) {
+  static const bool off = getenv("GT_NO_FUSED_COUNT") != nullptr;  // A/B experiments
+  const TcPlan tp = tc_plan(nf, 1);
+  return !off && tp.nbn == 2 && tp.cpb == 16;
+}
+
 // tensor engine: leaf + per chunk (byte-plane lanes, tcgen05 contraction)
 // Chunks alternate between two la8 buffers (each holds la8_blocks K blocks at
 // the deepest level): with a side stream, the contraction of chunk k runs
@@ -2136,6 +2213,7 @@ int stream_after(cudaStream_t to, cudaStream_t from, cudaEvent_t ev) {
 int launch_count_tc(const CountLaunch& c, const uint8_t* B8, uint64_t la8_blocks, int alpha, uint64_t t0,
                     uint64_t t1, cudaStream_t s, Side* side, int num_sms, Prof& P, uint64_t lo = 0,
                     uint64_t hi = ~0ull) {
+  if (count_fused_ok(c.nf)) return launch_count_fused(c, B8, alpha, t0, t1, s, num_sms, P, lo, hi);
   hi = std::min<uint64_t>(hi, c.N);
   const TcPlan tp = tc_plan(c.nf, c.n_h);
   // two chunk buffers when pipelining across streams, else one of twice the size
@@ -2745,6 +2823,13 @@ int gt_train_host(const gt_train_cfg* cfg, const uint64_t* features_h, const uin
   const HostIn hin{features_h, labels_h, filler_h, T_h, F_h};
   return train_impl(cfg, nullptr, nullptr, nullptr, nullptr, nullptr, depth_out, workspace, workspace_bytes, keys,
                     allreduce, allreduce_user, nullptr, nullptr, stream, nullptr, &hin);
+}
+
+// diagnostics: the fused count's phase timestamps of the last GT_COUNT_TS run (ns)
+int gt_diag_count_timestamps(unsigned long long* out, int n) {
+  if (!out || n < 0 || n > 128) return fail_inval("gt_diag_count_timestamps: bad output");
+  GT_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_cnt_ts, sizeof(unsigned long long) * n));
+  return GT_OK;
 }
 
 // diagnostics: the heuristic phase timestamps of the last GT_HC_TIMING run (ns)

@@ -24,7 +24,7 @@ import numpy as np
 from .ledger import REF_LANE_LIMIT, Ledger, Metrics, Transcript
 from .seeds import PARTIES, SeedSetup, derive_seed, filler_values, make_keys
 from .shares import RING64, AVec, ShareError, avecs_from_components, components_from_avecs, ring_of
-from .train import TrainConfig, TrainResult, as_config, resolved_depth, train_components
+from .train import TrainConfig, TrainResult, as_config, resolved_depth, train_pairs
 
 
 class TransportError(RuntimeError):
@@ -185,9 +185,9 @@ def train_tree(eng: PartyEngine, features, labels, cfg: TrainConfig) -> TrainRes
     cfg = as_config(cfg)
 
     def compute(payloads):
-        X = components_from_avecs([p[0] for p in payloads])
-        Y = components_from_avecs([p[1] for p in payloads])
-        T, F, depth = train_components(X, Y.reshape(3, -1), cfg, eng.seeds, eng.dealer_seed, device=eng.device)
+        T, F, depth = train_pairs([(p[0].lo, p[0].hi) for p in payloads],
+                                  [(p[1].lo.reshape(-1), p[1].hi.reshape(-1)) for p in payloads], cfg, eng.seeds,
+                                  eng.dealer_seed, device=eng.device)
         eng._ledger.train(n_samples, nf, resolved_depth(cfg, nf + 1), cfg.tau, cfg.score_ring.width,
                           grow_stop_level=depth - 1, policy=cfg.policy, heuristic=cfg.heuristic,
                           count_reshare=cfg.count_reshare)

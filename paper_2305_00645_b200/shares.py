@@ -120,6 +120,27 @@ def components_from_pairs(pairs: Sequence[Tuple[np.ndarray, np.ndarray]], ring: 
     return np.stack([ring.reduce(x) for x in los])
 
 
+def stage_pairs(pairs: Sequence[Tuple[np.ndarray, np.ndarray]], out: np.ndarray, check: bool = True) -> None:
+    """components_from_pairs written straight into `out` [3, ...] uint64 (the
+    pinned staging buffer of a host-operand device call): party i's lo is
+    component i; the replication check compares party i's hi with party
+    i+1's lo without temporaries beyond one reusable bool buffer."""
+    if len(pairs) != 3:
+        raise ShareError("need the share pairs of exactly three parties")
+    los = [np.asarray(p[0], dtype=np.uint64) for p in pairs]
+    his = [np.asarray(p[1], dtype=np.uint64) for p in pairs]
+    shape = out.shape[1:]
+    if any(x.shape != shape for x in los + his):
+        raise ShareError("share components disagree on shape")
+    eq = np.empty(shape, dtype=bool) if check else None
+    for i in range(3):
+        if check:
+            np.equal(his[i], los[(i + 1) % 3], out=eq)
+            if not eq.all():
+                raise ShareError("replication inconsistency between party pairs")
+        np.copyto(out[i], los[i])
+
+
 def components_from_avecs(vecs: Sequence, check: bool = True) -> np.ndarray:
     ring = ring_of(vecs[0])
     return components_from_pairs([(v.lo, v.hi) for v in vecs], ring, check)

@@ -277,6 +277,41 @@ def _cached_trainer(n: int, nf: int, cfg: TrainConfig, device, host_io: bool) ->
     return tr
 
 
+def train_pairs(x_pairs: Sequence, y_pairs: Sequence, cfg: TrainConfig, seeds: SeedSetup, dealer_seed: bytes,
+                *, device=None, check: bool = True) -> Tuple[np.ndarray, np.ndarray, int]:
+    """train_components on the three parties' (lo, hi) pairs (x: (N, nf), y:
+    (N,) per party): heuristic mpc stages the pairs straight into the cached
+    trainer's pinned buffers (replication check on the way), no intermediate
+    component array."""
+    from .shares import ShareError, components_from_pairs, stage_pairs
+
+    cfg = as_config(cfg)
+    lo0 = np.asarray(x_pairs[0][0])
+    if lo0.ndim != 2 or np.asarray(y_pairs[0][0]).shape != (lo0.shape[0],):
+        raise ValueError("features must be (n, nf) and labels (n,) per party")
+    n, nf = lo0.shape
+    if n == 0:
+        raise ValueError("dataset is empty")
+    if cfg.heuristic != "mpc":
+        X = components_from_pairs(x_pairs, RING64, check)
+        Y = components_from_pairs(y_pairs, RING64, check)
+        return train_components(X, Y, cfg, seeds, dealer_seed, device=device)
+    keys = make_keys(seeds, dealer_seed)
+    torch = _native.require_cuda()
+    with _TRAIN_LOCK:
+        tr = _cached_trainer(n, nf, cfg, device, True)
+        st = tr.staging
+        stage_pairs(x_pairs, st["X"].numpy().view(np.uint64), check)
+        stage_pairs(y_pairs, st["Y"].numpy().view(np.uint64), check)
+        st["fill"].numpy().view(np.uint64)[:] = filler_values(seeds.filler_seed, (1 << tr.depth) - 1, nf + 1)
+        s = torch.cuda.current_stream(tr.device)
+        depth = tr.run_host(st["X"], st["Y"], st["fill"], st["T"], st["F"], keys, stream=s)
+        s.synchronize()
+        slots = (1 << depth) - 1
+        return (st["T"].numpy().view(np.uint64)[:, :slots].copy(),
+                st["F"].numpy().view(np.uint64)[:, :slots].copy(), depth)
+
+
 def train_components(X: np.ndarray, Y: np.ndarray, cfg: TrainConfig, seeds: SeedSetup, dealer_seed: bytes,
                      *, device=None) -> Tuple[np.ndarray, np.ndarray, int]:
     """Whole-run entry on component-major shares: X [3, N, nf], Y [3, N]

@@ -55,6 +55,20 @@ def main():
         ks = ("prods", "partition", "count_lanes", "count_contract", "node_hc", "node_finish")
         print(f"[{tag}] C2 {ms:.4f} ms tree_ok={ok} |", " ".join(f"{k}={getattr(p, 'ms_' + k) * 1e3:.1f}us"
                                                               for k in ks), flush=True)
+    elif what == "cts":  # fused count phase timestamps per level (GT_COUNT_TS=1)
+        import ctypes
+        data, X, Y = bench._c2_inputs()
+        tr = DeviceTrainer(bench.N_C2, bench.NF_C2, TrainConfig(depth=bench.DEPTH_C2))
+        X, Y, F = t(X), t(Y), t(fill)
+        for _ in range(3):
+            tr.run(X, Y, F, keys)
+        torch.cuda.synchronize()
+        buf = (ctypes.c_ulonglong * 64)()
+        _native.check(_native.load().gt_diag_count_timestamps(buf, 64))
+        names = ["wait", "item0", "items", "mma", "done", "epi"]
+        for lv in range(bench.DEPTH_C2):
+            ts = buf[8 * lv: 8 * lv + 7]
+            print(f"level {lv}: " + " ".join(f"{n}=+{(ts[k + 1] - ts[0]) / 1e3:.1f}" for k, n in enumerate(names)) + " us")
     elif what == "c4":
         n, nf, depth = 10 ** 6, 32, 8
         rng = np.random.default_rng(3)
