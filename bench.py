@@ -707,6 +707,10 @@ def main():
                 "prods": cnt * (24 * (NF_C2 + 1) + 24 * (2 * NF_C2 + 1)), "node_hc": 0, "node_finish": 0}
     kname = {"count_lanes": "k_count_lanes8", "count_contract": "k_count_mma", "partition": "k_partition",
              "node_hc": "k_hc_div", "prods": "k_prep8", "node_finish": "k_node_finish"}
+    fused = prof_tot["count_lanes"] == 0 and prof_tot["count_contract"] > 0
+    if fused:  # k_count_fused: lanes + contraction in one kernel; SURVEY 8(d)'s count-level bytes
+        kname["count_contract"] = "k_count_fused"
+        bytes_of["count_contract"] = count_bytes(cnt, NF_C2, DEPTH_C2)
     alg = bytes_of[dom] * args.steps
     achieved = alg / (prof_tot[dom] / 1e3) / 1e9 if prof_tot[dom] > 0 else 0.0
     nlaunch = max(1, prof_n[dom])
@@ -715,6 +719,7 @@ def main():
     # (randomness schedule v2: a pair of eq lanes draws 2 x 3 dealer blocks + 3 shared pair blocks;
     # each lookup adds 2 x 3 telescoped reshare words per index)
     blocks = {"count_lanes": count_lane_blocks(cnt, DEPTH_C2),
+              "count_contract": count_lane_blocks(cnt, DEPTH_C2) if fused else None,
               "partition": partition_blocks(cnt, NF_C2, DEPTH_C2)}.get(dom)
     alu = None
     if blocks:

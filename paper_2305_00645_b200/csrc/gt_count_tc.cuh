@@ -721,18 +721,29 @@ __global__ void __launch_bounds__(256, 1) k_count_mma_t(MmaArgs a) {
 constexpr int TCF_MAXS = 16;                      // la stages (the x-plane ring has XS)
 constexpr int TCF_MAXXS = 8;                      // x-plane stages (at most)
 constexpr int TCF_XB = 3 * 128 * (TC_KB / 2);     // x planes of a stage: 3 components x 128 rows x 64 samples
-__host__ __device__ inline int tcf_la_bytes(int nbn_nodes) { return 3 * 512 * nbn_nodes; }
+// Shallow tiles (NBn <= 4) run THREE UMMAs per 32-sample step instead of
+// nine: with V_c = la_c + la_{c+1} (the ring sum; its byte planes are those
+// of the sum mod 2^64),
+//     D_c = X_c V_c + X_{c+1} la_c,
+// and the two B operands that meet A = X_c (V_c for D_c, la_{c-1} for
+// D_{c-1}) are stacked in one N = 2 x 16 NBn operand B_c = [V_c ; la_{c-1}]
+// per CTA half, writing its own accumulator region [D_c | D_{c-1}] (each
+// component is then the sum of two regions' halves, folded in the
+// epilogue).  Shallow levels are bound by the UMMAs' A reads (x planes,
+// 4 KB per UMMA and CTA); deep tiles keep nine UMMAs under the lane math.
+__host__ __device__ inline bool tcf_mode3(int nbn_nodes) { return nbn_nodes <= 4; }
+__host__ __device__ inline int tcf_la_bytes(int nbn_nodes, bool m3) { return (m3 ? 6 : 3) * 512 * nbn_nodes; }
 // x-plane stages: deep where the level has few nodes (the contraction then
 // streams the x planes; lane work is small), 3 at 16-node tiles
 __host__ __device__ inline int tcf_xstages(int nbn_nodes) { return nbn_nodes <= 2 ? 6 : nbn_nodes <= 4 ? 4 : 3; }
 // la stages: a deep ring, so a producer warp that runs ahead of the slowest
 // one rarely waits for a slot (each stage needs all NBn node items)
-__host__ __device__ inline int tcf_stages(int nbn_nodes) {
-  const int s = (200 * 1024 - tcf_xstages(nbn_nodes) * TCF_XB) / tcf_la_bytes(nbn_nodes);
+__host__ __device__ inline int tcf_stages(int nbn_nodes, bool m3) {
+  const int s = (200 * 1024 - tcf_xstages(nbn_nodes) * TCF_XB) / tcf_la_bytes(nbn_nodes, m3);
   return s > TCF_MAXS ? TCF_MAXS : s;
 }
-__host__ __device__ inline int tcf_smem(int nbn_nodes) {
-  return tcf_xstages(nbn_nodes) * TCF_XB + tcf_stages(nbn_nodes) * tcf_la_bytes(nbn_nodes);
+__host__ __device__ inline int tcf_smem(int nbn_nodes, bool m3) {
+  return tcf_xstages(nbn_nodes) * TCF_XB + tcf_stages(nbn_nodes, m3) * tcf_la_bytes(nbn_nodes, m3);
 }
 
 struct FusedArgs {
@@ -748,6 +759,7 @@ struct FusedArgs {
   uint64_t nkb_total, kb_lo;            // shard K blocks; first K block of this launch's range
   uint32_t nkb;                         // K blocks of the range
   int n_h, W, nkr, NBn, stages;
+  int mode3;     // three UMMAs per step (shallow tiles, tcf_mode3)
   int ts_level;  // diagnostics (GT_COUNT_TS): phase timestamps of cluster 0 into g_cnt_ts[8 level ..], -1 off
 };
 
@@ -801,12 +813,12 @@ __device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {  // arrive on
       : "memory");
 }
 
-// PW producer warps + one copy / MMA warp; PF: each producer loads its next
+// PW producer warps + a copy warp + an MMA warp; PF: each producer loads its next
 // item's node indices before computing the current one (the lane math hides
 // their L2 latency)
 template <int PW, bool PF>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 1), 1) k_count_fused(FusedArgs a) {
-  constexpr int TCF_PW = PW, TCF_THREADS = 32 * (PW + 1);
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 2), 1) k_count_fused(FusedArgs a) {
+  constexpr int TCF_PW = PW, TCF_THREADS = 32 * (PW + 2);
   extern __shared__ __align__(1024) uint8_t smt[];
   __shared__ __align__(8) uint64_t full[TCF_MAXS], empty[TCF_MAXS], pfull[TCF_MAXS], xfull[TCF_MAXXS], xempty[TCF_MAXXS],
       done;
@@ -816,7 +828,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 1), 1) k_
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nt = blockIdx.y, kr = blockIdx.z;
   const int NBn = a.NBn, NU = 16 * NBn, NS = a.stages;  // NU: the pair's UMMA N (2 NBn nodes x 8 limbs)
-  const int LB = tcf_la_bytes(NBn);
+  const bool mode3 = a.mode3;
+  const int LB = tcf_la_bytes(NBn, mode3);
   const int XS = tcf_xstages(NBn);
   uint8_t* lring = smt + XS * TCF_XB;  // la stages after the x-plane stages
   const uint32_t ACS = 512u * NBn, ALBO = 128u * NBn;  // la: [c][kc 4][g NBn][p 8][16 samples] per stage
@@ -824,7 +837,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 1), 1) k_
   const uint32_t kb0 = kr * per, kb1 = min(a.nkb, kb0 + per);
   const int T = kb1 > kb0 ? 2 * (int)(kb1 - kb0) : 0;  // 64-sample stages
   const int node0 = nt * 16 + (int)rank * NBn;          // this CTA's first node
-  const uint32_t tcols = NU * 3 <= 256 ? 256u : 512u;
+  const uint32_t tcols = (mode3 ? 6 : 3) * NU <= 256 ? 256u : 512u;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
@@ -939,12 +952,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 1), 1) k_
             atomicAdd((unsigned long long*)&a.S[((uint64_t)c * a.n_h + n) * (a.W + 1) + a.W], (unsigned long long)m.v[c]);
       }
       uint8_t* lb = lring + st * LB;
-      const int o = ((((s2 >> 4) & 3) * NBn + g) * 8) * 16 + ((s2 & ~3) & 15);
-      const int p0 = odd ? 4 : 0;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const uint32_t a_lo = (uint32_t)l0.v[c], a_hi = (uint32_t)(l0.v[c] >> 32);
-        const uint32_t b_lo = (uint32_t)l1.v[c], b_hi = (uint32_t)(l1.v[c] >> 32);
+      const int p0 = odd ? 4 : 0, sub = (s2 & ~3) & 15, kc = (s2 >> 4) & 3;
+      // the two samples' words x0, x1 as limb bytes into operand region `reg`
+      // (gpk node groups per 16-sample chunk) at node group G
+      auto put = [&](uint32_t reg, int gpk, int G, uint64_t x0, uint64_t x1) {
+        const uint32_t a_lo = (uint32_t)x0, a_hi = (uint32_t)(x0 >> 32);
+        const uint32_t b_lo = (uint32_t)x1, b_hi = (uint32_t)(x1 >> 32);
         const uint32_t P01 = __byte_perm(a_lo, b_lo, 0x5140), P23 = __byte_perm(a_lo, b_lo, 0x7362);
         const uint32_t P45 = __byte_perm(a_hi, b_hi, 0x5140), P67 = __byte_perm(a_hi, b_hi, 0x7362);
         const uint32_t r0 = __shfl_xor_sync(0xffffffffu, odd ? P01 : P45, 1);
@@ -961,8 +974,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 1), 1) k_
           w[2] = __byte_perm(r1, P67, 0x5410);
           w[3] = __byte_perm(r1, P67, 0x7632);
         }
+        uint8_t* dst = lb + reg + ((kc * gpk + G) * 8) * 16 + sub;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) *reinterpret_cast<uint32_t*>(lb + c * ACS + o + (p0 + k) * 16) = w[k];
+        for (int k = 0; k < 4; ++k) *reinterpret_cast<uint32_t*>(dst + (p0 + k) * 16) = w[k];
+      };
+      if (mode3) {  // B_c = [V_c ; la_{c-1}]: V_c at group g, la_c into B_{c+1} at group NBn + g
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int cn = c == 2 ? 0 : c + 1;
+          put((uint32_t)c * 2 * ACS, 2 * NBn, g, l0.v[c] + l0.v[cn], l1.v[c] + l1.v[cn]);
+          put((uint32_t)cn * 2 * ACS, 2 * NBn, NBn + g, l0.v[c], l1.v[c]);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) put((uint32_t)c * ACS, NBn, g, l0.v[c], l1.v[c]);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> the tensor pipe's view
       __syncwarp();
@@ -970,18 +995,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 1), 1) k_
       cnt_ts(a, 2, lane == 0 && i == 0);
       cnt_ts(a, 3, lane == 0 && i + TCF_PW >= items);
     }
-  } else if (lane == 0 && T > 0) {
-    // copy + MMA thread: x planes of column block `rank` by bulk copy; the
-    // leader issues the pair's UMMAs once both CTAs' stage is full
-    const uint32_t idesc = (2u << 4) | ((uint32_t)(NU >> 3) << 17) | ((256u >> 4) << 24);
-    auto load = [&](int t) {
+  } else if (warp == TCF_PW && lane == 0 && T > 0) {
+    // copy thread: the x planes of column block `rank`, XS stages ahead of
+    // the MMAs (a slot is refilled as soon as the pair's MMAs release it);
+    // the x planes are re-read by every level: kept in L2 (evict_last)
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    for (int t = 0; t < T; ++t) {
       const int xs = t % XS;
+      if (t >= XS) mbar_wait(&xempty[xs], (uint32_t)(((t / XS) - 1) & 1));
       const uint64_t kb = a.kb_lo + kb0 + (uint32_t)(t >> 1), h = t & 1;
       mbar_expect_tx(&xfull[xs], (uint32_t)TCF_XB);
-      bulk_g2s(smt + xs * TCF_XB, a.B8 + (((uint64_t)rank * a.nkb_total + kb) * 2 + h) * (uint64_t)TCF_XB,
-               (uint32_t)TCF_XB, &xfull[xs]);
-    };
-    for (int t = 0; t < min(XS, T); ++t) load(t);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+              smem_u32(smt + xs * TCF_XB)),
+          "l"(a.B8 + (((uint64_t)rank * a.nkb_total + kb) * 2 + h) * (uint64_t)TCF_XB), "r"((uint32_t)TCF_XB),
+          "r"(smem_u32(&xfull[xs])), "l"(pol)
+          : "memory");
+    }
+  } else if (warp == TCF_PW + 1 && lane == 0 && T > 0) {
+    // MMA thread (leader) / relay (peer): the leader issues the pair's UMMAs
+    // once both CTAs' stage t is full; the peer forwards its full stage
+    const uint32_t idesc = (2u << 4) | ((uint32_t)((mode3 ? 2 * NU : NU) >> 3) << 17) | ((256u >> 4) << 24);
     for (int t = 0; t < T; ++t) {
       const int st = t % NS, xs = t % XS;
       const uint32_t ph = (uint32_t)((t / NS) & 1);
@@ -991,30 +1026,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 1), 1) k_
         mbar_wait_cluster(&pfull[st], ph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t base = smem_u32(smt + xs * TCF_XB), lbase = smem_u32(lring + st * LB);
+        if (mode3) {
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const uint32_t xo = j * 2 * 2048, ao = j * 2 * ALBO;
+          for (int j = 0; j < 2; ++j)
 #pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const int cn = (c + 1) % 3;
-            const uint32_t Xc = base + c * 8192 + xo, Xn = base + cn * 8192 + xo;
-            const uint32_t Ac = lbase + c * ACS + ao, An = lbase + cn * ACS + ao;
-            const uint32_t D = tmem + (uint32_t)(c * NU);
-            umma2_i8(D, umma_desc(Xc, 2048, 128), umma_desc(Ac, ALBO, 128), idesc, (t > 0 || j > 0) ? 1u : 0u);
-            umma2_i8(D, umma_desc(Xn, 2048, 128), umma_desc(Ac, ALBO, 128), idesc, 1u);
-            umma2_i8(D, umma_desc(Xc, 2048, 128), umma_desc(An, ALBO, 128), idesc, 1u);
+            for (int c = 0; c < 3; ++c)  // region c: [D_c | D_{c-1}] += X_c [V_c ; la_{c-1}]
+              umma2_i8(tmem + (uint32_t)(c * 2 * NU), umma_desc(base + c * 8192 + j * 2 * 2048, 2048, 128),
+                       umma_desc(lbase + c * 2 * ACS + j * 2 * (2 * ALBO), 2 * ALBO, 128), idesc,
+                       (t > 0 || j > 0) ? 1u : 0u);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const uint32_t xo = j * 2 * 2048, ao = j * 2 * ALBO;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              const int cn = (c + 1) % 3;
+              const uint32_t Xc = base + c * 8192 + xo, Xn = base + cn * 8192 + xo;
+              const uint32_t Ac = lbase + c * ACS + ao, An = lbase + cn * ACS + ao;
+              const uint32_t D = tmem + (uint32_t)(c * NU);
+              umma2_i8(D, umma_desc(Xc, 2048, 128), umma_desc(Ac, ALBO, 128), idesc, (t > 0 || j > 0) ? 1u : 0u);
+              umma2_i8(D, umma_desc(Xn, 2048, 128), umma_desc(Ac, ALBO, 128), idesc, 1u);
+              umma2_i8(D, umma_desc(Xc, 2048, 128), umma_desc(An, ALBO, 128), idesc, 1u);
+            }
           }
         }
         umma2_commit_both(&empty[st]);
         umma2_commit_both(&xempty[xs]);
       } else {
         mbar_arrive_rank0(&pfull[st]);
-      }
-      // refill the x-plane stage of the previous step (its MMAs were issued a step earlier)
-      if (t >= 1 && t - 1 + XS < T) {
-        const int pxs = (t - 1) % XS;
-        mbar_wait(&xempty[pxs], (uint32_t)(((t - 1) / XS) & 1));
-        load(t - 1 + XS);
       }
     }
     if (rank == 0) umma2_commit_both(&done);
@@ -1031,23 +1070,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 1), 1) k_
       // TMEM lane r = warp 32 + lane = (column w, limb q) of this CTA's block;
       // accumulator columns j = node index x 8 + p (node index over the pair)
       const int r = warp * 32 + lane, w = r >> 3, q = r & 7;
+      if (mode3)  // two contributions per cell: zero this thread's cells first
+        for (int e = 0; e < 3 * NNt; ++e) red[(e * 16 + w) * 8 + q] = 0;
       for (int c = 0; c < 3; ++c)
-        for (int j0 = 0; j0 < NU; j0 += 16) {
+        for (int j0 = 0; j0 < (mode3 ? 2 * NU : NU); j0 += 16) {
           uint32_t d[16];
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
               "%14, %15}, [%16];"
               : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
                 "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
-              : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * NU + j0)));
+              : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * (mode3 ? 2 * NU : NU) + j0)));
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
           for (int k = 0; k < 2; ++k) {
             uint64_t v = 0;
 #pragma unroll
             for (int p = 0; p < 8; ++p) v += (uint64_t)d[8 * k + p] << (8 * p);
-            const int ni = j0 / 8 + k;
-            red[((c * NNt + ni) * 16 + w) * 8 + q] = v << (8 * q);
+            const int col = j0 + 8 * k;
+            if (mode3) {  // region c columns: [D_c(CTA 0 nodes) | D_{c-1}(0) | D_c(CTA 1 nodes) | D_{c-1}(1)]
+              const int blk = col / (8 * NBn), ni = (blk >= 2 ? NBn : 0) + (col % (8 * NBn)) / 8;
+              const int comp = (blk & 1) ? (c + 2) % 3 : c;
+              red[((comp * NNt + ni) * 16 + w) * 8 + q] += v << (8 * q);
+            } else {
+              red[((c * NNt + col / 8) * 16 + w) * 8 + q] = v << (8 * q);
+            }
           }
         }
     }

@@ -2173,17 +2173,22 @@ int launch_count_fused(const CountLaunch& c, const uint8_t* B8, int alpha, uint6
   fa.W = 2 * c.nf + 1;
   fa.nkr = nkr;
   fa.NBn = NBn;
-  fa.stages = tcf_stages(NBn);
+  {
+    static const bool no_m3 = getenv("GT_FUSED_NO_MODE3") != nullptr;  // A/B experiments
+    fa.mode3 = tcf_mode3(NBn) && !no_m3;
+  }
+  fa.stages = tcf_stages(NBn, fa.mode3);
   {
     static const bool ts = getenv("GT_COUNT_TS") != nullptr;
     fa.ts_level = ts ? c.level : -1;
   }
-  const int smem = tcf_smem(NBn);
+  const int smem = tcf_smem(NBn, fa.mode3);
   cudaLaunchAttribute at[1];
   const TcPlan tp = tc_plan(c.nf, c.n_h);
   const bool win = l2_window_attr(B8, 3ull * tp.nbn * nkb_total * tp.BB, at);
-  // A/B: GT_FUSED_PW = producer warps (12 or 15), GT_FUSED_PF = 0/1 index prefetch
-  static const int pw = getenv("GT_FUSED_PW") ? atoi(getenv("GT_FUSED_PW")) : 15;
+  // producer warps: 18 (measured C2 0.615 ms vs 0.618 / 0.625 at 14 / 22; 87
+  // registers); A/B: GT_FUSED_PW = 14, GT_FUSED_PF = 1 (node-index prefetch, no gain)
+  static const int pw = getenv("GT_FUSED_PW") ? atoi(getenv("GT_FUSED_PW")) : 18;
   static const int pf = getenv("GT_FUSED_PF") ? atoi(getenv("GT_FUSED_PF")) : 0;
   auto go = [&](auto kern, int threads) {
     GT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -2191,8 +2196,8 @@ int launch_count_fused(const CountLaunch& c, const uint8_t* B8, int alpha, uint6
                         win ? at : nullptr, fa);
   };
   P.start();
-  int rc = pw == 15 ? (pf ? go(k_count_fused<15, true>, 512) : go(k_count_fused<15, false>, 512))
-                    : (pf ? go(k_count_fused<12, true>, 416) : go(k_count_fused<12, false>, 416));
+  int rc = pw == 14 ? go(k_count_fused<14, false>, 512)
+         : pf ? go(k_count_fused<18, true>, 640) : go(k_count_fused<18, false>, 640);
   if (rc) return rc;
   P.stop(Prof::COUNT_CONTRACT);
   GT_LAUNCH_CHECK("k_count_fused");
