@@ -169,6 +169,13 @@ int gt_train_host(const gt_train_cfg* cfg, const uint64_t* features_h, const uin
                   uint64_t workspace_bytes, const gt_keys* keys, gt_allreduce_fn allreduce, void* allreduce_user,
                   void* stream);
 
+/* Host staging for the drop-in rendezvous (replaces the reference's per-party
+ * share handling, rss.py:222-228 consistency): lo[i] / hi[i] are party i+1's
+ * share pair (n words each); component i = lo[i] is written to out + i*n
+ * (pinned staging of gt_train_host); check != 0 requires hi[i] == lo[(i+1)%3].
+ * Host threads; no device work.  GT_ERR_INVALID on an inconsistent pair. */
+int gt_stage_pairs(const uint64_t* const* lo, const uint64_t* const* hi, uint64_t n, uint64_t* out, int check);
+
 /* ---- secure inference (infer_batch, infer.py:20-35) ---- */
 
 /* tree [3][2^depth-1] heap-ordered payload shares, queries [3][n][nf];

@@ -3,7 +3,11 @@
 // of lanes; the training and inference drivers use the same per-lane device
 // functions fused into larger kernels.
 #include <algorithm>
+#include <atomic>
+#include <cstring>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "gt_common.cuh"
 #include "gt_division.cuh"
@@ -224,6 +228,37 @@ using namespace gt;
 extern "C" {
 
 int gt_abi_version(void) { return GT_ABI_VERSION; }
+
+// Host staging of the three parties' replicated pairs (the drop-in's
+// rendezvous, rss.py:222-228 consistency): component i = party i+1's lo is
+// copied to out + i n; party i+1's hi must equal party i+2's lo word for word.
+// Split over host threads in 1 MB slices (memcmp + memcpy stream at memory
+// speed); returns GT_ERR_INVALID on an inconsistent pair.
+int gt_stage_pairs(const uint64_t* const* lo, const uint64_t* const* hi, uint64_t n, uint64_t* out, int check) {
+  if (!lo || !hi || !out) return fail_inval("gt_stage_pairs: NULL operand");
+  for (int i = 0; i < 3; ++i)
+    if (n && (!lo[i] || !hi[i])) return fail_inval("gt_stage_pairs: NULL component");
+  const uint64_t slice = 1ull << 17;  // words
+  const uint64_t nsl = (n + slice - 1) / slice;
+  std::atomic<uint64_t> next{0};
+  std::atomic<int> bad{0};
+  auto work = [&]() {
+    for (uint64_t k = next++; k < 3 * nsl && !bad.load(std::memory_order_relaxed); k = next++) {
+      const int i = (int)(k / nsl);
+      const uint64_t a = (k % nsl) * slice, len = std::min<uint64_t>(slice, n - a);
+      if (check && std::memcmp(hi[i] + a, lo[(i + 1) % 3] + a, len * 8) != 0) bad = 1;
+      std::memcpy(out + (uint64_t)i * n + a, lo[i] + a, len * 8);
+    }
+  };
+  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  const unsigned nth = (unsigned)std::min<uint64_t>(hw, 3 * nsl);
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < nth; ++t) pool.emplace_back(work);
+  work();
+  for (auto& t : pool) t.join();
+  if (bad) return fail_inval("replication inconsistency between party pairs");
+  return GT_OK;
+}
 const char* gt_last_error(void) { return g_last_error.c_str(); }
 
 int gt_mul(int width, const uint64_t* x, const uint64_t* y, uint64_t* z, uint64_t n, const gt_keys* keys, uint32_t op,

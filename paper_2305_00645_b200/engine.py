@@ -16,7 +16,6 @@ from __future__ import annotations
 
 import threading
 import time
-from dataclasses import dataclass
 from typing import Callable, List, Optional, Sequence, Union
 
 import numpy as np
@@ -128,11 +127,20 @@ def _own(eng) -> "PartyEngine":
     return eng
 
 
-@dataclass
 class LocalRun:
-    results: List
-    transcript: Transcript
-    metrics: Metrics
+    """rss.py:489-493: results per party, the transcript and its metrics
+    (summarised from the transcript on first access)."""
+
+    def __init__(self, results: List, transcript: Transcript, metrics: Optional[Metrics] = None):
+        self.results = results
+        self.transcript = transcript
+        self._metrics = metrics
+
+    @property
+    def metrics(self) -> Metrics:
+        if self._metrics is None:
+            self._metrics = Metrics.from_transcript(self.transcript)
+        return self._metrics
 
 
 def run_local(fn: Callable[[PartyEngine], object], *, seeds: Union[SeedSetup, int], materials: Optional[Sequence] = None,
@@ -174,7 +182,7 @@ def run_local(fn: Callable[[PartyEngine], object], *, seeds: Union[SeedSetup, in
     for e in errors:
         if e is not None:
             raise e
-    return LocalRun(results=results, transcript=ledger.transcript, metrics=ledger.metrics())
+    return LocalRun(results=results, transcript=ledger.transcript)
 
 
 def train_tree(eng: PartyEngine, features, labels, cfg: TrainConfig) -> TrainResult:

@@ -132,6 +132,18 @@ def stage_pairs(pairs: Sequence[Tuple[np.ndarray, np.ndarray]], out: np.ndarray,
     shape = out.shape[1:]
     if any(x.shape != shape for x in los + his):
         raise ShareError("share components disagree on shape")
+    if all(x.flags.c_contiguous for x in los + his) and out.flags.c_contiguous:
+        import ctypes
+
+        from . import _native
+
+        lib = _native.load()
+        arr = ctypes.c_void_p * 3
+        rc = lib.gt_stage_pairs(arr(*[x.ctypes.data for x in los]), arr(*[x.ctypes.data for x in his]),
+                                int(np.prod(shape, dtype=np.int64)), out.ctypes.data, 1 if check else 0)
+        if rc:
+            raise ShareError(lib.gt_last_error().decode())
+        return
     eq = np.empty(shape, dtype=bool) if check else None
     for i in range(3):
         if check:

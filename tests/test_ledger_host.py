@@ -109,6 +109,26 @@ def test_share_conversion_and_consistency_check():
     assert np.array_equal(reconstruct(comp, RING32), (comp[0] + comp[1] + comp[2]) & np.uint64(0xFFFFFFFF))
 
 
+def test_native_host_staging_of_party_pairs():
+    """gt_stage_pairs (host threads, no device work): the drop-in's pinned
+    staging equals components_from_pairs, and an inconsistent pair raises
+    ShareError like the reference's replication check (rss.py:222-228)."""
+    from paper_2305_00645_b200.shares import stage_pairs
+
+    rng = np.random.default_rng(1)
+    comp = rng.integers(0, 1 << 63, (3, 300_001), dtype=np.uint64)  # several 1 MB slices per component
+    pairs = pairs_from_components(comp)
+    out = np.empty_like(comp)
+    stage_pairs(pairs, out)
+    assert np.array_equal(out, comp)
+    bad = [pairs[0], (pairs[1][0], pairs[1][1].copy()), pairs[2]]
+    bad[1][1][299_999] ^= np.uint64(1)
+    with pytest.raises(ShareError):
+        stage_pairs(bad, out)
+    stage_pairs(bad, out, check=False)  # unchecked staging copies the lo components
+    assert np.array_equal(out, comp)
+
+
 def test_division_params_match_reference():
     assert L.div_params(32, 10) == {"bound": 20, "ti": 14, "sigma": 7, "kf": 17, "iters": 6, "w0": 47746}
     with pytest.raises(ValueError):

@@ -1,16 +1,35 @@
 """Summarise an ncu --metrics gpu__time_duration.sum launch list: per-kernel
-totals over the second half of the launches (steady state)."""
-import collections, csv, sys
+totals per tree (all launches / the number of k_init launches, i.e. trees),
+or over the second half of the launches when the list has no k_init."""
+import collections
+import csv
+import sys
+
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 5]
-hdr = rows[0]; ki = hdr.index("Kernel Name"); vi = hdr.index("Metric Value")
+hdr = rows[0]
+ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
 rows = rows[1:]
-if len(sys.argv) < 3 or sys.argv[2] != "all":
+
+
+def name(r):
+    n = r[ki].replace("void ", "").replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("gt::", "")
+    return n.split("(")[0].split("<")[0]
+
+
+trees = sum(1 for r in rows if name(r) == "k_init")
+if not trees:
     rows = rows[len(rows) // 2:]
-agg = collections.defaultdict(float); cnt = collections.Counter()
+trees = max(1, trees)
+agg = collections.defaultdict(float)
+cnt = collections.Counter()
 for r in rows:
-    n = r[ki].split("(")[0].split("<")[0].replace("void ", "").replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
-    agg[n] += float(r[vi].replace(",", "")); cnt[n] += 1
+    v = r[vi].replace(",", "")
+    if v in ("", "nan", "n/a"):
+        continue
+    agg[name(r)] += float(v) / trees
+    cnt[name(r)] += 1
 tot = sum(agg.values())
+print(f"per tree over {trees} tree(s)")
 for k, v in sorted(agg.items(), key=lambda x: -x[1]):
-    print(f"{k:34s} {cnt[k]:4d} {v / 1e3:9.1f} us {100 * v / tot:5.1f} %")
-print(f"{'total':34s} {sum(cnt.values()):4d} {tot / 1e3:9.1f} us")
+    print(f"{k:34s} {cnt[k] / trees:6.1f} {v / 1e3:9.1f} us {100 * v / tot:5.1f} %")
+print(f"{'total':34s} {sum(cnt.values()) / trees:6.1f} {tot / 1e3:9.1f} us")

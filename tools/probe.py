@@ -2,6 +2,8 @@
 
   python tools/probe.py c2      C2 tree: CUDA-graph replay median ms + per-kernel-class ms
   python tools/probe.py walk    C3 (10^4 x 13, 7 levels) and a C5 slice (2*10^6 x 32, 10 levels) inst/s
+  python tools/probe.py c2eager three eager C2 trees (launch lists)
+  python tools/probe.py cts     fused count phase timestamps per level (GT_COUNT_TS=1)
   python tools/probe.py c4      C4 tree (10^6 x 32, depth 8) graph replay median ms
 Launch switches (GT_PART_G, GT_WALK_G, ...) come from the environment;
 GT_PROBE_ENGINE=cuda runs the count contraction on the CUDA cores (A/B).
@@ -55,6 +57,15 @@ def main():
         ks = ("prods", "partition", "count_lanes", "count_contract", "node_hc", "node_finish")
         print(f"[{tag}] C2 {ms:.4f} ms tree_ok={ok} |", " ".join(f"{k}={getattr(p, 'ms_' + k) * 1e3:.1f}us"
                                                               for k in ks), flush=True)
+    elif what == "c2eager":  # launch lists: eager tree runs (ncu --graph-profiling graph)
+        data, X, Y = bench._c2_inputs()
+        tr = DeviceTrainer(bench.N_C2, bench.NF_C2, TrainConfig(depth=bench.DEPTH_C2))
+        X, Y, F = t(X), t(Y), t(fill)
+        for _ in range(3):
+            tr.run(X, Y, F, keys)
+        torch.cuda.synchronize()
+        z = np.load(os.path.join(bench.ROOT, "tests", "golden", "c2c3.npz"))
+        print("tree_ok", np.array_equal(tr.T.sum(0).cpu().numpy().view(np.uint64), z["T"]))
     elif what == "cts":  # fused count phase timestamps per level (GT_COUNT_TS=1)
         import ctypes
         data, X, Y = bench._c2_inputs()
