@@ -176,6 +176,15 @@ int gt_train_host(const gt_train_cfg* cfg, const uint64_t* features_h, const uin
  * Host threads; no device work.  GT_ERR_INVALID on an inconsistent pair. */
 int gt_stage_pairs(const uint64_t* const* lo, const uint64_t* const* hi, uint64_t n, uint64_t* out, int check);
 
+/* Device loading of dealt share files / material banks (reference
+ * rss.py:452-481 OBS1, dealer.py:131-176 OBD1): lo[i] / hi[i] are DEVICE
+ * pointers to party i+1's little-endian ring words (word_bytes 1/4/8, stride
+ * bytes apart: 2 words for OBS1's interleaved pairs); component i of out
+ * [3][n] (u64) = party i+1's lo words; if mismatches != NULL (device counter)
+ * every hi[i] word is compared with lo[(i+1)%3] and differences counted. */
+int gt_unpack_pairs(const void* const* lo, const void* const* hi, uint32_t stride_bytes, uint32_t word_bytes,
+                    uint64_t n, uint64_t* out, unsigned long long* mismatches, void* stream);
+
 /* ---- secure inference (infer_batch, infer.py:20-35) ---- */
 
 /* tree [3][2^depth-1] heap-ordered payload shares, queries [3][n][nf];

@@ -102,6 +102,9 @@ _SIGS = {
     "gt_diag_philox": (ctypes.c_int, [ctypes.c_uint32, ctypes.c_uint32, _u64p, ctypes.c_void_p]),
     "gt_diag_hc_timestamps": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "gt_diag_count_timestamps": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "gt_unpack_pairs": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p), ctypes.c_uint32,
+                                       ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p]),
     "gt_stage_pairs": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p), ctypes.c_uint64,
                                       ctypes.c_void_p, ctypes.c_int]),
 }

@@ -206,6 +206,29 @@ __global__ void __launch_bounds__(256) k_diag_philox(uint32_t iters, uint64_t* o
   out[t] = acc;
 }
 
+// Deal-directory / material-bank loading (reference rss.py:452-481,
+// dealer.py:131-176): party i's little-endian ring words at lo.p[i] (stride
+// bytes apart) become component i of out[3][n]; hi.p[i] must equal the next
+// party's lo word (replicated sharing), mismatches counted into *bad.
+struct Ptr3 {
+  const uint8_t* p[3];
+};
+__device__ __forceinline__ uint64_t le_word(const uint8_t* q, uint32_t wb) {
+  if (wb == 8 && (reinterpret_cast<uintptr_t>(q) & 7) == 0) return *reinterpret_cast<const uint64_t*>(q);
+  uint64_t v = 0;
+  for (uint32_t b = 0; b < wb; ++b) v |= (uint64_t)q[b] << (8 * b);
+  return v;
+}
+__global__ void k_unpack_pairs(Ptr3 lo, Ptr3 hi, uint32_t stride, uint32_t wb, uint64_t n, uint64_t* out,
+                               unsigned long long* bad) {
+  const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 3 * n) return;
+  const int i = (int)(e / n);
+  const uint64_t k = e - (uint64_t)i * n;
+  out[e] = le_word(lo.p[i] + k * stride, wb);
+  if (bad && le_word(hi.p[i] + k * stride, wb) != le_word(lo.p[(i + 1) % 3] + k * stride, wb)) atomicAdd(bad, 1ull);
+}
+
 }  // namespace
 }  // namespace gt
 
@@ -228,6 +251,24 @@ using namespace gt;
 extern "C" {
 
 int gt_abi_version(void) { return GT_ABI_VERSION; }
+
+int gt_unpack_pairs(const void* const* lo, const void* const* hi, uint32_t stride_bytes, uint32_t word_bytes,
+                    uint64_t n, uint64_t* out, unsigned long long* mismatches, void* stream) {
+  if (!lo || !hi || !out) return fail_inval("gt_unpack_pairs: NULL operand");
+  if (word_bytes != 1 && word_bytes != 4 && word_bytes != 8) return fail_inval("word_bytes must be 1, 4 or 8");
+  if (stride_bytes < word_bytes) return fail_inval("stride shorter than a word");
+  if (n == 0) return GT_OK;
+  Ptr3 l, h;
+  for (int i = 0; i < 3; ++i) {
+    if (!lo[i] || !hi[i]) return fail_inval("gt_unpack_pairs: NULL component");
+    l.p[i] = (const uint8_t*)lo[i];
+    h.p[i] = (const uint8_t*)hi[i];
+  }
+  k_unpack_pairs<<<blocks_for(3 * n), TPB, 0, (cudaStream_t)stream>>>(l, h, stride_bytes, word_bytes, n, out,
+                                                                       mismatches);
+  GT_LAUNCH_CHECK("gt_unpack_pairs");
+  return GT_OK;
+}
 
 // Host staging of the three parties' replicated pairs (the drop-in's
 // rendezvous, rss.py:222-228 consistency): component i = party i+1's lo is

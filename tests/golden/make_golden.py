@@ -491,12 +491,75 @@ def make_cli():
         json.dump(out, fh, indent=1, sort_keys=True)
 
 
+def make_deal():
+    """The reference dealer's outputs for the on-disk row:
+    training/inference material needs for a few shapes (train.py:309-346,
+    infer.py:38-43), the reference CLI's deal directory for tests/golden/cli
+    data.csv (depth 3, seed 21) -- every file except the three material.bin,
+    which are recorded by sha256 and size (the repo regenerates them) -- and
+    the revealed tree the reference trains from that directory."""
+    import hashlib
+    import shutil
+    import tempfile
+    from pathlib import Path
+
+    from obtree import cli as ref_cli
+    from obtree.infer import inference_needs
+    from obtree.ring import Ring
+    from obtree.train import training_needs
+
+    cases = {"train_90x6_d3": (90, 6, TrainConfig(depth=3)),
+             "train_90x6_tee_d4": (90, 6, TrainConfig(depth=4, heuristic="tee")),
+             "train_267x23_d4": (267, 23, TrainConfig(depth=4)),
+             "train_1500x8_d5": (1500, 8, TrainConfig(depth=5)),
+             "train_4000x10_s64_t12_d4": (4000, 10, TrainConfig(depth=4, tau=12, score_ring=Ring(64))),
+             "train_300x5_feature_cap": (300, 5, TrainConfig(policy="feature_cap"))}
+    out = {"training": {}, "inference": {}}
+    for name, (n, d, cfg) in cases.items():
+        out["training"][name] = {"n": n, "d": d, "depth": cfg.depth, "tau": cfg.tau, "heuristic": cfg.heuristic,
+                                 "policy": cfg.policy, "score_width": cfg.score_ring.width,
+                                 "needs": [[list(k), v] for k, v in sorted(training_needs(n, d, cfg).items(),
+                                                                           key=lambda kv: repr(kv[0]))]}
+    for nq, depth, ncol in ((40, 3, 6), (10_000, 7, 14)):
+        out["inference"][f"{nq}x{ncol}_d{depth}"] = {
+            "n": nq, "depth": depth, "n_columns": ncol,
+            "needs": [[list(k), v] for k, v in sorted(inference_needs(nq, depth, ncol).items(),
+                                                      key=lambda kv: repr(kv[0]))]}
+    gdir = Path(OUT) / "deal_train"
+    if gdir.exists():
+        shutil.rmtree(gdir)
+    with tempfile.TemporaryDirectory() as t:
+        deal = Path(t) / "deal"
+        assert ref_cli.main(["deal", "--data", str(Path(OUT) / "cli" / "data.csv"), "--depth", "3", "--seed", "21",
+                             "--out", str(deal)]) == 0
+        mats = {}
+        for p in sorted(deal.rglob("*")):
+            if p.is_dir():
+                continue
+            rel = p.relative_to(deal)
+            if p.name == "material.bin":
+                raw = p.read_bytes()
+                mats[str(rel)] = {"sha256": hashlib.sha256(raw).hexdigest(), "bytes": len(raw)}
+            else:
+                (gdir / rel).parent.mkdir(parents=True, exist_ok=True)
+                shutil.copy(p, gdir / rel)
+        run = Path(t) / "train"
+        assert ref_cli.main(["train", "--deal-dir", str(deal), "--depth", "3", "--profile", "test", "--reveal",
+                             "--out", str(run)]) == 0
+        tree = json.loads((run / "tree.json").read_text())
+    out["deal_train"] = {"argv": "deal --data cli/data.csv --depth 3 --seed 21", "material": mats,
+                         "material_seed_label": "deal/material", "tree": tree}
+    with open(os.path.join(OUT, "deal.json"), "w") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+    print("deal", len(mats), "material files")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-c2", action="store_true")
     ap.add_argument("--only", default=None)
     a = ap.parse_args()
-    steps = {"policies": make_policies, "cli": make_cli, "variants": make_variants,
+    steps = {"policies": make_policies, "cli": make_cli, "variants": make_variants, "deal": make_deal,
              "tee": make_tee,
              "kats": make_kats, "trees": make_trees, "infer": make_infer,
              "transcripts": make_transcripts, "c2c3": make_c2c3}
