@@ -3,7 +3,7 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
 PKG := paper_2305_00645_b200
-SRCS := $(PKG)/csrc/gt_gadget_api.cu $(PKG)/csrc/gt_train.cu $(PKG)/csrc/gt_infer.cu
+SRCS := $(PKG)/csrc/gt_gadget_api.cu $(PKG)/csrc/gt_train.cu $(PKG)/csrc/gt_infer.cu $(PKG)/csrc/gt_party.cu
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/gtree_b200.h
 OBJS := $(SRCS:.cu=.o)
 LIB := $(PKG)/libgtree_b200.so

@@ -185,6 +185,29 @@ int gt_stage_pairs(const uint64_t* const* lo, const uint64_t* const* hi, uint64_
 int gt_unpack_pairs(const void* const* lo, const void* const* hi, uint32_t stride_bytes, uint32_t word_bytes,
                     uint64_t n, uint64_t* out, unsigned long long* mismatches, void* stream);
 
+/* ---- three-host deployment: party-local steps (transport.py:374-475) ----
+ * One party (1..3) holds one replicated pair per shared vector, pair arrays
+ * [2][L] = (lo, hi) = (c_{p-1}, c_p); the host exchanges the ring messages
+ * between these calls (party.py).  keys: the party's two pairwise keys in
+ * pair[p-1] (shared with next) and pair[(p+1)%3] (shared with prev); the
+ * other slots are ignored.  Material pairs come from the party's dealt bank. */
+int gt_party_eq_mask(int party, const uint64_t* idx, uint64_t nq, uint64_t m, uint64_t off, const uint64_t* r,
+                     uint64_t* out, void* stream);
+int gt_party_eq_planes(int party, const uint64_t* masked, const uint64_t* recv, const uint64_t* rbits, uint64_t L,
+                       uint64_t* planes, void* stream);
+int gt_party_and_half(int party, const uint64_t* planes, uint64_t L, int width, const gt_keys* keys, uint32_t op,
+                      uint32_t sub, uint64_t lane0, uint64_t* z, void* stream);
+int gt_party_pack(const uint64_t* src, uint64_t L, int bits, uint8_t* out, void* stream);
+int gt_party_unpack(const uint8_t* in, uint64_t L, int bits, uint64_t* dst, void* stream);
+int gt_party_b2a_mask(const uint64_t* h, const uint8_t* bb, uint64_t L, uint64_t* e, void* stream);
+int gt_party_b2a_finish(int party, const uint64_t* e, const uint64_t* recv, const uint64_t* a, uint64_t L,
+                        uint64_t* out, void* stream);
+int gt_party_select_mul(int party, const uint64_t* ca, const uint64_t* table, uint64_t table_len, int per_row,
+                        uint64_t nq, uint64_t m, const gt_keys* keys, uint32_t op, uint32_t sub, uint64_t lane0,
+                        uint64_t* z, void* stream);
+int gt_party_lane_sum(const uint64_t* pair, uint64_t nq, uint64_t m, uint64_t* out, void* stream);
+int gt_party_slot_step(int party, uint64_t* slot, const uint64_t* branch, uint64_t nq, void* stream);
+
 /* ---- secure inference (infer_batch, infer.py:20-35) ---- */
 
 /* tree [3][2^depth-1] heap-ordered payload shares, queries [3][n][nf];

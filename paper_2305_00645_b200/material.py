@@ -38,6 +38,10 @@ from .shares import RING64, Ring, ShareError
 
 MaterialKey = tuple  # ("edabit", w) | ("dabit", w) | ("trunc", w, k)
 
+
+class MaterialError(RuntimeError):
+    """A bank ran out of a material kind (gadgets.py MaterialError)."""
+
 # ---------------------------------------------------------------------------
 # material needs
 # ---------------------------------------------------------------------------
