@@ -57,9 +57,10 @@ def main():
         ks = ("prods", "partition", "count_lanes", "count_contract", "node_hc", "node_finish")
         print(f"[{tag}] C2 {ms:.4f} ms tree_ok={ok} |", " ".join(f"{k}={getattr(p, 'ms_' + k) * 1e3:.1f}us"
                                                               for k in ks), flush=True)
-    elif what == "c2eager":  # launch lists: eager tree runs (ncu --graph-profiling graph)
+    elif what == "c2eager":  # launch lists: three eager tree runs (GT_PROBE_ENGINE selects the count engine)
         data, X, Y = bench._c2_inputs()
-        tr = DeviceTrainer(bench.N_C2, bench.NF_C2, TrainConfig(depth=bench.DEPTH_C2))
+        tr = DeviceTrainer(bench.N_C2, bench.NF_C2, TrainConfig(depth=bench.DEPTH_C2,
+                                                                count_engine=os.environ.get("GT_PROBE_ENGINE", "tensor")))
         X, Y, F = t(X), t(Y), t(fill)
         for _ in range(3):
             tr.run(X, Y, F, keys)
@@ -88,6 +89,11 @@ def main():
         F = t(np.zeros((1 << depth) - 1, dtype=np.uint64))
         tr = DeviceTrainer(n, nf, TrainConfig(depth=depth, count_engine=os.environ.get("GT_PROBE_ENGINE", "tensor")))
         print(f"[{tag}] C4 {timed(tr.capture(X, Y, F, keys), 10):.3f} ms", flush=True)
+        p = _native.gt_train_profile()
+        tr.run(X, Y, F, keys, profile=p)
+        torch.cuda.synchronize()
+        ks = ("prods", "partition", "count_lanes", "count_contract", "node_hc", "node_finish")
+        print(" ".join(f"{k}={getattr(p, 'ms_' + k):.2f}ms" for k in ks), flush=True)
     elif what == "walk":
         rng = np.random.default_rng(1)
         for depth, nf, n in ((7, 13, 10_000), (10, 32, 2_000_000)):
