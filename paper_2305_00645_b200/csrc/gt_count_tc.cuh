@@ -761,6 +761,8 @@ struct FusedArgs {
   int n_h, W, nkr, NBn, stages;
   int mode3;     // three UMMAs per step (shallow tiles, tcf_mode3)
   int ts_level;  // diagnostics (GT_COUNT_TS): phase timestamps of cluster 0 into g_cnt_ts[8 level ..], -1 off
+  int xpre;      // the x planes are complete before this launch's predecessor ran (levels >= 1): the copy
+                 // thread fills the first x stages before the PDL wait
 };
 
 __device__ unsigned long long g_cnt_ts[128];
@@ -783,9 +785,9 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAITC_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(MBAR_SUSPEND_NS)
       : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_local(uint64_t* bar) {
@@ -873,6 +875,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 2), 1) k_
       const int n = nt * 16 + ni, wg = (int)rank * 16 + w;
       if (cell < cells && n < a.n_h && wg < a.W) apre[k] = a.alpha_tab[((uint64_t)n * 3 + c) * a.W + wg];
     }
+  }
+  // the x planes of column block `rank`, stage t (one bulk copy; re-read by
+  // every level: kept in L2 with evict_last)
+  auto x_copy = [&](int t, uint64_t pol) {
+    const int xs = t % XS;
+    const uint64_t kb = a.kb_lo + kb0 + (uint32_t)(t >> 1), h = t & 1;
+    mbar_expect_tx(&xfull[xs], (uint32_t)TCF_XB);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(smt + xs * TCF_XB)),
+        "l"(a.B8 + (((uint64_t)rank * a.nkb_total + kb) * 2 + h) * (uint64_t)TCF_XB), "r"((uint32_t)TCF_XB),
+        "r"(smem_u32(&xfull[xs])), "l"(pol)
+        : "memory");
+  };
+  // levels >= 1: the prologue that wrote the x planes finished before the
+  // partition launch passed its own wait (and only then triggered this
+  // launch), so the first XS stages stream in while the partition drains
+  const int xpre = (a.xpre && T > 0) ? min(XS, T) : 0;
+  if (tid == 32 * TCF_PW && xpre) {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    for (int t = 0; t < xpre; ++t) x_copy(t, pol);
   }
   cnt_ts(a, 0, tid == 0);
   pdl_wait();  // m_idx, is_leaf, the zeroed sums (partition) and the x planes (prologue)
@@ -1001,17 +1025,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 2), 1) k_
     // the x planes are re-read by every level: kept in L2 (evict_last)
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    for (int t = 0; t < T; ++t) {
+    for (int t = xpre; t < T; ++t) {
       const int xs = t % XS;
       if (t >= XS) mbar_wait(&xempty[xs], (uint32_t)(((t / XS) - 1) & 1));
-      const uint64_t kb = a.kb_lo + kb0 + (uint32_t)(t >> 1), h = t & 1;
-      mbar_expect_tx(&xfull[xs], (uint32_t)TCF_XB);
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-              smem_u32(smt + xs * TCF_XB)),
-          "l"(a.B8 + (((uint64_t)rank * a.nkb_total + kb) * 2 + h) * (uint64_t)TCF_XB), "r"((uint32_t)TCF_XB),
-          "r"(smem_u32(&xfull[xs])), "l"(pol)
-          : "memory");
+      x_copy(t, pol);
     }
   } else if (warp == TCF_PW + 1 && lane == 0 && T > 0) {
     // MMA thread (leader) / relay (peer): the leader issues the pair's UMMAs

@@ -296,13 +296,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// The suspend-time hint lets the hardware park a waiting warp until the phase
+// completes (or the hint expires) instead of re-issuing the probe: the
+// count's single-thread copy / MMA warps otherwise spin on their barriers in
+// the producers' issue slots.
+constexpr uint32_t MBAR_SUSPEND_NS = 0x989680;
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(MBAR_SUSPEND_NS)
       : "memory");
 }
 
@@ -1850,12 +1855,13 @@ int launch_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint6
     const int tab_smem = 3 * m * 8 <= 24 * 1024;
     const size_t smem = tab_smem ? (size_t)3 * m * sizeof(uint64_t) : 0;
     const uint32_t oo = op_id(level, SITE_PART_OAA), orow = op_id(level, SITE_PART_ROW);
-    int rc = split == 1 ? launch_chain(k_partition_split<1>, dim3(grid), dim3(PS_TPB), smem, s, nullptr, X, midx, T,
-                                       slots, m, nf, N, base, K, oo, orow, aux, tab_smem)
-           : split == 2 ? launch_chain(k_partition_split<2>, dim3(grid), dim3(PS_TPB), smem, s, nullptr, X, midx, T,
-                                       slots, m, nf, N, base, K, oo, orow, aux, tab_smem)
-                        : launch_chain(k_partition_split<4>, dim3(grid), dim3(PS_TPB), smem, s, nullptr, X, midx, T,
-                                       slots, m, nf, N, base, K, oo, orow, aux, tab_smem);
+    const dim3 blk(PS_TPB);
+    int rc = split == 1 ? launch_chain(k_partition_split<1>, dim3(grid), blk, smem, s, nullptr, X, midx, T, slots, m,
+                                       nf, N, base, K, oo, orow, aux, tab_smem)
+           : split == 2 ? launch_chain(k_partition_split<2>, dim3(grid), blk, smem, s, nullptr, X, midx, T, slots, m,
+                                       nf, N, base, K, oo, orow, aux, tab_smem)
+                        : launch_chain(k_partition_split<4>, dim3(grid), blk, smem, s, nullptr, X, midx, T, slots, m,
+                                       nf, N, base, K, oo, orow, aux, tab_smem);
     if (rc) return rc;
     GT_LAUNCH_CHECK("k_partition_split");
     return GT_OK;
@@ -2181,6 +2187,10 @@ int launch_count_fused(const CountLaunch& c, const uint8_t* B8, int alpha, uint6
   {
     static const bool ts = getenv("GT_COUNT_TS") != nullptr;
     fa.ts_level = ts ? c.level : -1;
+  }
+  {
+    static const bool no_xpre = getenv("GT_FUSED_NO_XPRE") != nullptr;  // A/B experiments
+    fa.xpre = c.level > 0 && !no_xpre;
   }
   const int smem = tcf_smem(NBn, fa.mode3);
   cudaLaunchAttribute at[1];

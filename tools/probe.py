@@ -5,6 +5,8 @@
   python tools/probe.py c2eager three eager C2 trees (launch lists)
   python tools/probe.py cts     fused count phase timestamps per level (GT_COUNT_TS=1)
   python tools/probe.py c4      C4 tree (10^6 x 32, depth 8) graph replay median ms
+  python tools/probe.py tl      one eager C2 tree's level timeline: count + heuristic phase
+                                timestamps on one clock (GT_COUNT_TS=1 GT_HC_TIMING=1)
 Launch switches (GT_PART_G, GT_WALK_G, ...) come from the environment;
 GT_PROBE_ENGINE=cuda runs the count contraction on the CUDA cores (A/B).
 """
@@ -81,6 +83,28 @@ def main():
         for lv in range(bench.DEPTH_C2):
             ts = buf[8 * lv: 8 * lv + 7]
             print(f"level {lv}: " + " ".join(f"{n}=+{(ts[k + 1] - ts[0]) / 1e3:.1f}" for k, n in enumerate(names)) + " us")
+    elif what == "tl":  # timeline: count (cluster 0) + heuristic (node 0) phases, us from the level-0 count start
+        import ctypes
+        data, X, Y = bench._c2_inputs()
+        tr = DeviceTrainer(bench.N_C2, bench.NF_C2, TrainConfig(depth=bench.DEPTH_C2))
+        X, Y, F = t(X), t(Y), t(fill)
+        for _ in range(3):
+            tr.run(X, Y, F, keys)
+        torch.cuda.synchronize()
+        cb, hb = (ctypes.c_ulonglong * 64)(), (ctypes.c_ulonglong * 128)()
+        lib = _native.load()
+        _native.check(lib.gt_diag_count_timestamps(cb, 64))
+        _native.check(lib.gt_diag_hc_timestamps(hb, 128))
+        t0 = cb[0]
+        us = lambda v: f"{(v - t0) / 1e3:7.1f}" if v else "     - "  # noqa: E731
+        cn = ["c.start", "c.wait", "c.item0", "c.items", "c.mma", "c.done", "c.epi"]
+        pn = ["ctl.start", "ctl.tapes", "ctl.end", "ft.start", "ft.tape", "ft.end", "div.start", "div.end"]
+        qn = ["post.scores", "post.argmin", "post.budget", "post.split", "post.end", "p5", "p6", "ladder"]
+        for lv in range(bench.DEPTH_C2):
+            print(f"level {lv}")
+            print("   " + " ".join(f"{n}={us(cb[8 * lv + k])}" for k, n in enumerate(cn)))
+            print("   " + " ".join(f"{n}={us(hb[64 + 8 * lv + k])}" for k, n in enumerate(pn)))
+            print("   " + " ".join(f"{n}={us(hb[8 * lv + k])}" for k, n in enumerate(qn)))
     elif what == "c4":
         n, nf, depth = 10 ** 6, 32, 8
         rng = np.random.default_rng(3)
