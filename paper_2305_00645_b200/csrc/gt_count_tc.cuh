@@ -1081,39 +1081,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 2), 1) k_
   cnt_ts(a, 5, tid == 0);
   pdl_trigger();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  uint64_t* red = reinterpret_cast<uint64_t*>(smt);  // [3][NNt nodes][16 w][8 q] (the stages are idle now)
+  // [slot][3][NNt nodes][16 w][8 q] (the stages are idle now); mode3 cells get
+  // two contributions (regions c and c+1), kept in separate slots
+  uint64_t* red = reinterpret_cast<uint64_t*>(smt);
+  const int RSLOT = 3 * NNt * 16 * 8;
   if (T > 0) {
-    if (warp < 4) {
-      // TMEM lane r = warp 32 + lane = (column w, limb q) of this CTA's block;
-      // accumulator columns j = node index x 8 + p (node index over the pair)
-      const int r = warp * 32 + lane, w = r >> 3, q = r & 7;
-      if (mode3)  // two contributions per cell: zero this thread's cells first
-        for (int e = 0; e < 3 * NNt; ++e) red[(e * 16 + w) * 8 + q] = 0;
-      for (int c = 0; c < 3; ++c)
-        for (int j0 = 0; j0 < (mode3 ? 2 * NU : NU); j0 += 16) {
-          uint32_t d[16];
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-              "%14, %15}, [%16];"
-              : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
-                "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
-              : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * (mode3 ? 2 * NU : NU) + j0)));
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    // TMEM lane r = 32 (warp % 4) + lane = (column w, limb q) of this CTA's
+    // block; accumulator columns j = node index x 8 + p (node index over the
+    // pair).  Every warp takes the 16-column chunks warp / 4, + nq, ... of its
+    // lane quarter (nq warps per quarter) and issues them two per
+    // tcgen05.wait::ld.
+    const int quarter = warp & 3, r = quarter * 32 + lane, w = r >> 3, q = r & 7;
+    const int ccols = mode3 ? 2 * NU : NU, per_c = ccols / 16, chunks = 3 * per_c;
+    constexpr int nq = TCF_THREADS / 128;
+    auto fold = [&](const uint32_t(&d)[16], int ch) {
+      const int c = ch / per_c, j0 = (ch % per_c) * 16;
 #pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            uint64_t v = 0;
+      for (int k = 0; k < 2; ++k) {
+        uint64_t v = 0;
 #pragma unroll
-            for (int p = 0; p < 8; ++p) v += (uint64_t)d[8 * k + p] << (8 * p);
-            const int col = j0 + 8 * k;
-            if (mode3) {  // region c columns: [D_c(CTA 0 nodes) | D_{c-1}(0) | D_c(CTA 1 nodes) | D_{c-1}(1)]
-              const int blk = col / (8 * NBn), ni = (blk >= 2 ? NBn : 0) + (col % (8 * NBn)) / 8;
-              const int comp = (blk & 1) ? (c + 2) % 3 : c;
-              red[((comp * NNt + ni) * 16 + w) * 8 + q] += v << (8 * q);
-            } else {
-              red[((c * NNt + col / 8) * 16 + w) * 8 + q] = v << (8 * q);
-            }
-          }
+        for (int p = 0; p < 8; ++p) v += (uint64_t)d[8 * k + p] << (8 * p);
+        const int col = j0 + 8 * k;
+        if (mode3) {  // region c columns: [D_c(CTA 0 nodes) | D_{c-1}(0) | D_c(CTA 1 nodes) | D_{c-1}(1)]
+          const int blk = col / (8 * NBn), ni = (blk >= 2 ? NBn : 0) + (col % (8 * NBn)) / 8;
+          const int comp = (blk & 1) ? (c + 2) % 3 : c;
+          red[(blk & 1) * RSLOT + ((comp * NNt + ni) * 16 + w) * 8 + q] = v << (8 * q);
+        } else {
+          red[((c * NNt + col / 8) * 16 + w) * 8 + q] = v << (8 * q);
         }
+      }
+    };
+    auto tld = [&](uint32_t(&d)[16], int ch) {
+      const int c = ch / per_c, j0 = (ch % per_c) * 16;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+          "%14, %15}, [%16];"
+          : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
+            "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
+          : "r"(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(c * ccols + j0)));
+    };
+    for (int ch = warp >> 2; ch < chunks; ch += 2 * nq) {  // warp-uniform trip count
+      uint32_t d0[16], d1[16];
+      const bool two = ch + nq < chunks;
+      tld(d0, ch);
+      if (two) tld(d1, ch + nq);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      fold(d0, ch);
+      if (two) fold(d1, ch + nq);
     }
     __syncthreads();
     const uint64_t Sstride = (uint64_t)a.n_h * (a.W + 1);
@@ -1124,12 +1138,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 2), 1) k_
       const int w = cell & 15, cn = cell >> 4, ni = cn % NNt, c = cn / NNt;
       const int n = nt * 16 + ni, wg = (int)rank * 16 + w;
       if (n >= a.n_h || wg >= a.W) continue;
-      const uint4* rp = reinterpret_cast<const uint4*>(red + (uint64_t)cell * 8);
       uint64_t v = 0;
+      for (int sl = 0; sl < (mode3 ? 2 : 1); ++sl) {
+        const uint4* rp = reinterpret_cast<const uint4*>(red + sl * RSLOT + (uint64_t)cell * 8);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint4 x = rp[i];
-        v += ((uint64_t)x.y << 32 | x.x) + ((uint64_t)x.w << 32 | x.z);
+        for (int i = 0; i < 4; ++i) {
+          const uint4 x = rp[i];
+          v += ((uint64_t)x.y << 32 | x.x) + ((uint64_t)x.w << 32 | x.z);
+        }
       }
       if (a.alpha && kr == 0 && a.alpha_tab) {
         v += apre[k];

@@ -33,18 +33,17 @@ __device__ __forceinline__ A3 lookup_word(const Keys& K, uint32_t op, uint64_t g
   return r;
 }
 
-// Entry pair q (entries 2q, 2q+1) of one lookup: eq lanes vs the public
-// ramp, b2a of the hits, select against zero (oaa.py:26-34) -- the picked
-// shares of this pair, local cross terms only.
-template <int L, typename Entry>
-__device__ __forceinline__ A3 lookup_pair(const Keys& K, uint32_t op, uint64_t gidx, const A3& idx, int m, int q,
-                                          Entry entry) {
+// Entry pair q (entries 2q, 2q+1) of one lookup, data-independent of the
+// table: eq lanes vs the public ramp and b2a of the hits (oaa.py:26-32) --
+// the arithmetic shares ca0, ca1 of the two hit bits (ca1 = 0 past m).
+template <int L>
+__device__ __forceinline__ void lookup_pair_ca(const Keys& K, uint32_t op, uint64_t gidx, const A3& idx, int m, int q,
+                                               A3* ca0, A3* ca1) {
   const int mh = (m + 1) >> 1;
   W2 Z[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) Z[i] = word2(K.pair[i], op, 0, 0, gidx * (uint64_t)mh + (uint64_t)q);
-  const uint64_t F0[3] = {0, 0, 0};
-  A3 acc = a3(0, 0, 0);
+  *ca1 = a3(0, 0, 0);
   if (L == 64) {  // both entries' eq trees packed together (eq_arith64_x2)
     const int j0 = 2 * q, j1 = 2 * q + 1;
     const uint64_t lane0 = gidx * (uint64_t)m + (uint64_t)j0;
@@ -53,10 +52,9 @@ __device__ __forceinline__ A3 lookup_pair(const Keys& K, uint32_t op, uint64_t g
     const uint64_t Z0[3] = {Z[0].a, Z[1].a, Z[2].a}, Z1[3] = {Z[0].b, Z[1].b, Z[2].b};
     B3 h0, h1;
     eq_arith64_x2(d0, R0.r, R0.Rb0, R0.Rb1, Z0, d1, R1.r, R1.Rb0, R1.Rb1, Z1, &h0, &h1);
-    // select_share(zero, rows, hit): w2 - w1 = rows (oaa.py:33); local cross terms
-    acc = mul_z<L>(entry(j0), b2a_arith<L>(h0, R0.A0, R0.A1, R0.bits), F0);
-    if (j1 < m) acc = add<L>(acc, mul_z<L>(entry(j1), b2a_arith<L>(h1, R1.A0, R1.A1, R1.bits), F0));
-    return acc;
+    *ca0 = b2a_arith<L>(h0, R0.A0, R0.A1, R0.bits);
+    if (j1 < m) *ca1 = b2a_arith<L>(h1, R1.A0, R1.A1, R1.bits);
+    return;
   }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -67,9 +65,21 @@ __device__ __forceinline__ A3 lookup_pair(const Keys& K, uint32_t op, uint64_t g
     const DealerRand R = dealer_rand(K, op, lane);
     const uint64_t Zw[3] = {h ? Z[0].b : Z[0].a, h ? Z[1].b : Z[1].a, h ? Z[2].b : Z[2].a};
     const B3 hit = eq_arith<L>(d, R.r, R.Rb0, R.Rb1, Zw);
-    const A3 ca = b2a_arith<L>(hit, R.A0, R.A1, R.bits);
-    acc = add<L>(acc, mul_z<L>(entry(j), ca, F0));
+    *(h ? ca1 : ca0) = b2a_arith<L>(hit, R.A0, R.A1, R.bits);
   }
+}
+
+// Entry pair q of one lookup: the hits' shares select the entries against
+// zero (select_share(zero, rows, hit): w2 - w1 = rows, oaa.py:33) -- the
+// picked shares of this pair, local cross terms only.
+template <int L, typename Entry>
+__device__ __forceinline__ A3 lookup_pair(const Keys& K, uint32_t op, uint64_t gidx, const A3& idx, int m, int q,
+                                          Entry entry) {
+  const uint64_t F0[3] = {0, 0, 0};
+  A3 ca0, ca1;
+  lookup_pair_ca<L>(K, op, gidx, idx, m, q, &ca0, &ca1);
+  A3 acc = mul_z<L>(entry(2 * q), ca0, F0);
+  if (2 * q + 1 < m) acc = add<L>(acc, mul_z<L>(entry(2 * q + 1), ca1, F0));
   return acc;
 }
 

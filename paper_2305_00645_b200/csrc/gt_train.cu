@@ -142,6 +142,29 @@ __global__ void k_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T
   if (valid && t == 0) st3s(midx, N, s, add_pub<64>(add<64>(mul_pub<64>(idx, 2), dval), 1));
 }
 
+// Early oaa lanes of the NEXT level's partition (train.py:135-137): the
+// eq / b2a lanes of oaa(payloads_{h-1}, m_idx - (m - 1)) depend only on the
+// node index the previous partition produced, not on the payload table the
+// heuristic is still choosing, so they run beside the heuristic chain on a
+// side stream; the partition then only selects the table entries with them
+// (Σ_j ca_j T_j).  One thread per (sample, entry pair); ca[c][j][s] written
+// for consecutive samples.  Same lanes and randomness as lookup_pair, so the
+// partition's shares are unchanged.
+__global__ void __launch_bounds__(128) k_oaa_early(const uint64_t* midx, uint64_t* ca, uint64_t N, int m,
+                                                   uint64_t base, Keys K, uint32_t op_oaa) {
+  const int mh = (m + 1) >> 1;
+  const uint64_t total = N * (uint64_t)mh, cs = (uint64_t)m * N;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(t / N);
+    const uint64_t s = t - (uint64_t)q * N;
+    const A3 local = add_pub<64>(ld3s(midx, N, s), 0ull - (uint64_t)(m - 1));
+    A3 c0, c1;
+    lookup_pair_ca<64>(K, op_oaa, base + s, local, m, q, &c0, &c1);
+    st3s(ca, cs, (uint64_t)(2 * q) * N + s, c0);
+    if (2 * q + 1 < m) st3s(ca, cs, (uint64_t)(2 * q + 1) * N + s, c1);
+  }
+}
+
 // Split partition: B threads per sample, placed in DIFFERENT warps (thread t
 // of the 256-thread CTA serves sample t % S of the CTA's S = 256 / B samples
 // as member r = t / S), so every lane of a warp runs the same entry pair q
@@ -154,7 +177,8 @@ constexpr int PS_TPB = 256;
 template <int B>
 __global__ void __launch_bounds__(PS_TPB, 3)
     k_partition_split(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint64_t slots, int m, int nf, uint64_t N,
-                      uint64_t base, Keys K, uint32_t op_oaa, uint32_t op_row, PartAux aux, int tab_smem) {
+                      uint64_t base, Keys K, uint32_t op_oaa, uint32_t op_row, PartAux aux, int tab_smem,
+                      const uint64_t* __restrict__ ca) {
   constexpr int S = PS_TPB / B;
   __shared__ uint64_t part[B][3][S];  // members' partial sums
   __shared__ uint64_t feat[3][S];     // the sample's fetched feature index (shares)
@@ -185,7 +209,13 @@ __global__ void __launch_bounds__(PS_TPB, 3)
   A3 idx = a3(0, 0, 0), acc = a3(0, 0, 0);
   if (valid) {  // oaa on the level-(h-1) payloads at local = m_idx - (m - 1)   (train.py:135-137)
     idx = ld3s(midx, N, s);
-    acc = lookup_partial<64>(K, op_oaa, g, add_pub<64>(idx, 0ull - (uint64_t)(m - 1)), m, r, B, entryT);
+    if (ca) {  // hit shares drawn early (k_oaa_early): the telescope words + the entries' selects
+      for (int e = r; e < 6; e += B) acc = add<64>(acc, lookup_word<64>(K, op_oaa, g, m, e));
+      const uint64_t F0[3] = {0, 0, 0}, cs = (uint64_t)m * N;
+      for (int j = r; j < m; j += B) acc = add<64>(acc, mul_z<64>(entryT(j), ld3s(ca, cs, (uint64_t)j * N + s), F0));
+    } else {
+      acc = lookup_partial<64>(K, op_oaa, g, add_pub<64>(idx, 0ull - (uint64_t)(m - 1)), m, r, B, entryT);
+    }
   }
   if (B > 1) {
 #pragma unroll
@@ -1683,8 +1713,16 @@ inline uint64_t div_tape_level_off(int level, int nf, int TB) {  // W2 offset of
 
 bool count_fused_ok(int nf);
 
+// Early oaa lanes (k_oaa_early) for the split partition's sample counts, when
+// the largest level's hit shares [3][2^(depth-2)][N] fit 256 MB.
+bool early_oaa_ok(const gt_train_cfg& c) {
+  static const bool off = getenv("GT_NO_EARLY_OAA") != nullptr;  // A/B experiments
+  const uint64_t N = c.n_local;
+  return !off && c.depth >= 3 && N > 0 && N <= (1ull << 17) && 24ull * (1ull << (c.depth - 2)) * N <= (256ull << 20);
+}
+
 struct Layout {
-  uint64_t xin, yin, fin, tout, fout, cols, la, cols8, leaf, midx, divtape, divtable, posttape, posttable, nodetape, nodetable, feattape, alphatab, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, total;  // word offsets
+  uint64_t xin, yin, fin, tout, fout, cols, la, cols8, leaf, midx, divtape, divtable, posttape, posttable, nodetape, nodetable, feattape, alphatab, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, oaa, total;  // word offsets
 };
 
 Layout layout(const gt_train_cfg& c, bool host_io = false) {
@@ -1735,6 +1773,7 @@ Layout layout(const gt_train_cfg& c, bool host_io = false) {
   L.co = take(3 * nmax * 3 * cols);
   L.lab = take(3 * nmax);
   L.stop = take(4);
+  L.oaa = take(early_oaa_ok(c) ? 3ull * (nmax / 2) * N : 0);
   // device staging of the host-input entry (gt_train_host)
   const uint64_t slots = (1ull << c.depth) - 1;
   L.xin = take(host_io ? 3 * N * nf : 0);
@@ -1842,13 +1881,15 @@ int launch_partition_g(const uint64_t* X, uint64_t* midx, const uint64_t* T, uin
 // whenever N allows: no group shuffles, no divergent trip counts; measured
 // 181 vs 204 us per C2 tree against G = 2).
 int launch_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint64_t slots, int m, int nf, uint64_t N,
-                     uint64_t base, const Keys& K, int level, cudaStream_t s, int num_sms, const PartAux& aux) {
+                     uint64_t base, const Keys& K, int level, cudaStream_t s, int num_sms, const PartAux& aux,
+                     const uint64_t* ca = nullptr) {
   // A/B: GT_PART_SPLIT=B (1, 2, 4) forces the split kernel, 0 the group kernel.
   // Default (measured, C2 / C4): the split kernel with B = 2 while the level
   // has fewer than ~700 samples per SM (C2: 0.657 vs 0.669 ms per tree), the
   // one-thread-per-sample group kernel above that (C4: 20.95 vs 21.28 ms).
   static const int forced_split = getenv("GT_PART_SPLIT") ? atoi(getenv("GT_PART_SPLIT")) : -1;
-  const int split = forced_split >= 0 ? forced_split : (N <= (uint64_t)num_sms * 700 ? 2 : 0);
+  int split = forced_split >= 0 ? forced_split : (N <= (uint64_t)num_sms * 700 ? 2 : 0);
+  if (ca && split != 1 && split != 2 && split != 4) split = 2;  // early oaa lanes: the split kernel reads them
   if ((split == 1 || split == 2 || split == 4) && N) {
     const int S = PS_TPB / split;
     const unsigned grid = (unsigned)((N + S - 1) / S);
@@ -1857,11 +1898,11 @@ int launch_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint6
     const uint32_t oo = op_id(level, SITE_PART_OAA), orow = op_id(level, SITE_PART_ROW);
     const dim3 blk(PS_TPB);
     int rc = split == 1 ? launch_chain(k_partition_split<1>, dim3(grid), blk, smem, s, nullptr, X, midx, T, slots, m,
-                                       nf, N, base, K, oo, orow, aux, tab_smem)
+                                       nf, N, base, K, oo, orow, aux, tab_smem, ca)
            : split == 2 ? launch_chain(k_partition_split<2>, dim3(grid), blk, smem, s, nullptr, X, midx, T, slots, m,
-                                       nf, N, base, K, oo, orow, aux, tab_smem)
+                                       nf, N, base, K, oo, orow, aux, tab_smem, ca)
                         : launch_chain(k_partition_split<4>, dim3(grid), blk, smem, s, nullptr, X, midx, T, slots, m,
-                                       nf, N, base, K, oo, orow, aux, tab_smem);
+                                       nf, N, base, K, oo, orow, aux, tab_smem, ca);
     if (rc) return rc;
     GT_LAUNCH_CHECK("k_partition_split");
     return GT_OK;
@@ -2104,7 +2145,9 @@ bool l2_window_attr(const void* base, uint64_t bytes, cudaLaunchAttribute* at) {
 struct Side {
   cudaStream_t st = nullptr;  // compute side stream (high priority)
   cudaStream_t cp = nullptr;  // host <-> device copies of the host-input entry
+  cudaStream_t lo = nullptr;  // early oaa lanes beside the heuristic chain (low priority)
   cudaEvent_t ev[16] = {};
+  cudaEvent_t eo[2] = {};     // early oaa fork / join
 };
 // One Side per device, shared by every trainer on that device: train_impl
 // holds the device's side lock for its whole host-side enqueue, so calls
@@ -2125,7 +2168,9 @@ int side_of(int dev, Side** out) {
     GT_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     GT_CUDA_CHECK(cudaStreamCreateWithPriority(&sd.st, cudaStreamNonBlocking, hi));
     GT_CUDA_CHECK(cudaStreamCreateWithFlags(&sd.cp, cudaStreamNonBlocking));
+    GT_CUDA_CHECK(cudaStreamCreateWithPriority(&sd.lo, cudaStreamNonBlocking, lo));
     for (auto& e : sd.ev) GT_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : sd.eo) GT_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   *out = &sd;
   return GT_OK;
@@ -2666,13 +2711,23 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
     P.stop(Prof::PRODS);
   }
   int32_t trained = c.depth;
+  const bool early_oaa = early_oaa_ok(c);
+  bool oaa_forked = false;  // an early oaa launch on side->lo not yet joined
+  bool oaa_ready = false;   // the next partition's hit shares are (being) drawn
   for (int level = 0; level < c.depth; ++level) {
     const int n_h = 1 << level;
     const uint64_t swords = 3ull * n_h * (W + 1);
     if (level > 0 && N) {  // the partition also zeroes this level's count sums
+      const uint64_t* ca = nullptr;
+      if (oaa_ready) {
+        ca = ws + L.oaa;
+        if (oaa_forked) GT_CUDA_CHECK(cudaStreamWaitEvent(s, side->eo[1], 0));
+        oaa_forked = oaa_ready = false;
+      }
       P.start();
       PartAux aux{S, swords, c.count_engine == 0 ? ws + L.leaf : nullptr, f[cur], n_h, op_id(level, SITE_ISLEAF)};
-      int rc = launch_partition(features, midx, T, slots, n_h / 2, c.nf, N, c.sample_base, K, level, s, num_sms, aux);
+      int rc = launch_partition(features, midx, T, slots, n_h / 2, c.nf, N, c.sample_base, K, level, s, num_sms, aux,
+                                ca);
       if (rc) return rc;
       P.stop(Prof::PARTITION);
     }
@@ -2689,6 +2744,36 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
                                                        c.sample_base, c.sample_base + N);
       GT_LAUNCH_CHECK("k_count_alpha");
       P.count_launch();
+    }
+    static const int oaa_max = getenv("GT_OAA_MAXLEVEL") ? atoi(getenv("GT_OAA_MAXLEVEL")) : 99;  // A/B
+    static const int oaa_ctas = getenv("GT_OAA_CTAS") ? atoi(getenv("GT_OAA_CTAS")) : 0;          // A/B
+    const bool early_next = early_oaa && level >= 1 && level + 1 < c.depth && level + 1 <= oaa_max && N;
+    if (early_next) {
+      // the next partition's oaa lanes (hit shares of m_idx vs its 2^level
+      // entries) beside this level's heuristic chain
+      cudaStream_t os = s;
+      if (!prof && !no_side) {
+        int rc = stream_after(side->lo, s, side->eo[0]);
+        if (rc) return rc;
+        os = side->lo;
+      }
+      const int m = 1 << level;
+      const uint64_t thr = N * (uint64_t)(m / 2);
+      // a bounded footprint (4 CTAs of 128 per SM, grid-stride): the lanes
+      // fill the issue slots the latency-bound heuristic leaves idle without
+      // crowding its warps (C2: 0.607 ms vs 0.614 with one CTA per 128
+      // (sample, pair) items and 0.617 without early lanes)
+      uint64_t grid = std::min<uint64_t>((thr + 127) / 128, 4ull * num_sms);
+      if (oaa_ctas > 0) grid = std::min<uint64_t>((thr + 127) / 128, (uint64_t)oaa_ctas);
+      k_oaa_early<<<(unsigned)grid, 128, 0, os>>>(midx, ws + L.oaa, N, m, c.sample_base, K,
+                                                  op_id(level + 1, SITE_PART_OAA));
+      GT_LAUNCH_CHECK("k_oaa_early");
+      P.count_launch();
+      if (os != s) {
+        GT_CUDA_CHECK(cudaEventRecord(side->eo[1], side->lo));
+        oaa_forked = true;
+      }
+      oaa_ready = true;
     }
     if (allreduce) {
       int rc = allreduce(S, swords, stream, allreduce_user);
@@ -2809,6 +2894,7 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
       break;
     }
   }
+  if (oaa_forked) GT_CUDA_CHECK(cudaStreamWaitEvent(s, side->eo[1], 0));  // a grow stop left one unjoined
   if (hin) {
     GT_CUDA_CHECK(cudaMemcpyAsync(hin->T, T, 3 * slots * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     GT_CUDA_CHECK(cudaMemcpyAsync(hin->F, F, 3 * slots * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
