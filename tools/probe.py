@@ -97,7 +97,7 @@ def main():
         _native.check(lib.gt_diag_hc_timestamps(hb, 128))
         t0 = cb[0]
         us = lambda v: f"{(v - t0) / 1e3:7.1f}" if v else "     - "  # noqa: E731
-        cn = ["c.start", "c.wait", "c.item0", "c.items", "c.mma", "c.done", "c.epi"]
+        cn = ["c.start", "c.wait", "c.item0", "c.items", "c.mma", "c.done", "c.epi", "c.last"]
         pn = ["ctl.start", "ctl.tapes", "ctl.end", "ft.start", "ft.tape", "ft.end", "div.start", "div.end"]
         qn = ["post.scores", "post.argmin", "post.budget", "post.split", "post.end", "p5", "p6", "ladder"]
         for lv in range(bench.DEPTH_C2):
