@@ -766,11 +766,23 @@ struct FusedArgs {
 };
 
 __device__ unsigned long long g_cnt_ts[128];
+__device__ unsigned int g_cnt_done[16];
 __device__ __forceinline__ void cnt_ts(const FusedArgs& a, int slot, bool on) {
   if (a.ts_level < 0 || !on || blockIdx.y != 0 || blockIdx.z != 0 || blockIdx.x != 0) return;
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   g_cnt_ts[8 * a.ts_level + slot] = t;
+}
+// slot 7: the end of the level's LAST CTA (the grid's completion)
+__device__ __forceinline__ void cnt_ts_last(const FusedArgs& a) {
+  if (a.ts_level < 0 || threadIdx.x != 0) return;
+  const unsigned int total = gridDim.x * gridDim.y * gridDim.z;
+  if (atomicAdd(&g_cnt_done[a.ts_level], 1u) == total - 1) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_cnt_ts[8 * a.ts_level + 7] = t;
+    g_cnt_done[a.ts_level] = 0;
+  }
 }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -1164,6 +1176,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 2), 1) k_
     }
   }
   cnt_ts(a, 6, tid == 0);
+  cnt_ts_last(a);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync_all();  // both CTAs are past their TMEM reads before the pair's columns are freed
   if (warp == 0) {
