@@ -173,6 +173,7 @@ int gt_train_host(const gt_train_cfg* cfg, const uint64_t* features_h, const uin
  * share handling, rss.py:222-228 consistency): lo[i] / hi[i] are party i+1's
  * share pair (n words each); component i = lo[i] is written to out + i*n
  * (pinned staging of gt_train_host); check != 0 requires hi[i] == lo[(i+1)%3].
+ * out == NULL: the check alone (the drop-in runs it while the device trains).
  * Host threads; no device work.  GT_ERR_INVALID on an inconsistent pair. */
 int gt_stage_pairs(const uint64_t* const* lo, const uint64_t* const* hi, uint64_t n, uint64_t* out, int check);
 

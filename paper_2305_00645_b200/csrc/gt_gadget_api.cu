@@ -276,7 +276,7 @@ int gt_unpack_pairs(const void* const* lo, const void* const* hi, uint32_t strid
 // Split over host threads in 1 MB slices (memcmp + memcpy stream at memory
 // speed); returns GT_ERR_INVALID on an inconsistent pair.
 int gt_stage_pairs(const uint64_t* const* lo, const uint64_t* const* hi, uint64_t n, uint64_t* out, int check) {
-  if (!lo || !hi || !out) return fail_inval("gt_stage_pairs: NULL operand");
+  if (!lo || !hi || (!out && !check)) return fail_inval("gt_stage_pairs: NULL operand");
   for (int i = 0; i < 3; ++i)
     if (n && (!lo[i] || !hi[i])) return fail_inval("gt_stage_pairs: NULL component");
   const uint64_t slice = 1ull << 17;  // words
@@ -288,7 +288,7 @@ int gt_stage_pairs(const uint64_t* const* lo, const uint64_t* const* hi, uint64_
       const int i = (int)(k / nsl);
       const uint64_t a = (k % nsl) * slice, len = std::min<uint64_t>(slice, n - a);
       if (check && std::memcmp(hi[i] + a, lo[(i + 1) % 3] + a, len * 8) != 0) bad = 1;
-      std::memcpy(out + (uint64_t)i * n + a, lo[i] + a, len * 8);
+      if (out) std::memcpy(out + (uint64_t)i * n + a, lo[i] + a, len * 8);
     }
   };
   const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));

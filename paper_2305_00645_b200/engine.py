@@ -14,6 +14,7 @@ run's transcript is the analytic ledger of exactly that protocol
 
 from __future__ import annotations
 
+import queue
 import threading
 import time
 from typing import Callable, List, Optional, Sequence, Union
@@ -143,6 +144,56 @@ class LocalRun:
         return self._metrics
 
 
+class _PartyPool:
+    """Three persistent party threads (party1..party3) that run_local hands
+    its bodies to: starting three fresh threads per call costs ~0.5 ms of
+    thread start-up on the host path of every tree.  A call that times out
+    leaves its stuck threads behind and retires the pool (the next call
+    starts a new one)."""
+
+    def __init__(self):
+        self.tasks = [queue.SimpleQueue() for _ in PARTIES]
+        self.broken = False
+        for i in range(3):
+            threading.Thread(target=self._worker, args=(i,), name=f"party{i + 1}", daemon=True).start()
+
+    def _worker(self, i: int) -> None:
+        while True:
+            job, done = self.tasks[i].get()
+            try:
+                job()
+            finally:
+                done.release()
+
+    def run(self, jobs: Sequence[Callable[[], None]], timeout: float) -> bool:
+        """Run the three jobs on the party threads; False if they did not all
+        finish within `timeout` seconds."""
+        done = threading.Semaphore(0)
+        for i, job in enumerate(jobs):
+            self.tasks[i].put((job, done))
+        deadline = time.monotonic() + timeout
+        for _ in jobs:
+            if not done.acquire(timeout=max(0.0, deadline - time.monotonic())):
+                self.broken = True
+                return False
+        return True
+
+
+_POOL: Optional[_PartyPool] = None
+_POOL_LOCK = threading.Lock()
+
+
+def _party_pool() -> Optional[_PartyPool]:
+    """The process's party threads, or None when a run_local call is already
+    using them (a nested or concurrent call gets fresh threads)."""
+    global _POOL
+    if not _POOL_LOCK.acquire(blocking=False):
+        return None
+    if _POOL is None or _POOL.broken:
+        _POOL = _PartyPool()
+    return _POOL
+
+
 def run_local(fn: Callable[[PartyEngine], object], *, seeds: Union[SeedSetup, int], materials: Optional[Sequence] = None,
               enclave_handler=None, lane_limit: int = REF_LANE_LIMIT, timeout: float = 300.0,
               dealer_seed: Optional[bytes] = None, device=None) -> LocalRun:
@@ -168,14 +219,24 @@ def run_local(fn: Callable[[PartyEngine], object], *, seeds: Union[SeedSetup, in
             errors[idx] = e
             bridge.abort()
 
-    threads = [threading.Thread(target=body, args=(i,), name=f"party{i + 1}", daemon=True) for i in range(3)]
-    for t in threads:
-        t.start()
-    for t in threads:
-        t.join(timeout=timeout * 4)
-        if t.is_alive():
+    pool = _party_pool()
+    if pool is not None:
+        try:
+            finished = pool.run([lambda i=i: body(i) for i in range(3)], timeout * 4)
+        finally:
+            _POOL_LOCK.release()
+        if not finished:
             bridge.abort()
             raise TransportError("party thread failed to finish")
+    else:
+        threads = [threading.Thread(target=body, args=(i,), name=f"party{i + 1}", daemon=True) for i in range(3)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join(timeout=timeout * 4)
+            if t.is_alive():
+                bridge.abort()
+                raise TransportError("party thread failed to finish")
     for e in errors:
         if e is not None and not isinstance(e, TransportError):
             raise e

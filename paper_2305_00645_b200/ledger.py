@@ -302,7 +302,10 @@ class Ledger:
             Ledger._MEMO[key] = (recs, self.round_no - r0, ret)
             return ret
         recs, nrounds, ret = hit
-        self.transcript.records.extend((r + r0, s, t, n, tag) for r, s, t, n, tag in recs)
+        if r0 == 0:  # a fresh ledger (one run_local call): the cached records as they are
+            self.transcript.records.extend(recs)
+        else:
+            self.transcript.records.extend((r + r0, s, t, n, tag) for r, s, t, n, tag in recs)
         self.round_no = r0 + nrounds
         return ret
 

@@ -12,7 +12,7 @@ like ``reconstruct_pairs`` (rss.py:222-228).
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import List, Sequence, Tuple
+from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -120,19 +120,23 @@ def components_from_pairs(pairs: Sequence[Tuple[np.ndarray, np.ndarray]], ring: 
     return np.stack([ring.reduce(x) for x in los])
 
 
-def stage_pairs(pairs: Sequence[Tuple[np.ndarray, np.ndarray]], out: np.ndarray, check: bool = True) -> None:
+def stage_pairs(pairs: Sequence[Tuple[np.ndarray, np.ndarray]], out: Optional[np.ndarray], check: bool = True,
+                shape: Optional[Tuple[int, ...]] = None) -> None:
     """components_from_pairs written straight into `out` [3, ...] uint64 (the
     pinned staging buffer of a host-operand device call): party i's lo is
     component i; the replication check compares party i's hi with party
-    i+1's lo without temporaries beyond one reusable bool buffer."""
+    i+1's lo without temporaries beyond one reusable bool buffer.  out=None
+    runs the check alone (on `shape`)."""
     if len(pairs) != 3:
         raise ShareError("need the share pairs of exactly three parties")
     los = [np.asarray(p[0], dtype=np.uint64) for p in pairs]
     his = [np.asarray(p[1], dtype=np.uint64) for p in pairs]
-    shape = out.shape[1:]
+    shape = out.shape[1:] if out is not None else tuple(shape if shape is not None else los[0].shape)
     if any(x.shape != shape for x in los + his):
         raise ShareError("share components disagree on shape")
-    if all(x.flags.c_contiguous for x in los + his) and out.flags.c_contiguous:
+    if out is None and not check:
+        return
+    if all(x.flags.c_contiguous for x in los + his) and (out is None or out.flags.c_contiguous):
         import ctypes
 
         from . import _native
@@ -140,7 +144,8 @@ def stage_pairs(pairs: Sequence[Tuple[np.ndarray, np.ndarray]], out: np.ndarray,
         lib = _native.load()
         arr = ctypes.c_void_p * 3
         rc = lib.gt_stage_pairs(arr(*[x.ctypes.data for x in los]), arr(*[x.ctypes.data for x in his]),
-                                int(np.prod(shape, dtype=np.int64)), out.ctypes.data, 1 if check else 0)
+                                int(np.prod(shape, dtype=np.int64)), None if out is None else out.ctypes.data,
+                                1 if check else 0)
         if rc:
             raise ShareError(lib.gt_last_error().decode())
         return
@@ -150,7 +155,8 @@ def stage_pairs(pairs: Sequence[Tuple[np.ndarray, np.ndarray]], out: np.ndarray,
             np.equal(his[i], los[(i + 1) % 3], out=eq)
             if not eq.all():
                 raise ShareError("replication inconsistency between party pairs")
-        np.copyto(out[i], los[i])
+        if out is not None:
+            np.copyto(out[i], los[i])
 
 
 def components_from_avecs(vecs: Sequence, check: bool = True) -> np.ndarray:

@@ -10,6 +10,7 @@ per-level count allreduce of a sample-sharded run.
 
 from __future__ import annotations
 
+import collections
 import ctypes
 import threading
 from collections import OrderedDict
@@ -229,6 +230,24 @@ class DeviceTrainer:
         self._graph_host_refs = (Xh, Yh, filler_h, T_h, F_h, keys, allreduce)
         return g.replay
 
+    def host_graph(self, keys):
+        """Replay of a captured whole host-operand run on this trainer's pinned
+        staging buffers for these keys (the drop-in path: the graph is
+        captured on a key set's first use, then replayed), or None where the
+        run cannot be captured (grow, tee).  A few key sets are kept."""
+        if self.cfg.policy == "grow" or self.cfg.heuristic == "tee" or not getattr(self, "staging", None):
+            return None
+        graphs = self.__dict__.setdefault("_host_graphs", collections.OrderedDict())
+        kb = bytes(keys)
+        g = graphs.pop(kb, None)
+        if g is None:
+            st = self.staging
+            while len(graphs) >= 4:
+                graphs.popitem(last=False)
+            g = self.capture_host(st["X"], st["Y"], st["fill"], st["T"], st["F"], keys)
+        graphs[kb] = g
+        return g
+
     def capture(self, X, Y, filler, keys, allreduce=None):
         """Capture one whole training run (every level's kernels, and the
         per-level count allreduce of a sharded run when `allreduce` enqueues
@@ -301,12 +320,25 @@ def train_pairs(x_pairs: Sequence, y_pairs: Sequence, cfg: TrainConfig, seeds: S
     with _TRAIN_LOCK:
         tr = _cached_trainer(n, nf, cfg, device, True)
         st = tr.staging
-        stage_pairs(x_pairs, st["X"].numpy().view(np.uint64), check)
-        stage_pairs(y_pairs, st["Y"].numpy().view(np.uint64), check)
+        stage_pairs(x_pairs, st["X"].numpy().view(np.uint64), False)
+        stage_pairs(y_pairs, st["Y"].numpy().view(np.uint64), False)
         st["fill"].numpy().view(np.uint64)[:] = filler_values(seeds.filler_seed, (1 << tr.depth) - 1, nf + 1)
         s = torch.cuda.current_stream(tr.device)
-        depth = tr.run_host(st["X"], st["Y"], st["fill"], st["T"], st["F"], keys, stream=s)
-        s.synchronize()
+        replay = tr.host_graph(keys)
+        if replay is not None:  # one graph launch instead of ~370 eager launches per tree
+            with torch.cuda.device(tr.device):
+                replay()
+            depth = tr.depth
+        else:
+            depth = tr.run_host(st["X"], st["Y"], st["fill"], st["T"], st["F"], keys, stream=s)
+        # the replication check (rss.py:222-228) runs on host threads while the
+        # device trains; an inconsistent pair still raises, after the run
+        try:
+            if check:
+                stage_pairs(x_pairs, None, True)
+                stage_pairs(y_pairs, None, True)
+        finally:
+            s.synchronize()
         slots = (1 << depth) - 1
         return (st["T"].numpy().view(np.uint64)[:, :slots].copy(),
                 st["F"].numpy().view(np.uint64)[:, :slots].copy(), depth)

@@ -257,6 +257,38 @@ def test_dropin_run_local_c2_twice_equals_reference_tree():
         assert np.array_equal(sum(r.F.lo for r in run.results), z["F"])
 
 
+def test_dropin_inconsistent_pair_raises_after_the_device_run():
+    """The drop-in's replication check (rss.py:222-228) runs on host threads
+    while the device trains: a party whose hi disagrees with its neighbour's
+    lo still gets ShareError, and the next call (same cached trainer) trains
+    the reference tree."""
+    from paper_2305_00645_b200 import TrainConfig, run_local, train_tree
+    from paper_2305_00645_b200.seeds import SeedSetup, derive_seed
+    from paper_2305_00645_b200.shares import AVec, RING64, ShareError
+
+    z, meta = golden_npz("trees_mpc.npz")
+    k = next(i for i, m in enumerate(meta) if m["name"] == "spect_d4")
+    data, seed = z[f"data{k}"], bytes.fromhex(meta[k]["seed"])
+    setup = SeedSetup.from_master(derive_seed(seed, "run"))
+    rng = np.random.default_rng(81)
+    X, Y = share(data[:, :-1], rng), share(data[:, -1], rng)
+    for bad in (True, False):
+        def body(eng):
+            p = eng.party
+            hx = X[p % 3].copy()
+            if bad and p == 2:
+                hx[5, 1] ^= np.uint64(1)
+            return train_tree(eng, AVec(RING64, X[p - 1], hx), AVec(RING64, Y[p - 1], Y[p % 3]),
+                              TrainConfig(depth=meta[k]["depth"]))
+
+        if bad:
+            with pytest.raises(ShareError, match="replication"):
+                run_local(body, seeds=setup, dealer_seed=derive_seed(seed, "deal"))
+        else:
+            run = run_local(body, seeds=setup, dealer_seed=derive_seed(seed, "deal"))
+            assert np.array_equal(sum(r.T.lo for r in run.results), z[f"T{k}"])
+
+
 def test_tee_heuristic_bit_identical_to_plaintext_trainer():
     # reference acceptance criterion 4 (test_acceptance.py:180-193): the trusted
     # path equals plaintext_train exactly; golden oT/oF are the reference's own

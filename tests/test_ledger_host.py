@@ -127,6 +127,44 @@ def test_native_host_staging_of_party_pairs():
         stage_pairs(bad, out)
     stage_pairs(bad, out, check=False)  # unchecked staging copies the lo components
     assert np.array_equal(out, comp)
+    stage_pairs(pairs, None)  # the check alone (what the drop-in runs while the device trains)
+    with pytest.raises(ShareError):
+        stage_pairs(bad, None)
+
+
+def test_run_local_party_threads_reused_errors_propagate():
+    """run_local runs the three bodies on persistent party threads: results
+    come back per party, a body's exception reaches the caller (the others
+    see the broken rendezvous, as rss.py:518-541), the threads are reused by
+    the next call, and a nested run_local gets fresh threads."""
+    import threading
+
+    from paper_2305_00645_b200 import engine
+
+    names = []
+
+    def ok(eng):
+        names.append(threading.current_thread().name)
+        return eng.party * 10
+
+    run = engine.run_local(ok, seeds=5)
+    assert run.results == [10, 20, 30] and sorted(names) == ["party1", "party2", "party3"]
+    idents = {t.ident for t in threading.enumerate() if t.name.startswith("party")}
+
+    def boom(eng):
+        if eng.party == 2:
+            raise ValueError("party 2 failed")
+        return eng._bridge.call(eng.party, "x", None, lambda p: [0, 0, 0])
+
+    with pytest.raises(ValueError, match="party 2 failed"):
+        engine.run_local(boom, seeds=5)
+    assert engine.run_local(ok, seeds=5).results == [10, 20, 30]
+    assert idents <= {t.ident for t in threading.enumerate()}
+
+    def nested(eng):
+        return engine.run_local(ok, seeds=6).results[eng.party - 1]
+
+    assert engine.run_local(nested, seeds=5).results == [10, 20, 30]
 
 
 def test_division_params_match_reference():

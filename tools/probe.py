@@ -5,6 +5,7 @@
   python tools/probe.py c2eager three eager C2 trees (launch lists)
   python tools/probe.py cts     fused count phase timestamps per level (GT_COUNT_TS=1)
   python tools/probe.py c4      C4 tree (10^6 x 32, depth 8) graph replay median ms
+  python tools/probe.py api     C2 through run_local + train_tree: wall-clock split of the drop-in host path
   python tools/probe.py tl      one eager C2 tree's level timeline: count + heuristic phase
                                 timestamps on one clock (GT_COUNT_TS=1 GT_HC_TIMING=1)
 Launch switches (GT_PART_G, GT_WALK_G, ...) come from the environment;
@@ -105,6 +106,60 @@ def main():
             print("   " + " ".join(f"{n}={us(cb[8 * lv + k])}" for k, n in enumerate(cn)))
             print("   " + " ".join(f"{n}={us(hb[64 + 8 * lv + k])}" for k, n in enumerate(pn)))
             print("   " + " ".join(f"{n}={us(hb[8 * lv + k])}" for k, n in enumerate(qn)))
+    elif what == "api":  # drop-in host path breakdown (ms, medians of 10)
+        import time
+        import statistics
+        from paper_2305_00645_b200 import engine
+        from paper_2305_00645_b200.seeds import SeedSetup, derive_seed, filler_values, make_keys
+        from paper_2305_00645_b200.shares import RING64, AVec, stage_pairs, avecs_from_components
+        from paper_2305_00645_b200.train import _cached_trainer, as_config
+        data, Xc, Yc = bench._c2_inputs()
+        Xh = [np.ascontiguousarray(Xc[i]) for i in range(3)]
+        Xh2 = [x.copy() for x in Xh]  # separate hi arrays, as a real caller's pairs
+        Yh = [np.ascontiguousarray(Yc[i]) for i in range(3)]
+        Yh2 = [y.copy() for y in Yh]
+        setup = SeedSetup.from_master(derive_seed(bench.SEED_C2, "run"))
+        dseed = derive_seed(bench.SEED_C2, "deal")
+        cfg = TrainConfig(depth=bench.DEPTH_C2)
+        xp = [(Xh[i], Xh2[(i + 1) % 3]) for i in range(3)]
+        yp = [(Yh[i], Yh2[(i + 1) % 3]) for i in range(3)]
+        tr = _cached_trainer(bench.N_C2, bench.NF_C2, as_config(cfg), None, True)
+        st = tr.staging
+        res = {}
+        def tm(name, f, n=10):
+            ts = []
+            for _ in range(n):
+                a = time.perf_counter(); f(); ts.append(time.perf_counter() - a)
+            res[name] = statistics.median(ts) * 1e3
+        tm("make_keys", lambda: make_keys(setup, dseed))
+        tm("filler", lambda: filler_values(setup.filler_seed, 127, 14))
+        tm("stage_X", lambda: stage_pairs(xp, st["X"].numpy().view(np.uint64), True))
+        tm("stage_X_nocheck", lambda: stage_pairs(xp, st["X"].numpy().view(np.uint64), False))
+        tm("stage_Y", lambda: stage_pairs(yp, st["Y"].numpy().view(np.uint64), True))
+        keys = make_keys(setup, dseed)
+        s = torch.cuda.current_stream()
+        def run():
+            tr.run_host(st["X"], st["Y"], st["fill"], st["T"], st["F"], keys, stream=s); s.synchronize()
+        tm("run_host", run)
+        def body(eng):
+            p = eng.party
+            return engine.train_tree(eng, AVec(RING64, Xh[p - 1], Xh2[p % 3]), AVec(RING64, Yh[p - 1], Yh2[p % 3]), cfg)
+        from paper_2305_00645_b200.train import train_pairs
+        tm("train_pairs_direct", lambda: train_pairs(xp, yp, cfg, setup, dseed))
+        tm("run_local_total", lambda: engine.run_local(body, seeds=setup, dealer_seed=dseed))
+        tm("threads_only", lambda: engine.run_local(lambda eng: None, seeds=setup, dealer_seed=dseed))
+        print(" ".join(f"{k}={v:.3f}" for k, v in res.items()), flush=True)
+        if os.environ.get("GT_PROBE_PROFILE"):
+            import cProfile
+            import pstats
+            import threading
+            threading.setprofile(None)
+            pr = cProfile.Profile()
+            for _ in range(10):
+                pr.enable()
+                engine.run_local(body, seeds=setup, dealer_seed=dseed)
+                pr.disable()
+            pstats.Stats(pr).sort_stats("tottime").print_stats(15)
     elif what == "c4":
         n, nf, depth = 10 ** 6, 32, 8
         rng = np.random.default_rng(3)
