@@ -12,9 +12,8 @@
  *   - `width` is the ring width l in {8, 32, 64}; values are stored masked;
  *   - `stream` is a cudaStream_t (NULL = legacy default stream); calls are
  *     asynchronous on it, re-entrant per stream, and do not allocate: the
- *     caller owns all memory (workspace sizes are queried up front); the one
- *     exception is gt_argmin, which takes stream-ordered scratch
- *     (cudaMallocAsync) for its per-row tournament;
+ *     caller owns all memory (workspace / scratch sizes are queried up
+ *     front: gt_train_workspace_bytes, gt_argmin_scratch_words, ...);
  *   - return GT_OK, GT_EINVAL (bad arguments -> the reference's
  *     ValueError/UsageError) or GT_ECUDA (launch/runtime failure -> the
  *     reference's protocol errors, CLI exit code 2, cli.py:53-56);
@@ -78,9 +77,12 @@ int gt_truncate(int width, const uint64_t* x, uint64_t* out, uint64_t n, int k, 
 int gt_division(int width, const uint64_t* p, const uint64_t* q, uint64_t* out, uint64_t n, int tau,
                 const gt_keys* keys, uint32_t op, void* stream);
 /* argmin_masked, gadgets.py:366-401: scores [3][n][m] (width), avail [3][n][m]
- * bits, out [3][n] index shares in Z_2^64. */
+ * bits, out [3][n] index shares in Z_2^64; scratch: device memory of
+ * gt_argmin_scratch_words(n, m) words (the per-row tournament's values and
+ * indices), owned by the caller. */
+uint64_t gt_argmin_scratch_words(uint64_t n, uint64_t m);
 int gt_argmin(int width, const uint64_t* scores, const uint8_t* avail, uint64_t* out, uint64_t n, uint64_t m,
-              uint64_t worst, const gt_keys* keys, uint32_t op, void* stream);
+              uint64_t worst, const gt_keys* keys, uint32_t op, uint64_t* scratch, void* stream);
 /* oaa, oaa.py:20-35: out[i] = table[idx[i]] (0 when out of range). */
 int gt_oaa(int width, const uint64_t* table, uint64_t m, const uint64_t* idx, uint64_t* out, uint64_t n,
            const gt_keys* keys, uint32_t op, void* stream);

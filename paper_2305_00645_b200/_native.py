@@ -79,8 +79,9 @@ _SIGS = {
                                    ctypes.c_uint32, ctypes.c_void_p]),
     "gt_division": (ctypes.c_int, [ctypes.c_int, _u64p, _u64p, _u64p, ctypes.c_uint64, ctypes.c_int,
                                    ctypes.POINTER(gt_keys), ctypes.c_uint32, ctypes.c_void_p]),
+    "gt_argmin_scratch_words": (ctypes.c_uint64, [ctypes.c_uint64, ctypes.c_uint64]),
     "gt_argmin": (ctypes.c_int, [ctypes.c_int, _u64p, _u64p, _u64p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
-                                 ctypes.POINTER(gt_keys), ctypes.c_uint32, ctypes.c_void_p]),
+                                 ctypes.POINTER(gt_keys), ctypes.c_uint32, _u64p, ctypes.c_void_p]),
     "gt_oaa": (ctypes.c_int, [ctypes.c_int, _u64p, ctypes.c_uint64, _u64p, _u64p, ctypes.c_uint64,
                               ctypes.POINTER(gt_keys), ctypes.c_uint32, ctypes.c_void_p]),
     "gt_row_lookup": (ctypes.c_int, [ctypes.c_int, _u64p, ctypes.c_uint64, _u64p, _u64p, ctypes.c_uint64,

@@ -390,19 +390,16 @@ int gt_division(int width, const uint64_t* p, const uint64_t* q, uint64_t* out, 
   return GT_OK;
 }
 
+uint64_t gt_argmin_scratch_words(uint64_t n, uint64_t m) { return n * 6 * m; }
+
 int gt_argmin(int width, const uint64_t* scores, const uint8_t* avail, uint64_t* out, uint64_t n, uint64_t m,
-              uint64_t worst, const gt_keys* keys, uint32_t op, void* stream) {
+              uint64_t worst, const gt_keys* keys, uint32_t op, uint64_t* scratch, void* stream) {
   GT_CHECK_COMMON(width, keys);
   if (m == 0 || m > ARGMIN_MAX) return fail_inval("argmin: need 1 <= m <= 128 columns");
   if (n == 0) return GT_OK;
-  if (!scores || !avail || !out) return fail_inval("gt_argmin: NULL operand");
-  uint64_t* scratch = nullptr;
-  cudaStream_t s = (cudaStream_t)stream;
-  GT_CUDA_CHECK(cudaMallocAsync((void**)&scratch, n * 6 * m * sizeof(uint64_t), s));
+  if (!scores || !avail || !out || !scratch) return fail_inval("gt_argmin: NULL operand");
   GT_DISPATCH(width, k_argmin, blocks_for(n), scores, avail, out, n, m, worst, to_keys(keys), op, scratch);
-  cudaError_t e = cudaGetLastError();
-  cudaFreeAsync(scratch, s);
-  if (e != cudaSuccess) return fail_cuda(e, "gt_argmin");
+  GT_LAUNCH_CHECK("gt_argmin");
   return GT_OK;
 }
 

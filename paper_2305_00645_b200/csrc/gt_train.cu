@@ -2499,11 +2499,12 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
   uint64_t* ws = (uint64_t*)workspace;
   Side* side = nullptr;
   // A/B switches: GT_NO_SIDE keeps the division tapes on the main stream;
-  // GT_COUNT_OVERLAP=1 pipelines count chunks across the two streams (measured
-  // slower on C2: the lane kernel fills every SM's registers, so the
-  // contraction CTAs rarely co-reside, and the extra chunks cost more)
+  // the lanes8 + contraction count (shapes the fused count does not take,
+  // e.g. C4's 65 sample columns) pipelines its chunks across the two streams,
+  // the contraction of chunk k beside the lanes of chunk k+1 (C4: 20.2 vs
+  // 20.9 ms per tree); GT_NO_COUNT_OVERLAP=1 runs them in one stream
   static const bool no_side = getenv("GT_NO_SIDE") != nullptr;
-  static const bool count_overlap = getenv("GT_COUNT_OVERLAP") != nullptr;
+  static const bool count_overlap = getenv("GT_NO_COUNT_OVERLAP") == nullptr;
   if (dev < 0 || dev >= 64) return fail_inval("device index out of range");
   std::lock_guard<std::recursive_mutex> side_guard(side_lock(dev));
   {

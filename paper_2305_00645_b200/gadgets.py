@@ -100,8 +100,10 @@ def argmin_masked(width, scores, avail, worst, *, keys, op, stream=None):
         raise ValueError("scores and mask must be matching 2-d arrays")
     n, m = int(scores.shape[1]), int(scores.shape[2])
     out = torch.empty((3, n), dtype=torch.int64, device=scores.device)
-    _native.check(_native.load().gt_argmin(width, ptr(scores), ptr(avail), ptr(out), n, m, int(worst),
-                                           ctypes.byref(keys), op, _stream(scores, stream)))
+    lib = _native.load()
+    scratch = torch.empty(int(lib.gt_argmin_scratch_words(n, m)), dtype=torch.int64, device=scores.device)
+    _native.check(lib.gt_argmin(width, ptr(scores), ptr(avail), ptr(out), n, m, int(worst), ctypes.byref(keys), op,
+                                ptr(scratch), _stream(scores, stream)))
     return out
 
 
