@@ -150,18 +150,32 @@ __global__ void k_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T
 // (Σ_j ca_j T_j).  One thread per (sample, entry pair); ca[c][j][s] written
 // for consecutive samples.  Same lanes and randomness as lookup_pair, so the
 // partition's shares are unchanged.
+// Work is fetched dynamically (a warp takes OAA_CHUNK x 32 items per atomic
+// on *ctr): CTAs resident beside the count start early, the ones that only
+// find room after it take the rest.
+constexpr int OAA_CHUNK = 4;
 __global__ void __launch_bounds__(128) k_oaa_early(const uint64_t* midx, uint64_t* ca, uint64_t N, int m,
-                                                   uint64_t base, Keys K, uint32_t op_oaa) {
-  const int mh = (m + 1) >> 1;
+                                                   uint64_t base, Keys K, uint32_t op_oaa,
+                                                   unsigned long long* ctr) {
+  const int mh = (m + 1) >> 1, lane = threadIdx.x & 31;
   const uint64_t total = N * (uint64_t)mh, cs = (uint64_t)m * N;
-  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
-    const int q = (int)(t / N);
-    const uint64_t s = t - (uint64_t)q * N;
-    const A3 local = add_pub<64>(ld3s(midx, N, s), 0ull - (uint64_t)(m - 1));
-    A3 c0, c1;
-    lookup_pair_ca<64>(K, op_oaa, base + s, local, m, q, &c0, &c1);
-    st3s(ca, cs, (uint64_t)(2 * q) * N + s, c0);
-    if (2 * q + 1 < m) st3s(ca, cs, (uint64_t)(2 * q + 1) * N + s, c1);
+  for (;;) {
+    unsigned long long t0 = 0;
+    if (lane == 0) t0 = atomicAdd(ctr, 32ull * OAA_CHUNK);
+    t0 = __shfl_sync(0xffffffffu, t0, 0);
+    if (t0 >= total) break;
+#pragma unroll 1
+    for (int k = 0; k < OAA_CHUNK; ++k) {
+      const uint64_t t = t0 + (uint64_t)k * 32 + lane;  // consecutive samples across the warp
+      if (t >= total) break;
+      const int q = (int)(t / N);
+      const uint64_t s = t - (uint64_t)q * N;
+      const A3 local = add_pub<64>(ld3s(midx, N, s), 0ull - (uint64_t)(m - 1));
+      A3 c0, c1;
+      lookup_pair_ca<64>(K, op_oaa, base + s, local, m, q, &c0, &c1);
+      st3s(ca, cs, (uint64_t)(2 * q) * N + s, c0);
+      if (2 * q + 1 < m) st3s(ca, cs, (uint64_t)(2 * q + 1) * N + s, c1);
+    }
   }
 }
 
@@ -1722,7 +1736,7 @@ bool early_oaa_ok(const gt_train_cfg& c) {
 }
 
 struct Layout {
-  uint64_t xin, yin, fin, tout, fout, cols, la, cols8, leaf, midx, divtape, divtable, posttape, posttable, nodetape, nodetable, feattape, alphatab, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, oaa, total;  // word offsets
+  uint64_t xin, yin, fin, tout, fout, cols, la, cols8, leaf, midx, divtape, divtable, posttape, posttable, nodetape, nodetable, feattape, alphatab, S, f[2], gam[2], cst[2], ceff[2], hc, dv, co, lab, stop, oaa, oaactr, total;  // word offsets
 };
 
 Layout layout(const gt_train_cfg& c, bool host_io = false) {
@@ -1774,6 +1788,7 @@ Layout layout(const gt_train_cfg& c, bool host_io = false) {
   L.lab = take(3 * nmax);
   L.stop = take(4);
   L.oaa = take(early_oaa_ok(c) ? 3ull * (nmax / 2) * N : 0);
+  L.oaactr = take(early_oaa_ok(c) ? 16 : 0);
   // device staging of the host-input entry (gt_train_host)
   const uint64_t slots = (1ull << c.depth) - 1;
   L.xin = take(host_io ? 3 * N * nf : 0);
@@ -2715,6 +2730,44 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
   const bool early_oaa = early_oaa_ok(c);
   bool oaa_forked = false;  // an early oaa launch on side->lo not yet joined
   bool oaa_ready = false;   // the next partition's hit shares are (being) drawn
+  // the next partition's oaa lanes (hit shares of m_idx vs its 2^level
+  // entries), forked on the low-priority stream right after this level's
+  // partition: small CTAs (two warps) fit beside the count's CTAs and take
+  // idle issue slots there, more start beside the heuristic chain (at most
+  // 16 warps per SM); work is fetched dynamically (k_oaa_early).  Measured
+  // on one box, C2: 0.603 ms vs 0.615 launched after the count with 128-thread
+  // CTAs, 0.648 at 4 warps per SM; 32 / 96-thread CTAs 0.608 / 0.607
+  static const int oaa_max = getenv("GT_OAA_MAXLEVEL") ? atoi(getenv("GT_OAA_MAXLEVEL")) : 99;  // A/B
+  static const int oaa_ctas = getenv("GT_OAA_CTAS") ? atoi(getenv("GT_OAA_CTAS")) : 0;          // A/B
+  static const bool early_after_count = getenv("GT_OAA_AFTER_COUNT") != nullptr;              // A/B
+  static const int oaa_tpb = getenv("GT_OAA_TPB") ? atoi(getenv("GT_OAA_TPB")) : 64;            // A/B
+  if (early_oaa) GT_CUDA_CHECK(cudaMemsetAsync(ws + L.oaactr, 0, 16 * sizeof(uint64_t), s));
+  auto early_oaa_launch = [&](int level) -> int {
+    const bool early_next = early_oaa && level >= 1 && level + 1 < c.depth && level + 1 <= oaa_max && N;
+    if (!early_next) return GT_OK;
+    cudaStream_t os = s;
+    if (!prof && !no_side) {
+      int rc = stream_after(side->lo, s, side->eo[0]);
+      if (rc) return rc;
+      os = side->lo;
+    }
+    const int m = 1 << level;
+    const uint64_t thr = N * (uint64_t)(m / 2);
+    const uint64_t per_cta = (uint64_t)oaa_tpb * OAA_CHUNK;
+    uint64_t grid = std::min<uint64_t>((thr + per_cta - 1) / per_cta, (uint64_t)(16 * 32 / oaa_tpb) * num_sms);
+    if (oaa_ctas > 0) grid = std::min<uint64_t>(grid, (uint64_t)oaa_ctas);
+    k_oaa_early<<<(unsigned)grid, oaa_tpb, 0, os>>>(midx, ws + L.oaa, N, m, c.sample_base, K,
+                                                   op_id(level + 1, SITE_PART_OAA),
+                                                   reinterpret_cast<unsigned long long*>(ws + L.oaactr) + level);
+    GT_LAUNCH_CHECK("k_oaa_early");
+    P.count_launch();
+    if (os != s) {
+      GT_CUDA_CHECK(cudaEventRecord(side->eo[1], side->lo));
+      oaa_forked = true;
+    }
+    oaa_ready = true;
+    return GT_OK;
+  };
   for (int level = 0; level < c.depth; ++level) {
     const int n_h = 1 << level;
     const uint64_t swords = 3ull * n_h * (W + 1);
@@ -2731,6 +2784,10 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
                                 ca);
       if (rc) return rc;
       P.stop(Prof::PARTITION);
+      if (!early_after_count) {
+        int rc2 = early_oaa_launch(level);
+        if (rc2) return rc2;
+      }
     }
     if (!(level == 0 && count0_done)) {  // level 0 may already be counted chunk by chunk (host operands)
       if (!(level > 0 && N)) GT_CUDA_CHECK(cudaMemsetAsync(S, 0, swords * sizeof(uint64_t), s));
@@ -2746,35 +2803,9 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
       GT_LAUNCH_CHECK("k_count_alpha");
       P.count_launch();
     }
-    static const int oaa_max = getenv("GT_OAA_MAXLEVEL") ? atoi(getenv("GT_OAA_MAXLEVEL")) : 99;  // A/B
-    static const int oaa_ctas = getenv("GT_OAA_CTAS") ? atoi(getenv("GT_OAA_CTAS")) : 0;          // A/B
-    const bool early_next = early_oaa && level >= 1 && level + 1 < c.depth && level + 1 <= oaa_max && N;
-    if (early_next) {
-      // the next partition's oaa lanes (hit shares of m_idx vs its 2^level
-      // entries) beside this level's heuristic chain
-      cudaStream_t os = s;
-      if (!prof && !no_side) {
-        int rc = stream_after(side->lo, s, side->eo[0]);
-        if (rc) return rc;
-        os = side->lo;
-      }
-      const int m = 1 << level;
-      const uint64_t thr = N * (uint64_t)(m / 2);
-      // a bounded footprint (4 CTAs of 128 per SM, grid-stride): the lanes
-      // fill the issue slots the latency-bound heuristic leaves idle without
-      // crowding its warps (C2: 0.607 ms vs 0.614 with one CTA per 128
-      // (sample, pair) items and 0.617 without early lanes)
-      uint64_t grid = std::min<uint64_t>((thr + 127) / 128, 4ull * num_sms);
-      if (oaa_ctas > 0) grid = std::min<uint64_t>((thr + 127) / 128, (uint64_t)oaa_ctas);
-      k_oaa_early<<<(unsigned)grid, 128, 0, os>>>(midx, ws + L.oaa, N, m, c.sample_base, K,
-                                                  op_id(level + 1, SITE_PART_OAA));
-      GT_LAUNCH_CHECK("k_oaa_early");
-      P.count_launch();
-      if (os != s) {
-        GT_CUDA_CHECK(cudaEventRecord(side->eo[1], side->lo));
-        oaa_forked = true;
-      }
-      oaa_ready = true;
+    if (early_after_count) {
+      int rc = early_oaa_launch(level);
+      if (rc) return rc;
     }
     if (allreduce) {
       int rc = allreduce(S, swords, stream, allreduce_user);
