@@ -149,15 +149,13 @@ __global__ void __launch_bounds__(256) k_prep8(Prep8Args a) {
   // quad's x words are byte-transposed in registers (4x4 byte_perm
   // transposes) into one 32-bit word of each of the 8 limb rows; the four
   // quads of a row are adjacent threads
+  // thread t owns (column g, quad) = t % (4 cpb) and walks the (component,
+  // column block, 16-sample chunk) combinations: one division per thread
   const uint64_t HBX = (uint64_t)8 * a.cpb * (TC_KB / 2);
-  const int items = 3 * 2 * a.nbn * a.cpb * 4;
-  for (int it = tid; it < items; it += blockDim.x) {
-    const int quad = it & 3;
-    int r = it >> 2;
-    const int g = r % a.cpb;
-    r /= a.cpb;
-    const int kc = 2 * sub + (r & 1);
-    r >>= 1;
+  const int gq = 4 * a.cpb, combos = 3 * a.nbn * 2;
+  const int g = (tid % gq) >> 2, quad = tid & 3;
+  for (int cb = tid / gq; cb < combos; cb += blockDim.x / gq) {
+    const int kc = 2 * sub + (cb & 1), r = cb >> 1;
     const int nb = r % a.nbn, c = r / a.nbn;
     const int w = nb * a.cpb + g;
     const uint64_t* p0 = nullptr;
