@@ -160,6 +160,16 @@ def main():
                 engine.run_local(body, seeds=setup, dealer_seed=dseed)
                 pr.disable()
             pstats.Stats(pr).sort_stats("tottime").print_stats(15)
+    elif what == "small":  # sanitizer target: 4000 x 13, depth 5 (fused count, early oaa lanes, split partition)
+        rng = np.random.default_rng(5)
+        n, nf, depth = 4000, 13, 5
+        X = t(bench._share(rng.integers(0, 2, (n, nf)), rng))
+        Y = t(bench._share(rng.integers(0, 2, n), rng))
+        F = t(np.zeros((1 << depth) - 1, dtype=np.uint64))
+        tr = DeviceTrainer(n, nf, TrainConfig(depth=depth))
+        tr.run(X, Y, F, keys)
+        torch.cuda.synchronize()
+        print("small tree ok", flush=True)
     elif what == "c4":
         n, nf, depth = 10 ** 6, 32, 8
         rng = np.random.default_rng(3)

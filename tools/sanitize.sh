@@ -16,3 +16,13 @@ for tool in memcheck racecheck synccheck; do
     python -c "import __graft_entry__ as g; g.smoke()" > "$out/sanitize_${tool}_c1.out" 2>&1
   echo "$tool c1 rc=$?"
 done
+# the fused count, early oaa lanes and split partition on a small C2-shaped tree
+for tool in memcheck racecheck synccheck; do
+  $CS --tool $tool --log-file "$out/sanitize_${tool}_small_fused.log" \
+    python tools/probe.py small > "$out/sanitize_${tool}_small_fused.out" 2>&1
+  echo "$tool small_fused rc=$?"
+done
+# the full C2 tree (memcheck only: racecheck over ~120 launches of this size takes too long)
+$CS --tool memcheck --log-file "$out/sanitize_memcheck_c2_tree.log" python tools/probe.py c2eager \
+  > "$out/sanitize_memcheck_c2_tree.out" 2>&1
+echo "memcheck c2_tree rc=$?"
