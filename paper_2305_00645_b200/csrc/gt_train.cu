@@ -1085,6 +1085,7 @@ __global__ void k_div_table(uint32_t* table, DivParams d) {
   table[b] = (sub << 16) | (pidx << 8) | (uint32_t)(key + 1);
 }
 
+constexpr int DIV_TAPE_PER = 4;  // blocks per thread of k_div_tape
 template <int SL>
 __global__ void __launch_bounds__(256) k_div_tape(W2* tape, const uint32_t* __restrict__ table, uint64_t total,
                                                    int cols, int TB, Keys K) {
@@ -1094,15 +1095,32 @@ __global__ void __launch_bounds__(256) k_div_tape(W2* tape, const uint32_t* __re
   for (int i = threadIdx.x; i < (int)(sizeof(Keys) / 4); i += blockDim.x)
     reinterpret_cast<uint32_t*>(&ks)[i] = reinterpret_cast<const uint32_t*>(&K)[i];
   __syncthreads();
-  // 32-bit index math: the tape is capped at 256 MB (< 2^24 blocks)
-  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  // 32-bit index math: the tape is capped at 256 MB (< 2^24 blocks).  Each
+  // thread draws DIV_TAPE_PER blocks 32 apart (a warp writes 32 consecutive
+  // blocks per store; independent Philox chains in flight together; one index
+  // decomposition, then a carry per block)
+  const uint32_t lane = threadIdx.x & 31, wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  uint32_t e = wg * 32 * DIV_TAPE_PER + lane;
   if (e >= total) return;
-  const uint32_t g = e / (uint32_t)TB, nodes = g / (uint32_t)cols;
-  const uint32_t t = __ldg(table + (e - g * (uint32_t)TB));
-  const int level = 31 - __clz(nodes + 1);  // nodes in [2^h - 1, 2^{h+1} - 1)
-  const uint64_t li = g - ((1u << level) - 1) * (uint32_t)cols;
-  const int key = (int)(t & 0xff) - 1;
-  tape[e] = word2(key < 0 ? ks.dealer : ks.pair[key], op_id(level, SITE_HC), 13 + (t >> 16), (t >> 8) & 0xff, li);
+  uint32_t g = e / (uint32_t)TB, b = e - g * (uint32_t)TB;
+  uint32_t tt[DIV_TAPE_PER], gg[DIV_TAPE_PER];
+#pragma unroll
+  for (int k = 0; k < DIV_TAPE_PER; ++k) {
+    gg[k] = g;
+    tt[k] = e + 32 * k < total ? __ldg(table + b) : 0u;
+    b += 32;
+    while (b >= (uint32_t)TB) b -= (uint32_t)TB, ++g;
+  }
+#pragma unroll
+  for (int k = 0; k < DIV_TAPE_PER; ++k, e += 32) {
+    if (e >= total) break;
+    const uint32_t nodes = gg[k] / (uint32_t)cols;
+    const int level = 31 - __clz(nodes + 1);  // nodes in [2^h - 1, 2^{h+1} - 1)
+    const uint64_t li = gg[k] - ((1u << level) - 1) * (uint32_t)cols;
+    const uint32_t t = tt[k];
+    const int key = (int)(t & 0xff) - 1;
+    tape[e] = word2(key < 0 ? ks.dealer : ks.pair[key], op_id(level, SITE_HC), 13 + (t >> 16), (t >> 8) & 0xff, li);
+  }
 }
 
 // hc_post_body's shared scratch in words: vals/idxs/nvals/nidxs [3][nf], hit
@@ -2584,10 +2602,12 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
     P.start();
     if (c.score_width == 32) {
       k_div_table<32><<<(TB + 127) / 128, 128, 0, ts>>>(table, d);
-      k_div_tape<32><<<(unsigned)((tape_words + 255) / 256), 256, 0, ts>>>(tape, table, tape_words, cols_i, TB, K);
+      k_div_tape<32><<<(unsigned)((tape_words + 256 * DIV_TAPE_PER - 1) / (256 * DIV_TAPE_PER)), 256, 0, ts>>>(
+          tape, table, tape_words, cols_i, TB, K);
     } else {
       k_div_table<64><<<(TB + 127) / 128, 128, 0, ts>>>(table, d);
-      k_div_tape<64><<<(unsigned)((tape_words + 255) / 256), 256, 0, ts>>>(tape, table, tape_words, cols_i, TB, K);
+      k_div_tape<64><<<(unsigned)((tape_words + 256 * DIV_TAPE_PER - 1) / (256 * DIV_TAPE_PER)), 256, 0, ts>>>(
+          tape, table, tape_words, cols_i, TB, K);
     }
     const uint64_t post_words = post_tape_words(c);
     if (post_words) {
