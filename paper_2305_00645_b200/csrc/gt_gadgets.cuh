@@ -331,25 +331,29 @@ template <int L>
 __device__ __forceinline__ B3 prefix_borrow_blk(B3 g, B3 p, const W2* blk) {
   constexpr uint64_t M = Ring<L>::M;
   constexpr int NL = Levels<L>::n;
+  // g and p stay within M; the shifted words and the zero words are used
+  // unmasked and the gates' outputs are cut to the rows >= s (and < L) once,
+  // inside the combining LOP3 (the same rows the masked operands give: the
+  // AND terms vanish outside them because p does)
 #pragma unroll
   for (int lvl = 0; lvl < NL; ++lvl) {
     const int s = 1 << lvl;
-    const uint64_t hm = M & ~lowmask(s);
+    const uint64_t hm = M & ~lowmask(s), lm = lowmask(s);
     B3 gs, ps;
     uint64_t Zg[3], Zp[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      gs.v[i] = (g.v[i] << s) & M;
-      ps.v[i] = (p.v[i] << s) & M;
-      Zg[i] = blk[i * NL + lvl].a & hm;
-      Zp[i] = blk[i * NL + lvl].b & hm;
+      gs.v[i] = g.v[i] << s;
+      ps.v[i] = p.v[i] << s;
+      Zg[i] = blk[i * NL + lvl].a;
+      Zp[i] = blk[i * NL + lvl].b;
     }
     const B3 pg = and_z(p, gs, Zg);
     const B3 pp = and_z(p, ps, Zp);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      g.v[i] ^= pg.v[i];
-      p.v[i] = (p.v[i] & lowmask(s)) | pp.v[i];
+      g.v[i] ^= pg.v[i] & hm;
+      p.v[i] = (p.v[i] & lm) | (pp.v[i] & hm);
     }
   }
   return g;
