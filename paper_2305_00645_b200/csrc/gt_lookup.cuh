@@ -51,7 +51,7 @@ __device__ __forceinline__ void lookup_pair_ca(const Keys& K, uint32_t op, uint6
     const DealerRand R0 = dealer_rand(K, op, lane0), R1 = dealer_rand(K, op, lane0 + 1);
     const uint64_t Z0[3] = {Z[0].a, Z[1].a, Z[2].a}, Z1[3] = {Z[0].b, Z[1].b, Z[2].b};
     B3 h0, h1;
-    eq_arith64_x2(d0, R0.r, R0.Rb0, R0.Rb1, Z0, d1, R1.r, R1.Rb0, R1.Rb1, Z1, &h0, &h1);
+    eq_arith64_x2<false>(d0, R0.r, R0.Rb0, R0.Rb1, Z0, d1, R1.r, R1.Rb0, R1.Rb1, Z1, &h0, &h1);
     *ca0 = b2a_arith<L>(h0, R0.A0, R0.A1, R0.bits);
     if (j1 < m) *ca1 = b2a_arith<L>(h1, R1.A0, R1.A1, R1.bits);
     return;
