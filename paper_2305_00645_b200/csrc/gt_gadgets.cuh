@@ -549,10 +549,11 @@ __device__ __forceinline__ A3 b2a_arith(const B3& b, uint64_t A0, uint64_t A1, u
   constexpr uint64_t M = Ring<L>::M;
   A0 &= M;
   A1 &= M;
-  const uint64_t beta = bits & 1ull, Bb0 = (bits >> 1) & 1ull, Bb1 = (bits >> 2) & 1ull;
-  const uint64_t Bb2 = beta ^ Bb0 ^ Bb1;
+  const uint64_t beta = bits & 1ull;
   const uint64_t A2 = (beta - A0 - A1) & M;
-  const uint64_t e = ((b.v[0] ^ Bb0) ^ (b.v[1] ^ Bb1) ^ (b.v[2] ^ Bb2)) & 1ull;  // open_bits
+  // open_bits of b ^ beta: the dabit's bit shares Bb0, Bb1, Bb2 = beta ^ Bb0 ^
+  // Bb1 (bits 1, 2 of `bits`) cancel in the opened sum, leaving beta
+  const uint64_t e = (b.v[0] ^ b.v[1] ^ b.v[2] ^ bits) & 1ull;
   // A * (1 - 2e) as a conditional negate ((A ^ m) - m, m = -e): keeps the
   // IMAD pipe for the Philox rounds and the share products
   const uint64_t m = 0ull - e;
