@@ -73,6 +73,7 @@ struct Prep8Args {
   uint8_t* B8;
   uint64_t N, nkb, base, hb0;  // hb0: first 64-sample half block of this launch
   int nf, W, cpb, nbn;
+  int mask_cols;  // columns W, W+1 = the public constant 1 as shares (1,0,0) / (0,1,0) (k_count_fused's mask sums)
   Keys K;
   uint32_t op_prods;
 };
@@ -163,11 +164,13 @@ __global__ void __launch_bounds__(256) k_prep8(Prep8Args a) {
     if (w < nf) p0 = xs + c * HS * nf + w;
     else if (w < 2 * nf) p0 = ps + c * HS * nf + (w - nf);
     else if (w == 2 * nf) p0 = ys + c * HS, stride = 1;
+    // the mask columns: component c of the constant is 1 in column W + c (c < 2)
+    const uint64_t cval = (a.mask_cols && (w == a.W || w == a.W + 1) && c == w - a.W) ? 1ull : 0ull;
     uint32_t wx[2][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int sl = (kc & 1) * 16 + quad * 4 + i;
-      const uint64_t x = (p0 && sl < cnt) ? p0[sl * stride] : 0ull;
+      const uint64_t x = sl < cnt ? (p0 ? p0[sl * stride] : cval) : 0ull;
       wx[0][i] = (uint32_t)x, wx[1][i] = (uint32_t)(x >> 32);
     }
     uint8_t* dst = a.B8 + (((uint64_t)nb * a.nkb + kb) * 2 + half) * 3 * HBX + c * HBX +
@@ -759,6 +762,7 @@ struct FusedArgs {
   int n_h, W, nkr, NBn, stages;
   int mode3;     // three UMMAs per step (shallow tiles, tcf_mode3)
   int ts_level;  // diagnostics (GT_COUNT_TS): phase timestamps of cluster 0 into g_cnt_ts[8 level ..], -1 off
+  int mask_mma;  // s_mask from the x planes' constant columns W, W+1 (prep8 mask_cols) instead of warp sums
   int xpre;      // the x planes are complete before this launch's predecessor ran (levels >= 1): the copy
                  // thread fills the first x stages before the PDL wait
 };
@@ -974,7 +978,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 2), 1) k_
         for (int c = 0; c < 3; ++c) lf.v[c] = leaf[c][g];
         count_lane_pair(a.K, a.op_cnt, a.base + s, a.n_h, n, d0, d1, true, v1, lf, &l0, &l1);
       }
-      {  // s_mask (train.py:220): the warp's 64 samples of node n, one atomic per component
+      if (!a.mask_mma) {  // s_mask (train.py:220): the warp's 64 samples of node n, one atomic per component
         A3 m = v1 ? add<64>(l0, l1) : l0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1)
@@ -1147,7 +1151,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 2), 1) k_
       if (cell >= cells) break;
       const int w = cell & 15, cn = cell >> 4, ni = cn % NNt, c = cn / NNt;
       const int n = nt * 16 + ni, wg = (int)rank * 16 + w;
-      if (n >= a.n_h || wg >= a.W) continue;
+      const bool maskcell = a.mask_mma && ((c == 0 && (wg == a.W || wg == a.W + 1)) || (c == 2 && wg == a.W));
+      if (n >= a.n_h || (wg >= a.W && !maskcell)) continue;
       uint64_t v = 0;
       for (int sl = 0; sl < (mode3 ? 2 : 1); ++sl) {
         const uint4* rp = reinterpret_cast<const uint4*>(red + sl * RSLOT + (uint64_t)cell * 8);
@@ -1156,6 +1161,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 2), 1) k_
           const uint4 x = rp[i];
           v += ((uint64_t)x.y << 32 | x.x) + ((uint64_t)x.w << 32 | x.z);
         }
+      }
+      if (maskcell) {
+        // s_mask (train.py:220) from the constant columns: column W (shares
+        // (1,0,0)) gives D_0 = sum la_0 + la_1, D_2 = sum la_2; column W+1
+        // ((0,1,0)) gives D_0 = sum la_0 -- so mask_0 = D_0(W+1), mask_1 =
+        // D_0(W) - D_0(W+1), mask_2 = D_2(W)
+        unsigned long long* Sm = (unsigned long long*)&a.S[(uint64_t)n * (a.W + 1) + a.W];
+        if (c == 2) {
+          atomicAdd(Sm + 2 * Sstride, (unsigned long long)v);
+        } else if (wg == a.W) {
+          atomicAdd(Sm + Sstride, (unsigned long long)v);
+        } else {
+          atomicAdd(Sm, (unsigned long long)v);
+          atomicAdd(Sm + Sstride, (unsigned long long)(0ull - v));
+        }
+        continue;
       }
       if (a.alpha && kr == 0 && a.alpha_tab) {
         v += apre[k];

@@ -1744,6 +1744,13 @@ inline uint64_t div_tape_level_off(int level, int nf, int TB) {  // W2 offset of
 }
 
 bool count_fused_ok(int nf);
+// The fused count's mask sums on the tensor cores: two constant x-plane
+// columns after the W sample columns (room for them in the 32 columns of a
+// CTA pair's M tile: nf <= 14)
+bool count_mask_mma(int nf) {
+  static const bool off = getenv("GT_NO_MASK_MMA") != nullptr;  // A/B experiments
+  return !off && count_fused_ok(nf) && 2 * nf + 1 + 2 <= 32;
+}
 
 // Early oaa lanes (k_oaa_early) for the split partition's sample counts, when
 // the largest level's hit shares [3][2^(depth-2)][N] fit 256 MB.
@@ -2257,6 +2264,7 @@ int launch_count_fused(const CountLaunch& c, const uint8_t* B8, int alpha, uint6
   fa.W = 2 * c.nf + 1;
   fa.nkr = nkr;
   fa.NBn = NBn;
+  fa.mask_mma = count_mask_mma(c.nf) ? 1 : 0;
   {
     static const bool no_m3 = getenv("GT_FUSED_NO_MODE3") != nullptr;  // A/B experiments
     fa.mode3 = tcf_mode3(NBn) && !no_m3;
@@ -2444,6 +2452,7 @@ int launch_prep8(const gt_train_cfg& c, const uint64_t* features, const uint64_t
   pa.W = 2 * c.nf + 1;
   pa.cpb = tp.cpb;
   pa.nbn = tp.nbn;
+  pa.mask_cols = count_mask_mma(c.nf) ? 1 : 0;
   pa.K = K;
   pa.op_prods = op_id(0, SITE_PRODS);
   const int smem = 3 * (TC_KB / 4) * pa.W * (int)sizeof(uint64_t);  // one CTA per 32-sample quarter block
