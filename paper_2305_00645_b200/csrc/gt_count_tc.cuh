@@ -77,7 +77,12 @@ struct Prep8Args {
   Keys K;
   uint32_t op_prods;
 };
-__global__ void __launch_bounds__(256) k_prep8(Prep8Args a) {
+// 6 CTAs per SM (40 registers): C2 0.5808 vs 0.5846 ms at the default 48
+// registers / 5 CTAs (same-call A/B; 8 CTAs at 32 registers: 0.5830)
+#ifndef GT_PREP8_MINB
+#define GT_PREP8_MINB 6
+#endif
+__global__ void __launch_bounds__(256, GT_PREP8_MINB) k_prep8(Prep8Args a) {
   // one CTA per 32-sample quarter block (chunks kc = 2 sub, 2 sub + 1 of a
   // 64-sample half block: a grid of many small CTAs leaves no near-empty
   // second wave); shared memory (<= 99 KB at nf = 64): xs[3][HS][nf]
