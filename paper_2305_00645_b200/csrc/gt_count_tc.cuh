@@ -744,9 +744,13 @@ __host__ __device__ inline int tcf_la_bytes(int nbn_nodes, bool m3) { return (m3
 __host__ __device__ inline int tcf_xstages(int nbn_nodes) { return nbn_nodes <= 2 ? 6 : nbn_nodes <= 4 ? 4 : 3; }
 // la stages: a deep ring, so a producer warp that runs ahead of the slowest
 // one rarely waits for a slot (each stage needs all NBn node items)
+// (a power of two: the producers' stage index and phase are shifts and masks)
 __host__ __device__ inline int tcf_stages(int nbn_nodes, bool m3) {
-  const int s = (200 * 1024 - tcf_xstages(nbn_nodes) * TCF_XB) / tcf_la_bytes(nbn_nodes, m3);
-  return s > TCF_MAXS ? TCF_MAXS : s;
+  int s = (200 * 1024 - tcf_xstages(nbn_nodes) * TCF_XB) / tcf_la_bytes(nbn_nodes, m3);
+  s = s > TCF_MAXS ? TCF_MAXS : s;
+  int p = 1;
+  while (2 * p <= s) p *= 2;
+  return p;
 }
 __host__ __device__ inline int tcf_smem(int nbn_nodes, bool m3) {
   return tcf_xstages(nbn_nodes) * TCF_XB + tcf_stages(nbn_nodes, m3) * tcf_la_bytes(nbn_nodes, m3);
@@ -849,6 +853,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 2), 1) k_
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nt = blockIdx.y, kr = blockIdx.z;
   const int NBn = a.NBn, NU = 16 * NBn, NS = a.stages;  // NU: the pair's UMMA N (2 NBn nodes x 8 limbs)
+  // NBn and NS are powers of two: item -> (stage, node) and stage -> (slot,
+  // phase) by shifts and masks (runtime divisions cost ~20 instructions each)
+  const int nbn_sh = __ffs(NBn) - 1, ns_sh = __ffs(NS) - 1;
   const bool mode3 = a.mode3;
   const int LB = tcf_la_bytes(NBn, mode3);
   const int XS = tcf_xstages(NBn);
@@ -941,7 +948,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 2), 1) k_
     const bool odd = lane & 1;
     const int s2 = 2 * lane, items = T * NBn;
     auto sample_of = [&](int i) {
-      const int t = i / NBn;
+      const int t = i >> nbn_sh;
       return ((uint64_t)a.kb_lo + kb0 + (uint32_t)(t >> 1)) * TC_KB + (t & 1) * (TC_KB / 2) + s2;
     };
     auto load_idx = [&](int i, uint64_t (&m)[6]) {
@@ -959,7 +966,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 2), 1) k_
     uint64_t mnext[6];
     if (PF) load_idx(warp, mnext);
     for (int i = warp; i < items; i += TCF_PW) {
-      const int t = i / NBn, g = i - t * NBn, st = t % NS;
+      const int t = i >> nbn_sh, g = i & (NBn - 1), st = t & (NS - 1);
       uint64_t mc[6];
       if (PF) {
 #pragma unroll
@@ -968,7 +975,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 2), 1) k_
       } else {
         load_idx(i, mc);
       }
-      if (t >= NS) mbar_wait(&empty[st], (uint32_t)(((t / NS) - 1) & 1));
+      if (t >= NS) mbar_wait(&empty[st], (uint32_t)(((t >> ns_sh) - 1) & 1));
       const int n = node0 + g;
       const uint64_t s = sample_of(i);
       A3 l0 = a3(0, 0, 0), l1 = a3(0, 0, 0);
@@ -1054,8 +1061,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 2), 1) k_
     // once both CTAs' stage t is full; the peer forwards its full stage
     const uint32_t idesc = (2u << 4) | ((uint32_t)((mode3 ? 2 * NU : NU) >> 3) << 17) | ((256u >> 4) << 24);
     for (int t = 0; t < T; ++t) {
-      const int st = t % NS, xs = t % XS;
-      const uint32_t ph = (uint32_t)((t / NS) & 1);
+      const int st = t & (NS - 1), xs = t % XS;
+      const uint32_t ph = (uint32_t)((t >> ns_sh) & 1);
       mbar_wait(&xfull[xs], (uint32_t)((t / XS) & 1));
       mbar_wait(&full[st], ph);
       if (rank == 0) {
