@@ -357,11 +357,12 @@ __device__ __forceinline__ B3 prefix_borrow_blk(B3 g, B3 p, const W2* blk) {
       Zp[i] = blk[i * NL + lvl].b;
     }
     const B3 pg = and_z(p, gs, Zg);
-    const B3 pp = and_z(p, ps, Zp);
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      g.v[i] ^= pg.v[i] & hm;
-      p.v[i] = (p.v[i] & lm) | (pp.v[i] & hm);
+    for (int i = 0; i < 3; ++i) g.v[i] ^= pg.v[i] & hm;
+    if (lvl + 1 < NL) {  // the last level's propagate gates feed nothing: not computed (same g)
+      const B3 pp = and_z(p, ps, Zp);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) p.v[i] = (p.v[i] & lm) | (pp.v[i] & hm);
     }
   }
   return g;
