@@ -2186,6 +2186,8 @@ struct Side {
   cudaStream_t st = nullptr;  // compute side stream (high priority)
   cudaStream_t cp = nullptr;  // host <-> device copies of the host-input entry
   cudaStream_t lo = nullptr;  // early oaa lanes beside the heuristic chain (low priority)
+  cudaStream_t st2 = nullptr; // the epilogue / prologue / node tapes beside the division tapes (high priority)
+  cudaEvent_t et2[2] = {};    // st2 fork / join
   cudaEvent_t ev[16] = {};
   cudaEvent_t eo[2] = {};     // early oaa fork / join
 };
@@ -2209,6 +2211,8 @@ int side_of(int dev, Side** out) {
     GT_CUDA_CHECK(cudaStreamCreateWithPriority(&sd.st, cudaStreamNonBlocking, hi));
     GT_CUDA_CHECK(cudaStreamCreateWithFlags(&sd.cp, cudaStreamNonBlocking));
     GT_CUDA_CHECK(cudaStreamCreateWithPriority(&sd.lo, cudaStreamNonBlocking, lo));
+    GT_CUDA_CHECK(cudaStreamCreateWithPriority(&sd.st2, cudaStreamNonBlocking, hi));
+    for (auto& e : sd.et2) GT_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : sd.ev) GT_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : sd.eo) GT_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
@@ -2608,6 +2612,14 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
       if (rc) return rc;
       ts = side->st;
     }
+    // the other tapes on a second stream beside the division tape (their
+    // launches overlap instead of queueing behind it), joined back into ts
+    cudaStream_t ts2 = ts;
+    if (ts != s) {
+      GT_CUDA_CHECK(cudaEventRecord(side->et2[0], ts));
+      GT_CUDA_CHECK(cudaStreamWaitEvent(side->st2, side->et2[0], 0));
+      ts2 = side->st2;
+    }
     P.start();
     if (c.score_width == 32) {
       k_div_table<32><<<(TB + 127) / 128, 128, 0, ts>>>(table, d);
@@ -2624,10 +2636,10 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
       const uint32_t SA = 13 + div_subs(d);
       uint64_t* ptab = ws + L.posttable;
       if (c.score_width == 32)
-        k_post_table<32><<<(E + 127) / 128, 128, 0, ts>>>(ptab, c.nf, SA);
+        k_post_table<32><<<(E + 127) / 128, 128, 0, ts2>>>(ptab, c.nf, SA);
       else
-        k_post_table<64><<<(E + 127) / 128, 128, 0, ts>>>(ptab, c.nf, SA);
-      k_post_tape<<<(unsigned)((post_words + 255) / 256), 256, 0, ts>>>(reinterpret_cast<W2*>(ws + L.posttape), ptab,
+        k_post_table<64><<<(E + 127) / 128, 128, 0, ts2>>>(ptab, c.nf, SA);
+      k_post_tape<<<(unsigned)((post_words + 255) / 256), 256, 0, ts2>>>(reinterpret_cast<W2*>(ws + L.posttape), ptab,
                                                                        (uint32_t)post_words, c.nf, E, K);
       GT_LAUNCH_CHECK("k_post_tape");
       P.count_launch();
@@ -2635,7 +2647,7 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
     }
     if (feat_tape_words(c)) {  // prologue feature tapes
       const uint64_t fw = feat_tape_words(c);
-      k_feat_tape<<<(unsigned)((fw + 255) / 256), 256, 0, ts>>>(reinterpret_cast<W2*>(ws + L.feattape), (uint32_t)fw,
+      k_feat_tape<<<(unsigned)((fw + 255) / 256), 256, 0, ts2>>>(reinterpret_cast<W2*>(ws + L.feattape), (uint32_t)fw,
                                                                 c.nf, K);
       GT_LAUNCH_CHECK("k_feat_tape");
       P.count_launch();
@@ -2644,12 +2656,16 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
       const NodeTape NT = node_tape_plan(c.nf);
       const uint64_t nwords = ((1ull << c.depth) - 1) * (uint64_t)NT.total;
       uint64_t* ntab = ws + L.nodetable;
-      k_node_table<<<(NT.total + 127) / 128, 128, 0, ts>>>(ntab, c.nf);
-      k_node_tape<<<(unsigned)((nwords + 255) / 256), 256, 0, ts>>>(reinterpret_cast<W2*>(ws + L.nodetape), ntab,
+      k_node_table<<<(NT.total + 127) / 128, 128, 0, ts2>>>(ntab, c.nf);
+      k_node_tape<<<(unsigned)((nwords + 255) / 256), 256, 0, ts2>>>(reinterpret_cast<W2*>(ws + L.nodetape), ntab,
                                                                     (uint32_t)nwords, NT.total, K);
       GT_LAUNCH_CHECK("k_node_tape");
       P.count_launch();
       P.count_launch();
+    }
+    if (ts2 != ts) {
+      GT_CUDA_CHECK(cudaEventRecord(side->et2[1], ts2));
+      GT_CUDA_CHECK(cudaStreamWaitEvent(ts, side->et2[1], 0));
     }
     tape_forked = ts != s;
     P.count_launch();
