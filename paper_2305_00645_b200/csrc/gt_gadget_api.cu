@@ -4,7 +4,10 @@
 // functions fused into larger kernels.
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -275,6 +278,56 @@ int gt_unpack_pairs(const void* const* lo, const void* const* hi, uint32_t strid
 // copied to out + i n; party i+1's hi must equal party i+2's lo word for word.
 // Split over host threads in 1 MB slices (memcmp + memcpy stream at memory
 // speed); returns GT_ERR_INVALID on an inconsistent pair.
+namespace {
+// Persistent host workers for the staging copies / checks of the drop-in
+// path (a fresh std::thread per worker per call cost ~0.1 ms per call).  One
+// job at a time (callers serialise on run_mu); the caller works too.
+struct HostPool {
+  std::vector<std::thread> th;
+  std::mutex mu, run_mu;
+  std::condition_variable cv, done_cv;
+  std::function<void()> job;
+  uint64_t gen = 0;
+  unsigned pending = 0;
+  explicit HostPool(unsigned n) {
+    for (unsigned t = 0; t < n; ++t)
+      th.emplace_back([this] {
+        uint64_t seen = 0;
+        for (;;) {
+          std::function<void()> j;
+          {
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [&] { return gen != seen; });
+            seen = gen;
+            j = job;
+          }
+          j();
+          std::lock_guard<std::mutex> lk(mu);
+          if (--pending == 0) done_cv.notify_one();
+        }
+      });
+    for (auto& t : th) t.detach();  // process-lifetime workers
+  }
+  void run(const std::function<void()>& f) {  // f on every worker and the caller
+    std::lock_guard<std::mutex> rl(run_mu);
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      job = f;
+      pending = (unsigned)th.size();
+      ++gen;
+    }
+    cv.notify_all();
+    f();
+    std::unique_lock<std::mutex> lk(mu);
+    done_cv.wait(lk, [&] { return pending == 0; });
+  }
+};
+HostPool& host_pool() {
+  static HostPool* p = new HostPool(std::max(1u, std::min(8u, std::thread::hardware_concurrency())) - 1u);
+  return *p;
+}
+}  // namespace
+
 int gt_stage_pairs(const uint64_t* const* lo, const uint64_t* const* hi, uint64_t n, uint64_t* out, int check) {
   if (!lo || !hi || (!out && !check)) return fail_inval("gt_stage_pairs: NULL operand");
   for (int i = 0; i < 3; ++i)
@@ -291,12 +344,8 @@ int gt_stage_pairs(const uint64_t* const* lo, const uint64_t* const* hi, uint64_
       if (out) std::memcpy(out + (uint64_t)i * n + a, lo[i] + a, len * 8);
     }
   };
-  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
-  const unsigned nth = (unsigned)std::min<uint64_t>(hw, 3 * nsl);
-  std::vector<std::thread> pool;
-  for (unsigned t = 1; t < nth; ++t) pool.emplace_back(work);
-  work();
-  for (auto& t : pool) t.join();
+  if (3 * nsl <= 1) work();
+  else host_pool().run(work);
   if (bad) return fail_inval("replication inconsistency between party pairs");
   return GT_OK;
 }

@@ -44,7 +44,7 @@ __device__ __forceinline__ void lookup_pair_ca(const Keys& K, uint32_t op, uint6
 #pragma unroll
   for (int i = 0; i < 3; ++i) Z[i] = word2(K.pair[i], op, 0, 0, gidx * (uint64_t)mh + (uint64_t)q);
   *ca1 = a3(0, 0, 0);
-  if (L == 64) {  // both entries' eq trees packed together (eq_arith64_x2)
+  if constexpr (L == 64) {  // both entries' eq trees packed together (eq_arith64_x2)
     const int j0 = 2 * q, j1 = 2 * q + 1;
     const uint64_t lane0 = gidx * (uint64_t)m + (uint64_t)j0;
     const A3 d0 = add_pub<L>(idx, 0ull - (uint64_t)j0), d1 = add_pub<L>(idx, 0ull - (uint64_t)j1);
@@ -55,7 +55,7 @@ __device__ __forceinline__ void lookup_pair_ca(const Keys& K, uint32_t op, uint6
     *ca0 = b2a_arith<L>(h0, R0.A0, R0.A1, R0.bits);
     if (j1 < m) *ca1 = b2a_arith<L>(h1, R1.A0, R1.A1, R1.bits);
     return;
-  }
+  } else {
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int j = 2 * q + h;
@@ -66,6 +66,7 @@ __device__ __forceinline__ void lookup_pair_ca(const Keys& K, uint32_t op, uint6
     const uint64_t Zw[3] = {h ? Z[0].b : Z[0].a, h ? Z[1].b : Z[1].a, h ? Z[2].b : Z[2].a};
     const B3 hit = eq_arith<L>(d, R.r, R.Rb0, R.Rb1, Zw);
     *(h ? ca1 : ca0) = b2a_arith<L>(hit, R.A0, R.A1, R.bits);
+  }
   }
 }
 

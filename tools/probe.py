@@ -146,6 +146,27 @@ def main():
             return engine.train_tree(eng, AVec(RING64, Xh[p - 1], Xh2[p % 3]), AVec(RING64, Yh[p - 1], Yh2[p % 3]), cfg)
         from paper_2305_00645_b200.train import train_pairs
         tm("train_pairs_direct", lambda: train_pairs(xp, yp, cfg, setup, dseed))
+        # its steps one by one (wall clock marks, ms)
+        marks = []
+        for _ in range(10):
+            a = time.perf_counter()
+            stage_pairs(xp, st["X"].numpy().view(np.uint64), False)
+            stage_pairs(yp, st["Y"].numpy().view(np.uint64), False)
+            b = time.perf_counter()
+            st["fill"].numpy().view(np.uint64)[:] = filler_values(setup.filler_seed, 127, 14)
+            replay = tr.host_graph(keys)
+            replay()
+            c = time.perf_counter()
+            stage_pairs(xp, None, True)
+            stage_pairs(yp, None, True)
+            d = time.perf_counter()
+            s.synchronize()
+            e = time.perf_counter()
+            T = st["T"].numpy().view(np.uint64)[:, :127].copy()
+            f = time.perf_counter()
+            marks.append((b - a, c - b, d - c, e - d, f - e))
+        med = [statistics.median(m[k] for m in marks) * 1e3 for k in range(5)]
+        print("split: stage %.3f launch %.3f check %.3f sync %.3f copy %.3f" % tuple(med), flush=True)
         tm("run_local_total", lambda: engine.run_local(body, seeds=setup, dealer_seed=dseed))
         tm("threads_only", lambda: engine.run_local(lambda eng: None, seeds=setup, dealer_seed=dseed))
         print(" ".join(f"{k}={v:.3f}" for k, v in res.items()), flush=True)
