@@ -247,7 +247,17 @@ __global__ void __launch_bounds__(PS_TPB, 3)
   A3 d = a3(0, 0, 0);
   if (valid) {  // row_lookup of the sample's features at the fetched index   (train.py:138)
     auto entryX = [&](int f) { return ld3s(X, nfx, s * nf + f); };
-    d = lookup_partial<64>(K, op_row, g, acc, nf, r, B, entryX);
+    if (B == 2 && (((nf + 1) >> 1) & 1)) {
+      // an odd number of entry pairs: member 0 takes pairs 0, 2, ... (one
+      // more than member 1), member 1 the pairs 1, 3, ... and all six
+      // telescope words, so neither member's chain is longer than its pairs
+      d = a3(0, 0, 0);
+      if (r == 1)
+        for (int e = 0; e < 6; ++e) d = add<64>(d, lookup_word<64>(K, op_row, g, nf, e));
+      for (int q = r; q < ((nf + 1) >> 1); q += 2) d = add<64>(d, lookup_pair<64>(K, op_row, g, acc, nf, q, entryX));
+    } else {
+      d = lookup_partial<64>(K, op_row, g, acc, nf, r, B, entryX);
+    }
   }
   if (B > 1) {
     __syncthreads();
