@@ -200,13 +200,13 @@ def walk_blocks(n, nf, depth):
     return n * sum(lookup_blocks(1 << t) + lookup_blocks(nf) for t in range(depth))
 
 
-def _roof(alg_bytes, blocks, seconds, peak, peak_kind, philox_peak, what):
+def _roof(alg_bytes, blocks, seconds, peak, peak_kind, philox_peak, what, traffic=None):
     """HBM roof on algorithmic bytes and the integer-ALU roof on Philox blocks
     (the lane work is ALU bound) for one timed unit of work."""
     gbs = alg_bytes / seconds / 1e9
     bps = blocks / seconds
     return {"bound": "hbm", "kernel": what, "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
-            "peak_source": peak_kind, "algorithmic_bytes": alg_bytes, "traffic": None,
+            "peak_source": peak_kind, "algorithmic_bytes": alg_bytes, "traffic": traffic,
             "alu": {"bound": "int-alu (Philox4x32-10 blocks)", "blocks": blocks, "achieved_blocks_per_s": bps,
                     "peak_blocks_per_s": philox_peak, "frac": bps / philox_peak if philox_peak else None}}
 
@@ -705,7 +705,7 @@ def main():
                 "partition": partition_bytes(cnt, NF_C2, DEPTH_C2),
                 # prologue: features + labels in, the W sample columns (x | x*y | y) out
                 "prods": cnt * (24 * (NF_C2 + 1) + 24 * (2 * NF_C2 + 1)), "node_hc": 0, "node_finish": 0}
-    kname = {"count_lanes": "k_count_lanes8", "count_contract": "k_count_mma", "partition": "k_partition",
+    kname = {"count_lanes": "k_count_lanes8", "count_contract": "k_count_mma", "partition": "k_partition_split",
              "node_hc": "k_hc_div", "prods": "k_prep8", "node_finish": "k_node_finish"}
     fused = prof_tot["count_lanes"] == 0 and prof_tot["count_contract"] > 0
     if fused:  # k_count_fused: lanes + contraction in one kernel; SURVEY 8(d)'s count-level bytes
@@ -789,7 +789,7 @@ def main():
                       "e2e": {"value": N_C3 / inf_e2e_s, "unit": "instances/s",
                               "h2d_bytes_per_step": int(Qp.numel() * 8), "d2h_bytes_per_step": int(Oh.numel() * 8)},
                       "roofline": _roof(walk_alg, walk_blocks(qc, NF_C2, DEPTH_C2), inf_s, peak, peak_kind,
-                                        ctx["philox"], "k_walk")},
+                                        ctx["philox"], "k_walk", traffic=_traffic("k_walk"))},
         "tree_roofline": _roof(tree_bytes(cnt, NF_C2, DEPTH_C2), tree_blocks(cnt, NF_C2, DEPTH_C2), value_s, peak,
                                peak_kind, ctx["philox"], "whole C2 tree (all kernels, serial chain)"),
         "scale": scale,

@@ -362,13 +362,16 @@ def test_score_ring64_and_tau_variants_match_reference_and_oracle():
 
 
 @pytest.mark.parametrize("nf,n,depth", [(13, 4000, 5), (20, 3001, 4), (33, 1500, 3), (64, 700, 2),
-                                         (32, 60000, 8), (15, 3000, 4), (1, 5000, 3)])
+                                         (32, 60000, 8), (15, 3000, 4), (1, 5000, 3),
+                                         (10, 2500, 6), (14, 4100, 7)])
 def test_count_engines_share_exact_vs_oracle(nf, n, depth):
     """Tensor-core (tcgen05 kind::i8 limb) and CUDA-core count contractions
     give the oracle's shares, including several column blocks (nf > 15),
     partial sample blocks, (60000 x 32, depth 8) levels that take several
     lane chunks and K ranges, and the shallow levels' operand-swapped
-    contraction at its column-block limits (16 columns: nf = 15; 4: nf = 1)."""
+    contraction at its column-block limits (16 columns: nf = 15; 4: nf = 1);
+    the fused count's tensor-core mask sums over its whole range (nf = 10..14,
+    the two constant columns beside the 2 nf + 1 feature/label columns)."""
     from paper_2305_00645_b200.seeds import derive_seed
 
     rng = np.random.default_rng(nf * 1000 + n)
