@@ -200,7 +200,7 @@ def walk_blocks(n, nf, depth):
     return n * sum(lookup_blocks(1 << t) + lookup_blocks(nf) for t in range(depth))
 
 
-def _roof(alg_bytes, blocks, seconds, peak, peak_kind, philox_peak, what, traffic=None):
+def _roof(alg_bytes, blocks, seconds, peak, peak_kind, philox_peak, what, traffic=None, issue=None):
     """HBM roof on algorithmic bytes and the integer-ALU roof on Philox blocks
     (the lane work is ALU bound) for one timed unit of work."""
     gbs = alg_bytes / seconds / 1e9
@@ -208,7 +208,28 @@ def _roof(alg_bytes, blocks, seconds, peak, peak_kind, philox_peak, what, traffi
     return {"bound": "hbm", "kernel": what, "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
             "peak_source": peak_kind, "algorithmic_bytes": alg_bytes, "traffic": traffic,
             "alu": {"bound": "int-alu (Philox4x32-10 blocks)", "blocks": blocks, "achieved_blocks_per_s": bps,
-                    "peak_blocks_per_s": philox_peak, "frac": bps / philox_peak if philox_peak else None}}
+                    "peak_blocks_per_s": philox_peak, "frac": bps / philox_peak if philox_peak else None},
+            "issue": issue}
+
+
+def _issue(kernel: str, launch_s: float, clocks, sms: int):
+    """Issue roof of an ALU-bound kernel: its warp instructions per launch (the
+    committed ncu capture, profiles/ncu_inst.json) over the average launch time
+    against 4 warp instructions per SM per clock (one per SMSP) at the sampled
+    SM clock -- the ceiling no integer instruction mix can pass."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_inst.json")) as fh:
+            inst = json.load(fh).get(kernel)
+    except Exception:  # noqa: BLE001
+        inst = None
+    mhz = (clocks or {}).get("sm_mhz") or (clocks or {}).get("sm_max_mhz")
+    if not inst or not mhz or launch_s <= 0:
+        return None
+    peak = 4.0 * sms * mhz * 1e6
+    return {"bound": "warp-instruction issue (1 per SMSP per clock)", "kernel": kernel,
+            "warp_inst_per_launch": inst, "inst_source": "profiles/ncu_inst.json (ncu smsp__inst_executed.sum)",
+            "achieved_warp_inst_per_s": inst / launch_s, "peak_warp_inst_per_s": peak, "sm_mhz": mhz, "sms": sms,
+            "frac": inst / launch_s / peak}
 
 
 def _traffic(kernel: str):
@@ -697,6 +718,7 @@ def main():
         return
 
     # ---- roofline of the dominant kernel class ----
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
     # dominant single kernel: node_hc (k_hc_pre + k_hc_div + k_hc_post per level) and node_finish are
     # multi-kernel latency chains with no bulk data; their times are in kernel_ms_per_step
     dom = max((k for k in prof_tot if k not in ("node_hc", "node_finish")), key=lambda k: prof_tot[k])
@@ -733,6 +755,9 @@ def main():
             gbs = bytes_of[k] * args.steps / (prof_tot[k] / 1e3) / 1e9
             classes[k] = {"kernel": kname.get(k, k), "ms_per_step": prof_tot[k] / args.steps,
                           "achieved_gbs": gbs, "frac": gbs / peak}
+            iss = _issue(kname.get(k, k), prof_tot[k] / max(1, prof_n[k]) / 1e3, clocks, sms)
+            if iss:
+                classes[k]["issue_frac"] = iss["frac"]
     cpu_base = cpu_c3 = py_ref = None
     if ctx["cpu"]:
         import oracle
@@ -778,7 +803,9 @@ def main():
         "roofline": {"bound": "hbm", "kernel": kname.get(dom, dom), "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": bytes_of[dom] / max(1, prof_n[dom] // args.steps),
-                     "avg_launch_ms": prof_tot[dom] / nlaunch, "alu": alu, "classes": classes},
+                     "avg_launch_ms": prof_tot[dom] / nlaunch, "alu": alu,
+                     "issue": _issue(kname.get(dom, dom), prof_tot[dom] / nlaunch / 1e3, clocks, sms),
+                     "classes": classes},
         "kernel_ms_per_step": {k: v / args.steps for k, v in prof_tot.items()},
         "timing": ("value: CUDA-graph replay of the whole tree" + (" incl. the NCCL count allreduce" if world > 1 else "")
                    + ("" if graphed else " [eager stream launches: GT_BENCH_EAGER / non-NCCL backend]") + "; "
@@ -789,7 +816,8 @@ def main():
                       "e2e": {"value": N_C3 / inf_e2e_s, "unit": "instances/s",
                               "h2d_bytes_per_step": int(Qp.numel() * 8), "d2h_bytes_per_step": int(Oh.numel() * 8)},
                       "roofline": _roof(walk_alg, walk_blocks(qc, NF_C2, DEPTH_C2), inf_s, peak, peak_kind,
-                                        ctx["philox"], "k_walk", traffic=_traffic("k_walk"))},
+                                        ctx["philox"], "k_walk", traffic=_traffic("k_walk"),
+                                        issue=_issue("k_walk", inf_s, clocks, sms))},
         "tree_roofline": _roof(tree_bytes(cnt, NF_C2, DEPTH_C2), tree_blocks(cnt, NF_C2, DEPTH_C2), value_s, peak,
                                peak_kind, ctx["philox"], "whole C2 tree (all kernels, serial chain)"),
         "scale": scale,

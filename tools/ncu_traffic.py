@@ -1,7 +1,9 @@
-"""Per-launch DRAM traffic of each kernel from an ncu CSV capture with
---metrics dram__bytes_read.sum,dram__bytes_write.sum (one row per launch and
-metric): the average (read + write) bytes per launch of every kernel, merged
-into profiles/ncu_traffic.json (bench.py's roofline `traffic`).
+"""Per-launch DRAM traffic and warp instructions of each kernel from an ncu
+CSV capture with --metrics dram__bytes_read.sum,dram__bytes_write.sum,
+smsp__inst_executed.sum (one row per launch and metric): the average (read +
+write) bytes per launch of every kernel, merged into profiles/ncu_traffic.json
+(bench.py's roofline `traffic`), and the average warp instructions per launch,
+merged into profiles/ncu_inst.json (bench.py's issue roof).
 
     python tools/ncu_traffic.py [--grid KERNEL:GRIDX ...] CAPTURE.csv [CAPTURE2.csv ...]
 
@@ -28,6 +30,7 @@ def name(k):
 
 def main():
     per = collections.defaultdict(float)   # (kernel, launch id) -> bytes
+    inst = collections.defaultdict(float)  # (kernel, launch id) -> warp instructions
     args, grid = sys.argv[1:], {}
     while args and args[0] == "--grid":
         k, g = args[1].split(":")
@@ -39,14 +42,17 @@ def main():
         ki, ii, gi, mi, ui, vi = (hdr.index(c) for c in ("Kernel Name", "ID", "Grid Size", "Metric Name", "Metric Unit",
                                                          "Metric Value"))
         for r in rows[1:]:
-            if not r[mi].startswith("dram__bytes_"):
+            if not (r[mi].startswith("dram__bytes_") or r[mi] == "smsp__inst_executed.sum"):
                 continue
             if name(r[ki]) in grid and r[gi].strip("()").split(",")[0].strip() != grid[name(r[ki])]:
                 continue
             v = r[vi].replace(",", "")
             if v in ("", "nan", "n/a"):
                 continue
-            per[(path, name(r[ki]), r[ii])] += float(v) * UNIT.get(r[ui], 1.0)
+            if r[mi] == "smsp__inst_executed.sum":
+                inst[(path, name(r[ki]), r[ii])] += float(v) * {"inst": 1.0, "Kinst": 1e3, "Minst": 1e6}.get(r[ui], 1.0)
+            else:
+                per[(path, name(r[ki]), r[ii])] += float(v) * UNIT.get(r[ui], 1.0)
     tot, cnt = collections.defaultdict(float), collections.Counter()
     for (_, k, _), b in per.items():
         tot[k] += b
@@ -61,6 +67,21 @@ def main():
         print(f"{k:28s} {cnt[k]:5d} launches {cur[k] / 1e6:10.3f} MB/launch")
     with open(out_path, "w") as fh:
         json.dump(dict(sorted(cur.items())), fh, indent=1)
+    if inst:
+        itot, icnt = collections.defaultdict(float), collections.Counter()
+        for (_, k, _), b in inst.items():
+            itot[k] += b
+            icnt[k] += 1
+        ipath = out_path.replace("ncu_traffic.json", "ncu_inst.json")
+        try:
+            icur = json.load(open(ipath))
+        except Exception:  # noqa: BLE001
+            icur = {}
+        for k in itot:
+            icur[k] = itot[k] / icnt[k]
+            print(f"{k:28s} {icnt[k]:5d} launches {icur[k] / 1e6:10.3f} M warp instructions/launch")
+        with open(ipath, "w") as fh:
+            json.dump(dict(sorted(icur.items())), fh, indent=1)
 
 
 if __name__ == "__main__":
