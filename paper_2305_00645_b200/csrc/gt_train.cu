@@ -2160,13 +2160,18 @@ int launch_count(const CountLaunch& c, cudaStream_t s, int num_sms, Prof& P) {
   return GT_OK;
 }
 
-// Keep the level-invariant B operand (the byte-plane sample columns, read by
-// every level's contraction) resident in L2: a persisting access-policy
-// window over it on the launches that write and read it.  The persisting
-// carve-out is raised once per device to cover it (bounded by the device max).
+// Optional (GT_L2_WINDOW=1): keep the level-invariant B operand (the
+// byte-plane sample columns, read by every level's contraction) resident in
+// L2 with a persisting access-policy window on the launches that write and
+// read it, the carve-out raised once per device (bounded by the device max).
+// Measured slower at C2 and C4 (see below); the x-plane loads keep their
+// evict_last hint instead.
 bool l2_window_attr(const void* base, uint64_t bytes, cudaLaunchAttribute* at) {
   static int max_persist = -1, max_window = 0;
-  static const bool off = getenv("GT_NO_L2_WINDOW") != nullptr;  // A/B experiments
+  // off by default: the persisting carve-out (79 MB on B200) costs the rest of
+  // the level's traffic more than it saves the x planes (C2 0.566 ms without
+  // vs 0.576 ms with, same-call A/B); GT_L2_WINDOW=1 restores it
+  static const bool off = getenv("GT_L2_WINDOW") == nullptr;
   if (off) return false;
   if (max_persist < 0) {
     int dev = 0;
@@ -2174,6 +2179,8 @@ bool l2_window_attr(const void* base, uint64_t bytes, cudaLaunchAttribute* at) {
         cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev) != cudaSuccess)
       max_persist = 0;
+    if (getenv("GT_L2_LIMIT_MB") && max_persist > 0)  // A/B experiments
+      max_persist = std::min(max_persist, atoi(getenv("GT_L2_LIMIT_MB")) << 20);
     if (max_persist > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
     cudaGetLastError();
   }
