@@ -40,6 +40,16 @@ __device__ __forceinline__ void st3s(uint64_t* p, uint64_t stride, uint64_t i, c
   p[stride + i] = a.v[1];
   p[2 * stride + i] = a.v[2];
 }
+// streamed-once operands (the early hit shares: written once, read once):
+// evict-first in L2 so they do not push out the level-invariant planes
+__device__ __forceinline__ A3 ld3s_cs(const uint64_t* p, uint64_t stride, uint64_t i) {
+  return a3(__ldcs(p + i), __ldcs(p + stride + i), __ldcs(p + 2 * stride + i));
+}
+__device__ __forceinline__ void st3s_cs(uint64_t* p, uint64_t stride, uint64_t i, const A3& a) {
+  __stcs(p + i, a.v[0]);
+  __stcs(p + stride + i, a.v[1]);
+  __stcs(p + 2 * stride + i, a.v[2]);
+}
 __device__ __forceinline__ B3 ldb3s(const uint64_t* p, uint64_t stride, uint64_t i) {
   B3 b;
   b.v[0] = p[i];
@@ -173,8 +183,8 @@ __global__ void __launch_bounds__(128) k_oaa_early(const uint64_t* midx, uint64_
       const A3 local = add_pub<64>(ld3s(midx, N, s), 0ull - (uint64_t)(m - 1));
       A3 c0, c1;
       lookup_pair_ca<64>(K, op_oaa, base + s, local, m, q, &c0, &c1);
-      st3s(ca, cs, (uint64_t)(2 * q) * N + s, c0);
-      if (2 * q + 1 < m) st3s(ca, cs, (uint64_t)(2 * q + 1) * N + s, c1);
+      st3s_cs(ca, cs, (uint64_t)(2 * q) * N + s, c0);
+      if (2 * q + 1 < m) st3s_cs(ca, cs, (uint64_t)(2 * q + 1) * N + s, c1);
     }
   }
 }
@@ -226,7 +236,7 @@ __global__ void __launch_bounds__(PS_TPB, 3)
     if (ca) {  // hit shares drawn early (k_oaa_early): the telescope words + the entries' selects
       for (int e = r; e < 6; e += B) acc = add<64>(acc, lookup_word<64>(K, op_oaa, g, m, e));
       const uint64_t F0[3] = {0, 0, 0}, cs = (uint64_t)m * N;
-      for (int j = r; j < m; j += B) acc = add<64>(acc, mul_z<64>(entryT(j), ld3s(ca, cs, (uint64_t)j * N + s), F0));
+      for (int j = r; j < m; j += B) acc = add<64>(acc, mul_z<64>(entryT(j), ld3s_cs(ca, cs, (uint64_t)j * N + s), F0));
     } else {
       acc = lookup_partial<64>(K, op_oaa, g, add_pub<64>(idx, 0ull - (uint64_t)(m - 1)), m, r, B, entryT);
     }

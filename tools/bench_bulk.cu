@@ -90,7 +90,8 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   int cfg[][3] = {{16384, 4, 1}, {45056, 4, 2}, {45056, 4, 1}, {32768, 6, 1}, {16384, 12, 1}, {8192, 24, 1},
-                  {4096, 16, 1}, {65536, 3, 1}, {45056, 4, 4}, {16384, 12, 4}};
+                  {4096, 16, 1}, {65536, 3, 1}, {45056, 4, 4}, {16384, 12, 4},
+                  {24576, 4, 1}, {24576, 7, 1}};  // the fused count's x-plane stages
   for (auto& c : cfg) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(a);
@@ -103,16 +104,18 @@ int main() {
                       per * sms / ms / 1e6, per / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
     }
   }
-  // L2-resident: every CTA streams the same 48 MB window (wraps), 8 MB per CTA of traffic
+  // L2-resident: every CTA streams the same window (wraps), 8 MB per CTA of traffic
+  for (uint64_t win : {48ull << 20, 33ull << 20, 16ull << 20})
   for (auto& c : cfg) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(a);
-      k_stream_wrap<<<sms, 32, c[0] * c[1]>>>(buf, per, 48ull << 20, c[0], c[1], c[2]);
+      k_stream_wrap<<<sms, 32, c[0] * c[1]>>>(buf, per, win, c[0], c[1], c[2]);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
       cudaEventElapsedTime(&ms, a, b);
-      if (rep) printf("L2 %6d B x %2d stages, %d copies: %.1f GB/s total (%.1f per SM)\n", c[0], c[1], c[2],
+      if (rep) printf("L2 win %3llu MB %6d B x %2d stages, %d copies: %.1f GB/s total (%.1f per SM)\n",
+                      (unsigned long long)(win >> 20), c[0], c[1], c[2],
                       per * sms / ms / 1e6, per / ms / 1e6);
     }
   }
