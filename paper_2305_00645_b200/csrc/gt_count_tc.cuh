@@ -903,15 +903,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 2), 1) k_
     }
   }
   // the x planes of column block `rank`, stage t (one bulk copy; re-read by
-  // every level: kept in L2 with evict_last)
+  // every level: kept in L2 with evict_last).  With an even ring (XS even;
+  // T is always even) one copy fills the two stages of a 128-sample K block
+  // (adjacent in HBM and in the ring) and arms the even slot's barrier: a
+  // bulk copy's throughput per SM grows with its size (tools/bench_bulk.cu:
+  // 66 GB/s at 24 KB, 115 GB/s at 45 KB per copy, L2-resident)
+  const int xstep = (XS & 1) ? 1 : 2;
   auto x_copy = [&](int t, uint64_t pol) {
     const int xs = t % XS;
     const uint64_t kb = a.kb_lo + kb0 + (uint32_t)(t >> 1), h = t & 1;
-    mbar_expect_tx(&xfull[xs], (uint32_t)TCF_XB);
+    const uint32_t bytes = (uint32_t)(xstep * TCF_XB);
+    mbar_expect_tx(&xfull[xs], bytes);
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
             smem_u32(smt + xs * TCF_XB)),
-        "l"(a.B8 + (((uint64_t)rank * a.nkb_total + kb) * 2 + h) * (uint64_t)TCF_XB), "r"((uint32_t)TCF_XB),
+        "l"(a.B8 + (((uint64_t)rank * a.nkb_total + kb) * 2 + h) * (uint64_t)TCF_XB), "r"(bytes),
         "r"(smem_u32(&xfull[xs])), "l"(pol)
         : "memory");
   };
@@ -922,7 +928,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 2), 1) k_
   if (tid == 32 * TCF_PW && xpre) {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    for (int t = 0; t < xpre; ++t) x_copy(t, pol);
+    for (int t = 0; t < xpre; t += xstep) x_copy(t, pol);
   }
   cnt_ts(a, 0, tid == 0);
   pdl_wait();  // m_idx, is_leaf, the zeroed sums (partition) and the x planes (prologue)
@@ -1051,9 +1057,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 2), 1) k_
     // the x planes are re-read by every level: kept in L2 (evict_last)
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    for (int t = xpre; t < T; ++t) {
-      const int xs = t % XS;
-      if (t >= XS) mbar_wait(&xempty[xs], (uint32_t)(((t / XS) - 1) & 1));
+    for (int t = xpre; t < T; t += xstep) {
+      // the last stage this copy fills: its slot's MMAs completing implies the
+      // earlier slot's (a commit tracks all of the thread's prior UMMAs)
+      const int tl = t + xstep - 1, xs = tl % XS;
+      if (tl >= XS) mbar_wait(&xempty[xs], (uint32_t)(((tl / XS) - 1) & 1));
       x_copy(t, pol);
     }
   } else if (warp == TCF_PW + 1 && lane == 0 && T > 0) {
@@ -1063,7 +1071,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (PW + 2), 1) k_
     for (int t = 0; t < T; ++t) {
       const int st = t & (NS - 1), xs = t % XS;
       const uint32_t ph = (uint32_t)((t >> ns_sh) & 1);
-      mbar_wait(&xfull[xs], (uint32_t)((t / XS) & 1));
+      mbar_wait(&xfull[xstep == 2 ? (xs & ~1) : xs], (uint32_t)((t / XS) & 1));
       mbar_wait(&full[st], ph);
       if (rank == 0) {
         mbar_wait_cluster(&pfull[st], ph);
