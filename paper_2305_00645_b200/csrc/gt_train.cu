@@ -166,9 +166,9 @@ __global__ void k_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T
 constexpr int OAA_CHUNK = 4;
 __global__ void __launch_bounds__(128) k_oaa_early(const uint64_t* midx, uint64_t* ca, uint64_t N, int m,
                                                    uint64_t base, Keys K, uint32_t op_oaa,
-                                                   unsigned long long* ctr) {
+                                                   unsigned long long* ctr, int qe) {
   const int mh = (m + 1) >> 1, lane = threadIdx.x & 31;
-  const uint64_t total = N * (uint64_t)mh, cs = (uint64_t)m * N;
+  const uint64_t total = N * (uint64_t)min(mh, qe), cs = (uint64_t)m * N;
   for (;;) {
     unsigned long long t0 = 0;
     if (lane == 0) t0 = atomicAdd(ctr, 32ull * OAA_CHUNK);
@@ -202,7 +202,7 @@ template <int B>
 __global__ void __launch_bounds__(PS_TPB, 3)
     k_partition_split(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint64_t slots, int m, int nf, uint64_t N,
                       uint64_t base, Keys K, uint32_t op_oaa, uint32_t op_row, PartAux aux, int tab_smem,
-                      const uint64_t* __restrict__ ca) {
+                      const uint64_t* __restrict__ ca, int qe) {
   constexpr int S = PS_TPB / B;
   __shared__ uint64_t part[B][3][S];  // members' partial sums
   __shared__ uint64_t feat[3][S];     // the sample's fetched feature index (shares)
@@ -236,7 +236,12 @@ __global__ void __launch_bounds__(PS_TPB, 3)
     if (ca) {  // hit shares drawn early (k_oaa_early): the telescope words + the entries' selects
       for (int e = r; e < 6; e += B) acc = add<64>(acc, lookup_word<64>(K, op_oaa, g, m, e));
       const uint64_t F0[3] = {0, 0, 0}, cs = (uint64_t)m * N;
-      for (int j = r; j < m; j += B) acc = add<64>(acc, mul_z<64>(entryT(j), ld3s_cs(ca, cs, (uint64_t)j * N + s), F0));
+      const int mh = (m + 1) >> 1, je = min(m, 2 * qe);
+      for (int j = r; j < je; j += B) acc = add<64>(acc, mul_z<64>(entryT(j), ld3s_cs(ca, cs, (uint64_t)j * N + s), F0));
+      if (qe < mh) {  // the pairs the early lanes left: drawn here (same lanes, same randomness)
+        const A3 local = add_pub<64>(idx, 0ull - (uint64_t)(m - 1));
+        for (int q = qe + r; q < mh; q += B) acc = add<64>(acc, lookup_pair<64>(K, op_oaa, g, local, m, q, entryT));
+      }
     } else {
       acc = lookup_partial<64>(K, op_oaa, g, add_pub<64>(idx, 0ull - (uint64_t)(m - 1)), m, r, B, entryT);
     }
@@ -1942,7 +1947,7 @@ int launch_partition_g(const uint64_t* X, uint64_t* midx, const uint64_t* T, uin
 // 181 vs 204 us per C2 tree against G = 2).
 int launch_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint64_t slots, int m, int nf, uint64_t N,
                      uint64_t base, const Keys& K, int level, cudaStream_t s, int num_sms, const PartAux& aux,
-                     const uint64_t* ca = nullptr) {
+                     const uint64_t* ca = nullptr, int qe = 1 << 30) {
   // A/B: GT_PART_SPLIT=B (1, 2, 4) forces the split kernel, 0 the group kernel.
   // Default (measured, C2 / C4): the split kernel with B = 2 while the level
   // has fewer than ~700 samples per SM (C2: 0.657 vs 0.669 ms per tree), the
@@ -1958,11 +1963,11 @@ int launch_partition(const uint64_t* X, uint64_t* midx, const uint64_t* T, uint6
     const uint32_t oo = op_id(level, SITE_PART_OAA), orow = op_id(level, SITE_PART_ROW);
     const dim3 blk(PS_TPB);
     int rc = split == 1 ? launch_chain(k_partition_split<1>, dim3(grid), blk, smem, s, nullptr, X, midx, T, slots, m,
-                                       nf, N, base, K, oo, orow, aux, tab_smem, ca)
+                                       nf, N, base, K, oo, orow, aux, tab_smem, ca, qe)
            : split == 2 ? launch_chain(k_partition_split<2>, dim3(grid), blk, smem, s, nullptr, X, midx, T, slots, m,
-                                       nf, N, base, K, oo, orow, aux, tab_smem, ca)
+                                       nf, N, base, K, oo, orow, aux, tab_smem, ca, qe)
                         : launch_chain(k_partition_split<4>, dim3(grid), blk, smem, s, nullptr, X, midx, T, slots, m,
-                                       nf, N, base, K, oo, orow, aux, tab_smem, ca);
+                                       nf, N, base, K, oo, orow, aux, tab_smem, ca, qe);
     if (rc) return rc;
     GT_LAUNCH_CHECK("k_partition_split");
     return GT_OK;
@@ -2813,6 +2818,19 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
   static const int oaa_ctas = getenv("GT_OAA_CTAS") ? atoi(getenv("GT_OAA_CTAS")) : 0;          // A/B
   static const bool early_after_count = getenv("GT_OAA_AFTER_COUNT") != nullptr;              // A/B
   static const int oaa_tpb = getenv("GT_OAA_TPB") ? atoi(getenv("GT_OAA_TPB")) : 64;            // A/B
+  // the share of a partition's entry pairs drawn early (the rest inline in
+  // the partition) for partitions over >= oaa_split_min entries: at C2's last
+  // partition (32 entries) the early lanes are on the critical path (pausing
+  // them during the divisions costs 7 %); drawing 13 of its 16 pairs early and
+  // 3 inline: 0.5595 -> 0.554 ms (same-call A/B; 69-81 % tie, 50 / 88 % and
+  // splitting the 16-entry partition too are slower)
+  static const int oaa_split_pct = getenv("GT_OAA_SPLITPCT") ? atoi(getenv("GT_OAA_SPLITPCT")) : 80;  // A/B
+  static const int oaa_split_min = getenv("GT_OAA_SPLITMIN") ? atoi(getenv("GT_OAA_SPLITMIN")) : 32;    // A/B
+  auto oaa_qe = [&](int m) -> int {
+    const int mh = (m + 1) / 2;
+    if (m < oaa_split_min || oaa_split_pct >= 100) return mh;
+    return std::max(1, (mh * oaa_split_pct + 99) / 100);
+  };
   if (early_oaa) GT_CUDA_CHECK(cudaMemsetAsync(ws + L.oaactr, 0, 16 * sizeof(uint64_t), s));
   auto early_oaa_launch = [&](int level) -> int {
     const bool early_next = early_oaa && level >= 1 && level + 1 < c.depth && level + 1 <= oaa_max && N;
@@ -2830,7 +2848,8 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
     if (oaa_ctas > 0) grid = std::min<uint64_t>(grid, (uint64_t)oaa_ctas);
     k_oaa_early<<<(unsigned)grid, oaa_tpb, 0, os>>>(midx, ws + L.oaa, N, m, c.sample_base, K,
                                                    op_id(level + 1, SITE_PART_OAA),
-                                                   reinterpret_cast<unsigned long long*>(ws + L.oaactr) + level);
+                                                   reinterpret_cast<unsigned long long*>(ws + L.oaactr) + level,
+                                                   oaa_qe(m));
     GT_LAUNCH_CHECK("k_oaa_early");
     P.count_launch();
     if (os != s) {
@@ -2853,7 +2872,7 @@ static int train_impl(const gt_train_cfg* cfg, const uint64_t* features, const u
       P.start();
       PartAux aux{S, swords, c.count_engine == 0 ? ws + L.leaf : nullptr, f[cur], n_h, op_id(level, SITE_ISLEAF)};
       int rc = launch_partition(features, midx, T, slots, n_h / 2, c.nf, N, c.sample_base, K, level, s, num_sms, aux,
-                                ca);
+                                ca, oaa_qe(n_h / 2));
       if (rc) return rc;
       P.stop(Prof::PARTITION);
       if (!early_after_count) {
