@@ -181,9 +181,10 @@ def main():
                 engine.run_local(body, seeds=setup, dealer_seed=dseed)
                 pr.disable()
             pstats.Stats(pr).sort_stats("tottime").print_stats(15)
-    elif what == "small":  # sanitizer target: 4000 x 13, depth 5 (fused count, early oaa lanes, split partition)
+    elif what == "small":  # sanitizer target: 4000 x 13, depth 7 (fused count with paired x-plane copies, early oaa
+        # lanes, split partition; the last partition's 32 entries split between early and inline pairs)
         rng = np.random.default_rng(5)
-        n, nf, depth = 4000, 13, 5
+        n, nf, depth = 4000, 13, 7
         X = t(bench._share(rng.integers(0, 2, (n, nf)), rng))
         Y = t(bench._share(rng.integers(0, 2, n), rng))
         F = t(np.zeros((1 << depth) - 1, dtype=np.uint64))

@@ -16,7 +16,7 @@ for tool in memcheck racecheck synccheck; do
     python -c "import __graft_entry__ as g; g.smoke()" > "$out/sanitize_${tool}_c1.out" 2>&1
   echo "$tool c1 rc=$?"
 done
-# the fused count, early oaa lanes and split partition on a small C2-shaped tree
+# the fused count (paired x-plane copies), early oaa lanes, split partition (hybrid last partition) on a small depth-7 C2-shaped tree
 for tool in memcheck racecheck synccheck; do
   $CS --tool $tool --log-file "$out/sanitize_${tool}_small_fused.log" \
     python tools/probe.py small > "$out/sanitize_${tool}_small_fused.out" 2>&1
