@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(256, GT_PREP8_MINB) k_prep8(Prep8Args a) {
   // words of the same Philox block per key (mul's schedule), drawn once
   const int nfp = (nf + 1) >> 1;
   for (int e = tid; e < cnt * nfp; e += blockDim.x) {
-    const int sl = e / nfp, fp = e - sl * nfp, f0 = 2 * fp;
+    const int sl = (int)((uint32_t)e / (uint32_t)nfp), fp = e - sl * nfp, f0 = 2 * fp;
     W2 Z[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) Z[i] = word2(a.K.pair[i], a.op_prods, 0, (uint32_t)fp, a.base + s0 + sl);
@@ -158,11 +158,13 @@ __global__ void __launch_bounds__(256, GT_PREP8_MINB) k_prep8(Prep8Args a) {
   // thread t owns (column g, quad) = t % (4 cpb) and walks the (component,
   // column block, 16-sample chunk) combinations: one division per thread
   const uint64_t HBX = (uint64_t)8 * a.cpb * (TC_KB / 2);
-  const int gq = 4 * a.cpb, combos = 3 * a.nbn * 2;
-  const int g = (tid % gq) >> 2, quad = tid & 3;
-  for (int cb = tid / gq; cb < combos; cb += blockDim.x / gq) {
-    const int kc = 2 * sub + (cb & 1), r = cb >> 1;
-    const int nb = r % a.nbn, c = r / a.nbn;
+  // (unsigned index math: the runtime divisors cost half the instructions)
+  const uint32_t gq = 4u * (uint32_t)a.cpb, combos = 3u * (uint32_t)a.nbn * 2u, nbn = (uint32_t)a.nbn;
+  const int g = (int)(((uint32_t)tid % gq) >> 2), quad = tid & 3;
+  for (uint32_t cb = (uint32_t)tid / gq; cb < combos; cb += blockDim.x / gq) {
+    const int kc = 2 * sub + (int)(cb & 1);
+    const uint32_t r = cb >> 1;
+    const int nb = (int)(r % nbn), c = (int)(r / nbn);
     const int w = nb * a.cpb + g;
     const uint64_t* p0 = nullptr;
     int stride = nf;
